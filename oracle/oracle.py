@@ -1,0 +1,294 @@
+"""ctypes front-end of the CPU oracle -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+--impl reference) may import this module.  The product package
+(paper_1709_04057_b200) never imports it; its CUDA path fails loudly when the
+extension is missing instead of falling back here.
+
+Two checkers live behind this module:
+
+* ``Oracle``  -- oracle/liblinrec_oracle.so, the plain-C restatement of
+  recurrence.hpp (see oracle/linrec_oracle.c for the file:line map).
+* ``RefLib``  -- oracle/_ref/liblinrec_ref.so, the unmodified reference
+  compiled from /root/reference by oracle/Makefile (``make -C oracle ref``).
+  It travels to the GPU box prebuilt; /root/reference itself does not.
+
+All arrays are C-contiguous ``[T, batch, features]`` (time-major, tensor.hpp:49-75).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import importlib.machinery
+import importlib.util
+import os
+import sysconfig
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liblinrec_oracle.so")
+REF_DIR = os.path.join(HERE, "_ref")
+REF_SO = os.path.join(REF_DIR, "liblinrec_ref.so")
+REF_PY = os.path.join(REF_DIR, "linrec" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+_i64 = C.c_int64
+_vp = C.c_void_p
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(_vp)
+
+
+def _sfx(dtype):
+    dt = np.dtype(dtype)
+    if dt == np.float32:
+        return "f32"
+    if dt == np.float64:
+        return "f64"
+    raise TypeError(f"oracle: unsupported dtype {dt}")
+
+
+def max_rel_error(a, b):
+    """max|a-b| / max|b| -- tests/support/oracles.hpp:73-82 (normwise)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    max_diff = float(np.max(np.abs(a - b))) if a.size else 0.0
+    max_ref = float(np.max(np.abs(b))) if b.size else 0.0
+    if max_ref == 0.0:
+        return 0.0 if max_diff == 0.0 else float("inf")
+    return max_diff / max_ref
+
+
+def grads_agree(analytic, numeric, rel=1e-5, tiny=1e-7):
+    """tests/support/oracles.hpp:64-69."""
+    scale = max(abs(analytic), abs(numeric))
+    if scale <= tiny:
+        return True
+    return abs(analytic - numeric) <= rel * scale
+
+
+class Oracle:
+    """The C restatement (oracle/linrec_oracle.c)."""
+
+    def __init__(self, path: str = ORACLE_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle`")
+        lib = C.CDLL(path)
+        self.lib = lib
+        lib.oracle_plan_chunks.restype = _i64
+        lib.oracle_plan_chunks.argtypes = [_i64, C.c_int, _vp]
+        lib.oracle_predicted_speedup.restype = C.c_double
+        lib.oracle_predicted_speedup.argtypes = [C.c_int, _i64]
+        for s in ("f32", "f64"):
+            getattr(lib, f"oracle_scan_serial_{s}").argtypes = [_vp] * 4 + [_i64] * 2
+            getattr(lib, f"oracle_scan_parallel_{s}").argtypes = (
+                [_vp] * 4 + [_i64] * 2 + [_vp, _i64] + [_vp] * 3)
+            getattr(lib, f"oracle_scan_backward_{s}").argtypes = (
+                [_vp] * 7 + [_i64] * 2 + [_vp, _i64])
+            getattr(lib, f"oracle_first_nonfinite_{s}").argtypes = [_vp, _i64]
+            getattr(lib, f"oracle_first_nonfinite_{s}").restype = _i64
+            getattr(lib, f"oracle_rng_fill_{s}").argtypes = [_vp, _vp, _i64, C.c_double, C.c_double]
+        lib.oracle_scan_serial_f32_wide.argtypes = [_vp] * 4 + [_i64] * 2
+        lib.oracle_scan_backward_f32_wide.argtypes = [_vp] * 7 + [_i64] * 2
+        lib.oracle_rng_next_u64.restype = C.c_uint64
+        lib.oracle_rng_next_u64.argtypes = [_vp]
+        lib.oracle_rng_split.restype = C.c_uint64
+        lib.oracle_rng_split.argtypes = [C.c_uint64, C.c_uint64]
+        lib.oracle_fnv1a64.restype = C.c_uint64
+        lib.oracle_fnv1a64.argtypes = [_vp, C.c_size_t, C.c_uint64]
+
+    # -- plan / cost model --------------------------------------------------
+    def plan_chunks(self, T: int, workers: int):
+        p = self.lib.oracle_plan_chunks(T, workers, None)
+        if p < 0:
+            raise RuntimeError("plan_chunks: contract violation")
+        b = np.zeros(2 * p, dtype=np.int64)
+        self.lib.oracle_plan_chunks(T, workers, _ptr(b))
+        return [(int(b[2 * i]), int(b[2 * i + 1])) for i in range(p)]
+
+    def predicted_speedup(self, p: int, T: int) -> float:
+        return self.lib.oracle_predicted_speedup(p, T)
+
+    # -- scans ---------------------------------------------------------------
+    @staticmethod
+    def _shape(a):
+        T = a.shape[0]
+        W = int(np.prod(a.shape[1:])) if a.ndim > 1 else 1
+        return T, W
+
+    def scan_serial(self, lam, x, h0=None):
+        lam = np.ascontiguousarray(lam)
+        x = np.ascontiguousarray(x, dtype=lam.dtype)
+        h0 = None if h0 is None else np.ascontiguousarray(h0, dtype=lam.dtype)
+        h = np.empty_like(lam)
+        T, W = self._shape(lam)
+        getattr(self.lib, f"oracle_scan_serial_{_sfx(lam.dtype)}")(
+            _ptr(lam), _ptr(x), _ptr(h0), _ptr(h), T, W)
+        return h
+
+    def scan_parallel(self, lam, x, h0=None, workers=4, summaries=False):
+        lam = np.ascontiguousarray(lam)
+        x = np.ascontiguousarray(x, dtype=lam.dtype)
+        h0 = None if h0 is None else np.ascontiguousarray(h0, dtype=lam.dtype)
+        T, W = self._shape(lam)
+        plan = self.plan_chunks(T, workers)
+        b = np.asarray(plan, dtype=np.int64).reshape(-1)
+        p = len(plan)
+        h = np.empty_like(lam)
+        P = np.empty((p,) + lam.shape[1:], lam.dtype)
+        R = np.empty_like(P)
+        Cc = np.empty_like(P)
+        getattr(self.lib, f"oracle_scan_parallel_{_sfx(lam.dtype)}")(
+            _ptr(lam), _ptr(x), _ptr(h0), _ptr(h), T, W, _ptr(b), p,
+            _ptr(P), _ptr(R), _ptr(Cc))
+        return (h, P, R, Cc) if summaries else h
+
+    def scan_backward(self, lam, h0, h, dh, workers=None):
+        """workers=None -> ScanMode::Serial; else the parallel plan."""
+        lam = np.ascontiguousarray(lam)
+        h = np.ascontiguousarray(h, dtype=lam.dtype)
+        dh = np.ascontiguousarray(dh, dtype=lam.dtype)
+        h0 = None if h0 is None else np.ascontiguousarray(h0, dtype=lam.dtype)
+        T, W = self._shape(lam)
+        dlam = np.empty_like(lam)
+        dx = np.empty_like(lam)
+        dh0 = np.empty(lam.shape[1:], lam.dtype)
+        if workers is None:
+            b, p = None, 0
+        else:
+            plan = self.plan_chunks(T, workers)
+            b, p = np.asarray(plan, dtype=np.int64).reshape(-1), len(plan)
+        getattr(self.lib, f"oracle_scan_backward_{_sfx(lam.dtype)}")(
+            _ptr(lam), _ptr(h0), _ptr(h), _ptr(dh), _ptr(dlam), _ptr(dx),
+            _ptr(dh0), T, W, _ptr(b), p)
+        return dlam, dx, dh0
+
+    def scan_serial_wide(self, lam, x, h0=None):
+        """fp64-accumulated serial scan of fp32 data (fp64 error bound)."""
+        lam = np.ascontiguousarray(lam, dtype=np.float32)
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        h0 = None if h0 is None else np.ascontiguousarray(h0, dtype=np.float32)
+        h = np.empty(lam.shape, np.float64)
+        T, W = self._shape(lam)
+        self.lib.oracle_scan_serial_f32_wide(_ptr(lam), _ptr(x), _ptr(h0), _ptr(h), T, W)
+        return h
+
+    def scan_backward_wide(self, lam, h0, h, dh):
+        lam = np.ascontiguousarray(lam, dtype=np.float32)
+        h = np.ascontiguousarray(h, dtype=np.float32)
+        dh = np.ascontiguousarray(dh, dtype=np.float32)
+        h0 = None if h0 is None else np.ascontiguousarray(h0, dtype=np.float32)
+        T, W = self._shape(lam)
+        dlam = np.empty(lam.shape, np.float64)
+        dx = np.empty(lam.shape, np.float64)
+        dh0 = np.empty(lam.shape[1:], np.float64)
+        self.lib.oracle_scan_backward_f32_wide(
+            _ptr(lam), _ptr(h0), _ptr(h), _ptr(dh), _ptr(dlam), _ptr(dx), _ptr(dh0), T, W)
+        return dlam, dx, dh0
+
+    def first_nonfinite(self, a):
+        a = np.ascontiguousarray(a)
+        return int(getattr(self.lib, f"oracle_first_nonfinite_{_sfx(a.dtype)}")(_ptr(a), a.size))
+
+    # -- RNG (rng.hpp) -------------------------------------------------------
+    def rng(self, seed: int, split: int | None = None):
+        s = seed if split is None else int(self.lib.oracle_rng_split(seed, split))
+        return np.array([s, 0], dtype=np.uint64)
+
+    def rng_next(self, state):
+        return int(self.lib.oracle_rng_next_u64(_ptr(state)))
+
+    def rng_fill(self, state, shape, lo, hi, dtype=np.float32):
+        a = np.empty(shape, dtype)
+        getattr(self.lib, f"oracle_rng_fill_{_sfx(dtype)}")(_ptr(state), _ptr(a), a.size, lo, hi)
+        return a
+
+    def random_recurrence(self, seed, T, b, n, dtype=np.float32, split=None):
+        """bench.hpp:134-143: lam~U(0.05,0.95), x,h0~U(-1,1), one stream."""
+        st = self.rng(seed, split)
+        lam = self.rng_fill(st, (T, b, n), 0.05, 0.95, dtype)
+        x = self.rng_fill(st, (T, b, n), -1.0, 1.0, dtype)
+        h0 = self.rng_fill(st, (b, n), -1.0, 1.0, dtype)
+        return lam, x, h0
+
+    def fnv1a64(self, *arrays):
+        h = 0xCBF29CE484222325
+        for a in arrays:
+            a = np.ascontiguousarray(a)
+            h = int(self.lib.oracle_fnv1a64(_ptr(a), a.nbytes, h))
+        return h
+
+
+class RefLib:
+    """The unmodified reference, compiled from /root/reference (oracle/_ref)."""
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle ref` where /root/reference exists")
+        lib = C.CDLL(path)
+        self.lib = lib
+        lib.ref_last_error.restype = C.c_char_p
+        for s in ("f32", "f64"):
+            getattr(lib, f"ref_scan_{s}").argtypes = [_vp] * 4 + [_i64] * 3 + [C.c_int, C.c_int] + [_vp] * 3
+            getattr(lib, f"ref_scan_backward_{s}").argtypes = [_vp] * 7 + [_i64] * 3 + [C.c_int, C.c_int]
+        lib.ref_rng_fill_f32.argtypes = [C.c_uint64, _i64, _vp, _i64, C.c_double, C.c_double]
+        lib.ref_rng_first.restype = C.c_uint64
+        lib.ref_rng_first.argtypes = [C.c_uint64, C.c_int]
+        lib.ref_hardware_workers.restype = C.c_int
+
+    def _check(self, rc):
+        if rc != 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+
+    def scan(self, lam, x, h0=None, mode="parallel", workers=4, summaries=False):
+        lam = np.ascontiguousarray(lam)
+        x = np.ascontiguousarray(x, dtype=lam.dtype)
+        h0 = None if h0 is None else np.ascontiguousarray(h0, dtype=lam.dtype)
+        T, b, n = lam.shape
+        h = np.empty_like(lam)
+        p = min(workers, T)
+        P = np.empty((p, b, n), lam.dtype)
+        R = np.empty_like(P)
+        Cc = np.empty_like(P)
+        self._check(getattr(self.lib, f"ref_scan_{_sfx(lam.dtype)}")(
+            _ptr(lam), _ptr(x), _ptr(h0), _ptr(h), T, b, n,
+            0 if mode == "serial" else 1, workers, _ptr(P), _ptr(R), _ptr(Cc)))
+        return (h, P, R, Cc) if summaries else h
+
+    def scan_backward(self, lam, h0, h, dh, mode="parallel", workers=4):
+        lam = np.ascontiguousarray(lam)
+        h = np.ascontiguousarray(h, dtype=lam.dtype)
+        dh = np.ascontiguousarray(dh, dtype=lam.dtype)
+        h0 = None if h0 is None else np.ascontiguousarray(h0, dtype=lam.dtype)
+        T, b, n = lam.shape
+        dlam = np.empty_like(lam)
+        dx = np.empty_like(lam)
+        dh0 = np.empty((b, n), lam.dtype)
+        self._check(getattr(self.lib, f"ref_scan_backward_{_sfx(lam.dtype)}")(
+            _ptr(lam), _ptr(h0), _ptr(h), _ptr(dh), _ptr(dlam), _ptr(dx), _ptr(dh0),
+            T, b, n, 0 if mode == "serial" else 1, workers))
+        return dlam, dx, dh0
+
+    def rng_fill_f32(self, seed, split, count, lo, hi):
+        a = np.empty(count, np.float32)
+        self.lib.ref_rng_fill_f32(seed, -1 if split is None else split, _ptr(a), count, lo, hi)
+        return a
+
+    def rng_first(self, seed, which):
+        return int(self.lib.ref_rng_first(seed, which))
+
+    def hardware_workers(self):
+        return int(self.lib.ref_hardware_workers())
+
+
+def load_reference_module():
+    """The reference's own pybind11 module ``linrec`` (bindings/linrec_py.cpp)
+    built into oracle/_ref.  Loaded without touching sys.modules so it never
+    shadows the product module of the same name."""
+    if not os.path.exists(REF_PY):
+        raise FileNotFoundError(f"{REF_PY} missing: run `make -C oracle ref`")
+    loader = importlib.machinery.ExtensionFileLoader("linrec", REF_PY)
+    spec = importlib.util.spec_from_file_location("linrec", REF_PY, loader=loader)
+    mod = importlib.util.module_from_spec(spec)
+    loader.exec_module(mod)
+    return mod

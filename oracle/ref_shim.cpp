@@ -1,0 +1,127 @@
+// C shim over the UNMODIFIED reference recurrence core -- TEST INFRASTRUCTURE.
+//
+// Compiled by oracle/Makefile against the headers where they lie under
+// /root/reference/proj/include (never copied into this repo) into
+// oracle/_ref/liblinrec_ref.so.  It exposes linrec::scan_serial,
+// linrec::scan_parallel and linrec::scan_backward (recurrence.hpp:169-377)
+// on raw [T][b][n] buffers so the tests can pin oracle/linrec_oracle.c to the
+// reference bit for bit, and so bench.py can time the reference's own CPU
+// path (cpu_baseline kind "reference").
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "linrec/recurrence.hpp"
+#include "linrec/rng.hpp"
+
+namespace {
+thread_local std::string g_err;
+
+template <class S>
+linrec::Tensor3<S> t3(const S* p, int64_t T, int64_t b, int64_t n) {
+  linrec::Tensor3<S> t(T, b, n);
+  std::copy(p, p + t.size(), t.data.begin());
+  return t;
+}
+template <class S>
+linrec::Tensor2<S> t2(const S* p, int64_t b, int64_t n) {
+  linrec::Tensor2<S> t(b, n);
+  if (p) std::copy(p, p + t.size(), t.data.begin());
+  return t;
+}
+
+template <class S>
+int scan_impl(const S* lam, const S* x, const S* h0, S* h, int64_t T,
+              int64_t b, int64_t n, int mode, int workers, S* P, S* R, S* C) {
+  try {
+    auto L = t3(lam, T, b, n);
+    auto X = t3(x, T, b, n);
+    auto H0 = t2(h0, b, n);
+    linrec::Tensor3<S> out;
+    if (mode == 0) {
+      out = linrec::scan_serial(L, X, H0);
+    } else {
+      linrec::ThreadPool pool(workers);
+      linrec::ScanSummaries<S> s;
+      out = linrec::scan_parallel(L, X, H0, linrec::plan_chunks(T, workers),
+                                  pool, false, &s);
+      if (P) std::copy(s.P.data.begin(), s.P.data.end(), P);
+      if (R) std::copy(s.R.data.begin(), s.R.data.end(), R);
+      if (C) std::copy(s.C.data.begin(), s.C.data.end(), C);
+    }
+    std::copy(out.data.begin(), out.data.end(), h);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+template <class S>
+int bwd_impl(const S* lam, const S* h0, const S* h, const S* dh, S* dlam,
+             S* dx, S* dh0, int64_t T, int64_t b, int64_t n, int mode,
+             int workers) {
+  try {
+    auto L = t3(lam, T, b, n);
+    auto H = t3(h, T, b, n);
+    auto DH = t3(dh, T, b, n);
+    auto H0 = t2(h0, b, n);
+    linrec::ThreadPool pool(workers);
+    auto g = linrec::scan_backward(
+        L, H0, H, DH,
+        mode == 0 ? linrec::ScanMode::Serial : linrec::ScanMode::Parallel,
+        pool);
+    std::copy(g.d_decays.data.begin(), g.d_decays.data.end(), dlam);
+    std::copy(g.d_impulses.data.begin(), g.d_impulses.data.end(), dx);
+    std::copy(g.d_initial.data.begin(), g.d_initial.data.end(), dh0);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+}  // namespace
+
+extern "C" {
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_scan_f32(const float* lam, const float* x, const float* h0, float* h,
+                 int64_t T, int64_t b, int64_t n, int mode, int workers,
+                 float* P, float* R, float* C) {
+  return scan_impl(lam, x, h0, h, T, b, n, mode, workers, P, R, C);
+}
+int ref_scan_f64(const double* lam, const double* x, const double* h0,
+                 double* h, int64_t T, int64_t b, int64_t n, int mode,
+                 int workers, double* P, double* R, double* C) {
+  return scan_impl(lam, x, h0, h, T, b, n, mode, workers, P, R, C);
+}
+int ref_scan_backward_f32(const float* lam, const float* h0, const float* h,
+                          const float* dh, float* dlam, float* dx, float* dh0,
+                          int64_t T, int64_t b, int64_t n, int mode,
+                          int workers) {
+  return bwd_impl(lam, h0, h, dh, dlam, dx, dh0, T, b, n, mode, workers);
+}
+int ref_scan_backward_f64(const double* lam, const double* h0,
+                          const double* h, const double* dh, double* dlam,
+                          double* dx, double* dh0, int64_t T, int64_t b,
+                          int64_t n, int mode, int workers) {
+  return bwd_impl(lam, h0, h, dh, dlam, dx, dh0, T, b, n, mode, workers);
+}
+// linrec::Rng(seed).split(stream) then fill_uniform (rng.hpp:15-71).
+void ref_rng_fill_f32(uint64_t seed, int64_t split_stream, float* v,
+                      int64_t count, double lo, double hi) {
+  linrec::Rng root(seed);
+  linrec::Rng rng = split_stream >= 0 ? root.split(uint64_t(split_stream))
+                                      : root;
+  for (int64_t i = 0; i < count; ++i) v[i] = float(rng.uniform(lo, hi));
+}
+uint64_t ref_rng_first(uint64_t seed, int which) {
+  linrec::Rng rng(seed);
+  uint64_t v = 0;
+  for (int i = 0; i <= which; ++i) v = rng.next_u64();
+  return v;
+}
+int ref_hardware_workers() { return linrec::ThreadPool::hardware_workers(); }
+}
