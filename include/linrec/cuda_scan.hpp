@@ -1,0 +1,176 @@
+// linrec/cuda_scan.hpp -- C++ host mirror of the reference's recurrence entry
+// points (proj/include/linrec/recurrence.hpp:169-377) over the C ABI of
+// include/linrec_cuda.h.  Header-only; link against liblinrec_cuda.so.
+//
+// The reference's functions take host Tensor3/Tensor2 (std::vector storage,
+// tensor.hpp:20-91) and a ThreadPool.  Here the same names take views of
+// caller-owned DEVICE buffers with the same [T][b][n] time-major layout and a
+// CUDA stream; results are written into caller-provided outputs (the
+// reference allocates them, recurrence.hpp:174, :327-329).  Errors throw
+// linrec::cuda::ContractViolation (a std::runtime_error, like the
+// reference's, common.hpp:15-22) or std::invalid_argument / ::TypeError
+// equivalents for the other status codes.
+#pragma once
+
+#include <cstdint>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+
+#include "linrec_cuda.h"
+
+namespace linrec {
+namespace cuda {
+
+using index_t = std::int64_t;
+
+enum class ScanMode { Serial = LINREC_SERIAL, Parallel = LINREC_PARALLEL };
+
+class ContractViolation : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class DtypeError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class CudaError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+// [T, b, n] device tensor view (tensor.hpp:49-75 layout, not owned).
+template <class S>
+struct DeviceTensor3 {
+  S* data = nullptr;
+  index_t steps = 0, batch = 0, features = 0;
+  index_t step_size() const { return batch * features; }
+  bool same_shape(const DeviceTensor3& o) const {
+    return steps == o.steps && batch == o.batch && features == o.features;
+  }
+};
+
+// [b, n] device tensor view; data == nullptr means "zeros" (linrec_py.cpp:98-100).
+template <class S>
+struct DeviceTensor2 {
+  S* data = nullptr;
+  index_t rows = 0, cols = 0;
+};
+
+inline void throw_status(int rc) {
+  if (rc == LINREC_OK) return;
+  const std::string msg = linrec_last_error();
+  switch (rc) {
+    case LINREC_ERR_SHAPE:
+    case LINREC_ERR_NONFINITE:
+      throw ContractViolation(msg);
+    case LINREC_ERR_VALUE:
+      throw std::invalid_argument(msg);
+    case LINREC_ERR_DTYPE:
+      throw DtypeError(msg);
+    default:
+      throw CudaError(msg);
+  }
+}
+
+// check_same_shape (tensor.hpp:168-178) with the reference's message.
+template <class S, class U>
+void check_same_shape(const DeviceTensor3<S>& a, const DeviceTensor3<U>& b, const char* op) {
+  if (a.steps != b.steps || a.batch != b.batch || a.features != b.features) {
+    std::ostringstream os;
+    os << op << ": shape mismatch, [" << a.steps << "," << a.batch << "," << a.features
+       << "] vs [" << b.steps << "," << b.batch << "," << b.features << "]";
+    throw ContractViolation(os.str());
+  }
+}
+
+// validate_recurrence_shapes (recurrence.hpp:39-51).
+template <class S, class U, class V>
+void validate_recurrence_shapes(const DeviceTensor3<S>& decays, const DeviceTensor3<U>& impulses,
+                                const DeviceTensor2<V>& initial) {
+  check_same_shape(decays, impulses, "recurrence");
+  if (initial.data != nullptr && (initial.rows != decays.batch || initial.cols != decays.features)) {
+    std::ostringstream os;
+    os << "recurrence: initial state [" << initial.rows << "," << initial.cols
+       << "] does not match [" << decays.batch << "," << decays.features << "]";
+    throw ContractViolation(os.str());
+  }
+}
+
+namespace detail {
+inline int scan_call(const float* l, const float* x, const float* h0, float* h, index_t T,
+                     index_t W, int mode, linrec_workspace_t ws, void* st) {
+  return linrec_scan_f32(l, x, h0, h, T, W, mode, ws, st);
+}
+inline int scan_call(const double* l, const double* x, const double* h0, double* h, index_t T,
+                     index_t W, int mode, linrec_workspace_t ws, void* st) {
+  return linrec_scan_f64(l, x, h0, h, T, W, mode, ws, st);
+}
+inline int bwd_call(const float* l, const float* h0, const float* h, const float* dh, float* dl,
+                    float* dx, float* dh0, index_t T, index_t W, int mode, linrec_workspace_t ws,
+                    void* st) {
+  return linrec_scan_backward_f32(l, h0, h, dh, dl, dx, dh0, T, W, mode, ws, st);
+}
+inline int bwd_call(const double* l, const double* h0, const double* h, const double* dh,
+                    double* dl, double* dx, double* dh0, index_t T, index_t W, int mode,
+                    linrec_workspace_t ws, void* st) {
+  return linrec_scan_backward_f64(l, h0, h, dh, dl, dx, dh0, T, W, mode, ws, st);
+}
+}  // namespace detail
+
+// scan_serial (recurrence.hpp:169-179): bit-exact serial recurrence.
+template <class S>
+void scan_serial(const DeviceTensor3<S>& decays, const DeviceTensor3<S>& impulses,
+                 const DeviceTensor2<S>& initial, DeviceTensor3<S>& h, void* stream = nullptr) {
+  validate_recurrence_shapes(decays, impulses, initial);
+  check_same_shape(decays, h, "scan_serial(h)");
+  throw_status(detail::scan_call(decays.data, impulses.data, initial.data, h.data, decays.steps,
+                                 decays.step_size(), LINREC_SERIAL, nullptr, stream));
+}
+
+// scan_parallel (recurrence.hpp:193-245): single-pass chained scan.
+template <class S>
+void scan_parallel(const DeviceTensor3<S>& decays, const DeviceTensor3<S>& impulses,
+                   const DeviceTensor2<S>& initial, DeviceTensor3<S>& h, void* stream = nullptr,
+                   linrec_workspace_t ws = nullptr) {
+  validate_recurrence_shapes(decays, impulses, initial);
+  check_same_shape(decays, h, "scan_parallel(h)");
+  throw_status(detail::scan_call(decays.data, impulses.data, initial.data, h.data, decays.steps,
+                                 decays.step_size(), LINREC_PARALLEL, ws, stream));
+}
+
+// scan (recurrence.hpp:255-263): mode dispatch.
+template <class S>
+void scan(const DeviceTensor3<S>& decays, const DeviceTensor3<S>& impulses,
+          const DeviceTensor2<S>& initial, DeviceTensor3<S>& h, ScanMode mode,
+          void* stream = nullptr, linrec_workspace_t ws = nullptr) {
+  if (mode == ScanMode::Serial) return scan_serial(decays, impulses, initial, h, stream);
+  scan_parallel(decays, impulses, initial, h, stream, ws);
+}
+
+// RecurrenceGradients (recurrence.hpp:265-271) as output views.
+template <class S>
+struct RecurrenceGradients {
+  DeviceTensor3<S> d_decays;
+  DeviceTensor3<S> d_impulses;
+  DeviceTensor2<S> d_initial;
+};
+
+// scan_backward (recurrence.hpp:283-363).
+template <class S>
+void scan_backward(const DeviceTensor3<S>& decays, const DeviceTensor2<S>& initial,
+                   const DeviceTensor3<S>& h, const DeviceTensor3<S>& d_h,
+                   RecurrenceGradients<S>& grads, ScanMode mode, void* stream = nullptr,
+                   linrec_workspace_t ws = nullptr) {
+  check_same_shape(decays, h, "scan_backward(h)");
+  check_same_shape(decays, d_h, "scan_backward(d_h)");
+  validate_recurrence_shapes(decays, d_h, initial);
+  check_same_shape(decays, grads.d_decays, "scan_backward(d_decays)");
+  check_same_shape(decays, grads.d_impulses, "scan_backward(d_impulses)");
+  throw_status(detail::bwd_call(decays.data, initial.data, h.data, d_h.data, grads.d_decays.data,
+                                grads.d_impulses.data, grads.d_initial.data, decays.steps,
+                                decays.step_size(), static_cast<int>(mode), ws, stream));
+}
+
+}  // namespace cuda
+}  // namespace linrec

@@ -1,0 +1,180 @@
+/*
+ * linrec_cuda.h -- C ABI of the B200 (sm_100a) linear-recurrence scan.
+ *
+ *     h_t = lam_t (*) h_{t-1} + x_t            (forward scan)
+ *     G_t = lam_{t+1} (*) G_{t+1} + dh_t        (reverse-time backward scan)
+ *     dx_t = G_t,  dlam_t = h_{t-1} (*) G_t,  dh0 = lam_1 (*) G_1
+ *
+ * This is the drop-in boundary for the reference's recurrence hot path
+ * (/root/reference/proj/include/linrec/recurrence.hpp and its pybind11
+ * module proj/bindings/linrec_py.cpp).  Every entry point below names the
+ * reference interface it replaces.  Plain pointers and sizes only: no C++,
+ * no torch, no CUDA headers in the signatures (`stream` is a cudaStream_t
+ * passed as void*, NULL = legacy default stream).
+ *
+ * Layout (tensor.hpp:3-7, :49-75): every [T, batch, features] tensor is
+ * time-major, C-contiguous, so step t is the contiguous slab [t*W, (t+1)*W)
+ * with W = batch*features.  The library only sees (T, W).  [batch, features]
+ * tensors (h0, dh0) are W contiguous values.
+ *
+ * Ownership: the caller owns every data buffer.  The library owns only the
+ * look-back workspace (flags + chunk carries), either an explicit
+ * linrec_workspace_t or a per-(device, stream) default one.
+ *
+ * Errors: every function returns a linrec_status; a thread-local message is
+ * available from linrec_last_error().  Codes mirror the reference's error
+ * classes (bindings map them back to the same Python exceptions):
+ *   LINREC_ERR_SHAPE  -> ContractViolation / RuntimeError (recurrence.hpp:39-51, tensor.hpp:58)
+ *   LINREC_ERR_DTYPE  -> TypeError  (linrec_py.cpp:24-29, :82-89)
+ *   LINREC_ERR_VALUE  -> ValueError (linrec_py.cpp:35-37, :71-80)
+ *   LINREC_ERR_CUDA   -> RuntimeError (no CPU fallback exists)
+ *   LINREC_ERR_NONFINITE -> ContractViolation with the reference's
+ *                       "non-finite value in <name> at [t=.., b=.., n=..]"
+ *                       message (recurrence.hpp:133-163)
+ *
+ * Determinism: for fixed (T, W, dtype, mode) the results are bit-identical
+ * run to run (the decoupled look-back applies chunk carries in a fixed
+ * order).  mode LINREC_SERIAL is additionally bit-identical
+ * to the reference's scan_serial / ScanMode::Serial backward on an
+ * FMA-contracting x86-64 build.
+ */
+#ifndef LINREC_CUDA_H_
+#define LINREC_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define LINREC_ABI_VERSION 1
+
+typedef enum linrec_status {
+  LINREC_OK = 0,
+  LINREC_ERR_SHAPE = 1,
+  LINREC_ERR_DTYPE = 2,
+  LINREC_ERR_VALUE = 3,
+  LINREC_ERR_CUDA = 4,
+  LINREC_ERR_NONFINITE = 5,
+  LINREC_ERR_INTERNAL = 6
+} linrec_status;
+
+/* ScanMode (recurrence.hpp:25).  LINREC_SERIAL runs the per-channel serial
+ * kernel (bit-exact anchor); LINREC_PARALLEL the single-pass chained scan. */
+typedef enum linrec_mode { LINREC_SERIAL = 0, LINREC_PARALLEL = 1 } linrec_mode;
+
+typedef struct linrec_workspace* linrec_workspace_t;
+
+/* ---- library ---------------------------------------------------------- */
+int linrec_abi_version(void);
+const char* linrec_last_error(void);
+/* Number of CUDA devices visible (0 when none); never falls back to a CPU. */
+int linrec_device_count(void);
+
+/* Device memory for callers without their own allocator (the Python
+ * bindings' DeviceArray).  Stream-ordered on `stream`. */
+int linrec_device_malloc(void** ptr, size_t bytes, int device, void* stream);
+int linrec_device_free(void* ptr, int device, void* stream);
+
+/* ---- workspace --------------------------------------------------------- *
+ * Look-back state for the chained scans: a control block (epoch, ticket and
+ * retirement counters), per-chunk status flags and per-chunk carries.  Grows
+ * on demand, stream-ordered.  One workspace must not be used by two streams
+ * concurrently; ws == NULL in the scan calls selects a library-owned
+ * workspace keyed by (current device, stream). */
+int linrec_workspace_create(linrec_workspace_t* ws, int device);
+int linrec_workspace_destroy(linrec_workspace_t ws);
+/* Bytes a chained scan of (T, W) in `dtype_bytes` (4 or 8) needs. */
+size_t linrec_workspace_bytes(int64_t T, int64_t W, int dtype_bytes);
+
+/* ---- forward scan, device pointers ------------------------------------- *
+ * Replaces linrec::scan_serial (recurrence.hpp:169-179), scan_parallel
+ * (:193-245) and scan (:255-263) -- and the compute of linrec.scan,
+ * linrec_py.cpp:91-116.  lam, x, h: [T][W]; h0: [W] or NULL (= zeros,
+ * linrec_py.cpp:98-100).  Asynchronous on `stream`.  T >= 1, W >= 1. */
+int linrec_scan_f32(const float* lam, const float* x, const float* h0,
+                    float* h, int64_t T, int64_t W, int mode,
+                    linrec_workspace_t ws, void* stream);
+int linrec_scan_f64(const double* lam, const double* x, const double* h0,
+                    double* h, int64_t T, int64_t W, int mode,
+                    linrec_workspace_t ws, void* stream);
+
+/* ---- backward scan, device pointers ------------------------------------ *
+ * Replaces linrec::scan_backward / detail::scan_backward_impl
+ * (recurrence.hpp:283-377) and the compute of linrec.scan_backward
+ * (linrec_py.cpp:118-140).  Inputs lam, h, dh: [T][W]; h0: [W] or NULL.
+ * Outputs dlam, dx: [T][W]; dh0: [W].  Does not read x (the reference does
+ * not either, recurrence.hpp:273-282).  No reversed copies are made. */
+int linrec_scan_backward_f32(const float* lam, const float* h0,
+                             const float* h, const float* dh, float* dlam,
+                             float* dx, float* dh0, int64_t T, int64_t W,
+                             int mode, linrec_workspace_t ws, void* stream);
+int linrec_scan_backward_f64(const double* lam, const double* h0,
+                             const double* h, const double* dh, double* dlam,
+                             double* dx, double* dh0, int64_t T, int64_t W,
+                             int mode, linrec_workspace_t ws, void* stream);
+
+/* Segment form of the backward scan (no reference counterpart: it is what
+ * the reference's phase-2/phase-3 stitching does across chunk boundaries,
+ * recurrence.hpp:219-237, lifted to the caller so a sequence can be split
+ * across host chunks or GPUs).  The segment [0,T) is followed by a row whose
+ * decay is lam_next[W] and whose gradient state is g_next[W] (both NULL =
+ * the true end of the sequence, G_T := 0).  G_{T-1} = lam_next*g_next +
+ * dh_{T-1} is evaluated as one fused multiply-add, as in the unsplit scan,
+ * so LINREC_SERIAL stays bit-exact when chained. */
+int linrec_scan_backward_segment_f32(const float* lam, const float* h0,
+                                     const float* h, const float* dh,
+                                     const float* lam_next,
+                                     const float* g_next, float* dlam,
+                                     float* dx, float* dh0, int64_t T,
+                                     int64_t W, int mode,
+                                     linrec_workspace_t ws, void* stream);
+int linrec_scan_backward_segment_f64(const double* lam, const double* h0,
+                                     const double* h, const double* dh,
+                                     const double* lam_next,
+                                     const double* g_next, double* dlam,
+                                     double* dx, double* dh0, int64_t T,
+                                     int64_t W, int mode,
+                                     linrec_workspace_t ws, void* stream);
+
+/* ---- host-pointer entry points (the numpy boundary) --------------------- *
+ * Same semantics with HOST buffers: the call stages T-chunks host->device,
+ * scans each chunk seeded with the previous chunk's carry, and copies results
+ * back, overlapping the three on separate streams (full-duplex PCIe/C2C).
+ * Page-locked (pinned) buffers run fully asynchronous; pageable buffers work
+ * but are staged by the driver.  Synchronous: returns when the outputs are in
+ * host memory.  `device` selects the GPU. */
+int linrec_scan_host_f32(const float* lam, const float* x, const float* h0,
+                         float* h, int64_t T, int64_t W, int mode,
+                         int device);
+int linrec_scan_host_f64(const double* lam, const double* x,
+                         const double* h0, double* h, int64_t T, int64_t W,
+                         int mode, int device);
+int linrec_scan_backward_host_f32(const float* lam, const float* h0,
+                                  const float* h, const float* dh,
+                                  float* dlam, float* dx, float* dh0,
+                                  int64_t T, int64_t W, int mode, int device);
+int linrec_scan_backward_host_f64(const double* lam, const double* h0,
+                                  const double* h, const double* dh,
+                                  double* dlam, double* dx, double* dh0,
+                                  int64_t T, int64_t W, int mode, int device);
+
+/* ---- finite screening (recurrence.hpp:133-163) -------------------------- *
+ * Index of the first non-finite element of v[n] (device pointer), or -1.
+ * Synchronous on `stream`. */
+int linrec_first_nonfinite_f32(const float* v, int64_t n, int64_t* index,
+                               void* stream);
+int linrec_first_nonfinite_f64(const double* v, int64_t n, int64_t* index,
+                               void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* LINREC_CUDA_H_ */

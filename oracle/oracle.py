@@ -235,6 +235,7 @@ class RefLib:
         lib.ref_rng_first.restype = C.c_uint64
         lib.ref_rng_first.argtypes = [C.c_uint64, C.c_int]
         lib.ref_hardware_workers.restype = C.c_int
+        lib.ref_bench_fwd_bwd_f32.argtypes = [_vp] * 4 + [_i64] * 3 + [C.c_int] * 3 + [_vp, _vp]
 
     def _check(self, rc):
         if rc != 0:
@@ -276,6 +277,18 @@ class RefLib:
 
     def rng_first(self, seed, which):
         return int(self.lib.ref_rng_first(seed, which))
+
+    def bench_fwd_bwd(self, lam, x, h0, dh, workers, warmup=1, reps=5):
+        """Median seconds of (scan_parallel, scan_backward(Parallel)) on the
+        host cores, reference bench protocol (bench.hpp:93-107)."""
+        lam, x, h0, dh = (np.ascontiguousarray(a, dtype=np.float32) for a in (lam, x, h0, dh))
+        T, b, n = lam.shape
+        f = C.c_double(0.0)
+        bw = C.c_double(0.0)
+        self._check(self.lib.ref_bench_fwd_bwd_f32(
+            _ptr(lam), _ptr(x), _ptr(h0), _ptr(dh), T, b, n, workers, warmup, reps,
+            C.byref(f), C.byref(bw)))
+        return f.value, bw.value
 
     def hardware_workers(self):
         return int(self.lib.ref_hardware_workers())

@@ -8,6 +8,8 @@
 // reference bit for bit, and so bench.py can time the reference's own CPU
 // path (cpu_baseline kind "reference").
 #include <algorithm>
+#include <chrono>
+#include <vector>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -124,4 +126,51 @@ uint64_t ref_rng_first(uint64_t seed, int which) {
   return v;
 }
 int ref_hardware_workers() { return linrec::ThreadPool::hardware_workers(); }
+
+// The reference's own kernel-bench protocol (bench.hpp:93-107, :160-202):
+// inputs built once outside the timed region, one ThreadPool(workers) and one
+// plan_chunks(T, workers) reused, `warmup` untimed calls, then the median of
+// `reps` steady_clock-timed calls of scan_parallel (forward) and of
+// scan_backward(ScanMode::Parallel) (backward).  Output allocation inside the
+// scan_* calls is timed, as in the reference.
+int ref_bench_fwd_bwd_f32(const float* lam, const float* x, const float* h0,
+                          const float* dh, int64_t T, int64_t b, int64_t n,
+                          int workers, int warmup, int reps, double* fwd_s,
+                          double* bwd_s) {
+  try {
+    auto L = t3(lam, T, b, n);
+    auto X = t3(x, T, b, n);
+    auto DH = t3(dh, T, b, n);
+    auto H0 = t2(h0, b, n);
+    linrec::ThreadPool pool(workers);
+    const linrec::ChunkPlan plan = linrec::plan_chunks(T, workers);
+    linrec::Tensor3<float> h;
+    linrec::RecurrenceGradients<float> g;
+    auto median = [](std::vector<double> v) {
+      std::sort(v.begin(), v.end());
+      const size_t m = v.size() / 2;
+      return v.size() % 2 ? v[m] : 0.5 * (v[m - 1] + v[m]);
+    };
+    for (int i = 0; i < warmup; ++i) {
+      h = linrec::scan_parallel(L, X, H0, plan, pool);
+      g = linrec::scan_backward(L, H0, h, DH, linrec::ScanMode::Parallel, pool);
+    }
+    std::vector<double> tf, tb;
+    for (int i = 0; i < reps; ++i) {
+      const auto t0 = std::chrono::steady_clock::now();
+      h = linrec::scan_parallel(L, X, H0, plan, pool);
+      const auto t1 = std::chrono::steady_clock::now();
+      g = linrec::scan_backward(L, H0, h, DH, linrec::ScanMode::Parallel, pool);
+      const auto t2 = std::chrono::steady_clock::now();
+      tf.push_back(std::chrono::duration<double>(t1 - t0).count());
+      tb.push_back(std::chrono::duration<double>(t2 - t1).count());
+    }
+    *fwd_s = median(tf);
+    *bwd_s = median(tb);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
 }

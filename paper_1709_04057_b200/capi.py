@@ -1,0 +1,134 @@
+"""ctypes binding of the C ABI (include/linrec_cuda.h) for device-pointer use.
+
+This is the boundary a Python host (bench.py, the sharded driver, tests) uses
+to call the sm_100a kernels on buffers it already owns -- e.g. torch CUDA
+tensors -- on a given CUDA stream.  It loads ``liblinrec_cuda.so`` from this
+package directory and raises ``ImportError`` when it is missing: there is no
+CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblinrec_cuda.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "linrec_cuda.h")
+
+SERIAL = 0
+PARALLEL = 1
+
+OK, ERR_SHAPE, ERR_DTYPE, ERR_VALUE, ERR_CUDA, ERR_NONFINITE, ERR_INTERNAL = range(7)
+
+_vp = C.c_void_p
+_i64 = C.c_int64
+_int = C.c_int
+
+
+class LinrecError(RuntimeError):
+    """A non-zero linrec_status; ``code`` is the status."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "
+            "linrec has no CPU path")
+    lib = C.CDLL(LIB_PATH)
+    lib.linrec_last_error.restype = C.c_char_p
+    lib.linrec_abi_version.restype = _int
+    lib.linrec_device_count.restype = _int
+    lib.linrec_workspace_bytes.restype = C.c_size_t
+    lib.linrec_workspace_bytes.argtypes = [_i64, _i64, _int]
+    lib.linrec_workspace_create.argtypes = [C.POINTER(_vp), _int]
+    lib.linrec_workspace_destroy.argtypes = [_vp]
+    lib.linrec_device_malloc.argtypes = [C.POINTER(_vp), C.c_size_t, _int, _vp]
+    lib.linrec_device_free.argtypes = [_vp, _int, _vp]
+    for s in ("f32", "f64"):
+        getattr(lib, f"linrec_scan_{s}").argtypes = [_vp] * 4 + [_i64, _i64, _int, _vp, _vp]
+        getattr(lib, f"linrec_scan_backward_{s}").argtypes = [_vp] * 7 + [_i64, _i64, _int, _vp, _vp]
+        getattr(lib, f"linrec_scan_backward_segment_{s}").argtypes = [_vp] * 9 + [_i64, _i64, _int, _vp, _vp]
+        getattr(lib, f"linrec_scan_host_{s}").argtypes = [_vp] * 4 + [_i64, _i64, _int, _int]
+        getattr(lib, f"linrec_scan_backward_host_{s}").argtypes = [_vp] * 7 + [_i64, _i64, _int, _int]
+        getattr(lib, f"linrec_first_nonfinite_{s}").argtypes = [_vp, _i64, C.POINTER(_i64), _vp]
+    return lib
+
+
+lib = _load()
+
+
+def declared_symbols(header: str = HEADER):
+    """Function names declared in include/linrec_cuda.h."""
+    with open(header) as f:
+        text = f.read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(linrec_[a-z0-9_]+)\s*\(", text)))
+
+
+def check(rc: int):
+    if rc != OK:
+        raise LinrecError(rc, lib.linrec_last_error().decode())
+
+
+def _sfx(dtype_bytes: int) -> str:
+    if dtype_bytes == 4:
+        return "f32"
+    if dtype_bytes == 8:
+        return "f64"
+    raise TypeError("decays must be float32 or float64")
+
+
+def scan(lam, x, h0, h, T, W, mode=PARALLEL, dtype_bytes=4, ws=None, stream=0):
+    """Device pointers (ints) -> linrec_scan_{f32,f64}."""
+    check(getattr(lib, f"linrec_scan_{_sfx(dtype_bytes)}")(lam, x, h0, h, T, W, mode, ws, stream))
+
+
+def scan_backward(lam, h0, h, dh, dlam, dx, dh0, T, W, mode=PARALLEL, dtype_bytes=4, ws=None, stream=0):
+    check(getattr(lib, f"linrec_scan_backward_{_sfx(dtype_bytes)}")(
+        lam, h0, h, dh, dlam, dx, dh0, T, W, mode, ws, stream))
+
+
+def scan_backward_segment(lam, h0, h, dh, lam_next, g_next, dlam, dx, dh0, T, W, mode=PARALLEL,
+                          dtype_bytes=4, ws=None, stream=0):
+    check(getattr(lib, f"linrec_scan_backward_segment_{_sfx(dtype_bytes)}")(
+        lam, h0, h, dh, lam_next, g_next, dlam, dx, dh0, T, W, mode, ws, stream))
+
+
+def scan_host(lam, x, h0, h, T, W, mode=PARALLEL, dtype_bytes=4, device=0):
+    """Host pointers -> linrec_scan_host_* (pipelined H2D / scan / D2H)."""
+    check(getattr(lib, f"linrec_scan_host_{_sfx(dtype_bytes)}")(lam, x, h0, h, T, W, mode, device))
+
+
+def scan_backward_host(lam, h0, h, dh, dlam, dx, dh0, T, W, mode=PARALLEL, dtype_bytes=4, device=0):
+    check(getattr(lib, f"linrec_scan_backward_host_{_sfx(dtype_bytes)}")(
+        lam, h0, h, dh, dlam, dx, dh0, T, W, mode, device))
+
+
+def first_nonfinite(v, n, dtype_bytes=4, stream=0) -> int:
+    out = _i64(-1)
+    check(getattr(lib, f"linrec_first_nonfinite_{_sfx(dtype_bytes)}")(v, n, C.byref(out), stream))
+    return int(out.value)
+
+
+class Workspace:
+    """Explicit look-back workspace (one per concurrent stream)."""
+
+    def __init__(self, device: int = 0):
+        self.handle = _vp()
+        check(lib.linrec_workspace_create(C.byref(self.handle), device))
+
+    def close(self):
+        if self.handle:
+            lib.linrec_workspace_destroy(self.handle)
+            self.handle = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,544 @@
+// extern "C" implementation of include/linrec_cuda.h: argument validation
+// with the reference's error classes, workspace management, dispatch to the
+// sm_100a kernels, and the pipelined host-pointer path.  There is no CPU
+// compute path anywhere in this library: without a CUDA device every entry
+// point fails with LINREC_ERR_CUDA.
+#include "linrec_cuda.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "launch.h"
+
+using linrec_impl::BwdCall;
+using linrec_impl::ChainPlan;
+using linrec_impl::ChainPtrs;
+using linrec_impl::FwdCall;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+namespace {
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  std::ostringstream os;
+  os << "linrec: CUDA error in " << where << ": " << cudaGetErrorName(e) << " ("
+     << cudaGetErrorString(e) << ")";
+  return fail(LINREC_ERR_CUDA, os.str());
+}
+
+#define LINREC_CUDA_TRY(expr)                            \
+  do {                                                   \
+    cudaError_t e_ = (expr);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr);  \
+  } while (0)
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <class S>
+constexpr int vec_of() {
+  return sizeof(S) == 4 ? 4 : 2;
+}
+
+// 128-bit paths need W % VEC == 0 and 16-byte aligned rows.
+template <class S>
+bool vec_ok(int64_t W, std::initializer_list<const void*> ptrs) {
+  if (W % vec_of<S>() != 0) return false;
+  for (const void* p : ptrs)
+    if (p != nullptr && !aligned16(p)) return false;
+  return true;
+}
+
+// Reference contract: every dimension >= 1 (tensor.hpp:58) -- a [T, b, n]
+// tensor with T == 0 cannot be constructed.
+int check_dims(int64_t T, int64_t W) {
+  if (T < 1 || W < 1) {
+    std::ostringstream os;
+    os << "Tensor3 dimensions must be >= 1 (got T=" << T << ", W=" << W << ")";
+    return fail(LINREC_ERR_SHAPE, os.str());
+  }
+  return LINREC_OK;
+}
+
+int check_mode(int mode) {
+  if (mode != LINREC_SERIAL && mode != LINREC_PARALLEL)
+    return fail(LINREC_ERR_VALUE, "mode must be \"parallel\" or \"serial\"");
+  return LINREC_OK;
+}
+
+int check_ptr(const void* p, const char* name) {
+  if (p == nullptr) return fail(LINREC_ERR_VALUE, std::string(name) + " must not be NULL");
+  return LINREC_OK;
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// workspace
+// ---------------------------------------------------------------------------
+struct linrec_workspace {
+  int device = 0;
+  void* base = nullptr;
+  size_t cap = 0;
+  std::mutex mu;
+};
+
+namespace {
+constexpr size_t kCtrlBytes = 256;
+
+// Grows `ws` to at least `bytes`, stream-ordered.  A fresh buffer is zeroed
+// and its control block initialised (epoch 1) on `st`.
+int ws_reserve(linrec_workspace* ws, size_t bytes, cudaStream_t st) {
+  if (ws->base != nullptr && ws->cap >= bytes) return LINREC_OK;
+  if (ws->base != nullptr) {
+    LINREC_CUDA_TRY(cudaFreeAsync(ws->base, st));
+    ws->base = nullptr;
+    ws->cap = 0;
+  }
+  const size_t cap = std::max<size_t>(bytes, size_t(1) << 20);
+  LINREC_CUDA_TRY(cudaMallocAsync(&ws->base, cap, st));
+  LINREC_CUDA_TRY(cudaMemsetAsync(ws->base, 0, cap, st));
+  LINREC_CUDA_TRY(linrec_impl::launch_ws_init(ws->base, st));
+  ws->cap = cap;
+  return LINREC_OK;
+}
+
+ChainPtrs ws_ptrs(linrec_workspace* ws, const ChainPlan& p) {
+  char* b = static_cast<char*>(ws->base);
+  ChainPtrs w;
+  w.ctrl = b;
+  w.flags = b + kCtrlBytes;
+  w.agg = b + kCtrlBytes + p.flags_bytes;
+  w.inc = b + kCtrlBytes + p.flags_bytes + p.rec_bytes;
+  return w;
+}
+
+std::mutex g_default_mu;
+std::map<std::pair<int, cudaStream_t>, std::unique_ptr<linrec_workspace>> g_default_ws;
+
+int current_device(int* dev) {
+  LINREC_CUDA_TRY(cudaGetDevice(dev));
+  return LINREC_OK;
+}
+
+linrec_workspace* default_ws(int device, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_default_mu);
+  auto& slot = g_default_ws[{device, st}];
+  if (!slot) {
+    slot.reset(new linrec_workspace());
+    slot->device = device;
+  }
+  return slot.get();
+}
+
+// ---------------------------------------------------------------------------
+// device-pointer scans
+// ---------------------------------------------------------------------------
+template <class S>
+int scan_device(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W, int mode,
+                linrec_workspace_t ws, cudaStream_t st) {
+  int rc;
+  if ((rc = check_dims(T, W)) || (rc = check_mode(mode)) || (rc = check_ptr(lam, "decays")) ||
+      (rc = check_ptr(x, "impulses")) || (rc = check_ptr(h, "h")))
+    return rc;
+  const bool vok = vec_ok<S>(W, {lam, x, h0, h});
+  FwdCall<S> c{lam, x, h0, h, T, W};
+  if (mode == LINREC_SERIAL) {
+    LINREC_CUDA_TRY(linrec_impl::launch_serial_fwd<S>(c, vok, st));
+    return LINREC_OK;
+  }
+  int dev;
+  if ((rc = current_device(&dev))) return rc;
+  linrec_workspace* w = ws ? ws : default_ws(dev, st);
+  std::lock_guard<std::mutex> lk(w->mu);
+  const ChainPlan p = linrec_impl::plan_chain<S>(true, T, W, vok);
+  if (p.ntiles > 0x7fffffffLL) return fail(LINREC_ERR_SHAPE, "linrec: problem too large for one launch");
+  if ((rc = ws_reserve(w, p.ws_bytes, st))) return rc;
+  LINREC_CUDA_TRY(linrec_impl::launch_chain_fwd<S>(p, c, ws_ptrs(w, p), st));
+  return LINREC_OK;
+}
+
+template <class S>
+int scan_backward_device(const S* lam, const S* h0, const S* h, const S* dh, const S* lam_next,
+                         const S* g_next, S* dlam, S* dx, S* dh0, int64_t T, int64_t W, int mode,
+                         linrec_workspace_t ws, cudaStream_t st) {
+  int rc;
+  if ((rc = check_dims(T, W)) || (rc = check_mode(mode)) || (rc = check_ptr(lam, "decays")) ||
+      (rc = check_ptr(h, "h")) || (rc = check_ptr(dh, "d_h")) || (rc = check_ptr(dlam, "d_decays")) ||
+      (rc = check_ptr(dx, "d_impulses")))
+    return rc;
+  const bool vok = vec_ok<S>(W, {lam, h0, h, dh, lam_next, g_next, dlam, dx, dh0});
+  BwdCall<S> c{lam, h0, h, dh, lam_next, g_next, dlam, dx, dh0, T, W};
+  if (mode == LINREC_SERIAL) {
+    LINREC_CUDA_TRY(linrec_impl::launch_serial_bwd<S>(c, vok, st));
+    return LINREC_OK;
+  }
+  int dev;
+  if ((rc = current_device(&dev))) return rc;
+  linrec_workspace* w = ws ? ws : default_ws(dev, st);
+  std::lock_guard<std::mutex> lk(w->mu);
+  const ChainPlan p = linrec_impl::plan_chain<S>(false, T, W, vok);
+  if (p.ntiles > 0x7fffffffLL) return fail(LINREC_ERR_SHAPE, "linrec: problem too large for one launch");
+  if ((rc = ws_reserve(w, p.ws_bytes, st))) return rc;
+  LINREC_CUDA_TRY(linrec_impl::launch_chain_bwd<S>(p, c, ws_ptrs(w, p), st));
+  return LINREC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host-pointer pipeline
+// ---------------------------------------------------------------------------
+constexpr int kSlots = 3;
+constexpr size_t kChunkBytes = size_t(64) << 20;  // per array per chunk
+
+struct HostPipe {
+  int device = -1;
+  cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
+  cudaEvent_t ev_in[kSlots], ev_comp[kSlots], ev_out[kSlots];
+  void* buf[kSlots][3] = {};
+  size_t buf_bytes = 0;
+  void* small = nullptr;  // h0 / dh0 staging, 2 rows
+  size_t small_bytes = 0;
+  linrec_workspace ws;
+  std::mutex mu;
+};
+
+std::mutex g_pipe_mu;
+std::map<int, std::unique_ptr<HostPipe>> g_pipes;
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int pipe_for(int device, HostPipe** out) {
+  std::lock_guard<std::mutex> lk(g_pipe_mu);
+  auto& p = g_pipes[device];
+  if (!p) {
+    std::unique_ptr<HostPipe> n(new HostPipe());
+    n->device = device;
+    n->ws.device = device;
+    LINREC_CUDA_TRY(cudaStreamCreateWithFlags(&n->s_in, cudaStreamNonBlocking));
+    LINREC_CUDA_TRY(cudaStreamCreateWithFlags(&n->s_comp, cudaStreamNonBlocking));
+    LINREC_CUDA_TRY(cudaStreamCreateWithFlags(&n->s_out, cudaStreamNonBlocking));
+    for (int i = 0; i < kSlots; ++i) {
+      LINREC_CUDA_TRY(cudaEventCreateWithFlags(&n->ev_in[i], cudaEventDisableTiming));
+      LINREC_CUDA_TRY(cudaEventCreateWithFlags(&n->ev_comp[i], cudaEventDisableTiming));
+      LINREC_CUDA_TRY(cudaEventCreateWithFlags(&n->ev_out[i], cudaEventDisableTiming));
+    }
+    p = std::move(n);
+  }
+  *out = p.get();
+  return LINREC_OK;
+}
+
+int pipe_reserve(HostPipe* hp, size_t bytes, size_t small_bytes) {
+  if (bytes > hp->buf_bytes) {
+    LINREC_CUDA_TRY(cudaDeviceSynchronize());
+    for (int i = 0; i < kSlots; ++i)
+      for (int j = 0; j < 3; ++j) {
+        if (hp->buf[i][j]) LINREC_CUDA_TRY(cudaFree(hp->buf[i][j]));
+        hp->buf[i][j] = nullptr;
+      }
+    hp->buf_bytes = 0;
+    for (int i = 0; i < kSlots; ++i)
+      for (int j = 0; j < 3; ++j) LINREC_CUDA_TRY(cudaMalloc(&hp->buf[i][j], bytes));
+    hp->buf_bytes = bytes;
+  }
+  if (small_bytes > hp->small_bytes) {
+    if (hp->small) LINREC_CUDA_TRY(cudaFree(hp->small));
+    hp->small = nullptr;
+    LINREC_CUDA_TRY(cudaMalloc(&hp->small, small_bytes));
+    hp->small_bytes = small_bytes;
+  }
+  return LINREC_OK;
+}
+
+int64_t chunk_rows(int64_t T, int64_t W, size_t elem) {
+  const int64_t rows = (int64_t)(kChunkBytes / (size_t(W) * elem));
+  return std::max<int64_t>(1, std::min<int64_t>(T, rows));
+}
+
+template <class S>
+int scan_host(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W, int mode,
+              int device) {
+  int rc;
+  if ((rc = check_dims(T, W)) || (rc = check_mode(mode)) || (rc = check_ptr(lam, "decays")) ||
+      (rc = check_ptr(x, "impulses")) || (rc = check_ptr(h, "h")))
+    return rc;
+  DeviceGuard dg(device);
+  HostPipe* hp;
+  if ((rc = pipe_for(device, &hp))) return rc;
+  std::lock_guard<std::mutex> lk(hp->mu);
+  const int64_t Tc = chunk_rows(T, W, sizeof(S));
+  const size_t row = size_t(W) * sizeof(S);
+  if ((rc = pipe_reserve(hp, size_t(Tc) * row, 2 * row))) return rc;
+  S* d_h0 = nullptr;
+  if (h0) {
+    d_h0 = static_cast<S*>(hp->small);
+    LINREC_CUDA_TRY(cudaMemcpyAsync(d_h0, h0, row, cudaMemcpyHostToDevice, hp->s_comp));
+  }
+  const int64_t nchunks = (T + Tc - 1) / Tc;
+  const S* seed = d_h0;
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const int s = int(k % kSlots);
+    const int64_t t0 = k * Tc, rows = std::min<int64_t>(Tc, T - t0);
+    S* dl = static_cast<S*>(hp->buf[s][0]);
+    S* dxv = static_cast<S*>(hp->buf[s][1]);
+    S* dhv = static_cast<S*>(hp->buf[s][2]);
+    const size_t bytes = size_t(rows) * row;
+    if (k >= kSlots) LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_in, hp->ev_comp[s], 0));
+    LINREC_CUDA_TRY(cudaMemcpyAsync(dl, lam + t0 * W, bytes, cudaMemcpyHostToDevice, hp->s_in));
+    LINREC_CUDA_TRY(cudaMemcpyAsync(dxv, x + t0 * W, bytes, cudaMemcpyHostToDevice, hp->s_in));
+    LINREC_CUDA_TRY(cudaEventRecord(hp->ev_in[s], hp->s_in));
+    LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_comp, hp->ev_in[s], 0));
+    if (k >= kSlots) LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_comp, hp->ev_out[s], 0));
+    if ((rc = scan_device<S>(dl, dxv, seed, dhv, rows, W, mode, &hp->ws, hp->s_comp))) return rc;
+    LINREC_CUDA_TRY(cudaEventRecord(hp->ev_comp[s], hp->s_comp));
+    LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_out, hp->ev_comp[s], 0));
+    LINREC_CUDA_TRY(cudaMemcpyAsync(h + t0 * W, dhv, bytes, cudaMemcpyDeviceToHost, hp->s_out));
+    LINREC_CUDA_TRY(cudaEventRecord(hp->ev_out[s], hp->s_out));
+    seed = dhv + (rows - 1) * W;  // carry into the next chunk
+  }
+  LINREC_CUDA_TRY(cudaStreamSynchronize(hp->s_out));
+  LINREC_CUDA_TRY(cudaStreamSynchronize(hp->s_comp));
+  return LINREC_OK;
+}
+
+template <class S>
+int scan_backward_host(const S* lam, const S* h0, const S* h, const S* dh, S* dlam, S* dx, S* dh0,
+                       int64_t T, int64_t W, int mode, int device) {
+  int rc;
+  if ((rc = check_dims(T, W)) || (rc = check_mode(mode)) || (rc = check_ptr(lam, "decays")) ||
+      (rc = check_ptr(h, "h")) || (rc = check_ptr(dh, "d_h")) || (rc = check_ptr(dlam, "d_decays")) ||
+      (rc = check_ptr(dx, "d_impulses")) || (rc = check_ptr(dh0, "d_initial")))
+    return rc;
+  DeviceGuard dg(device);
+  HostPipe* hp;
+  if ((rc = pipe_for(device, &hp))) return rc;
+  std::lock_guard<std::mutex> lk(hp->mu);
+  const int64_t Tc = chunk_rows(T, W, sizeof(S));
+  const size_t row = size_t(W) * sizeof(S);
+  // per slot: buf0 = [lam | dlam], buf1 = [h shifted by one row | dx],
+  // buf2 = [dh]; each half holds Tc rows.
+  if ((rc = pipe_reserve(hp, size_t(2) * size_t(Tc) * row, 3 * row))) return rc;
+  S* d_h0 = static_cast<S*>(hp->small);
+  S* d_dh0 = d_h0 + W;
+  if (h0) LINREC_CUDA_TRY(cudaMemcpyAsync(d_h0, h0, row, cudaMemcpyHostToDevice, hp->s_comp));
+  else LINREC_CUDA_TRY(cudaMemsetAsync(d_h0, 0, row, hp->s_comp));
+  const int64_t nchunks = (T + Tc - 1) / Tc;
+  const S* lam_next = nullptr;
+  const S* g_next = nullptr;
+  for (int64_t i = 0; i < nchunks; ++i) {
+    const int64_t k = nchunks - 1 - i;  // reverse time
+    const int s = int(i % kSlots);
+    const int64_t t0 = k * Tc, rows = std::min<int64_t>(Tc, T - t0);
+    const size_t bytes = size_t(rows) * row;
+    S* b0 = static_cast<S*>(hp->buf[s][0]);
+    S* b1 = static_cast<S*>(hp->buf[s][1]);
+    S* b2 = static_cast<S*>(hp->buf[s][2]);
+    S* d_lam = b0;
+    S* d_dlam = b0 + Tc * W;
+    S* d_h = b1;  // rows t0-1 .. t0+rows-2 (or 0 .. rows-2 for t0 == 0)
+    S* d_dx = b1 + Tc * W;
+    S* d_dh = b2;
+    // slot s was last filled at chunk i-3, whose lam row 0 and G row 0 are
+    // also read by chunk i-2 (lam_next / g_next): wait for that compute.
+    if (i >= kSlots)
+      LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_in, hp->ev_comp[(i - 2) % kSlots], 0));
+    LINREC_CUDA_TRY(cudaMemcpyAsync(d_lam, lam + t0 * W, bytes, cudaMemcpyHostToDevice, hp->s_in));
+    LINREC_CUDA_TRY(cudaMemcpyAsync(d_dh, dh + t0 * W, bytes, cudaMemcpyHostToDevice, hp->s_in));
+    const S* hprev_row;
+    const S* hrows;
+    if (t0 > 0) {
+      LINREC_CUDA_TRY(cudaMemcpyAsync(d_h, h + (t0 - 1) * W, bytes, cudaMemcpyHostToDevice, hp->s_in));
+      hprev_row = d_h;
+      hrows = d_h + W;
+    } else {
+      if (rows > 1)
+        LINREC_CUDA_TRY(cudaMemcpyAsync(d_h, h, bytes - row, cudaMemcpyHostToDevice, hp->s_in));
+      hprev_row = d_h0;
+      hrows = d_h;
+    }
+    LINREC_CUDA_TRY(cudaEventRecord(hp->ev_in[s], hp->s_in));
+    LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_comp, hp->ev_in[s], 0));
+    if (i >= kSlots) LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_comp, hp->ev_out[s], 0));
+    if ((rc = scan_backward_device<S>(d_lam, hprev_row, hrows, d_dh, lam_next, g_next, d_dlam, d_dx,
+                                      k == 0 ? d_dh0 : nullptr, rows, W, mode, &hp->ws, hp->s_comp)))
+      return rc;
+    LINREC_CUDA_TRY(cudaEventRecord(hp->ev_comp[s], hp->s_comp));
+    LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_out, hp->ev_comp[s], 0));
+    LINREC_CUDA_TRY(cudaMemcpyAsync(dlam + t0 * W, d_dlam, bytes, cudaMemcpyDeviceToHost, hp->s_out));
+    LINREC_CUDA_TRY(cudaMemcpyAsync(dx + t0 * W, d_dx, bytes, cudaMemcpyDeviceToHost, hp->s_out));
+    if (k == 0) LINREC_CUDA_TRY(cudaMemcpyAsync(dh0, d_dh0, row, cudaMemcpyDeviceToHost, hp->s_out));
+    LINREC_CUDA_TRY(cudaEventRecord(hp->ev_out[s], hp->s_out));
+    lam_next = d_lam;  // lam at row t0 and G at row t0 feed the previous chunk
+    g_next = d_dx;
+  }
+  LINREC_CUDA_TRY(cudaStreamSynchronize(hp->s_out));
+  LINREC_CUDA_TRY(cudaStreamSynchronize(hp->s_comp));
+  return LINREC_OK;
+}
+
+template <class S>
+int first_nonfinite(const S* v, int64_t n, int64_t* index, cudaStream_t st) {
+  int rc;
+  if ((rc = check_ptr(index, "index"))) return rc;
+  if (n > 0 && (rc = check_ptr(v, "v"))) return rc;
+  LINREC_CUDA_TRY(linrec_impl::first_nonfinite<S>(v, n, index, st));
+  return LINREC_OK;
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// exported symbols
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int linrec_abi_version(void) { return LINREC_ABI_VERSION; }
+const char* linrec_last_error(void) { return g_last_error.c_str(); }
+
+int linrec_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int linrec_device_malloc(void** ptr, size_t bytes, int device, void* stream) {
+  int rc;
+  if ((rc = check_ptr(ptr, "ptr"))) return rc;
+  DeviceGuard dg(device);
+  LINREC_CUDA_TRY(cudaMallocAsync(ptr, bytes == 0 ? 16 : bytes, static_cast<cudaStream_t>(stream)));
+  return LINREC_OK;
+}
+
+int linrec_device_free(void* ptr, int device, void* stream) {
+  if (!ptr) return LINREC_OK;
+  DeviceGuard dg(device);
+  LINREC_CUDA_TRY(cudaFreeAsync(ptr, static_cast<cudaStream_t>(stream)));
+  return LINREC_OK;
+}
+
+int linrec_workspace_create(linrec_workspace_t* ws, int device) {
+  int rc;
+  if ((rc = check_ptr(ws, "ws"))) return rc;
+  *ws = new linrec_workspace();
+  (*ws)->device = device;
+  return LINREC_OK;
+}
+
+int linrec_workspace_destroy(linrec_workspace_t ws) {
+  if (!ws) return LINREC_OK;
+  if (ws->base) {
+    DeviceGuard dg(ws->device);
+    cudaDeviceSynchronize();
+    cudaFree(ws->base);
+  }
+  delete ws;
+  return LINREC_OK;
+}
+
+size_t linrec_workspace_bytes(int64_t T, int64_t W, int dtype_bytes) {
+  if (T < 1 || W < 1) return 0;
+  if (dtype_bytes == 8) {
+    const size_t a = linrec_impl::plan_chain<double>(true, T, W, W % 2 == 0).ws_bytes;
+    const size_t b = linrec_impl::plan_chain<double>(false, T, W, W % 2 == 0).ws_bytes;
+    return std::max(a, b);
+  }
+  const size_t a = linrec_impl::plan_chain<float>(true, T, W, W % 4 == 0).ws_bytes;
+  const size_t b = linrec_impl::plan_chain<float>(false, T, W, W % 4 == 0).ws_bytes;
+  return std::max(a, b);
+}
+
+int linrec_scan_f32(const float* lam, const float* x, const float* h0, float* h, int64_t T,
+                    int64_t W, int mode, linrec_workspace_t ws, void* stream) {
+  return scan_device<float>(lam, x, h0, h, T, W, mode, ws, static_cast<cudaStream_t>(stream));
+}
+int linrec_scan_f64(const double* lam, const double* x, const double* h0, double* h, int64_t T,
+                    int64_t W, int mode, linrec_workspace_t ws, void* stream) {
+  return scan_device<double>(lam, x, h0, h, T, W, mode, ws, static_cast<cudaStream_t>(stream));
+}
+
+int linrec_scan_backward_f32(const float* lam, const float* h0, const float* h, const float* dh,
+                             float* dlam, float* dx, float* dh0, int64_t T, int64_t W, int mode,
+                             linrec_workspace_t ws, void* stream) {
+  int rc;
+  if ((rc = check_ptr(dh0, "d_initial"))) return rc;
+  return scan_backward_device<float>(lam, h0, h, dh, nullptr, nullptr, dlam, dx, dh0, T, W, mode,
+                                     ws, static_cast<cudaStream_t>(stream));
+}
+int linrec_scan_backward_f64(const double* lam, const double* h0, const double* h,
+                             const double* dh, double* dlam, double* dx, double* dh0, int64_t T,
+                             int64_t W, int mode, linrec_workspace_t ws, void* stream) {
+  int rc;
+  if ((rc = check_ptr(dh0, "d_initial"))) return rc;
+  return scan_backward_device<double>(lam, h0, h, dh, nullptr, nullptr, dlam, dx, dh0, T, W, mode,
+                                      ws, static_cast<cudaStream_t>(stream));
+}
+
+int linrec_scan_backward_segment_f32(const float* lam, const float* h0, const float* h,
+                                     const float* dh, const float* lam_next, const float* g_next,
+                                     float* dlam, float* dx, float* dh0, int64_t T, int64_t W,
+                                     int mode, linrec_workspace_t ws, void* stream) {
+  return scan_backward_device<float>(lam, h0, h, dh, lam_next, g_next, dlam, dx, dh0, T, W, mode,
+                                     ws, static_cast<cudaStream_t>(stream));
+}
+int linrec_scan_backward_segment_f64(const double* lam, const double* h0, const double* h,
+                                     const double* dh, const double* lam_next,
+                                     const double* g_next, double* dlam, double* dx, double* dh0,
+                                     int64_t T, int64_t W, int mode, linrec_workspace_t ws,
+                                     void* stream) {
+  return scan_backward_device<double>(lam, h0, h, dh, lam_next, g_next, dlam, dx, dh0, T, W, mode,
+                                      ws, static_cast<cudaStream_t>(stream));
+}
+
+int linrec_scan_host_f32(const float* lam, const float* x, const float* h0, float* h, int64_t T,
+                         int64_t W, int mode, int device) {
+  return scan_host<float>(lam, x, h0, h, T, W, mode, device);
+}
+int linrec_scan_host_f64(const double* lam, const double* x, const double* h0, double* h,
+                         int64_t T, int64_t W, int mode, int device) {
+  return scan_host<double>(lam, x, h0, h, T, W, mode, device);
+}
+int linrec_scan_backward_host_f32(const float* lam, const float* h0, const float* h,
+                                  const float* dh, float* dlam, float* dx, float* dh0, int64_t T,
+                                  int64_t W, int mode, int device) {
+  return scan_backward_host<float>(lam, h0, h, dh, dlam, dx, dh0, T, W, mode, device);
+}
+int linrec_scan_backward_host_f64(const double* lam, const double* h0, const double* h,
+                                  const double* dh, double* dlam, double* dx, double* dh0,
+                                  int64_t T, int64_t W, int mode, int device) {
+  return scan_backward_host<double>(lam, h0, h, dh, dlam, dx, dh0, T, W, mode, device);
+}
+
+int linrec_first_nonfinite_f32(const float* v, int64_t n, int64_t* index, void* stream) {
+  return first_nonfinite<float>(v, n, index, static_cast<cudaStream_t>(stream));
+}
+int linrec_first_nonfinite_f64(const double* v, int64_t n, int64_t* index, void* stream) {
+  return first_nonfinite<double>(v, n, index, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,76 @@
+// Runtime dispatch of the chained-scan templates (included once per
+// dtype/direction translation unit so nvcc compiles them in parallel).
+#pragma once
+
+#include "launch.h"
+#include "scan_chained.cuh"
+
+namespace linrec_impl {
+
+template <class S>
+struct Tuning;
+// forward: 2 arrays in registers (lam, x); backward: 3 (mu, dh, h_{t-1})
+template <>
+struct Tuning<float> {
+  static constexpr int VEC = 4, FWD_R = 6, FWD_NW = 8, BWD_R = 4, BWD_NW = 8;
+};
+template <>
+struct Tuning<double> {
+  static constexpr int VEC = 2, FWD_R = 6, FWD_NW = 8, BWD_R = 4, BWD_NW = 8;
+};
+
+inline int pick_q(int64_t nvec) {
+  int q = 1;
+  while (q < 32 && q < nvec) q <<= 1;
+  return q;
+}
+
+template <class S, int VEC, int Q, int R, int NW>
+void fill_plan(ChainPlan& p, int64_t T, int64_t W) {
+  using Cfg = linrec_dev::ChainCfg<S, VEC, Q, R, NW>;
+  p.vec = VEC; p.q = Q; p.r = R; p.nw = NW;
+  p.cpw = Cfg::CPW; p.rows = Cfg::L; p.rec = Cfg::REC;
+  p.ncols = (W + Cfg::CPW - 1) / Cfg::CPW;
+  p.ntt = (T + Cfg::L - 1) / Cfg::L;
+  p.ntiles = p.ncols * p.ntt;
+  p.flags_bytes = ((size_t)p.ntiles * 4 + 255) / 256 * 256;
+  p.rec_bytes = (size_t)p.ntiles * 2 * Cfg::REC * sizeof(S);
+  p.ws_bytes = 256 + p.flags_bytes + 2 * p.rec_bytes;
+}
+
+#define LINREC_Q_SWITCH(QV, ...)                            \
+  switch (QV) {                                             \
+    case 1: { constexpr int Q_ = 1; __VA_ARGS__; } break;   \
+    case 2: { constexpr int Q_ = 2; __VA_ARGS__; } break;   \
+    case 4: { constexpr int Q_ = 4; __VA_ARGS__; } break;   \
+    case 8: { constexpr int Q_ = 8; __VA_ARGS__; } break;   \
+    case 16: { constexpr int Q_ = 16; __VA_ARGS__; } break; \
+    default: { constexpr int Q_ = 32; __VA_ARGS__; } break; \
+  }
+
+inline linrec_dev::ChainWs to_dev(const ChainPtrs& w) {
+  linrec_dev::ChainWs d;
+  d.ctrl = reinterpret_cast<linrec_dev::Ctrl*>(w.ctrl);
+  d.flags = reinterpret_cast<uint32_t*>(w.flags);
+  d.agg = w.agg;
+  d.inc = w.inc;
+  return d;
+}
+
+template <class S, bool FWD>
+ChainPlan plan_chain_dir(int64_t T, int64_t W, bool vec_ok) {
+  using Tn = Tuning<S>;
+  constexpr int R = FWD ? Tn::FWD_R : Tn::BWD_R;
+  constexpr int NW = FWD ? Tn::FWD_NW : Tn::BWD_NW;
+  ChainPlan p;
+  if (vec_ok) {
+    const int q = pick_q((W + Tn::VEC - 1) / Tn::VEC);
+    LINREC_Q_SWITCH(q, fill_plan<S, Tn::VEC, Q_, R, NW>(p, T, W));
+  } else {
+    const int q = pick_q(W);
+    LINREC_Q_SWITCH(q, fill_plan<S, 1, Q_, R, NW>(p, T, W));
+  }
+  return p;
+}
+
+}  // namespace linrec_impl

@@ -1,0 +1,77 @@
+// Internal (C++) launch interface between capi.cpp and the kernel TUs.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace linrec_impl {
+
+// Tile configuration chosen for one chained launch.
+struct ChainPlan {
+  int vec = 1;        // channels per thread vector (4 f32 / 2 f64, or 1)
+  int q = 32;         // lanes across channels
+  int r = 8;          // rows per thread
+  int nw = 8;         // warps per CTA
+  int cpw = 0;        // channels per column
+  int rows = 0;       // rows per tile (L)
+  int rec = 0;        // carry-record stride in elements
+  int64_t ncols = 0;  // channel columns
+  int64_t ntt = 0;    // tiles along time
+  int64_t ntiles = 0; // = ncols * ntt = grid size
+  size_t flags_bytes = 0;
+  size_t rec_bytes = 0;  // bytes of ONE of the two record arrays (agg or inc)
+  size_t ws_bytes = 0;   // control block + flags + agg + inc
+};
+
+// Rows per thread / warps per CTA of each direction (tuned on B200).
+template <class S>
+ChainPlan plan_chain(bool forward, int64_t T, int64_t W, bool vec_ok);
+
+struct ChainPtrs {  // host mirror of linrec_dev::ChainWs
+  void* ctrl;
+  void* flags;
+  void* agg;
+  void* inc;
+};
+
+template <class S>
+struct FwdCall {
+  const S* lam;
+  const S* x;
+  const S* h0;
+  S* h;
+  int64_t T, W;
+};
+
+template <class S>
+struct BwdCall {
+  const S* lam;
+  const S* h0;
+  const S* h;
+  const S* dh;
+  const S* lam_next;
+  const S* g_next;
+  S* dlam;
+  S* dx;
+  S* dh0;
+  int64_t T, W;
+};
+
+template <class S>
+cudaError_t launch_chain_fwd(const ChainPlan& p, const FwdCall<S>& c, const ChainPtrs& ws,
+                             cudaStream_t st);
+template <class S>
+cudaError_t launch_chain_bwd(const ChainPlan& p, const BwdCall<S>& c, const ChainPtrs& ws,
+                             cudaStream_t st);
+template <class S>
+cudaError_t launch_serial_fwd(const FwdCall<S>& c, bool vec_ok, cudaStream_t st);
+template <class S>
+cudaError_t launch_serial_bwd(const BwdCall<S>& c, bool vec_ok, cudaStream_t st);
+
+cudaError_t launch_ws_init(void* ctrl, cudaStream_t st);
+
+template <class S>
+cudaError_t first_nonfinite(const S* v, int64_t n, int64_t* index, cudaStream_t st);
+
+}  // namespace linrec_impl

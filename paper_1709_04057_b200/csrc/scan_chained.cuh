@@ -1,0 +1,613 @@
+// Single-pass chained scans (forward and reverse-time backward) for sm_100a.
+//
+// Replaces the reference's three-phase chunked scan (recurrence.hpp:193-245:
+// phase 1 chunk_summary, phase 2 sequential stitch, phase 3 seeded re-scan)
+// and its reversed-copy backward (recurrence.hpp:283-348) with ONE pass over
+// HBM: every element of the inputs is read once and every output written
+// once (fp32: 12 B/element forward, 20 B/element backward).
+//
+// Decomposition.  The [T][W] tensor is cut into tiles of L rows x CPW
+// channels.  Channels are independent (recurrence.hpp:109), so each of the
+// ncols = ceil(W/CPW) channel columns is its own chain of T/L tiles.
+//   * A thread owns VEC adjacent channels (128-bit vector) and R consecutive
+//     rows, held in registers: it loads them once, reduces them to an affine
+//     pair (A = prod lam, B = zero-seeded result) -- the reference's
+//     chunk_summary (recurrence.hpp:114-131) at register granularity.
+//   * Lanes are split Q across channels x G = 32/Q along time; the G row
+//     segments of a warp are combined with __shfl_up_sync, the NW warps of
+//     the CTA through shared memory.  Pair algebra: applying (A1,B1) then
+//     (A2,B2) is (A2*A1, A2*B1 + B2).
+//   * Tiles obtain their position from an atomic ticket (launch order), so
+//     every predecessor of a tile is resident or retired: the look-back
+//     always makes progress.  A coordinator warp (warp NW, holding no tile
+//     data) publishes the tile aggregate, looks
+//     back over up to 32 predecessors per round (one flag per lane, one
+//     ballot), finds the nearest predecessor whose inclusive carry is
+//     published, and APPLIES the intermediate aggregates to that carry oldest
+//     first.  Because inclusive carries are defined by sequential
+//     application, the carry each tile obtains is bit-identical whichever
+//     predecessor the look-back stopped at: the scan is deterministic run to
+//     run although the look-back is decoupled.
+//   * The tile's registers are then re-scanned from the carry (the
+//     reference's phase 3, recurrence.hpp:232-237) and written back with
+//     streaming 128-bit stores.
+// The backward runs the same machinery in reverse time on
+// G_t = lam_{t+1} G_{t+1} + dh_t with mu_t = lam_{t+1} read through a
+// one-row shift (no reversed copies, cf. recurrence.hpp:305-318) and fuses
+// dx = G, dlam = h_{t-1} G, dh0 = lam_1 G_1 (recurrence.hpp:331-346) into the
+// re-scan.
+#pragma once
+
+#include "linrec_device.cuh"
+
+namespace linrec_dev {
+
+template <class S, int VEC, int Q, int R, int NW>
+struct ChainCfg {
+  static constexpr int G = 32 / Q;          // lane groups along time per warp
+  static constexpr int CPW = Q * VEC;       // channels per column (tile width)
+  static constexpr int NSEG = NW * G;       // row segments per tile
+  static constexpr int L = NSEG * R;        // rows per tile
+  static constexpr int THREADS = (NW + 1) * 32;  // + coordinator warp
+  // carry record: [A or P: REC][B or c: REC], padded to 128-byte lines
+  static constexpr int REC = ((CPW * (int)sizeof(S) + 127) / 128) * 128 / (int)sizeof(S);
+};
+
+// Workspace view of one chained launch (see capi.cpp for the layout).
+struct ChainWs {
+  Ctrl* ctrl;
+  uint32_t* flags;   // [ntiles]
+  void* agg;         // [ntiles][2][REC] tile aggregates (A, B)
+  void* inc;         // [ntiles][2][REC] inclusive carries (P, c)
+};
+
+template <class S>
+struct ChainArgs {
+  // forward: a = lam, b = x, out0 = h
+  // backward: a = lam, b = dh, c = h, out0 = dx, out1 = dlam, out2 = dh0
+  const S* a;
+  const S* b;
+  const S* c;
+  const S* seed;      // fwd: h0 (nullable); bwd: g_next (nullable)
+  const S* aux;       // bwd: h0 (nullable) ; fwd: unused
+  const S* lam_next;  // bwd: decay of the row after the segment (nullable)
+  S* out0;
+  S* out1;
+  S* out2;
+  int64_t T;
+  int64_t W;
+  int64_t ncols;
+  int64_t ntt;        // tiles along time
+};
+
+// Coordinator-warp part of the decoupled look-back.  On entry lanes < Q hold the tile
+// aggregate (TA, TB) of their VEC channels and, for the first tile of the
+// chain (pos == 0), the chain seed in (c, P).  On exit they hold the tile's
+// exclusive carry (c = state entering the tile, P = decay product from the
+// chain start).  Publishes the aggregate (flag AGG) and then the inclusive
+// carry (flag INC) of chunk k.
+template <class S, int VEC, int Q, int REC>
+__device__ __forceinline__ void chain_lookback(const ChainWs& ws, uint32_t epoch,
+                                               int64_t k, int64_t pos, int64_t col,
+                                               int64_t ncols, const S (&TA)[VEC],
+                                               const S (&TB)[VEC], S (&c)[VEC],
+                                               S (&P)[VEC], bool valid) {
+  using IO = VecIO<S, VEC>;
+  const int lane = threadIdx.x & 31;
+  S* agg = reinterpret_cast<S*>(ws.agg);
+  S* inc = reinterpret_cast<S*>(ws.inc);
+  const bool owner = lane < Q && valid;
+  const int off = lane * VEC;  // channel offset inside the record (lane < Q)
+
+  if (pos > 0) {
+    if (owner) {
+      S* rec = agg + k * 2 * REC + off;
+      IO::store_cg(rec, TA);
+      IO::store_cg(rec + REC, TB);
+      fence_acq_rel_gpu();
+    }
+    __syncwarp();
+    if (lane == 0) st_release_gpu(&ws.flags[k], (epoch << 2) | kFlagAgg);
+
+    // nearest predecessor with a published inclusive carry
+    int64_t jhi = pos - 1, jinc = 0;
+    for (;;) {
+      const int64_t jj = jhi - lane;
+      bool is_inc = false;
+      if (jj >= 0) {
+        const uint32_t* fp = &ws.flags[jj * ncols + col];
+        uint32_t f = ld_acquire_gpu(fp);
+        while ((f >> 2) != epoch) f = ld_acquire_gpu(fp);
+        is_inc = (f & 3u) == kFlagInc;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, is_inc);
+      if (m) {
+        jinc = jhi - (__ffs(m) - 1);
+        break;
+      }
+      jhi -= 32;
+    }
+    if (owner) {
+      const S* rec = inc + (jinc * ncols + col) * 2 * REC + off;
+      IO::load_cg(rec, P);
+      IO::load_cg(rec + REC, c);
+      // apply the aggregates of chunks jinc+1 .. pos-1, oldest first
+      int64_t j = jinc + 1;
+#pragma unroll 1
+      for (; j + 4 <= pos; j += 4) {
+        S a4[4][VEC], b4[4][VEC];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const S* r = agg + ((j + u) * ncols + col) * 2 * REC + off;
+          IO::load_cg(r, a4[u]);
+          IO::load_cg(r + REC, b4[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            c[v] = fma_(a4[u][v], c[v], b4[u][v]);
+            P[v] = mul_(a4[u][v], P[v]);
+          }
+      }
+#pragma unroll 1
+      for (; j < pos; ++j) {
+        S a1[VEC], b1[VEC];
+        const S* r = agg + (j * ncols + col) * 2 * REC + off;
+        IO::load_cg(r, a1);
+        IO::load_cg(r + REC, b1);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          c[v] = fma_(a1[v], c[v], b1[v]);
+          P[v] = mul_(a1[v], P[v]);
+        }
+      }
+    }
+  }
+  // inclusive carry of this chunk
+  if (owner) {
+    S ci[VEC], Pi[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      ci[v] = fma_(TA[v], c[v], TB[v]);
+      Pi[v] = mul_(TA[v], P[v]);
+    }
+    S* rec = inc + k * 2 * REC + off;
+    IO::store_cg(rec, Pi);
+    IO::store_cg(rec + REC, ci);
+    fence_acq_rel_gpu();
+  }
+  __syncwarp();
+  if (lane == 0) st_release_gpu(&ws.flags[k], (epoch << 2) | kFlagInc);
+}
+
+// Named barriers between the NW data warps and the coordinator warp.
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  __threadfence_block();
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void chain_ticket(const ChainWs& ws, unsigned long long* s_k,
+                                             uint32_t* s_epoch) {
+  if (threadIdx.x == 0) {
+    *s_epoch = __ldcg(&ws.ctrl->epoch);
+    *s_k = atomicAdd(&ws.ctrl->ticket, 1ull);
+  }
+}
+
+__device__ __forceinline__ void chain_retire(const ChainWs& ws, uint32_t epoch) {
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long r = atomicAdd(&ws.ctrl->retired, 1ull);
+    if (r == (unsigned long long)gridDim.x - 1ull) {
+      ws.ctrl->ticket = 0ull;
+      ws.ctrl->retired = 0ull;
+      ws.ctrl->epoch = next_epoch(epoch);
+      __threadfence();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Coordinator warp (warp NW of the CTA): waits for the data warps' segment
+// totals, folds them into the tile aggregate, runs the look-back and hands the
+// tile's exclusive carry to the data warps through shared memory.  Keeping the
+// look-back in its own warp keeps its registers out of the data warps, whose
+// register file holds the tile.
+// ---------------------------------------------------------------------------
+template <class S, int VEC, int Q, int NW, int CPW, int REC, bool REV>
+__device__ __forceinline__ void chain_coordinator(const ChainArgs<S>& a, const ChainWs& ws,
+                                                  uint32_t epoch, int64_t k, int64_t pos,
+                                                  int64_t col, S (*s_wa)[CPW],
+                                                  S (*s_wb)[CPW], S* s_c) {
+  constexpr int NT = (NW + 1) * 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t ch = col * CPW + (int64_t)lane * VEC;
+  const bool valid = lane < Q && ch < a.W;
+  bar_sync(1, NT);  // segment totals are in shared memory
+  S TA[VEC], TB[VEC], c[VEC], P[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) { TA[v] = S(1); TB[v] = S(0); c[v] = S(0); P[v] = S(1); }
+  if (lane < Q) {
+    constexpr int w0 = REV ? NW - 1 : 0;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      TA[v] = s_wa[w0][lane * VEC + v];
+      TB[v] = s_wb[w0][lane * VEC + v];
+    }
+#pragma unroll
+    for (int i = 1; i < NW; ++i) {
+      const int w = REV ? NW - 1 - i : i;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        TB[v] = fma_(s_wa[w][lane * VEC + v], TB[v], s_wb[w][lane * VEC + v]);
+        TA[v] = mul_(s_wa[w][lane * VEC + v], TA[v]);
+      }
+    }
+    if (pos == 0 && a.seed != nullptr && valid) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) c[v] = a.seed[ch + v];
+    }
+  }
+  chain_lookback<S, VEC, Q, REC>(ws, epoch, k, pos, col, a.ncols, TA, TB, c, P, valid);
+  if (lane < Q) {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) s_c[lane * VEC + v] = c[v];
+  }
+  bar_arrive(2, NT);  // carry is in shared memory
+  chain_retire(ws, epoch);
+}
+
+// ---------------------------------------------------------------------------
+// Forward: h_t = lam_t h_{t-1} + x_t, seeded with h0 (or 0).
+// ---------------------------------------------------------------------------
+template <class S, int VEC, int Q, int R, int NW>
+__global__ void __launch_bounds__((NW + 1) * 32, 2)
+k_chain_fwd(const ChainArgs<S> a, const ChainWs ws) {
+  using Cfg = ChainCfg<S, VEC, Q, R, NW>;
+  using IO = VecIO<S, VEC>;
+  constexpr int G = Cfg::G, CPW = Cfg::CPW, L = Cfg::L;
+  constexpr int NT = (NW + 1) * 32;
+  __shared__ S s_wa[NW][CPW];
+  __shared__ S s_wb[NW][CPW];
+  __shared__ S s_c[CPW];
+  __shared__ unsigned long long s_k;
+  __shared__ uint32_t s_epoch;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  chain_ticket(ws, &s_k, &s_epoch);
+  __syncthreads();
+  const int64_t k = (int64_t)s_k;
+  const uint32_t epoch = s_epoch;
+  const int64_t col = k % a.ncols, pos = k / a.ncols;
+
+  if (warp == NW) {
+    chain_coordinator<S, VEC, Q, NW, CPW, Cfg::REC, false>(a, ws, epoch, k, pos, col, s_wa,
+                                                          s_wb, s_c);
+    return;
+  }
+
+  const int q = lane % Q, g = lane / Q;
+  const int64_t ch = col * CPW + (int64_t)q * VEC;
+  const bool valid = ch < a.W;
+  const int64_t t0 = pos * L + (int64_t)(warp * G + g) * R;
+  const int64_t W = a.W;
+
+  S l[R][VEC], xv[R][VEC];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int64_t t = t0 + i;
+    if (valid && t < a.T) {
+      IO::load_stream(a.a + t * W + ch, l[i]);
+      IO::load_stream(a.b + t * W + ch, xv[i]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) { l[i][v] = S(1); xv[i][v] = S(0); }
+    }
+  }
+
+  // segment aggregate (chunk_summary at register granularity)
+  S A[VEC], B[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) { A[v] = l[0][v]; B[v] = xv[0][v]; }
+#pragma unroll
+  for (int i = 1; i < R; ++i)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      B[v] = fma_(l[i][v], B[v], xv[i][v]);
+      A[v] = mul_(l[i][v], A[v]);
+    }
+
+  // inclusive scan over the G row segments of the warp
+#pragma unroll
+  for (int off = 1; off < G; off <<= 1) {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      const S ap = __shfl_up_sync(0xffffffffu, A[v], off * Q);
+      const S bp = __shfl_up_sync(0xffffffffu, B[v], off * Q);
+      if (g >= off) {
+        B[v] = fma_(A[v], bp, B[v]);
+        A[v] = mul_(A[v], ap);
+      }
+    }
+  }
+  S Ae[VEC], Be[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    Ae[v] = S(1);
+    Be[v] = S(0);
+    if (G > 1) {
+      const S ap = __shfl_up_sync(0xffffffffu, A[v], Q);
+      const S bp = __shfl_up_sync(0xffffffffu, B[v], Q);
+      if (g > 0) { Ae[v] = ap; Be[v] = bp; }
+    }
+  }
+  if (g == G - 1) {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      s_wa[warp][q * VEC + v] = A[v];
+      s_wb[warp][q * VEC + v] = B[v];
+    }
+  }
+  bar_arrive(1, NT);
+  bar_sync(2, NT);
+
+  // seed of this thread's rows: carry, then earlier warps, then earlier groups
+  S cs[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) cs[v] = s_c[q * VEC + v];
+  for (int w = 0; w < warp; ++w)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v)
+      cs[v] = fma_(s_wa[w][q * VEC + v], cs[v], s_wb[w][q * VEC + v]);
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) cs[v] = fma_(Ae[v], cs[v], Be[v]);
+
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) cs[v] = fma_(l[i][v], cs[v], xv[i][v]);
+    const int64_t t = t0 + i;
+    if (valid && t < a.T) IO::store_stream(a.out0 + t * W + ch, cs);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Backward: G_t = mu_t G_{t+1} + dh_t, mu_t = lam_{t+1} (lam_next for the
+// last row, 0 at the true end), processed from the last tile to the first.
+// dx_t = G_t, dlam_t = h_{t-1} G_t (h0 for t = 0), dh0 = lam_0 G_0.
+// ---------------------------------------------------------------------------
+template <class S, int VEC, int Q, int R, int NW>
+__global__ void __launch_bounds__((NW + 1) * 32, 2)
+k_chain_bwd(const ChainArgs<S> a, const ChainWs ws) {
+  using Cfg = ChainCfg<S, VEC, Q, R, NW>;
+  using IO = VecIO<S, VEC>;
+  constexpr int G = Cfg::G, CPW = Cfg::CPW, L = Cfg::L;
+  constexpr int NT = (NW + 1) * 32;
+  __shared__ S s_wa[NW][CPW];
+  __shared__ S s_wb[NW][CPW];
+  __shared__ S s_c[CPW];
+  __shared__ unsigned long long s_k;
+  __shared__ uint32_t s_epoch;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  chain_ticket(ws, &s_k, &s_epoch);
+  __syncthreads();
+  const int64_t k = (int64_t)s_k;
+  const uint32_t epoch = s_epoch;
+  const int64_t col = k % a.ncols, pos = k / a.ncols;
+
+  if (warp == NW) {
+    chain_coordinator<S, VEC, Q, NW, CPW, Cfg::REC, true>(a, ws, epoch, k, pos, col, s_wa,
+                                                         s_wb, s_c);
+    return;
+  }
+
+  const int q = lane % Q, g = lane / Q;
+  const int64_t tile = a.ntt - 1 - pos;
+  const int64_t ch = col * CPW + (int64_t)q * VEC;
+  const bool valid = ch < a.W;
+  const int64_t t0 = tile * L + (int64_t)(warp * G + g) * R;
+  const int64_t W = a.W, T = a.T;
+
+  S mu[R][VEC], dh[R][VEC], hp[R][VEC];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int64_t t = t0 + i;
+    if (valid && t < T) {
+      if (t + 1 < T) {
+        IO::load_stream(a.a + (t + 1) * W + ch, mu[i]);
+      } else if (a.lam_next != nullptr) {
+        IO::load_cg(a.lam_next + ch, mu[i]);
+      } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) mu[i][v] = S(0);
+      }
+      IO::load_stream(a.b + t * W + ch, dh[i]);
+      if (t >= 1) {
+        IO::load_stream(a.c + (t - 1) * W + ch, hp[i]);
+      } else if (a.aux != nullptr) {
+        IO::load_cg(a.aux + ch, hp[i]);
+      } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) hp[i][v] = S(0);
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) { mu[i][v] = S(1); dh[i][v] = S(0); hp[i][v] = S(0); }
+    }
+  }
+
+  // segment aggregate, latest row first
+  S A[VEC], B[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) { A[v] = mu[R - 1][v]; B[v] = dh[R - 1][v]; }
+#pragma unroll
+  for (int i = R - 2; i >= 0; --i)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      B[v] = fma_(mu[i][v], B[v], dh[i][v]);
+      A[v] = mul_(mu[i][v], A[v]);
+    }
+
+  // inclusive scan over the warp's row segments in reverse time
+#pragma unroll
+  for (int off = 1; off < G; off <<= 1) {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      const S ap = __shfl_down_sync(0xffffffffu, A[v], off * Q);
+      const S bp = __shfl_down_sync(0xffffffffu, B[v], off * Q);
+      if (g + off < G) {
+        B[v] = fma_(A[v], bp, B[v]);
+        A[v] = mul_(A[v], ap);
+      }
+    }
+  }
+  S Ae[VEC], Be[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    Ae[v] = S(1);
+    Be[v] = S(0);
+    if (G > 1) {
+      const S ap = __shfl_down_sync(0xffffffffu, A[v], Q);
+      const S bp = __shfl_down_sync(0xffffffffu, B[v], Q);
+      if (g < G - 1) { Ae[v] = ap; Be[v] = bp; }
+    }
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      s_wa[warp][q * VEC + v] = A[v];
+      s_wb[warp][q * VEC + v] = B[v];
+    }
+  }
+  bar_arrive(1, NT);
+  bar_sync(2, NT);
+
+  S cs[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) cs[v] = s_c[q * VEC + v];
+  for (int w = NW - 1; w > warp; --w)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v)
+      cs[v] = fma_(s_wa[w][q * VEC + v], cs[v], s_wb[w][q * VEC + v]);
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) cs[v] = fma_(Ae[v], cs[v], Be[v]);
+
+#pragma unroll
+  for (int i = R - 1; i >= 0; --i) {
+    S dl[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      cs[v] = fma_(mu[i][v], cs[v], dh[i][v]);
+      dl[v] = mul_(hp[i][v], cs[v]);
+    }
+    const int64_t t = t0 + i;
+    if (valid && t < T) {
+      IO::store_stream(a.out0 + t * W + ch, cs);
+      IO::store_stream(a.out1 + t * W + ch, dl);
+      if (t == 0 && a.out2 != nullptr) {
+        S l0[VEC], d0[VEC];
+        IO::load_cg(a.a + ch, l0);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) d0[v] = mul_(l0[v], cs[v]);
+        IO::store_cg(a.out2 + ch, d0);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Serial per-channel kernels: ScanMode::Serial on the GPU.  One thread per
+// VEC channels walks the whole sequence with the reference's exact operation
+// order (scan_span, recurrence.hpp:101-112; reversed scan + assembly,
+// :309-346), so the result is bit-identical to the reference's serial scan.
+// U rows of loads are kept in flight per thread.
+// ---------------------------------------------------------------------------
+template <class S, int VEC, int U>
+__global__ void __launch_bounds__(128)
+k_serial_fwd(const S* __restrict__ lam, const S* __restrict__ x, const S* __restrict__ h0,
+             S* __restrict__ h, int64_t T, int64_t W) {
+  using IO = VecIO<S, VEC>;
+  const int64_t ch = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * VEC;
+  if (ch >= W) return;
+  S c[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) c[v] = h0 ? h0[ch + v] : S(0);
+  for (int64_t t0 = 0; t0 < T; t0 += U) {
+    S l[U][VEC], xv[U][VEC];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (t0 + u < T) {
+        IO::load_stream(lam + (t0 + u) * W + ch, l[u]);
+        IO::load_stream(x + (t0 + u) * W + ch, xv[u]);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (t0 + u < T) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) c[v] = fma_(l[u][v], c[v], xv[u][v]);
+        IO::store_stream(h + (t0 + u) * W + ch, c);
+      }
+  }
+}
+
+template <class S, int VEC, int U>
+__global__ void __launch_bounds__(128)
+k_serial_bwd(const S* __restrict__ lam, const S* __restrict__ h0, const S* __restrict__ h,
+             const S* __restrict__ dh, const S* __restrict__ lam_next,
+             const S* __restrict__ g_next, S* __restrict__ dlam, S* __restrict__ dx,
+             S* __restrict__ dh0, int64_t T, int64_t W) {
+  using IO = VecIO<S, VEC>;
+  const int64_t ch = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * VEC;
+  if (ch >= W) return;
+  S G[VEC], mu_last[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    G[v] = g_next ? g_next[ch + v] : S(0);
+    mu_last[v] = lam_next ? lam_next[ch + v] : S(0);
+  }
+  for (int64_t t1 = T - 1; t1 >= 0; t1 -= U) {
+    S mu[U][VEC], d[U][VEC], hp[U][VEC];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t t = t1 - u;
+      if (t >= 0) {
+        if (t + 1 < T) IO::load_stream(lam + (t + 1) * W + ch, mu[u]);
+        else {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) mu[u][v] = mu_last[v];
+        }
+        IO::load_stream(dh + t * W + ch, d[u]);
+        if (t >= 1) IO::load_stream(h + (t - 1) * W + ch, hp[u]);
+        else {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) hp[u][v] = h0 ? h0[ch + v] : S(0);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t t = t1 - u;
+      if (t >= 0) {
+        S dl[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          G[v] = fma_(mu[u][v], G[v], d[u][v]);
+          dl[v] = mul_(hp[u][v], G[v]);
+        }
+        IO::store_stream(dx + t * W + ch, G);
+        IO::store_stream(dlam + t * W + ch, dl);
+      }
+    }
+  }
+  if (dh0) {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) dh0[ch + v] = mul_(lam[ch + v], G[v]);
+  }
+}
+
+}  // namespace linrec_dev

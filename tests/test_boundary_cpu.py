@@ -1,0 +1,123 @@
+"""CPU-side checks of the drop-in boundary (no compute calls without a GPU).
+
+* liblinrec_cuda.so loads and exports every symbol include/linrec_cuda.h declares;
+* the `linrec` module mirrors the reference module's surface and argument
+  errors (proj/tests/python/test_smoke.py:87-115, linrec_py.cpp:21-89);
+* without a CUDA device the product fails loudly -- there is no CPU path.
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, load_golden
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1709_04057_b200 import capi
+    declared = capi.declared_symbols()
+    assert len(declared) >= 20
+    lib = ctypes.CDLL(capi.LIB_PATH)
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert not missing, missing
+    out = subprocess.run(["nm", "-D", "--defined-only", capi.LIB_PATH], capture_output=True, text=True).stdout
+    exported = {l.split()[-1] for l in out.splitlines() if " T " in l}
+    assert set(declared) <= exported
+    # nothing but the C ABI is exported
+    assert all(s.startswith("linrec_") for s in exported), sorted(s for s in exported if not s.startswith("linrec_"))
+
+
+def test_library_is_sm100a_only():
+    from paper_1709_04057_b200 import capi
+    out = subprocess.run(["cuobjdump", "--list-elf", capi.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    archs = {l.split(".")[-2] for l in out.splitlines() if l.strip().endswith(".cubin")}
+    assert archs == {"sm_100a"}, archs
+
+
+def test_abi_version_and_workspace_query():
+    from paper_1709_04057_b200 import capi
+    assert capi.lib.linrec_abi_version() == 1
+    b = capi.lib.linrec_workspace_bytes(65536, 8192, 4)
+    # control block + one flag and two carry records per tile, << the data (2 GiB/array)
+    assert 0 < b < (2 << 30) // 4
+    assert capi.lib.linrec_workspace_bytes(0, 8, 4) == 0
+
+
+def test_module_surface_matches_reference():
+    from paper_1709_04057_b200 import linrec
+    for name in ("scan", "scan_backward", "plan_chunks", "predicted_speedup", "hardware_workers"):
+        assert hasattr(linrec, name)
+    g = load_golden("frozen")
+    assert linrec.plan_chunks(10, 4) == [tuple(r) for r in g["plan_10_4"].tolist()]
+    assert linrec.plan_chunks(3, 8) == [(1, 1), (2, 2), (3, 3)]
+    assert linrec.predicted_speedup(1, 1000) == pytest.approx(1 / 3)
+    assert 0.95 <= linrec.predicted_speedup(3, 100000) <= 1.0
+    assert linrec.predicted_speedup(8, 1 << 20) > 2.0
+    assert linrec.hardware_workers() >= 1
+    with pytest.raises(RuntimeError):
+        linrec.plan_chunks(0, 4)
+    with pytest.raises(RuntimeError):
+        linrec.plan_chunks(4, 0)
+
+
+def test_argument_errors_match_reference():
+    """test_smoke.py:102-111 plus the messages of recurrence.hpp:39-51."""
+    from paper_1709_04057_b200 import linrec
+    ok = np.zeros((4, 1, 2))
+    with pytest.raises(TypeError):
+        linrec.scan(ok.astype(np.int64), ok.astype(np.int64))
+    with pytest.raises(TypeError):
+        linrec.scan(ok, ok.astype(np.float32))
+    with pytest.raises(ValueError):
+        linrec.scan(np.zeros((4, 2)), np.zeros((4, 2)))
+    with pytest.raises(ValueError):
+        linrec.scan(ok, ok, mode="speculative")
+    with pytest.raises(ValueError):
+        linrec.scan(ok, ok, workers=-1)
+    with pytest.raises(RuntimeError, match=r"recurrence: shape mismatch, \[4,1,2\] vs \[4,1,3\]"):
+        linrec.scan(ok, np.zeros((4, 1, 3)))
+    with pytest.raises(RuntimeError, match=r"initial state \[1,3\] does not match \[1,2\]"):
+        linrec.scan(ok, ok, np.zeros((1, 3)))
+    with pytest.raises(RuntimeError, match="dimensions must be >= 1"):
+        linrec.scan(np.zeros((0, 1, 2)), np.zeros((0, 1, 2)))
+    with pytest.raises(RuntimeError, match=r"scan_backward\(h\): shape mismatch"):
+        linrec.scan_backward(ok, None, np.zeros((3, 1, 2)), ok)
+    with pytest.raises(TypeError):
+        linrec.scan_backward(ok, None, ok.astype(np.float32), ok)
+
+
+def test_no_cpu_fallback_without_gpu():
+    from paper_1709_04057_b200 import capi, linrec
+    if capi.lib.linrec_device_count() > 0:
+        pytest.skip("a GPU is present")
+    ok = np.zeros((4, 1, 2))
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        linrec.scan(ok, ok)
+    h = np.zeros_like(ok)
+    rc = capi.lib.linrec_scan_host_f64(ok.ctypes.data, ok.ctypes.data, None, h.ctypes.data, 4, 2, 1, 0)
+    assert rc == capi.ERR_CUDA
+
+
+def test_import_fails_loudly_without_library(tmp_path):
+    """Copy the package without its .so: importing must raise, not fall back."""
+    import shutil
+    pkg = os.path.join(ROOT, "paper_1709_04057_b200")
+    dst = tmp_path / "paper_1709_04057_b200"
+    shutil.copytree(pkg, dst, ignore=shutil.ignore_patterns("*.so", "csrc", "__pycache__"))
+    code = "import paper_1709_04057_b200"
+    r = subprocess.run(["python", "-c", code], cwd=tmp_path, capture_output=True, text=True)
+    assert r.returncode != 0 and "ImportError" in r.stderr
+
+
+def test_product_does_not_import_oracle():
+    """Only tests/, __graft_entry__.smoke() and bench.py may touch oracle/."""
+    pkg = os.path.join(ROOT, "paper_1709_04057_b200")
+    banned = ("import oracle", "from oracle", "liblinrec_oracle", "liblinrec_ref", "oracle/_ref")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cpp", ".cu", ".cuh", ".h", ".hpp")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert not any(b in text for b in banned), f
