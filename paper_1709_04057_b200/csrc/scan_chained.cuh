@@ -198,8 +198,11 @@ __device__ __forceinline__ void chain_ticket(const ChainWs& ws, unsigned long lo
   }
 }
 
+// Called by the coordinator warp once the CTA no longer needs the control
+// block; the CTA that retires last resets the ticket and advances the epoch
+// for the next launch on this workspace.
 __device__ __forceinline__ void chain_retire(const ChainWs& ws, uint32_t epoch) {
-  if (threadIdx.x == 0) {
+  if ((threadIdx.x & 31) == 0) {
     __threadfence();
     const unsigned long long r = atomicAdd(&ws.ctrl->retired, 1ull);
     if (r == (unsigned long long)gridDim.x - 1ull) {
