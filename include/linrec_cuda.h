@@ -75,6 +75,13 @@ const char* linrec_last_error(void);
 /* Number of CUDA devices visible (0 when none); never falls back to a CPU. */
 int linrec_device_count(void);
 
+/* Kernel selection for LINREC_PARALLEL.  AUTO (default) runs the persistent
+ * TMA-fed kernels whenever rows are 16-byte aligned and W is a multiple of
+ * the vector width, else the register-tiled kernels; REGISTER forces the
+ * latter (testing / comparison).  Process-wide. */
+typedef enum linrec_kernel_policy { LINREC_KERNEL_AUTO = 0, LINREC_KERNEL_REGISTER = 1 } linrec_kernel_policy;
+int linrec_set_kernel_policy(int policy);
+
 /* Device memory for callers without their own allocator (the Python
  * bindings' DeviceArray).  Stream-ordered on `stream`. */
 int linrec_device_malloc(void** ptr, size_t bytes, int device, void* stream);

@@ -18,6 +18,8 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "linrec_cuda.h")
 
 SERIAL = 0
 PARALLEL = 1
+KERNEL_AUTO = 0
+KERNEL_REGISTER = 1
 
 OK, ERR_SHAPE, ERR_DTYPE, ERR_VALUE, ERR_CUDA, ERR_NONFINITE, ERR_INTERNAL = range(7)
 
@@ -47,6 +49,7 @@ def _load():
     lib.linrec_workspace_bytes.argtypes = [_i64, _i64, _int]
     lib.linrec_workspace_create.argtypes = [C.POINTER(_vp), _int]
     lib.linrec_workspace_destroy.argtypes = [_vp]
+    lib.linrec_set_kernel_policy.argtypes = [_int]
     lib.linrec_device_malloc.argtypes = [C.POINTER(_vp), C.c_size_t, _int, _vp]
     lib.linrec_device_free.argtypes = [_vp, _int, _vp]
     for s in ("f32", "f64"):
@@ -68,6 +71,11 @@ def declared_symbols(header: str = HEADER):
         text = f.read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(linrec_[a-z0-9_]+)\s*\(", text)))
+
+
+def set_kernel_policy(policy: int):
+    """KERNEL_AUTO (TMA persistent kernels where eligible) or KERNEL_REGISTER."""
+    check(lib.linrec_set_kernel_policy(policy))
 
 
 def check(rc: int):

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -128,6 +129,13 @@ ChainPtrs ws_ptrs(linrec_workspace* ws, const ChainPlan& p) {
   return w;
 }
 
+std::atomic<int> g_kernel_policy{0};  // LINREC_KERNEL_AUTO
+
+bool tma_allowed(int64_t T, int64_t W) {
+  return g_kernel_policy.load() != LINREC_KERNEL_REGISTER && T < (int64_t(1) << 30) &&
+         W < (int64_t(1) << 30);
+}
+
 std::mutex g_default_mu;
 std::map<std::pair<int, cudaStream_t>, std::unique_ptr<linrec_workspace>> g_default_ws;
 
@@ -166,10 +174,13 @@ int scan_device(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t 
   if ((rc = current_device(&dev))) return rc;
   linrec_workspace* w = ws ? ws : default_ws(dev, st);
   std::lock_guard<std::mutex> lk(w->mu);
-  const ChainPlan p = linrec_impl::plan_chain<S>(true, T, W, vok);
+  ChainPlan p;
+  const bool tma = vok && tma_allowed(T, W) && linrec_impl::plan_tma<S>(true, T, W, &p);
+  if (!tma) p = linrec_impl::plan_chain<S>(true, T, W, vok);
   if (p.ntiles > 0x7fffffffLL) return fail(LINREC_ERR_SHAPE, "linrec: problem too large for one launch");
   if ((rc = ws_reserve(w, p.ws_bytes, st))) return rc;
-  LINREC_CUDA_TRY(linrec_impl::launch_chain_fwd<S>(p, c, ws_ptrs(w, p), st));
+  if (tma) LINREC_CUDA_TRY(linrec_impl::launch_tma_fwd<S>(p, c, ws_ptrs(w, p), st));
+  else LINREC_CUDA_TRY(linrec_impl::launch_chain_fwd<S>(p, c, ws_ptrs(w, p), st));
   return LINREC_OK;
 }
 
@@ -192,10 +203,13 @@ int scan_backward_device(const S* lam, const S* h0, const S* h, const S* dh, con
   if ((rc = current_device(&dev))) return rc;
   linrec_workspace* w = ws ? ws : default_ws(dev, st);
   std::lock_guard<std::mutex> lk(w->mu);
-  const ChainPlan p = linrec_impl::plan_chain<S>(false, T, W, vok);
+  ChainPlan p;
+  const bool tma = vok && tma_allowed(T, W) && linrec_impl::plan_tma<S>(false, T, W, &p);
+  if (!tma) p = linrec_impl::plan_chain<S>(false, T, W, vok);
   if (p.ntiles > 0x7fffffffLL) return fail(LINREC_ERR_SHAPE, "linrec: problem too large for one launch");
   if ((rc = ws_reserve(w, p.ws_bytes, st))) return rc;
-  LINREC_CUDA_TRY(linrec_impl::launch_chain_bwd<S>(p, c, ws_ptrs(w, p), st));
+  if (tma) LINREC_CUDA_TRY(linrec_impl::launch_tma_bwd<S>(p, c, ws_ptrs(w, p), st));
+  else LINREC_CUDA_TRY(linrec_impl::launch_chain_bwd<S>(p, c, ws_ptrs(w, p), st));
   return LINREC_OK;
 }
 
@@ -427,6 +441,13 @@ int linrec_device_count(void) {
   return n;
 }
 
+int linrec_set_kernel_policy(int policy) {
+  if (policy != LINREC_KERNEL_AUTO && policy != LINREC_KERNEL_REGISTER)
+    return fail(LINREC_ERR_VALUE, "kernel policy must be LINREC_KERNEL_AUTO or LINREC_KERNEL_REGISTER");
+  g_kernel_policy.store(policy);
+  return LINREC_OK;
+}
+
 int linrec_device_malloc(void** ptr, size_t bytes, int device, void* stream) {
   int rc;
   if ((rc = check_ptr(ptr, "ptr"))) return rc;
@@ -463,6 +484,7 @@ int linrec_workspace_destroy(linrec_workspace_t ws) {
 
 size_t linrec_workspace_bytes(int64_t T, int64_t W, int dtype_bytes) {
   if (T < 1 || W < 1) return 0;
+  // the register kernels use the smallest tiles, so they bound both kinds
   if (dtype_bytes == 8) {
     const size_t a = linrec_impl::plan_chain<double>(true, T, W, W % 2 == 0).ws_bytes;
     const size_t b = linrec_impl::plan_chain<double>(false, T, W, W % 2 == 0).ws_bytes;

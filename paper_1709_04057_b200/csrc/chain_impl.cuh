@@ -34,7 +34,7 @@ void fill_plan(ChainPlan& p, int64_t T, int64_t W) {
   p.ntt = (T + Cfg::L - 1) / Cfg::L;
   p.ntiles = p.ncols * p.ntt;
   p.flags_bytes = ((size_t)p.ntiles * 4 + 255) / 256 * 256;
-  p.rec_bytes = (size_t)p.ntiles * 2 * Cfg::REC * sizeof(S);
+  p.rec_bytes = (size_t)p.ntiles * 2 * Cfg::REC * 8;
   p.ws_bytes = 256 + p.flags_bytes + 2 * p.rec_bytes;
 }
 

@@ -9,6 +9,10 @@ namespace linrec_impl {
 
 // Tile configuration chosen for one chained launch.
 struct ChainPlan {
+  int kind = 0;       // 0 = register kernel (scan_chained.cuh), 1 = TMA persistent (scan_tma.cuh)
+  int stages = 0;     // TMA ring depth
+  int box_cols = 0, box_rows = 0;
+  int threads = 0, smem = 0, grid = 0;
   int vec = 1;        // channels per thread vector (4 f32 / 2 f64, or 1)
   int q = 32;         // lanes across channels
   int r = 8;          // rows per thread
@@ -68,6 +72,15 @@ template <class S>
 cudaError_t launch_serial_fwd(const FwdCall<S>& c, bool vec_ok, cudaStream_t st);
 template <class S>
 cudaError_t launch_serial_bwd(const BwdCall<S>& c, bool vec_ok, cudaStream_t st);
+
+// TMA persistent kernels: plan_tma returns false when the shape/alignment is
+// not eligible (then the register kernels run).
+template <class S>
+bool plan_tma(bool forward, int64_t T, int64_t W, ChainPlan* p);
+template <class S>
+cudaError_t launch_tma_fwd(const ChainPlan& p, const FwdCall<S>& c, const ChainPtrs& ws, cudaStream_t st);
+template <class S>
+cudaError_t launch_tma_bwd(const ChainPlan& p, const BwdCall<S>& c, const ChainPtrs& ws, cudaStream_t st);
 
 cudaError_t launch_ws_init(void* ctrl, cudaStream_t st);
 

@@ -49,8 +49,9 @@ struct ChainCfg {
   static constexpr int NSEG = NW * G;       // row segments per tile
   static constexpr int L = NSEG * R;        // rows per tile
   static constexpr int THREADS = (NW + 1) * 32;  // + coordinator warp
-  // carry record: [A or P: REC][B or c: REC], padded to 128-byte lines
-  static constexpr int REC = ((CPW * (int)sizeof(S) + 127) / 128) * 128 / (int)sizeof(S);
+  // carry record: two halves of REC 8-byte slots each (fp32: tagged words,
+  // fp64: values), padded to 128-byte lines
+  static constexpr int REC = ((CPW * 8 + 127) / 128) * 128 / 8;
 };
 
 // Workspace view of one chained launch (see capi.cpp for the layout).
@@ -80,26 +81,162 @@ struct ChainArgs {
   int64_t ntt;        // tiles along time
 };
 
-// Coordinator-warp part of the decoupled look-back.  On entry lanes < Q hold the tile
-// aggregate (TA, TB) of their VEC channels and, for the first tile of the
-// chain (pos == 0), the chain seed in (c, P).  On exit they hold the tile's
-// exclusive carry (c = state entering the tile, P = decay product from the
-// chain start).  Publishes the aggregate (flag AGG) and then the inclusive
-// carry (flag INC) of chunk k.
-template <class S, int VEC, int Q, int REC>
-__device__ __forceinline__ void chain_lookback(const ChainWs& ws, uint32_t epoch,
-                                               int64_t k, int64_t pos, int64_t col,
-                                               int64_t ncols, const S (&TA)[VEC],
-                                               const S (&TB)[VEC], S (&c)[VEC],
-                                               S (&P)[VEC], bool valid) {
-  using IO = VecIO<S, VEC>;
-  const int lane = threadIdx.x & 31;
-  S* agg = reinterpret_cast<S*>(ws.agg);
-  S* inc = reinterpret_cast<S*>(ws.inc);
-  const bool owner = lane < Q && valid;
-  const int off = lane * VEC;  // channel offset inside the record (lane < Q)
+// ---------------------------------------------------------------------------
+// Decoupled look-back, split in two so the tile's data warps can start their
+// re-scan before the tile's inclusive carry is published:
+//   Lookback<S,...>::exclusive()  -> exclusive carry (c = state entering the
+//                                    tile, P = decay product from the chain
+//                                    start) on lanes < Q; publishes the tile
+//                                    aggregate when it has to wait;
+//   Lookback<S,...>::publish()    -> inclusive carry of the tile.
+// Carries are APPLIED oldest first to the nearest published inclusive value,
+// so every tile obtains bit-identical carries whichever predecessor its look-
+// back stopped at (deterministic scan).
+//
+// fp32: every record element is one self-validating 64-bit word
+// (value << 32 | epoch << 2 | state) written and read with relaxed gpu-scope
+// 128-bit vector accesses (each 64-bit element is single-copy atomic), so no
+// memory fences and no separate flag are needed; each lane walks back over
+// its own channels.  fp64 values do not fit beside a tag, so the fp64 path
+// keeps value records + one release/acquire flag per tile.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void st_words2(uint64_t* p, uint64_t a, uint64_t b) {
+  asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_words2(const uint64_t* p, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st_word(uint64_t* p, uint64_t a) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(a) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_word(const uint64_t* p) {
+  uint64_t a;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(a) : "l"(p) : "memory");
+  return a;
+}
 
-  if (pos > 0) {
+template <int VEC>
+__device__ __forceinline__ void store_words(uint64_t* p, const float (&v)[VEC], uint32_t tag) {
+  uint64_t w[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) w[i] = ((uint64_t)__float_as_uint(v[i]) << 32) | tag;
+  if constexpr (VEC % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < VEC; i += 2) st_words2(p + i, w[i], w[i + 1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) st_word(p + i, w[i]);
+  }
+}
+
+// Loads VEC words; returns true when every tag equals `tag`.
+template <int VEC>
+__device__ __forceinline__ bool load_words(const uint64_t* p, float (&v)[VEC], uint32_t tag) {
+  uint64_t w[VEC];
+  if constexpr (VEC % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < VEC; i += 2) ld_words2(p + i, w[i], w[i + 1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) w[i] = ld_word(p + i);
+  }
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    ok = ok && (uint32_t)w[i] == tag;
+    v[i] = __uint_as_float((uint32_t)(w[i] >> 32));
+  }
+  return ok;
+}
+
+template <class S, int VEC, int Q, int REC, bool WANT_P>
+struct Lookback;
+
+// fp32: self-validating words.
+template <int VEC, int Q, int REC, bool WANT_P>
+struct Lookback<float, VEC, Q, REC, WANT_P> {
+  // agg record k: words [k*2*REC, +CPW) = A, [k*2*REC + REC, +CPW) = B
+  // inc record k: words [k*2*REC, +CPW) = c, [k*2*REC + REC, +CPW) = P
+  static __device__ __forceinline__ void exclusive(const ChainWs& ws, uint32_t epoch, int64_t k,
+                                                   int64_t pos, int64_t col, int64_t ncols,
+                                                   const float (&TA)[VEC], const float (&TB)[VEC],
+                                                   float (&c)[VEC], float (&P)[VEC], bool valid) {
+    const int lane = threadIdx.x & 31;
+    if (pos == 0 || !(lane < Q && valid)) return;
+    uint64_t* agg = reinterpret_cast<uint64_t*>(ws.agg);
+    const uint64_t* inc = reinterpret_cast<const uint64_t*>(ws.inc);
+    const int off = lane * VEC;
+    const uint32_t tinc = (epoch << 2) | kFlagInc, tagg = (epoch << 2) | kFlagAgg;
+    // fast path: the predecessor's inclusive carry is already visible
+    int64_t j = pos - 1;
+    const uint64_t* r0 = inc + (j * ncols + col) * 2 * REC + off;
+    bool have = load_words<VEC>(r0, c, tinc);
+    if (have && WANT_P) have = load_words<VEC>(r0 + REC, P, tinc);
+    if (have) return;
+    // publish our aggregate so successors need not wait for our carry
+    uint64_t* ra = agg + k * 2 * REC + off;
+    store_words<VEC>(ra, TA, tagg);
+    store_words<VEC>(ra + REC, TB, tagg);
+    // walk back to the nearest predecessor with an inclusive carry
+    for (;;) {
+      const uint64_t* ri = inc + (j * ncols + col) * 2 * REC + off;
+      bool ok = load_words<VEC>(ri, c, tinc);
+      if (ok && WANT_P) ok = load_words<VEC>(ri + REC, P, tinc);
+      if (ok) break;
+      float a[VEC], b[VEC];
+      const uint64_t* rg = agg + (j * ncols + col) * 2 * REC + off;
+      if (load_words<VEC>(rg, a, tagg) && load_words<VEC>(rg + REC, b, tagg)) --j;  // step back
+    }
+    // apply the aggregates of j+1 .. pos-1, oldest first (all visible now)
+#pragma unroll 1
+    for (int64_t i = j + 1; i < pos; ++i) {
+      float a[VEC], b[VEC];
+      const uint64_t* rg = agg + (i * ncols + col) * 2 * REC + off;
+      load_words<VEC>(rg, a, tagg);
+      load_words<VEC>(rg + REC, b, tagg);
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        c[v] = fma_(a[v], c[v], b[v]);
+        if (WANT_P) P[v] = mul_(a[v], P[v]);
+      }
+    }
+  }
+
+  static __device__ __forceinline__ void publish(const ChainWs& ws, uint32_t epoch, int64_t k,
+                                                 const float (&TA)[VEC], const float (&TB)[VEC],
+                                                 const float (&c)[VEC], const float (&P)[VEC],
+                                                 bool valid) {
+    const int lane = threadIdx.x & 31;
+    if (!(lane < Q && valid)) return;
+    uint64_t* inc = reinterpret_cast<uint64_t*>(ws.inc);
+    const uint32_t tinc = (epoch << 2) | kFlagInc;
+    float ci[VEC], Pi[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      ci[v] = fma_(TA[v], c[v], TB[v]);
+      Pi[v] = mul_(TA[v], P[v]);
+    }
+    uint64_t* r = inc + k * 2 * REC + lane * VEC;
+    if (WANT_P) store_words<VEC>(r + REC, Pi, tinc);
+    store_words<VEC>(r, ci, tinc);
+  }
+};
+
+// fp64: value records + per-tile release/acquire flag.
+template <int VEC, int Q, int REC, bool WANT_P>
+struct Lookback<double, VEC, Q, REC, WANT_P> {
+  using S = double;
+  using IO = VecIO<S, VEC>;
+  static __device__ __forceinline__ void exclusive(const ChainWs& ws, uint32_t epoch, int64_t k,
+                                                   int64_t pos, int64_t col, int64_t ncols,
+                                                   const S (&TA)[VEC], const S (&TB)[VEC],
+                                                   S (&c)[VEC], S (&P)[VEC], bool valid) {
+    if (pos == 0) return;
+    const int lane = threadIdx.x & 31;
+    S* agg = reinterpret_cast<S*>(ws.agg);
+    S* inc = reinterpret_cast<S*>(ws.inc);
+    const bool owner = lane < Q && valid;
+    const int off = lane * VEC;
     if (owner) {
       S* rec = agg + k * 2 * REC + off;
       IO::store_cg(rec, TA);
@@ -108,8 +245,6 @@ __device__ __forceinline__ void chain_lookback(const ChainWs& ws, uint32_t epoch
     }
     __syncwarp();
     if (lane == 0) st_release_gpu(&ws.flags[k], (epoch << 2) | kFlagAgg);
-
-    // nearest predecessor with a published inclusive carry
     int64_t jhi = pos - 1, jinc = 0;
     for (;;) {
       const int64_t jj = jhi - lane;
@@ -129,29 +264,10 @@ __device__ __forceinline__ void chain_lookback(const ChainWs& ws, uint32_t epoch
     }
     if (owner) {
       const S* rec = inc + (jinc * ncols + col) * 2 * REC + off;
-      IO::load_cg(rec, P);
-      IO::load_cg(rec + REC, c);
-      // apply the aggregates of chunks jinc+1 .. pos-1, oldest first
-      int64_t j = jinc + 1;
+      IO::load_cg(rec, c);
+      IO::load_cg(rec + REC, P);
 #pragma unroll 1
-      for (; j + 4 <= pos; j += 4) {
-        S a4[4][VEC], b4[4][VEC];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const S* r = agg + ((j + u) * ncols + col) * 2 * REC + off;
-          IO::load_cg(r, a4[u]);
-          IO::load_cg(r + REC, b4[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) {
-            c[v] = fma_(a4[u][v], c[v], b4[u][v]);
-            P[v] = mul_(a4[u][v], P[v]);
-          }
-      }
-#pragma unroll 1
-      for (; j < pos; ++j) {
+      for (int64_t j = jinc + 1; j < pos; ++j) {
         S a1[VEC], b1[VEC];
         const S* r = agg + (j * ncols + col) * 2 * REC + off;
         IO::load_cg(r, a1);
@@ -164,22 +280,28 @@ __device__ __forceinline__ void chain_lookback(const ChainWs& ws, uint32_t epoch
       }
     }
   }
-  // inclusive carry of this chunk
-  if (owner) {
-    S ci[VEC], Pi[VEC];
+
+  static __device__ __forceinline__ void publish(const ChainWs& ws, uint32_t epoch, int64_t k,
+                                                 const S (&TA)[VEC], const S (&TB)[VEC],
+                                                 const S (&c)[VEC], const S (&P)[VEC], bool valid) {
+    const int lane = threadIdx.x & 31;
+    S* inc = reinterpret_cast<S*>(ws.inc);
+    if (lane < Q && valid) {
+      S ci[VEC], Pi[VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      ci[v] = fma_(TA[v], c[v], TB[v]);
-      Pi[v] = mul_(TA[v], P[v]);
+      for (int v = 0; v < VEC; ++v) {
+        ci[v] = fma_(TA[v], c[v], TB[v]);
+        Pi[v] = mul_(TA[v], P[v]);
+      }
+      S* rec = inc + k * 2 * REC + lane * VEC;
+      IO::store_cg(rec, ci);
+      IO::store_cg(rec + REC, Pi);
+      fence_acq_rel_gpu();
     }
-    S* rec = inc + k * 2 * REC + off;
-    IO::store_cg(rec, Pi);
-    IO::store_cg(rec + REC, ci);
-    fence_acq_rel_gpu();
+    __syncwarp();
+    if (lane == 0) st_release_gpu(&ws.flags[k], (epoch << 2) | kFlagInc);
   }
-  __syncwarp();
-  if (lane == 0) st_release_gpu(&ws.flags[k], (epoch << 2) | kFlagInc);
-}
+};
 
 // Named barriers between the NW data warps and the coordinator warp.
 __device__ __forceinline__ void bar_arrive(int id, int n) {
@@ -255,12 +377,13 @@ __device__ __forceinline__ void chain_coordinator(const ChainArgs<S>& a, const C
       for (int v = 0; v < VEC; ++v) c[v] = a.seed[ch + v];
     }
   }
-  chain_lookback<S, VEC, Q, REC>(ws, epoch, k, pos, col, a.ncols, TA, TB, c, P, valid);
+  Lookback<S, VEC, Q, REC, false>::exclusive(ws, epoch, k, pos, col, a.ncols, TA, TB, c, P, valid);
   if (lane < Q) {
 #pragma unroll
     for (int v = 0; v < VEC; ++v) s_c[lane * VEC + v] = c[v];
   }
-  bar_arrive(2, NT);  // carry is in shared memory
+  bar_arrive(2, NT);  // carry is in shared memory: the data warps re-scan now
+  Lookback<S, VEC, Q, REC, false>::publish(ws, epoch, k, TA, TB, c, P, valid);
   chain_retire(ws, epoch);
 }
 

@@ -1,0 +1,462 @@
+// Persistent, warp-specialised chained scans fed by TMA (sm_100a).
+//
+// Same algorithm and bit-for-bit the same arithmetic order as the register
+// kernels of scan_chained.cuh (so the look-back stays deterministic), but the
+// memory system is kept busy continuously:
+//
+//   warp NW+1  producer     takes the next chunk ticket, issues one 2-D
+//                           cp.async.bulk.tensor per input array into a
+//                           STAGES-deep shared-memory ring (mbarrier
+//                           complete_tx), zero-filling rows/channels outside
+//                           the tensor;
+//   warps 0..NW-1 consumers copy their R rows x VEC channels of the staged tile
+//                           into registers, release the ring slot at once,
+//                           reduce them to an affine pair, publish warp
+//                           totals, wait for the tile's carry and re-scan,
+//                           storing results with 128-bit streaming stores;
+//   warp NW    coordinator  folds the warp totals into the tile aggregate and
+//                           runs the decoupled look-back (chain_lookback).
+//
+// One CTA (or two) per SM loops over tiles until the ticket counter passes the
+// tile count, so up to STAGES tiles per CTA are in flight while earlier tiles
+// wait for their carries: the look-back latency is hidden behind TMA traffic.
+#pragma once
+
+#include "scan_chained.cuh"
+#include "tma_util.cuh"
+
+namespace linrec_dev {
+
+template <class S, int VEC, int Q, int R, int NW, int STAGES, int NARR>
+struct TmaCfg {
+  static constexpr int kVEC = VEC, kQ = Q, kR = R, kNW = NW, kSTAGES = STAGES, kNARR = NARR;
+  static constexpr int G = 32 / Q;
+  static constexpr int CPW = Q * VEC;
+  static constexpr int NSEG = NW * G;
+  static constexpr int L = NSEG * R;
+  static constexpr int BOX_ROWS = L < 256 ? L : 256;
+  static constexpr int NBOX = L / BOX_ROWS;
+  static_assert(L % BOX_ROWS == 0, "tile rows must be a multiple of the TMA box");
+  static constexpr int ARR_BYTES = ((L * CPW * (int)sizeof(S) + 127) / 128) * 128;
+  static constexpr int STAGE_BYTES = NARR * ARR_BYTES;
+  static constexpr int TX_BYTES = NARR * L * CPW * (int)sizeof(S);
+  static constexpr int OFF_TOT = STAGES * STAGE_BYTES;  // [2][2][NW][CPW]
+  static constexpr int OFF_CARRY = OFF_TOT + 2 * 2 * NW * CPW * (int)sizeof(S);  // [2][CPW]
+  static constexpr int OFF_META = ((OFF_CARRY + 2 * CPW * (int)sizeof(S)) + 15) / 16 * 16;
+  static constexpr int OFF_BAR = OFF_META + STAGES * 8;
+  static constexpr int SMEM = OFF_BAR + (2 * STAGES + 4) * 8;
+  static constexpr int THREADS = (NW + 2) * 32;
+  static constexpr int REC = ChainCfg<S, VEC, Q, R, NW>::REC;
+};
+
+template <class Cfg, class S>
+struct TmaSmem {
+  unsigned char* base;
+  __device__ S* arr(int stage, int a) const {
+    return reinterpret_cast<S*>(base + stage * Cfg::STAGE_BYTES + a * Cfg::ARR_BYTES);
+  }
+  __device__ S* tot_a(int slot) const {
+    return reinterpret_cast<S*>(base + Cfg::OFF_TOT) + slot * 2 * Cfg::kNW * Cfg::CPW;
+  }
+  __device__ S* tot_b(int slot) const { return tot_a(slot) + Cfg::kNW * Cfg::CPW; }
+  __device__ S* carry(int slot) const {
+    return reinterpret_cast<S*>(base + Cfg::OFF_CARRY) + slot * Cfg::CPW;
+  }
+  __device__ long long* meta() const { return reinterpret_cast<long long*>(base + Cfg::OFF_META); }
+  __device__ uint64_t* full(int s) const { return reinterpret_cast<uint64_t*>(base + Cfg::OFF_BAR) + s; }
+  __device__ uint64_t* empty(int s) const {
+    return reinterpret_cast<uint64_t*>(base + Cfg::OFF_BAR) + Cfg::kSTAGES + s;
+  }
+  __device__ uint64_t* aggr(int slot) const {
+    return reinterpret_cast<uint64_t*>(base + Cfg::OFF_BAR) + 2 * Cfg::kSTAGES + slot;
+  }
+  __device__ uint64_t* carry_bar(int slot) const {
+    return reinterpret_cast<uint64_t*>(base + Cfg::OFF_BAR) + 2 * Cfg::kSTAGES + 2 + slot;
+  }
+};
+
+// Barrier setup shared by both directions.
+template <class Cfg, class SM>
+__device__ __forceinline__ void tma_init_barriers(const SM& sm) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::kSTAGES; ++s) {
+      mbar_init(sm.full(s), 1);
+      mbar_init(sm.empty(s), (Cfg::kNW + 1) * 32);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(sm.aggr(i), Cfg::kNW * 32);
+      mbar_init(sm.carry_bar(i), 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+}
+
+// Coordinator warp loop (both directions).
+template <class Cfg, class S, bool REV, class SM>
+__device__ __forceinline__ void tma_coordinator(const SM& sm, const ChainArgs<S>& a, const ChainWs& ws,
+                                                uint32_t epoch) {
+  constexpr int VEC = Cfg::kVEC, Q = Cfg::kQ, NW = Cfg::kNW, CPW = Cfg::CPW, STAGES = Cfg::kSTAGES;
+  const int lane = threadIdx.x & 31;
+  for (int n = 0;; ++n) {
+    const int s = n % STAGES;
+    mbar_wait(sm.full(s), (n / STAGES) & 1);
+    const long long k = sm.meta()[s];
+    mbar_arrive(sm.empty(s));
+    if (k < 0) break;
+    const int slot = n & 1;
+    mbar_wait(sm.aggr(slot), (n >> 1) & 1);
+    const int64_t col = k % a.ncols, pos = k / a.ncols;
+    const int64_t ch = col * CPW + (int64_t)lane * VEC;
+    const bool valid = lane < Q && ch < a.W;
+    S TA[VEC], TB[VEC], c[VEC], P[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) { TA[v] = S(1); TB[v] = S(0); c[v] = S(0); P[v] = S(1); }
+    if (lane < Q) {
+      const S* ta = sm.tot_a(slot);
+      const S* tb = sm.tot_b(slot);
+      constexpr int w0 = REV ? NW - 1 : 0;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        TA[v] = ta[w0 * CPW + lane * VEC + v];
+        TB[v] = tb[w0 * CPW + lane * VEC + v];
+      }
+#pragma unroll
+      for (int i = 1; i < NW; ++i) {
+        const int w = REV ? NW - 1 - i : i;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          TB[v] = fma_(ta[w * CPW + lane * VEC + v], TB[v], tb[w * CPW + lane * VEC + v]);
+          TA[v] = mul_(ta[w * CPW + lane * VEC + v], TA[v]);
+        }
+      }
+      if (pos == 0 && a.seed != nullptr && valid) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) c[v] = a.seed[ch + v];
+      }
+    }
+    Lookback<S, VEC, Q, Cfg::REC, false>::exclusive(ws, epoch, k, pos, col, a.ncols, TA, TB, c, P, valid);
+    if (lane < Q) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) sm.carry(slot)[lane * VEC + v] = c[v];
+    }
+    mbar_arrive(sm.carry_bar(slot));  // consumers re-scan while the carry is published
+    Lookback<S, VEC, Q, Cfg::REC, false>::publish(ws, epoch, k, TA, TB, c, P, valid);
+  }
+  chain_retire(ws, epoch);
+}
+
+// ---------------------------------------------------------------------------
+// forward
+// ---------------------------------------------------------------------------
+template <class S, int VEC, int Q, int R, int NW, int STAGES>
+__global__ void __launch_bounds__((NW + 2) * 32, 1)
+k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ CUtensorMap map_x,
+          const ChainArgs<S> a, const ChainWs ws, const long long ntiles) {
+  using Cfg = TmaCfg<S, VEC, Q, R, NW, STAGES, 2>;
+  using IO = VecIO<S, VEC>;
+  constexpr int G = Cfg::G, CPW = Cfg::CPW, L = Cfg::L;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const TmaSmem<Cfg, S> sm{smem_raw};
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  tma_init_barriers<Cfg>(sm);
+  const uint32_t epoch = __ldcg(&ws.ctrl->epoch);
+
+  if (warp == NW + 1) {  // ---------------- producer
+    if (lane == 0) {
+      prefetch_tmap(&map_lam);
+      prefetch_tmap(&map_x);
+      const uint64_t pol = policy_evict_first();
+      for (int n = 0;; ++n) {
+        const int s = n % STAGES;
+        if (n >= STAGES) mbar_wait(sm.empty(s), ((n / STAGES) + 1) & 1);
+        const long long k = (long long)atomicAdd(&ws.ctrl->ticket, 1ull);
+        if (k >= ntiles) {
+          sm.meta()[s] = -1;
+          mbar_arrive(sm.full(s));
+          break;
+        }
+        sm.meta()[s] = k;
+        const int c0 = (int)((k % a.ncols) * CPW);
+        const int r0 = (int)((k / a.ncols) * L);
+        mbar_arrive_expect_tx(sm.full(s), Cfg::TX_BYTES);
+#pragma unroll
+        for (int b = 0; b < Cfg::NBOX; ++b) {
+          tma_load_2d(sm.arr(s, 0) + b * Cfg::BOX_ROWS * CPW, &map_lam, c0, r0 + b * Cfg::BOX_ROWS, sm.full(s), pol);
+          tma_load_2d(sm.arr(s, 1) + b * Cfg::BOX_ROWS * CPW, &map_x, c0, r0 + b * Cfg::BOX_ROWS, sm.full(s), pol);
+        }
+      }
+    }
+    return;
+  }
+  if (warp == NW) {  // ---------------- coordinator
+    tma_coordinator<Cfg, S, false>(sm, a, ws, epoch);
+    return;
+  }
+
+  // ---------------------------------- consumers
+  const int q = lane % Q, g = lane / Q;
+  const int seg = warp * G + g;
+  const int64_t W = a.W;
+  for (int n = 0;; ++n) {
+    const int s = n % STAGES;
+    mbar_wait(sm.full(s), (n / STAGES) & 1);
+    const long long k = sm.meta()[s];
+    if (k < 0) break;
+    const int64_t col = k % a.ncols, pos = k / a.ncols;
+    const int64_t ch = col * CPW + (int64_t)q * VEC;
+    const bool valid = ch < W;
+    const int64_t t0 = pos * L + (int64_t)seg * R;
+    S l[R][VEC], xv[R][VEC];
+    const S* sl = sm.arr(s, 0) + seg * R * CPW + q * VEC;
+    const S* sx = sm.arr(s, 1) + seg * R * CPW + q * VEC;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      if (t0 + i < a.T) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) { l[i][v] = sl[i * CPW + v]; xv[i][v] = sx[i * CPW + v]; }
+      } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) { l[i][v] = S(1); xv[i][v] = S(0); }
+      }
+    }
+    mbar_arrive(sm.empty(s));  // tile is in registers: the ring slot can refill
+
+    S A[VEC], B[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) { A[v] = l[0][v]; B[v] = xv[0][v]; }
+#pragma unroll
+    for (int i = 1; i < R; ++i)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        B[v] = fma_(l[i][v], B[v], xv[i][v]);
+        A[v] = mul_(l[i][v], A[v]);
+      }
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const S ap = __shfl_up_sync(0xffffffffu, A[v], off * Q);
+        const S bp = __shfl_up_sync(0xffffffffu, B[v], off * Q);
+        if (g >= off) {
+          B[v] = fma_(A[v], bp, B[v]);
+          A[v] = mul_(A[v], ap);
+        }
+      }
+    }
+    S Ae[VEC], Be[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      Ae[v] = S(1);
+      Be[v] = S(0);
+      if (G > 1) {
+        const S ap = __shfl_up_sync(0xffffffffu, A[v], Q);
+        const S bp = __shfl_up_sync(0xffffffffu, B[v], Q);
+        if (g > 0) { Ae[v] = ap; Be[v] = bp; }
+      }
+    }
+    const int slot = n & 1;
+    S* ta = sm.tot_a(slot);
+    S* tb = sm.tot_b(slot);
+    if (g == G - 1) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        ta[warp * CPW + q * VEC + v] = A[v];
+        tb[warp * CPW + q * VEC + v] = B[v];
+      }
+    }
+    mbar_arrive(sm.aggr(slot));
+    mbar_wait(sm.carry_bar(slot), (n >> 1) & 1);
+
+    S cs[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) cs[v] = sm.carry(slot)[q * VEC + v];
+    for (int w = 0; w < warp; ++w)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) cs[v] = fma_(ta[w * CPW + q * VEC + v], cs[v], tb[w * CPW + q * VEC + v]);
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) cs[v] = fma_(Ae[v], cs[v], Be[v]);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) cs[v] = fma_(l[i][v], cs[v], xv[i][v]);
+      const int64_t t = t0 + i;
+      if (valid && t < a.T) IO::store_stream(a.out0 + t * W + ch, cs);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward (reverse time): arrays mu = lam shifted +1 row, dh, h shifted -1 row
+// ---------------------------------------------------------------------------
+template <class S, int VEC, int Q, int R, int NW, int STAGES>
+__global__ void __launch_bounds__((NW + 2) * 32, 1)
+k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ CUtensorMap map_dh,
+          const __grid_constant__ CUtensorMap map_h, const ChainArgs<S> a, const ChainWs ws,
+          const long long ntiles) {
+  using Cfg = TmaCfg<S, VEC, Q, R, NW, STAGES, 3>;
+  using IO = VecIO<S, VEC>;
+  constexpr int G = Cfg::G, CPW = Cfg::CPW, L = Cfg::L;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const TmaSmem<Cfg, S> sm{smem_raw};
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  tma_init_barriers<Cfg>(sm);
+  const uint32_t epoch = __ldcg(&ws.ctrl->epoch);
+
+  if (warp == NW + 1) {  // ---------------- producer
+    if (lane == 0) {
+      prefetch_tmap(&map_lam);
+      prefetch_tmap(&map_dh);
+      prefetch_tmap(&map_h);
+      const uint64_t pol = policy_evict_first();
+      for (int n = 0;; ++n) {
+        const int s = n % STAGES;
+        if (n >= STAGES) mbar_wait(sm.empty(s), ((n / STAGES) + 1) & 1);
+        const long long k = (long long)atomicAdd(&ws.ctrl->ticket, 1ull);
+        if (k >= ntiles) {
+          sm.meta()[s] = -1;
+          mbar_arrive(sm.full(s));
+          break;
+        }
+        sm.meta()[s] = k;
+        const int c0 = (int)((k % a.ncols) * CPW);
+        const int r0 = (int)((a.ntt - 1 - k / a.ncols) * L);
+        mbar_arrive_expect_tx(sm.full(s), Cfg::TX_BYTES);
+#pragma unroll
+        for (int b = 0; b < Cfg::NBOX; ++b) {
+          const int rb = r0 + b * Cfg::BOX_ROWS;
+          tma_load_2d(sm.arr(s, 0) + b * Cfg::BOX_ROWS * CPW, &map_lam, c0, rb + 1, sm.full(s), pol);
+          tma_load_2d(sm.arr(s, 1) + b * Cfg::BOX_ROWS * CPW, &map_dh, c0, rb, sm.full(s), pol);
+          tma_load_2d(sm.arr(s, 2) + b * Cfg::BOX_ROWS * CPW, &map_h, c0, rb - 1, sm.full(s), pol);
+        }
+      }
+    }
+    return;
+  }
+  if (warp == NW) {  // ---------------- coordinator
+    tma_coordinator<Cfg, S, true>(sm, a, ws, epoch);
+    return;
+  }
+
+  // ---------------------------------- consumers
+  const int q = lane % Q, g = lane / Q;
+  const int seg = warp * G + g;
+  const int64_t W = a.W, T = a.T;
+  for (int n = 0;; ++n) {
+    const int s = n % STAGES;
+    mbar_wait(sm.full(s), (n / STAGES) & 1);
+    const long long k = sm.meta()[s];
+    if (k < 0) break;
+    const int64_t col = k % a.ncols, pos = k / a.ncols;
+    const int64_t tile = a.ntt - 1 - pos;
+    const int64_t ch = col * CPW + (int64_t)q * VEC;
+    const bool valid = ch < W;
+    const int64_t t0 = tile * L + (int64_t)seg * R;
+    S mu[R][VEC], dh[R][VEC], hp[R][VEC];
+    const S* smu = sm.arr(s, 0) + seg * R * CPW + q * VEC;
+    const S* sdh = sm.arr(s, 1) + seg * R * CPW + q * VEC;
+    const S* shp = sm.arr(s, 2) + seg * R * CPW + q * VEC;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int64_t t = t0 + i;
+      if (t < T) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          mu[i][v] = smu[i * CPW + v];
+          dh[i][v] = sdh[i * CPW + v];
+          hp[i][v] = shp[i * CPW + v];
+        }
+        if (t == T - 1) {  // zero-filled past the end; the segment form supplies lam_next
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) mu[i][v] = (a.lam_next != nullptr && valid) ? a.lam_next[ch + v] : S(0);
+        }
+        if (t == 0) {  // zero-filled row -1 -> h0
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) hp[i][v] = (a.aux != nullptr && valid) ? a.aux[ch + v] : S(0);
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) { mu[i][v] = S(1); dh[i][v] = S(0); hp[i][v] = S(0); }
+      }
+    }
+    mbar_arrive(sm.empty(s));
+
+    S A[VEC], B[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) { A[v] = mu[R - 1][v]; B[v] = dh[R - 1][v]; }
+#pragma unroll
+    for (int i = R - 2; i >= 0; --i)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        B[v] = fma_(mu[i][v], B[v], dh[i][v]);
+        A[v] = mul_(mu[i][v], A[v]);
+      }
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const S ap = __shfl_down_sync(0xffffffffu, A[v], off * Q);
+        const S bp = __shfl_down_sync(0xffffffffu, B[v], off * Q);
+        if (g + off < G) {
+          B[v] = fma_(A[v], bp, B[v]);
+          A[v] = mul_(A[v], ap);
+        }
+      }
+    }
+    S Ae[VEC], Be[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      Ae[v] = S(1);
+      Be[v] = S(0);
+      if (G > 1) {
+        const S ap = __shfl_down_sync(0xffffffffu, A[v], Q);
+        const S bp = __shfl_down_sync(0xffffffffu, B[v], Q);
+        if (g < G - 1) { Ae[v] = ap; Be[v] = bp; }
+      }
+    }
+    const int slot = n & 1;
+    S* ta = sm.tot_a(slot);
+    S* tb = sm.tot_b(slot);
+    if (g == 0) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        ta[warp * CPW + q * VEC + v] = A[v];
+        tb[warp * CPW + q * VEC + v] = B[v];
+      }
+    }
+    mbar_arrive(sm.aggr(slot));
+    mbar_wait(sm.carry_bar(slot), (n >> 1) & 1);
+
+    S cs[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) cs[v] = sm.carry(slot)[q * VEC + v];
+    for (int w = NW - 1; w > warp; --w)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) cs[v] = fma_(ta[w * CPW + q * VEC + v], cs[v], tb[w * CPW + q * VEC + v]);
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) cs[v] = fma_(Ae[v], cs[v], Be[v]);
+#pragma unroll
+    for (int i = R - 1; i >= 0; --i) {
+      S dl[VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        cs[v] = fma_(mu[i][v], cs[v], dh[i][v]);
+        dl[v] = mul_(hp[i][v], cs[v]);
+      }
+      const int64_t t = t0 + i;
+      if (valid && t < T) {
+        IO::store_stream(a.out0 + t * W + ch, cs);
+        IO::store_stream(a.out1 + t * W + ch, dl);
+        if (t == 0 && a.out2 != nullptr) {
+          S l0[VEC], d0[VEC];
+          IO::load_cg(a.a + ch, l0);
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) d0[v] = mul_(l0[v], cs[v]);
+          IO::store_cg(a.out2 + ch, d0);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace linrec_dev

@@ -33,6 +33,16 @@ def lr():
     return linrec
 
 
+@pytest.fixture(params=["auto", "register"])
+def policy(request):
+    """Run a test with the TMA persistent kernels (auto) and with the
+    register-tiled kernels forced."""
+    from paper_1709_04057_b200 import capi
+    capi.set_kernel_policy(capi.KERNEL_AUTO if request.param == "auto" else capi.KERNEL_REGISTER)
+    yield request.param
+    capi.set_kernel_policy(capi.KERNEL_AUTO)
+
+
 @pytest.fixture(scope="module")
 def ops():
     from paper_1709_04057_b200 import torch_ops
@@ -77,7 +87,7 @@ def test_golden_numpy_boundary(lr, name):
 
 
 @pytest.mark.parametrize("name", RANDOM_CASES)
-def test_golden_device_boundary(ops, name):
+def test_golden_device_boundary(ops, policy, name):
     g = load_golden(name)
     lam, x, h0, dh = (cuda(g[k]) for k in ("lam", "x", "h0", "dh"))
     tol = tol_of(g["lam"])
@@ -93,7 +103,7 @@ def test_golden_device_boundary(ops, name):
         assert rel(got.cpu().numpy(), g[key]) <= tol, key
 
 
-def test_frozen_dyadic_values(lr):
+def test_frozen_dyadic_values(lr, policy):
     g = load_golden("frozen")
     for dt in (np.float64, np.float32):
         lam, x, h0 = (g[k].astype(dt) for k in ("dyadic_lam", "dyadic_x", "dyadic_h0"))
@@ -111,7 +121,7 @@ def test_frozen_dyadic_values(lr):
         assert np.array_equal(dh0, g["t1_dh0"])
 
 
-def test_identities_exact(lr):
+def test_identities_exact(lr, policy):
     g = load_golden("identities")
     for mode in ("serial", "parallel"):
         assert np.array_equal(lr.scan(g["ones_lam"], g["ones_x"], g["ones_h0"], mode=mode), g["ones_h"])
@@ -197,7 +207,7 @@ SWEEP_T = [1, 2, 31, 47, 48, 49, 257, 1000]
 
 @pytest.mark.parametrize("W", SWEEP_W)
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-def test_sweep_against_oracle(ops, oracle, W, dtype):
+def test_sweep_against_oracle(ops, oracle, policy, W, dtype):
     rng = np.random.default_rng(W)
     for T in SWEEP_T:
         lam = rng.uniform(-1, 1, (T, 1, W)).astype(dtype)
@@ -232,7 +242,7 @@ def test_unaligned_pointers_take_scalar_path(ops, oracle):
     assert rel(h.cpu().numpy(), ref) <= 1e-5
 
 
-def test_deterministic_run_to_run(ops):
+def test_deterministic_run_to_run(ops, policy):
     g = torch.Generator(device="cuda").manual_seed(0)
     T, W = 40000, 512
     lam = torch.rand(T, 1, W, device="cuda", generator=g) * 0.9 + 0.05
@@ -246,7 +256,7 @@ def test_deterministic_run_to_run(ops):
     assert all(torch.equal(a, b) for a, b in zip(g1, g2))
 
 
-def test_stress_decay_distributions(ops, oracle):
+def test_stress_decay_distributions(ops, oracle, policy):
     rng = np.random.default_rng(11)
     T, W = 20000, 96
     for lo, hi in ((0.99, 1.0), (-1.0, 1.0), (0.05, 0.95), (0.999, 1.0)):
@@ -283,7 +293,7 @@ def test_host_pipeline_multi_chunk(lr, oracle):
         assert rel(a, r) <= 1e-5
 
 
-def test_backward_segments_chain_bit_exactly(oracle):
+def test_backward_segments_chain_bit_exactly(oracle, policy):
     from paper_1709_04057_b200 import capi
     rng = np.random.default_rng(13)
     T, W, k = 1000, 36, 377
@@ -315,7 +325,7 @@ def test_backward_segments_chain_bit_exactly(oracle):
                 assert rel(a, r) <= 1e-5
 
 
-def test_workspace_reuse_and_cuda_graph_replay(ops, oracle):
+def test_workspace_reuse_and_cuda_graph_replay(ops, oracle, policy):
     """Epoch/ticket state lives on the device: a captured graph replays correctly."""
     from paper_1709_04057_b200 import capi
     ws = capi.Workspace(0)
@@ -381,3 +391,48 @@ def test_cuda_array_interface_zero_copy(lr, oracle):
     torch.cuda.synchronize()
     h = torch.as_tensor(out, device="cuda").cpu().numpy()
     assert rel(h, oracle.scan_serial(lam, x)) <= 1e-5
+
+
+@pytest.mark.parametrize("T,W", [(65536, 8192), (1 << 20, 128), (4096, 256), (3000, 1000)])
+def test_benchmark_shapes_channel_subset(ops, oracle, T, W):
+    """BASELINE configs at full size: every channel is an independent chain, so
+    the oracle is run on a strided subset of channels over the FULL T."""
+    g = torch.Generator(device="cuda").manual_seed(T + W)
+    lam = torch.rand(T, 1, W, device="cuda", generator=g) * 0.9 + 0.05
+    x = torch.rand(T, 1, W, device="cuda", generator=g) * 2 - 1
+    h0 = torch.rand(1, W, device="cuda", generator=g) * 2 - 1
+    dh = torch.rand(T, 1, W, device="cuda", generator=g) * 2 - 1
+    h = ops.scan(lam, x, h0)
+    dlam, dx, dh0 = ops.scan_backward(lam, h0, h, dh)
+    cols = sorted(set(list(range(0, W, max(1, W // 61))) + [W - 1]))
+    sub = lambda t: t[..., cols].contiguous().cpu().numpy()  # noqa: E731
+    ref = oracle.scan_serial(sub(lam), sub(x), sub(h0))
+    assert rel(sub(h), ref) <= 1e-5
+    gref = oracle.scan_backward(sub(lam), sub(h0), sub(h), sub(dh))
+    for a, r in zip((dlam, dx, dh0), gref):
+        assert rel(sub(a), r) <= 1e-5
+    # full-tensor properties: finite everywhere, and dx's first row = dh0 / lam_0
+    assert torch.isfinite(h).all() and torch.isfinite(dlam).all() and torch.isfinite(dx).all()
+    assert torch.allclose(dh0, lam[0] * dx[0], rtol=1e-6, atol=0)
+
+
+def test_tma_and_register_kernels_agree(ops):
+    from paper_1709_04057_b200 import capi
+    g = torch.Generator(device="cuda").manual_seed(3)
+    T, W = 20000, 2048
+    lam = torch.rand(T, 1, W, device="cuda", generator=g) * 0.9 + 0.05
+    x = torch.rand(T, 1, W, device="cuda", generator=g) * 2 - 1
+    dh = torch.rand(T, 1, W, device="cuda", generator=g) * 2 - 1
+    h_auto = ops.scan(lam, x)
+    g_auto = ops.scan_backward(lam, None, h_auto, dh)
+    capi.set_kernel_policy(capi.KERNEL_REGISTER)
+    try:
+        h_reg = ops.scan(lam, x)
+        g_reg = ops.scan_backward(lam, None, h_auto, dh)
+    finally:
+        capi.set_kernel_policy(capi.KERNEL_AUTO)
+    hs = ops.scan(lam, x, mode="serial")
+    for hh in (h_auto, h_reg):
+        assert ((hh - hs).abs().max() / hs.abs().max()).item() <= 1e-5
+    for a, b in zip(g_auto, g_reg):
+        assert ((a - b).abs().max() / b.abs().max()).item() <= 1e-5
