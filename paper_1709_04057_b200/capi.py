@@ -13,7 +13,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblinrec_cuda.so")
+LIB_PATH = os.environ.get("LINREC_LIB_PATH") or os.path.join(HERE, "liblinrec_cuda.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "linrec_cuda.h")
 
 SERIAL = 0

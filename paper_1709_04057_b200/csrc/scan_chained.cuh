@@ -97,7 +97,8 @@ struct ChainArgs {
 // (value << 32 | epoch << 2 | state) written and read with relaxed gpu-scope
 // 128-bit vector accesses (each 64-bit element is single-copy atomic), so no
 // memory fences and no separate flag are needed; each lane walks back over
-// its own channels.  fp64 values do not fit beside a tag, so the fp64 path
+// its own channels.  (A warp-wide flag window was measured slower on B200:
+// the per-lane word probe is one round trip shorter on the common path.)  fp64 values do not fit beside a tag, so the fp64 path
 // keeps value records + one release/acquire flag per tile.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void st_words2(uint64_t* p, uint64_t a, uint64_t b) {
@@ -167,25 +168,26 @@ struct Lookback<float, VEC, Q, REC, WANT_P> {
     const uint64_t* inc = reinterpret_cast<const uint64_t*>(ws.inc);
     const int off = lane * VEC;
     const uint32_t tinc = (epoch << 2) | kFlagInc, tagg = (epoch << 2) | kFlagAgg;
-    // fast path: the predecessor's inclusive carry is already visible
+    // fast path (one round trip): the predecessor's inclusive carry
     int64_t j = pos - 1;
     const uint64_t* r0 = inc + (j * ncols + col) * 2 * REC + off;
-    bool have = load_words<VEC>(r0, c, tinc);
-    if (have && WANT_P) have = load_words<VEC>(r0 + REC, P, tinc);
-    if (have) return;
+    if (load_words<VEC>(r0, c, tinc) && (!WANT_P || load_words<VEC>(r0 + REC, P, tinc))) return;
     // publish our aggregate so successors need not wait for our carry
     uint64_t* ra = agg + k * 2 * REC + off;
     store_words<VEC>(ra, TA, tagg);
     store_words<VEC>(ra + REC, TB, tagg);
-    // walk back to the nearest predecessor with an inclusive carry
+    // walk back: inclusive carry of j, or step over j once its aggregate is
+    // visible (one round trip per probe: both records are loaded together)
+    SpinGuard guard;
     for (;;) {
+      guard.tick();
       const uint64_t* ri = inc + (j * ncols + col) * 2 * REC + off;
-      bool ok = load_words<VEC>(ri, c, tinc);
-      if (ok && WANT_P) ok = load_words<VEC>(ri + REC, P, tinc);
-      if (ok) break;
-      float a[VEC], b[VEC];
       const uint64_t* rg = agg + (j * ncols + col) * 2 * REC + off;
-      if (load_words<VEC>(rg, a, tagg) && load_words<VEC>(rg + REC, b, tagg)) --j;  // step back
+      float a[VEC], b[VEC];
+      const bool oki = load_words<VEC>(ri, c, tinc) && (!WANT_P || load_words<VEC>(ri + REC, P, tinc));
+      const bool oka = load_words<VEC>(rg, a, tagg) & load_words<VEC>(rg + REC, b, tagg);
+      if (oki) break;
+      if (oka) --j;
     }
     // apply the aggregates of j+1 .. pos-1, oldest first (all visible now)
 #pragma unroll 1
@@ -206,6 +208,13 @@ struct Lookback<float, VEC, Q, REC, WANT_P> {
                                                  const float (&TA)[VEC], const float (&TB)[VEC],
                                                  const float (&c)[VEC], const float (&P)[VEC],
                                                  bool valid) {
+    publish_words(ws, epoch, k, TA, TB, c, P, valid);
+  }
+
+  static __device__ __forceinline__ void publish_words(const ChainWs& ws, uint32_t epoch, int64_t k,
+                                                       const float (&TA)[VEC], const float (&TB)[VEC],
+                                                       const float (&c)[VEC], const float (&P)[VEC],
+                                                       bool valid) {
     const int lane = threadIdx.x & 31;
     if (!(lane < Q && valid)) return;
     uint64_t* inc = reinterpret_cast<uint64_t*>(ws.inc);
@@ -220,6 +229,7 @@ struct Lookback<float, VEC, Q, REC, WANT_P> {
     if (WANT_P) store_words<VEC>(r + REC, Pi, tinc);
     store_words<VEC>(r, ci, tinc);
   }
+
 };
 
 // fp64: value records + per-tile release/acquire flag.
@@ -252,7 +262,11 @@ struct Lookback<double, VEC, Q, REC, WANT_P> {
       if (jj >= 0) {
         const uint32_t* fp = &ws.flags[jj * ncols + col];
         uint32_t f = ld_acquire_gpu(fp);
-        while ((f >> 2) != epoch) f = ld_acquire_gpu(fp);
+        SpinGuard guard;
+        while ((f >> 2) != epoch) {
+          guard.tick();
+          f = ld_acquire_gpu(fp);
+        }
         is_inc = (f & 3u) == kFlagInc;
       }
       const unsigned m = __ballot_sync(0xffffffffu, is_inc);

@@ -27,6 +27,13 @@
 
 namespace linrec_dev {
 
+// Largest divisor of L that fits a TMA box dimension (<= 256).
+constexpr int box_rows_for(int L) {
+  for (int b = L < 256 ? L : 256; b > 1; --b)
+    if (L % b == 0) return b;
+  return 1;
+}
+
 template <class S, int VEC, int Q, int R, int NW, int STAGES, int NARR>
 struct TmaCfg {
   static constexpr int kVEC = VEC, kQ = Q, kR = R, kNW = NW, kSTAGES = STAGES, kNARR = NARR;
@@ -34,7 +41,7 @@ struct TmaCfg {
   static constexpr int CPW = Q * VEC;
   static constexpr int NSEG = NW * G;
   static constexpr int L = NSEG * R;
-  static constexpr int BOX_ROWS = L < 256 ? L : 256;
+  static constexpr int BOX_ROWS = box_rows_for(L);
   static constexpr int NBOX = L / BOX_ROWS;
   static_assert(L % BOX_ROWS == 0, "tile rows must be a multiple of the TMA box");
   static constexpr int ARR_BYTES = ((L * CPW * (int)sizeof(S) + 127) / 128) * 128;

@@ -30,7 +30,7 @@ bool plan_tma_fwd_f32(int64_t T, int64_t W, ChainPlan* p);
 template <>
 bool plan_tma<float>(bool forward, int64_t T, int64_t W, ChainPlan* p) {
   if (forward) return plan_tma_fwd_f32(T, W, p);
-  const int q = pick_q(W / 4);
+  const int q = pick_q_tma(W / 4);
   if (q < 4) return false;
   const TmaChoice ch = tma_choice(false, false, q);
 #define X(Q, R, ST, NW)                                                                  \

@@ -47,7 +47,7 @@ cudaError_t launch_tma_bwd<double>(const ChainPlan& p, const BwdCall<double>& c,
 
 template <>
 bool plan_tma<double>(bool forward, int64_t T, int64_t W, ChainPlan* p) {
-  const int q = pick_q(W / 2);
+  const int q = pick_q_tma(W / 2);
   if (q < 4) return false;
   const TmaChoice ch = tma_choice(true, forward, q);
   if (forward) {

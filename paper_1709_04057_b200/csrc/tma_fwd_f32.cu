@@ -27,7 +27,7 @@ cudaError_t launch_tma_fwd<float>(const ChainPlan& p, const FwdCall<float>& c, c
 // forward planning for float lives here (the kernel pointers are needed for
 // the occupancy query); the backward planning is in tma_bwd_f32.cu.
 bool plan_tma_fwd_f32(int64_t T, int64_t W, ChainPlan* p) {
-  const int q = pick_q(W / 4);
+  const int q = pick_q_tma(W / 4);
   if (q < 4) return false;
   const TmaChoice ch = tma_choice(false, true, q);
 #define X(Q, R, ST, NW)                                                                  \

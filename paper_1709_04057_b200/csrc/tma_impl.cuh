@@ -19,14 +19,24 @@ struct TmaChoice {
 // the C2 workload, profiles/); LINREC_TMA_FWD / LINREC_TMA_BWD ("R,STAGES,NW")
 // override it for tuning runs when that triple is instantiated.
 inline TmaChoice tma_choice(bool f64, bool fwd, int q) {
-  TmaChoice c = fwd ? TmaChoice{8, 2, 8} : TmaChoice{8, 2, 8};
-  if (f64 || q != 32) c = fwd ? TmaChoice{4, 3, 8} : TmaChoice{4, 2, 8};
-  if (!f64 && q == 32) {
+  TmaChoice c = fwd ? TmaChoice{12, 2, 8} : TmaChoice{12, 1, 8};
+  if (f64) c = fwd ? TmaChoice{4, 3, 8} : TmaChoice{4, 2, 8};
+  if (!f64) {
     const char* e = std::getenv(fwd ? "LINREC_TMA_FWD" : "LINREC_TMA_BWD");
     int r = 0, s = 0, nw = 8;
     if (e && std::sscanf(e, "%d,%d,%d", &r, &s, &nw) >= 2) c = TmaChoice{r, s, nw};
   }
   return c;
+}
+
+// Lanes across channels for the TMA kernels: as wide as W allows (128-bit
+// vectors, up to 32 lanes), but narrow enough that there are at least 8
+// independent channel columns -- few columns turn the look-back into one long
+// serial chain (the 1M-step, 128-channel regime).
+inline int pick_q_tma(int64_t nvec) {
+  int q = pick_q(nvec);
+  while (q > 4 && (nvec + q - 1) / q < 8) q >>= 1;
+  return q;
 }
 
 inline int sm_count() {
@@ -125,12 +135,12 @@ linrec_dev::ChainArgs<S> bwd_args(const ChainPlan& p, const BwdCall<S>& c) {
 
 // Instantiation tables: (Q, R, STAGES, NW) compiled for each direction; the
 // first Q=32 rows are the defaults, the others tuning candidates.
-#define LINREC_TMA_FWD_TABLE(X)                                                            \
-  X(32, 8, 2, 8) X(32, 8, 3, 8) X(32, 12, 2, 8) X(32, 16, 2, 4) X(32, 16, 1, 8) X(32, 16, 3, 4) \
-  X(32, 4, 3, 8) X(16, 4, 3, 8) X(8, 4, 3, 8) X(4, 4, 3, 8)
-#define LINREC_TMA_BWD_TABLE(X)                                                            \
-  X(32, 8, 2, 8) X(32, 6, 2, 8) X(32, 12, 1, 8) X(32, 8, 2, 4) X(32, 12, 2, 4) X(32, 4, 3, 8)  \
-  X(16, 4, 2, 8) X(8, 4, 2, 8) X(4, 4, 2, 8)
+#define LINREC_TMA_FWD_TABLE(X)                                                     \
+  X(32, 12, 2, 8) X(32, 8, 2, 8) X(32, 16, 1, 8) X(32, 12, 1, 8) X(32, 10, 2, 8)       \
+  X(16, 12, 2, 8) X(8, 12, 2, 8) X(4, 12, 2, 8) X(16, 8, 2, 8) X(8, 8, 2, 8) X(4, 8, 2, 8)
+#define LINREC_TMA_BWD_TABLE(X)                                                     \
+  X(32, 12, 1, 8) X(32, 8, 2, 8) X(32, 10, 1, 8) X(32, 16, 1, 8)                       \
+  X(16, 12, 1, 8) X(8, 12, 1, 8) X(4, 12, 1, 8) X(16, 8, 2, 8) X(8, 8, 2, 8) X(4, 8, 2, 8)
 #define LINREC_TMA_F64_FWD_TABLE(X) X(32, 4, 3, 8) X(16, 4, 3, 8) X(8, 4, 3, 8) X(4, 4, 3, 8)
 #define LINREC_TMA_F64_BWD_TABLE(X) X(32, 4, 2, 8) X(16, 4, 2, 8) X(8, 4, 2, 8) X(4, 4, 2, 8)
 

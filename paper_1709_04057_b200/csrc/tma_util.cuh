@@ -4,6 +4,8 @@
 #include <cuda.h>  // CUtensorMap (type only; the driver is reached via cudaGetDriverEntryPoint)
 #include <cstdint>
 
+#include "linrec_device.cuh"
+
 namespace linrec_dev {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -45,8 +47,9 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
-  }
+  if (mbar_try_wait(bar, parity)) return;
+  SpinGuard g;
+  while (!mbar_try_wait(bar, parity)) g.tick();
 }
 
 // 2-D tiled TMA load: box at (c0 = innermost coordinate, c1 = row) of the

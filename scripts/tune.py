@@ -61,7 +61,14 @@ def err(a, b):
 
 
 peak = 6555.2
-configs = [("register", None, None)]
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    _h = pynvml.nvmlDeviceGetHandleByIndex(0)
+except Exception:
+    _h = None
+
+configs = [] if os.environ.get("TUNE_NO_REGISTER") else [("register", None, None)]
 configs += [("tma", f, None) for f in os.environ.get("TUNE_FWD", "8,2,8;8,3,8;12,2,8;16,2,4;16,3,4;16,1,8;4,3,8").split(";")]
 configs += [("tma", None, b) for b in os.environ.get("TUNE_BWD", "8,2,8;6,2,8;12,1,8;8,2,4;12,2,4;4,3,8").split(";")]
 for kind, fc, bc in configs:
@@ -72,6 +79,7 @@ for kind, fc, bc in configs:
         else:
             os.environ.pop(k, None)
     rec = {"kind": kind, "fwd_cfg": fc, "bwd_cfg": bc, "T": T, "W": W}
+    print("start", kind, fc, bc, file=sys.stderr, flush=True)
     if kind == "register" or fc:
         ms = timeit(fwd)
         rec.update(fwd_ms=ms, fwd_gbs=12 * N / ms / 1e6, fwd_frac=12 * N / ms / 1e6 / peak, fwd_err=err(h, ref_h))
@@ -79,4 +87,7 @@ for kind, fc, bc in configs:
         ms = timeit(bwd)
         rec.update(bwd_ms=ms, bwd_gbs=20 * N / ms / 1e6, bwd_frac=20 * N / ms / 1e6 / peak,
                    bwd_err=max(err(dx, ref_dx), err(dlam, ref_dlam)))
+    if _h is not None:
+        rec["sm_mhz"] = pynvml.nvmlDeviceGetClockInfo(_h, pynvml.NVML_CLOCK_SM)
+    rec["lib"] = os.path.basename(capi.LIB_PATH)
     print(json.dumps(rec), flush=True)
