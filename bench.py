@@ -281,7 +281,7 @@ def run_ours(args):
             },
             "roofline": {
                 "bound": "hbm",
-                "kernel": "k_chain_bwd (reverse-time chained scan, fused dlam/dx)",
+                "kernel": "k_tma_bwd (persistent TMA-fed reverse-time chained scan, fused dlam/dx/dh0)",
                 "achieved": bwd_gbs,
                 "peak": peak,
                 "peak_kind": peak_kind,
