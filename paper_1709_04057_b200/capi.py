@@ -59,6 +59,14 @@ def _load():
         getattr(lib, f"linrec_scan_host_{s}").argtypes = [_vp] * 4 + [_i64, _i64, _int, _int]
         getattr(lib, f"linrec_scan_backward_host_{s}").argtypes = [_vp] * 7 + [_i64, _i64, _int, _int]
         getattr(lib, f"linrec_first_nonfinite_{s}").argtypes = [_vp, _i64, C.POINTER(_i64), _vp]
+        getattr(lib, f"linrec_segment_scan_{s}").argtypes = [_vp] * 6 + [_i64, _i64, _vp, _vp]
+        getattr(lib, f"linrec_segment_scan_backward_{s}").argtypes = [_vp] * 10 + [_i64, _i64, _vp, _vp]
+        getattr(lib, f"linrec_backward_aggregate_{s}").argtypes = [_vp] * 4 + [_i64, _vp]
+        getattr(lib, f"linrec_compose_carries_{s}").argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp]
+        getattr(lib, f"linrec_segment_fixup_{s}").argtypes = [_vp] * 4 + [_i64, _i64, _i64, _vp]
+        getattr(lib, f"linrec_segment_fixup_backward_{s}").argtypes = [_vp] * 8 + [_i64, _i64, _i64, _vp]
+    lib.linrec_segment_tile_rows.restype = _i64
+    lib.linrec_segment_tile_rows.argtypes = [_i64, _i64, _int, _int]
     return lib
 
 
@@ -121,6 +129,39 @@ def first_nonfinite(v, n, dtype_bytes=4, stream=0) -> int:
     out = _i64(-1)
     check(getattr(lib, f"linrec_first_nonfinite_{_sfx(dtype_bytes)}")(v, n, C.byref(out), stream))
     return int(out.value)
+
+
+# ---- sequence sharding (see include/linrec_cuda.h) ---------------------------
+def segment_tile_rows(T, W, backward=False, dtype_bytes=4) -> int:
+    return int(lib.linrec_segment_tile_rows(T, W, dtype_bytes, 1 if backward else 0))
+
+
+def segment_scan(lam, x, h0, h, seg_prod, agg, T, W, dtype_bytes=4, ws=None, stream=0):
+    check(getattr(lib, f"linrec_segment_scan_{_sfx(dtype_bytes)}")(lam, x, h0, h, seg_prod, agg, T, W, ws, stream))
+
+
+def segment_scan_backward(lam, hprev, h, dh, lam_next, dlam, dx, dh0, seg_prod, agg, T, W, dtype_bytes=4,
+                          ws=None, stream=0):
+    check(getattr(lib, f"linrec_segment_scan_backward_{_sfx(dtype_bytes)}")(
+        lam, hprev, h, dh, lam_next, dlam, dx, dh0, seg_prod, agg, T, W, ws, stream))
+
+
+def backward_aggregate(lam, agg_loc, dh0_loc, agg_out, W, dtype_bytes=4, stream=0):
+    check(getattr(lib, f"linrec_backward_aggregate_{_sfx(dtype_bytes)}")(lam, agg_loc, dh0_loc, agg_out, W, stream))
+
+
+def compose_carries(aggs, first, last, step, seed, out, W, dtype_bytes=4, stream=0):
+    check(getattr(lib, f"linrec_compose_carries_{_sfx(dtype_bytes)}")(aggs, first, last, step, seed, out, W, stream))
+
+
+def segment_fixup(lam, h, seg_prod, c_in, T, W, tile_rows, dtype_bytes=4, stream=0):
+    check(getattr(lib, f"linrec_segment_fixup_{_sfx(dtype_bytes)}")(lam, h, seg_prod, c_in, T, W, tile_rows, stream))
+
+
+def segment_fixup_backward(lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T, W, tile_rows, dtype_bytes=4,
+                           stream=0):
+    check(getattr(lib, f"linrec_segment_fixup_backward_{_sfx(dtype_bytes)}")(
+        lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T, W, tile_rows, stream))
 
 
 class Workspace:

@@ -414,6 +414,77 @@ int scan_backward_host(const S* lam, const S* h0, const S* h, const S* dh, S* dl
   return LINREC_OK;
 }
 
+// ---------------------------------------------------------------------------
+// sequence sharding (segment.cu): deterministic plan per (T, W, dtype, dir)
+// ---------------------------------------------------------------------------
+template <class S>
+ChainPlan plan_segment(bool forward, int64_t T, int64_t W) {
+  ChainPlan p;
+  const bool v = W % vec_of<S>() == 0;
+  if (!(v && tma_allowed(T, W) && linrec_impl::plan_tma<S>(forward, T, W, &p)))
+    p = linrec_impl::plan_chain<S>(forward, T, W, v);
+  return p;
+}
+
+template <class S>
+int segment_scan(const S* lam, const S* x, const S* h0, S* h, S* seg_prod, S* agg, int64_t T, int64_t W,
+                 linrec_workspace_t ws, cudaStream_t st) {
+  int rc;
+  if ((rc = check_dims(T, W)) || (rc = check_ptr(lam, "decays")) || (rc = check_ptr(x, "impulses")) ||
+      (rc = check_ptr(h, "h")) || (rc = check_ptr(seg_prod, "seg_prod")) || (rc = check_ptr(agg, "agg")))
+    return rc;
+  const ChainPlan p = plan_segment<S>(true, T, W);
+  if (p.vec > 1 && !vec_ok<S>(W, {lam, x, h0, h, seg_prod, agg}))
+    return fail(LINREC_ERR_VALUE, "segment scans need 16-byte aligned buffers");
+  int dev;
+  if ((rc = current_device(&dev))) return rc;
+  linrec_workspace* w = ws ? ws : default_ws(dev, st);
+  std::lock_guard<std::mutex> lk(w->mu);
+  if ((rc = ws_reserve(w, p.ws_bytes, st))) return rc;
+  FwdCall<S> c{lam, x, h0, h, T, W, seg_prod, agg};
+  if (p.kind == 1) LINREC_CUDA_TRY(linrec_impl::launch_tma_fwd<S>(p, c, ws_ptrs(w, p), st));
+  else LINREC_CUDA_TRY(linrec_impl::launch_chain_fwd<S>(p, c, ws_ptrs(w, p), st));
+  return LINREC_OK;
+}
+
+template <class S>
+int segment_scan_backward(const S* lam, const S* hprev, const S* h, const S* dh, const S* lam_next, S* dlam,
+                          S* dx, S* dh0, S* seg_prod, S* agg, int64_t T, int64_t W, linrec_workspace_t ws,
+                          cudaStream_t st) {
+  int rc;
+  if ((rc = check_dims(T, W)) || (rc = check_ptr(lam, "decays")) || (rc = check_ptr(h, "h")) ||
+      (rc = check_ptr(dh, "d_h")) || (rc = check_ptr(dlam, "d_decays")) || (rc = check_ptr(dx, "d_impulses")) ||
+      (rc = check_ptr(dh0, "d_initial")) || (rc = check_ptr(seg_prod, "seg_prod")) || (rc = check_ptr(agg, "agg")))
+    return rc;
+  const ChainPlan p = plan_segment<S>(false, T, W);
+  if (p.vec > 1 && !vec_ok<S>(W, {lam, hprev, h, dh, lam_next, dlam, dx, dh0, seg_prod, agg}))
+    return fail(LINREC_ERR_VALUE, "segment scans need 16-byte aligned buffers");
+  int dev;
+  if ((rc = current_device(&dev))) return rc;
+  linrec_workspace* w = ws ? ws : default_ws(dev, st);
+  std::lock_guard<std::mutex> lk(w->mu);
+  if ((rc = ws_reserve(w, p.ws_bytes, st))) return rc;
+  BwdCall<S> c{lam, hprev, h, dh, lam_next, nullptr, dlam, dx, dh0, T, W, seg_prod, agg};
+  if (p.kind == 1) LINREC_CUDA_TRY(linrec_impl::launch_tma_bwd<S>(p, c, ws_ptrs(w, p), st));
+  else LINREC_CUDA_TRY(linrec_impl::launch_chain_bwd<S>(p, c, ws_ptrs(w, p), st));
+  return LINREC_OK;
+}
+
+template <class S>
+int segment_fixup(bool reverse, const S* lam, const S* hprev, const S* h, const S* lam_next, const S* seg_prod,
+                  const S* carry, S* out0, S* out1, int64_t T, int64_t W, int64_t rows, cudaStream_t st) {
+  int rc;
+  if ((rc = check_dims(T, W)) || (rc = check_ptr(lam, "decays")) || (rc = check_ptr(seg_prod, "seg_prod")) ||
+      (rc = check_ptr(carry, "carry")) || (rc = check_ptr(out0, "out")))
+    return rc;
+  if (reverse && ((rc = check_ptr(h, "h")) || (rc = check_ptr(out1, "d_decays")))) return rc;
+  if (rows < 1) return fail(LINREC_ERR_VALUE, "tile_rows must be >= 1");
+  const bool v = vec_ok<S>(W, {lam, hprev, h, lam_next, seg_prod, carry, out0, out1});
+  LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(reverse, lam, hprev, h, lam_next, seg_prod, carry, out0, out1,
+                                               T, W, rows, v, st));
+  return LINREC_OK;
+}
+
 template <class S>
 int first_nonfinite(const S* v, int64_t n, int64_t* index, cudaStream_t st) {
   int rc;
@@ -561,6 +632,95 @@ int linrec_first_nonfinite_f32(const float* v, int64_t n, int64_t* index, void* 
 }
 int linrec_first_nonfinite_f64(const double* v, int64_t n, int64_t* index, void* stream) {
   return first_nonfinite<double>(v, n, index, static_cast<cudaStream_t>(stream));
+}
+
+int64_t linrec_segment_tile_rows(int64_t T, int64_t W, int dtype_bytes, int backward) {
+  if (T < 1 || W < 1) return 0;
+  return dtype_bytes == 8 ? plan_segment<double>(!backward, T, W).rows : plan_segment<float>(!backward, T, W).rows;
+}
+
+int linrec_segment_scan_f32(const float* lam, const float* x, const float* h0, float* h, float* seg_prod,
+                            float* agg, int64_t T, int64_t W, linrec_workspace_t ws, void* stream) {
+  return segment_scan<float>(lam, x, h0, h, seg_prod, agg, T, W, ws, static_cast<cudaStream_t>(stream));
+}
+int linrec_segment_scan_f64(const double* lam, const double* x, const double* h0, double* h, double* seg_prod,
+                            double* agg, int64_t T, int64_t W, linrec_workspace_t ws, void* stream) {
+  return segment_scan<double>(lam, x, h0, h, seg_prod, agg, T, W, ws, static_cast<cudaStream_t>(stream));
+}
+int linrec_segment_scan_backward_f32(const float* lam, const float* hprev, const float* h, const float* dh,
+                                     const float* lam_next, float* dlam, float* dx, float* dh0,
+                                     float* seg_prod, float* agg, int64_t T, int64_t W, linrec_workspace_t ws,
+                                     void* stream) {
+  return segment_scan_backward<float>(lam, hprev, h, dh, lam_next, dlam, dx, dh0, seg_prod, agg, T, W, ws,
+                                      static_cast<cudaStream_t>(stream));
+}
+int linrec_segment_scan_backward_f64(const double* lam, const double* hprev, const double* h, const double* dh,
+                                     const double* lam_next, double* dlam, double* dx, double* dh0,
+                                     double* seg_prod, double* agg, int64_t T, int64_t W,
+                                     linrec_workspace_t ws, void* stream) {
+  return segment_scan_backward<double>(lam, hprev, h, dh, lam_next, dlam, dx, dh0, seg_prod, agg, T, W, ws,
+                                       static_cast<cudaStream_t>(stream));
+}
+int linrec_segment_fixup_f32(const float* lam, float* h, const float* seg_prod, const float* c_in, int64_t T,
+                             int64_t W, int64_t tile_rows, void* stream) {
+  return segment_fixup<float>(false, lam, nullptr, nullptr, nullptr, seg_prod, c_in, h, nullptr, T, W, tile_rows,
+                              static_cast<cudaStream_t>(stream));
+}
+int linrec_segment_fixup_f64(const double* lam, double* h, const double* seg_prod, const double* c_in,
+                             int64_t T, int64_t W, int64_t tile_rows, void* stream) {
+  return segment_fixup<double>(false, lam, nullptr, nullptr, nullptr, seg_prod, c_in, h, nullptr, T, W, tile_rows,
+                               static_cast<cudaStream_t>(stream));
+}
+int linrec_segment_fixup_backward_f32(const float* lam, const float* hprev, const float* h, const float* lam_next,
+                                      const float* seg_prod, const float* y_in, float* dlam, float* dx, int64_t T,
+                                      int64_t W, int64_t tile_rows, void* stream) {
+  return segment_fixup<float>(true, lam, hprev, h, lam_next, seg_prod, y_in, dx, dlam, T, W, tile_rows,
+                              static_cast<cudaStream_t>(stream));
+}
+int linrec_segment_fixup_backward_f64(const double* lam, const double* hprev, const double* h,
+                                      const double* lam_next, const double* seg_prod, const double* y_in,
+                                      double* dlam, double* dx, int64_t T, int64_t W, int64_t tile_rows,
+                                      void* stream) {
+  return segment_fixup<double>(true, lam, hprev, h, lam_next, seg_prod, y_in, dx, dlam, T, W, tile_rows,
+                               static_cast<cudaStream_t>(stream));
+}
+int linrec_compose_carries_f32(const float* aggs, int64_t first, int64_t last, int64_t step, const float* seed,
+                               float* out, int64_t W, void* stream) {
+  int rc;
+  if ((rc = check_ptr(aggs, "aggs")) || (rc = check_ptr(out, "out"))) return rc;
+  if (step != 1 && step != -1) return fail(LINREC_ERR_VALUE, "step must be +1 or -1");
+  LINREC_CUDA_TRY(linrec_impl::launch_compose<float>(aggs, first, last, step, seed, out, W,
+                                                     static_cast<cudaStream_t>(stream)));
+  return LINREC_OK;
+}
+int linrec_compose_carries_f64(const double* aggs, int64_t first, int64_t last, int64_t step, const double* seed,
+                               double* out, int64_t W, void* stream) {
+  int rc;
+  if ((rc = check_ptr(aggs, "aggs")) || (rc = check_ptr(out, "out"))) return rc;
+  if (step != 1 && step != -1) return fail(LINREC_ERR_VALUE, "step must be +1 or -1");
+  LINREC_CUDA_TRY(linrec_impl::launch_compose<double>(aggs, first, last, step, seed, out, W,
+                                                      static_cast<cudaStream_t>(stream)));
+  return LINREC_OK;
+}
+int linrec_backward_aggregate_f32(const float* lam, const float* agg_loc, const float* dh0_loc, float* agg_out,
+                                  int64_t W, void* stream) {
+  int rc;
+  if ((rc = check_ptr(lam, "decays")) || (rc = check_ptr(agg_loc, "agg_loc")) ||
+      (rc = check_ptr(dh0_loc, "dh0_loc")) || (rc = check_ptr(agg_out, "agg_out")))
+    return rc;
+  LINREC_CUDA_TRY(linrec_impl::launch_bwd_aggregate<float>(lam, agg_loc, dh0_loc, agg_out, W,
+                                                           static_cast<cudaStream_t>(stream)));
+  return LINREC_OK;
+}
+int linrec_backward_aggregate_f64(const double* lam, const double* agg_loc, const double* dh0_loc,
+                                  double* agg_out, int64_t W, void* stream) {
+  int rc;
+  if ((rc = check_ptr(lam, "decays")) || (rc = check_ptr(agg_loc, "agg_loc")) ||
+      (rc = check_ptr(dh0_loc, "dh0_loc")) || (rc = check_ptr(agg_out, "agg_out")))
+    return rc;
+  LINREC_CUDA_TRY(linrec_impl::launch_bwd_aggregate<double>(lam, agg_loc, dh0_loc, agg_out, W,
+                                                            static_cast<cudaStream_t>(stream)));
+  return LINREC_OK;
 }
 
 }  // extern "C"

@@ -18,6 +18,8 @@ cudaError_t launch_chain_bwd<float>(const ChainPlan& p, const BwdCall<float>& c,
   a.out0 = c.dx;
   a.out1 = c.dlam;
   a.out2 = c.dh0;
+  a.seg_prod = c.seg_prod;
+  a.agg_out = c.agg_out;
   a.T = c.T;
   a.W = c.W;
   a.ncols = p.ncols;

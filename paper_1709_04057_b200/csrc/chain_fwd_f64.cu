@@ -13,6 +13,8 @@ cudaError_t launch_chain_fwd<double>(const ChainPlan& p, const FwdCall<double>& 
   a.b = c.x;
   a.seed = c.h0;
   a.out0 = c.h;
+  a.seg_prod = c.seg_prod;
+  a.agg_out = c.agg_out;
   a.T = c.T;
   a.W = c.W;
   a.ncols = p.ncols;

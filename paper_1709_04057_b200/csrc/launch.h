@@ -46,6 +46,8 @@ struct FwdCall {
   const S* h0;
   S* h;
   int64_t T, W;
+  S* seg_prod = nullptr;  // sequence sharding outputs (see segment.cu)
+  S* agg_out = nullptr;
 };
 
 template <class S>
@@ -60,6 +62,8 @@ struct BwdCall {
   S* dx;
   S* dh0;
   int64_t T, W;
+  S* seg_prod = nullptr;
+  S* agg_out = nullptr;
 };
 
 template <class S>
@@ -83,6 +87,18 @@ template <class S>
 cudaError_t launch_tma_bwd(const ChainPlan& p, const BwdCall<S>& c, const ChainPtrs& ws, cudaStream_t st);
 
 cudaError_t launch_ws_init(void* ctrl, cudaStream_t st);
+
+// segment.cu
+template <class S>
+cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S* h, const S* lam_next,
+                         const S* seg_prod, const S* carry, S* out0, S* out1, int64_t T, int64_t W,
+                         int64_t rows, bool vec_ok, cudaStream_t st);
+template <class S>
+cudaError_t launch_compose(const S* aggs, int64_t first, int64_t last, int64_t step, const S* seed, S* out,
+                           int64_t W, cudaStream_t st);
+template <class S>
+cudaError_t launch_bwd_aggregate(const S* lam, const S* agg_loc, const S* dh0_loc, S* out, int64_t W,
+                                 cudaStream_t st);
 
 template <class S>
 cudaError_t first_nonfinite(const S* v, int64_t n, int64_t* index, cudaStream_t st);

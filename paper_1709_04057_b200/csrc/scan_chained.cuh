@@ -75,6 +75,10 @@ struct ChainArgs {
   S* out0;
   S* out1;
   S* out2;
+  // segment outputs (sequence sharding): exclusive decay product of every
+  // chain position [ntt][W] and the chain's final (P_incl, c_incl) [2][W]
+  S* seg_prod;
+  S* agg_out;
   int64_t T;
   int64_t W;
   int64_t ncols;
@@ -150,18 +154,19 @@ __device__ __forceinline__ bool load_words(const uint64_t* p, float (&v)[VEC], u
   return ok;
 }
 
-template <class S, int VEC, int Q, int REC, bool WANT_P>
+template <class S, int VEC, int Q, int REC>
 struct Lookback;
 
 // fp32: self-validating words.
-template <int VEC, int Q, int REC, bool WANT_P>
-struct Lookback<float, VEC, Q, REC, WANT_P> {
+template <int VEC, int Q, int REC>
+struct Lookback<float, VEC, Q, REC> {
   // agg record k: words [k*2*REC, +CPW) = A, [k*2*REC + REC, +CPW) = B
   // inc record k: words [k*2*REC, +CPW) = c, [k*2*REC + REC, +CPW) = P
   static __device__ __forceinline__ void exclusive(const ChainWs& ws, uint32_t epoch, int64_t k,
                                                    int64_t pos, int64_t col, int64_t ncols,
                                                    const float (&TA)[VEC], const float (&TB)[VEC],
-                                                   float (&c)[VEC], float (&P)[VEC], bool valid) {
+                                                   float (&c)[VEC], float (&P)[VEC], bool valid,
+                                                   bool WANT_P) {
     const int lane = threadIdx.x & 31;
     if (pos == 0 || !(lane < Q && valid)) return;
     uint64_t* agg = reinterpret_cast<uint64_t*>(ws.agg);
@@ -207,14 +212,14 @@ struct Lookback<float, VEC, Q, REC, WANT_P> {
   static __device__ __forceinline__ void publish(const ChainWs& ws, uint32_t epoch, int64_t k,
                                                  const float (&TA)[VEC], const float (&TB)[VEC],
                                                  const float (&c)[VEC], const float (&P)[VEC],
-                                                 bool valid) {
-    publish_words(ws, epoch, k, TA, TB, c, P, valid);
+                                                 bool valid, bool WANT_P) {
+    publish_words(ws, epoch, k, TA, TB, c, P, valid, WANT_P);
   }
 
   static __device__ __forceinline__ void publish_words(const ChainWs& ws, uint32_t epoch, int64_t k,
                                                        const float (&TA)[VEC], const float (&TB)[VEC],
                                                        const float (&c)[VEC], const float (&P)[VEC],
-                                                       bool valid) {
+                                                       bool valid, bool WANT_P) {
     const int lane = threadIdx.x & 31;
     if (!(lane < Q && valid)) return;
     uint64_t* inc = reinterpret_cast<uint64_t*>(ws.inc);
@@ -233,14 +238,15 @@ struct Lookback<float, VEC, Q, REC, WANT_P> {
 };
 
 // fp64: value records + per-tile release/acquire flag.
-template <int VEC, int Q, int REC, bool WANT_P>
-struct Lookback<double, VEC, Q, REC, WANT_P> {
+template <int VEC, int Q, int REC>
+struct Lookback<double, VEC, Q, REC> {
   using S = double;
   using IO = VecIO<S, VEC>;
   static __device__ __forceinline__ void exclusive(const ChainWs& ws, uint32_t epoch, int64_t k,
                                                    int64_t pos, int64_t col, int64_t ncols,
                                                    const S (&TA)[VEC], const S (&TB)[VEC],
-                                                   S (&c)[VEC], S (&P)[VEC], bool valid) {
+                                                   S (&c)[VEC], S (&P)[VEC], bool valid,
+                                                   bool /*want_p: fp64 records always carry P*/) {
     if (pos == 0) return;
     const int lane = threadIdx.x & 31;
     S* agg = reinterpret_cast<S*>(ws.agg);
@@ -297,7 +303,8 @@ struct Lookback<double, VEC, Q, REC, WANT_P> {
 
   static __device__ __forceinline__ void publish(const ChainWs& ws, uint32_t epoch, int64_t k,
                                                  const S (&TA)[VEC], const S (&TB)[VEC],
-                                                 const S (&c)[VEC], const S (&P)[VEC], bool valid) {
+                                                 const S (&c)[VEC], const S (&P)[VEC], bool valid,
+                                                 bool /*want_p*/) {
     const int lane = threadIdx.x & 31;
     S* inc = reinterpret_cast<S*>(ws.inc);
     if (lane < Q && valid) {
@@ -316,6 +323,29 @@ struct Lookback<double, VEC, Q, REC, WANT_P> {
     if (lane == 0) st_release_gpu(&ws.flags[k], (epoch << 2) | kFlagInc);
   }
 };
+
+// Segment outputs of the coordinator (no-ops unless the launch asked for them):
+// the tile's exclusive decay product per channel, and for the last tile of a
+// chain the chain's inclusive (P, c).
+template <class S, int VEC, int Q>
+__device__ __forceinline__ void write_segment_outputs(const ChainArgs<S>& a, int64_t pos, int64_t ch,
+                                                      bool valid, const S (&TA)[VEC],
+                                                      const S (&TB)[VEC], const S (&c)[VEC],
+                                                      const S (&P)[VEC]) {
+  const int lane = threadIdx.x & 31;
+  if (!(lane < Q && valid)) return;
+  if (a.seg_prod != nullptr) {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) a.seg_prod[pos * a.W + ch + v] = P[v];
+  }
+  if (a.agg_out != nullptr && pos == a.ntt - 1) {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      a.agg_out[ch + v] = mul_(TA[v], P[v]);
+      a.agg_out[a.W + ch + v] = fma_(TA[v], c[v], TB[v]);
+    }
+  }
+}
 
 // Named barriers between the NW data warps and the coordinator warp.
 __device__ __forceinline__ void bar_arrive(int id, int n) {
@@ -391,13 +421,15 @@ __device__ __forceinline__ void chain_coordinator(const ChainArgs<S>& a, const C
       for (int v = 0; v < VEC; ++v) c[v] = a.seed[ch + v];
     }
   }
-  Lookback<S, VEC, Q, REC, false>::exclusive(ws, epoch, k, pos, col, a.ncols, TA, TB, c, P, valid);
+  const bool want_p = a.seg_prod != nullptr || a.agg_out != nullptr;
+  Lookback<S, VEC, Q, REC>::exclusive(ws, epoch, k, pos, col, a.ncols, TA, TB, c, P, valid, want_p);
   if (lane < Q) {
 #pragma unroll
     for (int v = 0; v < VEC; ++v) s_c[lane * VEC + v] = c[v];
   }
   bar_arrive(2, NT);  // carry is in shared memory: the data warps re-scan now
-  Lookback<S, VEC, Q, REC, false>::publish(ws, epoch, k, TA, TB, c, P, valid);
+  Lookback<S, VEC, Q, REC>::publish(ws, epoch, k, TA, TB, c, P, valid, want_p);
+  write_segment_outputs<S, VEC, Q>(a, pos, ch, valid, TA, TB, c, P);
   chain_retire(ws, epoch);
 }
 

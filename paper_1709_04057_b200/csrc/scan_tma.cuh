@@ -142,13 +142,15 @@ __device__ __forceinline__ void tma_coordinator(const SM& sm, const ChainArgs<S>
         for (int v = 0; v < VEC; ++v) c[v] = a.seed[ch + v];
       }
     }
-    Lookback<S, VEC, Q, Cfg::REC, false>::exclusive(ws, epoch, k, pos, col, a.ncols, TA, TB, c, P, valid);
+    const bool want_p = a.seg_prod != nullptr || a.agg_out != nullptr;
+    Lookback<S, VEC, Q, Cfg::REC>::exclusive(ws, epoch, k, pos, col, a.ncols, TA, TB, c, P, valid, want_p);
     if (lane < Q) {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) sm.carry(slot)[lane * VEC + v] = c[v];
     }
     mbar_arrive(sm.carry_bar(slot));  // consumers re-scan while the carry is published
-    Lookback<S, VEC, Q, Cfg::REC, false>::publish(ws, epoch, k, TA, TB, c, P, valid);
+    Lookback<S, VEC, Q, Cfg::REC>::publish(ws, epoch, k, TA, TB, c, P, valid, want_p);
+    write_segment_outputs<S, VEC, Q>(a, pos, ch, valid, TA, TB, c, P);
   }
   chain_retire(ws, epoch);
 }

@@ -1,0 +1,237 @@
+// Sequence sharding support (BASELINE.json north_star: "each GPU reduces its
+// segment to a per-channel (A,B) carry, the GPUs exchange that tiny carry with
+// an NCCL all-gather over NVLink, and each GPU runs a local fix-up").
+//
+// A segment [S, E) of the sequence is first scanned with a zero carry by the
+// ordinary chained kernels, which additionally emit (chain_impl/tma launch
+// with ChainArgs::seg_prod / agg_out)
+//   seg_prod[p][ch]  exclusive decay product entering chain position p,
+//   agg[2][ch]       the segment aggregate (prod lam, zero-seeded result).
+// After the aggregates are exchanged and folded (k_compose) into the carry
+// c_in entering the segment, the true result differs from the zero-carry one
+// by P_t * c_in (forward) -- P_t the decay product from the segment start --
+// which these kernels add.  Each tile reads its entering product first and
+// exits at once when P * c_in is exactly zero for all of its channels: once
+// the running product underflows the correction is exactly zero, so only the
+// leading tiles of a segment are touched for decays < 1 (the bench
+// distribution: ~100 rows), while decays near 1 degrade to one extra pass.
+#include <cstdint>
+
+#include "chain_impl.cuh"
+
+namespace linrec_dev {
+
+// One CTA per (chain position, channel column); 8 warps; Q lanes across
+// channels x G groups along time, RF rows per thread per pass; a tile of
+// `rows` rows is covered in ceil(rows / (8*G*RF)) passes.
+template <class S, int VEC, int Q, bool REV>
+__global__ void __launch_bounds__(256)
+k_fixup(const S* __restrict__ lam, const S* __restrict__ hprev_row, const S* __restrict__ h,
+        const S* __restrict__ lam_next, const S* __restrict__ seg_prod, const S* __restrict__ carry,
+        S* __restrict__ out0 /* fwd: h; bwd: dx */, S* __restrict__ out1 /* bwd: dlam */, int64_t T,
+        int64_t W, int64_t rows, int64_t ncols, int64_t ntt) {
+  constexpr int NW = 8, RF = 4, G = 32 / Q, CPW = Q * VEC, NSEG = NW * G, PR = NSEG * RF;
+  using IO = VecIO<S, VEC>;
+  __shared__ S s_wp[NW][CPW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane % Q, g = lane / Q;
+  const int64_t col = blockIdx.x % ncols, pos = blockIdx.x / ncols;
+  const int64_t tile = REV ? ntt - 1 - pos : pos;
+  const int64_t ch = col * CPW + (int64_t)q * VEC;
+  const bool valid = ch < W;
+  // carry entering the tile: exclusive product * segment carry
+  S e[VEC];
+  bool nz = false;
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    e[v] = valid ? mul_(seg_prod[pos * W + ch + v], carry[ch + v]) : S(0);
+    nz = nz || e[v] != S(0);
+  }
+  if (!__syncthreads_or(nz)) return;
+
+  const int64_t t_lo = tile * rows, t_hi = (t_lo + rows < T ? t_lo + rows : T);
+  const int64_t npass = (rows + PR - 1) / PR;
+  for (int64_t ps = 0; ps < npass; ++ps) {
+    // rows of this pass, in processing order
+    const int64_t pbase = REV ? t_hi - (ps + 1) * PR : t_lo + ps * PR;
+    const int seg = warp * G + g;
+    S m[RF][VEC];
+#pragma unroll
+    for (int i = 0; i < RF; ++i) {
+      // processing index within the pass: REV walks rows downward
+      const int64_t t = REV ? pbase + (PR - 1 - (seg * RF + i)) : pbase + seg * RF + i;
+      const bool in = valid && t >= t_lo && t < t_hi;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) m[i][v] = S(1);
+      if (in) {
+        if (!REV) {
+          IO::load_cg(lam + t * W + ch, m[i]);
+        } else if (t + 1 < T) {
+          IO::load_cg(lam + (t + 1) * W + ch, m[i]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) m[i][v] = lam_next != nullptr ? lam_next[ch + v] : S(0);
+        }
+      }
+    }
+    // segment product, inclusive scan across the warp's groups, then warps
+    S A[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) A[v] = m[0][v];
+#pragma unroll
+    for (int i = 1; i < RF; ++i)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) A[v] = mul_(m[i][v], A[v]);
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const S ap = __shfl_up_sync(0xffffffffu, A[v], off * Q);
+        if (g >= off) A[v] = mul_(A[v], ap);
+      }
+    S Ae[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      Ae[v] = S(1);
+      if (G > 1) {
+        const S ap = __shfl_up_sync(0xffffffffu, A[v], Q);
+        if (g > 0) Ae[v] = ap;
+      }
+    }
+    __syncthreads();
+    if (g == G - 1) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) s_wp[warp][q * VEC + v] = A[v];
+    }
+    __syncthreads();
+    S ecur[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) ecur[v] = e[v];
+    for (int w = 0; w < warp; ++w)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) ecur[v] = mul_(s_wp[w][q * VEC + v], ecur[v]);
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) ecur[v] = mul_(Ae[v], ecur[v]);
+    // apply
+#pragma unroll
+    for (int i = 0; i < RF; ++i) {
+      const int64_t t = REV ? pbase + (PR - 1 - (seg * RF + i)) : pbase + seg * RF + i;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) ecur[v] = mul_(m[i][v], ecur[v]);
+      if (valid && t >= t_lo && t < t_hi) {
+        S o[VEC];
+        IO::load_cg(out0 + t * W + ch, o);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) o[v] = o[v] + ecur[v];
+        IO::store_cg(out0 + t * W + ch, o);
+        if (REV) {
+          S hp[VEC], d[VEC];
+          if (t >= 1) IO::load_cg(h + (t - 1) * W + ch, hp);
+          else {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) hp[v] = hprev_row != nullptr ? hprev_row[ch + v] : S(0);
+          }
+          IO::load_cg(out1 + t * W + ch, d);
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) d[v] = fma_(hp[v], ecur[v], d[v]);
+          IO::store_cg(out1 + t * W + ch, d);
+        }
+      }
+    }
+    // carry into the next pass = e * product of this whole pass
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      S tot = S(1);
+      for (int w = 0; w < NW; ++w) tot = mul_(s_wp[w][q * VEC + v], tot);
+      e[v] = mul_(tot, e[v]);
+    }
+  }
+}
+
+// out[j] = fold over q in [first, last) by `step` of c = A_q[j] * c + B_q[j],
+// c starting at seed[j] (0 if seed == nullptr).  aggs: [n][2][W].
+template <class S>
+__global__ void k_compose(const S* __restrict__ aggs, int64_t first, int64_t last, int64_t step,
+                          const S* __restrict__ seed, S* __restrict__ out, int64_t W) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < W;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    S c = seed != nullptr ? seed[j] : S(0);
+    for (int64_t q = first; q != last; q += step) c = fma_(aggs[q * 2 * W + j], c, aggs[q * 2 * W + W + j]);
+    out[j] = c;
+  }
+}
+
+// Backward segment aggregate for the exchange: A' = lam_0 * P'_segment,
+// B' = lam_0 * G_loc_0 (= the zero-carry scan's dh0).
+template <class S>
+__global__ void k_bwd_aggregate(const S* __restrict__ lam, const S* __restrict__ agg_loc,
+                                const S* __restrict__ dh0_loc, S* __restrict__ out, int64_t W) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < W;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    out[j] = mul_(lam[j], agg_loc[j]);
+    out[W + j] = dh0_loc[j];
+  }
+}
+
+}  // namespace linrec_dev
+
+namespace linrec_impl {
+
+template <class S>
+cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S* h, const S* lam_next,
+                         const S* seg_prod, const S* carry, S* out0, S* out1, int64_t T, int64_t W,
+                         int64_t rows, bool vec_ok, cudaStream_t st) {
+  constexpr int V = Tuning<S>::VEC;
+  const int64_t nvec = vec_ok ? (W + V - 1) / V : W;
+  const int q = pick_q(nvec);
+  const int cpw = q * (vec_ok ? V : 1);
+  const int64_t ncols = (W + cpw - 1) / cpw, ntt = (T + rows - 1) / rows;
+  const dim3 grid((unsigned)(ncols * ntt));
+#define FIX(VV)                                                                                   \
+  LINREC_Q_SWITCH(q, if (reverse) linrec_dev::k_fixup<S, VV, Q_, true><<<grid, 256, 0, st>>>(     \
+                         lam, hprev_row, h, lam_next, seg_prod, carry, out0, out1, T, W, rows, ncols, ntt); \
+                     else linrec_dev::k_fixup<S, VV, Q_, false><<<grid, 256, 0, st>>>(            \
+                         lam, hprev_row, h, lam_next, seg_prod, carry, out0, out1, T, W, rows, ncols, ntt));
+  if (vec_ok) {
+    FIX(V)
+  } else {
+    FIX(1)
+  }
+#undef FIX
+  return cudaGetLastError();
+}
+
+template <class S>
+cudaError_t launch_compose(const S* aggs, int64_t first, int64_t last, int64_t step, const S* seed, S* out,
+                           int64_t W, cudaStream_t st) {
+  const int64_t blocks = (W + 255) / 256;
+  linrec_dev::k_compose<S><<<(unsigned)(blocks < 1024 ? blocks : 1024), 256, 0, st>>>(aggs, first, last, step,
+                                                                                      seed, out, W);
+  return cudaGetLastError();
+}
+
+template <class S>
+cudaError_t launch_bwd_aggregate(const S* lam, const S* agg_loc, const S* dh0_loc, S* out, int64_t W,
+                                 cudaStream_t st) {
+  const int64_t blocks = (W + 255) / 256;
+  linrec_dev::k_bwd_aggregate<S><<<(unsigned)(blocks < 1024 ? blocks : 1024), 256, 0, st>>>(lam, agg_loc,
+                                                                                            dh0_loc, out, W);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_fixup<float>(bool, const float*, const float*, const float*, const float*,
+                                         const float*, const float*, float*, float*, int64_t, int64_t,
+                                         int64_t, bool, cudaStream_t);
+template cudaError_t launch_fixup<double>(bool, const double*, const double*, const double*, const double*,
+                                          const double*, const double*, double*, double*, int64_t, int64_t,
+                                          int64_t, bool, cudaStream_t);
+template cudaError_t launch_compose<float>(const float*, int64_t, int64_t, int64_t, const float*, float*,
+                                           int64_t, cudaStream_t);
+template cudaError_t launch_compose<double>(const double*, int64_t, int64_t, int64_t, const double*, double*,
+                                            int64_t, cudaStream_t);
+template cudaError_t launch_bwd_aggregate<float>(const float*, const float*, const float*, float*, int64_t,
+                                                 cudaStream_t);
+template cudaError_t launch_bwd_aggregate<double>(const double*, const double*, const double*, double*,
+                                                  int64_t, cudaStream_t);
+
+}  // namespace linrec_impl

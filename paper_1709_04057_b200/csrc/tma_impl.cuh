@@ -107,6 +107,8 @@ linrec_dev::ChainArgs<S> fwd_args(const ChainPlan& p, const FwdCall<S>& c) {
   a.b = c.x;
   a.seed = c.h0;
   a.out0 = c.h;
+  a.seg_prod = c.seg_prod;
+  a.agg_out = c.agg_out;
   a.T = c.T;
   a.W = c.W;
   a.ncols = p.ncols;
@@ -126,6 +128,8 @@ linrec_dev::ChainArgs<S> bwd_args(const ChainPlan& p, const BwdCall<S>& c) {
   a.out0 = c.dx;
   a.out1 = c.dlam;
   a.out2 = c.dh0;
+  a.seg_prod = c.seg_prod;
+  a.agg_out = c.agg_out;
   a.T = c.T;
   a.W = c.W;
   a.ncols = p.ncols;

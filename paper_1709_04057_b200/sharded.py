@@ -1,0 +1,199 @@
+"""Multi-GPU sharding of the linear recurrence.
+
+* Channel sharding -- channels are independent (recurrence.hpp:109): every
+  rank owns a [T, W/N] block and calls the single-GPU scans; there is no
+  collective on the data path (`channel_shard`).
+* Sequence sharding -- T is split into contiguous segments, one per rank
+  (`segment_bounds`).  Per direction each rank runs ONE zero-carry chained scan
+  of its segment (12 / 20 B/element), the ranks exchange a 2*W-value carry
+  with one all-gather, and a fix-up kernel adds the carry's decaying
+  contribution to the leading tiles of the segment (include/linrec_cuda.h,
+  csrc/segment.cu).  The collective is the only inter-GPU traffic: 2*W*4
+  bytes per rank per direction (1 KiB at W = 128).
+
+The orchestration is written against a small backend interface so that the
+same code drives the CUDA kernels (``CudaBackend``, NCCL) and, in the CPU test
+suite, a reference backend over gloo.  The product backend is the CUDA one;
+this module has no CPU compute path.
+"""
+from __future__ import annotations
+
+import contextlib
+
+import torch
+import torch.distributed as dist
+
+from . import capi
+
+
+def segment_bounds(T: int, world: int, rank: int):
+    """Rows [start, end) of rank's segment: contiguous, sizes differing by at
+    most one, longer segments first (the reference's plan_chunks rule,
+    recurrence.hpp:61-80, applied to ranks)."""
+    base, rem = divmod(T, world)
+    start = rank * base + min(rank, rem)
+    return start, start + base + (1 if rank < rem else 0)
+
+
+def segment_rows(T: int, world: int, rank: int) -> int:
+    s, e = segment_bounds(T, world, rank)
+    return e - s
+
+
+def channel_shard(W: int, world: int, rank: int):
+    """Channels [start, end) owned by rank under channel sharding."""
+    return segment_bounds(W, world, rank)
+
+
+class CudaBackend:
+    """Primitive operations of the sharded scan on the sm_100a kernels."""
+
+    def __init__(self, ws=None, stream=None):
+        self.ws = ws
+        self.stream = stream
+
+    def _st(self):
+        s = self.stream if self.stream is not None else torch.cuda.current_stream()
+        return s.cuda_stream
+
+    @staticmethod
+    def _p(t):
+        return None if t is None else t.data_ptr()
+
+    def tile_rows(self, T, W, backward):
+        return capi.segment_tile_rows(T, W, backward)
+
+    def segment_scan(self, lam, x, h0, h, seg_prod, agg, T, W):
+        capi.segment_scan(lam.data_ptr(), x.data_ptr(), self._p(h0), h.data_ptr(), seg_prod.data_ptr(),
+                          agg.data_ptr(), T, W, 4, None if self.ws is None else self.ws.handle, self._st())
+
+    def segment_scan_backward(self, lam, hprev, h, dh, lam_next, dlam, dx, dh0, seg_prod, agg, T, W):
+        capi.segment_scan_backward(lam.data_ptr(), self._p(hprev), h.data_ptr(), dh.data_ptr(),
+                                   self._p(lam_next), dlam.data_ptr(), dx.data_ptr(), dh0.data_ptr(),
+                                   seg_prod.data_ptr(), agg.data_ptr(), T, W, 4,
+                                   None if self.ws is None else self.ws.handle, self._st())
+
+    def backward_aggregate(self, lam, agg_loc, dh0_loc, agg_out, W):
+        capi.backward_aggregate(lam.data_ptr(), agg_loc.data_ptr(), dh0_loc.data_ptr(), agg_out.data_ptr(), W,
+                                4, self._st())
+
+    def compose(self, aggs, first, last, step, seed, out, W):
+        capi.compose_carries(aggs.data_ptr(), first, last, step, self._p(seed), out.data_ptr(), W, 4, self._st())
+
+    def fixup(self, lam, h, seg_prod, c_in, T, W, rows):
+        capi.segment_fixup(lam.data_ptr(), h.data_ptr(), seg_prod.data_ptr(), c_in.data_ptr(), T, W, rows, 4,
+                           self._st())
+
+    def fixup_backward(self, lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T, W, rows):
+        capi.segment_fixup_backward(lam.data_ptr(), self._p(hprev), h.data_ptr(), self._p(lam_next),
+                                    seg_prod.data_ptr(), y_in.data_ptr(), dlam.data_ptr(), dx.data_ptr(), T, W,
+                                    rows, 4, self._st())
+
+
+class SequenceShardedScan:
+    """h = scan(lam, x, h0) and its gradients with T split across the ranks
+    of `group`; rank r holds rows segment_bounds(T, world, r) of every
+    [T, ...] tensor (fp32, C-contiguous, W = prod of the trailing dims).
+
+    forward(lam, x, h0, h)                      h0 used on rank 0 only
+    backward(lam, h0, h, dh, dlam, dx, dh0)     dh0 written on rank 0 only
+    """
+
+    def __init__(self, T, W, group=None, ws=None, stream=None, backend=None, device=None):
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.T, self.W = T, W
+        self.Tl = segment_rows(T, self.world, self.rank)
+        self.be = backend if backend is not None else CudaBackend(ws, stream)
+        self.stream = stream
+        dev = device if device is not None else (torch.device("cuda", torch.cuda.current_device())
+                                                 if backend is None else torch.device("cpu"))
+        f = dict(dtype=torch.float32, device=dev)
+        self.rows_f = self.be.tile_rows(self.Tl, W, False)
+        self.rows_b = self.be.tile_rows(self.Tl, W, True)
+        nf = -(-self.Tl // self.rows_f)
+        nb = -(-self.Tl // self.rows_b)
+        self.seg_prod_f = torch.empty(nf, W, **f)
+        self.seg_prod_b = torch.empty(nb, W, **f)
+        self.agg = torch.empty(2, W, **f)
+        self.aggs = torch.empty(self.world, 2, W, **f)
+        self.c_in = torch.zeros(W, **f)
+        self.y_in = torch.zeros(W, **f)
+        self.agg_loc = torch.empty(2, W, **f)
+        self.dh0_loc = torch.empty(W, **f)
+        self.ones = torch.ones(W, **f)
+        self.zeros = torch.zeros(W, **f)
+        self.hprev = None
+        # kernels launched per step on this rank (for bench.py's gpu_launches)
+        r, R = self.rank, self.world
+        self.launches_per_step = (1 + (2 if r > 0 else 0)) + (2 + (2 if r < R - 1 else 0) + (1 if r == 0 else 0))
+
+    def _on_stream(self):
+        if self.stream is not None and torch.cuda.is_available() and isinstance(self.stream, torch.cuda.Stream):
+            return torch.cuda.stream(self.stream)
+        return contextlib.nullcontext()
+
+    # -- collectives -----------------------------------------------------------
+    def _all_gather(self, local, out):
+        if hasattr(dist, "all_gather_into_tensor") and dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(out.view(-1), local.reshape(-1), group=self.group)
+        else:
+            parts = list(out.unbind(0))
+            dist.all_gather(parts, local, group=self.group)
+
+    # -- forward -------------------------------------------------------------------
+    def forward(self, lam, x, h0, h):
+        """Rank r scans its segment; c_in (the true h before the segment) is
+        kept for the backward (hprev)."""
+        with self._on_stream():
+            return self._forward(lam, x, h0, h)
+
+    def _forward(self, lam, x, h0, h):
+        r, W, T = self.rank, self.W, self.Tl
+        self.be.segment_scan(lam, x, h0 if r == 0 else None, h, self.seg_prod_f, self.agg, T, W)
+        if r == 0:
+            self.agg[0].zero_()  # h0 is already folded into rank 0's segment
+        self._all_gather(self.agg, self.aggs)
+        if r > 0:
+            self.be.compose(self.aggs, 0, r, 1, None, self.c_in, W)
+            self.be.fixup(lam, h, self.seg_prod_f, self.c_in, T, W, self.rows_f)
+            self.hprev = self.c_in
+        else:
+            self.hprev = h0 if h0 is not None else self.zeros
+        return h
+
+    # -- backward ------------------------------------------------------------------
+    def backward(self, lam, h0, h, dh, dlam, dx, dh0, hprev=None):
+        """Gradients of the sharded recurrence.  hprev (the true h row before
+        the segment) defaults to the one the last forward() computed; pass it
+        explicitly when calling backward alone."""
+        with self._on_stream():
+            return self._backward(lam, h0, h, dh, dlam, dx, dh0, hprev)
+
+    def _backward(self, lam, h0, h, dh, dlam, dx, dh0, hprev):
+        r, R, W, T = self.rank, self.world, self.W, self.Tl
+        if hprev is None:
+            hprev = self.hprev if self.hprev is not None else self._halo(h, h0)
+        lam_next = self.ones if r < R - 1 else None
+        self.be.segment_scan_backward(lam, hprev, h, dh, lam_next, dlam, dx, self.dh0_loc, self.seg_prod_b,
+                                      self.agg_loc, T, W)
+        self.be.backward_aggregate(lam, self.agg_loc, self.dh0_loc, self.agg, W)
+        self._all_gather(self.agg, self.aggs)
+        if r < R - 1:
+            self.be.compose(self.aggs, R - 1, r, -1, None, self.y_in, W)
+            self.be.fixup_backward(lam, hprev, h, lam_next, self.seg_prod_b, self.y_in, dlam, dx, T, W,
+                                   self.rows_b)
+        else:
+            self.y_in.zero_()
+        if r == 0 and dh0 is not None:
+            self.be.compose(self.aggs, 0, 1, 1, self.y_in, dh0.view(-1), W)
+        return dlam, dx, dh0
+
+    def _halo(self, h, h0):
+        """True h row before this segment: last row of the previous rank's h."""
+        rows = torch.empty(self.world, self.W, dtype=h.dtype, device=h.device)
+        self._all_gather(h[-1].reshape(self.W).contiguous(), rows)
+        if self.rank == 0:
+            return h0.reshape(self.W) if h0 is not None else self.zeros
+        return rows[self.rank - 1].clone()
