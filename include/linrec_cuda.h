@@ -181,24 +181,27 @@ int linrec_first_nonfinite_f64(const double* v, int64_t n, int64_t* index,
 /* ---- sequence sharding across GPUs (BASELINE.json north_star) ----------- *
  * A sequence split into contiguous T-segments, one per rank.  Forward, rank r
  * (segment [S, E)):
- *   1. linrec_segment_scan_*: chained scan of the segment seeded with h0 on
- *      rank 0 and with 0 elsewhere; besides h it writes seg_prod[p][W] (the
- *      decay product entering chain position p) and agg[2][W] = (prod lam over
- *      the segment, state at its last row);
+ *   1. linrec_segment_scan_*: single-pass scan of the segment seeded with h0
+ *      on rank 0 and with 0 elsewhere; besides h it writes seg_prod (the decay
+ *      product from the segment start entering each chain position) and
+ *      agg[2][W] = (prod lam over the segment, state at its last row);
  *   2. all-gather of agg over the ranks (NCCL, the caller's communicator);
  *   3. linrec_compose_carries_*: c_in = fold of the aggregates of ranks
- *      0..r-1 (c = A_q*c + B_q, starting from 0; rank 0 publishes A = 0);
- *   4. linrec_segment_fixup_*: h_t += P_t * c_in for the tiles whose entering
+ *      0..r-1 (c = A_q*c + B_q from 0; rank 0 publishes A = 0);
+ *   4. linrec_segment_fixup_*: h_t += P_t * c_in on the tiles whose entering
  *      product is nonzero (exact: past the underflow the correction is 0).
- * Backward mirrors it in reverse time with lam_next = a row of ones (the
- * decay linking the segment to the next rank is applied by the carry):
+ * Backward, reverse time, with lam_next = a row of ones on every rank but the
+ * last (the decay linking to the next rank is applied through the carry):
  *   1. linrec_segment_scan_backward_* (hprev = the true h row before the
- *      segment), 2. linrec_backward_aggregate_* -> (A', B') = (lam_S * prod
- *      mu, lam_S * G_S), 3. all-gather, 4. compose ranks R-1..r+1 into y_in,
- *   5. linrec_segment_fixup_backward_* adds P'_t*y_in to dx and
- *      h_{t-1}*P'_t*y_in to dlam; rank 0's dh0 = A'_0*y_in + B'_0 (compose).
- * seg_prod holds ceil(T / linrec_segment_tile_rows(...)) rows of W values.
- * All buffers 16-byte aligned when W is a multiple of 4 (fp32) / 2 (fp64). */
+ *      segment) writes dlam, dx, seg_prod, agg = (A', B') = (lam_S * prod mu,
+ *      lam_S * G_S) and dh0 = B'; 2. all-gather agg; 3. compose ranks
+ *      R-1 .. r+1 into y_in; 4. linrec_segment_fixup_backward_* adds
+ *      P'_t*y_in to dx and h_{t-1}*P'_t*y_in to dlam; rank 0's
+ *      dh0 = A'_0*y_in + B'_0 (compose with seed y_in).
+ * seg_prod holds linrec_segment_prod_rows(...) rows of W values; pass
+ * linrec_segment_tile_rows(...) to the fix-up.  Buffers 16-byte aligned when
+ * W is a multiple of 4 (fp32) / 2 (fp64). */
+int64_t linrec_segment_prod_rows(int64_t T, int64_t W, int dtype_bytes, int backward);
 int64_t linrec_segment_tile_rows(int64_t T, int64_t W, int dtype_bytes, int backward);
 int linrec_segment_scan_f32(const float* lam, const float* x, const float* h0, float* h, float* seg_prod,
                             float* agg, int64_t T, int64_t W, linrec_workspace_t ws, void* stream);
@@ -212,10 +215,6 @@ int linrec_segment_scan_backward_f64(const double* lam, const double* hprev, con
                                      const double* lam_next, double* dlam, double* dx, double* dh0,
                                      double* seg_prod, double* agg, int64_t T, int64_t W,
                                      linrec_workspace_t ws, void* stream);
-int linrec_backward_aggregate_f32(const float* lam, const float* agg_loc, const float* dh0_loc, float* agg_out,
-                                  int64_t W, void* stream);
-int linrec_backward_aggregate_f64(const double* lam, const double* agg_loc, const double* dh0_loc,
-                                  double* agg_out, int64_t W, void* stream);
 int linrec_compose_carries_f32(const float* aggs, int64_t first, int64_t last, int64_t step, const float* seed,
                                float* out, int64_t W, void* stream);
 int linrec_compose_carries_f64(const double* aggs, int64_t first, int64_t last, int64_t step, const double* seed,

@@ -61,10 +61,11 @@ def _load():
         getattr(lib, f"linrec_first_nonfinite_{s}").argtypes = [_vp, _i64, C.POINTER(_i64), _vp]
         getattr(lib, f"linrec_segment_scan_{s}").argtypes = [_vp] * 6 + [_i64, _i64, _vp, _vp]
         getattr(lib, f"linrec_segment_scan_backward_{s}").argtypes = [_vp] * 10 + [_i64, _i64, _vp, _vp]
-        getattr(lib, f"linrec_backward_aggregate_{s}").argtypes = [_vp] * 4 + [_i64, _vp]
         getattr(lib, f"linrec_compose_carries_{s}").argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp]
         getattr(lib, f"linrec_segment_fixup_{s}").argtypes = [_vp] * 4 + [_i64, _i64, _i64, _vp]
         getattr(lib, f"linrec_segment_fixup_backward_{s}").argtypes = [_vp] * 8 + [_i64, _i64, _i64, _vp]
+    lib.linrec_segment_prod_rows.restype = _i64
+    lib.linrec_segment_prod_rows.argtypes = [_i64, _i64, _int, _int]
     lib.linrec_segment_tile_rows.restype = _i64
     lib.linrec_segment_tile_rows.argtypes = [_i64, _i64, _int, _int]
     return lib
@@ -132,6 +133,10 @@ def first_nonfinite(v, n, dtype_bytes=4, stream=0) -> int:
 
 
 # ---- sequence sharding (see include/linrec_cuda.h) ---------------------------
+def segment_prod_rows(T, W, backward=False, dtype_bytes=4) -> int:
+    return int(lib.linrec_segment_prod_rows(T, W, dtype_bytes, 1 if backward else 0))
+
+
 def segment_tile_rows(T, W, backward=False, dtype_bytes=4) -> int:
     return int(lib.linrec_segment_tile_rows(T, W, dtype_bytes, 1 if backward else 0))
 
@@ -144,10 +149,6 @@ def segment_scan_backward(lam, hprev, h, dh, lam_next, dlam, dx, dh0, seg_prod, 
                           ws=None, stream=0):
     check(getattr(lib, f"linrec_segment_scan_backward_{_sfx(dtype_bytes)}")(
         lam, hprev, h, dh, lam_next, dlam, dx, dh0, seg_prod, agg, T, W, ws, stream))
-
-
-def backward_aggregate(lam, agg_loc, dh0_loc, agg_out, W, dtype_bytes=4, stream=0):
-    check(getattr(lib, f"linrec_backward_aggregate_{_sfx(dtype_bytes)}")(lam, agg_loc, dh0_loc, agg_out, W, stream))
 
 
 def compose_carries(aggs, first, last, step, seed, out, W, dtype_bytes=4, stream=0):

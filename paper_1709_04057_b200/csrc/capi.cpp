@@ -129,6 +129,34 @@ ChainPtrs ws_ptrs(linrec_workspace* ws, const ChainPlan& p) {
   return w;
 }
 
+// Virtual-segment region, after the look-back records: vagg [nseg][2][W],
+// carry [nseg][W], scale [nseg][W], seg_prod [nseg*ntt][W].
+template <class S>
+struct VsegPtrs {
+  S* vagg;
+  S* carry;
+  S* scale;
+  S* seg_prod;
+};
+
+template <class S>
+size_t vseg_region_bytes(const ChainPlan& p, int64_t W) {
+  return sizeof(S) * (size_t)W * (size_t)(4 * p.nseg + p.nseg * p.ntt) + 1024;
+}
+
+template <class S>
+VsegPtrs<S> vseg_ptrs(linrec_workspace* ws, const ChainPlan& p, int64_t W) {
+  char* b = static_cast<char*>(ws->base) + kCtrlBytes + p.flags_bytes + 2 * p.rec_bytes;
+  b = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(b) + 255) & ~uintptr_t(255));
+  S* v = reinterpret_cast<S*>(b);
+  VsegPtrs<S> r;
+  r.vagg = v;
+  r.carry = v + 2 * p.nseg * W;
+  r.scale = r.carry + p.nseg * W;
+  r.seg_prod = r.scale + p.nseg * W;
+  return r;
+}
+
 std::atomic<int> g_kernel_policy{0};  // LINREC_KERNEL_AUTO
 
 bool tma_allowed(int64_t T, int64_t W) {
@@ -179,8 +207,21 @@ int scan_device(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t 
   if (!tma) p = linrec_impl::plan_chain<S>(true, T, W, vok);
   if (p.ntiles > 0x7fffffffLL) return fail(LINREC_ERR_SHAPE, "linrec: problem too large for one launch");
   if ((rc = ws_reserve(w, p.ws_bytes, st))) return rc;
+  VsegPtrs<S> vs{};
+  if (p.nseg > 1) {  // independent chains per virtual segment, stitched below
+    vs = vseg_ptrs<S>(w, p, W);
+    c.seg_prod = vs.seg_prod;
+    c.agg_out = vs.vagg;
+  }
   if (tma) LINREC_CUDA_TRY(linrec_impl::launch_tma_fwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_fwd<S>(p, c, ws_ptrs(w, p), st));
+  if (p.nseg > 1) {
+    LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, vs.vagg, p.nseg, p.tseg, vs.carry, nullptr,
+                                                         nullptr, nullptr, W, st));
+    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(false, lam, nullptr, nullptr, nullptr, vs.seg_prod, vs.carry, W,
+                                                 nullptr, h, nullptr, T, W, p.rows, p.nseg, p.tseg, p.ntt, vok,
+                                                 st));
+  }
   return LINREC_OK;
 }
 
@@ -208,8 +249,20 @@ int scan_backward_device(const S* lam, const S* h0, const S* h, const S* dh, con
   if (!tma) p = linrec_impl::plan_chain<S>(false, T, W, vok);
   if (p.ntiles > 0x7fffffffLL) return fail(LINREC_ERR_SHAPE, "linrec: problem too large for one launch");
   if ((rc = ws_reserve(w, p.ws_bytes, st))) return rc;
+  VsegPtrs<S> vs{};
+  if (p.nseg > 1) {
+    vs = vseg_ptrs<S>(w, p, W);
+    c.seg_prod = vs.seg_prod;
+    c.agg_out = vs.vagg;
+  }
   if (tma) LINREC_CUDA_TRY(linrec_impl::launch_tma_bwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_bwd<S>(p, c, ws_ptrs(w, p), st));
+  if (p.nseg > 1) {
+    LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, vs.vagg, p.nseg, p.tseg, vs.carry, nullptr,
+                                                         nullptr, dh0, W, st));
+    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(true, lam, h0, h, lam_next, vs.seg_prod, vs.carry, W, nullptr,
+                                                 dx, dlam, T, W, p.rows, p.nseg, p.tseg, p.ntt, vok, st));
+  }
   return LINREC_OK;
 }
 
@@ -441,9 +494,18 @@ int segment_scan(const S* lam, const S* x, const S* h0, S* h, S* seg_prod, S* ag
   linrec_workspace* w = ws ? ws : default_ws(dev, st);
   std::lock_guard<std::mutex> lk(w->mu);
   if ((rc = ws_reserve(w, p.ws_bytes, st))) return rc;
-  FwdCall<S> c{lam, x, h0, h, T, W, seg_prod, agg};
+  if ((rc = ws_reserve(w, p.ws_bytes + vseg_region_bytes<S>(p, W), st))) return rc;
+  const VsegPtrs<S> vs = vseg_ptrs<S>(w, p, W);
+  FwdCall<S> c{lam, x, h0, h, T, W, seg_prod, vs.vagg};
   if (p.kind == 1) LINREC_CUDA_TRY(linrec_impl::launch_tma_fwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_fwd<S>(p, c, ws_ptrs(w, p), st));
+  // carries / products of the virtual segments -> segment-level aggregate
+  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, vs.vagg, p.nseg, p.tseg, vs.carry, vs.scale,
+                                                       agg, nullptr, W, st));
+  if (p.nseg > 1)
+    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(false, lam, nullptr, nullptr, nullptr, seg_prod, vs.carry, W,
+                                                 vs.scale, h, nullptr, T, W, p.rows, p.nseg, p.tseg, p.ntt,
+                                                 p.vec > 1, st));
   return LINREC_OK;
 }
 
@@ -464,9 +526,17 @@ int segment_scan_backward(const S* lam, const S* hprev, const S* h, const S* dh,
   linrec_workspace* w = ws ? ws : default_ws(dev, st);
   std::lock_guard<std::mutex> lk(w->mu);
   if ((rc = ws_reserve(w, p.ws_bytes, st))) return rc;
-  BwdCall<S> c{lam, hprev, h, dh, lam_next, nullptr, dlam, dx, dh0, T, W, seg_prod, agg};
+  if ((rc = ws_reserve(w, p.ws_bytes + vseg_region_bytes<S>(p, W), st))) return rc;
+  const VsegPtrs<S> vs = vseg_ptrs<S>(w, p, W);
+  BwdCall<S> c{lam, hprev, h, dh, lam_next, nullptr, dlam, dx, dh0, T, W, seg_prod, vs.vagg};
   if (p.kind == 1) LINREC_CUDA_TRY(linrec_impl::launch_tma_bwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_bwd<S>(p, c, ws_ptrs(w, p), st));
+  // (A', B') of the segment for the exchange, dh0 = lam_S * G_S, fix-up
+  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, vs.vagg, p.nseg, p.tseg, vs.carry, vs.scale,
+                                                       agg, dh0, W, st));
+  if (p.nseg > 1)
+    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(true, lam, hprev, h, lam_next, seg_prod, vs.carry, W, vs.scale,
+                                                 dx, dlam, T, W, p.rows, p.nseg, p.tseg, p.ntt, p.vec > 1, st));
   return LINREC_OK;
 }
 
@@ -480,8 +550,11 @@ int segment_fixup(bool reverse, const S* lam, const S* hprev, const S* h, const 
   if (reverse && ((rc = check_ptr(h, "h")) || (rc = check_ptr(out1, "d_decays")))) return rc;
   if (rows < 1) return fail(LINREC_ERR_VALUE, "tile_rows must be >= 1");
   const bool v = vec_ok<S>(W, {lam, hprev, h, lam_next, seg_prod, carry, out0, out1});
-  LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(reverse, lam, hprev, h, lam_next, seg_prod, carry, out0, out1,
-                                               T, W, rows, v, st));
+  // the same (nseg, ntt) decomposition the segment scan used
+  const ChainPlan p = plan_segment<S>(!reverse, T, W);
+  if (p.rows != rows) return fail(LINREC_ERR_VALUE, "tile_rows does not match the segment scan's plan");
+  LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(reverse, lam, hprev, h, lam_next, const_cast<S*>(seg_prod), carry,
+                                               0, nullptr, out0, out1, T, W, rows, p.nseg, p.tseg, p.ntt, v, st));
   return LINREC_OK;
 }
 
@@ -634,6 +707,12 @@ int linrec_first_nonfinite_f64(const double* v, int64_t n, int64_t* index, void*
   return first_nonfinite<double>(v, n, index, static_cast<cudaStream_t>(stream));
 }
 
+int64_t linrec_segment_prod_rows(int64_t T, int64_t W, int dtype_bytes, int backward) {
+  if (T < 1 || W < 1) return 0;
+  const ChainPlan p = dtype_bytes == 8 ? plan_segment<double>(!backward, T, W) : plan_segment<float>(!backward, T, W);
+  return p.nseg * p.ntt;
+}
+
 int64_t linrec_segment_tile_rows(int64_t T, int64_t W, int dtype_bytes, int backward) {
   if (T < 1 || W < 1) return 0;
   return dtype_bytes == 8 ? plan_segment<double>(!backward, T, W).rows : plan_segment<float>(!backward, T, W).rows;
@@ -702,25 +781,4 @@ int linrec_compose_carries_f64(const double* aggs, int64_t first, int64_t last, 
                                                       static_cast<cudaStream_t>(stream)));
   return LINREC_OK;
 }
-int linrec_backward_aggregate_f32(const float* lam, const float* agg_loc, const float* dh0_loc, float* agg_out,
-                                  int64_t W, void* stream) {
-  int rc;
-  if ((rc = check_ptr(lam, "decays")) || (rc = check_ptr(agg_loc, "agg_loc")) ||
-      (rc = check_ptr(dh0_loc, "dh0_loc")) || (rc = check_ptr(agg_out, "agg_out")))
-    return rc;
-  LINREC_CUDA_TRY(linrec_impl::launch_bwd_aggregate<float>(lam, agg_loc, dh0_loc, agg_out, W,
-                                                           static_cast<cudaStream_t>(stream)));
-  return LINREC_OK;
-}
-int linrec_backward_aggregate_f64(const double* lam, const double* agg_loc, const double* dh0_loc,
-                                  double* agg_out, int64_t W, void* stream) {
-  int rc;
-  if ((rc = check_ptr(lam, "decays")) || (rc = check_ptr(agg_loc, "agg_loc")) ||
-      (rc = check_ptr(dh0_loc, "dh0_loc")) || (rc = check_ptr(agg_out, "agg_out")))
-    return rc;
-  LINREC_CUDA_TRY(linrec_impl::launch_bwd_aggregate<double>(lam, agg_loc, dh0_loc, agg_out, W,
-                                                            static_cast<cudaStream_t>(stream)));
-  return LINREC_OK;
-}
-
 }  // extern "C"

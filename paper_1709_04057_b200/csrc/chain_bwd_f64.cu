@@ -24,6 +24,8 @@ cudaError_t launch_chain_bwd<double>(const ChainPlan& p, const BwdCall<double>& 
   a.W = c.W;
   a.ncols = p.ncols;
   a.ntt = p.ntt;
+  a.nseg = p.nseg;
+  a.tseg = p.tseg;
   const linrec_dev::ChainWs d = to_dev(w);
   const dim3 grid((unsigned)p.ntiles), block((Tn::BWD_NW + 1) * 32);
   if (p.vec == Tn::VEC) {

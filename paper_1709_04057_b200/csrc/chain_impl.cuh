@@ -25,17 +25,40 @@ inline int pick_q(int64_t nvec) {
   return q;
 }
 
+// Virtual T-segments: few channel columns make each look-back chain long and
+// serial; splitting T into independent chains (stitched afterwards by a carry
+// fold + fix-up, segment.cu) restores parallelism.  Aim for >= 64 chains,
+// keeping >= 8 tiles per segment.
+inline void choose_segments(ChainPlan& p, int64_t T) {
+  const int64_t ntt_total = (T + p.rows - 1) / p.rows;
+  int64_t nseg = (64 + p.ncols - 1) / p.ncols;
+  if (nseg > ntt_total / 8) nseg = ntt_total / 8;
+  if (nseg < 1) nseg = 1;
+  const int64_t per = (ntt_total + nseg - 1) / nseg;
+  p.ntt = per;
+  p.tseg = per * p.rows;
+  p.nseg = (T + p.tseg - 1) / p.tseg;
+  p.ntiles = p.ncols * p.nseg * p.ntt;
+}
+
+// Extra workspace of a virtually segmented launch: vagg [nseg][2][W], carry,
+// scale [nseg][W] and the internal seg_prod [nseg*ntt][W].
+template <class S>
+size_t vseg_bytes(const ChainPlan& p, int64_t W) {
+  if (p.nseg <= 1) return 0;
+  return sizeof(S) * (size_t)W * (size_t)(4 * p.nseg + p.nseg * p.ntt) + 1024;
+}
+
 template <class S, int VEC, int Q, int R, int NW>
 void fill_plan(ChainPlan& p, int64_t T, int64_t W) {
   using Cfg = linrec_dev::ChainCfg<S, VEC, Q, R, NW>;
   p.vec = VEC; p.q = Q; p.r = R; p.nw = NW;
   p.cpw = Cfg::CPW; p.rows = Cfg::L; p.rec = Cfg::REC;
   p.ncols = (W + Cfg::CPW - 1) / Cfg::CPW;
-  p.ntt = (T + Cfg::L - 1) / Cfg::L;
-  p.ntiles = p.ncols * p.ntt;
+  choose_segments(p, T);
   p.flags_bytes = ((size_t)p.ntiles * 4 + 255) / 256 * 256;
   p.rec_bytes = (size_t)p.ntiles * 2 * Cfg::REC * 8;
-  p.ws_bytes = 256 + p.flags_bytes + 2 * p.rec_bytes;
+  p.ws_bytes = 256 + p.flags_bytes + 2 * p.rec_bytes + vseg_bytes<S>(p, W);
 }
 
 #define LINREC_Q_SWITCH(QV, ...)                            \

@@ -21,7 +21,9 @@ struct ChainPlan {
   int rows = 0;       // rows per tile (L)
   int rec = 0;        // carry-record stride in elements
   int64_t ncols = 0;  // channel columns
-  int64_t ntt = 0;    // tiles along time
+  int64_t ntt = 0;    // tiles along time per chain (per virtual segment)
+  int64_t nseg = 1;   // virtual T-segments (independent chains, stitched by segment.cu)
+  int64_t tseg = 0;   // rows per virtual segment
   int64_t ntiles = 0; // = ncols * ntt = grid size
   size_t flags_bytes = 0;
   size_t rec_bytes = 0;  // bytes of ONE of the two record arrays (agg or inc)
@@ -89,16 +91,22 @@ cudaError_t launch_tma_bwd(const ChainPlan& p, const BwdCall<S>& c, const ChainP
 cudaError_t launch_ws_init(void* ctrl, cudaStream_t st);
 
 // segment.cu
+// Fix-up of the tiles of (nseg x ntt) chain positions: e_in = seg_prod[pos] *
+// carry[seg or 0] (carry_stride W or 0); when scale != nullptr each position's
+// seg_prod row is also multiplied in place by scale[seg] (virtual -> segment
+// relative products).
 template <class S>
 cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S* h, const S* lam_next,
-                         const S* seg_prod, const S* carry, S* out0, S* out1, int64_t T, int64_t W,
-                         int64_t rows, bool vec_ok, cudaStream_t st);
+                         S* seg_prod, const S* carry, int64_t carry_stride, const S* scale, S* out0, S* out1,
+                         int64_t T, int64_t W, int64_t rows, int64_t nseg, int64_t tseg, int64_t ntt,
+                         bool vec_ok, cudaStream_t st);
+template <class S>
+cudaError_t launch_vseg_finalize(bool reverse, const S* lam, const S* vagg, int64_t nseg, int64_t tseg,
+                                 S* carry, S* scale, S* agg_rank, S* dh0, int64_t W, cudaStream_t st);
 template <class S>
 cudaError_t launch_compose(const S* aggs, int64_t first, int64_t last, int64_t step, const S* seed, S* out,
                            int64_t W, cudaStream_t st);
-template <class S>
-cudaError_t launch_bwd_aggregate(const S* lam, const S* agg_loc, const S* dh0_loc, S* out, int64_t W,
-                                 cudaStream_t st);
+
 
 template <class S>
 cudaError_t first_nonfinite(const S* v, int64_t n, int64_t* index, cudaStream_t st);

@@ -82,8 +82,41 @@ struct ChainArgs {
   int64_t T;
   int64_t W;
   int64_t ncols;
-  int64_t ntt;        // tiles along time
+  int64_t ntt;        // tiles along time per chain (per virtual segment)
+  int64_t nseg;       // virtual T-segments scanned as independent chains (>= 1)
+  int64_t tseg;       // rows per virtual segment (a multiple of the tile rows)
 };
+
+// Position of ticket k: chain = (virtual segment, channel column), tiles in
+// ticket order along the chain (so the look-back predecessor is k - nchains).
+struct ChainPos {
+  int64_t nchains, chain, pos, col, seg;
+};
+template <class S>
+__device__ __forceinline__ ChainPos chain_pos(const ChainArgs<S>& a, int64_t k) {
+  ChainPos p;
+  p.nchains = a.ncols * a.nseg;
+  p.chain = k % p.nchains;
+  p.pos = k / p.nchains;
+  p.col = p.chain % a.ncols;
+  p.seg = p.chain / a.ncols;
+  return p;
+}
+// first row of the tile at chain position pos; REV walks each segment from
+// its last tile to its first
+template <bool REV, class S>
+__device__ __forceinline__ int64_t tile_row0(const ChainArgs<S>& a, const ChainPos& p, int L) {
+  return p.seg * a.tseg + (REV ? a.ntt - 1 - p.pos : p.pos) * (int64_t)L;
+}
+// decay linking row t to row t+1 in the reverse scan (mu_t = lam_{t+1}),
+// except at the end of the sequence (lam_next, or 0) and at the end of a
+// non-final virtual segment (1: the link is applied by the carry fold)
+template <class S>
+__device__ __forceinline__ int mu_kind(const ChainArgs<S>& a, int64_t t) {
+  if (t + 1 >= a.T) return 2;                          // lam_next / 0
+  if (a.nseg > 1 && (t + 1) % a.tseg == 0) return 1;   // 1
+  return 0;                                            // lam[t+1]
+}
 
 // ---------------------------------------------------------------------------
 // Decoupled look-back, split in two so the tile's data warps can start their
@@ -328,21 +361,23 @@ struct Lookback<double, VEC, Q, REC> {
 // the tile's exclusive decay product per channel, and for the last tile of a
 // chain the chain's inclusive (P, c).
 template <class S, int VEC, int Q>
-__device__ __forceinline__ void write_segment_outputs(const ChainArgs<S>& a, int64_t pos, int64_t ch,
+__device__ __forceinline__ void write_segment_outputs(const ChainArgs<S>& a, const ChainPos& cp, int64_t ch,
                                                       bool valid, const S (&TA)[VEC],
                                                       const S (&TB)[VEC], const S (&c)[VEC],
                                                       const S (&P)[VEC]) {
   const int lane = threadIdx.x & 31;
   if (!(lane < Q && valid)) return;
   if (a.seg_prod != nullptr) {
+    S* sp = a.seg_prod + (cp.seg * a.ntt + cp.pos) * a.W + ch;
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) a.seg_prod[pos * a.W + ch + v] = P[v];
+    for (int v = 0; v < VEC; ++v) sp[v] = P[v];
   }
-  if (a.agg_out != nullptr && pos == a.ntt - 1) {
+  if (a.agg_out != nullptr && cp.pos == a.ntt - 1) {
+    S* ag = a.agg_out + cp.seg * 2 * a.W + ch;
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
-      a.agg_out[ch + v] = mul_(TA[v], P[v]);
-      a.agg_out[a.W + ch + v] = fma_(TA[v], c[v], TB[v]);
+      ag[v] = mul_(TA[v], P[v]);
+      ag[a.W + v] = fma_(TA[v], c[v], TB[v]);
     }
   }
 }
@@ -389,12 +424,11 @@ __device__ __forceinline__ void chain_retire(const ChainWs& ws, uint32_t epoch) 
 // ---------------------------------------------------------------------------
 template <class S, int VEC, int Q, int NW, int CPW, int REC, bool REV>
 __device__ __forceinline__ void chain_coordinator(const ChainArgs<S>& a, const ChainWs& ws,
-                                                  uint32_t epoch, int64_t k, int64_t pos,
-                                                  int64_t col, S (*s_wa)[CPW],
-                                                  S (*s_wb)[CPW], S* s_c) {
+                                                  uint32_t epoch, int64_t k, const ChainPos& cp,
+                                                  S (*s_wa)[CPW], S (*s_wb)[CPW], S* s_c) {
   constexpr int NT = (NW + 1) * 32;
   const int lane = threadIdx.x & 31;
-  const int64_t ch = col * CPW + (int64_t)lane * VEC;
+  const int64_t ch = cp.col * CPW + (int64_t)lane * VEC;
   const bool valid = lane < Q && ch < a.W;
   bar_sync(1, NT);  // segment totals are in shared memory
   S TA[VEC], TB[VEC], c[VEC], P[VEC];
@@ -416,20 +450,21 @@ __device__ __forceinline__ void chain_coordinator(const ChainArgs<S>& a, const C
         TA[v] = mul_(s_wa[w][lane * VEC + v], TA[v]);
       }
     }
-    if (pos == 0 && a.seed != nullptr && valid) {
+    if (cp.pos == 0 && cp.seg == 0 && a.seed != nullptr && valid) {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) c[v] = a.seed[ch + v];
     }
   }
   const bool want_p = a.seg_prod != nullptr || a.agg_out != nullptr;
-  Lookback<S, VEC, Q, REC>::exclusive(ws, epoch, k, pos, col, a.ncols, TA, TB, c, P, valid, want_p);
+  Lookback<S, VEC, Q, REC>::exclusive(ws, epoch, k, cp.pos, cp.chain, cp.nchains, TA, TB, c, P, valid,
+                                      want_p);
   if (lane < Q) {
 #pragma unroll
     for (int v = 0; v < VEC; ++v) s_c[lane * VEC + v] = c[v];
   }
   bar_arrive(2, NT);  // carry is in shared memory: the data warps re-scan now
   Lookback<S, VEC, Q, REC>::publish(ws, epoch, k, TA, TB, c, P, valid, want_p);
-  write_segment_outputs<S, VEC, Q>(a, pos, ch, valid, TA, TB, c, P);
+  write_segment_outputs<S, VEC, Q>(a, cp, ch, valid, TA, TB, c, P);
   chain_retire(ws, epoch);
 }
 
@@ -454,18 +489,17 @@ k_chain_fwd(const ChainArgs<S> a, const ChainWs ws) {
   __syncthreads();
   const int64_t k = (int64_t)s_k;
   const uint32_t epoch = s_epoch;
-  const int64_t col = k % a.ncols, pos = k / a.ncols;
+  const ChainPos cp = chain_pos(a, k);
 
   if (warp == NW) {
-    chain_coordinator<S, VEC, Q, NW, CPW, Cfg::REC, false>(a, ws, epoch, k, pos, col, s_wa,
-                                                          s_wb, s_c);
+    chain_coordinator<S, VEC, Q, NW, CPW, Cfg::REC, false>(a, ws, epoch, k, cp, s_wa, s_wb, s_c);
     return;
   }
 
   const int q = lane % Q, g = lane / Q;
-  const int64_t ch = col * CPW + (int64_t)q * VEC;
+  const int64_t ch = cp.col * CPW + (int64_t)q * VEC;
   const bool valid = ch < a.W;
-  const int64_t t0 = pos * L + (int64_t)(warp * G + g) * R;
+  const int64_t t0 = tile_row0<false>(a, cp, L) + (int64_t)(warp * G + g) * R;
   const int64_t W = a.W;
 
   S l[R][VEC], xv[R][VEC];
@@ -570,19 +604,17 @@ k_chain_bwd(const ChainArgs<S> a, const ChainWs ws) {
   __syncthreads();
   const int64_t k = (int64_t)s_k;
   const uint32_t epoch = s_epoch;
-  const int64_t col = k % a.ncols, pos = k / a.ncols;
+  const ChainPos cp = chain_pos(a, k);
 
   if (warp == NW) {
-    chain_coordinator<S, VEC, Q, NW, CPW, Cfg::REC, true>(a, ws, epoch, k, pos, col, s_wa,
-                                                         s_wb, s_c);
+    chain_coordinator<S, VEC, Q, NW, CPW, Cfg::REC, true>(a, ws, epoch, k, cp, s_wa, s_wb, s_c);
     return;
   }
 
   const int q = lane % Q, g = lane / Q;
-  const int64_t tile = a.ntt - 1 - pos;
-  const int64_t ch = col * CPW + (int64_t)q * VEC;
+  const int64_t ch = cp.col * CPW + (int64_t)q * VEC;
   const bool valid = ch < a.W;
-  const int64_t t0 = tile * L + (int64_t)(warp * G + g) * R;
+  const int64_t t0 = tile_row0<true>(a, cp, L) + (int64_t)(warp * G + g) * R;
   const int64_t W = a.W, T = a.T;
 
   S mu[R][VEC], dh[R][VEC], hp[R][VEC];
@@ -590,8 +622,12 @@ k_chain_bwd(const ChainArgs<S> a, const ChainWs ws) {
   for (int i = 0; i < R; ++i) {
     const int64_t t = t0 + i;
     if (valid && t < T) {
-      if (t + 1 < T) {
+      const int mk = mu_kind(a, t);
+      if (mk == 0) {
         IO::load_stream(a.a + (t + 1) * W + ch, mu[i]);
+      } else if (mk == 1) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) mu[i][v] = S(1);
       } else if (a.lam_next != nullptr) {
         IO::load_cg(a.lam_next + ch, mu[i]);
       } else {

@@ -113,8 +113,8 @@ __device__ __forceinline__ void tma_coordinator(const SM& sm, const ChainArgs<S>
     if (k < 0) break;
     const int slot = n & 1;
     mbar_wait(sm.aggr(slot), (n >> 1) & 1);
-    const int64_t col = k % a.ncols, pos = k / a.ncols;
-    const int64_t ch = col * CPW + (int64_t)lane * VEC;
+    const ChainPos cp = chain_pos(a, k);
+    const int64_t ch = cp.col * CPW + (int64_t)lane * VEC;
     const bool valid = lane < Q && ch < a.W;
     S TA[VEC], TB[VEC], c[VEC], P[VEC];
 #pragma unroll
@@ -137,20 +137,21 @@ __device__ __forceinline__ void tma_coordinator(const SM& sm, const ChainArgs<S>
           TA[v] = mul_(ta[w * CPW + lane * VEC + v], TA[v]);
         }
       }
-      if (pos == 0 && a.seed != nullptr && valid) {
+      if (cp.pos == 0 && cp.seg == 0 && a.seed != nullptr && valid) {
 #pragma unroll
         for (int v = 0; v < VEC; ++v) c[v] = a.seed[ch + v];
       }
     }
     const bool want_p = a.seg_prod != nullptr || a.agg_out != nullptr;
-    Lookback<S, VEC, Q, Cfg::REC>::exclusive(ws, epoch, k, pos, col, a.ncols, TA, TB, c, P, valid, want_p);
+    Lookback<S, VEC, Q, Cfg::REC>::exclusive(ws, epoch, k, cp.pos, cp.chain, cp.nchains, TA, TB, c, P, valid,
+                                             want_p);
     if (lane < Q) {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) sm.carry(slot)[lane * VEC + v] = c[v];
     }
     mbar_arrive(sm.carry_bar(slot));  // consumers re-scan while the carry is published
     Lookback<S, VEC, Q, Cfg::REC>::publish(ws, epoch, k, TA, TB, c, P, valid, want_p);
-    write_segment_outputs<S, VEC, Q>(a, pos, ch, valid, TA, TB, c, P);
+    write_segment_outputs<S, VEC, Q>(a, cp, ch, valid, TA, TB, c, P);
   }
   chain_retire(ws, epoch);
 }
@@ -186,8 +187,9 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
           break;
         }
         sm.meta()[s] = k;
-        const int c0 = (int)((k % a.ncols) * CPW);
-        const int r0 = (int)((k / a.ncols) * L);
+        const ChainPos cp = chain_pos(a, (int64_t)k);
+        const int c0 = (int)(cp.col * CPW);
+        const int r0 = (int)tile_row0<false>(a, cp, L);
         mbar_arrive_expect_tx(sm.full(s), Cfg::TX_BYTES);
 #pragma unroll
         for (int b = 0; b < Cfg::NBOX; ++b) {
@@ -212,10 +214,10 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
     mbar_wait(sm.full(s), (n / STAGES) & 1);
     const long long k = sm.meta()[s];
     if (k < 0) break;
-    const int64_t col = k % a.ncols, pos = k / a.ncols;
-    const int64_t ch = col * CPW + (int64_t)q * VEC;
+    const ChainPos cp = chain_pos(a, (int64_t)k);
+    const int64_t ch = cp.col * CPW + (int64_t)q * VEC;
     const bool valid = ch < W;
-    const int64_t t0 = pos * L + (int64_t)seg * R;
+    const int64_t t0 = tile_row0<false>(a, cp, L) + (int64_t)seg * R;
     S l[R][VEC], xv[R][VEC];
     const S* sl = sm.arr(s, 0) + seg * R * CPW + q * VEC;
     const S* sx = sm.arr(s, 1) + seg * R * CPW + q * VEC;
@@ -328,8 +330,9 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
           break;
         }
         sm.meta()[s] = k;
-        const int c0 = (int)((k % a.ncols) * CPW);
-        const int r0 = (int)((a.ntt - 1 - k / a.ncols) * L);
+        const ChainPos cp = chain_pos(a, (int64_t)k);
+        const int c0 = (int)(cp.col * CPW);
+        const int r0 = (int)tile_row0<true>(a, cp, L);
         mbar_arrive_expect_tx(sm.full(s), Cfg::TX_BYTES);
 #pragma unroll
         for (int b = 0; b < Cfg::NBOX; ++b) {
@@ -356,11 +359,10 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
     mbar_wait(sm.full(s), (n / STAGES) & 1);
     const long long k = sm.meta()[s];
     if (k < 0) break;
-    const int64_t col = k % a.ncols, pos = k / a.ncols;
-    const int64_t tile = a.ntt - 1 - pos;
-    const int64_t ch = col * CPW + (int64_t)q * VEC;
+    const ChainPos cp = chain_pos(a, (int64_t)k);
+    const int64_t ch = cp.col * CPW + (int64_t)q * VEC;
     const bool valid = ch < W;
-    const int64_t t0 = tile * L + (int64_t)seg * R;
+    const int64_t t0 = tile_row0<true>(a, cp, L) + (int64_t)seg * R;
     S mu[R][VEC], dh[R][VEC], hp[R][VEC];
     const S* smu = sm.arr(s, 0) + seg * R * CPW + q * VEC;
     const S* sdh = sm.arr(s, 1) + seg * R * CPW + q * VEC;
@@ -375,9 +377,13 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
           dh[i][v] = sdh[i * CPW + v];
           hp[i][v] = shp[i * CPW + v];
         }
-        if (t == T - 1) {  // zero-filled past the end; the segment form supplies lam_next
+        const int mk = mu_kind(a, t);
+        if (mk == 2) {  // zero-filled past the end; the segment form supplies lam_next
 #pragma unroll
           for (int v = 0; v < VEC; ++v) mu[i][v] = (a.lam_next != nullptr && valid) ? a.lam_next[ch + v] : S(0);
+        } else if (mk == 1) {  // end of a virtual segment: linked by the carry fold
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) mu[i][v] = S(1);
         }
         if (t == 0) {  // zero-filled row -1 -> h0
 #pragma unroll

@@ -23,37 +23,56 @@ namespace linrec_dev {
 
 // One CTA per (chain position, channel column); 8 warps; Q lanes across
 // channels x G groups along time, RF rows per thread per pass; a tile of
-// `rows` rows is covered in ceil(rows / (8*G*RF)) passes.
+// `rows` rows is covered in ceil(rows / (8*G*RF)) passes.  Chain positions
+// run over nseg virtual segments of ntt tiles (tile p of segment s starts at
+// row s*tseg + p*rows, or (ntt-1-p)*rows for the reverse scan).
 template <class S, int VEC, int Q, bool REV>
 __global__ void __launch_bounds__(256)
 k_fixup(const S* __restrict__ lam, const S* __restrict__ hprev_row, const S* __restrict__ h,
-        const S* __restrict__ lam_next, const S* __restrict__ seg_prod, const S* __restrict__ carry,
-        S* __restrict__ out0 /* fwd: h; bwd: dx */, S* __restrict__ out1 /* bwd: dlam */, int64_t T,
-        int64_t W, int64_t rows, int64_t ncols, int64_t ntt) {
+        const S* __restrict__ lam_next, S* __restrict__ seg_prod, const S* __restrict__ carry,
+        int64_t carry_stride, const S* __restrict__ scale, S* __restrict__ out0 /* fwd: h; bwd: dx */,
+        S* __restrict__ out1 /* bwd: dlam */, int64_t T, int64_t W, int64_t rows, int64_t ncols, int64_t nseg,
+        int64_t tseg, int64_t ntt) {
   constexpr int NW = 8, RF = 4, G = 32 / Q, CPW = Q * VEC, NSEG = NW * G, PR = NSEG * RF;
   using IO = VecIO<S, VEC>;
   __shared__ S s_wp[NW][CPW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = lane % Q, g = lane / Q;
   const int64_t col = blockIdx.x % ncols, pos = blockIdx.x / ncols;
-  const int64_t tile = REV ? ntt - 1 - pos : pos;
+  const int64_t vseg = pos / ntt, p_in = pos % ntt;
+  const int64_t tile_row = vseg * tseg + (REV ? ntt - 1 - p_in : p_in) * rows;
   const int64_t ch = col * CPW + (int64_t)q * VEC;
   const bool valid = ch < W;
   // carry entering the tile: exclusive product * segment carry
   S e[VEC];
   bool nz = false;
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) {
-    e[v] = valid ? mul_(seg_prod[pos * W + ch + v], carry[ch + v]) : S(0);
-    nz = nz || e[v] != S(0);
+  for (int v = 0; v < VEC; ++v) e[v] = S(0);
+  if (valid) {
+    const S* sp = seg_prod + pos * W + ch;
+    const S* cr = carry + vseg * carry_stride + ch;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      e[v] = mul_(sp[v], cr[v]);
+      nz = nz || e[v] != S(0);
+    }
   }
-  if (!__syncthreads_or(nz)) return;
+  nz = __syncthreads_or(nz);  // every thread has read seg_prod past this point
+  if (scale != nullptr && valid && warp == 0 && g == 0) {  // virtual -> segment-relative products
+    S* sp = seg_prod + pos * W + ch;
+    const S* sc = scale + vseg * W + ch;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) sp[v] = mul_(sp[v], sc[v]);
+  }
+  if (!nz) return;
 
-  const int64_t t_lo = tile * rows, t_hi = (t_lo + rows < T ? t_lo + rows : T);
+  const int64_t t_lo = tile_row;
+  const int64_t seg_end = (vseg + 1) * tseg < T ? (vseg + 1) * tseg : T;
+  const int64_t t_hi = (t_lo + rows < seg_end ? t_lo + rows : seg_end);
   const int64_t npass = (rows + PR - 1) / PR;
   for (int64_t ps = 0; ps < npass; ++ps) {
     // rows of this pass, in processing order
-    const int64_t pbase = REV ? t_hi - (ps + 1) * PR : t_lo + ps * PR;
+    const int64_t pbase = REV ? t_lo + rows - (ps + 1) * PR : t_lo + ps * PR;
     const int seg = warp * G + g;
     S m[RF][VEC];
 #pragma unroll
@@ -66,11 +85,13 @@ k_fixup(const S* __restrict__ lam, const S* __restrict__ hprev_row, const S* __r
       if (in) {
         if (!REV) {
           IO::load_cg(lam + t * W + ch, m[i]);
-        } else if (t + 1 < T) {
-          IO::load_cg(lam + (t + 1) * W + ch, m[i]);
-        } else {
+        } else if (t + 1 >= T) {
 #pragma unroll
           for (int v = 0; v < VEC; ++v) m[i][v] = lam_next != nullptr ? lam_next[ch + v] : S(0);
+        } else if (nseg > 1 && (t + 1) % tseg == 0) {
+          // end of a virtual segment: mu = 1 (m already 1)
+        } else {
+          IO::load_cg(lam + (t + 1) * W + ch, m[i]);
         }
       }
     }
@@ -161,15 +182,39 @@ __global__ void k_compose(const S* __restrict__ aggs, int64_t first, int64_t las
   }
 }
 
-// Backward segment aggregate for the exchange: A' = lam_0 * P'_segment,
-// B' = lam_0 * G_loc_0 (= the zero-carry scan's dh0).
-template <class S>
-__global__ void k_bwd_aggregate(const S* __restrict__ lam, const S* __restrict__ agg_loc,
-                                const S* __restrict__ dh0_loc, S* __restrict__ out, int64_t W) {
+// Virtual-segment finalisation (one thread per channel).
+// forward: carry[s] = state entering segment s (0 for s = 0, whose chain was
+//   seeded), scale[s] = decay product of the segments before s, agg_rank =
+//   (product over all, final state).
+// reverse: carry[s] = lam_E * G_E entering segment s from above (0 for the
+//   last), scale[s] = product of the A' of the segments after s, agg_rank =
+//   (A', B') of the whole range, dh0 = lam_0 * G_0 (the range's start).
+// vagg[s] = (P_incl, c_incl) of segment s's chains.
+template <class S, bool REV>
+__global__ void k_vseg_finalize(const S* __restrict__ lam, const S* __restrict__ vagg, int64_t nseg, int64_t tseg,
+                                S* __restrict__ carry, S* __restrict__ scale, S* __restrict__ agg_rank,
+                                S* __restrict__ dh0, int64_t W) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < W;
        j += (int64_t)gridDim.x * blockDim.x) {
-    out[j] = mul_(lam[j], agg_loc[j]);
-    out[W + j] = dh0_loc[j];
+    S c = S(0), pc = S(1);
+    for (int64_t i = 0; i < nseg; ++i) {
+      const int64_t s = REV ? nseg - 1 - i : i;
+      if (carry != nullptr) carry[s * W + j] = c;
+      if (scale != nullptr) scale[s * W + j] = pc;
+      S A = vagg[s * 2 * W + j], B = vagg[s * 2 * W + W + j];
+      if (REV) {
+        const S l0 = lam[(s * tseg) * W + j];
+        A = mul_(l0, A);
+        B = mul_(l0, B);
+      }
+      c = fma_(A, c, B);
+      pc = mul_(A, pc);
+    }
+    if (agg_rank != nullptr) {
+      agg_rank[j] = pc;
+      agg_rank[W + j] = c;
+    }
+    if (dh0 != nullptr) dh0[j] = c;
   }
 }
 
@@ -179,25 +224,40 @@ namespace linrec_impl {
 
 template <class S>
 cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S* h, const S* lam_next,
-                         const S* seg_prod, const S* carry, S* out0, S* out1, int64_t T, int64_t W,
-                         int64_t rows, bool vec_ok, cudaStream_t st) {
+                         S* seg_prod, const S* carry, int64_t carry_stride, const S* scale, S* out0, S* out1,
+                         int64_t T, int64_t W, int64_t rows, int64_t nseg, int64_t tseg, int64_t ntt,
+                         bool vec_ok, cudaStream_t st) {
   constexpr int V = Tuning<S>::VEC;
   const int64_t nvec = vec_ok ? (W + V - 1) / V : W;
   const int q = pick_q(nvec);
   const int cpw = q * (vec_ok ? V : 1);
-  const int64_t ncols = (W + cpw - 1) / cpw, ntt = (T + rows - 1) / rows;
-  const dim3 grid((unsigned)(ncols * ntt));
-#define FIX(VV)                                                                                   \
-  LINREC_Q_SWITCH(q, if (reverse) linrec_dev::k_fixup<S, VV, Q_, true><<<grid, 256, 0, st>>>(     \
-                         lam, hprev_row, h, lam_next, seg_prod, carry, out0, out1, T, W, rows, ncols, ntt); \
-                     else linrec_dev::k_fixup<S, VV, Q_, false><<<grid, 256, 0, st>>>(            \
-                         lam, hprev_row, h, lam_next, seg_prod, carry, out0, out1, T, W, rows, ncols, ntt));
+  const int64_t ncols = (W + cpw - 1) / cpw;
+  const dim3 grid((unsigned)(ncols * nseg * ntt));
+#define FIX(VV)                                                                                       \
+  LINREC_Q_SWITCH(q, if (reverse) linrec_dev::k_fixup<S, VV, Q_, true><<<grid, 256, 0, st>>>(         \
+                         lam, hprev_row, h, lam_next, seg_prod, carry, carry_stride, scale, out0, out1, T, \
+                         W, rows, ncols, nseg, tseg, ntt);                                            \
+                     else linrec_dev::k_fixup<S, VV, Q_, false><<<grid, 256, 0, st>>>(                \
+                         lam, hprev_row, h, lam_next, seg_prod, carry, carry_stride, scale, out0, out1, T, \
+                         W, rows, ncols, nseg, tseg, ntt));
   if (vec_ok) {
     FIX(V)
   } else {
     FIX(1)
   }
 #undef FIX
+  return cudaGetLastError();
+}
+
+template <class S>
+cudaError_t launch_vseg_finalize(bool reverse, const S* lam, const S* vagg, int64_t nseg, int64_t tseg, S* carry,
+                                 S* scale, S* agg_rank, S* dh0, int64_t W, cudaStream_t st) {
+  const int64_t blocks = (W + 127) / 128;
+  const unsigned g = (unsigned)(blocks < 1024 ? blocks : 1024);
+  if (reverse)
+    linrec_dev::k_vseg_finalize<S, true><<<g, 128, 0, st>>>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W);
+  else
+    linrec_dev::k_vseg_finalize<S, false><<<g, 128, 0, st>>>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W);
   return cudaGetLastError();
 }
 
@@ -210,28 +270,19 @@ cudaError_t launch_compose(const S* aggs, int64_t first, int64_t last, int64_t s
   return cudaGetLastError();
 }
 
-template <class S>
-cudaError_t launch_bwd_aggregate(const S* lam, const S* agg_loc, const S* dh0_loc, S* out, int64_t W,
-                                 cudaStream_t st) {
-  const int64_t blocks = (W + 255) / 256;
-  linrec_dev::k_bwd_aggregate<S><<<(unsigned)(blocks < 1024 ? blocks : 1024), 256, 0, st>>>(lam, agg_loc,
-                                                                                            dh0_loc, out, W);
-  return cudaGetLastError();
-}
-
-template cudaError_t launch_fixup<float>(bool, const float*, const float*, const float*, const float*,
-                                         const float*, const float*, float*, float*, int64_t, int64_t,
-                                         int64_t, bool, cudaStream_t);
+template cudaError_t launch_fixup<float>(bool, const float*, const float*, const float*, const float*, float*,
+                                         const float*, int64_t, const float*, float*, float*, int64_t, int64_t,
+                                         int64_t, int64_t, int64_t, int64_t, bool, cudaStream_t);
 template cudaError_t launch_fixup<double>(bool, const double*, const double*, const double*, const double*,
-                                          const double*, const double*, double*, double*, int64_t, int64_t,
-                                          int64_t, bool, cudaStream_t);
+                                          double*, const double*, int64_t, const double*, double*, double*,
+                                          int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, bool, cudaStream_t);
 template cudaError_t launch_compose<float>(const float*, int64_t, int64_t, int64_t, const float*, float*,
                                            int64_t, cudaStream_t);
 template cudaError_t launch_compose<double>(const double*, int64_t, int64_t, int64_t, const double*, double*,
                                             int64_t, cudaStream_t);
-template cudaError_t launch_bwd_aggregate<float>(const float*, const float*, const float*, float*, int64_t,
-                                                 cudaStream_t);
-template cudaError_t launch_bwd_aggregate<double>(const double*, const double*, const double*, double*,
-                                                  int64_t, cudaStream_t);
+template cudaError_t launch_vseg_finalize<float>(bool, const float*, const float*, int64_t, int64_t, float*,
+                                                 float*, float*, float*, int64_t, cudaStream_t);
+template cudaError_t launch_vseg_finalize<double>(bool, const double*, const double*, int64_t, int64_t, double*,
+                                                  double*, double*, double*, int64_t, cudaStream_t);
 
 }  // namespace linrec_impl

@@ -63,11 +63,10 @@ void fill_tma_plan(ChainPlan& p, int64_t T, int64_t W, Kern kern) {
   p.cpw = Cfg::CPW; p.rows = Cfg::L; p.rec = Cfg::REC;
   p.box_cols = Cfg::CPW; p.box_rows = Cfg::BOX_ROWS;
   p.ncols = (W + Cfg::CPW - 1) / Cfg::CPW;
-  p.ntt = (T + Cfg::L - 1) / Cfg::L;
-  p.ntiles = p.ncols * p.ntt;
+  choose_segments(p, T);
   p.flags_bytes = ((size_t)p.ntiles * 4 + 255) / 256 * 256;
   p.rec_bytes = (size_t)p.ntiles * 2 * Cfg::REC * 8;
-  p.ws_bytes = 256 + p.flags_bytes + 2 * p.rec_bytes;
+  p.ws_bytes = 256 + p.flags_bytes + 2 * p.rec_bytes + vseg_bytes<S>(p, W);
   p.threads = Cfg::THREADS;
   p.smem = Cfg::SMEM;
   p.grid = tma_grid(kern, Cfg::THREADS, Cfg::SMEM, p.ntiles);
@@ -113,6 +112,8 @@ linrec_dev::ChainArgs<S> fwd_args(const ChainPlan& p, const FwdCall<S>& c) {
   a.W = c.W;
   a.ncols = p.ncols;
   a.ntt = p.ntt;
+  a.nseg = p.nseg;
+  a.tseg = p.tseg;
   return a;
 }
 
@@ -134,6 +135,8 @@ linrec_dev::ChainArgs<S> bwd_args(const ChainPlan& p, const BwdCall<S>& c) {
   a.W = c.W;
   a.ncols = p.ncols;
   a.ntt = p.ntt;
+  a.nseg = p.nseg;
+  a.tseg = p.tseg;
   return a;
 }
 

@@ -63,6 +63,9 @@ class CudaBackend:
     def tile_rows(self, T, W, backward):
         return capi.segment_tile_rows(T, W, backward)
 
+    def prod_rows(self, T, W, backward):
+        return capi.segment_prod_rows(T, W, backward)
+
     def segment_scan(self, lam, x, h0, h, seg_prod, agg, T, W):
         capi.segment_scan(lam.data_ptr(), x.data_ptr(), self._p(h0), h.data_ptr(), seg_prod.data_ptr(),
                           agg.data_ptr(), T, W, 4, None if self.ws is None else self.ws.handle, self._st())
@@ -72,10 +75,6 @@ class CudaBackend:
                                    self._p(lam_next), dlam.data_ptr(), dx.data_ptr(), dh0.data_ptr(),
                                    seg_prod.data_ptr(), agg.data_ptr(), T, W, 4,
                                    None if self.ws is None else self.ws.handle, self._st())
-
-    def backward_aggregate(self, lam, agg_loc, dh0_loc, agg_out, W):
-        capi.backward_aggregate(lam.data_ptr(), agg_loc.data_ptr(), dh0_loc.data_ptr(), agg_out.data_ptr(), W,
-                                4, self._st())
 
     def compose(self, aggs, first, last, step, seed, out, W):
         capi.compose_carries(aggs.data_ptr(), first, last, step, self._p(seed), out.data_ptr(), W, 4, self._st())
@@ -112,22 +111,23 @@ class SequenceShardedScan:
         f = dict(dtype=torch.float32, device=dev)
         self.rows_f = self.be.tile_rows(self.Tl, W, False)
         self.rows_b = self.be.tile_rows(self.Tl, W, True)
-        nf = -(-self.Tl // self.rows_f)
-        nb = -(-self.Tl // self.rows_b)
+        nf = self.be.prod_rows(self.Tl, W, False)
+        nb = self.be.prod_rows(self.Tl, W, True)
         self.seg_prod_f = torch.empty(nf, W, **f)
         self.seg_prod_b = torch.empty(nb, W, **f)
         self.agg = torch.empty(2, W, **f)
         self.aggs = torch.empty(self.world, 2, W, **f)
         self.c_in = torch.zeros(W, **f)
         self.y_in = torch.zeros(W, **f)
-        self.agg_loc = torch.empty(2, W, **f)
         self.dh0_loc = torch.empty(W, **f)
         self.ones = torch.ones(W, **f)
         self.zeros = torch.zeros(W, **f)
         self.hprev = None
         # kernels launched per step on this rank (for bench.py's gpu_launches)
         r, R = self.rank, self.world
-        self.launches_per_step = (1 + (2 if r > 0 else 0)) + (2 + (2 if r < R - 1 else 0) + (1 if r == 0 else 0))
+        # fwd: scan + finalize (+ fix-up when virtually segmented) + compose/fix-up
+        # for r > 0; bwd likewise + the dh0 compose on rank 0
+        self.launches_per_step = (2 + (2 if r > 0 else 0)) + (2 + (2 if r < R - 1 else 0) + (1 if r == 0 else 0))
 
     def _on_stream(self):
         if self.stream is not None and torch.cuda.is_available() and isinstance(self.stream, torch.cuda.Stream):
@@ -177,8 +177,7 @@ class SequenceShardedScan:
             hprev = self.hprev if self.hprev is not None else self._halo(h, h0)
         lam_next = self.ones if r < R - 1 else None
         self.be.segment_scan_backward(lam, hprev, h, dh, lam_next, dlam, dx, self.dh0_loc, self.seg_prod_b,
-                                      self.agg_loc, T, W)
-        self.be.backward_aggregate(lam, self.agg_loc, self.dh0_loc, self.agg, W)
+                                      self.agg, T, W)
         self._all_gather(self.agg, self.aggs)
         if r < R - 1:
             self.be.compose(self.aggs, R - 1, r, -1, None, self.y_in, W)

@@ -20,6 +20,9 @@ class RefBackend:
     def tile_rows(self, T, W, backward):
         return self.rows
 
+    def prod_rows(self, T, W, backward):
+        return -(-T // self.rows)
+
     def segment_scan(self, lam, x, h0, h, seg_prod, agg, T, W):
         L, X, H = _np(lam).reshape(T, W), _np(x).reshape(T, W), _np(h).reshape(T, W)
         c = np.zeros(W) if h0 is None else _np(h0).reshape(W).copy()
@@ -54,13 +57,7 @@ class RefBackend:
             DL[t] = (H[t - 1] if t >= 1 else hp) * G
         _np(dh0).reshape(W)[:] = L[0] * G
         A = _np(agg)
-        A[0], A[1] = P, G
-
-    def backward_aggregate(self, lam, agg_loc, dh0_loc, agg_out, W):
-        L0 = _np(lam).reshape(-1, W)[0]
-        A = _np(agg_out)
-        A[0] = L0 * _np(agg_loc)[0]
-        A[1] = _np(dh0_loc).reshape(W)
+        A[0], A[1] = L[0] * P, L[0] * G  # (A', B') ready for the exchange
 
     def compose(self, aggs, first, last, step, seed, out, W):
         AG = _np(aggs)

@@ -436,3 +436,27 @@ def test_tma_and_register_kernels_agree(ops):
         assert ((hh - hs).abs().max() / hs.abs().max()).item() <= 1e-5
     for a, b in zip(g_auto, g_reg):
         assert ((a - b).abs().max() / b.abs().max()).item() <= 1e-5
+
+
+@pytest.mark.parametrize("T,W,lo,hi", [
+    (300000, 16, 0.05, 0.95),    # 1 column -> virtual T-segments (fix-up of the leading tile)
+    (100000, 8, 0.999, 1.0),     # decays ~1: fix-up spans whole segments
+    (50000, 3, -1.0, 1.0),       # scalar register kernels with virtual segments
+    (1 << 18, 128, 0.5, 1.0),
+])
+def test_virtual_segments_against_oracle(ops, oracle, policy, T, W, lo, hi):
+    rng = np.random.default_rng(T + W)
+    lam = rng.uniform(lo, hi, (T, 1, W)).astype(np.float32)
+    x = rng.uniform(-1, 1, (T, 1, W)).astype(np.float32)
+    h0 = rng.uniform(-1, 1, (1, W)).astype(np.float32)
+    dh = rng.uniform(-1, 1, (T, 1, W)).astype(np.float32)
+    tl, tx, th0, tdh = cuda(lam), cuda(x), cuda(h0), cuda(dh)
+    h = ops.scan(tl, tx, th0)
+    wide = oracle.scan_serial_wide(lam, x, h0)
+    assert rel(h.cpu().numpy(), wide) <= 1e-5
+    assert torch.equal(h, ops.scan(tl, tx, th0))  # deterministic with the stitch too
+    ref = oracle.scan_serial(lam, x, h0)
+    g = ops.scan_backward(tl, th0, cuda(ref), tdh)
+    gw = oracle.scan_backward_wide(lam, h0, ref, dh)
+    for a, r in zip(g, gw):
+        assert rel(a.cpu().numpy(), r) <= 1e-5

@@ -40,8 +40,8 @@ def emulate(lam, x, h0, dh, R):
         rf, rb = capi.segment_tile_rows(e - s, W, False), capi.segment_tile_rows(e - s, W, True)
         rows_f.append(rf)
         rows_b.append(rb)
-        sp_f.append(torch.empty(-(-(e - s) // rf), W, device=dev))
-        sp_b.append(torch.empty(-(-(e - s) // rb), W, device=dev))
+        sp_f.append(torch.empty(capi.segment_prod_rows(e - s, W, False), W, device=dev))
+        sp_b.append(torch.empty(capi.segment_prod_rows(e - s, W, True), W, device=dev))
     # forward: local scans
     for r, (s, e) in enumerate(segs):
         capi.segment_scan(lam[s].data_ptr(), x[s].data_ptr(), h0.data_ptr() if r == 0 else None, h[s].data_ptr(),
@@ -55,17 +55,14 @@ def emulate(lam, x, h0, dh, R):
                            rows_f[r], 4, st)
     # backward
     ones = torch.ones(W, device=dev)
-    agg_loc = torch.empty(2, W, device=dev)
     dh0_loc = [torch.empty(W, device=dev) for _ in range(R)]
     baggs = torch.zeros(R, 2, W, device=dev)
     for r, (s, e) in enumerate(segs):
         ln = ones if r < R - 1 else None
         capi.segment_scan_backward(lam[s].data_ptr(), c_in[r].data_ptr(), h[s].data_ptr(), dh[s].data_ptr(),
                                    None if ln is None else ln.data_ptr(), dlam[s].data_ptr(), dx[s].data_ptr(),
-                                   dh0_loc[r].data_ptr(), sp_b[r].data_ptr(), agg_loc.data_ptr(), e - s, W, 4,
+                                   dh0_loc[r].data_ptr(), sp_b[r].data_ptr(), baggs[r].data_ptr(), e - s, W, 4,
                                    None, st)
-        capi.backward_aggregate(lam[s].data_ptr(), agg_loc.data_ptr(), dh0_loc[r].data_ptr(), baggs[r].data_ptr(),
-                                W, 4, st)
     y0 = torch.zeros(W, device=dev)
     for r, (s, e) in enumerate(segs):
         if r == R - 1:

@@ -44,7 +44,7 @@ def _worker(rank, world, port, T, b, n, rows, use_h0, seed, q):
         DH0 = torch.zeros(b, n, dtype=torch.float64)
         runner = SequenceShardedScan(T, b * n, backend=RefBackend(rows), device=torch.device("cpu"))
         # the runner allocates float32 scratch; the reference backend works in float64
-        for name in ("seg_prod_f", "seg_prod_b", "agg", "aggs", "c_in", "y_in", "agg_loc", "dh0_loc", "ones", "zeros"):
+        for name in ("seg_prod_f", "seg_prod_b", "agg", "aggs", "c_in", "y_in", "dh0_loc", "ones", "zeros"):
             setattr(runner, name, getattr(runner, name).double())
         runner.forward(L, X, H0, H)
         runner.backward(L, H0, H, DH, DL, DX, DH0)
