@@ -77,6 +77,13 @@ int check_dims(int64_t T, int64_t W) {
   return LINREC_OK;
 }
 
+// The chained kernels index rows with 32-bit integers.
+int check_rows(int64_t T) {
+  if (T > (int64_t(1) << 31) - 65536)
+    return fail(LINREC_ERR_SHAPE, "linrec: T >= 2^31 - 65536 rows is not supported by the parallel kernels");
+  return LINREC_OK;
+}
+
 int check_mode(int mode) {
   if (mode != LINREC_SERIAL && mode != LINREC_PARALLEL)
     return fail(LINREC_ERR_VALUE, "mode must be \"parallel\" or \"serial\"");
@@ -199,7 +206,7 @@ int scan_device(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t 
     return LINREC_OK;
   }
   int dev;
-  if ((rc = current_device(&dev))) return rc;
+  if ((rc = check_rows(T)) || (rc = current_device(&dev))) return rc;
   linrec_workspace* w = ws ? ws : default_ws(dev, st);
   std::lock_guard<std::mutex> lk(w->mu);
   ChainPlan p;
@@ -241,7 +248,7 @@ int scan_backward_device(const S* lam, const S* h0, const S* h, const S* dh, con
     return LINREC_OK;
   }
   int dev;
-  if ((rc = current_device(&dev))) return rc;
+  if ((rc = check_rows(T)) || (rc = current_device(&dev))) return rc;
   linrec_workspace* w = ws ? ws : default_ws(dev, st);
   std::lock_guard<std::mutex> lk(w->mu);
   ChainPlan p;
@@ -486,6 +493,7 @@ int segment_scan(const S* lam, const S* x, const S* h0, S* h, S* seg_prod, S* ag
   if ((rc = check_dims(T, W)) || (rc = check_ptr(lam, "decays")) || (rc = check_ptr(x, "impulses")) ||
       (rc = check_ptr(h, "h")) || (rc = check_ptr(seg_prod, "seg_prod")) || (rc = check_ptr(agg, "agg")))
     return rc;
+  if ((rc = check_rows(T))) return rc;
   const ChainPlan p = plan_segment<S>(true, T, W);
   if (p.vec > 1 && !vec_ok<S>(W, {lam, x, h0, h, seg_prod, agg}))
     return fail(LINREC_ERR_VALUE, "segment scans need 16-byte aligned buffers");
@@ -518,6 +526,7 @@ int segment_scan_backward(const S* lam, const S* hprev, const S* h, const S* dh,
       (rc = check_ptr(dh, "d_h")) || (rc = check_ptr(dlam, "d_decays")) || (rc = check_ptr(dx, "d_impulses")) ||
       (rc = check_ptr(dh0, "d_initial")) || (rc = check_ptr(seg_prod, "seg_prod")) || (rc = check_ptr(agg, "agg")))
     return rc;
+  if ((rc = check_rows(T))) return rc;
   const ChainPlan p = plan_segment<S>(false, T, W);
   if (p.vec > 1 && !vec_ok<S>(W, {lam, hprev, h, dh, lam_next, dlam, dx, dh0, seg_prod, agg}))
     return fail(LINREC_ERR_VALUE, "segment scans need 16-byte aligned buffers");

@@ -89,33 +89,38 @@ struct ChainArgs {
 
 // Position of ticket k: chain = (virtual segment, channel column), tiles in
 // ticket order along the chain (so the look-back predecessor is k - nchains).
+// 32-bit arithmetic: tickets < 2^31 and T < 2^31 are enforced by the host.
 struct ChainPos {
-  int64_t nchains, chain, pos, col, seg;
+  int nchains, chain, pos, col, seg;
 };
 template <class S>
 __device__ __forceinline__ ChainPos chain_pos(const ChainArgs<S>& a, int64_t k) {
   ChainPos p;
-  p.nchains = a.ncols * a.nseg;
-  p.chain = k % p.nchains;
-  p.pos = k / p.nchains;
-  p.col = p.chain % a.ncols;
-  p.seg = p.chain / a.ncols;
+  p.nchains = (int)(a.ncols * a.nseg);
+  const unsigned kk = (unsigned)k, nc = (unsigned)p.nchains;
+  p.pos = (int)(kk / nc);
+  p.chain = (int)(kk - (unsigned)p.pos * nc);
+  p.seg = (int)((unsigned)p.chain / (unsigned)a.ncols);
+  p.col = p.chain - p.seg * (int)a.ncols;
   return p;
 }
 // first row of the tile at chain position pos; REV walks each segment from
 // its last tile to its first
 template <bool REV, class S>
-__device__ __forceinline__ int64_t tile_row0(const ChainArgs<S>& a, const ChainPos& p, int L) {
-  return p.seg * a.tseg + (REV ? a.ntt - 1 - p.pos : p.pos) * (int64_t)L;
+__device__ __forceinline__ int tile_row0(const ChainArgs<S>& a, const ChainPos& p, int L) {
+  return p.seg * (int)a.tseg + (REV ? (int)a.ntt - 1 - p.pos : p.pos) * L;
 }
-// decay linking row t to row t+1 in the reverse scan (mu_t = lam_{t+1}),
-// except at the end of the sequence (lam_next, or 0) and at the end of a
-// non-final virtual segment (1: the link is applied by the carry fold)
+// Row after which the reverse scan's decay is 1 (the end of a non-final
+// virtual segment: that link is applied by the carry fold), or INT_MAX.
 template <class S>
-__device__ __forceinline__ int mu_kind(const ChainArgs<S>& a, int64_t t) {
-  if (t + 1 >= a.T) return 2;                          // lam_next / 0
-  if (a.nseg > 1 && (t + 1) % a.tseg == 0) return 1;   // 1
-  return 0;                                            // lam[t+1]
+__device__ __forceinline__ int vseg_end(const ChainArgs<S>& a, const ChainPos& p) {
+  return (a.nseg > 1 && p.seg < a.nseg - 1) ? (p.seg + 1) * (int)a.tseg : 0x7fffffff;
+}
+// decay linking row t to row t+1 in the reverse scan (mu_t = lam_{t+1}):
+// 2 = end of the sequence (lam_next, or 0), 1 = end of a virtual segment (1),
+// 0 = lam[t+1]
+__device__ __forceinline__ int mu_kind(int t, int T, int seg_end) {
+  return t + 1 >= T ? 2 : (t + 1 == seg_end ? 1 : 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -450,7 +455,7 @@ __device__ __forceinline__ void chain_coordinator(const ChainArgs<S>& a, const C
         TA[v] = mul_(s_wa[w][lane * VEC + v], TA[v]);
       }
     }
-    if (cp.pos == 0 && cp.seg == 0 && a.seed != nullptr && valid) {
+    if (cp.pos == 0 && cp.seg == (REV ? a.nseg - 1 : 0) && a.seed != nullptr && valid) {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) c[v] = a.seed[ch + v];
     }
@@ -499,14 +504,15 @@ k_chain_fwd(const ChainArgs<S> a, const ChainWs ws) {
   const int q = lane % Q, g = lane / Q;
   const int64_t ch = cp.col * CPW + (int64_t)q * VEC;
   const bool valid = ch < a.W;
-  const int64_t t0 = tile_row0<false>(a, cp, L) + (int64_t)(warp * G + g) * R;
+  const int t0 = tile_row0<false>(a, cp, L) + (warp * G + g) * R;
+  const int Ti = (int)a.T;
   const int64_t W = a.W;
 
   S l[R][VEC], xv[R][VEC];
 #pragma unroll
   for (int i = 0; i < R; ++i) {
-    const int64_t t = t0 + i;
-    if (valid && t < a.T) {
+    const int t = t0 + i;
+    if (valid && t < Ti) {
       IO::load_stream(a.a + t * W + ch, l[i]);
       IO::load_stream(a.b + t * W + ch, xv[i]);
     } else {
@@ -576,8 +582,8 @@ k_chain_fwd(const ChainArgs<S> a, const ChainWs ws) {
   for (int i = 0; i < R; ++i) {
 #pragma unroll
     for (int v = 0; v < VEC; ++v) cs[v] = fma_(l[i][v], cs[v], xv[i][v]);
-    const int64_t t = t0 + i;
-    if (valid && t < a.T) IO::store_stream(a.out0 + t * W + ch, cs);
+    const int t = t0 + i;
+    if (valid && t < Ti) IO::store_stream(a.out0 + t * W + ch, cs);
   }
 }
 
@@ -614,15 +620,16 @@ k_chain_bwd(const ChainArgs<S> a, const ChainWs ws) {
   const int q = lane % Q, g = lane / Q;
   const int64_t ch = cp.col * CPW + (int64_t)q * VEC;
   const bool valid = ch < a.W;
-  const int64_t t0 = tile_row0<true>(a, cp, L) + (int64_t)(warp * G + g) * R;
+  const int t0 = tile_row0<true>(a, cp, L) + (warp * G + g) * R;
+  const int Ti = (int)a.T, se = vseg_end(a, cp);
   const int64_t W = a.W, T = a.T;
 
   S mu[R][VEC], dh[R][VEC], hp[R][VEC];
 #pragma unroll
   for (int i = 0; i < R; ++i) {
-    const int64_t t = t0 + i;
-    if (valid && t < T) {
-      const int mk = mu_kind(a, t);
+    const int t = t0 + i;
+    if (valid && t < Ti) {
+      const int mk = mu_kind(t, Ti, se);
       if (mk == 0) {
         IO::load_stream(a.a + (t + 1) * W + ch, mu[i]);
       } else if (mk == 1) {
@@ -713,8 +720,8 @@ k_chain_bwd(const ChainArgs<S> a, const ChainWs ws) {
       cs[v] = fma_(mu[i][v], cs[v], dh[i][v]);
       dl[v] = mul_(hp[i][v], cs[v]);
     }
-    const int64_t t = t0 + i;
-    if (valid && t < T) {
+    const int t = t0 + i;
+    if (valid && t < Ti) {
       IO::store_stream(a.out0 + t * W + ch, cs);
       IO::store_stream(a.out1 + t * W + ch, dl);
       if (t == 0 && a.out2 != nullptr) {

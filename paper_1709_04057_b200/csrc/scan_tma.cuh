@@ -137,7 +137,7 @@ __device__ __forceinline__ void tma_coordinator(const SM& sm, const ChainArgs<S>
           TA[v] = mul_(ta[w * CPW + lane * VEC + v], TA[v]);
         }
       }
-      if (cp.pos == 0 && cp.seg == 0 && a.seed != nullptr && valid) {
+      if (cp.pos == 0 && cp.seg == (REV ? a.nseg - 1 : 0) && a.seed != nullptr && valid) {
 #pragma unroll
         for (int v = 0; v < VEC; ++v) c[v] = a.seed[ch + v];
       }
@@ -217,13 +217,14 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
     const ChainPos cp = chain_pos(a, (int64_t)k);
     const int64_t ch = cp.col * CPW + (int64_t)q * VEC;
     const bool valid = ch < W;
-    const int64_t t0 = tile_row0<false>(a, cp, L) + (int64_t)seg * R;
+    const int t0 = tile_row0<false>(a, cp, L) + seg * R;
+    const int Ti = (int)a.T;
     S l[R][VEC], xv[R][VEC];
     const S* sl = sm.arr(s, 0) + seg * R * CPW + q * VEC;
     const S* sx = sm.arr(s, 1) + seg * R * CPW + q * VEC;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      if (t0 + i < a.T) {
+      if (t0 + i < Ti) {
 #pragma unroll
         for (int v = 0; v < VEC; ++v) { l[i][v] = sl[i * CPW + v]; xv[i][v] = sx[i * CPW + v]; }
       } else {
@@ -291,8 +292,8 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
     for (int i = 0; i < R; ++i) {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) cs[v] = fma_(l[i][v], cs[v], xv[i][v]);
-      const int64_t t = t0 + i;
-      if (valid && t < a.T) IO::store_stream(a.out0 + t * W + ch, cs);
+      const int t = t0 + i;
+      if (valid && t < Ti) IO::store_stream(a.out0 + t * W + ch, cs);
     }
   }
 }
@@ -362,22 +363,23 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
     const ChainPos cp = chain_pos(a, (int64_t)k);
     const int64_t ch = cp.col * CPW + (int64_t)q * VEC;
     const bool valid = ch < W;
-    const int64_t t0 = tile_row0<true>(a, cp, L) + (int64_t)seg * R;
+    const int t0 = tile_row0<true>(a, cp, L) + seg * R;
+    const int Ti = (int)a.T, se = vseg_end(a, cp);
     S mu[R][VEC], dh[R][VEC], hp[R][VEC];
     const S* smu = sm.arr(s, 0) + seg * R * CPW + q * VEC;
     const S* sdh = sm.arr(s, 1) + seg * R * CPW + q * VEC;
     const S* shp = sm.arr(s, 2) + seg * R * CPW + q * VEC;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      const int64_t t = t0 + i;
-      if (t < T) {
+      const int t = t0 + i;
+      if (t < Ti) {
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
           mu[i][v] = smu[i * CPW + v];
           dh[i][v] = sdh[i * CPW + v];
           hp[i][v] = shp[i * CPW + v];
         }
-        const int mk = mu_kind(a, t);
+        const int mk = mu_kind(t, Ti, se);
         if (mk == 2) {  // zero-filled past the end; the segment form supplies lam_next
 #pragma unroll
           for (int v = 0; v < VEC; ++v) mu[i][v] = (a.lam_next != nullptr && valid) ? a.lam_next[ch + v] : S(0);
@@ -458,8 +460,8 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
         cs[v] = fma_(mu[i][v], cs[v], dh[i][v]);
         dl[v] = mul_(hp[i][v], cs[v]);
       }
-      const int64_t t = t0 + i;
-      if (valid && t < T) {
+      const int t = t0 + i;
+      if (valid && t < Ti) {
         IO::store_stream(a.out0 + t * W + ch, cs);
         IO::store_stream(a.out1 + t * W + ch, dl);
         if (t == 0 && a.out2 != nullptr) {
