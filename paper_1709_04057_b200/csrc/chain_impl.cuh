@@ -2,6 +2,8 @@
 // dtype/direction translation unit so nvcc compiles them in parallel).
 #pragma once
 
+#include <cstdlib>
+
 #include "launch.h"
 #include "scan_chained.cuh"
 
@@ -27,11 +29,21 @@ inline int pick_q(int64_t nvec) {
 
 // Virtual T-segments: few channel columns make each look-back chain long and
 // serial; splitting T into independent chains (stitched afterwards by a carry
-// fold + fix-up, segment.cu) restores parallelism.  Aim for >= 64 chains,
-// keeping >= 8 tiles per segment.
+// fold + fix-up, segment.cu) restores parallelism.  Aim for >= 64 chains
+// (LINREC_CHAINS overrides for tuning), keeping >= 8 tiles per segment.
+inline int64_t chain_target() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("LINREC_CHAINS");
+    const long n = e ? std::atol(e) : 0;
+    return (int64_t)(n > 0 ? n : 64);
+  }();
+  return v;
+}
+
 inline void choose_segments(ChainPlan& p, int64_t T) {
   const int64_t ntt_total = (T + p.rows - 1) / p.rows;
-  int64_t nseg = (64 + p.ncols - 1) / p.ncols;
+  const int64_t target = chain_target();
+  int64_t nseg = (target + p.ncols - 1) / p.ncols;
   if (nseg > ntt_total / 8) nseg = ntt_total / 8;
   if (nseg < 1) nseg = 1;
   const int64_t per = (ntt_total + nseg - 1) / nseg;

@@ -220,17 +220,15 @@ struct Lookback<float, VEC, Q, REC> {
     store_words<VEC>(ra, TA, tagg);
     store_words<VEC>(ra + REC, TB, tagg);
     // walk back: inclusive carry of j, or step over j once its aggregate is
-    // visible (one round trip per probe: both records are loaded together)
+    // visible
     SpinGuard guard;
     for (;;) {
       guard.tick();
       const uint64_t* ri = inc + (j * ncols + col) * 2 * REC + off;
+      if (load_words<VEC>(ri, c, tinc) && (!WANT_P || load_words<VEC>(ri + REC, P, tinc))) break;
       const uint64_t* rg = agg + (j * ncols + col) * 2 * REC + off;
       float a[VEC], b[VEC];
-      const bool oki = load_words<VEC>(ri, c, tinc) && (!WANT_P || load_words<VEC>(ri + REC, P, tinc));
-      const bool oka = load_words<VEC>(rg, a, tagg) & load_words<VEC>(rg + REC, b, tagg);
-      if (oki) break;
-      if (oka) --j;
+      if (load_words<VEC>(rg, a, tagg) & load_words<VEC>(rg + REC, b, tagg)) --j;
     }
     // apply the aggregates of j+1 .. pos-1, oldest first (all visible now)
 #pragma unroll 1

@@ -30,13 +30,18 @@ inline TmaChoice tma_choice(bool f64, bool fwd, int q) {
 }
 
 // Lanes across channels for the TMA kernels: as wide as W allows (128-bit
-// vectors, up to 32 lanes), but narrow enough that there are at least 8
-// independent channel columns -- few columns turn the look-back into one long
-// serial chain (the 1M-step, 128-channel regime).
+// vectors, up to 32 lanes); chain parallelism for narrow W comes from virtual
+// T-segments (choose_segments).  LINREC_NARROW_COLUMNS=1 restores the older
+// "at least 8 channel columns" rule for comparison.
 inline int pick_q_tma(int64_t nvec) {
-  int q = pick_q(nvec);
-  while (q > 4 && (nvec + q - 1) / q < 8) q >>= 1;
-  return q;
+  if (const char* e = std::getenv("LINREC_NARROW_COLUMNS")) {
+    if (std::atoi(e) > 0) {
+      int q = pick_q(nvec);
+      while (q > 4 && (nvec + q - 1) / q < 8) q >>= 1;
+      return q;
+    }
+  }
+  return pick_q(nvec);
 }
 
 inline int sm_count() {
