@@ -123,16 +123,19 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def traffic_from_profile():
+def traffic_from_profile(elements):
     """dram bytes per launch of the backward kernel from the committed
-    `ncu --set full` summary (profiles/), or None."""
+    `ncu --set full` summary (profiles/) when it was captured on this
+    workload (same element count), else None."""
     path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d["bwd"]["dram_bytes_per_launch"], d["bwd"].get("elements_per_launch")
+        if d["bwd"].get("elements_per_launch") != elements:
+            return None
+        return d["bwd"]["dram_bytes_per_launch"]
     except Exception:
-        return None, None
+        return None
 
 
 # ---------------------------------------------------------------------------
@@ -246,9 +249,7 @@ def run_ours(args):
     bwd_gbs = BWD_BYTES * N_local / (bwd_avg / 1e3) / 1e9
     step_gbs = (FWD_BYTES + BWD_BYTES) * N_local / (ms_step / 1e3) / 1e9 if not seq_sharded else \
         (FWD_BYTES + BWD_BYTES) * N_local / (ms_step / 1e3) / 1e9
-    traffic, traffic_el = traffic_from_profile()
-    if traffic is not None and traffic_el:
-        traffic = traffic * (N_local / traffic_el)
+    traffic = traffic_from_profile(N_local)
 
     result = None
     if rank == 0:
@@ -299,9 +300,12 @@ def run_ours(args):
     torch.cuda.empty_cache()
     if world > 1:
         dist.barrier()
+    e2e = None
+    if not args.no_e2e and not seq_sharded:
+        e2e = e2e_leg(args, T, B, D, local, world)
     if rank == 0:
-        if not args.no_e2e and not seq_sharded:
-            result["e2e"] = e2e_leg(args, T, B, D, local)
+        if e2e is not None:
+            result["e2e"] = e2e
         if not args.no_cpu and world == 1:
             result["cpu_baseline"] = cpu_baseline_leg(args, T, B, D)
         print(json.dumps(result), flush=True)
@@ -310,10 +314,12 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def e2e_leg(args, T, B, D, device):
-    """Same metric through the host-pointer C ABI from pinned host memory."""
+def e2e_leg(args, T, B, D, device, world=1):
+    """Same metric through the host-pointer C ABI from pinned host memory; at
+    N > 1 every rank runs its own block concurrently (max time over ranks)."""
     import numpy as np
     import torch
+    import torch.distributed as dist
     from paper_1709_04057_b200 import capi
 
     W = B * D
@@ -341,19 +347,26 @@ def e2e_leg(args, T, B, D, device):
     steps = max(1, min(args.steps, args.e2e_steps))
     for _ in range(max(1, min(args.warmup, 2))):
         step()
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         step()
     dt = (time.perf_counter() - t0) / steps
+    if world > 1:
+        t = torch.tensor([dt], device=torch.device("cuda", device))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = t.item()
     return {
-        "value": N / dt,
+        "value": world * N / dt,
         "unit": "elements/s",
         "ms_per_step": dt * 1e3,
         "steps": steps,
         "h2d_bytes_per_step": 4 * (2 * N + W) + 4 * (3 * N + W),  # fwd: lam, x, h0; bwd: lam, h, dh, h0
         "d2h_bytes_per_step": 4 * N + 4 * (2 * N + W),  # fwd: h; bwd: dlam, dx, dh0
         "api": "linrec_scan_host_f32 + linrec_scan_backward_host_f32 (the numpy boundary of linrec.scan / linrec.scan_backward), pinned buffers",
-        "timing": "host wall clock, synchronous calls",
+        "timing": "host wall clock, synchronous calls, max over ranks",
+        "ranks": world,
     }
 
 
