@@ -362,8 +362,9 @@ def e2e_leg(args, T, B, D, device, world=1):
         "unit": "elements/s",
         "ms_per_step": dt * 1e3,
         "steps": steps,
-        "h2d_bytes_per_step": 4 * (2 * N + W) + 4 * (3 * N + W),  # fwd: lam, x, h0; bwd: lam, h, dh, h0
-        "d2h_bytes_per_step": 4 * N + 4 * (2 * N + W),  # fwd: h; bwd: dlam, dx, dh0
+        # per rank x ranks; fwd: lam, x, h0 in / h out; bwd: lam, h, dh, h0 in / dlam, dx, dh0 out
+        "h2d_bytes_per_step": world * (4 * (2 * N + W) + 4 * (3 * N + W)),
+        "d2h_bytes_per_step": world * (4 * N + 4 * (2 * N + W)),
         "api": "linrec_scan_host_f32 + linrec_scan_backward_host_f32 (the numpy boundary of linrec.scan / linrec.scan_backward), pinned buffers",
         "timing": "host wall clock, synchronous calls, max over ranks",
         "ranks": world,
