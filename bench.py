@@ -147,8 +147,16 @@ def run_ours(args):
     from paper_1709_04057_b200 import capi
 
     world, rank, local = dist_env()
+    # LINREC_BENCH_SHARE_GPU=1 (tests only): ranks share the visible GPUs and
+    # talk over gloo, to exercise the N > 1 code paths on a 1-GPU box.
+    share = os.environ.get("LINREC_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % max(1, torch.cuda.device_count())
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     wl = WORKLOADS[args.workload]
@@ -235,7 +243,7 @@ def run_ours(args):
     fwd_ms = [e[0].elapsed_time(e[1]) for e in ev]
     bwd_ms = [e[1].elapsed_time(e[2]) for e in ev]
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
+        t = torch.tensor([total_ms], device="cpu" if share else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = t.item()
     ms_step = total_ms / args.steps
@@ -302,7 +310,7 @@ def run_ours(args):
         dist.barrier()
     e2e = None
     if not args.no_e2e and not seq_sharded:
-        e2e = e2e_leg(args, T, B, D, local, world)
+        e2e = e2e_leg(args, T, B, D, local, world, share)
     if rank == 0:
         if e2e is not None:
             result["e2e"] = e2e
@@ -314,7 +322,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def e2e_leg(args, T, B, D, device, world=1):
+def e2e_leg(args, T, B, D, device, world=1, share=False):
     """Same metric through the host-pointer C ABI from pinned host memory; at
     N > 1 every rank runs its own block concurrently (max time over ranks)."""
     import numpy as np
@@ -354,7 +362,7 @@ def e2e_leg(args, T, B, D, device, world=1):
         step()
     dt = (time.perf_counter() - t0) / steps
     if world > 1:
-        t = torch.tensor([dt], device=torch.device("cuda", device))
+        t = torch.tensor([dt], device="cpu" if share else torch.device("cuda", device))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = t.item()
     return {

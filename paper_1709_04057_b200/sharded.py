@@ -136,8 +136,16 @@ class SequenceShardedScan:
 
     # -- collectives -----------------------------------------------------------
     def _all_gather(self, local, out):
-        if hasattr(dist, "all_gather_into_tensor") and dist.get_backend(self.group) == "nccl":
+        """all_gather of a small [..] tensor into out[world, ..]: NCCL over
+        NVLink on device buffers; gloo (CPU tests, or several ranks sharing
+        one GPU in tests) through host copies."""
+        if dist.get_backend(self.group) == "nccl":
             dist.all_gather_into_tensor(out.view(-1), local.reshape(-1), group=self.group)
+            return
+        if local.is_cuda:
+            parts = [torch.empty_like(local, device="cpu") for _ in range(self.world)]
+            dist.all_gather(parts, local.cpu(), group=self.group)
+            out.copy_(torch.stack(parts).to(out.device))
         else:
             parts = list(out.unbind(0))
             dist.all_gather(parts, local, group=self.group)

@@ -1,0 +1,81 @@
+"""Sequence sharding through the CUDA kernels with REAL ranks: 2 or 3
+processes share the one GPU of the test box and exchange carries over gloo
+(host-staged all-gather), running paper_1709_04057_b200.sharded exactly as
+bench.py does with NCCL on a multi-GPU box.  Checked against the oracle."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from conftest import ROOT  # noqa: E402
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, T, W, lo, hi, seed, q):
+    import sys
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1709_04057_b200.sharded import SequenceShardedScan, segment_bounds
+        torch.cuda.set_device(0)
+        rng = np.random.default_rng(seed)
+        lam = rng.uniform(lo, hi, (T, W)).astype(np.float32)
+        x = rng.uniform(-1, 1, (T, W)).astype(np.float32)
+        h0 = rng.uniform(-1, 1, (W,)).astype(np.float32)
+        dh = rng.uniform(-1, 1, (T, W)).astype(np.float32)
+        s, e = segment_bounds(T, world, rank)
+        cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+        L, X, DH, H0 = cu(lam[s:e]), cu(x[s:e]), cu(dh[s:e]), cu(h0)
+        H, DL, DX, DH0 = torch.empty_like(L), torch.empty_like(L), torch.empty_like(L), torch.zeros_like(H0)
+        run = SequenceShardedScan(T, W, stream=torch.cuda.current_stream())
+        run.forward(L, X, H0, H)
+        run.backward(L, H0, H, DH, DL, DX, DH0)
+        torch.cuda.synchronize()
+        q.put((rank, s, e, H.cpu().numpy(), DL.cpu().numpy(), DX.cpu().numpy(), DH0.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,T,W,lo,hi", [(2, 40000, 128, 0.05, 0.95), (3, 30001, 64, 0.99, 1.0),
+                                             (2, 5000, 12, -1.0, 1.0)])
+def test_sequence_sharded_ranks_on_gpu(oracle, world, T, W, lo, hi):
+    import torch.multiprocessing as mp
+    from oracle.oracle import max_rel_error
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    seed = T + W
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, T, W, lo, hi, seed, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(seed)
+    lam = rng.uniform(lo, hi, (T, W)).astype(np.float32)
+    x = rng.uniform(-1, 1, (T, W)).astype(np.float32)
+    h0 = rng.uniform(-1, 1, (W,)).astype(np.float32)
+    dh = rng.uniform(-1, 1, (T, W)).astype(np.float32)
+    h_wide = oracle.scan_serial_wide(lam, x, h0)
+    h_ref = oracle.scan_serial(lam, x, h0)
+    g = oracle.scan_backward_wide(lam, h0, h_ref, dh)
+    for rank, s, e, H, DL, DX, DH0 in outs:
+        assert max_rel_error(H, h_wide[s:e]) <= 1e-5, rank
+        assert max_rel_error(DL, g[0][s:e]) <= 1e-5, rank
+        assert max_rel_error(DX, g[1][s:e]) <= 1e-5, rank
+        if rank == 0:
+            assert max_rel_error(DH0, g[2]) <= 1e-5
