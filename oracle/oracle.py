@@ -186,6 +186,63 @@ class Oracle:
             _ptr(lam), _ptr(h0), _ptr(h), _ptr(dh), _ptr(dlam), _ptr(dx), _ptr(dh0), T, W)
         return dlam, dx, dh0
 
+    # -- GILR / GILR-LSTM layers (oracle/linrec_layers.c) -----------------------
+    def _layer_fns(self, dt):
+        sfx = _sfx(dt)
+        lib = self.lib
+        if not getattr(self, f"_layers_{sfx}", False):
+            getattr(lib, f"oracle_gilr_forward_{sfx}").argtypes = [_vp] * 6 + [C.c_int] + [_vp] * 3 + [_i64] * 4
+            getattr(lib, f"oracle_gilr_backward_{sfx}").argtypes = [_vp] * 4 + [C.c_int] + [_vp] * 10 + [_i64] * 4
+            getattr(lib, f"oracle_gilr_lstm_forward_{sfx}").argtypes = [_vp] * 16 + [_i64] * 4
+            getattr(lib, f"oracle_gilr_lstm_backward_{sfx}").argtypes = [_vp] * 23 + [_i64] * 4
+            setattr(self, f"_layers_{sfx}", True)
+        return sfx
+
+    def gilr_lstm_forward(self, P, x, htil0=None, c0=None):
+        """layers.hpp:245-293.  P: dict sU, sV, sbg, sbz, U, V, bias.
+        Returns h and the cache dict (sg, si, htil, gates, c)."""
+        x = np.ascontiguousarray(x)
+        dt = x.dtype
+        sfx = self._layer_fns(dt)
+        T, b, m = x.shape
+        n = P["U"].shape[1]
+        P = {k: np.ascontiguousarray(v, dtype=dt) for k, v in P.items()}
+        z = np.zeros((b, n), dt)
+        htil0 = z if htil0 is None else np.ascontiguousarray(htil0, dtype=dt)
+        c0 = z if c0 is None else np.ascontiguousarray(c0, dtype=dt)
+        h = np.empty((T, b, n), dt)
+        cache = {"sg": np.empty((T, b, n), dt), "si": np.empty((T, b, n), dt), "htil": np.empty((T, b, n), dt),
+                 "gates": np.empty((T, b, 4 * n), dt), "c": np.empty((T, b, n), dt)}
+        getattr(self.lib, f"oracle_gilr_lstm_forward_{sfx}")(
+            _ptr(x), _ptr(P["sU"]), _ptr(P["sV"]), _ptr(P["sbg"]), _ptr(P["sbz"]), _ptr(P["U"]), _ptr(P["V"]),
+            _ptr(P["bias"]), _ptr(htil0), _ptr(c0), _ptr(h), _ptr(cache["sg"]), _ptr(cache["si"]),
+            _ptr(cache["htil"]), _ptr(cache["gates"]), _ptr(cache["c"]), T, b, m, n)
+        return h, cache
+
+    def gilr_lstm_backward(self, P, x, htil0, c0, cache, dh):
+        """layers.hpp:295-375.  Returns (grads dict, dx, dhtil0, dc0); the
+        parameter gradients start at zero (the reference accumulates)."""
+        x = np.ascontiguousarray(x)
+        dt = x.dtype
+        sfx = self._layer_fns(dt)
+        T, b, m = x.shape
+        n = P["U"].shape[1]
+        P = {k: np.ascontiguousarray(v, dtype=dt) for k, v in P.items()}
+        z = np.zeros((b, n), dt)
+        htil0 = z if htil0 is None else np.ascontiguousarray(htil0, dtype=dt)
+        c0 = z if c0 is None else np.ascontiguousarray(c0, dtype=dt)
+        dh = np.ascontiguousarray(dh, dtype=dt)
+        g = {k: np.zeros_like(v) for k, v in P.items()}
+        dx = np.empty((T, b, m), dt)
+        dhtil0 = np.empty((b, n), dt)
+        dc0 = np.empty((b, n), dt)
+        getattr(self.lib, f"oracle_gilr_lstm_backward_{sfx}")(
+            _ptr(x), _ptr(P["sU"]), _ptr(P["sV"]), _ptr(P["U"]), _ptr(P["V"]), _ptr(htil0), _ptr(c0),
+            _ptr(cache["sg"]), _ptr(cache["si"]), _ptr(cache["htil"]), _ptr(cache["gates"]), _ptr(cache["c"]),
+            _ptr(dh), _ptr(g["sU"]), _ptr(g["sV"]), _ptr(g["sbg"]), _ptr(g["sbz"]), _ptr(g["U"]), _ptr(g["V"]),
+            _ptr(g["bias"]), _ptr(dx), _ptr(dhtil0), _ptr(dc0), T, b, m, n)
+        return g, dx, dhtil0, dc0
+
     def first_nonfinite(self, a):
         a = np.ascontiguousarray(a)
         return int(getattr(self.lib, f"oracle_first_nonfinite_{_sfx(a.dtype)}")(_ptr(a), a.size))
@@ -236,6 +293,8 @@ class RefLib:
         lib.ref_rng_first.argtypes = [C.c_uint64, C.c_int]
         lib.ref_hardware_workers.restype = C.c_int
         lib.ref_bench_fwd_bwd_f32.argtypes = [_vp] * 4 + [_i64] * 3 + [C.c_int] * 3 + [_vp, _vp]
+        lib.ref_gilr_lstm_oracle.argtypes = [_vp] * 11 + [_i64] * 4
+        lib.ref_gilr_oracle.argtypes = [_vp] * 7 + [_i64] * 4
 
     def _check(self, rc):
         if rc != 0:
@@ -290,6 +349,19 @@ class RefLib:
             C.byref(f), C.byref(bw)))
         return f.value, bw.value
 
+    def gilr_lstm_oracle(self, P, x, htil0, c0):
+        """The reference's per-step GILR-LSTM (layer_oracles.hpp:52-82), fp64."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        T, b, m = x.shape
+        n = P["U"].shape[1]
+        P = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in P.items()}
+        h = np.empty((T, b, n))
+        self._check(self.lib.ref_gilr_lstm_oracle(
+            _ptr(x), _ptr(P["sU"]), _ptr(P["sV"]), _ptr(P["sbg"]), _ptr(P["sbz"]), _ptr(P["U"]), _ptr(P["V"]),
+            _ptr(P["bias"]), _ptr(np.ascontiguousarray(htil0, dtype=np.float64)),
+            _ptr(np.ascontiguousarray(c0, dtype=np.float64)), _ptr(h), T, b, m, n))
+        return h
+
     def hardware_workers(self):
         return int(self.lib.ref_hardware_workers())
 
@@ -305,3 +377,15 @@ def load_reference_module():
     mod = importlib.util.module_from_spec(spec)
     loader.exec_module(mod)
     return mod
+
+
+def gilr_lstm_params(rng, m, n, dtype=np.float64, gate_bias=1.0):
+    """Random GILR-LSTM parameters shaped like gilr_lstm_init (layers.hpp:165-175):
+    U ~ U(+-1/sqrt(n)), V ~ U(+-1/sqrt(m)), gate bias on the f block."""
+    sm, sn = 1.0 / np.sqrt(m), 1.0 / np.sqrt(n)
+    bias = np.zeros(4 * n)
+    bias[:n] = gate_bias
+    P = {"sU": rng.uniform(-sm, sm, (n, m)), "sV": rng.uniform(-sm, sm, (n, m)),
+         "sbg": np.full(n, gate_bias), "sbz": np.zeros(n),
+         "U": rng.uniform(-sn, sn, (4 * n, n)), "V": rng.uniform(-sm, sm, (4 * n, m)), "bias": bias}
+    return {k: v.astype(dtype) for k, v in P.items()}

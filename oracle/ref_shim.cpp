@@ -17,6 +17,7 @@
 
 #include "linrec/recurrence.hpp"
 #include "linrec/rng.hpp"
+#include "support/layer_oracles.hpp"  // proj/tests/support: per-step layer oracles
 
 namespace {
 thread_local std::string g_err;
@@ -167,6 +168,59 @@ int ref_bench_fwd_bwd_f32(const float* lam, const float* x, const float* h0,
     }
     *fwd_s = median(tf);
     *bwd_s = median(tb);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// The reference's per-step GILR / GILR-LSTM oracles
+// (proj/tests/support/layer_oracles.hpp:28-82, fp64).  Parameters row-major
+// as GilrParams / GilrLstmParams (layers.hpp:28-40, :148-165).
+static linrec::Tensor2<double> t2d(const double* p, int64_t r, int64_t c) {
+  linrec::Tensor2<double> t(r, c);
+  std::copy(p, p + r * c, t.data.begin());
+  return t;
+}
+int ref_gilr_lstm_oracle(const double* x, const double* sU, const double* sV, const double* sbg,
+                         const double* sbz, const double* U, const double* V, const double* bias,
+                         const double* htil0, const double* c0, double* h, int64_t T, int64_t b,
+                         int64_t m, int64_t n) {
+  try {
+    linrec::GilrLstmParams<double> p;
+    p.surrogate.U = t2d(sU, n, m);
+    p.surrogate.V = t2d(sV, n, m);
+    p.surrogate.b_g = t2d(sbg, 1, n);
+    p.surrogate.b_z = t2d(sbz, 1, n);
+    p.surrogate.act = linrec::Activation::Tanh;
+    p.U = t2d(U, 4 * n, n);
+    p.V = t2d(V, 4 * n, m);
+    p.bias = t2d(bias, 1, 4 * n);
+    auto X = t3(x, T, b, m);
+    auto H0 = t2(htil0, b, n);
+    auto C0 = t2(c0, b, n);
+    auto out = oracle::gilr_lstm(p, X, H0, C0);
+    std::copy(out.data.begin(), out.data.end(), h);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+int ref_gilr_oracle(const double* x, const double* U, const double* V, const double* bg, const double* bz,
+                    const double* h0, double* h, int64_t T, int64_t b, int64_t m, int64_t n) {
+  try {
+    linrec::GilrParams<double> p;
+    p.U = t2d(U, n, m);
+    p.V = t2d(V, n, m);
+    p.b_g = t2d(bg, 1, n);
+    p.b_z = t2d(bz, 1, n);
+    p.act = linrec::Activation::Tanh;
+    auto X = t3(x, T, b, m);
+    auto H0 = t2(h0, b, n);
+    auto out = oracle::gilr(p, X, H0);
+    std::copy(out.data.begin(), out.data.end(), h);
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();
