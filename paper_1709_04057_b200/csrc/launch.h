@@ -111,4 +111,33 @@ cudaError_t launch_compose(const S* aggs, int64_t first, int64_t last, int64_t s
 template <class S>
 cudaError_t first_nonfinite(const S* v, int64_t n, int64_t* index, cudaStream_t st);
 
+// tcgen05 TF32 GEMM (gemm_tc.cu): C[M][N] = sum_k A(m,k) B(n,k) with the
+// K range optionally split over two operand pairs.  K-major operands are
+// [rows][K] with pitch lda (elements), MN-major ones [K][rows].
+struct GemmOperands {
+  const float* a1 = nullptr;
+  const float* b1 = nullptr;
+  int64_t K1 = 0, lda1 = 0, ldb1 = 0;
+  const float* a2 = nullptr;
+  const float* b2 = nullptr;
+  int64_t K2 = 0, lda2 = 0, ldb2 = 0;
+  int64_t M = 0, N = 0;
+  bool a_mn = false, b_mn = false;
+};
+struct GemmEpilogue {
+  float* C = nullptr;
+  int64_t ldc = 0;
+  bool accumulate = false;
+  int k_splits = 1;
+  float* scratch = nullptr;  // split-K partials, k_splits * M * N floats
+  const float* bias = nullptr;
+  float* o0 = nullptr;
+  float* o1 = nullptr;
+  float* o2 = nullptr;
+  float* o3 = nullptr;
+  int64_t ldo = 0;
+};
+cudaError_t gemm_tf32(const GemmOperands& op, int epi, const GemmEpilogue& ep, cudaStream_t st);
+int gemm_splits_for(int64_t M, int64_t N, int64_t K);
+
 }  // namespace linrec_impl
