@@ -231,16 +231,24 @@ int linrec_segment_fixup_backward_f64(const double* lam, const double* hprev, co
                                       double* dlam, double* dx, int64_t T, int64_t W, int64_t tile_rows,
                                       void* stream);
 
-/* ---- layer building block: tcgen05 TF32 GEMM ---------------------------- *
+/* ---- layer building block: tcgen05 GEMM ---------------------------------- *
  * C[M][N] (row-major, pitch ldc) (+)= sum_k A(m,k) * B(n,k) on the sm_100a
- * tensor cores (kind::tf32, fp32 accumulate in TMEM).  A is K-major
+ * tensor cores (kind::tf32 MMAs, fp32 accumulate in TMEM).  A is K-major
  * ([M][K], pitch lda) when a_mn == 0, MN-major ([K][M], pitch lda) when 1;
- * likewise B.  k_splits > 1 splits K across CTAs and reduces the partials
- * (scratch: k_splits*M*N floats) in a fixed order.  The dense transforms of
- * the reference's layers (tensor.hpp:104-141 gemm_nn/nt/tn) map onto it. */
-int linrec_gemm_tf32(const float* A, int a_mn, int64_t lda, const float* B, int b_mn, int64_t ldb, float* C,
-                     int64_t ldc, int64_t M, int64_t N, int64_t K, int accumulate, int k_splits, float* scratch,
-                     void* stream);
+ * likewise B.  precision LINREC_PREC_FP32 runs 3xTF32 (hi/lo operand split,
+ * fp32-grade results), LINREC_PREC_TF32 one TF32 pass.  k_splits > 1 splits
+ * K across CTAs and reduces the partials (scratch: k_splits*M*N floats) in a
+ * fixed order (deterministic).  Pitches and pointers must be 16-byte
+ * aligned.  The dense transforms of the reference's layers
+ * (tensor.hpp:104-141 gemm_nn/nt/tn, :249-308) map onto it. */
+#define LINREC_PREC_FP32 0
+#define LINREC_PREC_TF32 1
+int linrec_gemm_f32(const float* A, int a_mn, int64_t lda, const float* B, int b_mn, int64_t ldb, float* C,
+                    int64_t ldc, int64_t M, int64_t N, int64_t K, int accumulate, int precision, int k_splits,
+                    float* scratch, void* stream);
+/* split count linrec_gemm_f32 would pick for an M x N x K product (fills the
+ * persistent grid); scratch for it is k_splits*M*N floats. */
+int linrec_gemm_splits(int64_t M, int64_t N, int64_t K);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

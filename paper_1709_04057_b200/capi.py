@@ -64,8 +64,9 @@ def _load():
         getattr(lib, f"linrec_compose_carries_{s}").argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp]
         getattr(lib, f"linrec_segment_fixup_{s}").argtypes = [_vp] * 4 + [_i64, _i64, _i64, _vp]
         getattr(lib, f"linrec_segment_fixup_backward_{s}").argtypes = [_vp] * 8 + [_i64, _i64, _i64, _vp]
-    lib.linrec_gemm_tf32.argtypes = [_vp, _int, _i64, _vp, _int, _i64, _vp, _i64, _i64, _i64, _i64, _int, _int,
-                                     _vp, _vp]
+    lib.linrec_gemm_f32.argtypes = [_vp, _int, _i64, _vp, _int, _i64, _vp, _i64, _i64, _i64, _i64, _int, _int,
+                                    _int, _vp, _vp]
+    lib.linrec_gemm_splits.argtypes = [_i64, _i64, _i64]
     lib.linrec_segment_prod_rows.restype = _i64
     lib.linrec_segment_prod_rows.argtypes = [_i64, _i64, _int, _int]
     lib.linrec_segment_tile_rows.restype = _i64
@@ -167,10 +168,19 @@ def segment_fixup_backward(lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T,
         lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T, W, tile_rows, stream))
 
 
-def gemm_tf32(A, a_mn, lda, B, b_mn, ldb, C, ldc, M, N, K, accumulate=False, k_splits=1, scratch=None, stream=0):
-    """tcgen05 TF32 GEMM (device pointers), see include/linrec_cuda.h."""
-    check(lib.linrec_gemm_tf32(A, int(a_mn), lda, B, int(b_mn), ldb, C, ldc, M, N, K, int(accumulate), k_splits,
-                               scratch, stream))
+PREC_FP32 = 0
+PREC_TF32 = 1
+
+
+def gemm(A, a_mn, lda, B, b_mn, ldb, C, ldc, M, N, K, accumulate=False, precision=PREC_FP32, k_splits=1,
+         scratch=None, stream=0):
+    """tcgen05 GEMM (device pointers), see include/linrec_cuda.h."""
+    check(lib.linrec_gemm_f32(A, int(a_mn), lda, B, int(b_mn), ldb, C, ldc, M, N, K, int(accumulate), precision,
+                              k_splits, scratch, stream))
+
+
+def gemm_splits(M, N, K) -> int:
+    return int(lib.linrec_gemm_splits(M, N, K))
 
 
 class Workspace:

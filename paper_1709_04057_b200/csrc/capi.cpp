@@ -790,14 +790,19 @@ int linrec_compose_carries_f64(const double* aggs, int64_t first, int64_t last, 
                                                       static_cast<cudaStream_t>(stream)));
   return LINREC_OK;
 }
-int linrec_gemm_tf32(const float* A, int a_mn, int64_t lda, const float* B, int b_mn, int64_t ldb, float* C,
-                     int64_t ldc, int64_t M, int64_t N, int64_t K, int accumulate, int k_splits, float* scratch,
-                     void* stream) {
+int linrec_gemm_f32(const float* A, int a_mn, int64_t lda, const float* B, int b_mn, int64_t ldb, float* C,
+                    int64_t ldc, int64_t M, int64_t N, int64_t K, int accumulate, int precision, int k_splits,
+                    float* scratch, void* stream) {
   int rc;
   if ((rc = check_ptr(A, "A")) || (rc = check_ptr(B, "B")) || (rc = check_ptr(C, "C"))) return rc;
   if (M < 1 || N < 1 || K < 1) return fail(LINREC_ERR_SHAPE, "gemm: M, N, K must be >= 1");
+  if (M >= (int64_t(1) << 31) || N >= (int64_t(1) << 31)) return fail(LINREC_ERR_SHAPE, "gemm: M, N must be < 2^31");
+  if (precision != LINREC_PREC_FP32 && precision != LINREC_PREC_TF32)
+    return fail(LINREC_ERR_VALUE, "gemm: precision must be LINREC_PREC_FP32 or LINREC_PREC_TF32");
   if ((lda * 4) % 16 || (ldb * 4) % 16 || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
     return fail(LINREC_ERR_VALUE, "gemm: operand pitches and pointers must be 16-byte aligned");
+  if ((ldc * 4) % 16 || (reinterpret_cast<uintptr_t>(C) & 15))
+    return fail(LINREC_ERR_VALUE, "gemm: C pitch and pointer must be 16-byte aligned");
   linrec_impl::GemmOperands op;
   op.a1 = A;
   op.b1 = B;
@@ -805,18 +810,21 @@ int linrec_gemm_tf32(const float* A, int a_mn, int64_t lda, const float* B, int 
   op.lda1 = lda;
   op.ldb1 = ldb;
   op.M = M;
-  op.N = N;
+  op.units = N;
   op.a_mn = a_mn != 0;
   op.b_mn = b_mn != 0;
   linrec_impl::GemmEpilogue ep;
   ep.C = C;
   ep.ldc = ldc;
   ep.accumulate = accumulate != 0;
+  ep.split3 = precision == LINREC_PREC_FP32;
   ep.k_splits = k_splits < 1 ? 1 : k_splits;
   ep.scratch = scratch;
   if (ep.k_splits > 1 && scratch == nullptr) return fail(LINREC_ERR_VALUE, "gemm: split-K needs scratch");
   LINREC_CUDA_TRY(linrec_impl::gemm_tf32(op, 0, ep, static_cast<cudaStream_t>(stream)));
   return LINREC_OK;
 }
+
+int linrec_gemm_splits(int64_t M, int64_t N, int64_t K) { return linrec_impl::gemm_splits_for(M, N, K); }
 
 }  // extern "C"

@@ -1,19 +1,22 @@
-// Host side of the tcgen05 TF32 GEMM (gemm_tc.cuh): tensor maps, launch,
-// deterministic split-K reduction.
+// Host side of the tcgen05 GEMM (gemm_tc.cuh): tensor maps, persistent
+// launch, split-K planning and the deterministic split-K reduction.
 #include <cstdio>
 
 #include "gemm_tc.cuh"
 #include "launch.h"
-#include "tma_impl.cuh"
 
 namespace linrec_impl {
 
 namespace {
 
-// 2-D fp32 tensor map with a 128-byte swizzle: `inner` contiguous elements,
-// `outer` rows at `pitch` elements; box {32, box_outer}.
-cudaError_t make_tmap_sw128(CUtensorMap* map, const float* ptr, int64_t inner, int64_t outer, int64_t pitch,
-                            int box_outer) {
+using linrec_dev::tc::BK;
+using linrec_dev::tc::BM;
+
+// 2-D fp32 tensor map: `inner` contiguous elements, `outer` rows at `pitch`
+// elements; box {32, box_outer}.  swizzle: 128B (K-major operands) or
+// 128B with 32-byte atoms (MN-major tf32 operands).
+cudaError_t make_tmap(CUtensorMap* map, const float* ptr, int64_t inner, int64_t outer, int64_t pitch, int box_outer,
+                      CUtensorMapSwizzle swz) {
   using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                           CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -31,16 +34,17 @@ cudaError_t make_tmap_sw128(CUtensorMap* map, const float* ptr, int64_t inner, i
   const cuuint32_t box[2] = {32u, (cuuint32_t)box_outer};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-// Operand map: K-major [rows][K] (pitch >= K) or MN-major [K][rows].
+// Operand map: K-major [rows][K] (pitch >= K), box {32 k, tile_rows}, or
+// MN-major [K][rows], box {32 rows, BK k}.
 cudaError_t operand_map(CUtensorMap* map, const float* p, bool mn, int64_t rows, int64_t K, int64_t pitch,
                         int tile_rows) {
-  if (mn) return make_tmap_sw128(map, p, rows, K, pitch, linrec_dev::tc::BK);
-  return make_tmap_sw128(map, p, K, rows, pitch, tile_rows);
+  if (mn) return make_tmap(map, p, rows, K, pitch, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  return make_tmap(map, p, K, rows, pitch, tile_rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 __global__ void k_splitk_reduce(const float* __restrict__ part, int splits, int64_t MN, int64_t N, int64_t ldc,
@@ -54,98 +58,125 @@ __global__ void k_splitk_reduce(const float* __restrict__ part, int splits, int6
   }
 }
 
-template <bool A_MN, bool B_MN, int BN, int STAGES, int EPI>
-cudaError_t launch_cfg(const GemmOperands& op, const linrec_dev::tc::GemmParams& p, int k_splits,
-                       cudaStream_t st) {
-  using Cfg = linrec_dev::tc::GemmCfg<A_MN, B_MN, BN, STAGES>;
+int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+template <bool A_MN, bool B_MN, int NB, bool SPLIT3, int EPI>
+cudaError_t launch_cfg(const GemmOperands& op, linrec_dev::tc::GemmParams p, cudaStream_t st) {
+  constexpr int BN = 128;
+  constexpr int STAGES = SPLIT3 ? 3 : 6;
+  using Cfg = linrec_dev::tc::GemmCfg<A_MN, B_MN, BN, NB, STAGES, SPLIT3>;
+  constexpr int UNITS = Cfg::UNITS;
+  const int64_t b_rows = NB == 1 ? op.units : (NB - 1) * op.b_bstride + op.units;
   CUtensorMap a1, b1, a2, b2;
   cudaError_t e;
-  if ((e = operand_map(&a1, op.a1, A_MN, op.M, op.K1, op.lda1, linrec_dev::tc::BM)) != cudaSuccess) return e;
-  if ((e = operand_map(&b1, op.b1, B_MN, op.N, op.K1, op.ldb1, BN)) != cudaSuccess) return e;
+  if ((e = operand_map(&a1, op.a1, A_MN, op.M, op.K1, op.lda1, BM)) != cudaSuccess) return e;
+  if ((e = operand_map(&b1, op.b1, B_MN, b_rows, op.K1, op.ldb1, UNITS)) != cudaSuccess) return e;
   if (op.a2 != nullptr) {
-    if ((e = operand_map(&a2, op.a2, A_MN, op.M, op.K2, op.lda2, linrec_dev::tc::BM)) != cudaSuccess) return e;
-    if ((e = operand_map(&b2, op.b2, B_MN, op.N, op.K2, op.ldb2, BN)) != cudaSuccess) return e;
+    if ((e = operand_map(&a2, op.a2, A_MN, op.M, op.K2, op.lda2, BM)) != cudaSuccess) return e;
+    if ((e = operand_map(&b2, op.b2, B_MN, b_rows, op.K2, op.ldb2, UNITS)) != cudaSuccess) return e;
   } else {
     a2 = a1;
     b2 = b1;
   }
-  auto kern = linrec_dev::tc::k_gemm_tf32<A_MN, B_MN, BN, STAGES, EPI>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-  const dim3 grid((unsigned)((op.N + BN - 1) / BN), (unsigned)((op.M + 127) / 128), (unsigned)k_splits);
-  kern<<<grid, 256, Cfg::SMEM, st>>>(a1, b1, a2, b2, p);
+  p.ntm = (int)((op.M + BM - 1) / BM);
+  p.ntn = (int)((op.units + UNITS - 1) / UNITS);
+  p.b_bstride = (int)op.b_bstride;
+  auto kern = linrec_dev::tc::k_gemm<A_MN, B_MN, BN, NB, STAGES, SPLIT3, EPI>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (int64_t)p.ntm * p.ntn * p.nz;
+  const int grid = (int)(ntiles < sm_count() ? ntiles : sm_count());
+  kern<<<grid, linrec_dev::tc::kThreads, Cfg::SMEM, st>>>(a1, b1, a2, b2, p);
   return cudaGetLastError();
+}
+
+template <bool SPLIT3>
+cudaError_t dispatch(const GemmOperands& op, int epi, const linrec_dev::tc::GemmParams& p, cudaStream_t st) {
+  using namespace linrec_dev::tc;
+  if (epi == kEpiPlain) {
+    if (op.nb != 1) return cudaErrorInvalidValue;
+    if (!op.a_mn && !op.b_mn) return launch_cfg<false, false, 1, SPLIT3, kEpiPlain>(op, p, st);
+    if (!op.a_mn && op.b_mn) return launch_cfg<false, true, 1, SPLIT3, kEpiPlain>(op, p, st);
+    if (op.a_mn && op.b_mn) return launch_cfg<true, true, 1, SPLIT3, kEpiPlain>(op, p, st);
+    return launch_cfg<true, false, 1, SPLIT3, kEpiPlain>(op, p, st);
+  }
+  if (op.a_mn || op.b_mn) return cudaErrorInvalidValue;
+  if (epi == kEpiGilr && op.nb == 2) return launch_cfg<false, false, 2, SPLIT3, kEpiGilr>(op, p, st);
+  if (epi == kEpiGates && op.nb == 4) return launch_cfg<false, false, 4, SPLIT3, kEpiGates>(op, p, st);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
+int gemm_splits_for(int64_t M, int64_t N, int64_t K) {
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + 127) / 128);
+  const int64_t kb = (K + BK - 1) / BK;
+  const int64_t sms = sm_count();
+  if (tiles >= sms || kb < 8) return 1;
+  // fill the persistent grid evenly: the split count whose last wave is
+  // fullest, preferring fewer partials, with >= 4 k-blocks per split
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= 32 && s <= kb / 4; ++s) {
+    const double waves = double(tiles * s) / double(sms);
+    const double eff = waves / double((tiles * s + sms - 1) / sms);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return best;
+}
+
 cudaError_t gemm_tf32(const GemmOperands& op, int epi, const GemmEpilogue& ep, cudaStream_t st) {
-  using linrec_dev::tc::BK;
   const int kb1 = (int)((op.K1 + BK - 1) / BK);
   const int kb2 = op.a2 != nullptr ? (int)((op.K2 + BK - 1) / BK) : 0;
   const int kb_total = kb1 + kb2;
   int splits = ep.k_splits < 1 ? 1 : ep.k_splits;
   if (splits > kb_total) splits = kb_total > 0 ? kb_total : 1;
-  const int kb_per = (kb_total + splits - 1) / splits;
-  splits = kb_total > 0 ? (kb_total + kb_per - 1) / kb_per : 1;
+  const int kb_per = kb_total > 0 ? (kb_total + splits - 1) / splits : 0;
+  splits = kb_per > 0 ? (kb_total + kb_per - 1) / kb_per : 1;
 
   linrec_dev::tc::GemmParams p{};
   p.M = (int)op.M;
-  p.N = (int)op.N;
+  p.units = (int)op.units;
+  p.nz = splits;
   p.kb1 = kb1;
   p.kb = kb_per;
   p.kb_total = kb_total;
-  p.k_splits = splits;
+  p.kchunk = ep.split3 ? 4 : 16;  // K = 128 (3xTF32) / 512 (TF32) per TMEM accumulation
   p.ldc = (int)ep.ldc;
   p.C = ep.C;
   p.mode = ep.accumulate ? 1 : 0;
-  p.bias = ep.bias;
-  p.o0 = ep.o0;
-  p.o1 = ep.o1;
-  p.o2 = ep.o2;
-  p.o3 = ep.o3;
-  p.ldo = (int)ep.ldo;
+  p.act = ep.act;
+  p.ldo = ep.ldo;
+  for (int i = 0; i < 4; ++i) p.bias[i] = ep.bias[i];
+  for (int i = 0; i < 5; ++i) p.out[i] = ep.out[i];
   float* partial = nullptr;
   if (splits > 1) {
     if (epi != linrec_dev::tc::kEpiPlain || ep.scratch == nullptr) return cudaErrorInvalidValue;
     partial = ep.scratch;
     p.C = partial;
-    p.ldc = (int)op.N;
+    p.ldc = (int)op.units;
     p.mode = 2;
   }
-  cudaError_t e;
-#define GEMM_CASE(AM, BMN, EP)                                                          \
-  if (op.a_mn == AM && op.b_mn == BMN && epi == EP) {                                   \
-    e = launch_cfg<AM, BMN, 128, 4, EP>(op, p, splits, st);                            \
-    goto launched;                                                                      \
-  }
-  GEMM_CASE(false, false, linrec_dev::tc::kEpiPlain)
-  GEMM_CASE(false, false, linrec_dev::tc::kEpiGilr)
-  GEMM_CASE(false, false, linrec_dev::tc::kEpiGates)
-  GEMM_CASE(false, true, linrec_dev::tc::kEpiPlain)
-  GEMM_CASE(true, true, linrec_dev::tc::kEpiPlain)
-  GEMM_CASE(true, false, linrec_dev::tc::kEpiPlain)
-#undef GEMM_CASE
-  return cudaErrorInvalidConfiguration;
-launched:
+  cudaError_t e = ep.split3 ? dispatch<true>(op, epi, p, st) : dispatch<false>(op, epi, p, st);
   if (e != cudaSuccess) return e;
   if (splits > 1) {
-    const int64_t MN = op.M * op.N;
+    const int64_t MN = op.M * op.units;
     const int64_t blocks = (MN + 255) / 256;
-    k_splitk_reduce<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(partial, splits, MN, op.N, ep.ldc,
+    k_splitk_reduce<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(partial, splits, MN, op.units, ep.ldc,
                                                                                ep.C, ep.accumulate ? 1 : 0);
     e = cudaGetLastError();
   }
   return e;
-}
-
-int gemm_splits_for(int64_t M, int64_t N, int64_t K) {
-  const int64_t tiles = ((M + 127) / 128) * ((N + 127) / 128);
-  const int64_t kb = (K + 31) / 32;
-  int64_t s = (2 * 148 + tiles - 1) / tiles;  // ~2 waves of CTAs
-  if (s > kb / 4) s = kb / 4;                  // >= 4 k-blocks per split
-  if (s < 1) s = 1;
-  if (s > 64) s = 64;
-  return (int)s;
 }
 
 }  // namespace linrec_impl

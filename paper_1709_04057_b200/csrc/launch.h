@@ -121,22 +121,25 @@ struct GemmOperands {
   const float* a2 = nullptr;
   const float* b2 = nullptr;
   int64_t K2 = 0, lda2 = 0, ldb2 = 0;
-  int64_t M = 0, N = 0;
+  int64_t M = 0;
+  int64_t units = 0;      // output columns (per block when nb > 1)
+  int nb = 1;             // blocked K-major B: nb row blocks of `units` rows ...
+  int64_t b_bstride = 0;  // ... block q starting at row q * b_bstride
   bool a_mn = false, b_mn = false;
 };
 struct GemmEpilogue {
   float* C = nullptr;
   int64_t ldc = 0;
   bool accumulate = false;
+  bool split3 = false;       // 3xTF32 (fp32-grade) instead of plain TF32
   int k_splits = 1;
-  float* scratch = nullptr;  // split-K partials, k_splits * M * N floats
-  const float* bias = nullptr;
-  float* o0 = nullptr;
-  float* o1 = nullptr;
-  float* o2 = nullptr;
-  float* o3 = nullptr;
+  float* scratch = nullptr;  // split-K partials, k_splits * M * units floats
+  int act = 0;               // GILR candidate activation (0 tanh, 1 identity, 2 relu)
+  const float* bias[4] = {nullptr, nullptr, nullptr, nullptr};
+  float* out[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   int64_t ldo = 0;
 };
+// epi: 0 plain (C / accumulate / split-K), 1 GILR gates (nb 2), 2 LSTM gates (nb 4)
 cudaError_t gemm_tf32(const GemmOperands& op, int epi, const GemmEpilogue& ep, cudaStream_t st);
 int gemm_splits_for(int64_t M, int64_t N, int64_t K);
 
