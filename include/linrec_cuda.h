@@ -250,6 +250,92 @@ int linrec_gemm_f32(const float* A, int a_mn, int64_t lda, const float* B, int b
  * persistent grid); scratch for it is k_splits*M*N floats. */
 int linrec_gemm_splits(int64_t M, int64_t N, int64_t K);
 
+/* ---- GILR and GILR-LSTM layers (layers.hpp:23-375) ------------------------ *
+ * The paper's recurrent layers on the GPU: gate projections on the tensor
+ * cores (linrec_gemm_f32 with fused activation epilogues), recurrences on the
+ * chained scans above.  All buffers are caller-owned device memory, fp32,
+ * time-major [T][b][.] C-contiguous (x: [T][b][m], activations [T][b][n]),
+ * parameters row-major exactly as GilrParams / GilrLstmParams
+ * (layers.hpp:30-40, :146-160): gate blocks f, i, o, z stacked along rows.
+ * m and n must be multiples of 4 (16-byte TMA rows).  Parameter gradients
+ * ACCUMULATE into the grads buffers (the reference's += semantics,
+ * tensor.hpp:272-296); dx is overwritten.  `scratch` is device memory of at
+ * least linrec_gilr[_lstm]_scratch_bytes(); `precision` is LINREC_PREC_FP32
+ * (3xTF32, the default) or LINREC_PREC_TF32; `mode` is the ScanMode of the
+ * recurrences.  NULL h0 / htil0 / c0 mean zeros; NULL dh0 / dhtil0 / dc0 are
+ * not written. */
+#define LINREC_ACT_TANH 0     /* Activation::Tanh     (common.hpp:49-71) */
+#define LINREC_ACT_IDENTITY 1 /* Activation::Identity */
+#define LINREC_ACT_RELU 2     /* Activation::Relu     */
+
+typedef struct linrec_gilr_params_f32 { /* GilrParams<float> (layers.hpp:30-40) */
+  const float* U;   /* [n][m] gate weights */
+  const float* V;   /* [n][m] candidate weights */
+  const float* b_g; /* [n] gate bias */
+  const float* b_z; /* [n] candidate bias */
+  int act;          /* candidate activation, LINREC_ACT_* */
+} linrec_gilr_params_f32;
+
+typedef struct linrec_gilr_grads_f32 { /* GilrGrads<float> (layers.hpp:66-76) */
+  float* U;
+  float* V;
+  float* b_g;
+  float* b_z;
+} linrec_gilr_grads_f32;
+
+typedef struct linrec_gilr_lstm_params_f32 { /* GilrLstmParams<float> (layers.hpp:146-160) */
+  linrec_gilr_params_f32 surrogate; /* m -> n; its act must be tanh in the reference init */
+  const float* U;                   /* [4n][n], applied to htil_{t-1} */
+  const float* V;                   /* [4n][m], applied to x_t */
+  const float* bias;                /* [4n] */
+} linrec_gilr_lstm_params_f32;
+
+typedef struct linrec_gilr_lstm_grads_f32 { /* GilrLstmGrads<float> (layers.hpp:192-211) */
+  linrec_gilr_grads_f32 surrogate;
+  float* U;
+  float* V;
+  float* bias;
+} linrec_gilr_lstm_grads_f32;
+
+/* GilrLstmCache<float> (layers.hpp:183-188), device buffers:
+ *   sg, si   [T][b][n]     surrogate gate / candidate (GilrCache::g, ::i)
+ *   htil     [T+1][b][n]   row 0 = htil0, rows 1..T = surrogate output, so
+ *                          rows 0..T-1 are htil_prev (detail::shift_right)
+ *   gates    [4][T][b][n]  activated f, i, o, z planes (the reference keeps
+ *                          them interleaved as [T][b][4n])
+ *   c        [T][b][n]     cell state */
+typedef struct linrec_gilr_lstm_cache_f32 {
+  float* sg;
+  float* si;
+  float* htil;
+  float* gates;
+  float* c;
+} linrec_gilr_lstm_cache_f32;
+
+size_t linrec_gilr_scratch_bytes(int64_t T, int64_t b, int64_t m, int64_t n);
+size_t linrec_gilr_lstm_scratch_bytes(int64_t T, int64_t b, int64_t m, int64_t n);
+
+/* gilr_forward (layers.hpp:78-100): h [T][b][n]; g, i (the cache) [T][b][n]. */
+int linrec_gilr_forward_f32(const linrec_gilr_params_f32* p, const float* x, const float* h0, float* h, float* g,
+                            float* i, int64_t T, int64_t b, int64_t m, int64_t n, int mode, int precision,
+                            void* scratch, size_t scratch_bytes, void* stream);
+/* gilr_backward (layers.hpp:102-133). */
+int linrec_gilr_backward_f32(const linrec_gilr_params_f32* p, const float* x, const float* h0, const float* g,
+                             const float* i, const float* h, const float* dh, linrec_gilr_grads_f32* grads,
+                             float* dx, float* dh0, int64_t T, int64_t b, int64_t m, int64_t n, int mode,
+                             int precision, void* scratch, size_t scratch_bytes, void* stream);
+/* gilr_lstm_forward (layers.hpp:245-293): h [T][b][n]; fills the cache. */
+int linrec_gilr_lstm_forward_f32(const linrec_gilr_lstm_params_f32* p, const float* x, const float* htil0,
+                                 const float* c0, float* h, const linrec_gilr_lstm_cache_f32* cache, int64_t T,
+                                 int64_t b, int64_t m, int64_t n, int mode, int precision, void* scratch,
+                                 size_t scratch_bytes, void* stream);
+/* gilr_lstm_backward (layers.hpp:295-375). */
+int linrec_gilr_lstm_backward_f32(const linrec_gilr_lstm_params_f32* p, const float* x, const float* htil0,
+                                  const float* c0, const linrec_gilr_lstm_cache_f32* cache, const float* dh,
+                                  linrec_gilr_lstm_grads_f32* grads, float* dx, float* dhtil0, float* dc0,
+                                  int64_t T, int64_t b, int64_t m, int64_t n, int mode, int precision,
+                                  void* scratch, size_t scratch_bytes, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

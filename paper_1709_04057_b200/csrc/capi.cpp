@@ -96,6 +96,10 @@ int check_ptr(const void* p, const char* name) {
 }
 }  // namespace
 
+namespace linrec_impl {
+int set_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace linrec_impl
+
 // ---------------------------------------------------------------------------
 // workspace
 // ---------------------------------------------------------------------------

@@ -7,6 +7,9 @@
 
 namespace linrec_impl {
 
+// Sets the thread-local linrec_last_error() message; returns `code`.
+int set_error(int code, const char* msg);
+
 // Tile configuration chosen for one chained launch.
 struct ChainPlan {
   int kind = 0;       // 0 = register kernel (scan_chained.cuh), 1 = TMA persistent (scan_tma.cuh)

@@ -1,0 +1,392 @@
+"""GILR and GILR-LSTM layers on the B200 (reference: proj/include/linrec/layers.hpp).
+
+Same names and semantics as the reference's layer API, over torch CUDA
+tensors on the current stream; every FLOP runs in liblinrec_cuda.so (the
+tcgen05 gate GEMMs with fused activation epilogues and the chained scans):
+
+    gilr_init / gilr_forward / gilr_backward                  layers.hpp:42-133
+    gilr_lstm_init / gilr_lstm_forward / gilr_lstm_backward   layers.hpp:165-375
+
+Parameters are row-major exactly as GilrParams / GilrLstmParams (gate blocks
+f, i, o, z stacked along the rows of U, V, bias).  Gradients ACCUMULATE into
+the grads objects (tensor.hpp:272-296); dx is returned.  ``precision`` is
+"fp32" (3xTF32 on the tensor cores, fp32-grade; default) or "tf32" (one TF32
+pass, ~1e-3 relative).  Inputs: x [T, b, m] fp32 contiguous; m, n multiples
+of 4.  ``GilrLstm`` wraps the pair as a torch.nn.Module with autograd.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import capi
+
+_vp = C.c_void_p
+_i64 = C.c_int64
+_int = C.c_int
+ACT = {"tanh": 0, "identity": 1, "relu": 2}
+PRECISION = {"fp32": capi.PREC_FP32, "tf32": capi.PREC_TF32}
+MODE = {"serial": capi.SERIAL, "parallel": capi.PARALLEL}
+
+
+class _GilrParamsC(C.Structure):
+    _fields_ = [("U", _vp), ("V", _vp), ("b_g", _vp), ("b_z", _vp), ("act", _int)]
+
+
+class _GilrGradsC(C.Structure):
+    _fields_ = [("U", _vp), ("V", _vp), ("b_g", _vp), ("b_z", _vp)]
+
+
+class _LstmParamsC(C.Structure):
+    _fields_ = [("surrogate", _GilrParamsC), ("U", _vp), ("V", _vp), ("bias", _vp)]
+
+
+class _LstmGradsC(C.Structure):
+    _fields_ = [("surrogate", _GilrGradsC), ("U", _vp), ("V", _vp), ("bias", _vp)]
+
+
+class _LstmCacheC(C.Structure):
+    _fields_ = [("sg", _vp), ("si", _vp), ("htil", _vp), ("gates", _vp), ("c", _vp)]
+
+
+def _bind():
+    lib = capi.lib
+    if getattr(lib, "_layers_bound", False):
+        return lib
+    lib.linrec_gilr_scratch_bytes.restype = C.c_size_t
+    lib.linrec_gilr_scratch_bytes.argtypes = [_i64] * 4
+    lib.linrec_gilr_lstm_scratch_bytes.restype = C.c_size_t
+    lib.linrec_gilr_lstm_scratch_bytes.argtypes = [_i64] * 4
+    tail = [_i64] * 4 + [_int, _int, _vp, C.c_size_t, _vp]
+    lib.linrec_gilr_forward_f32.argtypes = [C.POINTER(_GilrParamsC)] + [_vp] * 5 + tail
+    lib.linrec_gilr_backward_f32.argtypes = ([C.POINTER(_GilrParamsC)] + [_vp] * 6 + [C.POINTER(_GilrGradsC)]
+                                             + [_vp] * 2 + tail)
+    lib.linrec_gilr_lstm_forward_f32.argtypes = ([C.POINTER(_LstmParamsC)] + [_vp] * 4 + [C.POINTER(_LstmCacheC)]
+                                                 + tail)
+    lib.linrec_gilr_lstm_backward_f32.argtypes = ([C.POINTER(_LstmParamsC)] + [_vp] * 3 + [C.POINTER(_LstmCacheC)]
+                                                  + [_vp] + [C.POINTER(_LstmGradsC)] + [_vp] * 3 + tail)
+    lib._layers_bound = True
+    return lib
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _check_f32(t, name):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32 (the layers' device path is fp32)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be C-contiguous")
+
+
+_scratch = {}
+
+
+def _scratch_for(nbytes, device):
+    """Per-(device, stream) scratch, grown on demand (torch caching allocator)."""
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+    buf = _scratch.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        _scratch[key] = buf
+    return buf
+
+
+def release_scratch():
+    _scratch.clear()
+
+
+# ---- parameters (layers.hpp:30-76, :146-211) ---------------------------------
+@dataclass
+class GilrParams:
+    U: torch.Tensor    # [n, m]
+    V: torch.Tensor    # [n, m]
+    b_g: torch.Tensor  # [n]
+    b_z: torch.Tensor  # [n]
+    act: str = "tanh"
+
+    def input(self):
+        return self.U.shape[1]
+
+    def hidden(self):
+        return self.U.shape[0]
+
+    def tensors(self):
+        return [self.U, self.V, self.b_g, self.b_z]
+
+    def _c(self):
+        return _GilrParamsC(_p(self.U), _p(self.V), _p(self.b_g), _p(self.b_z), ACT[self.act])
+
+
+@dataclass
+class GilrGrads:
+    U: torch.Tensor
+    V: torch.Tensor
+    b_g: torch.Tensor
+    b_z: torch.Tensor
+
+    @staticmethod
+    def zeros_like(p: GilrParams) -> "GilrGrads":
+        return GilrGrads(*(torch.zeros_like(t) for t in p.tensors()))
+
+    def tensors(self):
+        return [self.U, self.V, self.b_g, self.b_z]
+
+    def _c(self):
+        return _GilrGradsC(_p(self.U), _p(self.V), _p(self.b_g), _p(self.b_z))
+
+
+@dataclass
+class GilrLstmParams:
+    surrogate: GilrParams
+    U: torch.Tensor     # [4n, n]
+    V: torch.Tensor     # [4n, m]
+    bias: torch.Tensor  # [4n]
+
+    def input(self):
+        return self.V.shape[1]
+
+    def hidden(self):
+        return self.U.shape[1]
+
+    def tensors(self):
+        return self.surrogate.tensors() + [self.U, self.V, self.bias]
+
+    def _c(self):
+        return _LstmParamsC(self.surrogate._c(), _p(self.U), _p(self.V), _p(self.bias))
+
+
+@dataclass
+class GilrLstmGrads:
+    surrogate: GilrGrads
+    U: torch.Tensor
+    V: torch.Tensor
+    bias: torch.Tensor
+
+    @staticmethod
+    def zeros_like(p: GilrLstmParams) -> "GilrLstmGrads":
+        return GilrLstmGrads(GilrGrads.zeros_like(p.surrogate), torch.zeros_like(p.U), torch.zeros_like(p.V),
+                             torch.zeros_like(p.bias))
+
+    def tensors(self):
+        return self.surrogate.tensors() + [self.U, self.V, self.bias]
+
+    def _c(self):
+        return _LstmGradsC(self.surrogate._c(), _p(self.U), _p(self.V), _p(self.bias))
+
+
+@dataclass
+class GilrCache:
+    g: torch.Tensor = None
+    i: torch.Tensor = None
+    h: torch.Tensor = None
+
+
+@dataclass
+class GilrLstmCache:
+    """GilrLstmCache (layers.hpp:183-188) on the device.  htil is [T+1, b, n]
+    (row 0 = htil0) so htil_prev = htil[:-1] without a copy; gates are the
+    four activated planes [4, T, b, n] (the reference interleaves them as
+    [T, b, 4n]; ``gates_interleaved()`` gives that view)."""
+    sg: torch.Tensor = None
+    si: torch.Tensor = None
+    htil: torch.Tensor = None
+    gates: torch.Tensor = None
+    c: torch.Tensor = None
+
+    def allocate(self, T, b, n, device):
+        kw = dict(dtype=torch.float32, device=device)
+        self.sg = torch.empty(T, b, n, **kw)
+        self.si = torch.empty(T, b, n, **kw)
+        self.htil = torch.empty(T + 1, b, n, **kw)
+        self.gates = torch.empty(4, T, b, n, **kw)
+        self.c = torch.empty(T, b, n, **kw)
+        return self
+
+    def surrogate_h(self):
+        return self.htil[1:]
+
+    def htil_prev(self):
+        return self.htil[:-1]
+
+    def gates_interleaved(self):
+        return self.gates.permute(1, 2, 0, 3).reshape(self.gates.shape[1], self.gates.shape[2], -1)
+
+    def _c(self):
+        return _LstmCacheC(_p(self.sg), _p(self.si), _p(self.htil), _p(self.gates), _p(self.c))
+
+
+def _uniform(gen, rows, cols, scale, device):
+    return ((torch.rand(rows, cols, generator=gen, dtype=torch.float64) * 2 - 1) * scale).to(
+        device=device, dtype=torch.float32)
+
+
+def gilr_init(gen: torch.Generator, m: int, n: int, gate_bias: float = 1.0, device="cuda",
+              act: str = "tanh") -> GilrParams:
+    """gilr_init (layers.hpp:42-55): U, V ~ U(+-1/sqrt(m)), b_g = gate_bias, b_z = 0."""
+    s = 1.0 / math.sqrt(m)
+    return GilrParams(_uniform(gen, n, m, s, device), _uniform(gen, n, m, s, device),
+                      torch.full((n,), gate_bias, dtype=torch.float32, device=device),
+                      torch.zeros(n, dtype=torch.float32, device=device), act)
+
+
+def gilr_lstm_init(gen: torch.Generator, m: int, n: int, gate_bias: float = 1.0, device="cuda") -> GilrLstmParams:
+    """gilr_lstm_init (layers.hpp:165-176): surrogate as gilr_init, U ~ U(+-1/sqrt(n)),
+    V ~ U(+-1/sqrt(m)), bias = gate_bias on the f block."""
+    sur = gilr_init(gen, m, n, gate_bias, device)
+    bias = torch.zeros(4 * n, dtype=torch.float32, device=device)
+    bias[:n] = gate_bias
+    return GilrLstmParams(sur, _uniform(gen, 4 * n, n, 1.0 / math.sqrt(n), device),
+                          _uniform(gen, 4 * n, m, 1.0 / math.sqrt(m), device), bias)
+
+
+def _dims(x, n):
+    _check_f32(x, "x")
+    if x.dim() != 3:
+        raise ValueError("x must have shape [T, batch, features]")
+    T, b, m = x.shape
+    return T, b, m, n
+
+
+def _call(rc):
+    capi.check(rc)
+
+
+# ---- GILR ------------------------------------------------------------------------
+def gilr_forward(p: GilrParams, x, h0=None, mode="parallel", precision="fp32", cache: GilrCache | None = None):
+    """gilr_forward (layers.hpp:78-100) -> h [T, b, n]; fills ``cache`` (g, i, h)."""
+    lib = _bind()
+    T, b, m, n = _dims(x, p.hidden())
+    if m != p.input():
+        raise RuntimeError("gilr_forward: input feature mismatch")
+    for t, nm in zip(p.tensors(), ("U", "V", "b_g", "b_z")):
+        _check_f32(t, nm)
+    if h0 is not None:
+        _check_f32(h0, "h0")
+    dev = x.device
+    h = torch.empty(T, b, n, dtype=torch.float32, device=dev)
+    g = torch.empty_like(h)
+    i = torch.empty_like(h)
+    need = lib.linrec_gilr_scratch_bytes(T, b, m, n)
+    scr = _scratch_for(need, dev)
+    pc = p._c()
+    _call(lib.linrec_gilr_forward_f32(C.byref(pc), _p(x), _p(h0), _p(h), _p(g), _p(i), T, b, m, n, MODE[mode],
+                                      PRECISION[precision], _p(scr), scr.numel(),
+                                      torch.cuda.current_stream(dev).cuda_stream))
+    if cache is not None:
+        cache.g, cache.i, cache.h = g, i, h
+    return h
+
+
+def gilr_backward(p: GilrParams, x, h0, cache: GilrCache, d_h, grads: GilrGrads, mode="parallel",
+                  precision="fp32", want_dh0=True):
+    """gilr_backward (layers.hpp:102-133): accumulates into ``grads``; returns (dx, dh0)."""
+    lib = _bind()
+    T, b, m, n = _dims(x, p.hidden())
+    _check_f32(d_h, "d_h")
+    dev = x.device
+    dx = torch.empty(T, b, m, dtype=torch.float32, device=dev)
+    dh0 = torch.empty(b, n, dtype=torch.float32, device=dev) if want_dh0 else None
+    need = lib.linrec_gilr_scratch_bytes(T, b, m, n)
+    scr = _scratch_for(need, dev)
+    pc, gc = p._c(), grads._c()
+    _call(lib.linrec_gilr_backward_f32(C.byref(pc), _p(x), _p(h0), _p(cache.g), _p(cache.i), _p(cache.h), _p(d_h),
+                                       C.byref(gc), _p(dx), _p(dh0), T, b, m, n, MODE[mode], PRECISION[precision],
+                                       _p(scr), scr.numel(), torch.cuda.current_stream(dev).cuda_stream))
+    return dx, dh0
+
+
+# ---- GILR-LSTM ---------------------------------------------------------------------
+def gilr_lstm_forward(p: GilrLstmParams, x, htil0=None, c0=None, mode="parallel", precision="fp32",
+                      cache: GilrLstmCache | None = None):
+    """gilr_lstm_forward (layers.hpp:245-293) -> h [T, b, n]; fills ``cache``."""
+    lib = _bind()
+    T, b, m, n = _dims(x, p.hidden())
+    if m != p.input():
+        raise RuntimeError("gilr_lstm_forward: input feature mismatch")
+    for t in p.tensors():
+        _check_f32(t, "parameter")
+    for t, nm in ((htil0, "htil0"), (c0, "c0")):
+        if t is not None:
+            _check_f32(t, nm)
+    dev = x.device
+    if cache is None:
+        cache = GilrLstmCache()
+    cache.allocate(T, b, n, dev)
+    h = torch.empty(T, b, n, dtype=torch.float32, device=dev)
+    need = lib.linrec_gilr_lstm_scratch_bytes(T, b, m, n)
+    scr = _scratch_for(need, dev)
+    pc, cc = p._c(), cache._c()
+    _call(lib.linrec_gilr_lstm_forward_f32(C.byref(pc), _p(x), _p(htil0), _p(c0), _p(h), C.byref(cc), T, b, m, n,
+                                           MODE[mode], PRECISION[precision], _p(scr), scr.numel(),
+                                           torch.cuda.current_stream(dev).cuda_stream))
+    return h
+
+
+def gilr_lstm_backward(p: GilrLstmParams, x, htil0, c0, cache: GilrLstmCache, d_h, grads: GilrLstmGrads,
+                       mode="parallel", precision="fp32", want_initial=True):
+    """gilr_lstm_backward (layers.hpp:295-375): accumulates into ``grads``;
+    returns (dx, d_htil0, d_c0)."""
+    lib = _bind()
+    T, b, m, n = _dims(x, p.hidden())
+    _check_f32(d_h, "d_h")
+    dev = x.device
+    dx = torch.empty(T, b, m, dtype=torch.float32, device=dev)
+    dht0 = torch.empty(b, n, dtype=torch.float32, device=dev) if want_initial else None
+    dc0 = torch.empty(b, n, dtype=torch.float32, device=dev) if want_initial else None
+    need = lib.linrec_gilr_lstm_scratch_bytes(T, b, m, n)
+    scr = _scratch_for(need, dev)
+    pc, cc, gc = p._c(), cache._c(), grads._c()
+    _call(lib.linrec_gilr_lstm_backward_f32(C.byref(pc), _p(x), _p(htil0), _p(c0), C.byref(cc), _p(d_h),
+                                            C.byref(gc), _p(dx), _p(dht0), _p(dc0), T, b, m, n, MODE[mode],
+                                            PRECISION[precision], _p(scr), scr.numel(),
+                                            torch.cuda.current_stream(dev).cuda_stream))
+    return dx, dht0, dc0
+
+
+# ---- torch autograd / nn.Module ---------------------------------------------------------
+class _GilrLstmFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, htil0, c0, sU, sV, sbg, sbz, U, V, bias, precision):
+        p = GilrLstmParams(GilrParams(sU, sV, sbg, sbz), U, V, bias)
+        cache = GilrLstmCache()
+        h = gilr_lstm_forward(p, x.contiguous(), htil0, c0, precision=precision, cache=cache)
+        ctx.p, ctx.cache, ctx.precision = p, cache, precision
+        ctx.save_for_backward(x, htil0, c0)
+        return h
+
+    @staticmethod
+    def backward(ctx, dh):
+        x, htil0, c0 = ctx.saved_tensors
+        p = ctx.p
+        grads = GilrLstmGrads.zeros_like(p)
+        dx, dht0, dc0 = gilr_lstm_backward(p, x, htil0, c0, ctx.cache, dh.contiguous(), grads,
+                                           precision=ctx.precision)
+        return (dx, dht0, dc0, *grads.tensors(), None)
+
+
+class GilrLstm(torch.nn.Module):
+    """One GILR-LSTM layer (m -> n) with B200 forward/backward."""
+
+    def __init__(self, m, n, gate_bias=1.0, seed=0, device="cuda", precision="fp32"):
+        super().__init__()
+        gen = torch.Generator().manual_seed(seed)
+        p = gilr_lstm_init(gen, m, n, gate_bias, device)
+        self.names = ["sU", "sV", "sbg", "sbz", "U", "V", "bias"]
+        for nm, t in zip(self.names, p.tensors()):
+            self.register_parameter(nm, torch.nn.Parameter(t))
+        self.precision = precision
+        self.n = n
+
+    def forward(self, x, htil0=None, c0=None):
+        T, b, _ = x.shape
+        z = torch.zeros(b, self.n, device=x.device, dtype=x.dtype)
+        htil0 = z if htil0 is None else htil0
+        c0 = z if c0 is None else c0
+        return _GilrLstmFn.apply(x, htil0, c0, *[getattr(self, nm) for nm in self.names], self.precision)
