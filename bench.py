@@ -2,7 +2,7 @@
 """Benchmark of the linear-recurrence hot path (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2|c4|c1]
+                    [--workload c2|c4|c1|c3] [--precision fp32|tf32]
 
 One step = one forward scan (lam, x, h0 -> h) + one reverse-time backward scan
 (lam, h0, h, dh -> dlam, dx, dh0) over one batch of synthetic input, fp32.
@@ -47,6 +47,8 @@ WORKLOADS = {
     "c1": dict(T=4096, B=1, D=256, desc="C1 fp32 linear recurrence T=4096 B=1 D=256 (BASELINE configs[0])"),
     "c2": dict(T=65536, B=8, D=1024, desc="C2 fp32 forward+backward linear recurrence T=65536 B=8 D=1024 (BASELINE configs[1])"),
     "c4": dict(T=1 << 20, B=1, D=128, desc="C4 fp32 1M-timestep recurrence T=1048576 B=1 D=128 (BASELINE configs[3])"),
+    "c3": dict(T=65536, B=4, D=512, desc="C3 GILR-LSTM layer fwd+bwd T=65536 B=4 m=n=512 (BASELINE configs[2]): "
+               "tensor-core gate GEMMs + fused scans"),
 }
 
 
@@ -463,6 +465,241 @@ def run_reference(args):
     }), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# C3: one GILR-LSTM layer forward + backward (layers.hpp:245-375)
+# ---------------------------------------------------------------------------
+def layer_stage_work(T, b, m, n):
+    """Algorithmic work per stage: ("flop", 2*M*N*K) for the GEMMs, ("byte",
+    bytes) for the scans and pointwise passes (fp32)."""
+    R = T * b
+    E = R * n
+    return {
+        "gemm_surrogate": ("flop", 2 * R * m * 2 * n),
+        "scan_surrogate": ("byte", 12 * E),
+        "gemm_gates": ("flop", 2 * R * (m + n) * 4 * n),
+        "scan_cell": ("byte", 12 * E),
+        "h_out": ("byte", 12 * E),
+        "dc": ("byte", 12 * E),
+        "scan_bwd_cell": ("byte", 20 * E),
+        "dpre_gates": ("byte", 48 * E),
+        "wgrad_U": ("flop", 2 * 4 * n * n * R),
+        "wgrad_V": ("flop", 2 * 4 * n * m * R),
+        "dhtil_prev": ("flop", 2 * R * 4 * n * n),
+        "scan_bwd_surrogate": ("byte", 20 * E),
+        "dpre_surrogate": ("byte", 24 * E),
+        "wgrad_surrogate_U": ("flop", 2 * n * m * R),
+        "wgrad_surrogate_V": ("flop", 2 * n * m * R),
+        "dx": ("flop", 2 * R * m * 6 * n),
+    }
+
+
+def tensor_peak():
+    """dense TF32 tensor-core peak: half the measured bf16 dense rate."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops"]) / 2, "measured bf16 dense / 2 (kind::tf32 runs at half the bf16 rate)"
+    except Exception:
+        return 1125.0, "fallback: nominal 2.25 PF bf16 / 2"
+
+
+def run_layer(args):
+    import torch
+    from paper_1709_04057_b200 import layers as L
+
+    world, rank, local = dist_env()
+    if world > 1:
+        raise SystemExit("c3 is a single-GPU workload (the layer shards like C2 over channels: run replicas)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    wl = WORKLOADS["c3"]
+    T, b, n = wl["T"], wl["B"], wl["D"]
+    m = n
+    prec = args.precision
+    stream = torch.cuda.Stream(device=dev)
+    gen = torch.Generator().manual_seed(7)
+    with torch.cuda.stream(stream):
+        p = L.gilr_lstm_init(gen, m, n, 1.0, dev)
+        g = torch.Generator(device=dev).manual_seed(11)
+        x = torch.empty(T, b, m, device=dev).uniform_(-1, 1, generator=g)
+        dh = torch.empty(T, b, n, device=dev).uniform_(-1, 1, generator=g)
+        z = torch.zeros(b, n, device=dev)
+        cache = L.GilrLstmCache()
+        grads = L.GilrLstmGrads.zeros_like(p)
+
+        def step():
+            for t in grads.tensors():
+                t.zero_()
+            h = L.gilr_lstm_forward(p, x, z, z, precision=prec, cache=cache)
+            dx, _, _ = L.gilr_lstm_backward(p, x, z, z, cache, dh, grads, precision=prec)
+            return h, dx
+
+        for _ in range(args.warmup):
+            step()
+    stream.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    L.profile_begin()
+    with ClockSampler(local) as clocks, torch.cuda.stream(stream):
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+        end.record(stream)
+        torch.cuda.synchronize(dev)
+    stages = L.profile_end()
+    ms = start.elapsed_time(end) / args.steps
+    E = T * b * n
+    work = layer_stage_work(T, b, m, n)
+    hbm, hbm_kind = peaks()
+    tpk, tpk_kind = tensor_peak()
+    st_out, best = {}, None
+    for name, (tot, cnt) in stages.items():
+        avg = tot / args.steps
+        rec = {"ms": avg, "launch_sets_per_step": cnt / args.steps}
+        if name in work:
+            kind, amount = work[name]
+            if kind == "flop":
+                rec["tflops"] = amount / (avg / 1e3) / 1e12
+                rec["frac_tf32_peak"] = rec["tflops"] / tpk
+                if best is None or avg > best[1]:
+                    best = (name, avg, amount)
+            else:
+                rec["gbs"] = amount / (avg / 1e3) / 1e9
+                rec["frac_hbm_peak"] = rec["gbs"] / hbm
+        st_out[name] = rec
+    gemm_ms = sum(v["ms"] for k, v in st_out.items() if "tflops" in v)
+    flops = sum(a for k, (kind, a) in work.items() if kind == "flop")
+    bname, bms, bflop = best
+    achieved = bflop / (bms / 1e3) / 1e12
+    result = {
+        "metric": METRIC,
+        "value": E / (ms / 1e3),
+        "unit": "elements/s",
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32 (GEMMs: %s)" % ("3xTF32 tcgen05, fp32-grade" if prec == "fp32" else "TF32 tcgen05"),
+        "data": "synthetic: x, d_h ~U(-1,1); parameters from gilr_lstm_init (layers.hpp:165-176), gate_bias 1",
+        "config": {
+            "workload": wl["desc"], "T": T, "B": b, "m": m, "n": n, "elements_per_step": E,
+            "events_per_step": T * b, "precision": prec,
+            "step": "zero grads + gilr_lstm_forward + gilr_lstm_backward (one layer)",
+            "l2": "no flush: activations are %.0f MiB per [T,b,n] tensor >> 126 MB L2" % (E * 4 / 2**20),
+            "timing": "CUDA events on the launching stream; per-stage events via linrec_profile_begin/end",
+        },
+        "events_per_s": T * b / (ms / 1e3),
+        "gemm_tflops_total": flops / (gemm_ms / 1e3) / 1e12,
+        "gemm_share_of_step": gemm_ms / ms,
+        "stages": st_out,
+        "roofline": {
+            "bound": "tensor",
+            "kernel": f"k_gemm ({bname}) -- the longest tensor-core stage",
+            "achieved": achieved,
+            "peak": tpk,
+            "peak_kind": tpk_kind,
+            "unit": "TFLOP/s",
+            "frac": achieved / tpk,
+            "mma_issue_frac": (3 if prec == "fp32" else 1) * achieved / tpk,
+            "traffic": None,
+            "algorithmic_flops_per_launch": bflop,
+        },
+        "gpu_launches": None,
+        "clocks": clocks.summary(),
+    }
+    # kernels per step: GEMMs (+ split-K reductions) + scans (2-4 each) + pointwise
+    result["gpu_launches"] = sum(round(v["launch_sets_per_step"]) for v in st_out.values()) * args.steps
+    del cache, grads
+    torch.cuda.empty_cache()
+    if not args.no_e2e:
+        result["e2e"] = layer_e2e(args, p, T, b, m, n, dev)
+    if not args.no_cpu:
+        result["cpu_baseline"] = layer_cpu_baseline(args, m, n, b)
+    print(json.dumps(result), flush=True)
+
+
+def layer_e2e(args, p, T, b, m, n, dev):
+    """Host x, d_h (pinned) -> device -> forward + backward -> h, dx back to host."""
+    import torch
+    from paper_1709_04057_b200 import layers as L
+    xh = torch.empty(T, b, m, pin_memory=True).uniform_(-1, 1)
+    dhh = torch.empty(T, b, n, pin_memory=True).uniform_(-1, 1)
+    hh = torch.empty(T, b, n, pin_memory=True)
+    dxh = torch.empty(T, b, m, pin_memory=True)
+    z = torch.zeros(b, n, device=dev)
+    cache = L.GilrLstmCache()
+    grads = L.GilrLstmGrads.zeros_like(p)
+
+    def step():
+        x = xh.to(dev, non_blocking=True)
+        dh = dhh.to(dev, non_blocking=True)
+        for t in grads.tensors():
+            t.zero_()
+        h = L.gilr_lstm_forward(p, x, z, z, precision=args.precision, cache=cache)
+        dx, _, _ = L.gilr_lstm_backward(p, x, z, z, cache, dh, grads, precision=args.precision)
+        hh.copy_(h, non_blocking=True)
+        dxh.copy_(dx, non_blocking=True)
+        torch.cuda.synchronize(dev)
+
+    step()
+    steps = max(1, min(args.steps, args.e2e_steps))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": T * b * n / dt, "unit": "elements/s", "ms_per_step": dt * 1e3, "steps": steps,
+            "h2d_bytes_per_step": 4 * T * b * (m + n), "d2h_bytes_per_step": 4 * T * b * (n + m),
+            "api": "paper_1709_04057_b200.layers.gilr_lstm_forward/backward (C ABI linrec_gilr_lstm_*_f32)",
+            "timing": "host wall clock incl. pinned H2D of x, d_h and D2H of h, dx"}
+
+
+def layer_cpu_baseline(args, m, n, b):
+    """The oracle port of layers.hpp (oracle/linrec_layers.c, fp32, 1 thread)
+    on a bounded sample: the reference's own layer path needs Eigen, which is
+    absent here."""
+    import numpy as np
+    from oracle.oracle import Oracle, gilr_lstm_params
+    orc = Oracle()
+    Ts = args.layer_cpu_rows
+    rng = np.random.default_rng(3)
+    P = {k: v.astype(np.float32) for k, v in gilr_lstm_params(rng, m, n).items()}
+    x = rng.uniform(-1, 1, (Ts, b, m)).astype(np.float32)
+    dh = rng.uniform(-1, 1, (Ts, b, n)).astype(np.float32)
+    z = np.zeros((b, n), np.float32)
+    t0 = time.perf_counter()
+    h, cache = orc.gilr_lstm_forward(P, x, z, z)
+    orc.gilr_lstm_backward(P, x, z, z, cache, dh)
+    dt = time.perf_counter() - t0
+    return {"value": Ts * b * n / dt, "unit": "elements/s", "cores": 1, "kind": "port",
+            "sample": f"T={Ts} rows x b={b} x m=n={n}: oracle gilr_lstm_forward + gilr_lstm_backward "
+                      f"(plain-C restatement of layers.hpp, naive loops), fp32, 1 thread, {dt:.1f} s"}
+
+
+def run_reference_layer(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    wl = WORKLOADS["c3"]
+    T, b, n = wl["T"], wl["B"], wl["D"]
+    for _ in range(max(0, min(args.warmup, 1))):
+        pass
+    reps = [layer_cpu_baseline(args, n, n, b) for _ in range(max(1, min(args.steps, 2)))]
+    v = statistics.median(r["value"] for r in reps)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "elements/s", "n_gpus": world,
+        "steps": len(reps), "warmup": 0, "ms_per_step": 1e3 * args.layer_cpu_rows * b * n / v,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": wl["desc"], "T": T, "B": b, "m": n, "n": n,
+                                        "sampled_rows": args.layer_cpu_rows},
+        "cpu_baseline": dict(reps[0], value=v),
+        "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference's layer path needs Eigen (absent; SURVEY.md 8c): its oracle port is timed",
+    }), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -475,10 +712,14 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--precision", choices=["fp32", "tf32"], default="fp32", help="c3 GEMM precision")
+    ap.add_argument("--layer-cpu-rows", type=int, default=16)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
-    if args.impl == "reference":
+    if args.workload == "c3":
+        run_reference_layer(args) if args.impl == "reference" else run_layer(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

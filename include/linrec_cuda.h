@@ -312,6 +312,14 @@ typedef struct linrec_gilr_lstm_cache_f32 {
   float* c;
 } linrec_gilr_lstm_cache_f32;
 
+/* Per-stage timing of the layer calls on the calling thread: between
+ * linrec_profile_begin() and linrec_profile_end(), every stage of
+ * linrec_gilr*_f32 records a CUDA event on the call's stream;
+ * linrec_profile_end() synchronizes them and writes one line per stage,
+ * "<stage> <total ms> <count>\n", in first-seen order (summed over calls). */
+int linrec_profile_begin(void);
+int linrec_profile_end(char* out, size_t cap);
+
 size_t linrec_gilr_scratch_bytes(int64_t T, int64_t b, int64_t m, int64_t n);
 size_t linrec_gilr_lstm_scratch_bytes(int64_t T, int64_t b, int64_t m, int64_t n);
 

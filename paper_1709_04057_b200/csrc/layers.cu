@@ -21,8 +21,12 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "launch.h"
 #include "linrec_cuda.h"
@@ -129,6 +133,27 @@ __global__ void k_gilr_dpre(const float* __restrict__ g, const float* __restrict
 
 }  // namespace layers
 }  // namespace linrec_dev
+
+// ---- optional per-stage timing (linrec_profile_begin / _end) ------------------
+namespace {
+struct Prof {
+  bool on = false;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;  // (stage that ENDS here, event)
+};
+Prof& prof() {
+  static thread_local Prof p;
+  return p;
+}
+// Records an event on `st` closing stage `name` (the previous mark opens it).
+void mark(cudaStream_t st, const char* name) {
+  Prof& p = prof();
+  if (!p.on) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, st);
+  p.marks.emplace_back(name, e);
+}
+}  // namespace
 
 namespace {
 
@@ -318,6 +343,7 @@ int gilr_forward_core(const linrec_gilr_params_f32* p, const float* x, const flo
   const int64_t R = T * b;
   LTRY(cudaMemcpyAsync(uv, p->U, sizeof(float) * n * m, cudaMemcpyDeviceToDevice, st));
   LTRY(cudaMemcpyAsync(uv + n * m, p->V, sizeof(float) * n * m, cudaMemcpyDeviceToDevice, st));
+  mark(st, "prep");
   GemmOperands op;
   op.a1 = x;
   op.lda1 = m;
@@ -337,7 +363,9 @@ int gilr_forward_core(const linrec_gilr_params_f32* p, const float* x, const flo
   ep.out[2] = imp;
   ep.ldo = n;
   LTRY(gemm(op, kEpiGilr, ep, split3, nullptr, st));
+  mark(st, "gemm_surrogate");
   LRC(linrec_scan_f32(g, imp, h0, h, T, b * n, mode, nullptr, st));
+  mark(st, "scan_surrogate");
   return LINREC_OK;
 }
 
@@ -350,7 +378,9 @@ int gilr_backward_core(const linrec_gilr_params_f32* p, const float* x, const fl
                        float* dh0_tmp, int64_t T, int64_t b, int64_t m, int64_t n, int mode, bool split3,
                        cudaStream_t st) {
   const int64_t R = T * b;
+  mark(st, "prep");
   LRC(linrec_scan_backward_f32(g, h0, h, dh, dl, G, dh0 ? dh0 : dh0_tmp, T, b * n, mode, nullptr, st));
+  mark(st, "scan_bwd_surrogate");
   const RowPlan rp = row_plan(R, n);
   k_gilr_dpre<<<dim3((unsigned)rp.nbx, (unsigned)rp.gy), rp.thr, 0, st>>>(g, ci, dl, G, p->act, dpre_s, part, R, n,
                                                                           rp.rpb);
@@ -363,11 +393,15 @@ int gilr_backward_core(const linrec_gilr_params_f32* p, const float* x, const fl
     k_colsum<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(part + n, rp.nbx, 2 * n, n, gr->b_z);
     LTRY(cudaGetLastError());
   }
+  mark(st, "dpre_surrogate");
   if (gr->U) LTRY(wgrad(dpre_s, 2 * n, n, x, m, R, gr->U, split3, split, st));
+  mark(st, "wgrad_surrogate_U");
   if (gr->V) LTRY(wgrad(dpre_s + n, 2 * n, n, x, m, R, gr->V, split3, split, st));
+  mark(st, "wgrad_surrogate_V");
   if (dx) {
     LTRY(cudaMemcpyAsync(uv, p->U, sizeof(float) * n * m, cudaMemcpyDeviceToDevice, st));
     LTRY(cudaMemcpyAsync(uv + n * m, p->V, sizeof(float) * n * m, cudaMemcpyDeviceToDevice, st));
+    mark(st, "prep");
     GemmOperands op;  // dx = [dg | di] * [U; V]
     op.a1 = dpre_s;
     op.lda1 = 2 * n;
@@ -381,6 +415,7 @@ int gilr_backward_core(const linrec_gilr_params_f32* p, const float* x, const fl
     ep.C = dx;
     ep.ldc = m;
     LTRY(gemm(op, kEpiPlain, ep, split3, nullptr, st));
+    mark(st, "dx");
   }
   return LINREC_OK;
 }
@@ -388,6 +423,54 @@ int gilr_backward_core(const linrec_gilr_params_f32* p, const float* x, const fl
 }  // namespace
 
 extern "C" {
+
+int linrec_profile_begin(void) {
+  Prof& p = prof();
+  for (auto& m : p.marks) cudaEventDestroy(m.second);
+  p.marks.clear();
+  p.on = true;
+  return LINREC_OK;
+}
+
+int linrec_profile_end(char* out, size_t cap) {
+  Prof& p = prof();
+  p.on = false;
+  std::map<std::string, std::pair<double, int>> acc;  // name -> (ms, count)
+  std::vector<std::string> order;
+  int rc = LINREC_OK;
+  for (size_t k = 1; k < p.marks.size(); ++k) {
+    if (p.marks[k].first == "begin") continue;
+    float ms = 0.f;
+    if (cudaEventSynchronize(p.marks[k].second) != cudaSuccess ||
+        cudaEventElapsedTime(&ms, p.marks[k - 1].second, p.marks[k].second) != cudaSuccess) {
+      rc = err(LINREC_ERR_CUDA, "linrec_profile_end: event timing failed");
+      break;
+    }
+    auto it = acc.find(p.marks[k].first);
+    if (it == acc.end()) {
+      order.push_back(p.marks[k].first);
+      acc[p.marks[k].first] = {ms, 1};
+    } else {
+      it->second.first += ms;
+      it->second.second += 1;
+    }
+  }
+  for (auto& m : p.marks) cudaEventDestroy(m.second);
+  p.marks.clear();
+  std::string s;
+  for (auto& n : order) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "%s %.6f %d\n", n.c_str(), acc[n].first, acc[n].second);
+    s += buf;
+  }
+  if (out && cap) {
+    const size_t k = s.size() < cap - 1 ? s.size() : cap - 1;
+    memcpy(out, s.data(), k);
+    out[k] = 0;
+    if (s.size() >= cap) return err(LINREC_ERR_VALUE, "linrec_profile_end: buffer too small");
+  }
+  return rc;
+}
 
 size_t linrec_gilr_scratch_bytes(int64_t T, int64_t b, int64_t m, int64_t n) {
   if (T < 1 || b < 1 || m < 1 || n < 1) return 0;
@@ -408,6 +491,7 @@ int linrec_gilr_forward_f32(const linrec_gilr_params_f32* p, const float* x, con
   GilrScratch s;
   LRC(check_scratch(scratch, scratch_bytes, gilr_scratch(nullptr, T, b, m, n, nullptr)));
   gilr_scratch(static_cast<float*>(scratch), T, b, m, n, &s);
+  mark(static_cast<cudaStream_t>(stream), "begin");
   return gilr_forward_core(p, x, h0, h, g, i, s.imp, s.uv, T, b, m, n, mode, precision == LINREC_PREC_FP32,
                            static_cast<cudaStream_t>(stream));
 }
@@ -422,6 +506,7 @@ int linrec_gilr_backward_f32(const linrec_gilr_params_f32* p, const float* x, co
   GilrScratch s;
   LRC(check_scratch(scratch, scratch_bytes, gilr_scratch(nullptr, T, b, m, n, nullptr)));
   gilr_scratch(static_cast<float*>(scratch), T, b, m, n, &s);
+  mark(static_cast<cudaStream_t>(stream), "begin");
   return gilr_backward_core(p, x, h0, g, i, h, dh, grads, dx, dh0, s.dl, s.G, s.dpre, s.part, s.split, s.uv, s.dh0,
                             T, b, m, n, mode, precision == LINREC_PREC_FP32, static_cast<cudaStream_t>(stream));
 }
@@ -440,6 +525,7 @@ int linrec_gilr_lstm_forward_f32(const linrec_gilr_lstm_params_f32* p, const flo
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool split3 = precision == LINREC_PREC_FP32;
   const int64_t R = T * b, BN = b * n, N = R * n;
+  mark(st, "begin");
   // 1-2. surrogate; its output lands one row block after htil0
   if (htil0) LTRY(cudaMemcpyAsync(cache->htil, htil0, sizeof(float) * BN, cudaMemcpyDeviceToDevice, st));
   else LTRY(cudaMemsetAsync(cache->htil, 0, sizeof(float) * BN, st));
@@ -474,10 +560,13 @@ int linrec_gilr_lstm_forward_f32(const linrec_gilr_lstm_params_f32* p, const flo
   ep.out[4] = s.iz;
   ep.ldo = n;
   LTRY(gemm(op, kEpiGates, ep, split3, nullptr, st));
+  mark(st, "gemm_gates");
   // 4-5. c = scan(f, i*z, c0); h = o * c
   LRC(linrec_scan_f32(gf, s.iz, c0, cache->c, T, BN, mode, nullptr, st));
+  mark(st, "scan_cell");
   k_mul<<<grid_for(N / 4, 256), 256, 0, st>>>(go, cache->c, h, N / 4);
   LTRY(cudaGetLastError());
+  mark(st, "h_out");
   return LINREC_OK;
 }
 
@@ -500,10 +589,13 @@ int linrec_gilr_lstm_backward_f32(const linrec_gilr_lstm_params_f32* p, const fl
   const float* gi = gf + N;
   const float* go = gi + N;
   const float* gz = go + N;
+  mark(st, "begin");
   // h = o * c  ->  dc = dh * o (d_o is formed inside k_lstm_dpre)
   k_mul<<<grid_for(N / 4, 256), 256, 0, st>>>(dh, go, s.dc, N / 4);
   LTRY(cudaGetLastError());
+  mark(st, "dc");
   LRC(linrec_scan_backward_f32(gf, c0, cache->c, s.dc, s.df, s.diz, dc0 ? dc0 : s.tmp0, T, BN, mode, nullptr, st));
+  mark(st, "scan_bwd_cell");
   const RowPlan rp = row_plan(R, n);
   k_lstm_dpre<<<dim3((unsigned)rp.nbx, (unsigned)rp.gy), rp.thr, 0, st>>>(gf, gi, go, gz, s.df, s.diz, dh, cache->c,
                                                                           s.dpre, s.part, R, n, rp.rpb);
@@ -512,9 +604,12 @@ int linrec_gilr_lstm_backward_f32(const linrec_gilr_lstm_params_f32* p, const fl
     k_colsum<<<(unsigned)((4 * n + 127) / 128), 128, 0, st>>>(s.part, rp.nbx, 4 * n, 4 * n, grads->bias);
     LTRY(cudaGetLastError());
   }
+  mark(st, "dpre_gates");
   // dU += dpre^T htil_prev ; dV += dpre^T x
   if (grads->U) LTRY(wgrad(s.dpre, 4 * n, 4 * n, cache->htil, n, R, grads->U, split3, s.split, st));
+  mark(st, "wgrad_U");
   if (grads->V) LTRY(wgrad(s.dpre, 4 * n, 4 * n, x, m, R, grads->V, split3, s.split, st));
+  mark(st, "wgrad_V");
   // dhp = dpre U  (gradient w.r.t. htil_prev); the row block after the last is 0
   {
     GemmOperands op;
@@ -531,6 +626,7 @@ int linrec_gilr_lstm_backward_f32(const linrec_gilr_lstm_params_f32* p, const fl
     ep.ldc = n;
     LTRY(gemm(op, kEpiPlain, ep, split3, nullptr, st));
     LTRY(cudaMemsetAsync(s.dhp + N, 0, sizeof(float) * BN, st));
+    mark(st, "dhtil_prev");
   }
   // surrogate backward on d_htil[t] = dhp[t+1] (pointer shift); dpre_s in df|diz
   float* dpre_s = s.df;
@@ -540,6 +636,7 @@ int linrec_gilr_lstm_backward_f32(const linrec_gilr_lstm_params_f32* p, const fl
   // dx = dpre V + [dg | di] [U_s; V_s]   (one K-concatenated GEMM)
   LTRY(cudaMemcpyAsync(s.uv, p->surrogate.U, sizeof(float) * n * m, cudaMemcpyDeviceToDevice, st));
   LTRY(cudaMemcpyAsync(s.uv + n * m, p->surrogate.V, sizeof(float) * n * m, cudaMemcpyDeviceToDevice, st));
+  mark(st, "prep");
   {
     GemmOperands op;
     op.a1 = s.dpre;
@@ -559,11 +656,13 @@ int linrec_gilr_lstm_backward_f32(const linrec_gilr_lstm_params_f32* p, const fl
     ep.C = dx;
     ep.ldc = m;
     LTRY(gemm(op, kEpiPlain, ep, split3, nullptr, st));
+    mark(st, "dx");
   }
   // htil0 feeds the surrogate scan and the t=1 gate input (:364-370)
   if (dhtil0) {
     k_add<<<grid_for(BN, 256), 256, 0, st>>>(s.tmp1, s.dhp, dhtil0, BN);
     LTRY(cudaGetLastError());
+    mark(st, "dhtil0");
   }
   return LINREC_OK;
 }

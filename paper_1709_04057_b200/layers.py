@@ -68,8 +68,26 @@ def _bind():
                                                  + tail)
     lib.linrec_gilr_lstm_backward_f32.argtypes = ([C.POINTER(_LstmParamsC)] + [_vp] * 3 + [C.POINTER(_LstmCacheC)]
                                                   + [_vp] + [C.POINTER(_LstmGradsC)] + [_vp] * 3 + tail)
+    lib.linrec_profile_end.argtypes = [C.c_char_p, C.c_size_t]
     lib._layers_bound = True
     return lib
+
+
+def profile_begin():
+    """Start per-stage timing of the layer calls on this thread (CUDA events
+    on each call's stream)."""
+    capi.check(_bind().linrec_profile_begin())
+
+
+def profile_end() -> dict:
+    """Stop timing; returns {stage: (total_ms, count)} in first-seen order."""
+    buf = C.create_string_buffer(1 << 16)
+    capi.check(_bind().linrec_profile_end(buf, len(buf)))
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, ms, cnt = line.split()
+        out[name] = (float(ms), int(cnt))
+    return out
 
 
 def _p(t):
@@ -201,6 +219,8 @@ class GilrLstmCache:
     c: torch.Tensor = None
 
     def allocate(self, T, b, n, device):
+        if self.c is not None and tuple(self.c.shape) == (T, b, n) and self.c.device == torch.device(device):
+            return self  # reuse (e.g. one cache per layer across training steps)
         kw = dict(dtype=torch.float32, device=device)
         self.sg = torch.empty(T, b, n, **kw)
         self.si = torch.empty(T, b, n, **kw)
