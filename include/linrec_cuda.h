@@ -237,8 +237,8 @@ int linrec_segment_fixup_backward_f64(const double* lam, const double* hprev, co
  * ([M][K], pitch lda) when a_mn == 0, MN-major ([K][M], pitch lda) when 1;
  * likewise B.  precision LINREC_PREC_FP32 runs 3xTF32 (hi/lo operand split,
  * fp32-grade results), LINREC_PREC_TF32 one TF32 pass.  k_splits > 1 splits
- * K across CTAs and reduces the partials (scratch: k_splits*M*N floats) in a
- * fixed order (deterministic).  Pitches and pointers must be 16-byte
+ * K across CTA pairs and reduces the partials (scratch: at least
+ * linrec_gemm_scratch_bytes(M, N, k_splits)) in a fixed order (deterministic).  Pitches and pointers must be 16-byte
  * aligned.  The dense transforms of the reference's layers
  * (tensor.hpp:104-141 gemm_nn/nt/tn, :249-308) map onto it. */
 #define LINREC_PREC_FP32 0
@@ -246,9 +246,10 @@ int linrec_segment_fixup_backward_f64(const double* lam, const double* hprev, co
 int linrec_gemm_f32(const float* A, int a_mn, int64_t lda, const float* B, int b_mn, int64_t ldb, float* C,
                     int64_t ldc, int64_t M, int64_t N, int64_t K, int accumulate, int precision, int k_splits,
                     float* scratch, void* stream);
-/* split count linrec_gemm_f32 would pick for an M x N x K product (fills the
- * persistent grid); scratch for it is k_splits*M*N floats. */
+/* split count the layers pick for an M x N x K product (fills the persistent
+ * grid of CTA pairs) and the scratch a given split count needs. */
 int linrec_gemm_splits(int64_t M, int64_t N, int64_t K);
+size_t linrec_gemm_scratch_bytes(int64_t M, int64_t N, int k_splits);
 
 /* ---- GILR and GILR-LSTM layers (layers.hpp:23-375) ------------------------ *
  * The paper's recurrent layers on the GPU: gate projections on the tensor

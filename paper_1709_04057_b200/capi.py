@@ -67,6 +67,8 @@ def _load():
     lib.linrec_gemm_f32.argtypes = [_vp, _int, _i64, _vp, _int, _i64, _vp, _i64, _i64, _i64, _i64, _int, _int,
                                     _int, _vp, _vp]
     lib.linrec_gemm_splits.argtypes = [_i64, _i64, _i64]
+    lib.linrec_gemm_scratch_bytes.restype = C.c_size_t
+    lib.linrec_gemm_scratch_bytes.argtypes = [_i64, _i64, _int]
     lib.linrec_segment_prod_rows.restype = _i64
     lib.linrec_segment_prod_rows.argtypes = [_i64, _i64, _int, _int]
     lib.linrec_segment_tile_rows.restype = _i64
@@ -181,6 +183,10 @@ def gemm(A, a_mn, lda, B, b_mn, ldb, C, ldc, M, N, K, accumulate=False, precisio
 
 def gemm_splits(M, N, K) -> int:
     return int(lib.linrec_gemm_splits(M, N, K))
+
+
+def gemm_scratch_bytes(M, N, k_splits) -> int:
+    return int(lib.linrec_gemm_scratch_bytes(M, N, k_splits))
 
 
 class Workspace:

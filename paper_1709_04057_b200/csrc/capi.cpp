@@ -831,4 +831,9 @@ int linrec_gemm_f32(const float* A, int a_mn, int64_t lda, const float* B, int b
 
 int linrec_gemm_splits(int64_t M, int64_t N, int64_t K) { return linrec_impl::gemm_splits_for(M, N, K); }
 
+size_t linrec_gemm_scratch_bytes(int64_t M, int64_t N, int k_splits) {
+  if (M < 1 || N < 1) return 0;
+  return (size_t)linrec_impl::gemm_partial_floats(M, N, k_splits) * sizeof(float);
+}
+
 }  // extern "C"

@@ -11,6 +11,7 @@ namespace {
 
 using linrec_dev::tc::BK;
 using linrec_dev::tc::BM;
+using linrec_dev::tc::BN;
 
 // 2-D fp32 tensor map: `inner` contiguous elements, `outer` rows at `pitch`
 // elements; box {32, box_outer}.  swizzle: 128B (K-major operands) or
@@ -47,12 +48,15 @@ cudaError_t operand_map(CUtensorMap* map, const float* p, bool mn, int64_t rows,
   return make_tmap(map, p, K, rows, pitch, tile_rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-__global__ void k_splitk_reduce(const float* __restrict__ part, int splits, int64_t MN, int64_t N, int64_t ldc,
-                                float* __restrict__ C, int accumulate) {
+// Partials [nz][Mp][ldp] (Mp = M rounded up to the 256-row tile, so tail
+// rows of one split never land in the next) -> C, summed in split order.
+__global__ void k_splitk_reduce(const float* __restrict__ part, int splits, int64_t M, int64_t Mp, int64_t N,
+                                int64_t ldp, int64_t ldc, float* __restrict__ C, int accumulate) {
+  const int64_t MN = M * N;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < MN; i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += part[(size_t)z * MN + i];  // fixed order: deterministic
     const int64_t r = i / N, c = i - r * N;
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += part[((int64_t)z * Mp + r) * ldp + c];  // fixed order: deterministic
     float* d = C + r * ldc + c;
     *d = accumulate ? *d + s : s;
   }
@@ -67,72 +71,97 @@ int sm_count() {
   return n;
 }
 
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// Output map over a [rows][cols] fp32 plane (pitch elements), 32x32 boxes,
+// 128B swizzle (the epilogue's staging layout).
+cudaError_t out_map(CUtensorMap* map, float* ptr, int64_t cols, int64_t rows, int64_t pitch) {
+  return make_tmap(map, ptr, cols, rows, pitch, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 template <bool A_MN, bool B_MN, int NB, bool SPLIT3, int EPI>
-cudaError_t launch_cfg(const GemmOperands& op, linrec_dev::tc::GemmParams p, cudaStream_t st) {
-  constexpr int BN = 128;
-  constexpr int STAGES = SPLIT3 ? 3 : 6;
-  using Cfg = linrec_dev::tc::GemmCfg<A_MN, B_MN, BN, NB, STAGES, SPLIT3>;
+cudaError_t launch_cfg(const GemmOperands& op, const GemmEpilogue& ep, linrec_dev::tc::GemmParams p,
+                       float* partial, int64_t Mp, int64_t ldp, cudaStream_t st) {
+  constexpr int STAGES = SPLIT3 ? 3 : 5;
+  using Cfg = linrec_dev::tc::GemmCfg<A_MN, B_MN, NB, STAGES, SPLIT3>;
   constexpr int UNITS = Cfg::UNITS;
+  constexpr int BROWS = NB == 1 ? BN / 2 : UNITS;  // rows of one K-major B box
   const int64_t b_rows = NB == 1 ? op.units : (NB - 1) * op.b_bstride + op.units;
   CUtensorMap a1, b1, a2, b2;
+  linrec_dev::tc::OutMaps om;
   cudaError_t e;
   if ((e = operand_map(&a1, op.a1, A_MN, op.M, op.K1, op.lda1, BM)) != cudaSuccess) return e;
-  if ((e = operand_map(&b1, op.b1, B_MN, b_rows, op.K1, op.ldb1, UNITS)) != cudaSuccess) return e;
+  if ((e = operand_map(&b1, op.b1, B_MN, b_rows, op.K1, op.ldb1, BROWS)) != cudaSuccess) return e;
   if (op.a2 != nullptr) {
     if ((e = operand_map(&a2, op.a2, A_MN, op.M, op.K2, op.lda2, BM)) != cudaSuccess) return e;
-    if ((e = operand_map(&b2, op.b2, B_MN, b_rows, op.K2, op.ldb2, UNITS)) != cudaSuccess) return e;
+    if ((e = operand_map(&b2, op.b2, B_MN, b_rows, op.K2, op.ldb2, BROWS)) != cudaSuccess) return e;
   } else {
     a2 = a1;
     b2 = b1;
   }
-  p.ntm = (int)((op.M + BM - 1) / BM);
+  if (EPI == linrec_dev::tc::kEpiPlain) {
+    if (partial) e = out_map(&om.m[0], partial, op.units, Mp * p.nz, ldp);
+    else e = out_map(&om.m[0], ep.C, op.units, op.M, ep.ldc);
+    if (e != cudaSuccess) return e;
+  } else {
+    const int nout = EPI == linrec_dev::tc::kEpiGilr ? 3 : 5;
+    for (int i = 0; i < nout; ++i)
+      if ((e = out_map(&om.m[i], ep.out[i], op.units, op.M, ep.ldo)) != cudaSuccess) return e;
+  }
+  p.ntm = (int)((op.M + 2 * BM - 1) / (2 * BM));
   p.ntn = (int)((op.units + UNITS - 1) / UNITS);
   p.b_bstride = (int)op.b_bstride;
-  auto kern = linrec_dev::tc::k_gemm<A_MN, B_MN, BN, NB, STAGES, SPLIT3, EPI>;
+  auto kern = linrec_dev::tc::k_gemm<A_MN, B_MN, NB, STAGES, SPLIT3, EPI>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
   if (e != cudaSuccess) return e;
   const int64_t ntiles = (int64_t)p.ntm * p.ntn * p.nz;
-  const int grid = (int)(ntiles < sm_count() ? ntiles : sm_count());
-  kern<<<grid, linrec_dev::tc::kThreads, Cfg::SMEM, st>>>(a1, b1, a2, b2, p);
+  const int64_t clusters = sm_count() / 2;
+  const int grid = 2 * (int)(ntiles < clusters ? ntiles : clusters);
+  kern<<<grid, linrec_dev::tc::kThreads, Cfg::SMEM, st>>>(a1, b1, a2, b2, om, p);
   return cudaGetLastError();
 }
 
 template <bool SPLIT3>
-cudaError_t dispatch(const GemmOperands& op, int epi, const linrec_dev::tc::GemmParams& p, cudaStream_t st) {
+cudaError_t dispatch(const GemmOperands& op, int epi, const GemmEpilogue& ep, const linrec_dev::tc::GemmParams& p,
+                     float* partial, int64_t Mp, int64_t ldp, cudaStream_t st) {
   using namespace linrec_dev::tc;
   if (epi == kEpiPlain) {
     if (op.nb != 1) return cudaErrorInvalidValue;
-    if (!op.a_mn && !op.b_mn) return launch_cfg<false, false, 1, SPLIT3, kEpiPlain>(op, p, st);
-    if (!op.a_mn && op.b_mn) return launch_cfg<false, true, 1, SPLIT3, kEpiPlain>(op, p, st);
-    if (op.a_mn && op.b_mn) return launch_cfg<true, true, 1, SPLIT3, kEpiPlain>(op, p, st);
-    return launch_cfg<true, false, 1, SPLIT3, kEpiPlain>(op, p, st);
+    if (!op.a_mn && !op.b_mn) return launch_cfg<false, false, 1, SPLIT3, kEpiPlain>(op, ep, p, partial, Mp, ldp, st);
+    if (!op.a_mn && op.b_mn) return launch_cfg<false, true, 1, SPLIT3, kEpiPlain>(op, ep, p, partial, Mp, ldp, st);
+    if (op.a_mn && op.b_mn) return launch_cfg<true, true, 1, SPLIT3, kEpiPlain>(op, ep, p, partial, Mp, ldp, st);
+    return launch_cfg<true, false, 1, SPLIT3, kEpiPlain>(op, ep, p, partial, Mp, ldp, st);
   }
   if (op.a_mn || op.b_mn) return cudaErrorInvalidValue;
-  if (epi == kEpiGilr && op.nb == 2) return launch_cfg<false, false, 2, SPLIT3, kEpiGilr>(op, p, st);
-  if (epi == kEpiGates && op.nb == 4) return launch_cfg<false, false, 4, SPLIT3, kEpiGates>(op, p, st);
+  if (epi == kEpiGilr && op.nb == 2) return launch_cfg<false, false, 2, SPLIT3, kEpiGilr>(op, ep, p, nullptr, 0, 0, st);
+  if (epi == kEpiGates && op.nb == 4) return launch_cfg<false, false, 4, SPLIT3, kEpiGates>(op, ep, p, nullptr, 0, 0, st);
   return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
 int gemm_splits_for(int64_t M, int64_t N, int64_t K) {
-  const int64_t tiles = ((M + BM - 1) / BM) * ((N + 127) / 128);
+  const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
   const int64_t kb = (K + BK - 1) / BK;
-  const int64_t sms = sm_count();
-  if (tiles >= sms || kb < 8) return 1;
-  // fill the persistent grid evenly: the split count whose last wave is
-  // fullest, preferring fewer partials, with >= 4 k-blocks per split
+  const int64_t clusters = sm_count() / 2;
+  if (tiles >= clusters || kb < 8) return 1;
+  // fill the persistent grid of CTA pairs evenly: the split count whose last
+  // wave is fullest, preferring fewer partials, with >= 4 k-blocks per split
   int best = 1;
   double best_eff = 0.0;
-  for (int s = 1; s <= 32 && s <= kb / 4; ++s) {
-    const double waves = double(tiles * s) / double(sms);
-    const double eff = waves / double((tiles * s + sms - 1) / sms);
+  for (int s = 1; s <= 64 && s <= kb / 4; ++s) {
+    const double waves = double(tiles * s) / double(clusters);
+    const double eff = waves / double((tiles * s + clusters - 1) / clusters);
     if (eff > best_eff + 0.02) {
       best_eff = eff;
       best = s;
     }
   }
   return best;
+}
+
+int64_t gemm_partial_floats(int64_t M, int64_t N, int splits) {
+  return splits > 1 ? (int64_t)splits * round_up(M, 2 * BM) * round_up(N, 4) : 0;
 }
 
 cudaError_t gemm_tf32(const GemmOperands& op, int epi, const GemmEpilogue& ep, cudaStream_t st) {
@@ -152,28 +181,25 @@ cudaError_t gemm_tf32(const GemmOperands& op, int epi, const GemmEpilogue& ep, c
   p.kb = kb_per;
   p.kb_total = kb_total;
   p.kchunk = ep.split3 ? 4 : 16;  // K = 128 (3xTF32) / 512 (TF32) per TMEM accumulation
-  p.ldc = (int)ep.ldc;
-  p.C = ep.C;
   p.mode = ep.accumulate ? 1 : 0;
   p.act = ep.act;
-  p.ldo = ep.ldo;
   for (int i = 0; i < 4; ++i) p.bias[i] = ep.bias[i];
-  for (int i = 0; i < 5; ++i) p.out[i] = ep.out[i];
   float* partial = nullptr;
+  const int64_t Mp = round_up(op.M, 2 * BM), ldp = round_up(op.units, 4);
   if (splits > 1) {
     if (epi != linrec_dev::tc::kEpiPlain || ep.scratch == nullptr) return cudaErrorInvalidValue;
     partial = ep.scratch;
-    p.C = partial;
-    p.ldc = (int)op.units;
     p.mode = 2;
+    p.Mp = (int)Mp;
   }
-  cudaError_t e = ep.split3 ? dispatch<true>(op, epi, p, st) : dispatch<false>(op, epi, p, st);
+  cudaError_t e = ep.split3 ? dispatch<true>(op, epi, ep, p, partial, Mp, ldp, st)
+                            : dispatch<false>(op, epi, ep, p, partial, Mp, ldp, st);
   if (e != cudaSuccess) return e;
   if (splits > 1) {
     const int64_t MN = op.M * op.units;
     const int64_t blocks = (MN + 255) / 256;
-    k_splitk_reduce<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(partial, splits, MN, op.units, ep.ldc,
-                                                                               ep.C, ep.accumulate ? 1 : 0);
+    k_splitk_reduce<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(
+        partial, splits, op.M, Mp, op.units, ldp, ep.ldc, ep.C, ep.accumulate ? 1 : 0);
     e = cudaGetLastError();
   }
   return e;

@@ -11,25 +11,36 @@
 //   dpre^T * x     (weight gradients, split-K)    A MN-major, B MN-major
 // The K range may be the concatenation of two (A, B) operand pairs (the gate
 // projection [x | htil_{t-1}] * [V | U]^T in one pass).  A K-major B may be
-// "blocked": the BN rows of a tile are NB sub-boxes taken from NB row blocks
+// "blocked": the B rows of a tile are NB sub-boxes taken from NB row blocks
 // of the weight (rows q*bstride + j0 ..), so the f/i/o/z (or g/i) rows of the
 // same hidden units land in one tile and the epilogue sees every gate of a
 // unit without any host-side weight permutation.
 //
-// Precision: kind::tf32 reads 10 mantissa bits of each operand.  With SPLIT3
-// the kernel runs 3xTF32: two split warps write lo = v - tf32(v) of every
-// staged A and B tile next to it and the MMA warp issues
-//   A_lo*B + A*B_lo + A*B   per k-step,
-// which recovers ~fp32 accuracy (the default for the layers); without it the
-// kernel is plain TF32.
+// CTA pair (cluster of 2, tcgen05 cta_group::2): one MMA is M=256 x N=256 x
+// K=8; CTA r holds A rows [128r, 128r+128) and B rows [128r, 128r+128) of the
+// tile in its own shared memory (each SM streams half of each operand) and
+// rows [128r, +128) x all 256 columns of the accumulator in its TMEM.  The
+// leader CTA's single MMA thread issues for both.
 //
-// Structure: persistent (grid <= #SMs, one CTA per SM), 256 threads:
-//   warp 0      TMA producer (STAGES-deep ring of 128B-swizzled boxes)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//               (M=128, N=BN, K=8), two TMEM accumulators (2*BN columns) so
-//               the epilogue of tile t overlaps the mainloop of tile t+1
-//   warps 2-3   3xTF32 split (SPLIT3 only)
-//   warps 4-7   epilogue: tcgen05.ld, fused epilogue, stores
+// Precision: kind::tf32 reads 10 mantissa bits of each operand.  With SPLIT3
+// the kernel runs 3xTF32: split warps write lo = v - tf32(v) of every staged
+// A and B tile next to it and the MMA issues  A_lo*B + A*B_lo + A*B  per
+// k-step (~fp32 accuracy, the layers' default).  The tensor-core accumulator
+// itself drops bits at every K=8 step, so K is accumulated in chunks of KCHUNK
+// k-blocks in TMEM and the chunks are summed in fp32 registers by the
+// epilogue ("promotion"): the error no longer grows with K.
+//
+// Persistent, 384 threads per CTA:
+//   warp 0      TMA producer (STAGES-deep ring)
+//   warp 1      TMEM allocator (cta_group::2); leader: tcgen05.mma issuer,
+//               two 256-column accumulators so the epilogue of tile t
+//               overlaps the mainloop of tile t+1
+//   warps 2-3   3xTF32 split (SPLIT3) and relay of "stage landed + split" to
+//               the leader
+//   warps 4-11  epilogue: 2 warps per TMEM lane quadrant, 128 fp32 register
+//               accumulators each; fused epilogue -> 128B-swizzled smem box
+//               -> TMA store (or TMA reduce-add for C += A*B)
+//   setmaxnreg moves registers from warps 0-3 (56) to the epilogue (224).
 //
 // Shared-memory operand layouts (canonical UMMA layouts):
 //   K-major:  TMA box {32 elems = 128 B, rows}, SWIZZLE_128B
@@ -48,45 +59,135 @@
 namespace linrec_dev {
 namespace tc {
 
-constexpr int BM = 128;
-constexpr int BK = 32;  // fp32 elements per k-block = one 128-byte swizzle row
-constexpr int kThreads = 256;
+constexpr int BM = 128;      // A rows per CTA (the MMA's M = 256 spans the pair)
+constexpr int BN = 256;      // MMA N; each CTA stages BN/2 = 128 B rows
+constexpr int BK = 32;       // fp32 elements per k-block = one 128-byte swizzle row
+constexpr int kThreads = 384;
+constexpr int kEpiWarps = 8;
 
-// ---- tcgen05 wrappers -------------------------------------------------------
-__device__ __forceinline__ void tmem_alloc(uint32_t* smem_dst, uint32_t ncols) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
+// ---- tcgen05 / cluster wrappers ----------------------------------------------
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Address of the same shared variable in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait_cluster(bar, parity)) return;
+  SpinGuard g;
+  while (!mbar_try_wait_cluster(bar, parity)) g.tick();
+}
+
+// 2-D TMA load into this CTA's smem whose completion is signalled on the
+// leader CTA's mbarrier (cta_group::2 form).
+__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                                 uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* smem_src, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* smem_src, int32_t c0,
+                                                  int32_t c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_alloc2(uint32_t* smem_dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
                "r"(ncols)
                : "memory");
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// Arrive on an mbarrier once all previously issued tcgen05.mma have completed.
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
+// Arrive on the mbarrier at this smem offset in both CTAs of the pair once
+// all previously issued tcgen05.mma have completed.
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
 }
-// 32 lanes x 8 consecutive fp32 columns; thread i of the warp gets lane
-// (base lane + i).  The caller waits with tmem_wait_ld().
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
+// 32 lanes x 32 consecutive fp32 columns; thread i of the warp gets lane
+// (base lane + i).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+// 32 lanes x 16 consecutive fp32 columns.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 
 // UMMA shared-memory descriptor (sm_100 SmemDescriptor):
 // start[0,14) LBO[16,30) SBO[32,46) version[46,48)=1 base[49,52) layout[61,64)
@@ -129,100 +230,149 @@ enum Epi : int { kEpiPlain = 0, kEpiGilr = 1, kEpiGates = 2 };
 struct GemmParams {
   int M;             // output rows
   int units;         // output columns per block (N for NB == 1)
-  int ntm, ntn, nz;  // tiles along M, along units, K splits
+  int ntm, ntn, nz;  // tiles along M (256 rows), along units, K splits
   int kb1, kb, kb_total;
   int kchunk;        // k-blocks per TMEM accumulation unit (promotion to fp32 registers)
   int b_bstride;     // row offset between B blocks (blocked K-major B)
-  // plain epilogue
-  float* C;
-  int ldc;
-  int mode;          // 0 store, 1 accumulate, 2 split-K partial (C + z*M*ldc)
-  // layer epilogues
+  int mode;          // plain: 0 store, 1 accumulate (TMA reduce-add), 2 split-K partial (rows z*Mp + row)
+  int Mp;            // partial rows per split (M rounded up to the 256-row tile)
   int act;           // candidate activation (common.hpp:49-71): 0 tanh, 1 identity, 2 relu
-  int64_t ldo;       // pitch (elements) of the [M][units] output planes
   const float* bias[4];
-  float* out[5];
 };
 
-template <bool A_MN, bool B_MN, int BN, int NB, int STAGES, bool SPLIT3>
+template <bool A_MN, bool B_MN, int NB, int STAGES, bool SPLIT3>
 struct GemmCfg {
   using GA = TileGeom<A_MN, BM>;
-  using GB = TileGeom<B_MN, BN>;
+  using GB = TileGeom<B_MN, BN / 2>;
   static constexpr int UNITS = BN / NB;  // output columns (hidden units) per tile
-  static constexpr int STAGE_BYTES = GA::BYTES + GB::BYTES;
-  static constexpr int LO_OFF = STAGES * STAGE_BYTES;  // 3xTF32 lo tiles, same layout
-  static constexpr int OFF_BAR = LO_OFF + (SPLIT3 ? STAGES * STAGE_BYTES : 0);
+  static constexpr int STAGE_BYTES = GA::BYTES + GB::BYTES;  // this CTA's halves
+  static constexpr int LO_OFF = STAGES * STAGE_BYTES;        // 3xTF32 lo tiles, same layout
+  static constexpr int EPI_OFF = LO_OFF + (SPLIT3 ? STAGES * STAGE_BYTES : 0);
+  static constexpr int EPI_BYTES = 32 * 128;                  // one 32x32 fp32 staging box per epilogue warp
+  static constexpr int OFF_BAR = EPI_OFF + kEpiWarps * EPI_BYTES;
   static constexpr int NBARS = 3 * STAGES + 4;
   static constexpr int SMEM = OFF_BAR + NBARS * 8 + 16 + 1024;  // + alignment slack
-  static constexpr uint32_t IDESC = idesc_tf32(BM, BN, A_MN, B_MN);
+  static constexpr uint32_t IDESC = idesc_tf32(2 * BM, BN, A_MN, B_MN);
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static_assert(!B_MN || NB == 1, "blocked B operands are K-major weights");
-  static_assert(UNITS % 8 == 0 && (NB == 1 || UNITS >= 8), "epilogue works in 8-column chunks");
+  static_assert(NB == 1 || NB == 2 || NB == 4, "NB");
+  static_assert(SMEM <= 232448, "shared memory");
 };
 
-__device__ __forceinline__ float sigmoidf_(float z) { return 1.f / (1.f + expf(-z)); }
-__device__ __forceinline__ float actf_(int a, float z) { return a == 0 ? tanhf(z) : a == 1 ? z : fmaxf(z, 0.f); }
-
-__device__ __forceinline__ void store8(float* dst, const float (&v)[8], bool full, int left) {
-  if (full) {
-    reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
-    reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (i < left) dst[i] = v[i];
-  }
+// Activations on the SFU (ex2.approx / rcp.approx, ~2 ulp each): far inside
+// the layers' 2e-5 normwise bar and branch-free.  tanh via 1 - 2/(e^{2z}+1)
+// keeps an absolute error of a few 1e-8 near 0.
+__device__ __forceinline__ float ex2_(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
+__device__ __forceinline__ float rcp_(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sigmoidf_(float z) { return rcp_(1.f + ex2_(-1.4426950408889634f * z)); }
+__device__ __forceinline__ float tanhf_(float z) {
+  const float e = ex2_(2.8853900817779268f * fminf(fmaxf(z, -15.f), 15.f));
+  return fmaf(-2.f, rcp_(e + 1.f), 1.f);
+}
+__device__ __forceinline__ float actf_(int a, float z) { return a == 0 ? tanhf_(z) : a == 1 ? z : fmaxf(z, 0.f); }
+// bias[u0 + lane] for this warp's 32 units (0 beyond `units`); element i is
+// then __shfl_sync(.., i) -- one load per lane instead of 32 per thread.
+__device__ __forceinline__ float bias_lane(const float* b, int u0, int lane, int units) {
+  const int j = u0 + lane;
+  return j < units ? __ldg(b + j) : 0.f;
+}
+#define LINREC_BCAST(v, i) __shfl_sync(0xffffffffu, (v), (i))
 
 // tf32 part the tensor core uses (it ignores the low 13 mantissa bits).
 __device__ __forceinline__ float tf32_hi(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
 
-template <bool A_MN, bool B_MN, int BN, int NB, int STAGES, bool SPLIT3, int EPI>
-__global__ void __launch_bounds__(kThreads, 1)
+// One 32-row x 32-column fp32 box in the 128B-swizzled layout TMA expects:
+// lane = row; 16-byte chunk j of the row lives at chunk (j ^ (row & 7)).
+__device__ __forceinline__ void stage_row(unsigned char* box, int lane, const float (&v)[32]) {
+  float4* row = reinterpret_cast<float4*>(box + lane * 128);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) row[j ^ (lane & 7)] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+}
+
+// Start writing the staged box to global memory (one lane).  `red` = TMA
+// reduce-add instead of a store.  box_wait() must precede the next
+// stage_row() into the same box: callers compute the next values first, so
+// the TMA engine's read of the box overlaps that math.
+__device__ __forceinline__ void flush_box(const CUtensorMap* map, unsigned char* box, int lane, int c0, int c1,
+                                          bool red) {
+  fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) {
+    if (red) tma_reduce_add_2d(map, box, c0, c1);
+    else tma_store_2d(map, box, c0, c1);
+    bulk_commit();
+  }
+}
+__device__ __forceinline__ void box_wait(int lane) {
+  if (lane == 0) bulk_wait_read0();
+  __syncwarp();
+}
+
+struct OutMaps {
+  CUtensorMap m[5];
+};
+
+template <bool A_MN, bool B_MN, int NB, int STAGES, bool SPLIT3, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensorMap tb1,
-       const __grid_constant__ CUtensorMap ta2, const __grid_constant__ CUtensorMap tb2, const GemmParams p) {
-  using Cfg = GemmCfg<A_MN, B_MN, BN, NB, STAGES, SPLIT3>;
+       const __grid_constant__ CUtensorMap ta2, const __grid_constant__ CUtensorMap tb2,
+       const __grid_constant__ OutMaps om, const GemmParams p) {
+  using Cfg = GemmCfg<A_MN, B_MN, NB, STAGES, SPLIT3>;
   using GA = typename Cfg::GA;
   using GB = typename Cfg::GB;
   constexpr int UNITS = Cfg::UNITS;
+  constexpr int HALF = UNITS / 2;  // units per epilogue warp of a quadrant pair
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint64_t* empty = full + STAGES;
-  uint64_t* split = empty + STAGES;
-  uint64_t* acc_full = split + STAGES;
+  uint64_t* ready = empty + STAGES;  // leader: stage landed and split in both CTAs (SPLIT3)
+  uint64_t* acc_full = ready + STAGES;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int ncl = gridDim.x >> 1, cid = blockIdx.x >> 1;
   const int ntiles = p.ntm * p.ntn * p.nz;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&split[s], 64);
+      mbar_init(&ready[s], 2 * 64);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], 128);
+      mbar_init(&acc_empty[a], 2 * kEpiWarps);
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  if (warp == 1) tmem_alloc2(tmem_slot, Cfg::TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {  // ------------------------------------------ TMA producer
+    setmaxnreg_dec<56>();
     if (lane == 0) {
       prefetch_tmap(&ta1);
       prefetch_tmap(&tb1);
+      const uint32_t full_leader = mapa(smem_u32(full), 0);
       uint32_t it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = cid; t < ntiles; t += ncl) {
         const int tn = t % p.ntn, tm = (t / p.ntn) % p.ntm, z = t / (p.ntn * p.ntm);
-        const int m0 = tm * BM, u0 = tn * UNITS;
+        const int m0 = tm * 2 * BM + (int)rank * BM, u0 = tn * UNITS;
         const int kb_begin = z * p.kb, kb_end = min(kb_begin + p.kb, p.kb_total);
         for (int kb = kb_begin; kb < kb_end; ++kb, ++it) {
           const int s = it % STAGES;
@@ -233,43 +383,57 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
           const int k0 = (second ? kb - p.kb1 : kb) * BK;
           unsigned char* sa = smem + s * Cfg::STAGE_BYTES;
           unsigned char* sb = sa + GA::BYTES;
-          mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+          // SPLIT3: local completion (the split warps relay to the leader);
+          // else both CTAs' loads complete on the leader's barrier, which
+          // the leader armed with the bytes of both halves.
+          const uint32_t bar = full_leader + 8u * (uint32_t)s;
+          if (SPLIT3) mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+          else if (leader) mbar_arrive_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
+#define LINREC_LOAD(dst, map, c0, c1)                          \
+  do {                                                         \
+    if (SPLIT3) tma_load_2d_nohint(dst, map, c0, c1, &full[s]); \
+    else tma_load_2d_pair(dst, map, c0, c1, bar);              \
+  } while (0)
           if (A_MN) {
 #pragma unroll
-            for (int j = 0; j < GA::NBOX; ++j) tma_load_2d_nohint(sa + j * GA::BOX_BYTES, ta, m0 + 32 * j, k0, &full[s]);
+            for (int j = 0; j < GA::NBOX; ++j) LINREC_LOAD(sa + j * GA::BOX_BYTES, ta, m0 + 32 * j, k0);
           } else {
-            tma_load_2d_nohint(sa, ta, k0, m0, &full[s]);
+            LINREC_LOAD(sa, ta, k0, m0);
           }
           if (B_MN) {
 #pragma unroll
-            for (int j = 0; j < GB::NBOX; ++j) tma_load_2d_nohint(sb + j * GB::BOX_BYTES, tb, u0 + 32 * j, k0, &full[s]);
+            for (int j = 0; j < GB::NBOX; ++j)
+              LINREC_LOAD(sb + j * GB::BOX_BYTES, tb, u0 + (int)rank * (BN / 2) + 32 * j, k0);
+          } else if (NB == 1) {
+            LINREC_LOAD(sb, tb, k0, u0 + (int)rank * (BN / 2));
           } else {
 #pragma unroll
-            for (int q = 0; q < NB; ++q)
-              tma_load_2d_nohint(sb + q * UNITS * 128, tb, k0, q * p.b_bstride + u0, &full[s]);
+            for (int qq = 0; qq < NB / 2; ++qq)
+              LINREC_LOAD(sb + qq * UNITS * 128, tb, k0, ((int)rank * (NB / 2) + qq) * p.b_bstride + u0);
           }
+#undef LINREC_LOAD
         }
       }
     }
   } else if (warp == 1) {  // ------------------------------------- MMA issuer
-    if (lane == 0) {
+    setmaxnreg_dec<56>();
+    if (leader && lane == 0) {
       // One accumulation unit = KCHUNK k-blocks of one tile, accumulated from
-      // zero in TMEM slot (unit & 1); the epilogue sums the units in fp32
-      // registers (the tensor-core accumulator loses ~2^-23 per K=8 step).
+      // zero in TMEM slot (unit & 1); the epilogue sums the units in fp32.
       uint32_t it = 0, unit = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = cid; t < ntiles; t += ncl) {
         const int z = t / (p.ntn * p.ntm);
         const int kb_begin = z * p.kb, kb_end = min(kb_begin + p.kb, p.kb_total);
         for (int c0 = kb_begin; c0 < kb_end; c0 += p.kchunk, ++unit) {
           const uint32_t as = unit & 1, use = unit >> 1;
-          if (use > 0) mbar_wait(&acc_empty[as], (use - 1) & 1);
+          if (use > 0) mbar_wait_cluster(&acc_empty[as], (use - 1) & 1);
           tc_fence_after();
           const uint32_t acc = tmem + as * BN;
           const int c1 = min(c0 + p.kchunk, kb_end);
           for (int kb = c0; kb < c1; ++kb, ++it) {
             const int s = it % STAGES;
-            mbar_wait(&full[s], (it / STAGES) & 1);
-            if (SPLIT3) mbar_wait(&split[s], (it / STAGES) & 1);
+            if (SPLIT3) mbar_wait_cluster(&ready[s], (it / STAGES) & 1);
+            else mbar_wait_cluster(&full[s], (it / STAGES) & 1);
             tc_fence_after();
             const uint32_t sa = smem_u32(smem + s * Cfg::STAGE_BYTES);
             const uint32_t sb = sa + GA::BYTES;
@@ -281,23 +445,25 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
               if (SPLIT3) {
                 const uint64_t adl = smem_desc(sa + Cfg::LO_OFF + kk * GA::KSTEP, GA::LBO, GA::SBO, GA::LAYOUT);
                 const uint64_t bdl = smem_desc(sb + Cfg::LO_OFF + kk * GB::KSTEP, GB::LBO, GB::SBO, GB::LAYOUT);
-                mma_tf32(acc, adl, bd, Cfg::IDESC, accum);
-                mma_tf32(acc, ad, bdl, Cfg::IDESC, 1u);
+                mma_tf32_pair(acc, adl, bd, Cfg::IDESC, accum);
+                mma_tf32_pair(acc, ad, bdl, Cfg::IDESC, 1u);
                 accum = 1u;
               }
-              mma_tf32(acc, ad, bd, Cfg::IDESC, accum);
+              mma_tf32_pair(acc, ad, bd, Cfg::IDESC, accum);
             }
-            mma_commit(&empty[s]);  // stage (and its lo tiles) free once these MMAs have read it
+            mma_commit_pair(&empty[s]);  // both CTAs' stage s (and lo tiles) free once read
           }
-          mma_commit(&acc_full[as]);
+          mma_commit_pair(&acc_full[as]);
         }
       }
     }
-  } else if (warp < 4) {  // --------------------------------------- 3xTF32 split
+  } else if (warp < 4) {  // -------------------------------------- 3xTF32 split
+    setmaxnreg_dec<56>();
     if (SPLIT3) {
       const int st = threadIdx.x - 64;  // 0..63
+      const uint32_t ready_leader = mapa(smem_u32(ready), 0);
       uint32_t it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = cid; t < ntiles; t += ncl) {
         const int z = t / (p.ntn * p.ntm);
         const int kb_begin = z * p.kb, kb_end = min(kb_begin + p.kb, p.kb_total);
         for (int kb = kb_begin; kb < kb_end; ++kb, ++it) {
@@ -305,107 +471,129 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
           mbar_wait(&full[s], (it / STAGES) & 1);
           const float4* src = reinterpret_cast<const float4*>(smem + s * Cfg::STAGE_BYTES);
           float4* dst = reinterpret_cast<float4*>(smem + Cfg::LO_OFF + s * Cfg::STAGE_BYTES);
-#pragma unroll 8
+#pragma unroll 4
           for (int e = st; e < Cfg::STAGE_BYTES / 16; e += 64) {
             const float4 v = src[e];
             dst[e] = make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z), v.w - tf32_hi(v.w));
           }
           fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
-          mbar_arrive(&split[s]);
+          mbar_arrive_cluster(ready_leader + 8u * (uint32_t)s);
         }
       }
     }
   } else {  // ------------------------------------------------------- epilogue
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    setmaxnreg_inc<224>();
+    const int q = warp & 3;          // TMEM lane quadrant this warp may access
+    const int hf = (warp - 4) >> 2;  // which half of the tile's units
+    unsigned char* box = smem + Cfg::EPI_OFF + (warp - 4) * Cfg::EPI_BYTES;
+    const uint32_t acc_empty_leader = mapa(smem_u32(acc_empty), 0);
     uint32_t unit = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int t = cid; t < ntiles; t += ncl) {
       const int tn = t % p.ntn, tm = (t / p.ntn) % p.ntm, z = t / (p.ntn * p.ntm);
       const int kb_begin = z * p.kb, kb_end = min(kb_begin + p.kb, p.kb_total);
-      float acc[BN];
+      float acc[128];
 #pragma unroll
-      for (int i = 0; i < BN; ++i) acc[i] = 0.f;
+      for (int i = 0; i < 128; ++i) acc[i] = 0.f;
       for (int c0 = kb_begin; c0 < kb_end; c0 += p.kchunk, ++unit) {
         const uint32_t as = unit & 1, use = unit >> 1;
         mbar_wait(&acc_full[as], use & 1);
         tc_fence_after();
         const uint32_t tbase = tmem + as * BN + ((uint32_t)(q * 32) << 16);
 #pragma unroll
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t r[4][8];
+        for (int g = 0; g < 4; ++g) {
+          // accumulator group g (32 values) <- TMEM columns of block b
+          const int b = g / (4 / NB);
+          const int col = b * UNITS + hf * HALF + (g % (4 / NB)) * 32;
 #pragma unroll
-          for (int g = 0; g < 4; ++g) tmem_ld8(tbase + (uint32_t)(c + 8 * g), r[g]);
-          tmem_wait_ld();
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t r[16];
+            tmem_ld16(tbase + (uint32_t)(col + 16 * hh), r);
+            tmem_wait_ld();
 #pragma unroll
-          for (int g = 0; g < 4; ++g)
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[c + 8 * g + i] += __uint_as_float(r[g][i]);
+            for (int i = 0; i < 16; ++i) acc[32 * g + 16 * hh + i] += __uint_as_float(r[i]);
+          }
         }
         tc_fence_before();
-        mbar_arrive(&acc_empty[as]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(acc_empty_leader + 8u * as);
       }
-      const int row = tm * BM + q * 32 + lane;
-      const int u0 = tn * UNITS;
-      if (row >= p.M) continue;
+      const int row0 = tm * 2 * BM + (int)rank * BM + q * 32;  // this warp's 32 output rows
+      const int u0 = tn * UNITS + hf * HALF;                   // and its first unit
+      if (EPI == kEpiPlain) {
+        const int rowc = row0 + (p.mode == 2 ? z * p.Mp : 0);
 #pragma unroll
-      for (int c = 0; c < UNITS; c += 8) {
-        const int j = u0 + c;  // first unit (column) of this chunk
-        if (j >= p.units) break;
-        const bool full8 = j + 8 <= p.units;
-        if (EPI == kEpiPlain) {
-          float* dst = p.C + (size_t)(p.mode == 2 ? z : 0) * p.M * p.ldc + (size_t)row * p.ldc + j;
-          float w[8];
+        for (int g = 0; g < 4; ++g) {
+          float v[32];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) w[i] = acc[c + i];
-          if (p.mode == 1) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (full8 || j + i < p.units) w[i] += dst[i];
-          }
-          store8(dst, w, full8, p.units - j);
-        } else if (EPI == kEpiGilr) {
-          // blocks (g, i) of hidden units j..j+7: g = sigmoid, i = act,
-          // impulse = (1 - g) * i  (layers.hpp:86-92)
-          float g[8], ci[8], imp[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int jj = min(j + i, p.units - 1);
-            g[i] = sigmoidf_(acc[c + i] + p.bias[0][jj]);
-            ci[i] = actf_(p.act, acc[(NB - 1) * UNITS + c + i] + p.bias[1][jj]);
-            imp[i] = (1.f - g[i]) * ci[i];
-          }
-          const size_t o = (size_t)row * p.ldo + j;
-          store8(p.out[0] + o, g, full8, p.units - j);
-          store8(p.out[1] + o, ci, full8, p.units - j);
-          store8(p.out[2] + o, imp, full8, p.units - j);
-        } else {  // kEpiGates
-          // blocks (f, i, o, z) of units j..j+7: f, i, o = sigmoid, z = tanh
-          // (layers.hpp:263, activate_gates :226-236); planes f, i, o, z and
-          // the cell impulse i*z (:271-279)
-          constexpr int B1 = NB > 1 ? 1 : 0, B2 = NB > 2 ? 2 : 0, B3 = NB > 3 ? 3 : 0;
-          float f[8], ig[8], og[8], zg[8], iz[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int jj = min(j + i, p.units - 1);
-            f[i] = sigmoidf_(acc[c + i] + p.bias[0][jj]);
-            ig[i] = sigmoidf_(acc[B1 * UNITS + c + i] + p.bias[1][jj]);
-            og[i] = sigmoidf_(acc[B2 * UNITS + c + i] + p.bias[2][jj]);
-            zg[i] = tanhf(acc[B3 * UNITS + c + i] + p.bias[3][jj]);
-            iz[i] = ig[i] * zg[i];
-          }
-          const size_t o = (size_t)row * p.ldo + j;
-          store8(p.out[0] + o, f, full8, p.units - j);
-          store8(p.out[1] + o, ig, full8, p.units - j);
-          store8(p.out[2] + o, og, full8, p.units - j);
-          store8(p.out[3] + o, zg, full8, p.units - j);
-          store8(p.out[4] + o, iz, full8, p.units - j);
+          for (int i = 0; i < 32; ++i) v[i] = acc[32 * g + i];
+          box_wait(lane);
+          stage_row(box, lane, v);
+          flush_box(&om.m[0], box, lane, u0 + 32 * g, rowc, p.mode == 1);
         }
+      } else if (EPI == kEpiGilr) {
+        // blocks (g, i) of hidden units: g = sigmoid, i = act,
+        // impulse = (1 - g) * i  (layers.hpp:86-92)
+#pragma unroll
+        for (int k = 0; k < HALF / 32; ++k) {
+          const float bg = bias_lane(p.bias[0], u0 + 32 * k, lane, p.units);
+          const float bz = bias_lane(p.bias[1], u0 + 32 * k, lane, p.units);
+          float gv[32], cv[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) gv[i] = sigmoidf_(acc[32 * k + i] + LINREC_BCAST(bg, i));
+          box_wait(lane);
+          stage_row(box, lane, gv);
+          flush_box(&om.m[0], box, lane, u0 + 32 * k, row0, false);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) cv[i] = actf_(p.act, acc[HALF + 32 * k + i] + LINREC_BCAST(bz, i));
+          box_wait(lane);
+          stage_row(box, lane, cv);
+          flush_box(&om.m[1], box, lane, u0 + 32 * k, row0, false);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) gv[i] = (1.f - gv[i]) * cv[i];
+          box_wait(lane);
+          stage_row(box, lane, gv);
+          flush_box(&om.m[2], box, lane, u0 + 32 * k, row0, false);
+        }
+      } else {  // kEpiGates
+        // blocks (f, i, o, z): f, i, o = sigmoid, z = tanh (layers.hpp:263,
+        // activate_gates :226-236); planes f, i, o, z and the impulse i*z
+        const float b0 = bias_lane(p.bias[0], u0, lane, p.units), b1 = bias_lane(p.bias[1], u0, lane, p.units);
+        const float b2 = bias_lane(p.bias[2], u0, lane, p.units), b3 = bias_lane(p.bias[3], u0, lane, p.units);
+        float v[32], iv[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = sigmoidf_(acc[i] + LINREC_BCAST(b0, i));
+        box_wait(lane);
+        stage_row(box, lane, v);
+        flush_box(&om.m[0], box, lane, u0, row0, false);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) iv[i] = sigmoidf_(acc[32 + i] + LINREC_BCAST(b1, i));
+        box_wait(lane);
+        stage_row(box, lane, iv);
+        flush_box(&om.m[1], box, lane, u0, row0, false);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = sigmoidf_(acc[64 + i] + LINREC_BCAST(b2, i));
+        box_wait(lane);
+        stage_row(box, lane, v);
+        flush_box(&om.m[2], box, lane, u0, row0, false);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = tanhf_(acc[96 + i] + LINREC_BCAST(b3, i));
+        box_wait(lane);
+        stage_row(box, lane, v);
+        flush_box(&om.m[3], box, lane, u0, row0, false);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= iv[i];
+        box_wait(lane);
+        stage_row(box, lane, v);
+        flush_box(&om.m[4], box, lane, u0, row0, false);
       }
     }
+    if (lane == 0) bulk_wait0();
   }
-  __syncthreads();
+  tc_fence_before();
+  cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, Cfg::TMEM_COLS);
+    tmem_dealloc2(tmem, Cfg::TMEM_COLS);
   }
 }
 

@@ -136,7 +136,7 @@ struct GemmEpilogue {
   bool accumulate = false;
   bool split3 = false;       // 3xTF32 (fp32-grade) instead of plain TF32
   int k_splits = 1;
-  float* scratch = nullptr;  // split-K partials, k_splits * M * units floats
+  float* scratch = nullptr;  // split-K partials, gemm_partial_floats() floats
   int act = 0;               // GILR candidate activation (0 tanh, 1 identity, 2 relu)
   const float* bias[4] = {nullptr, nullptr, nullptr, nullptr};
   float* out[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -145,5 +145,7 @@ struct GemmEpilogue {
 // epi: 0 plain (C / accumulate / split-K), 1 GILR gates (nb 2), 2 LSTM gates (nb 4)
 cudaError_t gemm_tf32(const GemmOperands& op, int epi, const GemmEpilogue& ep, cudaStream_t st);
 int gemm_splits_for(int64_t M, int64_t N, int64_t K);
+// split-K partial buffer (floats) gemm_tf32 needs for `splits` splits (0 for 1)
+int64_t gemm_partial_floats(int64_t M, int64_t N, int splits);
 
 }  // namespace linrec_impl

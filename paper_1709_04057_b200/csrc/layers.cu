@@ -203,8 +203,7 @@ struct Carve {
 };
 
 int64_t wsplit_floats(int64_t R, int64_t M, int64_t N) {
-  const int s = linrec_impl::gemm_splits_for(M, N, R);
-  return s > 1 ? (int64_t)s * M * N : 0;
+  return linrec_impl::gemm_partial_floats(M, N, linrec_impl::gemm_splits_for(M, N, R));
 }
 
 // ---- scratch layouts (one function drives sizing and carving) -------------

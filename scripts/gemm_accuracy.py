@@ -21,7 +21,7 @@ for K in (256, 1024, 4096, 16384, 65536, 262144):
             if splits > K // 128:
                 continue
             C = torch.zeros(M, N, device="cuda")
-            scr = torch.empty(splits * M * N, device="cuda")
+            scr = torch.empty(max(1, capi.gemm_scratch_bytes(M, N, splits) // 4), device="cuda")
             capi.gemm(A.data_ptr(), True, M, B.data_ptr(), True, N, C.data_ptr(), N, M, N, K, False, prec, splits,
                       scr.data_ptr(), st)
             torch.cuda.synchronize()

@@ -30,7 +30,7 @@ def run(M, N, K, a_mn, b_mn, accumulate=False, splits=1, seed=0, precision=0):
     ldc = (N + 3) // 4 * 4
     Cbuf = torch.zeros(M, ldc, device="cuda")
     Cbuf[:, :N] = C0
-    scratch = torch.empty(max(1, splits) * M * N, device="cuda") if splits > 1 else None
+    scratch = torch.empty(capi.gemm_scratch_bytes(M, N, splits) // 4 + 1, device="cuda") if splits > 1 else None
     capi.gemm(Ast.data_ptr(), a_mn, Ast.shape[1], Bst.data_ptr(), b_mn, Bst.shape[1], Cbuf.data_ptr(), ldc, M, N,
               K, accumulate, precision, splits, None if scratch is None else scratch.data_ptr(),
               torch.cuda.current_stream().cuda_stream)
@@ -54,9 +54,10 @@ def test_gemm_split_k_and_accumulate(splits, precision):
 
 
 def test_gemm_many_tiles_persistent():
-    # more tiles than SMs: every CTA walks several tiles through both TMEM accumulators
-    assert run(4096, 1024, 256, False, False) < TOL[0]
-    assert run(2048, 640, 96, False, True, precision=1) < TOL[1]
+    # more tiles than CTA pairs: every pair walks several tiles through both TMEM accumulators
+    assert run(8192, 1024, 256, False, False) < TOL[0]
+    assert run(20000, 640, 96, False, True, precision=1) < TOL[1]
+    assert run(300, 1000, 4096, True, False, splits=5) < TOL[0]
 
 
 def test_tf32_operand_truncation():
@@ -90,7 +91,7 @@ def test_gemm_deterministic():
     outs = []
     for _ in range(2):
         C = torch.zeros(M, N, device="cuda")
-        scratch = torch.empty(16 * M * N, device="cuda")
+        scratch = torch.empty(capi.gemm_scratch_bytes(M, N, 16) // 4, device="cuda")
         capi.gemm(A.data_ptr(), True, M, B.data_ptr(), True, N, C.data_ptr(), N, M, N, K, False, capi.PREC_FP32, 16,
                   scratch.data_ptr(), torch.cuda.current_stream().cuda_stream)
         outs.append(C)
