@@ -4,6 +4,7 @@
  * Plain-C restatement of /root/reference/proj/include/linrec/layers.hpp:
  *   gilr_forward       :78-100    gilr_backward       :102-133
  *   gilr_lstm_forward  :245-293   gilr_lstm_backward  :295-375
+ *   qrnn_forward       :449-494   qrnn_backward       :496-548
  * with the dense transforms of tensor.hpp (affine :249-270,
  * accumulate_weight_grad :272-284, accumulate_bias_grad :286-296,
  * accumulate_input_grad :298-308) written as loops and the recurrence as the
@@ -220,6 +221,77 @@ typedef int64_t index_t;
       for (index_t k = 0; k < BN; ++k) dhtil0[k] = dh0s[k] + dhp[k];                  \
     free(dc); free(dO); free(f); free(df); free(diz); free(dpre); free(hp);           \
     free(dhp); free(dht); free(dxs); free(dh0s);                                      \
+  }                                                                                      \
+                                                                                      \
+  /* qrnn_forward :449-494.  W: k taps packed [k][3n][m] (QrnnParams::W).        \
+   * Writes h; gates [R][3n] activated (f, o, z), c (QrnnCache :420-423). */         \
+  void oracle_qrnn_forward_##SUF(const S* x, const S* W, const S* bias, const S* c0,  \
+                                 S* h, S* gates, S* c, index_t T, index_t b,          \
+                                 index_t m, index_t n, index_t k) {                   \
+    const index_t R = T * b, N = R * n;                                               \
+    S* f = (S*)malloc(sizeof(S) * (size_t)N);                                         \
+    S* imp = (S*)malloc(sizeof(S) * (size_t)N);                                       \
+    for (index_t r = 0; r < R; ++r)                                                   \
+      for (index_t j = 0; j < 3 * n; ++j) gates[r * 3 * n + j] = bias[j];             \
+    /* tap s: rows s*b.. accumulate x rows 0.. against W_s (:468-470) */              \
+    for (index_t s = 0; s < k && s < T; ++s)                                          \
+      affine_##SUF(x, (T - s) * b, m, W + s * 3 * n * m, 3 * n, (const S*)0,          \
+                   gates + s * b * 3 * n, 1);                                         \
+    for (index_t r = 0; r < R; ++r) {                                                 \
+      S* gr = gates + r * 3 * n;                                                      \
+      for (index_t j = 0; j < 2 * n; ++j) gr[j] = sig_##SUF(gr[j]);                   \
+      for (index_t j = 2 * n; j < 3 * n; ++j) gr[j] = TANH(gr[j]);                    \
+      for (index_t j = 0; j < n; ++j) {                                               \
+        f[r * n + j] = gr[j];                                                         \
+        imp[r * n + j] = ((S)1 - gr[j]) * gr[2 * n + j];                              \
+      }                                                                               \
+    }                                                                                 \
+    scan_##SUF(f, imp, c0, c, T, b * n);                                              \
+    for (index_t r = 0; r < R; ++r)                                                   \
+      for (index_t j = 0; j < n; ++j) h[r * n + j] = gates[r * 3 * n + n + j] * c[r * n + j]; \
+    free(f); free(imp);                                                               \
+  }                                                                                   \
+                                                                                      \
+  /* qrnn_backward :496-548.  Accumulates dW (packed [k][3n][m]) and dbias;      \
+   * writes dx and dc0. */                                                            \
+  void oracle_qrnn_backward_##SUF(const S* x, const S* W, const S* c0, const S* gates, \
+                                  const S* c, const S* dh, S* dW, S* dbias, S* dx,    \
+                                  S* dc0, index_t T, index_t b, index_t m, index_t n, \
+                                  index_t k) {                                        \
+    const index_t R = T * b, N = R * n;                                               \
+    S* dc = (S*)malloc(sizeof(S) * (size_t)N);                                        \
+    S* dO = (S*)malloc(sizeof(S) * (size_t)N);                                        \
+    S* f = (S*)malloc(sizeof(S) * (size_t)N);                                         \
+    S* df = (S*)malloc(sizeof(S) * (size_t)N);                                        \
+    S* dimp = (S*)malloc(sizeof(S) * (size_t)N);                                      \
+    S* dpre = (S*)malloc(sizeof(S) * (size_t)(3 * N));                                \
+    for (index_t r = 0; r < R; ++r)                                                   \
+      for (index_t j = 0; j < n; ++j) {                                               \
+        const S* gr = gates + r * 3 * n;                                              \
+        dO[r * n + j] = dh[r * n + j] * c[r * n + j];                                 \
+        dc[r * n + j] = dh[r * n + j] * gr[n + j];                                    \
+        f[r * n + j] = gr[j];                                                         \
+      }                                                                               \
+    scan_bwd_##SUF(f, c0, c, dc, df, dimp, dc0, T, b * n);                            \
+    for (index_t r = 0; r < R; ++r) {                                                 \
+      const S* gr = gates + r * 3 * n;                                                \
+      S* o = dpre + r * 3 * n;                                                        \
+      for (index_t j = 0; j < n; ++j) {                                               \
+        const S fv = gr[j], ov = gr[n + j], zv = gr[2 * n + j];                       \
+        const S dfj = df[r * n + j], dij = dimp[r * n + j];                           \
+        o[j] = (dfj - dij * zv) * fv * ((S)1 - fv);                                   \
+        o[n + j] = dO[r * n + j] * ov * ((S)1 - ov);                                  \
+        o[2 * n + j] = dij * ((S)1 - fv) * ((S)1 - zv * zv);                          \
+      }                                                                               \
+    }                                                                                 \
+    bgrad_##SUF(dpre, R, 3 * n, dbias);                                               \
+    for (index_t q = 0; q < R * m; ++q) dx[q] = 0;                                    \
+    for (index_t s = 0; s < k && s < T; ++s) {                                        \
+      const index_t nr = (T - s) * b;                                                 \
+      wgrad_##SUF(dpre + s * b * 3 * n, nr, 3 * n, x, m, dW + s * 3 * n * m);         \
+      igrad_##SUF(dpre + s * b * 3 * n, nr, 3 * n, W + s * 3 * n * m, m, dx, 1);      \
+    }                                                                                 \
+    free(dc); free(dO); free(f); free(df); free(dimp); free(dpre);                    \
   }
 
 DEFINE_LAYERS(double, f64, fma, exp, tanh)

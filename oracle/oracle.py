@@ -195,6 +195,8 @@ class Oracle:
             getattr(lib, f"oracle_gilr_backward_{sfx}").argtypes = [_vp] * 4 + [C.c_int] + [_vp] * 10 + [_i64] * 4
             getattr(lib, f"oracle_gilr_lstm_forward_{sfx}").argtypes = [_vp] * 16 + [_i64] * 4
             getattr(lib, f"oracle_gilr_lstm_backward_{sfx}").argtypes = [_vp] * 23 + [_i64] * 4
+            getattr(lib, f"oracle_qrnn_forward_{sfx}").argtypes = [_vp] * 7 + [_i64] * 5
+            getattr(lib, f"oracle_qrnn_backward_{sfx}").argtypes = [_vp] * 10 + [_i64] * 5
             setattr(self, f"_layers_{sfx}", True)
         return sfx
 
@@ -242,6 +244,44 @@ class Oracle:
             _ptr(dh), _ptr(g["sU"]), _ptr(g["sV"]), _ptr(g["sbg"]), _ptr(g["sbz"]), _ptr(g["U"]), _ptr(g["V"]),
             _ptr(g["bias"]), _ptr(dx), _ptr(dhtil0), _ptr(dc0), T, b, m, n)
         return g, dx, dhtil0, dc0
+
+    def qrnn_forward(self, P, x, c0=None):
+        """qrnn_forward (layers.hpp:449-494).  P: dict W [k, 3n, m], bias [3n].
+        Returns h and the cache dict (gates [T, b, 3n] activated f,o,z; c)."""
+        x = np.ascontiguousarray(x)
+        dt = x.dtype
+        sfx = self._layer_fns(dt)
+        T, b, m = x.shape
+        W = np.ascontiguousarray(P["W"], dtype=dt)
+        k, n3, _ = W.shape
+        n = n3 // 3
+        bias = np.ascontiguousarray(P["bias"], dtype=dt)
+        c0 = np.zeros((b, n), dt) if c0 is None else np.ascontiguousarray(c0, dtype=dt)
+        h = np.empty((T, b, n), dt)
+        cache = {"gates": np.empty((T, b, 3 * n), dt), "c": np.empty((T, b, n), dt)}
+        getattr(self.lib, f"oracle_qrnn_forward_{sfx}")(
+            _ptr(x), _ptr(W), _ptr(bias), _ptr(c0), _ptr(h), _ptr(cache["gates"]), _ptr(cache["c"]), T, b, m, n, k)
+        return h, cache
+
+    def qrnn_backward(self, P, x, c0, cache, dh):
+        """qrnn_backward (layers.hpp:496-548).  Returns (grads dict W, bias;
+        dx; dc0); gradients start at zero."""
+        x = np.ascontiguousarray(x)
+        dt = x.dtype
+        sfx = self._layer_fns(dt)
+        T, b, m = x.shape
+        W = np.ascontiguousarray(P["W"], dtype=dt)
+        k, n3, _ = W.shape
+        n = n3 // 3
+        c0 = np.zeros((b, n), dt) if c0 is None else np.ascontiguousarray(c0, dtype=dt)
+        g = {"W": np.zeros_like(W), "bias": np.zeros(3 * n, dt)}
+        dx = np.empty((T, b, m), dt)
+        dc0 = np.empty((b, n), dt)
+        getattr(self.lib, f"oracle_qrnn_backward_{sfx}")(
+            _ptr(x), _ptr(W), _ptr(c0), _ptr(cache["gates"]), _ptr(cache["c"]),
+            _ptr(np.ascontiguousarray(dh, dtype=dt)), _ptr(g["W"]), _ptr(g["bias"]), _ptr(dx), _ptr(dc0),
+            T, b, m, n, k)
+        return g, dx, dc0
 
     def first_nonfinite(self, a):
         a = np.ascontiguousarray(a)
@@ -295,6 +335,7 @@ class RefLib:
         lib.ref_bench_fwd_bwd_f32.argtypes = [_vp] * 4 + [_i64] * 3 + [C.c_int] * 3 + [_vp, _vp]
         lib.ref_gilr_lstm_oracle.argtypes = [_vp] * 11 + [_i64] * 4
         lib.ref_gilr_oracle.argtypes = [_vp] * 7 + [_i64] * 4
+        lib.ref_qrnn_oracle.argtypes = [_vp] * 5 + [_i64] * 5
 
     def _check(self, rc):
         if rc != 0:
@@ -362,6 +403,18 @@ class RefLib:
             _ptr(np.ascontiguousarray(c0, dtype=np.float64)), _ptr(h), T, b, m, n))
         return h
 
+    def qrnn_oracle(self, P, x, c0):
+        """The reference's per-step QRNN (layer_oracles.hpp:84-114), fp64."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        T, b, m = x.shape
+        W = np.ascontiguousarray(P["W"], dtype=np.float64)
+        k, n3, _ = W.shape
+        h = np.empty((T, b, n3 // 3))
+        self._check(self.lib.ref_qrnn_oracle(
+            _ptr(x), _ptr(W), _ptr(np.ascontiguousarray(P["bias"], dtype=np.float64)),
+            _ptr(np.ascontiguousarray(c0, dtype=np.float64)), _ptr(h), T, b, m, n3 // 3, k))
+        return h
+
     def hardware_workers(self):
         return int(self.lib.ref_hardware_workers())
 
@@ -377,6 +430,15 @@ def load_reference_module():
     mod = importlib.util.module_from_spec(spec)
     loader.exec_module(mod)
     return mod
+
+
+def qrnn_params(rng, m, n, k, dtype=np.float64, gate_bias=1.0):
+    """Random QRNN parameters shaped like qrnn_init (layers.hpp:411-422):
+    k taps W_s ~ U(+-1/sqrt(m k)) packed [k, 3n, m], bias = gate_bias on f."""
+    s = 1.0 / np.sqrt(m * k)
+    bias = np.zeros(3 * n)
+    bias[:n] = gate_bias
+    return {"W": rng.uniform(-s, s, (k, 3 * n, m)).astype(dtype), "bias": bias.astype(dtype)}
 
 
 def gilr_lstm_params(rng, m, n, dtype=np.float64, gate_bias=1.0):

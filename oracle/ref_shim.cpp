@@ -227,4 +227,21 @@ int ref_gilr_oracle(const double* x, const double* U, const double* V, const dou
     return 1;
   }
 }
+int ref_qrnn_oracle(const double* x, const double* W, const double* bias, const double* c0, double* h,
+                    int64_t T, int64_t b, int64_t m, int64_t n, int64_t k) {
+  // per-step QRNN (proj/tests/support/layer_oracles.hpp:84-114); W packed [k][3n][m]
+  try {
+    linrec::QrnnParams<double> p;
+    for (int64_t s = 0; s < k; ++s) p.W.push_back(t2d(W + s * 3 * n * m, 3 * n, m));
+    p.bias = t2d(bias, 1, 3 * n);
+    auto X = t3(x, T, b, m);
+    auto C0 = t2(c0, b, n);
+    auto out = oracle::qrnn(p, X, C0);
+    std::copy(out.data.begin(), out.data.end(), h);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
 }

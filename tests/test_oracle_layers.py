@@ -76,3 +76,58 @@ def test_float32_oracle_close_to_float64(oracle):
     for k in P:
         assert max_rel_error(g32[0][k], g64[0][k]) < 1e-4, k
     assert max_rel_error(g32[1], g64[1]) < 1e-4
+
+
+# ---- QRNN (layers.hpp:376-548) ----------------------------------------------------
+def test_qrnn_forward_matches_reference_layer_oracle(oracle):
+    """Forward against the reference's per-step QRNN (layer_oracles.hpp:84-114),
+    windows k = 1, 2, 3 (test_layers.cpp:133-146)."""
+    import os
+    from oracle.oracle import REF_SO, RefLib, max_rel_error, qrnn_params
+    g = load_golden("qrnn")
+    for k in (1, 2, 3):
+        P = {"W": g[f"k{k}_W"], "bias": g[f"k{k}_bias"]}
+        h, _ = oracle.qrnn_forward(P, g[f"k{k}_x"], g[f"k{k}_c0"])
+        assert max_rel_error(h, g[f"k{k}_h_ref"]) <= 1e-12, k
+    if os.path.exists(REF_SO):
+        rng = np.random.default_rng(4)
+        P = qrnn_params(rng, 6, 5, 4)
+        x = rng.uniform(-1, 1, (9, 2, 6))
+        c0 = rng.uniform(-1, 1, (2, 5))
+        h, _ = oracle.qrnn_forward(P, x, c0)
+        assert max_rel_error(h, RefLib().qrnn_oracle(P, x, c0)) <= 1e-12
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_qrnn_backward_matches_finite_differences(oracle, k):
+    """test_layers.cpp:241-270: every W, bias, x and c0 entry."""
+    from oracle.oracle import grads_agree, qrnn_params
+    rng = np.random.default_rng(10 + k)
+    T, b, m, n = 6, 2, 3, 4
+    P = qrnn_params(rng, m, n, k)
+    x = rng.uniform(-1, 1, (T, b, m))
+    c0 = rng.uniform(-1, 1, (b, n))
+    w = rng.uniform(-1, 1, (T, b, n))
+
+    def loss(P_, x_, c0_):
+        h, _ = oracle.qrnn_forward(P_, x_, c0_)
+        return float((h * w).sum())
+
+    _, cache = oracle.qrnn_forward(P, x, c0)
+    grads, dx, dc0 = oracle.qrnn_backward(P, x, c0, cache, w)
+    eps = 1e-6
+
+    def fd(arr, idx, rebuild):
+        hi, lo = arr.copy(), arr.copy()
+        hi[idx] += eps
+        lo[idx] -= eps
+        return (rebuild(hi) - rebuild(lo)) / (2 * eps)
+
+    for name in ("W", "bias"):
+        for idx in np.ndindex(P[name].shape):
+            num = fd(P[name], idx, lambda a: loss({**P, name: a}, x, c0))
+            assert grads_agree(grads[name][idx], num, 1e-6), (name, idx)
+    for idx in np.ndindex(x.shape):
+        assert grads_agree(dx[idx], fd(x, idx, lambda a: loss(P, a, c0)), 1e-6)
+    for idx in np.ndindex(c0.shape):
+        assert grads_agree(dc0[idx], fd(c0, idx, lambda a: loss(P, x, a)), 1e-6)
