@@ -345,6 +345,21 @@ int linrec_gilr_lstm_backward_f32(const linrec_gilr_lstm_params_f32* p, const fl
                                   int64_t T, int64_t b, int64_t m, int64_t n, int mode, int precision,
                                   void* scratch, size_t scratch_bytes, void* stream);
 
+/* ---- QRNN (layers.hpp:376-548) ------------------------------------------- *
+ * [f o z]_t = act(sum_{s<k} W_s x_{t-s} + b), c_t = f c_{t-1} + (1-f) z,
+ * h_t = o c_t.  W: the k taps packed [k][3n][m] (QrnnParams::W[s] at
+ * W + s*3n*m), bias [3n] (blocks f, o, z).  Cache (QrnnCache :420-423):
+ * gates [3][T][b][n] activated f, o, z planes, c [T][b][n].  dW (packed like
+ * W) and dbias accumulate; dx is overwritten.  1 <= k <= T. */
+size_t linrec_qrnn_scratch_bytes(int64_t T, int64_t b, int64_t m, int64_t n, int64_t k);
+int linrec_qrnn_forward_f32(const float* W, const float* bias, const float* x, const float* c0, float* h,
+                            float* gates, float* c, int64_t T, int64_t b, int64_t m, int64_t n, int64_t k, int mode,
+                            int precision, void* scratch, size_t scratch_bytes, void* stream);
+int linrec_qrnn_backward_f32(const float* W, const float* x, const float* c0, const float* gates, const float* c,
+                             const float* dh, float* dW, float* dbias, float* dx, float* dc0, int64_t T, int64_t b,
+                             int64_t m, int64_t n, int64_t k, int mode, int precision, void* scratch,
+                             size_t scratch_bytes, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

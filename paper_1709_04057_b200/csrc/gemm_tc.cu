@@ -79,19 +79,22 @@ cudaError_t out_map(CUtensorMap* map, float* ptr, int64_t cols, int64_t rows, in
   return make_tmap(map, ptr, cols, rows, pitch, 32, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-template <bool A_MN, bool B_MN, int NB, bool SPLIT3, int EPI>
+template <bool A_MN, bool B_MN, int NB, int BNT, bool SPLIT3, int EPI>
 cudaError_t launch_cfg(const GemmOperands& op, const GemmEpilogue& ep, linrec_dev::tc::GemmParams p,
                        float* partial, int64_t Mp, int64_t ldp, cudaStream_t st) {
   constexpr int STAGES = SPLIT3 ? 3 : 5;
-  using Cfg = linrec_dev::tc::GemmCfg<A_MN, B_MN, NB, STAGES, SPLIT3>;
+  using Cfg = linrec_dev::tc::GemmCfg<A_MN, B_MN, NB, BNT, STAGES, SPLIT3>;
   constexpr int UNITS = Cfg::UNITS;
-  constexpr int BROWS = NB == 1 ? BN / 2 : UNITS;  // rows of one K-major B box
-  const int64_t b_rows = NB == 1 ? op.units : (NB - 1) * op.b_bstride + op.units;
+  constexpr int BROWS = Cfg::SB;  // rows of one K-major B box
+  // rows (K-major) / K extent (MN-major) the B map must cover, all taps included
+  int64_t b_rows = NB == 1 ? op.units : (NB - 1) * op.b_bstride + op.units;
+  if (op.ntaps > 1 && !B_MN) b_rows += (op.ntaps - 1) * op.b_tap;
+  const int64_t b_k1 = op.ntaps > 1 && B_MN ? (op.ntaps - 1) * op.b_tap + op.K1 : op.K1;
   CUtensorMap a1, b1, a2, b2;
   linrec_dev::tc::OutMaps om;
   cudaError_t e;
   if ((e = operand_map(&a1, op.a1, A_MN, op.M, op.K1, op.lda1, BM)) != cudaSuccess) return e;
-  if ((e = operand_map(&b1, op.b1, B_MN, b_rows, op.K1, op.ldb1, BROWS)) != cudaSuccess) return e;
+  if ((e = operand_map(&b1, op.b1, B_MN, b_rows, b_k1, op.ldb1, BROWS)) != cudaSuccess) return e;
   if (op.a2 != nullptr) {
     if ((e = operand_map(&a2, op.a2, A_MN, op.M, op.K2, op.lda2, BM)) != cudaSuccess) return e;
     if ((e = operand_map(&b2, op.b2, B_MN, b_rows, op.K2, op.ldb2, BROWS)) != cudaSuccess) return e;
@@ -104,14 +107,14 @@ cudaError_t launch_cfg(const GemmOperands& op, const GemmEpilogue& ep, linrec_de
     else e = out_map(&om.m[0], ep.C, op.units, op.M, ep.ldc);
     if (e != cudaSuccess) return e;
   } else {
-    const int nout = EPI == linrec_dev::tc::kEpiGilr ? 3 : 5;
+    const int nout = EPI == linrec_dev::tc::kEpiGilr ? 3 : EPI == linrec_dev::tc::kEpiQrnn ? 4 : 5;
     for (int i = 0; i < nout; ++i)
       if ((e = out_map(&om.m[i], ep.out[i], op.units, op.M, ep.ldo)) != cudaSuccess) return e;
   }
   p.ntm = (int)((op.M + 2 * BM - 1) / (2 * BM));
   p.ntn = (int)((op.units + UNITS - 1) / UNITS);
   p.b_bstride = (int)op.b_bstride;
-  auto kern = linrec_dev::tc::k_gemm<A_MN, B_MN, NB, STAGES, SPLIT3, EPI>;
+  auto kern = linrec_dev::tc::k_gemm<A_MN, B_MN, NB, BNT, STAGES, SPLIT3, EPI>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
   if (e != cudaSuccess) return e;
   const int64_t ntiles = (int64_t)p.ntm * p.ntn * p.nz;
@@ -127,14 +130,18 @@ cudaError_t dispatch(const GemmOperands& op, int epi, const GemmEpilogue& ep, co
   using namespace linrec_dev::tc;
   if (epi == kEpiPlain) {
     if (op.nb != 1) return cudaErrorInvalidValue;
-    if (!op.a_mn && !op.b_mn) return launch_cfg<false, false, 1, SPLIT3, kEpiPlain>(op, ep, p, partial, Mp, ldp, st);
-    if (!op.a_mn && op.b_mn) return launch_cfg<false, true, 1, SPLIT3, kEpiPlain>(op, ep, p, partial, Mp, ldp, st);
-    if (op.a_mn && op.b_mn) return launch_cfg<true, true, 1, SPLIT3, kEpiPlain>(op, ep, p, partial, Mp, ldp, st);
-    return launch_cfg<true, false, 1, SPLIT3, kEpiPlain>(op, ep, p, partial, Mp, ldp, st);
+    if (!op.a_mn && !op.b_mn) return launch_cfg<false, false, 1, BN, SPLIT3, kEpiPlain>(op, ep, p, partial, Mp, ldp, st);
+    if (!op.a_mn && op.b_mn) return launch_cfg<false, true, 1, BN, SPLIT3, kEpiPlain>(op, ep, p, partial, Mp, ldp, st);
+    if (op.a_mn && op.b_mn) return launch_cfg<true, true, 1, BN, SPLIT3, kEpiPlain>(op, ep, p, partial, Mp, ldp, st);
+    return launch_cfg<true, false, 1, BN, SPLIT3, kEpiPlain>(op, ep, p, partial, Mp, ldp, st);
   }
   if (op.a_mn || op.b_mn) return cudaErrorInvalidValue;
-  if (epi == kEpiGilr && op.nb == 2) return launch_cfg<false, false, 2, SPLIT3, kEpiGilr>(op, ep, p, nullptr, 0, 0, st);
-  if (epi == kEpiGates && op.nb == 4) return launch_cfg<false, false, 4, SPLIT3, kEpiGates>(op, ep, p, nullptr, 0, 0, st);
+  if (epi == kEpiGilr && op.nb == 2)
+    return launch_cfg<false, false, 2, BN, SPLIT3, kEpiGilr>(op, ep, p, nullptr, 0, 0, st);
+  if (epi == kEpiGates && op.nb == 4)
+    return launch_cfg<false, false, 4, BN, SPLIT3, kEpiGates>(op, ep, p, nullptr, 0, 0, st);
+  if (epi == kEpiQrnn && op.nb == 3)
+    return launch_cfg<false, false, 3, 192, SPLIT3, kEpiQrnn>(op, ep, p, nullptr, 0, 0, st);
   return cudaErrorInvalidValue;
 }
 
@@ -165,7 +172,8 @@ int64_t gemm_partial_floats(int64_t M, int64_t N, int splits) {
 }
 
 cudaError_t gemm_tf32(const GemmOperands& op, int epi, const GemmEpilogue& ep, cudaStream_t st) {
-  const int kb1 = (int)((op.K1 + BK - 1) / BK);
+  if (op.ntaps > 1 && (op.a2 != nullptr || op.a_mn)) return cudaErrorInvalidValue;
+  const int kb1 = (int)((op.K1 + BK - 1) / BK) * (op.ntaps > 1 ? op.ntaps : 1);
   const int kb2 = op.a2 != nullptr ? (int)((op.K2 + BK - 1) / BK) : 0;
   const int kb_total = kb1 + kb2;
   int splits = ep.k_splits < 1 ? 1 : ep.k_splits;
@@ -181,6 +189,11 @@ cudaError_t gemm_tf32(const GemmOperands& op, int epi, const GemmEpilogue& ep, c
   p.kb = kb_per;
   p.kb_total = kb_total;
   p.kchunk = ep.split3 ? 4 : 16;  // K = 128 (3xTF32) / 512 (TF32) per TMEM accumulation
+  if (op.ntaps > 1) {
+    p.tap_kb = (int)((op.K1 + BK - 1) / BK);
+    p.a_tap = (int)op.a_tap;
+    p.b_tap = (int)op.b_tap;
+  }
   p.mode = ep.accumulate ? 1 : 0;
   p.act = ep.act;
   for (int i = 0; i < 4; ++i) p.bias[i] = ep.bias[i];

@@ -60,7 +60,7 @@ namespace linrec_dev {
 namespace tc {
 
 constexpr int BM = 128;      // A rows per CTA (the MMA's M = 256 spans the pair)
-constexpr int BN = 256;      // MMA N; each CTA stages BN/2 = 128 B rows
+constexpr int BN = 256;      // widest MMA N; each CTA stages BN/2 B rows (QRNN tiles use N = 192)
 constexpr int BK = 32;       // fp32 elements per k-block = one 128-byte swizzle row
 constexpr int kThreads = 384;
 constexpr int kEpiWarps = 8;
@@ -225,7 +225,7 @@ struct TileGeom {
   static constexpr int BOX_BYTES = MN ? BK * 128 : BYTES;
 };
 
-enum Epi : int { kEpiPlain = 0, kEpiGilr = 1, kEpiGates = 2 };
+enum Epi : int { kEpiPlain = 0, kEpiGilr = 1, kEpiGates = 2, kEpiQrnn = 3 };
 
 struct GemmParams {
   int M;             // output rows
@@ -234,17 +234,26 @@ struct GemmParams {
   int kb1, kb, kb_total;
   int kchunk;        // k-blocks per TMEM accumulation unit (promotion to fp32 registers)
   int b_bstride;     // row offset between B blocks (blocked K-major B)
+  // tap-shifted K (QRNN causal convolution, layers.hpp:376-388): k-block kb
+  // belongs to tap s = kb / tap_kb and reads A rows shifted by s*a_tap and B
+  // rows (K-major) / K (MN-major) offset by s*b_tap.  tap_kb = 0: off.
+  int tap_kb, a_tap, b_tap;
   int mode;          // plain: 0 store, 1 accumulate (TMA reduce-add), 2 split-K partial (rows z*Mp + row)
   int Mp;            // partial rows per split (M rounded up to the 256-row tile)
   int act;           // candidate activation (common.hpp:49-71): 0 tanh, 1 identity, 2 relu
   const float* bias[4];
 };
 
-template <bool A_MN, bool B_MN, int NB, int STAGES, bool SPLIT3>
+template <bool A_MN, bool B_MN, int NB, int BNT, int STAGES, bool SPLIT3>
 struct GemmCfg {
   using GA = TileGeom<A_MN, BM>;
-  using GB = TileGeom<B_MN, BN / 2>;
-  static constexpr int UNITS = BN / NB;  // output columns (hidden units) per tile
+  using GB = TileGeom<B_MN, BNT / 2>;
+  static constexpr int UNITS = BNT / NB;  // output columns (hidden units) per tile
+  static constexpr int HALF = UNITS / 2;  // units per epilogue warp of a quadrant pair
+  static constexpr int ACCN = BNT / 2;    // fp32 accumulators per epilogue thread
+  // K-major B: each CTA loads its BNT/2 tile rows as NSB boxes of SB rows
+  static constexpr int SB = NB == 1 ? BNT / 2 : (NB == 3 ? 32 : UNITS);
+  static constexpr int NSB = (BNT / 2) / SB;
   static constexpr int STAGE_BYTES = GA::BYTES + GB::BYTES;  // this CTA's halves
   static constexpr int LO_OFF = STAGES * STAGE_BYTES;        // 3xTF32 lo tiles, same layout
   static constexpr int EPI_OFF = LO_OFF + (SPLIT3 ? STAGES * STAGE_BYTES : 0);
@@ -252,10 +261,11 @@ struct GemmCfg {
   static constexpr int OFF_BAR = EPI_OFF + kEpiWarps * EPI_BYTES;
   static constexpr int NBARS = 3 * STAGES + 4;
   static constexpr int SMEM = OFF_BAR + NBARS * 8 + 16 + 1024;  // + alignment slack
-  static constexpr uint32_t IDESC = idesc_tf32(2 * BM, BN, A_MN, B_MN);
-  static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static constexpr uint32_t IDESC = idesc_tf32(2 * BM, BNT, A_MN, B_MN);
+  static constexpr uint32_t TMEM_COLS = 2 * BNT <= 256 ? 256 : 512;  // two accumulators
   static_assert(!B_MN || NB == 1, "blocked B operands are K-major weights");
-  static_assert(NB == 1 || NB == 2 || NB == 4, "NB");
+  static_assert(BNT % (NB * 64) == 0 && BNT <= BN, "NB / tile width");
+  static_assert(HALF % 32 == 0 && ACCN % 32 == 0 && (BNT / 2) % SB == 0, "epilogue groups");
   static_assert(SMEM <= 232448, "shared memory");
 };
 
@@ -320,16 +330,17 @@ struct OutMaps {
   CUtensorMap m[5];
 };
 
-template <bool A_MN, bool B_MN, int NB, int STAGES, bool SPLIT3, int EPI>
+template <bool A_MN, bool B_MN, int NB, int BNT, int STAGES, bool SPLIT3, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensorMap tb1,
        const __grid_constant__ CUtensorMap ta2, const __grid_constant__ CUtensorMap tb2,
        const __grid_constant__ OutMaps om, const GemmParams p) {
-  using Cfg = GemmCfg<A_MN, B_MN, NB, STAGES, SPLIT3>;
+  using Cfg = GemmCfg<A_MN, B_MN, NB, BNT, STAGES, SPLIT3>;
   using GA = typename Cfg::GA;
   using GB = typename Cfg::GB;
   constexpr int UNITS = Cfg::UNITS;
-  constexpr int HALF = UNITS / 2;  // units per epilogue warp of a quadrant pair
+  constexpr int HALF = Cfg::HALF;
+  constexpr int ACCN = Cfg::ACCN;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
@@ -380,7 +391,14 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
           const bool second = kb >= p.kb1;
           const CUtensorMap* ta = second ? &ta2 : &ta1;
           const CUtensorMap* tb = second ? &tb2 : &tb1;
-          const int k0 = (second ? kb - p.kb1 : kb) * BK;
+          int kk = second ? kb - p.kb1 : kb, a_off = 0, b_off = 0;
+          if (p.tap_kb) {
+            const int tap = kb / p.tap_kb;
+            kk = kb - tap * p.tap_kb;
+            a_off = tap * p.a_tap;
+            b_off = tap * p.b_tap;
+          }
+          const int k0 = kk * BK;
           unsigned char* sa = smem + s * Cfg::STAGE_BYTES;
           unsigned char* sb = sa + GA::BYTES;
           // SPLIT3: local completion (the split warps relay to the leader);
@@ -398,18 +416,19 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
 #pragma unroll
             for (int j = 0; j < GA::NBOX; ++j) LINREC_LOAD(sa + j * GA::BOX_BYTES, ta, m0 + 32 * j, k0);
           } else {
-            LINREC_LOAD(sa, ta, k0, m0);
+            LINREC_LOAD(sa, ta, k0, m0 + a_off);
           }
           if (B_MN) {
 #pragma unroll
             for (int j = 0; j < GB::NBOX; ++j)
-              LINREC_LOAD(sb + j * GB::BOX_BYTES, tb, u0 + (int)rank * (BN / 2) + 32 * j, k0);
-          } else if (NB == 1) {
-            LINREC_LOAD(sb, tb, k0, u0 + (int)rank * (BN / 2));
+              LINREC_LOAD(sb + j * GB::BOX_BYTES, tb, u0 + (int)rank * (BNT / 2) + 32 * j, k0 + b_off);
           } else {
+            // tile row rho -> gate block rho / UNITS, unit u0 + rho % UNITS
 #pragma unroll
-            for (int qq = 0; qq < NB / 2; ++qq)
-              LINREC_LOAD(sb + qq * UNITS * 128, tb, k0, ((int)rank * (NB / 2) + qq) * p.b_bstride + u0);
+            for (int j = 0; j < Cfg::NSB; ++j) {
+              const int rho = (int)rank * (BNT / 2) + j * Cfg::SB;
+              LINREC_LOAD(sb + j * Cfg::SB * 128, tb, k0, (rho / UNITS) * p.b_bstride + u0 + rho % UNITS + b_off);
+            }
           }
 #undef LINREC_LOAD
         }
@@ -428,7 +447,7 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
           const uint32_t as = unit & 1, use = unit >> 1;
           if (use > 0) mbar_wait_cluster(&acc_empty[as], (use - 1) & 1);
           tc_fence_after();
-          const uint32_t acc = tmem + as * BN;
+          const uint32_t acc = tmem + as * BNT;
           const int c1 = min(c0 + p.kchunk, kb_end);
           for (int kb = c0; kb < c1; ++kb, ++it) {
             const int s = it % STAGES;
@@ -491,19 +510,19 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
     for (int t = cid; t < ntiles; t += ncl) {
       const int tn = t % p.ntn, tm = (t / p.ntn) % p.ntm, z = t / (p.ntn * p.ntm);
       const int kb_begin = z * p.kb, kb_end = min(kb_begin + p.kb, p.kb_total);
-      float acc[128];
+      float acc[ACCN];
 #pragma unroll
-      for (int i = 0; i < 128; ++i) acc[i] = 0.f;
+      for (int i = 0; i < ACCN; ++i) acc[i] = 0.f;
       for (int c0 = kb_begin; c0 < kb_end; c0 += p.kchunk, ++unit) {
         const uint32_t as = unit & 1, use = unit >> 1;
         mbar_wait(&acc_full[as], use & 1);
         tc_fence_after();
-        const uint32_t tbase = tmem + as * BN + ((uint32_t)(q * 32) << 16);
+        const uint32_t tbase = tmem + as * BNT + ((uint32_t)(q * 32) << 16);
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          // accumulator group g (32 values) <- TMEM columns of block b
-          const int b = g / (4 / NB);
-          const int col = b * UNITS + hf * HALF + (g % (4 / NB)) * 32;
+        for (int g = 0; g < ACCN / 32; ++g) {
+          // accumulator group g (32 values) <- TMEM columns of gate block b
+          const int b = (32 * g) / HALF;
+          const int col = b * UNITS + hf * HALF + (32 * g) % HALF;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             uint32_t r[16];
@@ -554,6 +573,32 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
           stage_row(box, lane, gv);
           flush_box(&om.m[2], box, lane, u0 + 32 * k, row0, false);
         }
+      } else if (EPI == kEpiQrnn) {
+        // blocks (f, o, z): f, o = sigmoid, z = tanh (layers.hpp:472);
+        // planes f, o, z and the cell impulse (1 - f) * z (:475-482)
+        const float b0 = bias_lane(p.bias[0], u0, lane, p.units), b1 = bias_lane(p.bias[1], u0, lane, p.units);
+        const float b2 = bias_lane(p.bias[2], u0, lane, p.units);
+        float v[32], fv[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) fv[i] = sigmoidf_(acc[i] + LINREC_BCAST(b0, i));
+        box_wait(lane);
+        stage_row(box, lane, fv);
+        flush_box(&om.m[0], box, lane, u0, row0, false);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = sigmoidf_(acc[32 + i] + LINREC_BCAST(b1, i));
+        box_wait(lane);
+        stage_row(box, lane, v);
+        flush_box(&om.m[1], box, lane, u0, row0, false);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = tanhf_(acc[64 + i] + LINREC_BCAST(b2, i));
+        box_wait(lane);
+        stage_row(box, lane, v);
+        flush_box(&om.m[2], box, lane, u0, row0, false);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= 1.f - fv[i];
+        box_wait(lane);
+        stage_row(box, lane, v);
+        flush_box(&om.m[3], box, lane, u0, row0, false);
       } else {  // kEpiGates
         // blocks (f, i, o, z): f, i, o = sigmoid, z = tanh (layers.hpp:263,
         // activate_gates :226-236); planes f, i, o, z and the impulse i*z

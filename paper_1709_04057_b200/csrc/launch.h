@@ -128,6 +128,11 @@ struct GemmOperands {
   int64_t units = 0;      // output columns (per block when nb > 1)
   int nb = 1;             // blocked K-major B: nb row blocks of `units` rows ...
   int64_t b_bstride = 0;  // ... block q starting at row q * b_bstride
+  // ntaps > 1: K = ntaps segments of K1 (each padded to whole k-blocks); tap s
+  // reads A (K-major) rows shifted by s*a_tap and B rows (K-major) / K rows
+  // (MN-major) offset by s*b_tap -- the QRNN causal convolution as one GEMM
+  int ntaps = 1;
+  int64_t a_tap = 0, b_tap = 0;
   bool a_mn = false, b_mn = false;
 };
 struct GemmEpilogue {
@@ -142,7 +147,8 @@ struct GemmEpilogue {
   float* out[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   int64_t ldo = 0;
 };
-// epi: 0 plain (C / accumulate / split-K), 1 GILR gates (nb 2), 2 LSTM gates (nb 4)
+// epi: 0 plain (C / accumulate / split-K), 1 GILR gates (nb 2), 2 LSTM gates (nb 4),
+// 3 QRNN gates (nb 3)
 cudaError_t gemm_tf32(const GemmOperands& op, int epi, const GemmEpilogue& ep, cudaStream_t st);
 int gemm_splits_for(int64_t M, int64_t N, int64_t K);
 // split-K partial buffer (floats) gemm_tf32 needs for `splits` splits (0 for 1)

@@ -131,6 +131,39 @@ __global__ void k_gilr_dpre(const float* __restrict__ g, const float* __restrict
   st4(pp + n, si);
 }
 
+// QRNN fused pre-activation gradients (layers.hpp:519-531), blocked [R][3n]
+// (f, o, z), plus per-block partial column sums for the bias gradient.
+__global__ void k_qrnn_dpre(const float* __restrict__ gf, const float* __restrict__ go, const float* __restrict__ gz,
+                            const float* __restrict__ df, const float* __restrict__ dimp,
+                            const float* __restrict__ dh, const float* __restrict__ c, float* __restrict__ dpre,
+                            float* __restrict__ part, int64_t R, int64_t n, int64_t rpb) {
+  const int64_t u = 4 * ((int64_t)blockIdx.y * blockDim.x + threadIdx.x);
+  if (u >= n) return;
+  const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(r0 + rpb, R);
+  float4 sf = make_float4(0, 0, 0, 0), so = sf, sz = sf;
+  for (int64_t r = r0; r < r1; ++r) {
+    const int64_t o = r * n + u;
+    const float4 f = ld4(gf + o), og = ld4(go + o), z = ld4(gz + o);
+    const float4 d_f = ld4(df + o), d_i = ld4(dimp + o), d_h = ld4(dh + o), cc = ld4(c + o);
+    float4 pf, po, pz;
+#define LINREC_QDPRE(X)                                              \
+  pf.X = (d_f.X - d_i.X * z.X) * f.X * (1.f - f.X);                  \
+  po.X = (d_h.X * cc.X) * og.X * (1.f - og.X);                       \
+  pz.X = d_i.X * (1.f - f.X) * (1.f - z.X * z.X);                    \
+  sf.X += pf.X; so.X += po.X; sz.X += pz.X;
+    LINREC_QDPRE(x) LINREC_QDPRE(y) LINREC_QDPRE(z) LINREC_QDPRE(w)
+#undef LINREC_QDPRE
+    float* d = dpre + r * 3 * n + u;
+    st4(d, pf);
+    st4(d + n, po);
+    st4(d + 2 * n, pz);
+  }
+  float* pp = part + (int64_t)blockIdx.x * 3 * n + u;
+  st4(pp, sf);
+  st4(pp + n, so);
+  st4(pp + 2 * n, sz);
+}
+
 }  // namespace layers
 }  // namespace linrec_dev
 
@@ -161,7 +194,7 @@ using namespace linrec_dev::layers;
 using linrec_impl::GemmEpilogue;
 using linrec_impl::GemmOperands;
 
-constexpr int kEpiPlain = 0, kEpiGilr = 1, kEpiGates = 2;
+constexpr int kEpiPlain = 0, kEpiGilr = 1, kEpiGates = 2, kEpiQrnn = 3;
 
 int sms() {
   static int n = [] {
@@ -260,6 +293,32 @@ int64_t lstm_scratch(float* base, int64_t T, int64_t b, int64_t m, int64_t n, Ls
   t.dpre = bw.take(4 * R * n);
   t.dhp = bw.take((R + b) * n);
   t.G = bw.take(R * n);
+  if (s) *s = t;
+  return f.off > bw.off ? f.off : bw.off;
+}
+
+struct QrnnScratch {
+  float *part, *split, *tmp0;
+  float *imp;                // forward
+  float *dc, *df, *dimp, *dpre;  // backward
+};
+int64_t qrnn_scratch(float* base, int64_t T, int64_t b, int64_t m, int64_t n, int64_t k, QrnnScratch* s) {
+  const int64_t R = T * b;
+  Carve c{base};
+  QrnnScratch t;
+  t.tmp0 = c.take(b * n);
+  const RowPlan rp = row_plan(R, n);
+  t.part = c.take(rp.nbx * 3 * n);
+  t.split = c.take(wsplit_floats(R, 3 * n, m));
+  (void)k;
+  const int64_t common = c.off;
+  Carve f{base, common};
+  t.imp = f.take(R * n);
+  Carve bw{base, common};
+  t.dc = bw.take(R * n);
+  t.df = bw.take(R * n);
+  t.dimp = bw.take(R * n);
+  t.dpre = bw.take(3 * R * n);
   if (s) *s = t;
   return f.off > bw.off ? f.off : bw.off;
 }
@@ -422,6 +481,122 @@ int gilr_backward_core(const linrec_gilr_params_f32* p, const float* x, const fl
 }  // namespace
 
 extern "C" {
+
+size_t linrec_qrnn_scratch_bytes(int64_t T, int64_t b, int64_t m, int64_t n, int64_t k) {
+  if (T < 1 || b < 1 || m < 1 || n < 1 || k < 1) return 0;
+  return (size_t)qrnn_scratch(nullptr, T, b, m, n, k, nullptr) * 4;
+}
+
+int linrec_qrnn_forward_f32(const float* W, const float* bias, const float* x, const float* c0, float* h,
+                            float* gates, float* c, int64_t T, int64_t b, int64_t m, int64_t n, int64_t k, int mode,
+                            int precision, void* scratch, size_t scratch_bytes, void* stream) {
+  LRC(check_common(T, b, m, n, mode, precision, x));
+  if (k < 1) return err(LINREC_ERR_SHAPE, "qrnn_init: window must be >= 1");
+  if (k > T) return err(LINREC_ERR_SHAPE, "qrnn_forward: filter window exceeds sequence length");
+  if (!W || !bias || !h || !gates || !c)
+    return err(LINREC_ERR_VALUE, "qrnn_forward: W, bias, h, gates and c must not be NULL");
+  LRC(check_scratch(scratch, scratch_bytes, qrnn_scratch(nullptr, T, b, m, n, k, nullptr)));
+  QrnnScratch s;
+  qrnn_scratch(static_cast<float*>(scratch), T, b, m, n, k, &s);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t R = T * b, N = R * n;
+  float* gf = gates;
+  float* go = gf + N;
+  float* gz = go + N;
+  mark(st, "begin");
+  // pre[r] = bias + sum_s x[r - s*b] W_s^T: one GEMM whose K runs over the k
+  // taps, tap s reading x shifted s*b rows down (zero-filled above row 0)
+  GemmOperands op;
+  op.a1 = x;
+  op.lda1 = m;
+  op.b1 = W;
+  op.ldb1 = m;
+  op.K1 = m;
+  op.ntaps = (int)k;
+  op.a_tap = -b;
+  op.b_tap = 3 * n;
+  op.M = R;
+  op.units = n;
+  op.nb = 3;
+  op.b_bstride = n;
+  GemmEpilogue ep;
+  for (int q = 0; q < 3; ++q) ep.bias[q] = bias + q * n;
+  ep.out[0] = gf;
+  ep.out[1] = go;
+  ep.out[2] = gz;
+  ep.out[3] = s.imp;
+  ep.ldo = n;
+  LTRY(gemm(op, kEpiQrnn, ep, precision == LINREC_PREC_FP32, nullptr, st));
+  mark(st, "gemm_gates");
+  LRC(linrec_scan_f32(gf, s.imp, c0, c, T, b * n, mode, nullptr, st));
+  mark(st, "scan_cell");
+  k_mul<<<grid_for(N / 4, 256), 256, 0, st>>>(go, c, h, N / 4);
+  LTRY(cudaGetLastError());
+  mark(st, "h_out");
+  return LINREC_OK;
+}
+
+int linrec_qrnn_backward_f32(const float* W, const float* x, const float* c0, const float* gates, const float* c,
+                             const float* dh, float* dW, float* dbias, float* dx, float* dc0, int64_t T, int64_t b,
+                             int64_t m, int64_t n, int64_t k, int mode, int precision, void* scratch,
+                             size_t scratch_bytes, void* stream) {
+  LRC(check_common(T, b, m, n, mode, precision, x));
+  if (k < 1 || k > T) return err(LINREC_ERR_SHAPE, "qrnn_backward: window must be in [1, T]");
+  if (!W || !gates || !c || !dh || !dx)
+    return err(LINREC_ERR_VALUE, "qrnn_backward: W, gates, c, d_h and dx must not be NULL");
+  LRC(check_scratch(scratch, scratch_bytes, qrnn_scratch(nullptr, T, b, m, n, k, nullptr)));
+  QrnnScratch s;
+  qrnn_scratch(static_cast<float*>(scratch), T, b, m, n, k, &s);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool split3 = precision == LINREC_PREC_FP32;
+  const int64_t R = T * b, N = R * n;
+  const float* gf = gates;
+  const float* go = gf + N;
+  const float* gz = go + N;
+  mark(st, "begin");
+  k_mul<<<grid_for(N / 4, 256), 256, 0, st>>>(dh, go, s.dc, N / 4);
+  LTRY(cudaGetLastError());
+  mark(st, "dc");
+  LRC(linrec_scan_backward_f32(gf, c0, c, s.dc, s.df, s.dimp, dc0 ? dc0 : s.tmp0, T, b * n, mode, nullptr, st));
+  mark(st, "scan_bwd_cell");
+  const RowPlan rp = row_plan(R, n);
+  k_qrnn_dpre<<<dim3((unsigned)rp.nbx, (unsigned)rp.gy), rp.thr, 0, st>>>(gf, go, gz, s.df, s.dimp, dh, c, s.dpre,
+                                                                          s.part, R, n, rp.rpb);
+  LTRY(cudaGetLastError());
+  if (dbias) {
+    k_colsum<<<(unsigned)((3 * n + 127) / 128), 128, 0, st>>>(s.part, rp.nbx, 3 * n, 3 * n, dbias);
+    LTRY(cudaGetLastError());
+  }
+  mark(st, "dpre_gates");
+  // dW_s += dpre[s*b ..]^T x[.. R - s*b]  (layers.hpp:536-539)
+  if (dW)
+    for (int64_t tap = 0; tap < k; ++tap)
+      LTRY(wgrad(s.dpre + tap * b * 3 * n, 3 * n, 3 * n, x, m, R - tap * b, dW + tap * 3 * n * m, split3, s.split,
+                 st));
+  mark(st, "wgrad_W");
+  // dx[r] = sum_s dpre[r + s*b] W_s  (:540-543): one GEMM over the taps,
+  // tap s reading dpre shifted s*b rows up (zero-filled past row R)
+  {
+    GemmOperands op;
+    op.a1 = s.dpre;
+    op.lda1 = 3 * n;
+    op.b1 = W;
+    op.ldb1 = m;
+    op.K1 = 3 * n;
+    op.ntaps = (int)k;
+    op.a_tap = b;
+    op.b_tap = 3 * n;
+    op.M = R;
+    op.units = m;
+    op.b_mn = true;
+    GemmEpilogue ep;
+    ep.C = dx;
+    ep.ldc = m;
+    LTRY(gemm(op, kEpiPlain, ep, split3, nullptr, st));
+  }
+  mark(st, "dx");
+  return LINREC_OK;
+}
 
 int linrec_profile_begin(void) {
   Prof& p = prof();

@@ -6,6 +6,7 @@ tcgen05 gate GEMMs with fused activation epilogues and the chained scans):
 
     gilr_init / gilr_forward / gilr_backward                  layers.hpp:42-133
     gilr_lstm_init / gilr_lstm_forward / gilr_lstm_backward   layers.hpp:165-375
+    qrnn_init / qrnn_forward / qrnn_backward                  layers.hpp:376-548
 
 Parameters are row-major exactly as GilrParams / GilrLstmParams (gate blocks
 f, i, o, z stacked along the rows of U, V, bias).  Gradients ACCUMULATE into
@@ -69,6 +70,11 @@ def _bind():
     lib.linrec_gilr_lstm_backward_f32.argtypes = ([C.POINTER(_LstmParamsC)] + [_vp] * 3 + [C.POINTER(_LstmCacheC)]
                                                   + [_vp] + [C.POINTER(_LstmGradsC)] + [_vp] * 3 + tail)
     lib.linrec_profile_end.argtypes = [C.c_char_p, C.c_size_t]
+    lib.linrec_qrnn_scratch_bytes.restype = C.c_size_t
+    lib.linrec_qrnn_scratch_bytes.argtypes = [_i64] * 5
+    qtail = [_i64] * 5 + [_int, _int, _vp, C.c_size_t, _vp]
+    lib.linrec_qrnn_forward_f32.argtypes = [_vp] * 7 + qtail
+    lib.linrec_qrnn_backward_f32.argtypes = [_vp] * 10 + qtail
     lib._layers_bound = True
     return lib
 
@@ -368,6 +374,109 @@ def gilr_lstm_backward(p: GilrLstmParams, x, htil0, c0, cache: GilrLstmCache, d_
                                             PRECISION[precision], _p(scr), scr.numel(),
                                             torch.cuda.current_stream(dev).cuda_stream))
     return dx, dht0, dc0
+
+
+# ---- QRNN (layers.hpp:376-548) -----------------------------------------------------------
+@dataclass
+class QrnnParams:
+    """QrnnParams (layers.hpp:390-405): k taps W_s [3n, m] (blocks f, o, z),
+    stored packed as W [k, 3n, m] (W[s] sees x_{t-s}); bias [3n]."""
+    W: torch.Tensor
+    bias: torch.Tensor
+
+    def input(self):
+        return self.W.shape[2]
+
+    def hidden(self):
+        return self.bias.shape[0] // 3
+
+    def window(self):
+        return self.W.shape[0]
+
+    def tensors(self):
+        return [self.W, self.bias]
+
+
+@dataclass
+class QrnnGrads:
+    W: torch.Tensor
+    bias: torch.Tensor
+
+    @staticmethod
+    def zeros_like(p: QrnnParams) -> "QrnnGrads":
+        return QrnnGrads(torch.zeros_like(p.W), torch.zeros_like(p.bias))
+
+    def tensors(self):
+        return [self.W, self.bias]
+
+
+@dataclass
+class QrnnCache:
+    """QrnnCache (layers.hpp:420-423): gates [3, T, b, n] activated f, o, z
+    planes (the reference interleaves them as [T, b, 3n]), c [T, b, n]."""
+    gates: torch.Tensor = None
+    c: torch.Tensor = None
+
+    def gates_interleaved(self):
+        return self.gates.permute(1, 2, 0, 3).reshape(self.gates.shape[1], self.gates.shape[2], -1)
+
+
+def qrnn_init(gen: torch.Generator, m: int, n: int, k: int, gate_bias: float = 1.0, device="cuda") -> QrnnParams:
+    """qrnn_init (layers.hpp:411-422): W_s ~ U(+-1/sqrt(m k)), bias = gate_bias on f."""
+    if k < 1:
+        raise RuntimeError("qrnn_init: window must be >= 1")
+    s = 1.0 / math.sqrt(m * k)
+    W = torch.stack([_uniform(gen, 3 * n, m, s, device) for _ in range(k)])
+    bias = torch.zeros(3 * n, dtype=torch.float32, device=device)
+    bias[:n] = gate_bias
+    return QrnnParams(W.contiguous(), bias)
+
+
+def qrnn_forward(p: QrnnParams, x, c0=None, mode="parallel", precision="fp32", cache: QrnnCache | None = None):
+    """qrnn_forward (layers.hpp:449-494) -> h [T, b, n]; fills ``cache``."""
+    lib = _bind()
+    T, b, m, n = _dims(x, p.hidden())
+    k = p.window()
+    if m != p.input():
+        raise RuntimeError("qrnn_forward: input feature mismatch")
+    if k > T:
+        raise RuntimeError("qrnn_forward: filter window exceeds sequence length")
+    for t, nm in ((p.W, "W"), (p.bias, "bias")):
+        _check_f32(t, nm)
+    if c0 is not None:
+        _check_f32(c0, "c0")
+    dev = x.device
+    if cache is None:
+        cache = QrnnCache()
+    if cache.c is None or tuple(cache.c.shape) != (T, b, n):
+        cache.gates = torch.empty(3, T, b, n, dtype=torch.float32, device=dev)
+        cache.c = torch.empty(T, b, n, dtype=torch.float32, device=dev)
+    h = torch.empty(T, b, n, dtype=torch.float32, device=dev)
+    need = lib.linrec_qrnn_scratch_bytes(T, b, m, n, k)
+    scr = _scratch_for(need, dev)
+    _call(lib.linrec_qrnn_forward_f32(_p(p.W), _p(p.bias), _p(x), _p(c0), _p(h), _p(cache.gates), _p(cache.c),
+                                      T, b, m, n, k, MODE[mode], PRECISION[precision], _p(scr), scr.numel(),
+                                      torch.cuda.current_stream(dev).cuda_stream))
+    return h
+
+
+def qrnn_backward(p: QrnnParams, x, c0, cache: QrnnCache, d_h, grads: QrnnGrads, mode="parallel",
+                  precision="fp32", want_dc0=True):
+    """qrnn_backward (layers.hpp:496-548): accumulates into ``grads``; returns (dx, dc0)."""
+    lib = _bind()
+    T, b, m, n = _dims(x, p.hidden())
+    k = p.window()
+    _check_f32(d_h, "d_h")
+    dev = x.device
+    dx = torch.empty(T, b, m, dtype=torch.float32, device=dev)
+    dc0 = torch.empty(b, n, dtype=torch.float32, device=dev) if want_dc0 else None
+    need = lib.linrec_qrnn_scratch_bytes(T, b, m, n, k)
+    scr = _scratch_for(need, dev)
+    _call(lib.linrec_qrnn_backward_f32(_p(p.W), _p(x), _p(c0), _p(cache.gates), _p(cache.c), _p(d_h),
+                                       _p(grads.W), _p(grads.bias), _p(dx), _p(dc0), T, b, m, n, k, MODE[mode],
+                                       PRECISION[precision], _p(scr), scr.numel(),
+                                       torch.cuda.current_stream(dev).cuda_stream))
+    return dx, dc0
 
 
 # ---- torch autograd / nn.Module ---------------------------------------------------------

@@ -187,3 +187,46 @@ def test_module_autograd_matches_explicit_backward():
     torch.cuda.synchronize()
     assert torch.equal(dx, x.grad)
     assert torch.equal(grads.U, mod.U.grad)
+
+
+# ---- QRNN ----------------------------------------------------------------------------
+QRNN_SHAPES = [(1, 1, 4, 4, 1), (37, 3, 8, 12, 2), (64, 2, 36, 20, 3), (200, 2, 16, 32, 10), (129, 4, 64, 128, 2)]
+
+
+@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+@pytest.mark.parametrize("T,b,m,n,k", QRNN_SHAPES)
+def test_qrnn_forward_backward_vs_oracle(oracle, T, b, m, n, k, precision):
+    from oracle.oracle import qrnn_params
+    from paper_1709_04057_b200 import layers as L
+    rng = np.random.default_rng(T * 7 + k)
+    P = qrnn_params(rng, m, n, k)
+    x = rng.uniform(-1, 1, (T, b, m))
+    c0 = rng.uniform(-1, 1, (b, n))
+    dh = rng.uniform(-1, 1, (T, b, n))
+    h_ref, cache_ref = oracle.qrnn_forward(P, x, c0)
+    g_ref, dx_ref, dc0_ref = oracle.qrnn_backward(P, x, c0, cache_ref, dh)
+    p = L.QrnnParams(_dev(P["W"]), _dev(P["bias"]))
+    cache = L.QrnnCache()
+    xd, c0d = _dev(x), _dev(c0)
+    h = L.qrnn_forward(p, xd, c0d, precision=precision, cache=cache)
+    grads = L.QrnnGrads.zeros_like(p)
+    dx, dc0 = L.qrnn_backward(p, xd, c0d, cache, _dev(dh), grads, precision=precision)
+    torch.cuda.synchronize()
+    tol = TOL[precision]
+    assert _err(h, h_ref) < tol
+    assert _err(cache.gates_interleaved(), cache_ref["gates"]) < tol
+    assert _err(cache.c, cache_ref["c"]) < tol
+    assert _err(grads.W, g_ref["W"]) < tol
+    assert _err(grads.bias, g_ref["bias"]) < tol
+    assert _err(dx, dx_ref) < tol
+    assert _err(dc0, dc0_ref) < tol
+
+
+def test_qrnn_errors():
+    from paper_1709_04057_b200 import layers as L
+    gen = torch.Generator().manual_seed(0)
+    p = L.qrnn_init(gen, 8, 8, 5)
+    with pytest.raises(RuntimeError, match="window exceeds"):
+        L.qrnn_forward(p, torch.zeros(4, 1, 8, device="cuda"))
+    with pytest.raises(RuntimeError, match="window must be"):
+        L.qrnn_init(gen, 8, 8, 0)
