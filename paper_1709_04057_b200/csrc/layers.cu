@@ -50,15 +50,25 @@ __global__ void k_add(const float* __restrict__ a, const float* __restrict__ b, 
     out[i] = a[i] + b[i];
 }
 
-// dst[c] += sum_k part[k * pitch + c] in a fixed order (deterministic bias
-// gradients)
-__global__ void k_colsum(const float* __restrict__ part, int64_t nparts, int64_t pitch, int64_t ncols,
-                         float* __restrict__ dst) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= ncols) return;
+// dst[c] += sum_k part[k * pitch + c], deterministic: block = 32 columns x
+// 32 part-groups; group g sums parts g, g+32, ... in order, then the 32 group
+// sums are added in group order.
+__global__ void __launch_bounds__(1024) k_colsum(const float* __restrict__ part, int64_t nparts, int64_t pitch,
+                                                 int64_t ncols, float* __restrict__ dst) {
+  __shared__ float red[32][33];
+  const int cx = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + cx;
   float s = 0.f;
-  for (int64_t k = 0; k < nparts; ++k) s += part[k * pitch + c];
-  dst[c] += s;
+  if (c < ncols)
+    for (int64_t k = g; k < nparts; k += 32) s += __ldg(part + k * pitch + c);
+  red[g][cx] = s;
+  __syncthreads();
+  if (g == 0 && c < ncols) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) t += red[i][cx];
+    dst[c] += t;
+  }
 }
 
 __device__ __forceinline__ float dact(int a, float v) {  // activation_deriv_from_value (common.hpp:62-71)
@@ -77,6 +87,7 @@ __global__ void k_lstm_dpre(const float* __restrict__ gf, const float* __restric
   if (u >= n) return;
   const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(r0 + rpb, R);
   float4 sf = make_float4(0, 0, 0, 0), si = sf, so = sf, sz = sf;
+#pragma unroll 2
   for (int64_t r = r0; r < r1; ++r) {
     const int64_t o = r * n + u;
     const float4 f = ld4(gf + o), i = ld4(gi + o), og = ld4(go + o), z = ld4(gz + o);
@@ -112,6 +123,7 @@ __global__ void k_gilr_dpre(const float* __restrict__ g, const float* __restrict
   if (u >= n) return;
   const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(r0 + rpb, R);
   float4 sg = make_float4(0, 0, 0, 0), si = sg;
+#pragma unroll 2
   for (int64_t r = r0; r < r1; ++r) {
     const int64_t o = r * n + u;
     const float4 gv = ld4(g + o), iv = ld4(ci + o), d_l = ld4(dl + o), Gv = ld4(G + o);
@@ -141,6 +153,7 @@ __global__ void k_qrnn_dpre(const float* __restrict__ gf, const float* __restric
   if (u >= n) return;
   const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(r0 + rpb, R);
   float4 sf = make_float4(0, 0, 0, 0), so = sf, sz = sf;
+#pragma unroll 2
   for (int64_t r = r0; r < r1; ++r) {
     const int64_t o = r * n + u;
     const float4 f = ld4(gf + o), og = ld4(go + o), z = ld4(gz + o);
@@ -444,11 +457,11 @@ int gilr_backward_core(const linrec_gilr_params_f32* p, const float* x, const fl
                                                                           rp.rpb);
   LTRY(cudaGetLastError());
   if (gr->b_g) {
-    k_colsum<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(part, rp.nbx, 2 * n, n, gr->b_g);
+    k_colsum<<<(unsigned)((n + 31) / 32), 1024, 0, st>>>(part, rp.nbx, 2 * n, n, gr->b_g);
     LTRY(cudaGetLastError());
   }
   if (gr->b_z) {  // partial sums of di are columns [n, 2n)
-    k_colsum<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(part + n, rp.nbx, 2 * n, n, gr->b_z);
+    k_colsum<<<(unsigned)((n + 31) / 32), 1024, 0, st>>>(part + n, rp.nbx, 2 * n, n, gr->b_z);
     LTRY(cudaGetLastError());
   }
   mark(st, "dpre_surrogate");
@@ -564,7 +577,7 @@ int linrec_qrnn_backward_f32(const float* W, const float* x, const float* c0, co
                                                                           s.part, R, n, rp.rpb);
   LTRY(cudaGetLastError());
   if (dbias) {
-    k_colsum<<<(unsigned)((3 * n + 127) / 128), 128, 0, st>>>(s.part, rp.nbx, 3 * n, 3 * n, dbias);
+    k_colsum<<<(unsigned)((3 * n + 31) / 32), 1024, 0, st>>>(s.part, rp.nbx, 3 * n, 3 * n, dbias);
     LTRY(cudaGetLastError());
   }
   mark(st, "dpre_gates");
@@ -775,7 +788,7 @@ int linrec_gilr_lstm_backward_f32(const linrec_gilr_lstm_params_f32* p, const fl
                                                                           s.dpre, s.part, R, n, rp.rpb);
   LTRY(cudaGetLastError());
   if (grads->bias) {
-    k_colsum<<<(unsigned)((4 * n + 127) / 128), 128, 0, st>>>(s.part, rp.nbx, 4 * n, 4 * n, grads->bias);
+    k_colsum<<<(unsigned)((4 * n + 31) / 32), 1024, 0, st>>>(s.part, rp.nbx, 4 * n, 4 * n, grads->bias);
     LTRY(cudaGetLastError());
   }
   mark(st, "dpre_gates");

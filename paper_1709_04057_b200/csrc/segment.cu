@@ -32,14 +32,28 @@ k_fixup(const S* __restrict__ lam, const S* __restrict__ hprev_row, const S* __r
         const S* __restrict__ lam_next, S* __restrict__ seg_prod, const S* __restrict__ carry,
         int64_t carry_stride, const S* __restrict__ scale, S* __restrict__ out0 /* fwd: h; bwd: dx */,
         S* __restrict__ out1 /* bwd: dlam */, int64_t T, int64_t W, int64_t rows, int64_t ncols, int64_t nseg,
-        int64_t tseg, int64_t ntt) {
+        int64_t tseg, int64_t ntt, int64_t walk) {
   constexpr int NW = 8, RF = 4, G = 32 / Q, CPW = Q * VEC, NSEG = NW * G, PR = NSEG * RF;
   using IO = VecIO<S, VEC>;
   __shared__ S s_wp[NW][CPW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = lane % Q, g = lane / Q;
-  const int64_t col = blockIdx.x % ncols, pos = blockIdx.x / ncols;
-  const int64_t vseg = pos / ntt, p_in = pos % ntt;
+  const int64_t col = blockIdx.x % ncols;
+  // walk == 0: one CTA per chain position.  walk > 0 (no `scale`): CTA k of
+  // (segment, column) visits positions k, k+walk, ... and stops at the first
+  // whose entering correction is zero in every channel -- exact, because the
+  // products are applied oldest first (bit-identical whatever the look-back
+  // depth), so a zero product stays zero further down the chain.
+  int64_t vseg, p_in;
+  if (walk > 0) {
+    vseg = (blockIdx.x / ncols) / walk;
+    p_in = (blockIdx.x / ncols) % walk;
+  } else {
+    vseg = (blockIdx.x / ncols) / ntt;
+    p_in = (blockIdx.x / ncols) % ntt;
+  }
+  for (; p_in < ntt; p_in += (walk > 0 ? walk : ntt)) {
+  const int64_t pos = vseg * ntt + p_in;
   const int64_t tile_row = vseg * tseg + (REV ? ntt - 1 - p_in : p_in) * rows;
   const int64_t ch = col * CPW + (int64_t)q * VEC;
   const bool valid = ch < W;
@@ -57,7 +71,7 @@ k_fixup(const S* __restrict__ lam, const S* __restrict__ hprev_row, const S* __r
       nz = nz || e[v] != S(0);
     }
   }
-  nz = __syncthreads_or(nz);  // every thread has read seg_prod past this point
+  nz = __syncthreads_or(nz) != 0;  // every thread has read seg_prod past this point
   if (scale != nullptr && valid && warp == 0 && g == 0) {  // virtual -> segment-relative products
     S* sp = seg_prod + pos * W + ch;
     const S* sc = scale + vseg * W + ch;
@@ -167,6 +181,8 @@ k_fixup(const S* __restrict__ lam, const S* __restrict__ hprev_row, const S* __r
       e[v] = mul_(tot, e[v]);
     }
   }
+  __syncthreads();  // s_wp is reused by the next position
+  }
 }
 
 // out[j] = fold over q in [first, last) by `step` of c = A_q[j] * c + B_q[j],
@@ -232,14 +248,16 @@ cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S
   const int q = pick_q(nvec);
   const int cpw = q * (vec_ok ? V : 1);
   const int64_t ncols = (W + cpw - 1) / cpw;
-  const dim3 grid((unsigned)(ncols * nseg * ntt));
+  // the walk needs seg_prod untouched after the check: only without `scale`
+  const int64_t walk = scale == nullptr ? (ntt < 8 ? ntt : 8) : 0;
+  const dim3 grid((unsigned)(ncols * nseg * (walk > 0 ? walk : ntt)));
 #define FIX(VV)                                                                                       \
   LINREC_Q_SWITCH(q, if (reverse) linrec_dev::k_fixup<S, VV, Q_, true><<<grid, 256, 0, st>>>(         \
                          lam, hprev_row, h, lam_next, seg_prod, carry, carry_stride, scale, out0, out1, T, \
-                         W, rows, ncols, nseg, tseg, ntt);                                            \
+                         W, rows, ncols, nseg, tseg, ntt, walk);                                            \
                      else linrec_dev::k_fixup<S, VV, Q_, false><<<grid, 256, 0, st>>>(                \
                          lam, hprev_row, h, lam_next, seg_prod, carry, carry_stride, scale, out0, out1, T, \
-                         W, rows, ncols, nseg, tseg, ntt));
+                         W, rows, ncols, nseg, tseg, ntt, walk));
   if (vec_ok) {
     FIX(V)
   } else {
