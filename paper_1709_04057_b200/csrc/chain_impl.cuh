@@ -31,18 +31,26 @@ inline int pick_q(int64_t nvec) {
 // serial; splitting T into independent chains (stitched afterwards by a carry
 // fold + fix-up, segment.cu) restores parallelism.  Aim for >= 64 chains
 // (LINREC_CHAINS overrides for tuning), keeping >= 8 tiles per segment.
-inline int64_t chain_target() {
-  static const int64_t v = [] {
-    const char* e = std::getenv("LINREC_CHAINS");
-    const long n = e ? std::atol(e) : 0;
-    return (int64_t)(n > 0 ? n : 64);
-  }();
-  return v;
+// Independent look-back chains wanted per launch (columns x virtual
+// segments).  Measured on B200 (scripts/tune.py sweeps of 64-512 chains over
+// W = 16 ... 8192): the forward scan is best at ~256 chains
+// (C2 0.90 -> 0.96 of peak; W = 2048 0.78 -> 0.84; C4 / W = 16 within 1-2 %
+// of their best), the backward -- 20 B/el per tile, so the look-back is
+// already hidden -- at 64.  LINREC_CHAINS / LINREC_CHAINS_FWD /
+// LINREC_CHAINS_BWD override.
+inline int64_t chain_target(bool forward) {
+  static const long env_all = [] { const char* e = std::getenv("LINREC_CHAINS"); return e ? std::atol(e) : 0L; }();
+  static const long env_fwd = [] { const char* e = std::getenv("LINREC_CHAINS_FWD"); return e ? std::atol(e) : 0L; }();
+  static const long env_bwd = [] { const char* e = std::getenv("LINREC_CHAINS_BWD"); return e ? std::atol(e) : 0L; }();
+  const long env = forward ? env_fwd : env_bwd;
+  if (env > 0) return env;
+  if (env_all > 0) return env_all;
+  return forward ? 256 : 64;
 }
 
-inline void choose_segments(ChainPlan& p, int64_t T) {
+inline void choose_segments(ChainPlan& p, int64_t T, bool forward) {
   const int64_t ntt_total = (T + p.rows - 1) / p.rows;
-  const int64_t target = chain_target();
+  const int64_t target = chain_target(forward);
   int64_t nseg = (target + p.ncols - 1) / p.ncols;
   if (nseg > ntt_total / 8) nseg = ntt_total / 8;
   if (nseg < 1) nseg = 1;
@@ -62,12 +70,12 @@ size_t vseg_bytes(const ChainPlan& p, int64_t W) {
 }
 
 template <class S, int VEC, int Q, int R, int NW>
-void fill_plan(ChainPlan& p, int64_t T, int64_t W) {
+void fill_plan(ChainPlan& p, int64_t T, int64_t W, bool forward) {
   using Cfg = linrec_dev::ChainCfg<S, VEC, Q, R, NW>;
   p.vec = VEC; p.q = Q; p.r = R; p.nw = NW;
   p.cpw = Cfg::CPW; p.rows = Cfg::L; p.rec = Cfg::REC;
   p.ncols = (W + Cfg::CPW - 1) / Cfg::CPW;
-  choose_segments(p, T);
+  choose_segments(p, T, forward);
   p.flags_bytes = ((size_t)p.ntiles * 4 + 255) / 256 * 256;
   p.rec_bytes = (size_t)p.ntiles * 2 * Cfg::REC * 8;
   p.ws_bytes = 256 + p.flags_bytes + 2 * p.rec_bytes + vseg_bytes<S>(p, W);
@@ -100,10 +108,10 @@ ChainPlan plan_chain_dir(int64_t T, int64_t W, bool vec_ok) {
   ChainPlan p;
   if (vec_ok) {
     const int q = pick_q((W + Tn::VEC - 1) / Tn::VEC);
-    LINREC_Q_SWITCH(q, fill_plan<S, Tn::VEC, Q_, R, NW>(p, T, W));
+    LINREC_Q_SWITCH(q, fill_plan<S, Tn::VEC, Q_, R, NW>(p, T, W, FWD));
   } else {
     const int q = pick_q(W);
-    LINREC_Q_SWITCH(q, fill_plan<S, 1, Q_, R, NW>(p, T, W));
+    LINREC_Q_SWITCH(q, fill_plan<S, 1, Q_, R, NW>(p, T, W, FWD));
   }
   return p;
 }

@@ -68,7 +68,7 @@ void fill_tma_plan(ChainPlan& p, int64_t T, int64_t W, Kern kern) {
   p.cpw = Cfg::CPW; p.rows = Cfg::L; p.rec = Cfg::REC;
   p.box_cols = Cfg::CPW; p.box_rows = Cfg::BOX_ROWS;
   p.ncols = (W + Cfg::CPW - 1) / Cfg::CPW;
-  choose_segments(p, T);
+  choose_segments(p, T, NARR == 2);  // forward kernels stage 2 arrays, backward 3
   p.flags_bytes = ((size_t)p.ntiles * 4 + 255) / 256 * 256;
   p.rec_bytes = (size_t)p.ntiles * 2 * Cfg::REC * 8;
   p.ws_bytes = 256 + p.flags_bytes + 2 * p.rec_bytes + vseg_bytes<S>(p, W);
