@@ -360,6 +360,27 @@ int linrec_qrnn_backward_f32(const float* W, const float* x, const float* c0, co
                              int64_t m, int64_t n, int64_t k, int mode, int precision, void* scratch,
                              size_t scratch_bytes, void* stream);
 
+/* ---- training loop (training.hpp) ----------------------------------------- *
+ * The reference's synthetic long-dependency task: generate_batch (:30-43)
+ * from the reference Rng's counter-based splitmix64 stream (rng.hpp:21-27;
+ * `counter` = draws taken so far, the batch takes b*T), one-hot x [T][b][p]
+ * and labels [b] on the device; the readout + softmax cross-entropy of
+ * model_forward / softmax_loss (:160-222) with loss_acc = (mean loss,
+ * accuracy) as two device doubles; its backward (:229-240, dW_out / db_out
+ * accumulate, d_hlast = the gradient of the last step); and
+ * clip_global_norm + Adam (:248-288) fused over one flat parameter buffer with
+ * fp64 moments (norm_out: device double, pre-clip norm; may be NULL). */
+int linrec_synthetic_batch_f32(uint64_t seed, uint64_t counter, int64_t T, int64_t b, int64_t p, float* x,
+                               int32_t* labels, void* stream);
+int linrec_readout_loss_f32(const float* h_last, const float* W_out, const float* b_out, const int32_t* labels,
+                            float* logits, float* d_logits, double* loss_acc, int64_t b, int64_t n, void* stream);
+int linrec_readout_backward_f32(const float* d_logits, const float* h_last, const float* W_out, float* dW_out,
+                                float* db_out, float* d_hlast, int64_t b, int64_t n, void* stream);
+size_t linrec_adam_scratch_bytes(void);
+int linrec_clip_adam_f32(float* params, float* grads, double* m, double* v, int64_t count, double lr, double beta1,
+                         double beta2, double eps, int64_t step, double clip_norm, double* norm_out, void* scratch,
+                         size_t scratch_bytes, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif
