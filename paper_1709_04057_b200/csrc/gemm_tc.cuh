@@ -35,12 +35,13 @@
 //   warp 1      TMEM allocator (cta_group::2); leader: tcgen05.mma issuer,
 //               two 256-column accumulators so the epilogue of tile t
 //               overlaps the mainloop of tile t+1
-//   warps 2-3   3xTF32 split (SPLIT3) and relay of "stage landed + split" to
-//               the leader
-//   warps 4-11  epilogue: 2 warps per TMEM lane quadrant, 128 fp32 register
+//   warps 2-7   3xTF32 split (SPLIT3) and relay of "stage landed + split" to
+//               the leader (six warps: with two, the split's smem round trip
+//               and not the tensor core bounded 3xTF32)
+//   warps 8-15  epilogue: 2 warps per TMEM lane quadrant, 128 fp32 register
 //               accumulators each; fused epilogue -> 128B-swizzled smem box
 //               -> TMA store (or TMA reduce-add for C += A*B)
-//   setmaxnreg moves registers from warps 0-3 (56) to the epilogue (224).
+//   setmaxnreg moves registers from warps 0-7 (64) to the epilogue (192).
 //
 // Shared-memory operand layouts (canonical UMMA layouts):
 //   K-major:  TMA box {32 elems = 128 B, rows}, SWIZZLE_128B
@@ -62,8 +63,10 @@ namespace tc {
 constexpr int BM = 128;      // A rows per CTA (the MMA's M = 256 spans the pair)
 constexpr int BN = 256;      // widest MMA N; each CTA stages BN/2 B rows (QRNN tiles use N = 192)
 constexpr int BK = 32;       // fp32 elements per k-block = one 128-byte swizzle row
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 constexpr int kEpiWarps = 8;
+constexpr int kSplitWarps = 6;   // warps 2..7
+constexpr int kEpiWarp0 = 8;     // first epilogue warp
 
 // ---- tcgen05 / cluster wrappers ----------------------------------------------
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -360,7 +363,7 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&ready[s], 2 * 64);
+      mbar_init(&ready[s], 2 * kSplitWarps * 32);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
@@ -375,7 +378,7 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {  // ------------------------------------------ TMA producer
-    setmaxnreg_dec<56>();
+    setmaxnreg_dec<64>();
     if (lane == 0) {
       prefetch_tmap(&ta1);
       prefetch_tmap(&tb1);
@@ -435,7 +438,7 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
       }
     }
   } else if (warp == 1) {  // ------------------------------------- MMA issuer
-    setmaxnreg_dec<56>();
+    setmaxnreg_dec<64>();
     if (leader && lane == 0) {
       // One accumulation unit = KCHUNK k-blocks of one tile, accumulated from
       // zero in TMEM slot (unit & 1); the epilogue sums the units in fp32.
@@ -476,10 +479,10 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
         }
       }
     }
-  } else if (warp < 4) {  // -------------------------------------- 3xTF32 split
-    setmaxnreg_dec<56>();
+  } else if (warp < kEpiWarp0) {  // ------------------------------- 3xTF32 split
+    setmaxnreg_dec<64>();
     if (SPLIT3) {
-      const int st = threadIdx.x - 64;  // 0..63
+      const int st = threadIdx.x - 64;  // 0 .. kSplitWarps*32-1
       const uint32_t ready_leader = mapa(smem_u32(ready), 0);
       uint32_t it = 0;
       for (int t = cid; t < ntiles; t += ncl) {
@@ -491,7 +494,7 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
           const float4* src = reinterpret_cast<const float4*>(smem + s * Cfg::STAGE_BYTES);
           float4* dst = reinterpret_cast<float4*>(smem + Cfg::LO_OFF + s * Cfg::STAGE_BYTES);
 #pragma unroll 4
-          for (int e = st; e < Cfg::STAGE_BYTES / 16; e += 64) {
+          for (int e = st; e < Cfg::STAGE_BYTES / 16; e += kSplitWarps * 32) {
             const float4 v = src[e];
             dst[e] = make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z), v.w - tf32_hi(v.w));
           }
@@ -501,10 +504,10 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
       }
     }
   } else {  // ------------------------------------------------------- epilogue
-    setmaxnreg_inc<224>();
+    setmaxnreg_inc<192>();
     const int q = warp & 3;          // TMEM lane quadrant this warp may access
-    const int hf = (warp - 4) >> 2;  // which half of the tile's units
-    unsigned char* box = smem + Cfg::EPI_OFF + (warp - 4) * Cfg::EPI_BYTES;
+    const int hf = (warp - kEpiWarp0) >> 2;  // which half of the tile's units
+    unsigned char* box = smem + Cfg::EPI_OFF + (warp - kEpiWarp0) * Cfg::EPI_BYTES;
     const uint32_t acc_empty_leader = mapa(smem_u32(acc_empty), 0);
     uint32_t unit = 0;
     for (int t = cid; t < ntiles; t += ncl) {

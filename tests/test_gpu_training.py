@@ -97,3 +97,19 @@ def test_config_errors():
         run_experiment(TrainConfig(arch="gru"))
     with pytest.raises(RuntimeError, match="counts out of range"):
         run_experiment(TrainConfig(layers=3))
+
+
+def test_long_sequence_step_follows_the_oracle(oracle):
+    """T = 300: the gradient reaching step 1 through both layers and the
+    readout matches the fp64 oracle after two Adam steps."""
+    from oracle.train_oracle import run_experiment as orun, tensors
+    from paper_1709_04057_b200.training import run_experiment
+    cfg, ocfg = _cfgs(seq_len=300, max_iters=2, learning_rate=3e-3, gate_bias=3.0)
+    keep = []
+    rep = run_experiment(cfg, trainer_out=keep)
+    orep, otr = orun(ocfg, oracle=oracle)
+    for row, (it, loss, acc) in zip(rep.trace, orep.trace):
+        assert row.loss == pytest.approx(loss, rel=1e-4)
+    for a, b in zip(keep[0].model.tensors(), tensors(otr.model)):
+        d = np.abs(a.cpu().numpy().astype(np.float64) - b).max() / max(np.abs(b).max(), 1e-30)
+        assert d < 1e-4
