@@ -494,14 +494,11 @@ def layer_stage_work(T, b, m, n):
 
 
 def tensor_peak():
-    """dense TF32 tensor-core peak: half the measured bf16 dense rate."""
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    try:
-        with open(path) as f:
-            p = json.load(f)
-        return float(p["bf16_tflops"]) / 2, "measured bf16 dense / 2 (kind::tf32 runs at half the bf16 rate)"
-    except Exception:
-        return 1125.0, "fallback: nominal 2.25 PF bf16 / 2"
+    """Dense TF32 tensor-core peak for the roofline: the nominal 1.1 PFLOP/s
+    of B200_PROFILING.md.  MEASURED_PEAKS.json has no TF32 figure, and half of
+    its measured bf16 rate (cuBLAS) is no upper bound here: the 3xTF32 GEMMs
+    issue MMAs at ~900 TF/s with the split disabled."""
+    return 1100.0, "nominal dense TF32 (B200_PROFILING.md); no measured TF32 peak exists"
 
 
 def run_layer(args):
@@ -561,6 +558,7 @@ def run_layer(args):
             if kind == "flop":
                 rec["tflops"] = amount / (avg / 1e3) / 1e12
                 rec["frac_tf32_peak"] = rec["tflops"] / tpk
+                rec["mma_issue_frac"] = rec["frac_tf32_peak"] * (3 if prec == "fp32" else 1)
                 if best is None or avg > best[1]:
                     best = (name, avg, amount)
             else:
@@ -603,7 +601,9 @@ def run_layer(args):
             "peak_kind": tpk_kind,
             "unit": "TFLOP/s",
             "frac": achieved / tpk,
+            # 3xTF32 issues three MMAs per algorithmic product
             "mma_issue_frac": (3 if prec == "fp32" else 1) * achieved / tpk,
+            "effective_peak_for_precision": tpk / (3 if prec == "fp32" else 1),
             "traffic": None,
             "algorithmic_flops_per_launch": bflop,
         },
