@@ -33,7 +33,7 @@ k_fixup(const S* __restrict__ lam, const S* __restrict__ hprev_row, const S* __r
         int64_t carry_stride, const S* __restrict__ scale, S* __restrict__ out0 /* fwd: h; bwd: dx */,
         S* __restrict__ out1 /* bwd: dlam */, int64_t T, int64_t W, int64_t rows, int64_t ncols, int64_t nseg,
         int64_t tseg, int64_t ntt, int64_t walk) {
-  constexpr int NW = 8, RF = 4, G = 32 / Q, CPW = Q * VEC, NSEG = NW * G, PR = NSEG * RF;
+  constexpr int NW = 8, RF = 12, G = 32 / Q, CPW = Q * VEC, NSEG = NW * G, PR = NSEG * RF;  // PR = a TMA tile
   using IO = VecIO<S, VEC>;
   __shared__ S s_wp[NW][CPW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -198,7 +198,7 @@ __global__ void k_compose(const S* __restrict__ aggs, int64_t first, int64_t las
   }
 }
 
-// Virtual-segment finalisation (one thread per channel).
+// Virtual-segment finalisation.
 // forward: carry[s] = state entering segment s (0 for s = 0, whose chain was
 //   seeded), scale[s] = decay product of the segments before s, agg_rank =
 //   (product over all, final state).
@@ -206,26 +206,68 @@ __global__ void k_compose(const S* __restrict__ aggs, int64_t first, int64_t las
 //   last), scale[s] = product of the A' of the segments after s, agg_rank =
 //   (A', B') of the whole range, dh0 = lam_0 * G_0 (the range's start).
 // vagg[s] = (P_incl, c_incl) of segment s's chains.
+// Block = 32 channels x G segment groups: each group composes its contiguous
+// range of segments (processing order), the groups' composites are folded in
+// group order, and each group re-walks its range from its incoming state --
+// a fixed association (deterministic), sequential depth 2*nseg/G + G instead
+// of nseg (C4: 256 segments, 49 -> a few us).
 template <class S, bool REV>
-__global__ void k_vseg_finalize(const S* __restrict__ lam, const S* __restrict__ vagg, int64_t nseg, int64_t tseg,
-                                S* __restrict__ carry, S* __restrict__ scale, S* __restrict__ agg_rank,
-                                S* __restrict__ dh0, int64_t W) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < W;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    S c = S(0), pc = S(1);
-    for (int64_t i = 0; i < nseg; ++i) {
-      const int64_t s = REV ? nseg - 1 - i : i;
-      if (carry != nullptr) carry[s * W + j] = c;
-      if (scale != nullptr) scale[s * W + j] = pc;
-      S A = vagg[s * 2 * W + j], B = vagg[s * 2 * W + W + j];
-      if (REV) {
-        const S l0 = lam[(s * tseg) * W + j];
-        A = mul_(l0, A);
-        B = mul_(l0, B);
-      }
-      c = fma_(A, c, B);
-      pc = mul_(A, pc);
+__device__ __forceinline__ void vseg_pair(const S* __restrict__ lam, const S* __restrict__ vagg, int64_t nseg,
+                                          int64_t tseg, int64_t W, int64_t i, int64_t j, S& A, S& B) {
+  const int64_t s = REV ? nseg - 1 - i : i;
+  A = vagg[s * 2 * W + j];
+  B = vagg[s * 2 * W + W + j];
+  if (REV) {
+    const S l0 = lam[(s * tseg) * W + j];
+    A = mul_(l0, A);
+    B = mul_(l0, B);
+  }
+}
+
+template <class S, bool REV, int G>
+__global__ void __launch_bounds__(32 * G)
+k_vseg_finalize(const S* __restrict__ lam, const S* __restrict__ vagg, int64_t nseg, int64_t tseg,
+                S* __restrict__ carry, S* __restrict__ scale, S* __restrict__ agg_rank, S* __restrict__ dh0,
+                int64_t W) {
+  __shared__ S sA[G][32], sB[G][32];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+  const bool ok = j < W;
+  const int64_t per = (nseg + G - 1) / G;
+  const int64_t i0 = (int64_t)g * per, i1 = i0 + per < nseg ? i0 + per : nseg;
+  // phase 1: composite (A, B) of this group's segments, oldest first
+  S Ac = S(1), Bc = S(0);
+  if (ok) {
+#pragma unroll 4
+    for (int64_t i = i0; i < i1; ++i) {
+      S A, B;
+      vseg_pair<S, REV>(lam, vagg, nseg, tseg, W, i, j, A, B);
+      Bc = fma_(A, Bc, B);
+      Ac = mul_(A, Ac);
     }
+  }
+  sA[g][lane] = Ac;
+  sB[g][lane] = Bc;
+  __syncthreads();
+  // phase 2: state and product entering this group (groups folded in order)
+  S c = S(0), pc = S(1);
+  for (int q = 0; q < g; ++q) {
+    c = fma_(sA[q][lane], c, sB[q][lane]);
+    pc = mul_(sA[q][lane], pc);
+  }
+  if (!ok) return;
+  // phase 3: re-walk, writing each segment's incoming state / product
+#pragma unroll 4
+  for (int64_t i = i0; i < i1; ++i) {
+    const int64_t s = REV ? nseg - 1 - i : i;
+    if (carry != nullptr) carry[s * W + j] = c;
+    if (scale != nullptr) scale[s * W + j] = pc;
+    S A, B;
+    vseg_pair<S, REV>(lam, vagg, nseg, tseg, W, i, j, A, B);
+    c = fma_(A, c, B);
+    pc = mul_(A, pc);
+  }
+  if (i1 == nseg && i0 < i1) {  // the group holding the last segment reports the whole range
     if (agg_rank != nullptr) {
       agg_rank[j] = pc;
       agg_rank[W + j] = c;
@@ -270,12 +312,12 @@ cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S
 template <class S>
 cudaError_t launch_vseg_finalize(bool reverse, const S* lam, const S* vagg, int64_t nseg, int64_t tseg, S* carry,
                                  S* scale, S* agg_rank, S* dh0, int64_t W, cudaStream_t st) {
-  const int64_t blocks = (W + 127) / 128;
-  const unsigned g = (unsigned)(blocks < 1024 ? blocks : 1024);
+  constexpr int G = 16;
+  const unsigned g = (unsigned)((W + 31) / 32);
   if (reverse)
-    linrec_dev::k_vseg_finalize<S, true><<<g, 128, 0, st>>>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W);
+    linrec_dev::k_vseg_finalize<S, true, G><<<g, 32 * G, 0, st>>>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W);
   else
-    linrec_dev::k_vseg_finalize<S, false><<<g, 128, 0, st>>>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W);
+    linrec_dev::k_vseg_finalize<S, false, G><<<g, 32 * G, 0, st>>>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W);
   return cudaGetLastError();
 }
 
