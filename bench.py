@@ -279,7 +279,9 @@ def run_ours(args):
             "config": {
                 "workload": wl["desc"],
                 "T": T, "B": B, "D": D, "elements_per_step": N_total,
-                "parallelism": ("sequence-sharded x%d (carry all-gather)" % world) if seq_sharded
+                "parallelism": ("sequence-sharded x%d (carry exchange: %s)" % (
+                    world, "peer-memory mailboxes over NVLink" if runner.exchange == "p2p" else "all-gather"))
+                if seq_sharded
                 else ("single GPU" if world == 1 else "channel-sharded x%d (independent [T,W] blocks, no collective)" % world),
                 "l2": "no flush: every tensor is %.0f MiB >> 126 MB L2" % (N_local * 4 / 2**20),
                 "timing": "CUDA events on the launching stream, max over ranks",
@@ -320,6 +322,8 @@ def run_ours(args):
             result["cpu_baseline"] = cpu_baseline_leg(args, T, B, D)
         print(json.dumps(result), flush=True)
     if world > 1:
+        if seq_sharded:
+            runner.close()
         dist.barrier()
         dist.destroy_process_group()
 

@@ -381,6 +381,32 @@ int linrec_clip_adam_f32(float* params, float* grads, double* m, double* v, int6
                          double beta2, double eps, int64_t step, double clip_norm, double* norm_out, void* scratch,
                          size_t scratch_bytes, void* stream);
 
+/* ---- sequence-sharding carry exchange over peer memory -------------------- *
+ * The NCCL all-gather of the carries (linrec_segment_* above) replaced by
+ * direct stores into the consumers' memory over NVLink plus release/acquire
+ * flags (csrc/p2p.cu).  Each rank allocates one mailbox of
+ * linrec_p2p_mailbox_bytes(W, world) with linrec_ipc_alloc (cudaMalloc +
+ * cudaIpcGetMemHandle, 64-byte handle), exchanges handles out of band, opens
+ * the peers' with linrec_ipc_open and passes a DEVICE array of the world
+ * mailbox pointers (own at index rank).  dir 0 = forward, 1 = backward;
+ * epoch = 1, 2, ... per call, equal on all ranks.
+ * publish: this rank's aggregate agg [2][W] -> slot [dir][rank] of ranks
+ *   [q0, q1) (waits until each consumer acked epoch-1).
+ * compose: out = fold over sources first, first+step, ... != last of
+ *   c = A_q c + B_q from seed (NULL = 0), q == rank taken from `local`;
+ *   waits for the sources' flags, then acks them -- the same fold, in the
+ *   same order, as linrec_compose_carries_f32. */
+size_t linrec_p2p_mailbox_bytes(int64_t W, int world);
+int linrec_ipc_alloc(size_t bytes, void** ptr, unsigned char* handle64);
+int linrec_ipc_open(const unsigned char* handle64, void** ptr);
+int linrec_ipc_close(void* ptr);
+int linrec_ipc_free(void* ptr);
+int linrec_p2p_publish_f32(const float* agg, int64_t W, int world, int rank, int dir, uint64_t epoch,
+                           void* const* mboxes, int q0, int q1, void* stream);
+int linrec_p2p_compose_f32(int64_t W, int world, int rank, int dir, uint64_t epoch, void* const* mboxes,
+                           const float* local, int64_t first, int64_t last, int64_t step, const float* seed,
+                           float* out, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -67,6 +67,15 @@ def _load():
     lib.linrec_gemm_f32.argtypes = [_vp, _int, _i64, _vp, _int, _i64, _vp, _i64, _i64, _i64, _i64, _int, _int,
                                     _int, _vp, _vp]
     lib.linrec_gemm_splits.argtypes = [_i64, _i64, _i64]
+    lib.linrec_p2p_mailbox_bytes.restype = C.c_size_t
+    lib.linrec_p2p_mailbox_bytes.argtypes = [_i64, _int]
+    lib.linrec_ipc_alloc.argtypes = [C.c_size_t, C.POINTER(_vp), C.c_char_p]
+    lib.linrec_ipc_open.argtypes = [C.c_char_p, C.POINTER(_vp)]
+    lib.linrec_ipc_close.argtypes = [_vp]
+    lib.linrec_ipc_free.argtypes = [_vp]
+    lib.linrec_p2p_publish_f32.argtypes = [_vp, _i64, _int, _int, _int, C.c_uint64, _vp, _int, _int, _vp]
+    lib.linrec_p2p_compose_f32.argtypes = [_i64, _int, _int, _int, C.c_uint64, _vp, _vp, _i64, _i64, _i64, _vp,
+                                           _vp, _vp]
     lib.linrec_gemm_scratch_bytes.restype = C.c_size_t
     lib.linrec_gemm_scratch_bytes.argtypes = [_i64, _i64, _int]
     lib.linrec_segment_prod_rows.restype = _i64

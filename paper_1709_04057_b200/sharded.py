@@ -6,10 +6,15 @@
 * Sequence sharding -- T is split into contiguous segments, one per rank
   (`segment_bounds`).  Per direction each rank runs ONE zero-carry chained scan
   of its segment (12 / 20 B/element), the ranks exchange a 2*W-value carry
-  with one all-gather, and a fix-up kernel adds the carry's decaying
-  contribution to the leading tiles of the segment (include/linrec_cuda.h,
-  csrc/segment.cu).  The collective is the only inter-GPU traffic: 2*W*4
-  bytes per rank per direction (1 KiB at W = 128).
+  and a fix-up kernel adds the carry's decaying contribution to the leading
+  tiles of the segment (include/linrec_cuda.h, csrc/segment.cu).  The
+  exchange is the only inter-GPU traffic: 2*W*4 bytes per rank per direction
+  (1 KiB at W = 128).  By default it goes over peer memory (``PeerMailboxes``,
+  csrc/p2p.cu): each rank stores its aggregate straight into the consumers'
+  mailboxes over NVLink and raises a release flag that their fold kernel
+  acquires -- no collective launch, a few microseconds instead of an NCCL
+  all-gather's ~15.  Ranks on different nodes (no CUDA IPC) fall back to the
+  all-gather.
 
 The orchestration is written against a small backend interface so that the
 same code drives the CUDA kernels (``CudaBackend``, NCCL) and, in the CPU test
@@ -89,6 +94,61 @@ class CudaBackend:
                                     rows, 4, self._st())
 
 
+class PeerMailboxes:
+    """One CUDA-IPC mailbox per rank (csrc/p2p.cu); every rank maps every
+    peer's.  Handles travel once through the process group."""
+
+    def __init__(self, W, group, device):
+        import ctypes as C
+        lib = capi.lib
+        self.group, self.W = group, W
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        nbytes = lib.linrec_p2p_mailbox_bytes(W, self.world)
+        own, handle = C.c_void_p(), C.create_string_buffer(64)
+        capi.check(lib.linrec_ipc_alloc(nbytes, C.byref(own), handle))
+        self.own = own.value
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle.raw, group=group)
+        self.opened, ptrs = [], []
+        for q, h in enumerate(handles):
+            if q == self.rank:
+                ptrs.append(self.own)
+                continue
+            p = C.c_void_p()
+            capi.check(lib.linrec_ipc_open(h, C.byref(p)))
+            self.opened.append(p.value)
+            ptrs.append(p.value)
+        self.ptrs = torch.tensor(ptrs, dtype=torch.int64, device=device)  # device array of mailbox pointers
+        self.epoch = [0, 0]
+
+    def publish(self, agg, direction, q0, q1, stream):
+        capi.check(capi.lib.linrec_p2p_publish_f32(agg.data_ptr(), self.W, self.world, self.rank, direction,
+                                                   self.epoch[direction], self.ptrs.data_ptr(), q0, q1, stream))
+
+    def compose(self, direction, local, first, last, step, seed, out, stream):
+        capi.check(capi.lib.linrec_p2p_compose_f32(self.W, self.world, self.rank, direction, self.epoch[direction],
+                                                   self.ptrs.data_ptr(), local.data_ptr(), first, last, step,
+                                                   None if seed is None else seed.data_ptr(), out.data_ptr(), stream))
+
+    def close(self):
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        for p in self.opened:
+            capi.lib.linrec_ipc_close(p)
+        self.opened = []
+        dist.barrier(group=self.group)
+        if self.own:
+            capi.lib.linrec_ipc_free(self.own)
+            self.own = None
+
+
+def _same_node(group) -> bool:
+    import socket
+    names = [None] * dist.get_world_size(group)
+    dist.all_gather_object(names, socket.gethostname(), group=group)
+    return len(set(names)) == 1
+
+
 class SequenceShardedScan:
     """h = scan(lam, x, h0) and its gradients with T split across the ranks
     of `group`; rank r holds rows segment_bounds(T, world, r) of every
@@ -98,7 +158,10 @@ class SequenceShardedScan:
     backward(lam, h0, h, dh, dlam, dx, dh0)     dh0 written on rank 0 only
     """
 
-    def __init__(self, T, W, group=None, ws=None, stream=None, backend=None, device=None):
+    def __init__(self, T, W, group=None, ws=None, stream=None, backend=None, device=None, exchange="auto"):
+        """exchange: "p2p" (peer-memory mailboxes, csrc/p2p.cu), "collective"
+        (all-gather) or "auto" (p2p when every rank is on this node and the
+        CUDA backend runs)."""
         self.group = group if group is not None else dist.group.WORLD
         self.world = dist.get_world_size(self.group)
         self.rank = dist.get_rank(self.group)
@@ -123,11 +186,20 @@ class SequenceShardedScan:
         self.ones = torch.ones(W, **f)
         self.zeros = torch.zeros(W, **f)
         self.hprev = None
+        use_p2p = exchange == "p2p" or (exchange == "auto" and backend is None and self.world > 1
+                                        and _same_node(self.group))
+        self.mb = PeerMailboxes(W, self.group, dev) if use_p2p else None
+        self.exchange = "p2p" if use_p2p else "collective"
         # kernels launched per step on this rank (for bench.py's gpu_launches)
         r, R = self.rank, self.world
         # fwd: scan + finalize (+ fix-up when virtually segmented) + compose/fix-up
         # for r > 0; bwd likewise + the dh0 compose on rank 0
-        self.launches_per_step = (2 + (2 if r > 0 else 0)) + (2 + (2 if r < R - 1 else 0) + (1 if r == 0 else 0))
+        if use_p2p:  # scan(+finalize), publish, compose + ack, fix-up; likewise backward (+ dh0 fold)
+            self.launches_per_step = ((2 + (1 if r < R - 1 else 0) + (3 if r > 0 else 0))
+                                      + (2 + (1 if r > 0 else 0) + (3 if r < R - 1 else 0) + (1 if r == 0 else 0)))
+        else:
+            self.launches_per_step = ((2 + (2 if r > 0 else 0))
+                                      + (2 + (2 if r < R - 1 else 0) + (1 if r == 0 else 0)))
 
     def _on_stream(self):
         if self.stream is not None and torch.cuda.is_available() and isinstance(self.stream, torch.cuda.Stream):
@@ -158,13 +230,22 @@ class SequenceShardedScan:
             return self._forward(lam, x, h0, h)
 
     def _forward(self, lam, x, h0, h):
-        r, W, T = self.rank, self.W, self.Tl
+        r, R, W, T = self.rank, self.world, self.W, self.Tl
         self.be.segment_scan(lam, x, h0 if r == 0 else None, h, self.seg_prod_f, self.agg, T, W)
         if r == 0:
             self.agg[0].zero_()  # h0 is already folded into rank 0's segment
-        self._all_gather(self.agg, self.aggs)
+        if self.mb is not None:
+            st = self.be._st()
+            self.mb.epoch[0] += 1
+            if r < R - 1:
+                self.mb.publish(self.agg, 0, r + 1, R, st)
+            if r > 0:
+                self.mb.compose(0, self.agg, 0, r, 1, None, self.c_in, st)
+        else:
+            self._all_gather(self.agg, self.aggs)
+            if r > 0:
+                self.be.compose(self.aggs, 0, r, 1, None, self.c_in, W)
         if r > 0:
-            self.be.compose(self.aggs, 0, r, 1, None, self.c_in, W)
             self.be.fixup(lam, h, self.seg_prod_f, self.c_in, T, W, self.rows_f)
             self.hprev = self.c_in
         else:
@@ -186,16 +267,32 @@ class SequenceShardedScan:
         lam_next = self.ones if r < R - 1 else None
         self.be.segment_scan_backward(lam, hprev, h, dh, lam_next, dlam, dx, self.dh0_loc, self.seg_prod_b,
                                       self.agg, T, W)
-        self._all_gather(self.agg, self.aggs)
+        if self.mb is not None:
+            st = self.be._st()
+            self.mb.epoch[1] += 1
+            if r > 0:
+                self.mb.publish(self.agg, 1, 0, r, st)
+            if r < R - 1:
+                self.mb.compose(1, self.agg, R - 1, r, -1, None, self.y_in, st)
+        else:
+            self._all_gather(self.agg, self.aggs)
+            if r < R - 1:
+                self.be.compose(self.aggs, R - 1, r, -1, None, self.y_in, W)
         if r < R - 1:
-            self.be.compose(self.aggs, R - 1, r, -1, None, self.y_in, W)
             self.be.fixup_backward(lam, hprev, h, lam_next, self.seg_prod_b, self.y_in, dlam, dx, T, W,
                                    self.rows_b)
         else:
             self.y_in.zero_()
         if r == 0 and dh0 is not None:
+            # own aggregate only: the local fold of the all-gather path
+            self.aggs[0].copy_(self.agg)
             self.be.compose(self.aggs, 0, 1, 1, self.y_in, dh0.view(-1), W)
         return dlam, dx, dh0
+
+    def close(self):
+        if self.mb is not None:
+            self.mb.close()
+            self.mb = None
 
     def _halo(self, h, h0):
         """True h row before this segment: last row of the previous rank's h."""

@@ -1,7 +1,9 @@
 """Sequence sharding through the CUDA kernels with REAL ranks: 2 or 3
-processes share the one GPU of the test box and exchange carries over gloo
-(host-staged all-gather), running paper_1709_04057_b200.sharded exactly as
-bench.py does with NCCL on a multi-GPU box.  Checked against the oracle."""
+processes share the one GPU of the test box and exchange carries either over
+peer memory (CUDA-IPC mailboxes + release/acquire flags, csrc/p2p.cu -- the
+default on one node; here the "peers" are processes on the same device) or
+over gloo (host-staged all-gather), running paper_1709_04057_b200.sharded
+exactly as bench.py does on a multi-GPU box.  Checked against the oracle."""
 import os
 import socket
 
@@ -20,7 +22,7 @@ def _port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, T, W, lo, hi, seed, q):
+def _worker(rank, world, port, T, W, lo, hi, seed, q, exchange="auto", reps=1):
     import sys
     import torch.distributed as dist
     sys.path.insert(0, ROOT)
@@ -38,18 +40,22 @@ def _worker(rank, world, port, T, W, lo, hi, seed, q):
         cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
         L, X, DH, H0 = cu(lam[s:e]), cu(x[s:e]), cu(dh[s:e]), cu(h0)
         H, DL, DX, DH0 = torch.empty_like(L), torch.empty_like(L), torch.empty_like(L), torch.zeros_like(H0)
-        run = SequenceShardedScan(T, W, stream=torch.cuda.current_stream())
-        run.forward(L, X, H0, H)
-        run.backward(L, H0, H, DH, DL, DX, DH0)
+        run = SequenceShardedScan(T, W, stream=torch.cuda.current_stream(), exchange=exchange)
+        assert run.exchange == ("collective" if exchange == "collective" else "p2p")
+        for _ in range(reps):  # repeated steps reuse the mailboxes (epochs, acks)
+            run.forward(L, X, H0, H)
+            run.backward(L, H0, H, DH, DL, DX, DH0)
         torch.cuda.synchronize()
+        run.close()
         q.put((rank, s, e, H.cpu().numpy(), DL.cpu().numpy(), DX.cpu().numpy(), DH0.cpu().numpy()))
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("exchange,reps", [("p2p", 3), ("collective", 1)])
 @pytest.mark.parametrize("world,T,W,lo,hi", [(2, 40000, 128, 0.05, 0.95), (3, 30001, 64, 0.99, 1.0),
                                              (2, 5000, 12, -1.0, 1.0)])
-def test_sequence_sharded_ranks_on_gpu(oracle, world, T, W, lo, hi):
+def test_sequence_sharded_ranks_on_gpu(oracle, world, T, W, lo, hi, exchange, reps):
     import torch.multiprocessing as mp
     from oracle.oracle import max_rel_error
     if not torch.cuda.is_available():
@@ -58,7 +64,8 @@ def test_sequence_sharded_ranks_on_gpu(oracle, world, T, W, lo, hi):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, T, W, lo, hi, seed, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, T, W, lo, hi, seed, q, exchange, reps))
+             for r in range(world)]
     for p in procs:
         p.start()
     outs = [q.get(timeout=300) for _ in range(world)]
@@ -79,3 +86,28 @@ def test_sequence_sharded_ranks_on_gpu(oracle, world, T, W, lo, hi):
         assert max_rel_error(DX, g[1][s:e]) <= 1e-5, rank
         if rank == 0:
             assert max_rel_error(DH0, g[2]) <= 1e-5
+
+
+@pytest.mark.parametrize("workload", ["c4", "c2"])
+def test_bench_two_ranks_sharing_the_gpu(workload):
+    """bench.py at --gpus 2 under torchrun (ranks share the one GPU: gloo for
+    the host-side plumbing, CUDA IPC for the C4 carry mailboxes): one JSON line
+    from rank 0 with the whole-job value."""
+    import json
+    import subprocess
+    import sys
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, LINREC_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--workload", workload, "--no-e2e", "--no-cpu"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["scaling"] == ("strong" if workload == "c4" else "weak")
+    if workload == "c4":
+        assert "peer-memory" in d["config"]["parallelism"]
