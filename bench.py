@@ -538,6 +538,14 @@ def run_layer(args):
 
         for _ in range(args.warmup):
             step()
+        # correctness guard (untimed; bench.hpp:375-384 analogue): the same
+        # layer forward with the per-channel serial scans vs the chained ones
+        h_par = L.gilr_lstm_forward(p, x, z, z, precision=prec, cache=L.GilrLstmCache())
+        h_ser = L.gilr_lstm_forward(p, x, z, z, mode="serial", precision=prec, cache=L.GilrLstmCache())
+        guard = ((h_par - h_ser).abs().max() / h_ser.abs().max().clamp_min(1.0)).item()
+        del h_par, h_ser
+        if guard > 2e-4:
+            raise SystemExit(f"bench guard: serial/parallel layer disagreement {guard:.3e}")
     stream.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     L.profile_begin()
@@ -590,6 +598,7 @@ def run_layer(args):
             "workload": wl["desc"], "T": T, "B": b, "m": m, "n": n, "elements_per_step": E,
             "events_per_step": T * b, "precision": prec,
             "step": "zero grads + gilr_lstm_forward + gilr_lstm_backward (one layer)",
+            "guard_serial_vs_parallel": guard,
             "l2": "no flush: activations are %.0f MiB per [T,b,n] tensor >> 126 MB L2" % (E * 4 / 2**20),
             "timing": "CUDA events on the launching stream; per-stage events via linrec_profile_begin/end",
         },

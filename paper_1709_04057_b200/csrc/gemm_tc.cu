@@ -90,7 +90,7 @@ cudaError_t launch_cfg(const GemmOperands& op, const GemmEpilogue& ep, linrec_de
   int64_t b_rows = NB == 1 ? op.units : (NB - 1) * op.b_bstride + op.units;
   if (op.ntaps > 1 && !B_MN) b_rows += (op.ntaps - 1) * op.b_tap;
   const int64_t b_k1 = op.ntaps > 1 && B_MN ? (op.ntaps - 1) * op.b_tap + op.K1 : op.K1;
-  CUtensorMap a1, b1, a2, b2;
+  CUtensorMap a1, b1, a2, b2, b1l, b2l;
   linrec_dev::tc::OutMaps om;
   cudaError_t e;
   if ((e = operand_map(&a1, op.a1, A_MN, op.M, op.K1, op.lda1, BM)) != cudaSuccess) return e;
@@ -101,6 +101,18 @@ cudaError_t launch_cfg(const GemmOperands& op, const GemmEpilogue& ep, linrec_de
   } else {
     a2 = a1;
     b2 = b1;
+  }
+  p.b_lo = SPLIT3 && op.b1_lo != nullptr && (op.a2 == nullptr || op.b2_lo != nullptr) ? 1 : 0;
+  if (p.b_lo) {
+    if ((e = operand_map(&b1l, op.b1_lo, B_MN, b_rows, b_k1, op.ldb1, BROWS)) != cudaSuccess) return e;
+    if (op.a2 != nullptr) {
+      if ((e = operand_map(&b2l, op.b2_lo, B_MN, b_rows, op.K2, op.ldb2, BROWS)) != cudaSuccess) return e;
+    } else {
+      b2l = b1l;
+    }
+  } else {
+    b1l = b1;
+    b2l = b2;
   }
   if (EPI == linrec_dev::tc::kEpiPlain) {
     if (partial) e = out_map(&om.m[0], partial, op.units, Mp * p.nz, ldp);
@@ -120,7 +132,7 @@ cudaError_t launch_cfg(const GemmOperands& op, const GemmEpilogue& ep, linrec_de
   const int64_t ntiles = (int64_t)p.ntm * p.ntn * p.nz;
   const int64_t clusters = sm_count() / 2;
   const int grid = 2 * (int)(ntiles < clusters ? ntiles : clusters);
-  kern<<<grid, linrec_dev::tc::kThreads, Cfg::SMEM, st>>>(a1, b1, a2, b2, om, p);
+  kern<<<grid, linrec_dev::tc::kThreads, Cfg::SMEM, st>>>(a1, b1, a2, b2, b1l, b2l, om, p);
   return cudaGetLastError();
 }
 
@@ -165,6 +177,17 @@ int gemm_splits_for(int64_t M, int64_t N, int64_t K) {
     }
   }
   return best;
+}
+
+__global__ void k_tf32_lo(const float* __restrict__ src, float* __restrict__ dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i] - linrec_dev::tc::tf32_hi(src[i]);
+}
+
+cudaError_t tf32_lo(const float* src, float* dst, int64_t count, cudaStream_t st) {
+  const int64_t blocks = (count + 255) / 256;
+  k_tf32_lo<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(src, dst, count);
+  return cudaGetLastError();
 }
 
 int64_t gemm_partial_floats(int64_t M, int64_t N, int splits) {

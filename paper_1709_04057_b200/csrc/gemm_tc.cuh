@@ -241,6 +241,7 @@ struct GemmParams {
   // belongs to tap s = kb / tap_kb and reads A rows shifted by s*a_tap and B
   // rows (K-major) / K (MN-major) offset by s*b_tap.  tap_kb = 0: off.
   int tap_kb, a_tap, b_tap;
+  int b_lo;          // SPLIT3: B's lo part comes precomputed (tb1lo/tb2lo); split only A
   int mode;          // plain: 0 store, 1 accumulate (TMA reduce-add), 2 split-K partial (rows z*Mp + row)
   int Mp;            // partial rows per split (M rounded up to the 256-row tile)
   int act;           // candidate activation (common.hpp:49-71): 0 tanh, 1 identity, 2 relu
@@ -337,6 +338,7 @@ template <bool A_MN, bool B_MN, int NB, int BNT, int STAGES, bool SPLIT3, int EP
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensorMap tb1,
        const __grid_constant__ CUtensorMap ta2, const __grid_constant__ CUtensorMap tb2,
+       const __grid_constant__ CUtensorMap tb1lo, const __grid_constant__ CUtensorMap tb2lo,
        const __grid_constant__ OutMaps om, const GemmParams p) {
   using Cfg = GemmCfg<A_MN, B_MN, NB, BNT, STAGES, SPLIT3>;
   using GA = typename Cfg::GA;
@@ -394,6 +396,7 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
           const bool second = kb >= p.kb1;
           const CUtensorMap* ta = second ? &ta2 : &ta1;
           const CUtensorMap* tb = second ? &tb2 : &tb1;
+          const CUtensorMap* tbl = second ? &tb2lo : &tb1lo;
           int kk = second ? kb - p.kb1 : kb, a_off = 0, b_off = 0;
           if (p.tap_kb) {
             const int tap = kb / p.tap_kb;
@@ -408,7 +411,7 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
           // else both CTAs' loads complete on the leader's barrier, which
           // the leader armed with the bytes of both halves.
           const uint32_t bar = full_leader + 8u * (uint32_t)s;
-          if (SPLIT3) mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+          if (SPLIT3) mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES + (p.b_lo ? GB::BYTES : 0));
           else if (leader) mbar_arrive_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
 #define LINREC_LOAD(dst, map, c0, c1)                          \
   do {                                                         \
@@ -421,16 +424,21 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
           } else {
             LINREC_LOAD(sa, ta, k0, m0 + a_off);
           }
-          if (B_MN) {
+          // B hi into the stage; with b_lo also B lo into the stage's lo tile
+          for (int pass = 0; pass < (SPLIT3 && p.b_lo ? 2 : 1); ++pass) {
+            unsigned char* dstb = pass == 0 ? sb : smem + Cfg::LO_OFF + s * Cfg::STAGE_BYTES + GA::BYTES;
+            const CUtensorMap* mb = pass == 0 ? tb : tbl;
+            if (B_MN) {
 #pragma unroll
-            for (int j = 0; j < GB::NBOX; ++j)
-              LINREC_LOAD(sb + j * GB::BOX_BYTES, tb, u0 + (int)rank * (BNT / 2) + 32 * j, k0 + b_off);
-          } else {
-            // tile row rho -> gate block rho / UNITS, unit u0 + rho % UNITS
+              for (int j = 0; j < GB::NBOX; ++j)
+                LINREC_LOAD(dstb + j * GB::BOX_BYTES, mb, u0 + (int)rank * (BNT / 2) + 32 * j, k0 + b_off);
+            } else {
+              // tile row rho -> gate block rho / UNITS, unit u0 + rho % UNITS
 #pragma unroll
-            for (int j = 0; j < Cfg::NSB; ++j) {
-              const int rho = (int)rank * (BNT / 2) + j * Cfg::SB;
-              LINREC_LOAD(sb + j * Cfg::SB * 128, tb, k0, (rho / UNITS) * p.b_bstride + u0 + rho % UNITS + b_off);
+              for (int j = 0; j < Cfg::NSB; ++j) {
+                const int rho = (int)rank * (BNT / 2) + j * Cfg::SB;
+                LINREC_LOAD(dstb + j * Cfg::SB * 128, mb, k0, (rho / UNITS) * p.b_bstride + u0 + rho % UNITS + b_off);
+              }
             }
           }
 #undef LINREC_LOAD
@@ -494,7 +502,8 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
           const float4* src = reinterpret_cast<const float4*>(smem + s * Cfg::STAGE_BYTES);
           float4* dst = reinterpret_cast<float4*>(smem + Cfg::LO_OFF + s * Cfg::STAGE_BYTES);
 #pragma unroll 4
-          for (int e = st; e < Cfg::STAGE_BYTES / 16; e += kSplitWarps * 32) {
+          const int nsplit = (p.b_lo ? GA::BYTES : Cfg::STAGE_BYTES) / 16;  // A only when B's lo is loaded
+          for (int e = st; e < nsplit; e += kSplitWarps * 32) {
             const float4 v = src[e];
             dst[e] = make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z), v.w - tf32_hi(v.w));
           }

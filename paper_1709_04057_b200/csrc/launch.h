@@ -133,6 +133,10 @@ struct GemmOperands {
   // (MN-major) offset by s*b_tap -- the QRNN causal convolution as one GEMM
   int ntaps = 1;
   int64_t a_tap = 0, b_tap = 0;
+  // optional precomputed lo parts (v - tf32(v)) of b1 / b2, same layout and
+  // pitch: with 3xTF32 the kernel then splits only A in shared memory
+  const float* b1_lo = nullptr;
+  const float* b2_lo = nullptr;
   bool a_mn = false, b_mn = false;
 };
 struct GemmEpilogue {
@@ -150,6 +154,8 @@ struct GemmEpilogue {
 // epi: 0 plain (C / accumulate / split-K), 1 GILR gates (nb 2), 2 LSTM gates (nb 4),
 // 3 QRNN gates (nb 3)
 cudaError_t gemm_tf32(const GemmOperands& op, int epi, const GemmEpilogue& ep, cudaStream_t st);
+// dst[i] = src[i] - tf32(src[i]) (the 3xTF32 lo part), count floats
+cudaError_t tf32_lo(const float* src, float* dst, int64_t count, cudaStream_t st);
 int gemm_splits_for(int64_t M, int64_t N, int64_t K);
 // split-K partial buffer (floats) gemm_tf32 needs for `splits` splits (0 for 1)
 int64_t gemm_partial_floats(int64_t M, int64_t N, int splits);

@@ -254,13 +254,14 @@ int64_t wsplit_floats(int64_t R, int64_t M, int64_t N) {
 
 // ---- scratch layouts (one function drives sizing and carving) -------------
 struct GilrScratch {
-  float *imp, *uv, *dl, *G, *dpre, *part, *split, *dh0;
+  float *imp, *uv, *uv_lo, *dl, *G, *dpre, *part, *split, *dh0;
 };
 int64_t gilr_scratch(float* base, int64_t T, int64_t b, int64_t m, int64_t n, GilrScratch* s) {
   const int64_t R = T * b;
   Carve c{base};
   GilrScratch t;
   t.uv = c.take(2 * n * m);
+  t.uv_lo = c.take(2 * n * m);
   t.dh0 = c.take(b * n);
   const RowPlan rp = row_plan(R, n);
   t.part = c.take(rp.nbx * 2 * n);
@@ -278,7 +279,7 @@ int64_t gilr_scratch(float* base, int64_t T, int64_t b, int64_t m, int64_t n, Gi
 }
 
 struct LstmScratch {
-  float *uv, *part, *split, *tmp0, *tmp1;
+  float *uv, *uv_lo, *v_lo, *u_lo, *part, *split, *tmp0, *tmp1;
   float *iz;                                  // forward (also the surrogate impulses)
   float *dc, *df, *diz, *dpre, *dhp, *G;      // backward; dpre_s aliases df|diz, dls aliases dc
 };
@@ -287,6 +288,9 @@ int64_t lstm_scratch(float* base, int64_t T, int64_t b, int64_t m, int64_t n, Ls
   Carve c{base};
   LstmScratch t;
   t.uv = c.take(2 * n * m);
+  t.uv_lo = c.take(2 * n * m);
+  t.v_lo = c.take(4 * n * m);
+  t.u_lo = c.take(4 * n * n);
   t.tmp0 = c.take(b * n);
   t.tmp1 = c.take(b * n);
   const RowPlan rp = row_plan(R, n);
@@ -311,7 +315,7 @@ int64_t lstm_scratch(float* base, int64_t T, int64_t b, int64_t m, int64_t n, Ls
 }
 
 struct QrnnScratch {
-  float *part, *split, *tmp0;
+  float *part, *split, *tmp0, *w_lo;
   float *imp;                // forward
   float *dc, *df, *dimp, *dpre;  // backward
 };
@@ -320,10 +324,10 @@ int64_t qrnn_scratch(float* base, int64_t T, int64_t b, int64_t m, int64_t n, in
   Carve c{base};
   QrnnScratch t;
   t.tmp0 = c.take(b * n);
+  t.w_lo = c.take(k * 3 * n * m);
   const RowPlan rp = row_plan(R, n);
   t.part = c.take(rp.nbx * 3 * n);
   t.split = c.take(wsplit_floats(R, 3 * n, m));
-  (void)k;
   const int64_t common = c.off;
   Carve f{base, common};
   t.imp = f.take(R * n);
@@ -409,11 +413,12 @@ cudaError_t wgrad(const float* dpre, int64_t lda, int64_t M, const float* act, i
 
 // gilr_forward core: g, i (cache), imp; then h = scan(g, imp, h0)
 int gilr_forward_core(const linrec_gilr_params_f32* p, const float* x, const float* h0, float* h, float* g, float* ci,
-                      float* imp, float* uv, int64_t T, int64_t b, int64_t m, int64_t n, int mode, bool split3,
-                      cudaStream_t st) {
+                      float* imp, float* uv, float* uv_lo, int64_t T, int64_t b, int64_t m, int64_t n, int mode,
+                      bool split3, cudaStream_t st) {
   const int64_t R = T * b;
   LTRY(cudaMemcpyAsync(uv, p->U, sizeof(float) * n * m, cudaMemcpyDeviceToDevice, st));
   LTRY(cudaMemcpyAsync(uv + n * m, p->V, sizeof(float) * n * m, cudaMemcpyDeviceToDevice, st));
+  if (split3) LTRY(linrec_impl::tf32_lo(uv, uv_lo, 2 * n * m, st));
   mark(st, "prep");
   GemmOperands op;
   op.a1 = x;
@@ -425,6 +430,7 @@ int gilr_forward_core(const linrec_gilr_params_f32* p, const float* x, const flo
   op.units = n;
   op.nb = 2;
   op.b_bstride = n;
+  if (split3) op.b1_lo = uv_lo;
   GemmEpilogue ep;
   ep.act = p->act;
   ep.bias[0] = p->b_g;
@@ -446,8 +452,8 @@ int gilr_forward_core(const linrec_gilr_params_f32* p, const float* x, const flo
 int gilr_backward_core(const linrec_gilr_params_f32* p, const float* x, const float* h0, const float* g,
                        const float* ci, const float* h, const float* dh, linrec_gilr_grads_f32* gr, float* dx,
                        float* dh0, float* dl, float* G, float* dpre_s, float* part, float* split, float* uv,
-                       float* dh0_tmp, int64_t T, int64_t b, int64_t m, int64_t n, int mode, bool split3,
-                       cudaStream_t st) {
+                       float* uv_lo, float* dh0_tmp, int64_t T, int64_t b, int64_t m, int64_t n, int mode,
+                       bool split3, cudaStream_t st) {
   const int64_t R = T * b;
   mark(st, "prep");
   LRC(linrec_scan_backward_f32(g, h0, h, dh, dl, G, dh0 ? dh0 : dh0_tmp, T, b * n, mode, nullptr, st));
@@ -472,6 +478,7 @@ int gilr_backward_core(const linrec_gilr_params_f32* p, const float* x, const fl
   if (dx) {
     LTRY(cudaMemcpyAsync(uv, p->U, sizeof(float) * n * m, cudaMemcpyDeviceToDevice, st));
     LTRY(cudaMemcpyAsync(uv + n * m, p->V, sizeof(float) * n * m, cudaMemcpyDeviceToDevice, st));
+    if (split3) LTRY(linrec_impl::tf32_lo(uv, uv_lo, 2 * n * m, st));
     mark(st, "prep");
     GemmOperands op;  // dx = [dg | di] * [U; V]
     op.a1 = dpre_s;
@@ -482,6 +489,7 @@ int gilr_backward_core(const linrec_gilr_params_f32* p, const float* x, const fl
     op.M = R;
     op.units = m;
     op.b_mn = true;
+    if (split3) op.b1_lo = uv_lo;
     GemmEpilogue ep;
     ep.C = dx;
     ep.ldc = m;
@@ -517,6 +525,7 @@ int linrec_qrnn_forward_f32(const float* W, const float* bias, const float* x, c
   float* go = gf + N;
   float* gz = go + N;
   mark(st, "begin");
+  if (precision == LINREC_PREC_FP32) LTRY(linrec_impl::tf32_lo(W, s.w_lo, k * 3 * n * m, st));
   // pre[r] = bias + sum_s x[r - s*b] W_s^T: one GEMM whose K runs over the k
   // taps, tap s reading x shifted s*b rows down (zero-filled above row 0)
   GemmOperands op;
@@ -532,6 +541,7 @@ int linrec_qrnn_forward_f32(const float* W, const float* bias, const float* x, c
   op.units = n;
   op.nb = 3;
   op.b_bstride = n;
+  if (precision == LINREC_PREC_FP32) op.b1_lo = s.w_lo;
   GemmEpilogue ep;
   for (int q = 0; q < 3; ++q) ep.bias[q] = bias + q * n;
   ep.out[0] = gf;
@@ -602,6 +612,10 @@ int linrec_qrnn_backward_f32(const float* W, const float* x, const float* c0, co
     op.M = R;
     op.units = m;
     op.b_mn = true;
+    if (split3) {
+      LTRY(linrec_impl::tf32_lo(W, s.w_lo, k * 3 * n * m, st));
+      op.b1_lo = s.w_lo;
+    }
     GemmEpilogue ep;
     ep.C = dx;
     ep.ldc = m;
@@ -679,8 +693,8 @@ int linrec_gilr_forward_f32(const linrec_gilr_params_f32* p, const float* x, con
   LRC(check_scratch(scratch, scratch_bytes, gilr_scratch(nullptr, T, b, m, n, nullptr)));
   gilr_scratch(static_cast<float*>(scratch), T, b, m, n, &s);
   mark(static_cast<cudaStream_t>(stream), "begin");
-  return gilr_forward_core(p, x, h0, h, g, i, s.imp, s.uv, T, b, m, n, mode, precision == LINREC_PREC_FP32,
-                           static_cast<cudaStream_t>(stream));
+  return gilr_forward_core(p, x, h0, h, g, i, s.imp, s.uv, s.uv_lo, T, b, m, n, mode,
+                           precision == LINREC_PREC_FP32, static_cast<cudaStream_t>(stream));
 }
 
 int linrec_gilr_backward_f32(const linrec_gilr_params_f32* p, const float* x, const float* h0, const float* g,
@@ -694,8 +708,9 @@ int linrec_gilr_backward_f32(const linrec_gilr_params_f32* p, const float* x, co
   LRC(check_scratch(scratch, scratch_bytes, gilr_scratch(nullptr, T, b, m, n, nullptr)));
   gilr_scratch(static_cast<float*>(scratch), T, b, m, n, &s);
   mark(static_cast<cudaStream_t>(stream), "begin");
-  return gilr_backward_core(p, x, h0, g, i, h, dh, grads, dx, dh0, s.dl, s.G, s.dpre, s.part, s.split, s.uv, s.dh0,
-                            T, b, m, n, mode, precision == LINREC_PREC_FP32, static_cast<cudaStream_t>(stream));
+  return gilr_backward_core(p, x, h0, g, i, h, dh, grads, dx, dh0, s.dl, s.G, s.dpre, s.part, s.split, s.uv,
+                            s.uv_lo, s.dh0, T, b, m, n, mode, precision == LINREC_PREC_FP32,
+                            static_cast<cudaStream_t>(stream));
 }
 
 int linrec_gilr_lstm_forward_f32(const linrec_gilr_lstm_params_f32* p, const float* x, const float* htil0,
@@ -716,8 +731,12 @@ int linrec_gilr_lstm_forward_f32(const linrec_gilr_lstm_params_f32* p, const flo
   // 1-2. surrogate; its output lands one row block after htil0
   if (htil0) LTRY(cudaMemcpyAsync(cache->htil, htil0, sizeof(float) * BN, cudaMemcpyDeviceToDevice, st));
   else LTRY(cudaMemsetAsync(cache->htil, 0, sizeof(float) * BN, st));
-  LRC(gilr_forward_core(&p->surrogate, x, htil0, cache->htil + BN, cache->sg, cache->si, s.iz, s.uv, T, b, m, n, mode,
-                        split3, st));
+  LRC(gilr_forward_core(&p->surrogate, x, htil0, cache->htil + BN, cache->sg, cache->si, s.iz, s.uv, s.uv_lo, T, b,
+                        m, n, mode, split3, st));
+  if (split3) {
+    LTRY(linrec_impl::tf32_lo(p->V, s.v_lo, 4 * n * m, st));
+    LTRY(linrec_impl::tf32_lo(p->U, s.u_lo, 4 * n * n, st));
+  }
   // 3. gates = act([x | htil_prev] [V | U]^T + bias)
   float* gf = cache->gates;
   float* gi = gf + N;
@@ -738,6 +757,10 @@ int linrec_gilr_lstm_forward_f32(const linrec_gilr_lstm_params_f32* p, const flo
   op.units = n;
   op.nb = 4;
   op.b_bstride = n;
+  if (split3) {
+    op.b1_lo = s.v_lo;
+    op.b2_lo = s.u_lo;
+  }
   GemmEpilogue ep;
   for (int q = 0; q < 4; ++q) ep.bias[q] = p->bias + q * n;
   ep.out[0] = gf;
@@ -777,6 +800,10 @@ int linrec_gilr_lstm_backward_f32(const linrec_gilr_lstm_params_f32* p, const fl
   const float* go = gi + N;
   const float* gz = go + N;
   mark(st, "begin");
+  if (split3) {
+    LTRY(linrec_impl::tf32_lo(p->V, s.v_lo, 4 * n * m, st));
+    LTRY(linrec_impl::tf32_lo(p->U, s.u_lo, 4 * n * n, st));
+  }
   // h = o * c  ->  dc = dh * o (d_o is formed inside k_lstm_dpre)
   k_mul<<<grid_for(N / 4, 256), 256, 0, st>>>(dh, go, s.dc, N / 4);
   LTRY(cudaGetLastError());
@@ -808,6 +835,7 @@ int linrec_gilr_lstm_backward_f32(const linrec_gilr_lstm_params_f32* p, const fl
     op.M = R;
     op.units = n;
     op.b_mn = true;
+    if (split3) op.b1_lo = s.u_lo;
     GemmEpilogue ep;
     ep.C = s.dhp;
     ep.ldc = n;
@@ -818,11 +846,12 @@ int linrec_gilr_lstm_backward_f32(const linrec_gilr_lstm_params_f32* p, const fl
   // surrogate backward on d_htil[t] = dhp[t+1] (pointer shift); dpre_s in df|diz
   float* dpre_s = s.df;
   LRC(gilr_backward_core(&p->surrogate, x, htil0, cache->sg, cache->si, cache->htil + BN, s.dhp + BN,
-                         &grads->surrogate, nullptr, nullptr, s.dc, s.G, dpre_s, s.part, s.split, s.uv, s.tmp1, T, b,
-                         m, n, mode, split3, st));
+                         &grads->surrogate, nullptr, nullptr, s.dc, s.G, dpre_s, s.part, s.split, s.uv, s.uv_lo, s.tmp1,
+                         T, b, m, n, mode, split3, st));
   // dx = dpre V + [dg | di] [U_s; V_s]   (one K-concatenated GEMM)
   LTRY(cudaMemcpyAsync(s.uv, p->surrogate.U, sizeof(float) * n * m, cudaMemcpyDeviceToDevice, st));
   LTRY(cudaMemcpyAsync(s.uv + n * m, p->surrogate.V, sizeof(float) * n * m, cudaMemcpyDeviceToDevice, st));
+  if (split3) LTRY(linrec_impl::tf32_lo(s.uv, s.uv_lo, 2 * n * m, st));
   mark(st, "prep");
   {
     GemmOperands op;
@@ -839,6 +868,10 @@ int linrec_gilr_lstm_backward_f32(const linrec_gilr_lstm_params_f32* p, const fl
     op.M = R;
     op.units = m;
     op.b_mn = true;
+    if (split3) {
+      op.b1_lo = s.v_lo;
+      op.b2_lo = s.uv_lo;
+    }
     GemmEpilogue ep;
     ep.C = dx;
     ep.ldc = m;
