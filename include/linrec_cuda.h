@@ -366,14 +366,17 @@ int linrec_qrnn_backward_f32(const float* W, const float* x, const float* c0, co
  * `counter` = draws taken so far, the batch takes b*T), one-hot x [T][b][p]
  * and labels [b] on the device; the readout + softmax cross-entropy of
  * model_forward / softmax_loss (:160-222) with loss_acc = (mean loss,
- * accuracy) as two device doubles; its backward (:229-240, dW_out / db_out
+ * accuracy) as two device doubles -- means over b_total rows (b_total > b
+ * when this rank holds b of a data-parallel global batch: the ranks' loss,
+ * accuracy and gradients then SUM to the global ones); its backward (:229-240, dW_out / db_out
  * accumulate, d_hlast = the gradient of the last step); and
  * clip_global_norm + Adam (:248-288) fused over one flat parameter buffer with
  * fp64 moments (norm_out: device double, pre-clip norm; may be NULL). */
 int linrec_synthetic_batch_f32(uint64_t seed, uint64_t counter, int64_t T, int64_t b, int64_t p, float* x,
                                int32_t* labels, void* stream);
 int linrec_readout_loss_f32(const float* h_last, const float* W_out, const float* b_out, const int32_t* labels,
-                            float* logits, float* d_logits, double* loss_acc, int64_t b, int64_t n, void* stream);
+                            float* logits, float* d_logits, double* loss_acc, int64_t b, int64_t n, int64_t b_total,
+                            void* stream);
 int linrec_readout_backward_f32(const float* d_logits, const float* h_last, const float* W_out, float* dW_out,
                                 float* db_out, float* d_hlast, int64_t b, int64_t n, void* stream);
 size_t linrec_adam_scratch_bytes(void);

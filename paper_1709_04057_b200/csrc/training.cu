@@ -49,7 +49,8 @@ __global__ void k_synthetic_batch(uint64_t seed, uint64_t counter, int64_t T, in
 // accuracy) summed in row order by one block (deterministic).
 __global__ void k_readout_loss(const float* __restrict__ h, const float* __restrict__ W, const float* __restrict__ bo,
                                const int32_t* __restrict__ labels, float* __restrict__ logits,
-                               float* __restrict__ dlogits, double* __restrict__ loss_acc, int64_t b, int64_t n) {
+                               float* __restrict__ dlogits, double* __restrict__ loss_acc, int64_t b, int64_t n,
+                               int64_t b_total) {
   __shared__ double s_loss[256], s_ok[256];
   double loss = 0.0, ok = 0.0;
   for (int64_t r = threadIdx.x; r < b; r += blockDim.x) {
@@ -67,8 +68,8 @@ __global__ void k_readout_loss(const float* __restrict__ h, const float* __restr
     const int y = labels[r];
     loss -= log((y == 1 ? ec : ea) / zs);
     if ((c > a ? 1 : 0) == y) ok += 1.0;
-    dlogits[r * 2] = (float)((ea / zs - (y == 0 ? 1.0 : 0.0)) / (double)b);
-    dlogits[r * 2 + 1] = (float)((ec / zs - (y == 1 ? 1.0 : 0.0)) / (double)b);
+    dlogits[r * 2] = (float)((ea / zs - (y == 0 ? 1.0 : 0.0)) / (double)b_total);
+    dlogits[r * 2 + 1] = (float)((ec / zs - (y == 1 ? 1.0 : 0.0)) / (double)b_total);
   }
   s_loss[threadIdx.x] = loss;
   s_ok[threadIdx.x] = ok;
@@ -79,8 +80,8 @@ __global__ void k_readout_loss(const float* __restrict__ h, const float* __restr
       L += s_loss[i];
       A += s_ok[i];
     }
-    loss_acc[0] = L / (double)b;
-    loss_acc[1] = A / (double)b;
+    loss_acc[0] = L / (double)b_total;
+    loss_acc[1] = A / (double)b_total;
   }
 }
 
@@ -186,12 +187,15 @@ int linrec_synthetic_batch_f32(uint64_t seed, uint64_t counter, int64_t T, int64
 }
 
 int linrec_readout_loss_f32(const float* h_last, const float* W_out, const float* b_out, const int32_t* labels,
-                            float* logits, float* d_logits, double* loss_acc, int64_t b, int64_t n, void* stream) {
+                            float* logits, float* d_logits, double* loss_acc, int64_t b, int64_t n, int64_t b_total,
+                            void* stream) {
   if (b < 1 || n < 1) return terr(LINREC_ERR_SHAPE, "softmax_loss: b, n must be >= 1");
+  if (b_total < b) return terr(LINREC_ERR_VALUE, "softmax_loss: b_total must cover the local batch");
   if (!h_last || !W_out || !b_out || !labels || !logits || !d_logits || !loss_acc)
     return terr(LINREC_ERR_VALUE, "softmax_loss: NULL buffer");
   linrec_dev::train::k_readout_loss<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(h_last, W_out, b_out, labels,
-                                                                                      logits, d_logits, loss_acc, b, n);
+                                                                                      logits, d_logits, loss_acc, b, n,
+                                                                                      b_total);
   TTRY(cudaGetLastError());
   return LINREC_OK;
 }

@@ -19,6 +19,13 @@ Everything numeric runs in liblinrec_cuda.so; the parameters, gradients and
 Adam moments each live in ONE flat device buffer (fp32 / fp64) that the layer
 calls address by offset.  Only the "gilr-lstm" arch is built (the serial
 LSTM baseline is out of scope).
+
+Data parallel over a process group (``run_experiment(cfg, group=...)``, one
+rank per GPU): the global batch of cfg.batch rows is split across the ranks,
+each rank drawing ITS rows of the same reference stream (row r uses draws
+r*T+1 ...), the readout scales by the global batch, and one all-reduce of
+the flat gradient buffer (plus the 2-double loss / accuracy) per step makes
+every rank's clip + Adam identical -- the same trajectory as one GPU.
 """
 from __future__ import annotations
 
@@ -178,7 +185,7 @@ def _lib():
     if not getattr(lib, "_train_bound", False):
         vp, i64 = C.c_void_p, C.c_int64
         lib.linrec_synthetic_batch_f32.argtypes = [C.c_uint64, C.c_uint64, i64, i64, i64, vp, vp, vp]
-        lib.linrec_readout_loss_f32.argtypes = [vp] * 7 + [i64, i64, vp]
+        lib.linrec_readout_loss_f32.argtypes = [vp] * 7 + [i64, i64, i64, vp]
         lib.linrec_readout_backward_f32.argtypes = [vp] * 6 + [i64, i64, vp]
         lib.linrec_adam_scratch_bytes.restype = C.c_size_t
         lib.linrec_adam_scratch_bytes.argtypes = []
@@ -198,13 +205,18 @@ class SyntheticBatch:
     labels: torch.Tensor  # [b] int32, device
 
 
-def generate_batch(rng: Rng, T: int, b: int, p: int, device="cuda", out: SyntheticBatch | None = None):
-    """training.hpp:30-43 on the GPU: the same draws from the same stream."""
+def generate_batch(rng: Rng, T: int, b: int, p: int, device="cuda", out: SyntheticBatch | None = None,
+                   rows: tuple | None = None):
+    """training.hpp:30-43 on the GPU: the same draws from the same stream.
+    rows = (r0, r1): only rows [r0, r1) of the b-row batch (data-parallel
+    shard); the stream still advances by the whole batch."""
     dev = torch.device(device)
-    if out is None or tuple(out.inputs.shape) != (T, b, p):
-        out = SyntheticBatch(torch.empty(T, b, p, dtype=torch.float32, device=dev),
-                             torch.empty(b, dtype=torch.int32, device=dev))
-    capi.check(_lib().linrec_synthetic_batch_f32(rng.seed, rng.counter, T, b, p, out.inputs.data_ptr(),
+    r0, r1 = rows if rows is not None else (0, b)
+    bl = r1 - r0
+    if out is None or tuple(out.inputs.shape) != (T, bl, p):
+        out = SyntheticBatch(torch.empty(T, bl, p, dtype=torch.float32, device=dev),
+                             torch.empty(bl, dtype=torch.int32, device=dev))
+    capi.check(_lib().linrec_synthetic_batch_f32(rng.seed, rng.counter + r0 * T, T, bl, p, out.inputs.data_ptr(),
                                                  out.labels.data_ptr(), _stream(dev)))
     if p >= 2 and T >= 1:
         rng.skip(b * T)
@@ -231,9 +243,10 @@ def model_forward(m: Model, x, mode="parallel", cache: ModelCache | None = None)
     return cache
 
 
-def softmax_loss(m: Model, cache: ModelCache, labels):
+def softmax_loss(m: Model, cache: ModelCache, labels, b_total=None, group=None):
     """Readout on the last step + softmax_loss (:182-222) on the GPU; leaves
-    d_logits in the cache.  Returns (loss, accuracy) as Python floats."""
+    d_logits in the cache.  Returns (loss, accuracy) as Python floats (over
+    the global batch when data parallel: b_total rows, summed over `group`)."""
     T, b, n = cache.h2.shape
     dev = cache.h2.device
     if cache.logits is None or cache.logits.shape[0] != b:
@@ -242,7 +255,10 @@ def softmax_loss(m: Model, cache: ModelCache, labels):
         cache.loss_acc = torch.empty(2, dtype=torch.float64, device=dev)
     capi.check(_lib().linrec_readout_loss_f32(cache.h2[T - 1].data_ptr(), m.W_out.data_ptr(), m.b_out.data_ptr(),
                                               labels.data_ptr(), cache.logits.data_ptr(), cache.d_logits.data_ptr(),
-                                              cache.loss_acc.data_ptr(), b, n, _stream(dev)))
+                                              cache.loss_acc.data_ptr(), b, n, b if b_total is None else b_total,
+                                              _stream(dev)))
+    if group is not None:
+        _all_reduce(cache.loss_acc, group)
     la = cache.loss_acc.cpu()
     return float(la[0]), float(la[1])
 
@@ -262,6 +278,18 @@ def model_backward(m: Model, x, cache: ModelCache, mode="parallel"):
                                       mode=mode, precision=prec, want_initial=False)
     L.gilr_lstm_backward(m.layers[0], x, None, None, cache.gl[0], d_h1, m.layer_grads[0], mode=mode,
                          precision=prec, want_initial=False)
+
+
+def _all_reduce(t, group):
+    """Sum over the data-parallel group: NCCL on device buffers; gloo (CPU
+    tests, ranks sharing one GPU) through a host copy."""
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(t, group=group)
+    else:
+        h = t.cpu()
+        dist.all_reduce(h, group=group)
+        t.copy_(h)
 
 
 class Adam:
@@ -288,10 +316,11 @@ class Adam:
 
 
 class Trainer:
-    """Trainer (:291-333)."""
+    """Trainer (:291-333); `group` makes it data parallel (see module doc)."""
 
-    def __init__(self, cfg: TrainConfig, rng: Rng, device="cuda"):
+    def __init__(self, cfg: TrainConfig, rng: Rng, device="cuda", group=None):
         self.cfg = cfg
+        self.group = group
         self.model = build_model(cfg, rng, device)
         self.opt = Adam(self.model, lr=cfg.learning_rate)
         self.clip_norm = cfg.clip_norm
@@ -300,11 +329,13 @@ class Trainer:
     def train_step(self, batch: SyntheticBatch, mode="parallel"):
         m = self.model
         model_forward(m, batch.inputs, mode, self.cache)
-        loss, acc = softmax_loss(m, self.cache, batch.labels)
+        loss, acc = softmax_loss(m, self.cache, batch.labels, self.cfg.batch, self.group)
         if not math.isfinite(loss):
             return loss, acc  # caller handles divergence
         m.grads.flat.zero_()
         model_backward(m, batch.inputs, self.cache, mode)
+        if self.group is not None:
+            _all_reduce(m.grads.flat, self.group)  # the one exchange of the step
         self.opt.clip_and_update(m, self.clip_norm)
         return loss, acc
 
@@ -351,13 +382,27 @@ def run_loop(cfg: TrainConfig, step, clock=None) -> RunReport:
     return report
 
 
-def run_experiment(cfg: TrainConfig, mode="parallel", device="cuda", trainer_out: list | None = None) -> RunReport:
+def run_experiment(cfg: TrainConfig, mode="parallel", device="cuda", trainer_out: list | None = None,
+                   group=None) -> RunReport:
     """run_experiment (:384-436): fresh batches every iteration from
-    root.split(2), parameters from root.split(1)."""
+    root.split(2), parameters from root.split(1).  With a process group the
+    global batch is split across its ranks (data parallel)."""
     cfg.validate()
+    rows = None
+    if group is not None:
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        if world == 1:
+            group = None
+        else:
+            if cfg.batch < world:
+                raise RuntimeError("data parallel: batch must be >= the number of ranks")
+            base, rem = divmod(cfg.batch, world)
+            r0 = rank * base + min(rank, rem)
+            rows = (r0, r0 + base + (1 if rank < rem else 0))
     root = Rng(cfg.seed)
     param_rng, data_rng = root.split(1), root.split(2)
-    trainer = Trainer(cfg, param_rng, device)
+    trainer = Trainer(cfg, param_rng, device, group)
     if trainer_out is not None:
         trainer_out.append(trainer)
     batch = None
@@ -366,7 +411,7 @@ def run_experiment(cfg: TrainConfig, mode="parallel", device="cuda", trainer_out
     if cfg.time_data_gen:
         def step(_):
             nonlocal batch
-            batch = generate_batch(data_rng, cfg.seq_len, cfg.batch, cfg.input_dim, dev, batch)
+            batch = generate_batch(data_rng, cfg.seq_len, cfg.batch, cfg.input_dim, dev, batch, rows)
             return trainer.train_step(batch, mode)
         return run_loop(cfg, step)
 
@@ -374,7 +419,7 @@ def run_experiment(cfg: TrainConfig, mode="parallel", device="cuda", trainer_out
 
     def step_k(_):  # kernel-only accounting: data generation outside the stopwatch
         nonlocal batch
-        batch = generate_batch(data_rng, cfg.seq_len, cfg.batch, cfg.input_dim, dev, batch)
+        batch = generate_batch(data_rng, cfg.seq_len, cfg.batch, cfg.input_dim, dev, batch, rows)
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         r = trainer.train_step(batch, mode)

@@ -113,3 +113,52 @@ def test_long_sequence_step_follows_the_oracle(oracle):
     for a, b in zip(keep[0].model.tensors(), tensors(otr.model)):
         d = np.abs(a.cpu().numpy().astype(np.float64) - b).max() / max(np.abs(b).max(), 1e-30)
         assert d < 1e-4
+
+
+def _dp_worker(rank, world, port, q):
+    import os
+    import sys
+    import torch.distributed as dist
+    from conftest import ROOT
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1709_04057_b200.training import TrainConfig, run_experiment
+        cfg = TrainConfig(seq_len=40, input_dim=8, hidden=8, batch=6, max_iters=4, seed=5, learning_rate=1e-2)
+        keep = []
+        rep = run_experiment(cfg, trainer_out=keep, group=dist.group.WORLD)
+        q.put((rank, [(r.loss, r.accuracy) for r in rep.trace], keep[0].model.params.flat.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_data_parallel_matches_single_gpu():
+    """Two ranks sharing the GPU, each holding half of the global batch,
+    follow the single-GPU trajectory (gradient sums in a different order:
+    1e-5 relative) and stay bit-identical to each other."""
+    import socket
+    import torch.multiprocessing as mp
+    from paper_1709_04057_b200.training import TrainConfig, run_experiment
+    cfg = TrainConfig(seq_len=40, input_dim=8, hidden=8, batch=6, max_iters=4, seed=5, learning_rate=1e-2)
+    keep = []
+    ref = run_experiment(cfg, trainer_out=keep)
+    ref_params = keep[0].model.params.flat.cpu().numpy()
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = sorted(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, t0, p0), (_, t1, p1) = outs
+    assert t0 == t1 and np.array_equal(p0, p1)
+    for (l, a), r in zip(t0, ref.trace):
+        assert l == pytest.approx(r.loss, rel=1e-5) and a == r.accuracy
+    assert np.abs(p0 - ref_params).max() < 1e-5 * max(np.abs(ref_params).max(), 1.0)
