@@ -484,12 +484,12 @@ def layer_stage_work(T, b, m, n):
         "scan_cell": ("byte", 12 * E),
         "h_out": ("byte", 12 * E),
         "dc": ("byte", 12 * E),
-        "scan_bwd_cell": ("byte", 20 * E),
-        "dpre_gates": ("byte", 48 * E),
+        "scan_bwd_cell": ("byte", 16 * E),       # dlam not stored: dpre forms it from c
+        "dpre_gates": ("byte", 44 * E),          # f i o z diz dh c in, 4 dpre planes out
         "wgrad_U": ("flop", 2 * 4 * n * n * R),
         "wgrad_V": ("flop", 2 * 4 * n * m * R),
         "dhtil_prev": ("flop", 2 * R * 4 * n * n),
-        "scan_bwd_surrogate": ("byte", 20 * E),
+        "scan_bwd_surrogate": ("byte", 16 * E),
         "dpre_surrogate": ("byte", 24 * E),
         "wgrad_surrogate_U": ("flop", 2 * n * m * R),
         "wgrad_surrogate_V": ("flop", 2 * n * m * R),

@@ -115,7 +115,10 @@ int linrec_scan_f64(const double* lam, const double* x, const double* h0,
  * (recurrence.hpp:283-377) and the compute of linrec.scan_backward
  * (linrec_py.cpp:118-140).  Inputs lam, h, dh: [T][W]; h0: [W] or NULL.
  * Outputs dlam, dx: [T][W]; dh0: [W].  Does not read x (the reference does
- * not either, recurrence.hpp:273-282).  No reversed copies are made. */
+ * not either, recurrence.hpp:273-282).  No reversed copies are made.
+ * dlam may be NULL (device entry points only): it is then not written --
+ * callers that fold dlam = h_{t-1} * dx into their own pass (the layers)
+ * save its 4 B/element store. */
 int linrec_scan_backward_f32(const float* lam, const float* h0,
                              const float* h, const float* dh, float* dlam,
                              float* dx, float* dh0, int64_t T, int64_t W,

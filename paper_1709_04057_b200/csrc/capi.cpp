@@ -242,7 +242,7 @@ int scan_backward_device(const S* lam, const S* h0, const S* h, const S* dh, con
                          linrec_workspace_t ws, cudaStream_t st) {
   int rc;
   if ((rc = check_dims(T, W)) || (rc = check_mode(mode)) || (rc = check_ptr(lam, "decays")) ||
-      (rc = check_ptr(h, "h")) || (rc = check_ptr(dh, "d_h")) || (rc = check_ptr(dlam, "d_decays")) ||
+      (rc = check_ptr(h, "h")) || (rc = check_ptr(dh, "d_h")) ||
       (rc = check_ptr(dx, "d_impulses")))
     return rc;
   const bool vok = vec_ok<S>(W, {lam, h0, h, dh, lam_next, g_next, dlam, dx, dh0});

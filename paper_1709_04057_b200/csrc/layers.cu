@@ -79,10 +79,13 @@ __device__ __forceinline__ float dact(int a, float v) {  // activation_deriv_fro
 // blocked [R][4n] (f, i, o, z) like the reference's dpre, plus per-block
 // partial column sums for the bias gradient.  Thread = 4 units of one row
 // range; rows [blockIdx.x * rpb, ...).
+// The decay gradient df = c_{t-1} * diz (recurrence.hpp:338-343) is formed
+// here from the cell state instead of being stored by the scan: row r - b of
+// c (c0 for t = 0), read b rows after this thread last touched it.
 __global__ void k_lstm_dpre(const float* __restrict__ gf, const float* __restrict__ gi, const float* __restrict__ go,
-                            const float* __restrict__ gz, const float* __restrict__ df, const float* __restrict__ diz,
+                            const float* __restrict__ gz, const float* __restrict__ c0, const float* __restrict__ diz,
                             const float* __restrict__ dh, const float* __restrict__ c, float* __restrict__ dpre,
-                            float* __restrict__ part, int64_t R, int64_t n, int64_t rpb) {
+                            float* __restrict__ part, int64_t R, int64_t n, int64_t b, int64_t rpb) {
   const int64_t u = 4 * ((int64_t)blockIdx.y * blockDim.x + threadIdx.x);
   if (u >= n) return;
   const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(r0 + rpb, R);
@@ -91,10 +94,12 @@ __global__ void k_lstm_dpre(const float* __restrict__ gf, const float* __restric
   for (int64_t r = r0; r < r1; ++r) {
     const int64_t o = r * n + u;
     const float4 f = ld4(gf + o), i = ld4(gi + o), og = ld4(go + o), z = ld4(gz + o);
-    const float4 d_f = ld4(df + o), d_iz = ld4(diz + o), d_h = ld4(dh + o), cc = ld4(c + o);
+    const float4 d_iz = ld4(diz + o), d_h = ld4(dh + o), cc = ld4(c + o);
+    const float4 cp = r >= b ? *reinterpret_cast<const float4*>(c + o - b * n)
+                             : (c0 != nullptr ? *reinterpret_cast<const float4*>(c0 + r * n + u) : make_float4(0, 0, 0, 0));
     float4 pf, pi, po, pz;
 #define LINREC_DPRE(X)                                                 \
-  pf.X = d_f.X * f.X * (1.f - f.X);                                    \
+  pf.X = (cp.X * d_iz.X) * f.X * (1.f - f.X);                          \
   pi.X = d_iz.X * z.X * i.X * (1.f - i.X);                             \
   po.X = (d_h.X * cc.X) * og.X * (1.f - og.X);                         \
   pz.X = d_iz.X * i.X * (1.f - z.X * z.X);                             \
@@ -116,9 +121,11 @@ __global__ void k_lstm_dpre(const float* __restrict__ gf, const float* __restric
 
 // GILR pre-activation gradients (layers.hpp:112-121): dg, di written blocked
 // [R][2n], plus partial column sums for b_g, b_z.
-__global__ void k_gilr_dpre(const float* __restrict__ g, const float* __restrict__ ci, const float* __restrict__ dl,
-                            const float* __restrict__ G, int act, float* __restrict__ dpre, float* __restrict__ part,
-                            int64_t R, int64_t n, int64_t rpb) {
+// dl = h_{t-1} * G formed here (h0 for t = 0), see k_lstm_dpre.
+__global__ void k_gilr_dpre(const float* __restrict__ g, const float* __restrict__ ci, const float* __restrict__ h,
+                            const float* __restrict__ h0, const float* __restrict__ G, int act,
+                            float* __restrict__ dpre, float* __restrict__ part, int64_t R, int64_t n, int64_t b,
+                            int64_t rpb) {
   const int64_t u = 4 * ((int64_t)blockIdx.y * blockDim.x + threadIdx.x);
   if (u >= n) return;
   const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(r0 + rpb, R);
@@ -126,10 +133,12 @@ __global__ void k_gilr_dpre(const float* __restrict__ g, const float* __restrict
 #pragma unroll 2
   for (int64_t r = r0; r < r1; ++r) {
     const int64_t o = r * n + u;
-    const float4 gv = ld4(g + o), iv = ld4(ci + o), d_l = ld4(dl + o), Gv = ld4(G + o);
+    const float4 gv = ld4(g + o), iv = ld4(ci + o), Gv = ld4(G + o);
+    const float4 hp = r >= b ? *reinterpret_cast<const float4*>(h + o - b * n)
+                             : (h0 != nullptr ? *reinterpret_cast<const float4*>(h0 + r * n + u) : make_float4(0, 0, 0, 0));
     float4 pg, pi;
 #define LINREC_GDPRE(X)                                              \
-  pg.X = (d_l.X - Gv.X * iv.X) * gv.X * (1.f - gv.X);                \
+  pg.X = (hp.X * Gv.X - Gv.X * iv.X) * gv.X * (1.f - gv.X);          \
   pi.X = Gv.X * (1.f - gv.X) * dact(act, iv.X);                      \
   sg.X += pg.X; si.X += pi.X;
     LINREC_GDPRE(x) LINREC_GDPRE(y) LINREC_GDPRE(z) LINREC_GDPRE(w)
@@ -145,10 +154,11 @@ __global__ void k_gilr_dpre(const float* __restrict__ g, const float* __restrict
 
 // QRNN fused pre-activation gradients (layers.hpp:519-531), blocked [R][3n]
 // (f, o, z), plus per-block partial column sums for the bias gradient.
+// df = c_{t-1} * dimp formed here (c0 for t = 0), see k_lstm_dpre.
 __global__ void k_qrnn_dpre(const float* __restrict__ gf, const float* __restrict__ go, const float* __restrict__ gz,
-                            const float* __restrict__ df, const float* __restrict__ dimp,
+                            const float* __restrict__ c0, const float* __restrict__ dimp,
                             const float* __restrict__ dh, const float* __restrict__ c, float* __restrict__ dpre,
-                            float* __restrict__ part, int64_t R, int64_t n, int64_t rpb) {
+                            float* __restrict__ part, int64_t R, int64_t n, int64_t b, int64_t rpb) {
   const int64_t u = 4 * ((int64_t)blockIdx.y * blockDim.x + threadIdx.x);
   if (u >= n) return;
   const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = min(r0 + rpb, R);
@@ -157,10 +167,12 @@ __global__ void k_qrnn_dpre(const float* __restrict__ gf, const float* __restric
   for (int64_t r = r0; r < r1; ++r) {
     const int64_t o = r * n + u;
     const float4 f = ld4(gf + o), og = ld4(go + o), z = ld4(gz + o);
-    const float4 d_f = ld4(df + o), d_i = ld4(dimp + o), d_h = ld4(dh + o), cc = ld4(c + o);
+    const float4 d_i = ld4(dimp + o), d_h = ld4(dh + o), cc = ld4(c + o);
+    const float4 cp = r >= b ? *reinterpret_cast<const float4*>(c + o - b * n)
+                             : (c0 != nullptr ? *reinterpret_cast<const float4*>(c0 + r * n + u) : make_float4(0, 0, 0, 0));
     float4 pf, po, pz;
 #define LINREC_QDPRE(X)                                              \
-  pf.X = (d_f.X - d_i.X * z.X) * f.X * (1.f - f.X);                  \
+  pf.X = (cp.X * d_i.X - d_i.X * z.X) * f.X * (1.f - f.X);           \
   po.X = (d_h.X * cc.X) * og.X * (1.f - og.X);                       \
   pz.X = d_i.X * (1.f - f.X) * (1.f - z.X * z.X);                    \
   sf.X += pf.X; so.X += po.X; sz.X += pz.X;
@@ -456,11 +468,12 @@ int gilr_backward_core(const linrec_gilr_params_f32* p, const float* x, const fl
                        bool split3, cudaStream_t st) {
   const int64_t R = T * b;
   mark(st, "prep");
-  LRC(linrec_scan_backward_f32(g, h0, h, dh, dl, G, dh0 ? dh0 : dh0_tmp, T, b * n, mode, nullptr, st));
+  LRC(linrec_scan_backward_f32(g, h0, h, dh, nullptr, G, dh0 ? dh0 : dh0_tmp, T, b * n, mode, nullptr, st));
   mark(st, "scan_bwd_surrogate");
   const RowPlan rp = row_plan(R, n);
-  k_gilr_dpre<<<dim3((unsigned)rp.nbx, (unsigned)rp.gy), rp.thr, 0, st>>>(g, ci, dl, G, p->act, dpre_s, part, R, n,
-                                                                          rp.rpb);
+  (void)dl;
+  k_gilr_dpre<<<dim3((unsigned)rp.nbx, (unsigned)rp.gy), rp.thr, 0, st>>>(g, ci, h, h0, G, p->act, dpre_s, part, R, n,
+                                                                          b, rp.rpb);
   LTRY(cudaGetLastError());
   if (gr->b_g) {
     k_colsum<<<(unsigned)((n + 31) / 32), 1024, 0, st>>>(part, rp.nbx, 2 * n, n, gr->b_g);
@@ -580,11 +593,11 @@ int linrec_qrnn_backward_f32(const float* W, const float* x, const float* c0, co
   k_mul<<<grid_for(N / 4, 256), 256, 0, st>>>(dh, go, s.dc, N / 4);
   LTRY(cudaGetLastError());
   mark(st, "dc");
-  LRC(linrec_scan_backward_f32(gf, c0, c, s.dc, s.df, s.dimp, dc0 ? dc0 : s.tmp0, T, b * n, mode, nullptr, st));
+  LRC(linrec_scan_backward_f32(gf, c0, c, s.dc, nullptr, s.dimp, dc0 ? dc0 : s.tmp0, T, b * n, mode, nullptr, st));
   mark(st, "scan_bwd_cell");
   const RowPlan rp = row_plan(R, n);
-  k_qrnn_dpre<<<dim3((unsigned)rp.nbx, (unsigned)rp.gy), rp.thr, 0, st>>>(gf, go, gz, s.df, s.dimp, dh, c, s.dpre,
-                                                                          s.part, R, n, rp.rpb);
+  k_qrnn_dpre<<<dim3((unsigned)rp.nbx, (unsigned)rp.gy), rp.thr, 0, st>>>(gf, go, gz, c0, s.dimp, dh, c, s.dpre,
+                                                                          s.part, R, n, b, rp.rpb);
   LTRY(cudaGetLastError());
   if (dbias) {
     k_colsum<<<(unsigned)((3 * n + 31) / 32), 1024, 0, st>>>(s.part, rp.nbx, 3 * n, 3 * n, dbias);
@@ -808,11 +821,11 @@ int linrec_gilr_lstm_backward_f32(const linrec_gilr_lstm_params_f32* p, const fl
   k_mul<<<grid_for(N / 4, 256), 256, 0, st>>>(dh, go, s.dc, N / 4);
   LTRY(cudaGetLastError());
   mark(st, "dc");
-  LRC(linrec_scan_backward_f32(gf, c0, cache->c, s.dc, s.df, s.diz, dc0 ? dc0 : s.tmp0, T, BN, mode, nullptr, st));
+  LRC(linrec_scan_backward_f32(gf, c0, cache->c, s.dc, nullptr, s.diz, dc0 ? dc0 : s.tmp0, T, BN, mode, nullptr, st));
   mark(st, "scan_bwd_cell");
   const RowPlan rp = row_plan(R, n);
-  k_lstm_dpre<<<dim3((unsigned)rp.nbx, (unsigned)rp.gy), rp.thr, 0, st>>>(gf, gi, go, gz, s.df, s.diz, dh, cache->c,
-                                                                          s.dpre, s.part, R, n, rp.rpb);
+  k_lstm_dpre<<<dim3((unsigned)rp.nbx, (unsigned)rp.gy), rp.thr, 0, st>>>(gf, gi, go, gz, c0, s.diz, dh, cache->c,
+                                                                          s.dpre, s.part, R, n, b, rp.rpb);
   LTRY(cudaGetLastError());
   if (grads->bias) {
     k_colsum<<<(unsigned)((4 * n + 31) / 32), 1024, 0, st>>>(s.part, rp.nbx, 4 * n, 4 * n, grads->bias);

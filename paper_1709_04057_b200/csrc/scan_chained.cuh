@@ -721,7 +721,7 @@ k_chain_bwd(const ChainArgs<S> a, const ChainWs ws) {
     const int t = t0 + i;
     if (valid && t < Ti) {
       IO::store_stream(a.out0 + t * W + ch, cs);
-      IO::store_stream(a.out1 + t * W + ch, dl);
+      if (a.out1 != nullptr) IO::store_stream(a.out1 + t * W + ch, dl);
       if (t == 0 && a.out2 != nullptr) {
         S l0[VEC], d0[VEC];
         IO::load_cg(a.a + ch, l0);
@@ -813,7 +813,7 @@ k_serial_bwd(const S* __restrict__ lam, const S* __restrict__ h0, const S* __res
           dl[v] = mul_(hp[u][v], G[v]);
         }
         IO::store_stream(dx + t * W + ch, G);
-        IO::store_stream(dlam + t * W + ch, dl);
+        if (dlam != nullptr) IO::store_stream(dlam + t * W + ch, dl);
       }
     }
   }

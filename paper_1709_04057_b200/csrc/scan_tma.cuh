@@ -463,7 +463,7 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
       const int t = t0 + i;
       if (valid && t < Ti) {
         IO::store_stream(a.out0 + t * W + ch, cs);
-        IO::store_stream(a.out1 + t * W + ch, dl);
+        if (a.out1 != nullptr) IO::store_stream(a.out1 + t * W + ch, dl);
         if (t == 0 && a.out2 != nullptr) {
           S l0[VEC], d0[VEC];
           IO::load_cg(a.a + ch, l0);

@@ -159,7 +159,7 @@ k_fixup(const S* __restrict__ lam, const S* __restrict__ hprev_row, const S* __r
 #pragma unroll
         for (int v = 0; v < VEC; ++v) o[v] = o[v] + ecur[v];
         IO::store_cg(out0 + t * W + ch, o);
-        if (REV) {
+        if (REV && out1 != nullptr) {
           S hp[VEC], d[VEC];
           if (t >= 1) IO::load_cg(h + (t - 1) * W + ch, hp);
           else {
