@@ -34,8 +34,18 @@ OBJS        := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(KERNEL_SRCS)) $(BUILD)/cap
 LIB   := $(PKG)/liblinrec_cuda.so
 PYMOD := $(PKG)/linrec$(EXT)
 
-.PHONY: all lib py oracle ref clean
-all: lib py oracle
+CPPTEST := $(BUILD)/test_cuda_api
+
+.PHONY: all lib py oracle ref clean cpp-tests
+all: lib py oracle cpp-tests
+
+# C++ caller of include/linrec/cuda_scan.hpp + cuda_layers.hpp (host code only:
+# g++ against the C ABI and the CUDA runtime for device buffers).
+cpp-tests: $(CPPTEST)
+$(CPPTEST): tests/cpp/test_cuda_api.cpp include/linrec/cuda_scan.hpp include/linrec/cuda_layers.hpp include/linrec_cuda.h $(LIB)
+	@mkdir -p $(BUILD)
+	$(CXX) -std=c++17 -O2 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -llinrec_cuda \
+	  -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
 
 lib: $(LIB)
 py: $(PYMOD)
