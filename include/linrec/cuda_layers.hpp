@@ -184,8 +184,8 @@ inline void qrnn_forward(const QrnnParams& p, const DeviceTensor3<float>& x, con
   const size_t need = linrec_qrnn_scratch_bytes(x.steps, x.batch, p.m, p.n, p.k);
   void* scr = ctx.scratch(need);  // grow first: capacity() below must see it
   throw_status(linrec_qrnn_forward_f32(p.W, p.bias, x.data, c0.data, h.data, cache.gates, cache.c, x.steps, x.batch,
-                                       p.m, p.n, p.k, static_cast<int>(mode), ctx.precision(), ctx.scratch(need),
-                                       ctx.capacity(), ctx.stream()));
+                                       p.m, p.n, p.k, static_cast<int>(mode), ctx.precision(), scr, ctx.capacity(),
+                                       ctx.stream()));
 }
 
 // qrnn_backward (:496-548).
