@@ -1,0 +1,268 @@
+// Device building blocks of the virtual-segment / sequence-segment stitch,
+// shared by the standalone kernels of segment.cu and by the fused tail of the
+// persistent TMA scans (scan_tma.cuh, phase 2):
+//
+//   vseg_fold      carries entering each virtual segment from the segments'
+//                  aggregates (blocked three-phase fold, fixed association)
+//   fixup_position add the decaying contribution P_t * e of a segment's
+//                  incoming carry to one tile (chain position) and report
+//                  whether it was non-zero (a zero entering correction stays
+//                  exactly zero further down the chain: the walk stops)
+//
+// Both run on a team of 8 warps (256 threads) that synchronises through a
+// policy: the whole CTA (__syncthreads) in the standalone kernels, or named
+// barrier 1 over the 8 data warps inside the persistent scan kernels.
+#pragma once
+
+#include <cstdint>
+
+#include "scan_chained.cuh"
+
+namespace linrec_dev {
+
+struct CtaSync {
+  static __device__ __forceinline__ void sync() { __syncthreads(); }
+  static __device__ __forceinline__ bool sync_or(bool p) { return __syncthreads_or(p) != 0; }
+};
+// Named barrier 1 over threads [0, 256) of a larger CTA.
+struct TeamSync {
+  static __device__ __forceinline__ void sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+  static __device__ __forceinline__ bool sync_or(bool p) {
+    uint32_t r;
+    asm volatile(
+        "{\n\t.reg .pred ip, op;\n\t"
+        "setp.ne.u32 ip, %1, 0;\n\t"
+        "bar.red.or.pred op, 1, 256, ip;\n\t"
+        "selp.u32 %0, 1, 0, op;\n\t}"
+        : "=r"(r)
+        : "r"((uint32_t)p)
+        : "memory");
+    return r != 0;
+  }
+};
+
+template <class S>
+struct FixupArgs {
+  const S* lam;
+  const S* hprev_row;  // bwd: h row before the range (h0 / the previous rank's last row)
+  const S* h;
+  const S* lam_next;   // bwd: decay of the row after the range
+  S* seg_prod;         // exclusive decay product entering each chain position [nseg*ntt][W]
+  S* out0;             // fwd: h; bwd: dx
+  S* out1;             // bwd: dlam (nullable)
+  int64_t T, W, rows, nseg, tseg, ntt;
+};
+
+// One tile (chain position p_in of virtual segment vseg, channel column col)
+// of the stitch.  carry[ch] is the carry entering the segment (fwd: state;
+// bwd: lam_E * G_E from above).  With `scale` the position's seg_prod row is
+// also rescaled in place (virtual -> segment-relative products).  Returns
+// whether any channel's entering correction was non-zero.
+template <class S, int VEC, int Q, bool REV, class Sync>
+__device__ __forceinline__ bool fixup_position(const FixupArgs<S>& f, int64_t vseg, int64_t col, int64_t p_in,
+                                               const S* __restrict__ carry, const S* __restrict__ scale,
+                                               S (*s_wp)[Q * VEC]) {
+  constexpr int NW = 8, RF = 12, G = 32 / Q, CPW = Q * VEC, NSEG = NW * G, PR = NSEG * RF;  // PR = a TMA tile
+  using IO = VecIO<S, VEC>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane % Q, g = lane / Q;
+  const int64_t W = f.W, T = f.T, rows = f.rows;
+  const int64_t pos = vseg * f.ntt + p_in;
+  const int64_t tile_row = vseg * f.tseg + (REV ? f.ntt - 1 - p_in : p_in) * rows;
+  const int64_t ch = col * CPW + (int64_t)q * VEC;
+  const bool valid = ch < W;
+  S e[VEC];
+  bool nz = false;
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) e[v] = S(0);
+  if (valid) {
+    const S* sp = f.seg_prod + pos * W + ch;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      e[v] = mul_(sp[v], carry[ch + v]);
+      nz = nz || e[v] != S(0);
+    }
+  }
+  nz = Sync::sync_or(nz);  // every thread has read seg_prod past this point
+  if (scale != nullptr && valid && warp == 0 && g == 0) {
+    S* sp = f.seg_prod + pos * W + ch;
+    const S* sc = scale + vseg * W + ch;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) sp[v] = mul_(sp[v], sc[v]);
+  }
+  if (!nz) return false;
+
+  const int64_t t_lo = tile_row;
+  const int64_t seg_end = (vseg + 1) * f.tseg < T ? (vseg + 1) * f.tseg : T;
+  const int64_t t_hi = (t_lo + rows < seg_end ? t_lo + rows : seg_end);
+  const int64_t npass = (rows + PR - 1) / PR;
+  for (int64_t ps = 0; ps < npass; ++ps) {
+    const int64_t pbase = REV ? t_lo + rows - (ps + 1) * PR : t_lo + ps * PR;
+    const int seg = warp * G + g;
+    S m[RF][VEC];
+#pragma unroll
+    for (int i = 0; i < RF; ++i) {
+      const int64_t t = REV ? pbase + (PR - 1 - (seg * RF + i)) : pbase + seg * RF + i;
+      const bool in = valid && t >= t_lo && t < t_hi;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) m[i][v] = S(1);
+      if (in) {
+        if (!REV) {
+          IO::load_cg(f.lam + t * W + ch, m[i]);
+        } else if (t + 1 >= T) {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) m[i][v] = f.lam_next != nullptr ? f.lam_next[ch + v] : S(0);
+        } else if (f.nseg > 1 && (t + 1) % f.tseg == 0) {
+          // end of a virtual segment: mu = 1 (m already 1)
+        } else {
+          IO::load_cg(f.lam + (t + 1) * W + ch, m[i]);
+        }
+      }
+    }
+    S A[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) A[v] = m[0][v];
+#pragma unroll
+    for (int i = 1; i < RF; ++i)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) A[v] = mul_(m[i][v], A[v]);
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const S ap = __shfl_up_sync(0xffffffffu, A[v], off * Q);
+        if (g >= off) A[v] = mul_(A[v], ap);
+      }
+    S Ae[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      Ae[v] = S(1);
+      if (G > 1) {
+        const S ap = __shfl_up_sync(0xffffffffu, A[v], Q);
+        if (g > 0) Ae[v] = ap;
+      }
+    }
+    Sync::sync();
+    if (g == G - 1) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) s_wp[warp][q * VEC + v] = A[v];
+    }
+    Sync::sync();
+    S ecur[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) ecur[v] = e[v];
+    for (int w = 0; w < warp; ++w)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) ecur[v] = mul_(s_wp[w][q * VEC + v], ecur[v]);
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) ecur[v] = mul_(Ae[v], ecur[v]);
+#pragma unroll
+    for (int i = 0; i < RF; ++i) {
+      const int64_t t = REV ? pbase + (PR - 1 - (seg * RF + i)) : pbase + seg * RF + i;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) ecur[v] = mul_(m[i][v], ecur[v]);
+      if (valid && t >= t_lo && t < t_hi) {
+        S o[VEC];
+        IO::load_cg(f.out0 + t * W + ch, o);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) o[v] = o[v] + ecur[v];
+        IO::store_cg(f.out0 + t * W + ch, o);
+        if (REV && f.out1 != nullptr) {
+          S hp[VEC], d[VEC];
+          if (t >= 1) IO::load_cg(f.h + (t - 1) * W + ch, hp);
+          else {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) hp[v] = f.hprev_row != nullptr ? f.hprev_row[ch + v] : S(0);
+          }
+          IO::load_cg(f.out1 + t * W + ch, d);
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) d[v] = fma_(hp[v], ecur[v], d[v]);
+          IO::store_cg(f.out1 + t * W + ch, d);
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      S tot = S(1);
+      for (int w = 0; w < NW; ++w) tot = mul_(s_wp[w][q * VEC + v], tot);
+      e[v] = mul_(tot, e[v]);
+    }
+  }
+  Sync::sync();  // s_wp is reused by the next position
+  return true;
+}
+
+// Virtual-segment finalisation for one 32-channel chunk, on a team of 32*G
+// threads (lane = channel, group = a contiguous range of segments).
+// forward: carry[s] = state entering segment s (0 for s = 0, whose chain was
+//   seeded), scale[s] = decay product of the segments before s, agg_rank =
+//   (product over all, final state).
+// reverse: carry[s] = lam_E * G_E entering segment s from above (0 for the
+//   last), scale[s] = product of the A' of the segments after s, agg_rank =
+//   (A', B') of the whole range, dh0 = lam_0 * G_0 (the range's start).
+// vagg[s] = (P_incl, c_incl) of segment s's chains.  Fixed association:
+// deterministic.
+template <class S, bool REV>
+__device__ __forceinline__ void vseg_pair(const S* __restrict__ lam, const S* __restrict__ vagg, int64_t nseg,
+                                          int64_t tseg, int64_t W, int64_t i, int64_t j, S& A, S& B) {
+  const int64_t s = REV ? nseg - 1 - i : i;
+  A = vagg[s * 2 * W + j];
+  B = vagg[s * 2 * W + W + j];
+  if (REV) {
+    const S l0 = lam[(s * tseg) * W + j];
+    A = mul_(l0, A);
+    B = mul_(l0, B);
+  }
+}
+
+template <class S, bool REV, int G, class Sync>
+__device__ __forceinline__ void vseg_fold(const S* __restrict__ lam, const S* __restrict__ vagg, int64_t nseg,
+                                          int64_t tseg, S* __restrict__ carry, S* __restrict__ scale,
+                                          S* __restrict__ agg_rank, S* __restrict__ dh0, int64_t W, int64_t chunk,
+                                          S (*sA)[32], S (*sB)[32]) {
+  const int lane = threadIdx.x & 31, g = (threadIdx.x >> 5) % G;
+  const int64_t j = chunk * 32 + lane;
+  const bool ok = j < W;
+  const int64_t per = (nseg + G - 1) / G;
+  const int64_t i0 = (int64_t)g * per, i1 = i0 + per < nseg ? i0 + per : nseg;
+  S Ac = S(1), Bc = S(0);
+  if (ok) {
+#pragma unroll 4
+    for (int64_t i = i0; i < i1; ++i) {
+      S A, B;
+      vseg_pair<S, REV>(lam, vagg, nseg, tseg, W, i, j, A, B);
+      Bc = fma_(A, Bc, B);
+      Ac = mul_(A, Ac);
+    }
+  }
+  sA[g][lane] = Ac;
+  sB[g][lane] = Bc;
+  Sync::sync();
+  S c = S(0), pc = S(1);
+  for (int qq = 0; qq < g; ++qq) {
+    c = fma_(sA[qq][lane], c, sB[qq][lane]);
+    pc = mul_(sA[qq][lane], pc);
+  }
+  if (ok) {
+#pragma unroll 4
+    for (int64_t i = i0; i < i1; ++i) {
+      const int64_t s = REV ? nseg - 1 - i : i;
+      if (carry != nullptr) carry[s * W + j] = c;
+      if (scale != nullptr) scale[s * W + j] = pc;
+      S A, B;
+      vseg_pair<S, REV>(lam, vagg, nseg, tseg, W, i, j, A, B);
+      c = fma_(A, c, B);
+      pc = mul_(A, pc);
+    }
+    if (i1 == nseg && i0 < i1) {  // the group holding the last segment reports the whole range
+      if (agg_rank != nullptr) {
+        agg_rank[j] = pc;
+        agg_rank[W + j] = c;
+      }
+      if (dh0 != nullptr) dh0[j] = c;
+    }
+  }
+  Sync::sync();  // sA / sB reusable
+}
+
+}  // namespace linrec_dev

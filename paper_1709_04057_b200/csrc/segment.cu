@@ -18,171 +18,31 @@
 #include <cstdint>
 
 #include "chain_impl.cuh"
+#include "fixup_impl.cuh"
 
 namespace linrec_dev {
 
-// One CTA per (chain position, channel column); 8 warps; Q lanes across
-// channels x G groups along time, RF rows per thread per pass; a tile of
-// `rows` rows is covered in ceil(rows / (8*G*RF)) passes.  Chain positions
-// run over nseg virtual segments of ntt tiles (tile p of segment s starts at
-// row s*tseg + p*rows, or (ntt-1-p)*rows for the reverse scan).
+// One CTA per (chain position, channel column) -- or, with walk > 0, CTA k
+// of (segment, column) visiting positions k, k+walk, ... until the first
+// whose entering correction is zero in every channel (exact: a zero product
+// stays zero further down the chain).  8 warps; see fixup_impl.cuh.
 template <class S, int VEC, int Q, bool REV>
 __global__ void __launch_bounds__(256)
-k_fixup(const S* __restrict__ lam, const S* __restrict__ hprev_row, const S* __restrict__ h,
-        const S* __restrict__ lam_next, S* __restrict__ seg_prod, const S* __restrict__ carry,
-        int64_t carry_stride, const S* __restrict__ scale, S* __restrict__ out0 /* fwd: h; bwd: dx */,
-        S* __restrict__ out1 /* bwd: dlam */, int64_t T, int64_t W, int64_t rows, int64_t ncols, int64_t nseg,
-        int64_t tseg, int64_t ntt, int64_t walk) {
-  constexpr int NW = 8, RF = 12, G = 32 / Q, CPW = Q * VEC, NSEG = NW * G, PR = NSEG * RF;  // PR = a TMA tile
-  using IO = VecIO<S, VEC>;
-  __shared__ S s_wp[NW][CPW];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int q = lane % Q, g = lane / Q;
+k_fixup(FixupArgs<S> f, const S* __restrict__ carry, int64_t carry_stride, const S* __restrict__ scale,
+        int64_t ncols, int64_t walk) {
+  __shared__ S s_wp[8][Q * VEC];
   const int64_t col = blockIdx.x % ncols;
-  // walk == 0: one CTA per chain position.  walk > 0 (no `scale`): CTA k of
-  // (segment, column) visits positions k, k+walk, ... and stops at the first
-  // whose entering correction is zero in every channel -- exact, because the
-  // products are applied oldest first (bit-identical whatever the look-back
-  // depth), so a zero product stays zero further down the chain.
   int64_t vseg, p_in;
   if (walk > 0) {
     vseg = (blockIdx.x / ncols) / walk;
     p_in = (blockIdx.x / ncols) % walk;
   } else {
-    vseg = (blockIdx.x / ncols) / ntt;
-    p_in = (blockIdx.x / ncols) % ntt;
+    vseg = (blockIdx.x / ncols) / f.ntt;
+    p_in = (blockIdx.x / ncols) % f.ntt;
   }
-  for (; p_in < ntt; p_in += (walk > 0 ? walk : ntt)) {
-  const int64_t pos = vseg * ntt + p_in;
-  const int64_t tile_row = vseg * tseg + (REV ? ntt - 1 - p_in : p_in) * rows;
-  const int64_t ch = col * CPW + (int64_t)q * VEC;
-  const bool valid = ch < W;
-  // carry entering the tile: exclusive product * segment carry
-  S e[VEC];
-  bool nz = false;
-#pragma unroll
-  for (int v = 0; v < VEC; ++v) e[v] = S(0);
-  if (valid) {
-    const S* sp = seg_prod + pos * W + ch;
-    const S* cr = carry + vseg * carry_stride + ch;
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      e[v] = mul_(sp[v], cr[v]);
-      nz = nz || e[v] != S(0);
-    }
-  }
-  nz = __syncthreads_or(nz) != 0;  // every thread has read seg_prod past this point
-  if (scale != nullptr && valid && warp == 0 && g == 0) {  // virtual -> segment-relative products
-    S* sp = seg_prod + pos * W + ch;
-    const S* sc = scale + vseg * W + ch;
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) sp[v] = mul_(sp[v], sc[v]);
-  }
-  if (!nz) return;
-
-  const int64_t t_lo = tile_row;
-  const int64_t seg_end = (vseg + 1) * tseg < T ? (vseg + 1) * tseg : T;
-  const int64_t t_hi = (t_lo + rows < seg_end ? t_lo + rows : seg_end);
-  const int64_t npass = (rows + PR - 1) / PR;
-  for (int64_t ps = 0; ps < npass; ++ps) {
-    // rows of this pass, in processing order
-    const int64_t pbase = REV ? t_lo + rows - (ps + 1) * PR : t_lo + ps * PR;
-    const int seg = warp * G + g;
-    S m[RF][VEC];
-#pragma unroll
-    for (int i = 0; i < RF; ++i) {
-      // processing index within the pass: REV walks rows downward
-      const int64_t t = REV ? pbase + (PR - 1 - (seg * RF + i)) : pbase + seg * RF + i;
-      const bool in = valid && t >= t_lo && t < t_hi;
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) m[i][v] = S(1);
-      if (in) {
-        if (!REV) {
-          IO::load_cg(lam + t * W + ch, m[i]);
-        } else if (t + 1 >= T) {
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) m[i][v] = lam_next != nullptr ? lam_next[ch + v] : S(0);
-        } else if (nseg > 1 && (t + 1) % tseg == 0) {
-          // end of a virtual segment: mu = 1 (m already 1)
-        } else {
-          IO::load_cg(lam + (t + 1) * W + ch, m[i]);
-        }
-      }
-    }
-    // segment product, inclusive scan across the warp's groups, then warps
-    S A[VEC];
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) A[v] = m[0][v];
-#pragma unroll
-    for (int i = 1; i < RF; ++i)
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) A[v] = mul_(m[i][v], A[v]);
-#pragma unroll
-    for (int off = 1; off < G; off <<= 1)
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        const S ap = __shfl_up_sync(0xffffffffu, A[v], off * Q);
-        if (g >= off) A[v] = mul_(A[v], ap);
-      }
-    S Ae[VEC];
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      Ae[v] = S(1);
-      if (G > 1) {
-        const S ap = __shfl_up_sync(0xffffffffu, A[v], Q);
-        if (g > 0) Ae[v] = ap;
-      }
-    }
-    __syncthreads();
-    if (g == G - 1) {
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) s_wp[warp][q * VEC + v] = A[v];
-    }
-    __syncthreads();
-    S ecur[VEC];
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) ecur[v] = e[v];
-    for (int w = 0; w < warp; ++w)
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) ecur[v] = mul_(s_wp[w][q * VEC + v], ecur[v]);
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) ecur[v] = mul_(Ae[v], ecur[v]);
-    // apply
-#pragma unroll
-    for (int i = 0; i < RF; ++i) {
-      const int64_t t = REV ? pbase + (PR - 1 - (seg * RF + i)) : pbase + seg * RF + i;
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) ecur[v] = mul_(m[i][v], ecur[v]);
-      if (valid && t >= t_lo && t < t_hi) {
-        S o[VEC];
-        IO::load_cg(out0 + t * W + ch, o);
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) o[v] = o[v] + ecur[v];
-        IO::store_cg(out0 + t * W + ch, o);
-        if (REV && out1 != nullptr) {
-          S hp[VEC], d[VEC];
-          if (t >= 1) IO::load_cg(h + (t - 1) * W + ch, hp);
-          else {
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) hp[v] = hprev_row != nullptr ? hprev_row[ch + v] : S(0);
-          }
-          IO::load_cg(out1 + t * W + ch, d);
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) d[v] = fma_(hp[v], ecur[v], d[v]);
-          IO::store_cg(out1 + t * W + ch, d);
-        }
-      }
-    }
-    // carry into the next pass = e * product of this whole pass
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      S tot = S(1);
-      for (int w = 0; w < NW; ++w) tot = mul_(s_wp[w][q * VEC + v], tot);
-      e[v] = mul_(tot, e[v]);
-    }
-  }
-  __syncthreads();  // s_wp is reused by the next position
-  }
+  for (; p_in < f.ntt; p_in += (walk > 0 ? walk : f.ntt))
+    if (!fixup_position<S, VEC, Q, REV, CtaSync>(f, vseg, col, p_in, carry + vseg * carry_stride, scale, s_wp))
+      return;
 }
 
 // out[j] = fold over q in [first, last) by `step` of c = A_q[j] * c + B_q[j],
@@ -198,82 +58,16 @@ __global__ void k_compose(const S* __restrict__ aggs, int64_t first, int64_t las
   }
 }
 
-// Virtual-segment finalisation.
-// forward: carry[s] = state entering segment s (0 for s = 0, whose chain was
-//   seeded), scale[s] = decay product of the segments before s, agg_rank =
-//   (product over all, final state).
-// reverse: carry[s] = lam_E * G_E entering segment s from above (0 for the
-//   last), scale[s] = product of the A' of the segments after s, agg_rank =
-//   (A', B') of the whole range, dh0 = lam_0 * G_0 (the range's start).
-// vagg[s] = (P_incl, c_incl) of segment s's chains.
-// Block = 32 channels x G segment groups: each group composes its contiguous
-// range of segments (processing order), the groups' composites are folded in
-// group order, and each group re-walks its range from its incoming state --
-// a fixed association (deterministic), sequential depth 2*nseg/G + G instead
-// of nseg (C4: 256 segments, 49 -> a few us).
-template <class S, bool REV>
-__device__ __forceinline__ void vseg_pair(const S* __restrict__ lam, const S* __restrict__ vagg, int64_t nseg,
-                                          int64_t tseg, int64_t W, int64_t i, int64_t j, S& A, S& B) {
-  const int64_t s = REV ? nseg - 1 - i : i;
-  A = vagg[s * 2 * W + j];
-  B = vagg[s * 2 * W + W + j];
-  if (REV) {
-    const S l0 = lam[(s * tseg) * W + j];
-    A = mul_(l0, A);
-    B = mul_(l0, B);
-  }
-}
-
+// Virtual-segment finalisation: one CTA of 32 x G threads per 32-channel
+// chunk (fixup_impl.cuh::vseg_fold): sequential depth 2*nseg/G + G instead of
+// nseg (C4: 256 segments, 49 -> 8 us).
 template <class S, bool REV, int G>
 __global__ void __launch_bounds__(32 * G)
 k_vseg_finalize(const S* __restrict__ lam, const S* __restrict__ vagg, int64_t nseg, int64_t tseg,
                 S* __restrict__ carry, S* __restrict__ scale, S* __restrict__ agg_rank, S* __restrict__ dh0,
                 int64_t W) {
   __shared__ S sA[G][32], sB[G][32];
-  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
-  const bool ok = j < W;
-  const int64_t per = (nseg + G - 1) / G;
-  const int64_t i0 = (int64_t)g * per, i1 = i0 + per < nseg ? i0 + per : nseg;
-  // phase 1: composite (A, B) of this group's segments, oldest first
-  S Ac = S(1), Bc = S(0);
-  if (ok) {
-#pragma unroll 4
-    for (int64_t i = i0; i < i1; ++i) {
-      S A, B;
-      vseg_pair<S, REV>(lam, vagg, nseg, tseg, W, i, j, A, B);
-      Bc = fma_(A, Bc, B);
-      Ac = mul_(A, Ac);
-    }
-  }
-  sA[g][lane] = Ac;
-  sB[g][lane] = Bc;
-  __syncthreads();
-  // phase 2: state and product entering this group (groups folded in order)
-  S c = S(0), pc = S(1);
-  for (int q = 0; q < g; ++q) {
-    c = fma_(sA[q][lane], c, sB[q][lane]);
-    pc = mul_(sA[q][lane], pc);
-  }
-  if (!ok) return;
-  // phase 3: re-walk, writing each segment's incoming state / product
-#pragma unroll 4
-  for (int64_t i = i0; i < i1; ++i) {
-    const int64_t s = REV ? nseg - 1 - i : i;
-    if (carry != nullptr) carry[s * W + j] = c;
-    if (scale != nullptr) scale[s * W + j] = pc;
-    S A, B;
-    vseg_pair<S, REV>(lam, vagg, nseg, tseg, W, i, j, A, B);
-    c = fma_(A, c, B);
-    pc = mul_(A, pc);
-  }
-  if (i1 == nseg && i0 < i1) {  // the group holding the last segment reports the whole range
-    if (agg_rank != nullptr) {
-      agg_rank[j] = pc;
-      agg_rank[W + j] = c;
-    }
-    if (dh0 != nullptr) dh0[j] = c;
-  }
+  vseg_fold<S, REV, G, CtaSync>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W, blockIdx.x, sA, sB);
 }
 
 }  // namespace linrec_dev
@@ -293,13 +87,12 @@ cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S
   // the walk needs seg_prod untouched after the check: only without `scale`
   const int64_t walk = scale == nullptr ? (ntt < 8 ? ntt : 8) : 0;
   const dim3 grid((unsigned)(ncols * nseg * (walk > 0 ? walk : ntt)));
+  const linrec_dev::FixupArgs<S> fa{lam, hprev_row, h, lam_next, seg_prod, out0, out1, T, W, rows, nseg, tseg, ntt};
 #define FIX(VV)                                                                                       \
   LINREC_Q_SWITCH(q, if (reverse) linrec_dev::k_fixup<S, VV, Q_, true><<<grid, 256, 0, st>>>(         \
-                         lam, hprev_row, h, lam_next, seg_prod, carry, carry_stride, scale, out0, out1, T, \
-                         W, rows, ncols, nseg, tseg, ntt, walk);                                            \
+                         fa, carry, carry_stride, scale, ncols, walk);                                \
                      else linrec_dev::k_fixup<S, VV, Q_, false><<<grid, 256, 0, st>>>(                \
-                         lam, hprev_row, h, lam_next, seg_prod, carry, carry_stride, scale, out0, out1, T, \
-                         W, rows, ncols, nseg, tseg, ntt, walk));
+                         fa, carry, carry_stride, scale, ncols, walk));
   if (vec_ok) {
     FIX(V)
   } else {
