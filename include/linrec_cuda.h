@@ -201,7 +201,10 @@ int linrec_first_nonfinite_f64(const double* v, int64_t n, int64_t* index,
  *      R-1 .. r+1 into y_in; 4. linrec_segment_fixup_backward_* adds
  *      P'_t*y_in to dx and h_{t-1}*P'_t*y_in to dlam; rank 0's
  *      dh0 = A'_0*y_in + B'_0 (compose with seed y_in).
- * seg_prod holds linrec_segment_prod_rows(...) rows of W values; pass
+ * seg_prod holds linrec_segment_prod_rows(...) rows of W values (the
+ * products entering each chain position relative to its virtual segment,
+ * then one row per virtual segment: the product from the segment start to
+ * the virtual segment's start; the fix-up multiplies the two); pass
  * linrec_segment_tile_rows(...) to the fix-up.  Buffers 16-byte aligned when
  * W is a multiple of 4 (fp32) / 2 (fp64). */
 int64_t linrec_segment_prod_rows(int64_t T, int64_t W, int dtype_bytes, int backward);

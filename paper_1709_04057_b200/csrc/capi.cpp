@@ -511,12 +511,13 @@ int segment_scan(const S* lam, const S* x, const S* h0, S* h, S* seg_prod, S* ag
   FwdCall<S> c{lam, x, h0, h, T, W, seg_prod, vs.vagg};
   if (p.kind == 1) LINREC_CUDA_TRY(linrec_impl::launch_tma_fwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_fwd<S>(p, c, ws_ptrs(w, p), st));
-  // carries / products of the virtual segments -> segment-level aggregate
-  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, vs.vagg, p.nseg, p.tseg, vs.carry, vs.scale,
-                                                       agg, nullptr, W, st));
+  // carries / products of the virtual segments -> segment-level aggregate;
+  // the per-segment scale rows follow the position rows of seg_prod
+  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, vs.vagg, p.nseg, p.tseg, vs.carry,
+                                                       seg_prod + p.nseg * p.ntt * W, agg, nullptr, W, st));
   if (p.nseg > 1)
     LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(false, lam, nullptr, nullptr, nullptr, seg_prod, vs.carry, W,
-                                                 vs.scale, h, nullptr, T, W, p.rows, p.nseg, p.tseg, p.ntt,
+                                                 nullptr, h, nullptr, T, W, p.rows, p.nseg, p.tseg, p.ntt,
                                                  p.vec > 1, st));
   return LINREC_OK;
 }
@@ -545,10 +546,10 @@ int segment_scan_backward(const S* lam, const S* hprev, const S* h, const S* dh,
   if (p.kind == 1) LINREC_CUDA_TRY(linrec_impl::launch_tma_bwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_bwd<S>(p, c, ws_ptrs(w, p), st));
   // (A', B') of the segment for the exchange, dh0 = lam_S * G_S, fix-up
-  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, vs.vagg, p.nseg, p.tseg, vs.carry, vs.scale,
-                                                       agg, dh0, W, st));
+  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, vs.vagg, p.nseg, p.tseg, vs.carry,
+                                                       seg_prod + p.nseg * p.ntt * W, agg, dh0, W, st));
   if (p.nseg > 1)
-    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(true, lam, hprev, h, lam_next, seg_prod, vs.carry, W, vs.scale,
+    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(true, lam, hprev, h, lam_next, seg_prod, vs.carry, W, nullptr,
                                                  dx, dlam, T, W, p.rows, p.nseg, p.tseg, p.ntt, p.vec > 1, st));
   return LINREC_OK;
 }
@@ -566,8 +567,8 @@ int segment_fixup(bool reverse, const S* lam, const S* hprev, const S* h, const 
   // the same (nseg, ntt) decomposition the segment scan used
   const ChainPlan p = plan_segment<S>(!reverse, T, W);
   if (p.rows != rows) return fail(LINREC_ERR_VALUE, "tile_rows does not match the segment scan's plan");
-  LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(reverse, lam, hprev, h, lam_next, const_cast<S*>(seg_prod), carry,
-                                               0, nullptr, out0, out1, T, W, rows, p.nseg, p.tseg, p.ntt, v, st));
+  LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(reverse, lam, hprev, h, lam_next, seg_prod, carry, 0,
+                                               seg_prod + p.nseg * p.ntt * W, out0, out1, T, W, rows, p.nseg, p.tseg, p.ntt, v, st));
   return LINREC_OK;
 }
 
@@ -723,7 +724,7 @@ int linrec_first_nonfinite_f64(const double* v, int64_t n, int64_t* index, void*
 int64_t linrec_segment_prod_rows(int64_t T, int64_t W, int dtype_bytes, int backward) {
   if (T < 1 || W < 1) return 0;
   const ChainPlan p = dtype_bytes == 8 ? plan_segment<double>(!backward, T, W) : plan_segment<float>(!backward, T, W);
-  return p.nseg * p.ntt;
+  return p.nseg * p.ntt + p.nseg;  // position rows, then one scale row per virtual segment
 }
 
 int64_t linrec_segment_tile_rows(int64_t T, int64_t W, int dtype_bytes, int backward) {

@@ -3,6 +3,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 namespace linrec_impl {
@@ -43,6 +44,16 @@ struct ChainPtrs {  // host mirror of linrec_dev::ChainWs
   void* agg;
   void* inc;
 };
+
+inline int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+// CTAs per (segment, column) chain of the stitch fix-up (fixup_chain).
+inline int fixup_walkers() {
+  static const int k = env_int("LINREC_FIXUP_WALK", 2);
+  return k < 1 ? 1 : (k > 8 ? 8 : k);
+}
 
 template <class S>
 struct FwdCall {
@@ -100,7 +111,7 @@ cudaError_t launch_ws_init(void* ctrl, cudaStream_t st);
 // relative products).
 template <class S>
 cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S* h, const S* lam_next,
-                         S* seg_prod, const S* carry, int64_t carry_stride, const S* scale, S* out0, S* out1,
+                         const S* seg_prod, const S* carry, int64_t carry_stride, const S* scale, S* out0, S* out1,
                          int64_t T, int64_t W, int64_t rows, int64_t nseg, int64_t tseg, int64_t ntt,
                          bool vec_ok, cudaStream_t st);
 template <class S>

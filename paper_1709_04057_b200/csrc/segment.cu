@@ -22,27 +22,18 @@
 
 namespace linrec_dev {
 
-// One CTA per (chain position, channel column) -- or, with walk > 0, CTA k
-// of (segment, column) visiting positions k, k+walk, ... until the first
-// whose entering correction is zero in every channel (exact: a zero product
-// stays zero further down the chain).  8 warps; see fixup_impl.cuh.
+// CTA j of the J walkers of chain (virtual segment, channel column):
+// fixup_chain (fixup_impl.cuh), 8 warps.
 template <class S, int VEC, int Q, bool REV>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
 k_fixup(FixupArgs<S> f, const S* __restrict__ carry, int64_t carry_stride, const S* __restrict__ scale,
-        int64_t ncols, int64_t walk) {
+        int64_t ncols, int walkers) {
   __shared__ S s_wp[8][Q * VEC];
+  __shared__ int s_flag[8];
   const int64_t col = blockIdx.x % ncols;
-  int64_t vseg, p_in;
-  if (walk > 0) {
-    vseg = (blockIdx.x / ncols) / walk;
-    p_in = (blockIdx.x / ncols) % walk;
-  } else {
-    vseg = (blockIdx.x / ncols) / f.ntt;
-    p_in = (blockIdx.x / ncols) % f.ntt;
-  }
-  for (; p_in < f.ntt; p_in += (walk > 0 ? walk : f.ntt))
-    if (!fixup_position<S, VEC, Q, REV, CtaSync>(f, vseg, col, p_in, carry + vseg * carry_stride, scale, s_wp))
-      return;
+  const int j = (int)((blockIdx.x / ncols) % walkers);
+  const int64_t vseg = (blockIdx.x / ncols) / walkers;
+  fixup_chain<S, VEC, Q, REV, CtaSync>(f, vseg, col, j, walkers, carry + vseg * carry_stride, scale, s_wp, s_flag);
 }
 
 // out[j] = fold over q in [first, last) by `step` of c = A_q[j] * c + B_q[j],
@@ -76,7 +67,7 @@ namespace linrec_impl {
 
 template <class S>
 cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S* h, const S* lam_next,
-                         S* seg_prod, const S* carry, int64_t carry_stride, const S* scale, S* out0, S* out1,
+                         const S* seg_prod, const S* carry, int64_t carry_stride, const S* scale, S* out0, S* out1,
                          int64_t T, int64_t W, int64_t rows, int64_t nseg, int64_t tseg, int64_t ntt,
                          bool vec_ok, cudaStream_t st) {
   constexpr int V = Tuning<S>::VEC;
@@ -84,9 +75,8 @@ cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S
   const int q = pick_q(nvec);
   const int cpw = q * (vec_ok ? V : 1);
   const int64_t ncols = (W + cpw - 1) / cpw;
-  // the walk needs seg_prod untouched after the check: only without `scale`
-  const int64_t walk = scale == nullptr ? (ntt < 8 ? ntt : 8) : 0;
-  const dim3 grid((unsigned)(ncols * nseg * (walk > 0 ? walk : ntt)));
+  const int walk = fixup_walkers();
+  const dim3 grid((unsigned)(ncols * nseg * walk));
   const linrec_dev::FixupArgs<S> fa{lam, hprev_row, h, lam_next, seg_prod, out0, out1, T, W, rows, nseg, tseg, ntt};
 #define FIX(VV)                                                                                       \
   LINREC_Q_SWITCH(q, if (reverse) linrec_dev::k_fixup<S, VV, Q_, true><<<grid, 256, 0, st>>>(         \
@@ -123,11 +113,11 @@ cudaError_t launch_compose(const S* aggs, int64_t first, int64_t last, int64_t s
   return cudaGetLastError();
 }
 
-template cudaError_t launch_fixup<float>(bool, const float*, const float*, const float*, const float*, float*,
+template cudaError_t launch_fixup<float>(bool, const float*, const float*, const float*, const float*, const float*,
                                          const float*, int64_t, const float*, float*, float*, int64_t, int64_t,
                                          int64_t, int64_t, int64_t, int64_t, bool, cudaStream_t);
 template cudaError_t launch_fixup<double>(bool, const double*, const double*, const double*, const double*,
-                                          double*, const double*, int64_t, const double*, double*, double*,
+                                          const double*, const double*, int64_t, const double*, double*, double*,
                                           int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, bool, cudaStream_t);
 template cudaError_t launch_compose<float>(const float*, int64_t, int64_t, int64_t, const float*, float*,
                                            int64_t, cudaStream_t);
