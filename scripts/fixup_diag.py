@@ -35,7 +35,7 @@ for back in (False, True):
     # n = nseg*ntt + nseg ; ntt*rows ~ tseg
     cands = [k for k in range(1, n + 1) if n % k == 0 and n // k > 1
              and k * (n // k - 1) * rows >= T and (k - 1) * (n // k - 1) * rows < T]
-    nseg = cands[0]
+    nseg = cands[-1]  # the finest split consistent with the row count
     ntt = n // nseg - 1
     pos = sp[: nseg * ntt].view(nseg, ntt, W)
     nzpos = (pos != 0).any(dim=2)  # [nseg][ntt]
