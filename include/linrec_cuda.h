@@ -185,26 +185,27 @@ int linrec_first_nonfinite_f64(const double* v, int64_t n, int64_t* index,
  * A sequence split into contiguous T-segments, one per rank.  Forward, rank r
  * (segment [S, E)):
  *   1. linrec_segment_scan_*: single-pass scan of the segment seeded with h0
- *      on rank 0 and with 0 elsewhere; besides h it writes seg_prod (the decay
- *      product from the segment start entering each chain position) and
- *      agg[2][W] = (prod lam over the segment, state at its last row);
+ *      on rank 0 and with 0 elsewhere, split internally into virtual
+ *      segments whose stitch is left to step 4; it writes seg_prod (the decay
+ *      products entering each chain position, plus the virtual segments'
+ *      scale and carry rows) and agg[2][W] = (prod lam over the segment,
+ *      zero-carry state at its last row);
  *   2. all-gather of agg over the ranks (NCCL, the caller's communicator);
  *   3. linrec_compose_carries_*: c_in = fold of the aggregates of ranks
  *      0..r-1 (c = A_q*c + B_q from 0; rank 0 publishes A = 0);
- *   4. linrec_segment_fixup_*: h_t += P_t * c_in on the tiles whose entering
- *      product is nonzero (exact: past the underflow the correction is 0).
+ *   4. linrec_segment_fixup_* on EVERY rank (c_in = NULL on rank 0): one
+ *      pass adding P_t * (virtual-segment carry + scale * c_in) on the tiles
+ *      whose entering correction is non-zero (exact: past the underflow the
+ *      correction is 0).
  * Backward, reverse time, with lam_next = a row of ones on every rank but the
  * last (the decay linking to the next rank is applied through the carry):
  *   1. linrec_segment_scan_backward_* (hprev = the true h row before the
  *      segment) writes dlam, dx, seg_prod, agg = (A', B') = (lam_S * prod mu,
  *      lam_S * G_S) and dh0 = B'; 2. all-gather agg; 3. compose ranks
- *      R-1 .. r+1 into y_in; 4. linrec_segment_fixup_backward_* adds
- *      P'_t*y_in to dx and h_{t-1}*P'_t*y_in to dlam; rank 0's
- *      dh0 = A'_0*y_in + B'_0 (compose with seed y_in).
- * seg_prod holds linrec_segment_prod_rows(...) rows of W values (the
- * products entering each chain position relative to its virtual segment,
- * then one row per virtual segment: the product from the segment start to
- * the virtual segment's start; the fix-up multiplies the two); pass
+ *      R-1 .. r+1 into y_in; 4. linrec_segment_fixup_backward_* on every
+ *      rank (y_in = NULL on the last) adds P'_t*y to dx and h_{t-1}*P'_t*y to
+ *      dlam; rank 0's dh0 = A'_0*y_in + B'_0 (compose with seed y_in).
+ * seg_prod holds linrec_segment_prod_rows(...) rows of W values; pass
  * linrec_segment_tile_rows(...) to the fix-up.  Buffers 16-byte aligned when
  * W is a multiple of 4 (fp32) / 2 (fp64). */
 int64_t linrec_segment_prod_rows(int64_t T, int64_t W, int dtype_bytes, int backward);

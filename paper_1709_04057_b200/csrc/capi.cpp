@@ -229,9 +229,9 @@ int scan_device(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t 
   if (p.nseg > 1) {
     LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, vs.vagg, p.nseg, p.tseg, vs.carry, nullptr,
                                                          nullptr, nullptr, W, st));
-    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(false, lam, nullptr, nullptr, nullptr, vs.seg_prod, vs.carry, W,
-                                                 nullptr, h, nullptr, T, W, p.rows, p.nseg, p.tseg, p.ntt, vok,
-                                                 st));
+    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(false, lam, nullptr, nullptr, nullptr, vs.seg_prod, vs.carry,
+                                                 nullptr, nullptr, h, nullptr, T, W, p.rows, p.nseg, p.tseg, p.ntt,
+                                                 vok, st));
   }
   return LINREC_OK;
 }
@@ -271,8 +271,8 @@ int scan_backward_device(const S* lam, const S* h0, const S* h, const S* dh, con
   if (p.nseg > 1) {
     LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, vs.vagg, p.nseg, p.tseg, vs.carry, nullptr,
                                                          nullptr, dh0, W, st));
-    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(true, lam, h0, h, lam_next, vs.seg_prod, vs.carry, W, nullptr,
-                                                 dx, dlam, T, W, p.rows, p.nseg, p.tseg, p.ntt, vok, st));
+    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(true, lam, h0, h, lam_next, vs.seg_prod, vs.carry, nullptr,
+                                                 nullptr, dx, dlam, T, W, p.rows, p.nseg, p.tseg, p.ntt, vok, st));
   }
   return LINREC_OK;
 }
@@ -490,6 +490,16 @@ ChainPlan plan_segment(bool forward, int64_t T, int64_t W) {
   return p;
 }
 
+// seg_prod layout: [nseg*ntt] position rows, [nseg] scale rows, [nseg] carry rows
+template <class P>
+P seg_scale_rows(P seg_prod, const ChainPlan& p, int64_t W) {
+  return seg_prod + p.nseg * p.ntt * W;
+}
+template <class P>
+P seg_carry_rows(P seg_prod, const ChainPlan& p, int64_t W) {
+  return seg_prod + p.nseg * (p.ntt + 1) * W;
+}
+
 template <class S>
 int segment_scan(const S* lam, const S* x, const S* h0, S* h, S* seg_prod, S* agg, int64_t T, int64_t W,
                  linrec_workspace_t ws, cudaStream_t st) {
@@ -511,14 +521,10 @@ int segment_scan(const S* lam, const S* x, const S* h0, S* h, S* seg_prod, S* ag
   FwdCall<S> c{lam, x, h0, h, T, W, seg_prod, vs.vagg};
   if (p.kind == 1) LINREC_CUDA_TRY(linrec_impl::launch_tma_fwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_fwd<S>(p, c, ws_ptrs(w, p), st));
-  // carries / products of the virtual segments -> segment-level aggregate;
-  // the per-segment scale rows follow the position rows of seg_prod
-  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, vs.vagg, p.nseg, p.tseg, vs.carry,
-                                                       seg_prod + p.nseg * p.ntt * W, agg, nullptr, W, st));
-  if (p.nseg > 1)
-    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(false, lam, nullptr, nullptr, nullptr, seg_prod, vs.carry, W,
-                                                 nullptr, h, nullptr, T, W, p.rows, p.nseg, p.tseg, p.ntt,
-                                                 p.vec > 1, st));
+  // the segment-level aggregate, and the virtual segments' scale and own
+  // carry rows (seg_prod's tail) for the fix-up, which applies both at once
+  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, vs.vagg, p.nseg, p.tseg, seg_carry_rows(seg_prod, p, W),
+                                                       seg_scale_rows(seg_prod, p, W), agg, nullptr, W, st));
   return LINREC_OK;
 }
 
@@ -546,11 +552,8 @@ int segment_scan_backward(const S* lam, const S* hprev, const S* h, const S* dh,
   if (p.kind == 1) LINREC_CUDA_TRY(linrec_impl::launch_tma_bwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_bwd<S>(p, c, ws_ptrs(w, p), st));
   // (A', B') of the segment for the exchange, dh0 = lam_S * G_S, fix-up
-  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, vs.vagg, p.nseg, p.tseg, vs.carry,
-                                                       seg_prod + p.nseg * p.ntt * W, agg, dh0, W, st));
-  if (p.nseg > 1)
-    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(true, lam, hprev, h, lam_next, seg_prod, vs.carry, W, nullptr,
-                                                 dx, dlam, T, W, p.rows, p.nseg, p.tseg, p.ntt, p.vec > 1, st));
+  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, vs.vagg, p.nseg, p.tseg, seg_carry_rows(seg_prod, p, W),
+                                                       seg_scale_rows(seg_prod, p, W), agg, dh0, W, st));
   return LINREC_OK;
 }
 
@@ -559,16 +562,17 @@ int segment_fixup(bool reverse, const S* lam, const S* hprev, const S* h, const 
                   const S* carry, S* out0, S* out1, int64_t T, int64_t W, int64_t rows, cudaStream_t st) {
   int rc;
   if ((rc = check_dims(T, W)) || (rc = check_ptr(lam, "decays")) || (rc = check_ptr(seg_prod, "seg_prod")) ||
-      (rc = check_ptr(carry, "carry")) || (rc = check_ptr(out0, "out")))
-    return rc;
+      (rc = check_ptr(out0, "out")))
+    return rc;  // carry may be NULL: the first rank (forward) / the last (backward)
   if (reverse && ((rc = check_ptr(h, "h")) || (rc = check_ptr(out1, "d_decays")))) return rc;
   if (rows < 1) return fail(LINREC_ERR_VALUE, "tile_rows must be >= 1");
   const bool v = vec_ok<S>(W, {lam, hprev, h, lam_next, seg_prod, carry, out0, out1});
   // the same (nseg, ntt) decomposition the segment scan used
   const ChainPlan p = plan_segment<S>(!reverse, T, W);
   if (p.rows != rows) return fail(LINREC_ERR_VALUE, "tile_rows does not match the segment scan's plan");
-  LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(reverse, lam, hprev, h, lam_next, seg_prod, carry, 0,
-                                               seg_prod + p.nseg * p.ntt * W, out0, out1, T, W, rows, p.nseg, p.tseg, p.ntt, v, st));
+  LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(reverse, lam, hprev, h, lam_next, seg_prod,
+                                               seg_carry_rows(seg_prod, p, W), seg_scale_rows(seg_prod, p, W), carry,
+                                               out0, out1, T, W, rows, p.nseg, p.tseg, p.ntt, v, st));
   return LINREC_OK;
 }
 
@@ -724,7 +728,7 @@ int linrec_first_nonfinite_f64(const double* v, int64_t n, int64_t* index, void*
 int64_t linrec_segment_prod_rows(int64_t T, int64_t W, int dtype_bytes, int backward) {
   if (T < 1 || W < 1) return 0;
   const ChainPlan p = dtype_bytes == 8 ? plan_segment<double>(!backward, T, W) : plan_segment<float>(!backward, T, W);
-  return p.nseg * p.ntt + p.nseg;  // position rows, then one scale row per virtual segment
+  return p.nseg * (p.ntt + 2);  // position rows, then a scale and a carry row per virtual segment
 }
 
 int64_t linrec_segment_tile_rows(int64_t T, int64_t W, int dtype_bytes, int backward) {

@@ -6,10 +6,9 @@
 //   fixup_position add the decaying contribution P_t * e of a segment's
 //                  incoming carry to one tile (chain position)
 //   fixup_chain    the positions of one (segment, column) chain that need it:
-//                  the entering corrections are checked 8 positions per round
-//                  and the non-zero ones form a prefix (a zero correction
-//                  stays exactly zero further down the chain), so the walk
-//                  stops at the first zero without touching the rest
+//                  the non-zero entering corrections form a prefix (a zero
+//                  correction stays exactly zero further down the chain), so
+//                  the walk stops at the first zero without touching the rest
 //
 // All run on a team of 8 warps (256 threads) synchronising through a policy
 // class (CtaSync: the whole CTA).  A fused variant -- the stitch as the tail
@@ -41,71 +40,109 @@ struct FixupArgs {
   int64_t T, W, rows, nseg, tseg, ntt;
 };
 
-// Entering correction of chain position p_in of (vseg, column ch): the
-// position's product times the carry -- with `scale` (the product from the
-// range start to the virtual segment's start, one row per segment) first
-// multiplied in, exactly as a rescaled product would have been rounded.
+// The carry entering each virtual segment: its own (the fold of the earlier
+// virtual segments of the range, rows[vseg]) plus the range's incoming carry
+// cin carried to it (scale[vseg] = the decay product from the range start to
+// the virtual segment).  Any pointer may be null (no such term).
+template <class S>
+struct Carries {
+  const S* rows;   // [nseg][W]
+  const S* scale;  // [nseg][W]
+  const S* cin;    // [W]
+};
+
+// Entering correction of chain position p_in of (vseg, channels ch..): the
+// position's product times the segment's carry.
 template <class S, int VEC>
 __device__ __forceinline__ bool entering(const FixupArgs<S>& f, int64_t vseg, int64_t p_in, int64_t ch,
-                                         const S* __restrict__ carry, const S* __restrict__ scale, S (&e)[VEC]) {
+                                         const Carries<S>& cr, S (&e)[VEC]) {
+  using IO = VecIO<S, VEC>;
+  S p[VEC], c[VEC], sc[VEC], ci[VEC];
+  IO::load_cg(f.seg_prod + (vseg * f.ntt + p_in) * f.W + ch, p);
+  if (cr.rows != nullptr) IO::load_cg(cr.rows + vseg * f.W + ch, c);
+  if (cr.cin != nullptr) {
+    IO::load_cg(cr.scale + vseg * f.W + ch, sc);
+    IO::load_cg(cr.cin + ch, ci);
+  }
   bool nz = false;
-  const S* sp = f.seg_prod + (vseg * f.ntt + p_in) * f.W + ch;
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
-    S p = sp[v];
-    if (scale != nullptr) p = mul_(p, scale[vseg * f.W + ch + v]);
-    e[v] = mul_(p, carry[ch + v]);
+    if (cr.rows == nullptr) c[v] = S(0);
+    if (cr.cin != nullptr) c[v] = fma_(sc[v], ci[v], c[v]);
+    e[v] = mul_(p[v], c[v]);
     nz = nz || e[v] != S(0);
   }
   return nz;
 }
 
 // One tile (chain position p_in of virtual segment vseg, channel column col)
-// of the stitch.  carry[ch] is the carry entering the segment (fwd: state;
-// bwd: lam_E * G_E from above); scale as in entering().
+// of the stitch; cr gives the carry entering the segment (fwd: state; bwd:
+// lam_E * G_E from above).  The tile's rows are
+// loaded together with its entering correction and, for p_next >= 0, the
+// correction entering p_next (*more: non-zero in this thread's channels);
+// returns false (nothing stored) when this position's correction is zero in
+// every channel of the tile.
 template <class S, int VEC, int Q, bool REV, class Sync>
-__device__ __forceinline__ void fixup_position(const FixupArgs<S>& f, int64_t vseg, int64_t col, int64_t p_in,
-                                               const S* __restrict__ carry, const S* __restrict__ scale,
-                                               S (*s_wp)[Q * VEC]) {
+__device__ __forceinline__ bool fixup_position(const FixupArgs<S>& f, int64_t vseg, int64_t col, int64_t p_in,
+                                               const Carries<S>& cr, S (*s_wp)[Q * VEC], int64_t p_next = -1,
+                                               bool* more = nullptr) {
   constexpr int NW = 8, RF = 12, G = 32 / Q, CPW = Q * VEC, NSEG = NW * G, PR = NSEG * RF;  // PR = a TMA tile
   using IO = VecIO<S, VEC>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = lane % Q, g = lane / Q;
+  const int seg = warp * G + g;
   const int64_t W = f.W, T = f.T, rows = f.rows;
-  const int64_t tile_row = vseg * f.tseg + (REV ? f.ntt - 1 - p_in : p_in) * rows;
+  const int64_t t_lo = vseg * f.tseg + (REV ? f.ntt - 1 - p_in : p_in) * rows;
   const int64_t ch = col * CPW + (int64_t)q * VEC;
   const bool valid = ch < W;
   S e[VEC];
 #pragma unroll
   for (int v = 0; v < VEC; ++v) e[v] = S(0);
-  if (valid) entering<S, VEC>(f, vseg, p_in, ch, carry, scale, e);
 
-  const int64_t t_lo = tile_row;
-  const int64_t seg_end = (vseg + 1) * f.tseg < T ? (vseg + 1) * f.tseg : T;
-  const int64_t t_hi = (t_lo + rows < seg_end ? t_lo + rows : seg_end);
+  // the virtual segment's last row + 1 (its top, where the backward decay
+  // mu = lam_{t+1} is replaced by 1 -- or by lam_next at T)
+  const int64_t seg_top = (vseg + 1) * f.tseg < T ? (vseg + 1) * f.tseg : T;
+  const int64_t t_hi = t_lo + rows < seg_top ? t_lo + rows : seg_top;
   const int64_t npass = (rows + PR - 1) / PR;
+  const bool dl = REV && f.out1 != nullptr;
   for (int64_t ps = 0; ps < npass; ++ps) {
+    // this thread's rows: t = t0 + i (forward) / t0 - i (backward), i < RF,
+    // those in [t_lo, t_hi) being i in [ilo, ihi)
     const int64_t pbase = REV ? t_lo + rows - (ps + 1) * PR : t_lo + ps * PR;
-    const int seg = warp * G + g;
+    const int64_t t0 = REV ? pbase + PR - 1 - seg * RF : pbase + seg * RF;
+    int ilo, ihi;
+    if (!REV) {
+      ilo = (int)(t_lo - t0 > 0 ? t_lo - t0 : 0);
+      ihi = (int)(t_hi - t0 < RF ? t_hi - t0 : RF);
+    } else {
+      ilo = (int)(t0 - t_hi + 1 > 0 ? t0 - t_hi + 1 : 0);
+      ihi = (int)(t0 - t_lo + 1 < RF ? t0 - t_lo + 1 : RF);
+    }
+    if (!valid) ihi = 0;
+    const int64_t step = REV ? -W : W;
+    const S* lam_p = f.lam + (t0 + (REV ? 1 : 0)) * W + ch;  // the decay applied at row t0
+    S* out_p = f.out0 + t0 * W + ch;
+    const int itop = REV ? (int)(t0 - (seg_top - 1)) : -1;  // i of the segment's top row
     S m[RF][VEC], o[RF][VEC];
 #pragma unroll
     for (int i = 0; i < RF; ++i) {
-      const int64_t t = REV ? pbase + (PR - 1 - (seg * RF + i)) : pbase + seg * RF + i;
-      const bool in = valid && t >= t_lo && t < t_hi;
 #pragma unroll
       for (int v = 0; v < VEC; ++v) m[i][v] = S(1);
-      if (in) IO::load_cg(f.out0 + t * W + ch, o[i]);  // in flight with the decays
-      if (in) {
-        if (!REV) {
-          IO::load_cg(f.lam + t * W + ch, m[i]);
-        } else if (t + 1 >= T) {
+      if (i >= ilo && i < ihi) {
+        if (!dl) IO::load_cg(out_p + i * step, o[i]);  // in flight with the decays
+        if (!REV || i != itop) {
+          IO::load_cg(lam_p + i * step, m[i]);
+        } else if (seg_top == T) {
 #pragma unroll
           for (int v = 0; v < VEC; ++v) m[i][v] = f.lam_next != nullptr ? f.lam_next[ch + v] : S(0);
-        } else if (f.nseg > 1 && (t + 1) % f.tseg == 0) {
-          // end of a virtual segment: mu = 1 (m already 1)
-        } else {
-          IO::load_cg(f.lam + (t + 1) * W + ch, m[i]);
-        }
+        }  // else the top of an inner virtual segment: mu = 1
+      }
+    }
+    if (ps == 0 && valid) {  // issued behind the tile's loads: one load round
+      entering<S, VEC>(f, vseg, p_in, ch, cr, e);
+      if (p_next >= 0) {
+        S en[VEC];
+        *more = entering<S, VEC>(f, vseg, p_next, ch, cr, en);
       }
     }
     S A[VEC];
@@ -131,7 +168,10 @@ __device__ __forceinline__ void fixup_position(const FixupArgs<S>& f, int64_t vs
         if (g > 0) Ae[v] = ap;
       }
     }
-    Sync::sync();
+    bool nzl = false;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) nzl = nzl || e[v] != S(0);
+    if (!Sync::sync_or(nzl)) return false;  // uniform: the rest of the walk is zero too
     if (g == G - 1) {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) s_wp[warp][q * VEC + v] = A[v];
@@ -145,27 +185,55 @@ __device__ __forceinline__ void fixup_position(const FixupArgs<S>& f, int64_t vs
       for (int v = 0; v < VEC; ++v) ecur[v] = mul_(s_wp[w][q * VEC + v], ecur[v]);
 #pragma unroll
     for (int v = 0; v < VEC; ++v) ecur[v] = mul_(Ae[v], ecur[v]);
+    // m[i] <- the correction of row i
 #pragma unroll
-    for (int i = 0; i < RF; ++i) {
-      const int64_t t = REV ? pbase + (PR - 1 - (seg * RF + i)) : pbase + seg * RF + i;
+    for (int i = 0; i < RF; ++i)
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) ecur[v] = mul_(m[i][v], ecur[v]);
-      if (valid && t >= t_lo && t < t_hi) {
+      for (int v = 0; v < VEC; ++v) {
+        ecur[v] = mul_(m[i][v], ecur[v]);
+        m[i][v] = ecur[v];
+      }
+    if (!dl) {
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) o[i][v] = o[i][v] + ecur[v];
-        IO::store_cg(f.out0 + t * W + ch, o[i]);
-        if (REV && f.out1 != nullptr) {
-          S hp[VEC], d[VEC];
-          if (t >= 1) IO::load_cg(f.h + (t - 1) * W + ch, hp);
-          else {
+      for (int i = 0; i < RF; ++i)
+        if (i >= ilo && i < ihi) {
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) hp[v] = f.hprev_row != nullptr ? f.hprev_row[ch + v] : S(0);
-          }
-          IO::load_cg(f.out1 + t * W + ch, d);
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) d[v] = fma_(hp[v], ecur[v], d[v]);
-          IO::store_cg(f.out1 + t * W + ch, d);
+          for (int v = 0; v < VEC; ++v) o[i][v] = o[i][v] + m[i][v];
+          IO::store_cg(out_p + i * step, o[i]);
         }
+    } else {
+      // backward with dlam: dx, dlam and h_{t-1} of CH rows per load round
+      // (loads ahead of the stores, which may alias them)
+      constexpr int CH = 6;
+      S* d_p = f.out1 + t0 * W + ch;
+      const S* h_p = f.h + (t0 - 1) * W + ch;
+      const int izero = (int)t0;  // i of row 0 (h_{-1} = hprev_row)
+#pragma unroll
+      for (int c = 0; c < RF; c += CH) {
+        S oc[CH][VEC], hp[CH][VEC], d[CH][VEC];
+#pragma unroll
+        for (int i = 0; i < CH; ++i)
+          if (c + i >= ilo && c + i < ihi) {
+            IO::load_cg(out_p + (c + i) * step, oc[i]);
+            IO::load_cg(d_p + (c + i) * step, d[i]);
+            if (c + i != izero) {
+              IO::load_cg(h_p + (c + i) * step, hp[i]);
+            } else {
+#pragma unroll
+              for (int v = 0; v < VEC; ++v) hp[i][v] = f.hprev_row != nullptr ? f.hprev_row[ch + v] : S(0);
+            }
+          }
+#pragma unroll
+        for (int i = 0; i < CH; ++i)
+          if (c + i >= ilo && c + i < ihi) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+              oc[i][v] = oc[i][v] + m[c + i][v];
+              d[i][v] = fma_(hp[i][v], m[c + i][v], d[i][v]);
+            }
+            IO::store_cg(out_p + (c + i) * step, oc[i]);
+            IO::store_cg(d_p + (c + i) * step, d[i]);
+          }
       }
     }
 #pragma unroll
@@ -176,39 +244,29 @@ __device__ __forceinline__ void fixup_position(const FixupArgs<S>& f, int64_t vs
     }
   }
   Sync::sync();  // s_wp is reused by the next position
+  return true;
 }
 
-// Fix-up of chain (vseg, col) by walker j of J: rounds of 8 positions, warp w
-// checking position base + w; walker j then fixes the positions p = j mod J
-// of the non-zero prefix.  s_flag: 8 ints of shared memory.
+// Fix-up of chain (vseg, col) by walker j of J: positions p_lo + j, + J, ...
+// in order, each tile loaded together with the entering correction of the
+// walker's next position (one load round per position); the walk stops at
+// the first position whose correction is zero in every channel.
 template <class S, int VEC, int Q, bool REV, class Sync>
 __device__ __forceinline__ void fixup_chain(const FixupArgs<S>& f, int64_t vseg, int64_t col, int j, int J,
-                                            const S* __restrict__ carry, const S* __restrict__ scale,
-                                            S (*s_wp)[Q * VEC], int* s_flag) {
-  constexpr int NW = 8, CPW = Q * VEC;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                                            const Carries<S>& cr, S (*s_wp)[Q * VEC]) {
+  constexpr int CPW = Q * VEC;
+  const int lane = threadIdx.x & 31;
   const int64_t ch = col * CPW + (int64_t)(lane % Q) * VEC;
   // positions holding rows < T: the last virtual segment is usually short,
   // and its tiles past T (decay 1, nothing to fix) would keep the walk going
   const int64_t seg_rows = (vseg + 1) * f.tseg < f.T ? f.tseg : f.T - vseg * f.tseg;
   const int64_t nreal = seg_rows > 0 ? (seg_rows + f.rows - 1) / f.rows : 0;
   const int64_t p_lo = REV ? f.ntt - nreal : 0, p_hi = REV ? f.ntt : nreal;
-  for (int64_t base = p_lo; base < p_hi; base += NW) {
-    const int64_t p = base + warp;
-    bool nz = false;
-    if (p < p_hi && ch < f.W) {
-      S e[VEC];
-      nz = entering<S, VEC>(f, vseg, p, ch, carry, scale, e);
-    }
-    nz = __any_sync(0xffffffffu, nz);
-    if (lane == 0) s_flag[warp] = nz ? 1 : 0;
-    Sync::sync();
-    int n = 0;
-    while (n < NW && s_flag[n]) ++n;
-    Sync::sync();  // flags read before the next round rewrites them
-    for (int k = 0; k < n; ++k)
-      if ((base + k - p_lo) % J == j) fixup_position<S, VEC, Q, REV, Sync>(f, vseg, col, base + k, carry, scale, s_wp);
-    if (n < NW) return;
+  for (int64_t p = p_lo + j; p < p_hi; p += J) {
+    bool more = false;
+    if (!fixup_position<S, VEC, Q, REV, Sync>(f, vseg, col, p, cr, s_wp, p + J < p_hi ? p + J : -1, &more))
+      return;
+    if (!Sync::sync_or(more)) return;
   }
 }
 

@@ -111,7 +111,7 @@ cudaError_t launch_ws_init(void* ctrl, cudaStream_t st);
 // relative products).
 template <class S>
 cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S* h, const S* lam_next,
-                         const S* seg_prod, const S* carry, int64_t carry_stride, const S* scale, S* out0, S* out1,
+                         const S* seg_prod, const S* carry_rows, const S* scale_rows, const S* cin, S* out0, S* out1,
                          int64_t T, int64_t W, int64_t rows, int64_t nseg, int64_t tseg, int64_t ntt,
                          bool vec_ok, cudaStream_t st);
 template <class S>

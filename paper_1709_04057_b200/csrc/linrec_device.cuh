@@ -30,6 +30,12 @@ struct VecIO<float, 4> {
   static __device__ __forceinline__ void store_cg(float* p, const float (&v)[4]) {
     __stcg(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
   }
+  // store with an L2 eviction-priority policy (createpolicy)
+  static __device__ __forceinline__ void store_hint(float* p, const float (&v)[4], uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3]), "l"(pol)
+                 : "memory");
+  }
 };
 
 template <>
@@ -47,6 +53,10 @@ struct VecIO<double, 2> {
   }
   static __device__ __forceinline__ void store_cg(double* p, const double (&v)[2]) {
     __stcg(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
+  }
+  static __device__ __forceinline__ void store_hint(double* p, const double (&v)[2], uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v[0]), "d"(v[1]), "l"(pol)
+                 : "memory");
   }
 };
 

@@ -176,7 +176,7 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
     if (lane == 0) {
       prefetch_tmap(&map_lam);
       prefetch_tmap(&map_x);
-      const uint64_t pol = policy_evict_first();
+      const uint64_t pol = policy_evict_first(), pol_keep = policy_evict_last();
       for (int n = 0;; ++n) {
         const int s = n % STAGES;
         if (n >= STAGES) mbar_wait(sm.empty(s), ((n / STAGES) + 1) & 1);
@@ -190,10 +190,12 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
         const ChainPos cp = chain_pos(a, (int64_t)k);
         const int c0 = (int)(cp.col * CPW);
         const int r0 = (int)tile_row0<false>(a, cp, L);
+        const bool keep = a.seg_prod != nullptr && cp.pos < kKeepPositions;  // revisited by the fix-up
         mbar_arrive_expect_tx(sm.full(s), Cfg::TX_BYTES);
 #pragma unroll
         for (int b = 0; b < Cfg::NBOX; ++b) {
-          tma_load_2d(sm.arr(s, 0) + b * Cfg::BOX_ROWS * CPW, &map_lam, c0, r0 + b * Cfg::BOX_ROWS, sm.full(s), pol);
+          tma_load_2d(sm.arr(s, 0) + b * Cfg::BOX_ROWS * CPW, &map_lam, c0, r0 + b * Cfg::BOX_ROWS, sm.full(s),
+                      keep ? pol_keep : pol);
           tma_load_2d(sm.arr(s, 1) + b * Cfg::BOX_ROWS * CPW, &map_x, c0, r0 + b * Cfg::BOX_ROWS, sm.full(s), pol);
         }
       }
@@ -206,6 +208,7 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
   }
 
   // ---------------------------------- consumers
+  const uint64_t pol_keep = policy_evict_last();
   const int q = lane % Q, g = lane / Q;
   const int seg = warp * G + g;
   const int64_t W = a.W;
@@ -215,6 +218,7 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
     const long long k = sm.meta()[s];
     if (k < 0) break;
     const ChainPos cp = chain_pos(a, (int64_t)k);
+    const bool keep = a.seg_prod != nullptr && cp.pos < kKeepPositions;
     const int64_t ch = cp.col * CPW + (int64_t)q * VEC;
     const bool valid = ch < W;
     const int t0 = tile_row0<false>(a, cp, L) + seg * R;
@@ -293,7 +297,10 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
 #pragma unroll
       for (int v = 0; v < VEC; ++v) cs[v] = fma_(l[i][v], cs[v], xv[i][v]);
       const int t = t0 + i;
-      if (valid && t < Ti) IO::store_stream(a.out0 + t * W + ch, cs);
+      if (valid && t < Ti) {
+        if (keep) IO::store_hint(a.out0 + t * W + ch, cs, pol_keep);
+        else IO::store_stream(a.out0 + t * W + ch, cs);
+      }
     }
   }
 }
@@ -320,7 +327,7 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
       prefetch_tmap(&map_lam);
       prefetch_tmap(&map_dh);
       prefetch_tmap(&map_h);
-      const uint64_t pol = policy_evict_first();
+      const uint64_t pol = policy_evict_first(), pol_keep = policy_evict_last();
       for (int n = 0;; ++n) {
         const int s = n % STAGES;
         if (n >= STAGES) mbar_wait(sm.empty(s), ((n / STAGES) + 1) & 1);
@@ -334,13 +341,16 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
         const ChainPos cp = chain_pos(a, (int64_t)k);
         const int c0 = (int)(cp.col * CPW);
         const int r0 = (int)tile_row0<true>(a, cp, L);
+        const bool keep = a.seg_prod != nullptr && cp.pos < kKeepPositions;  // revisited by the fix-up
         mbar_arrive_expect_tx(sm.full(s), Cfg::TX_BYTES);
 #pragma unroll
         for (int b = 0; b < Cfg::NBOX; ++b) {
           const int rb = r0 + b * Cfg::BOX_ROWS;
-          tma_load_2d(sm.arr(s, 0) + b * Cfg::BOX_ROWS * CPW, &map_lam, c0, rb + 1, sm.full(s), pol);
+          tma_load_2d(sm.arr(s, 0) + b * Cfg::BOX_ROWS * CPW, &map_lam, c0, rb + 1, sm.full(s),
+                      keep ? pol_keep : pol);
           tma_load_2d(sm.arr(s, 1) + b * Cfg::BOX_ROWS * CPW, &map_dh, c0, rb, sm.full(s), pol);
-          tma_load_2d(sm.arr(s, 2) + b * Cfg::BOX_ROWS * CPW, &map_h, c0, rb - 1, sm.full(s), pol);
+          tma_load_2d(sm.arr(s, 2) + b * Cfg::BOX_ROWS * CPW, &map_h, c0, rb - 1, sm.full(s),
+                      keep ? pol_keep : pol);
         }
       }
     }
@@ -352,6 +362,7 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
   }
 
   // ---------------------------------- consumers
+  const uint64_t pol_keep = policy_evict_last();
   const int q = lane % Q, g = lane / Q;
   const int seg = warp * G + g;
   const int64_t W = a.W, T = a.T;
@@ -361,6 +372,7 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
     const long long k = sm.meta()[s];
     if (k < 0) break;
     const ChainPos cp = chain_pos(a, (int64_t)k);
+    const bool keep = a.seg_prod != nullptr && cp.pos < kKeepPositions;
     const int64_t ch = cp.col * CPW + (int64_t)q * VEC;
     const bool valid = ch < W;
     const int t0 = tile_row0<true>(a, cp, L) + seg * R;
@@ -462,8 +474,13 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
       }
       const int t = t0 + i;
       if (valid && t < Ti) {
-        IO::store_stream(a.out0 + t * W + ch, cs);
-        if (a.out1 != nullptr) IO::store_stream(a.out1 + t * W + ch, dl);
+        if (keep) {
+          IO::store_hint(a.out0 + t * W + ch, cs, pol_keep);
+          if (a.out1 != nullptr) IO::store_hint(a.out1 + t * W + ch, dl, pol_keep);
+        } else {
+          IO::store_stream(a.out0 + t * W + ch, cs);
+          if (a.out1 != nullptr) IO::store_stream(a.out1 + t * W + ch, dl);
+        }
         if (t == 0 && a.out2 != nullptr) {
           S l0[VEC], d0[VEC];
           IO::load_cg(a.a + ch, l0);

@@ -25,15 +25,13 @@ namespace linrec_dev {
 // CTA j of the J walkers of chain (virtual segment, channel column):
 // fixup_chain (fixup_impl.cuh), 8 warps.
 template <class S, int VEC, int Q, bool REV>
-__global__ void __launch_bounds__(256, 2)
-k_fixup(FixupArgs<S> f, const S* __restrict__ carry, int64_t carry_stride, const S* __restrict__ scale,
-        int64_t ncols, int walkers) {
+__global__ void __launch_bounds__(256, REV ? 1 : 2)  // backward: dx, dlam, h rows in flight
+k_fixup(FixupArgs<S> f, Carries<S> cr, int64_t ncols, int walkers) {
   __shared__ S s_wp[8][Q * VEC];
-  __shared__ int s_flag[8];
   const int64_t col = blockIdx.x % ncols;
   const int j = (int)((blockIdx.x / ncols) % walkers);
   const int64_t vseg = (blockIdx.x / ncols) / walkers;
-  fixup_chain<S, VEC, Q, REV, CtaSync>(f, vseg, col, j, walkers, carry + vseg * carry_stride, scale, s_wp, s_flag);
+  fixup_chain<S, VEC, Q, REV, CtaSync>(f, vseg, col, j, walkers, cr, s_wp);
 }
 
 // out[j] = fold over q in [first, last) by `step` of c = A_q[j] * c + B_q[j],
@@ -67,7 +65,7 @@ namespace linrec_impl {
 
 template <class S>
 cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S* h, const S* lam_next,
-                         const S* seg_prod, const S* carry, int64_t carry_stride, const S* scale, S* out0, S* out1,
+                         const S* seg_prod, const S* carry_rows, const S* scale_rows, const S* cin, S* out0, S* out1,
                          int64_t T, int64_t W, int64_t rows, int64_t nseg, int64_t tseg, int64_t ntt,
                          bool vec_ok, cudaStream_t st) {
   constexpr int V = Tuning<S>::VEC;
@@ -78,11 +76,12 @@ cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S
   const int walk = fixup_walkers();
   const dim3 grid((unsigned)(ncols * nseg * walk));
   const linrec_dev::FixupArgs<S> fa{lam, hprev_row, h, lam_next, seg_prod, out0, out1, T, W, rows, nseg, tseg, ntt};
+  const linrec_dev::Carries<S> cr{carry_rows, scale_rows, cin};
 #define FIX(VV)                                                                                       \
   LINREC_Q_SWITCH(q, if (reverse) linrec_dev::k_fixup<S, VV, Q_, true><<<grid, 256, 0, st>>>(         \
-                         fa, carry, carry_stride, scale, ncols, walk);                                \
+                         fa, cr, ncols, walk);                                \
                      else linrec_dev::k_fixup<S, VV, Q_, false><<<grid, 256, 0, st>>>(                \
-                         fa, carry, carry_stride, scale, ncols, walk));
+                         fa, cr, ncols, walk));
   if (vec_ok) {
     FIX(V)
   } else {
@@ -114,10 +113,11 @@ cudaError_t launch_compose(const S* aggs, int64_t first, int64_t last, int64_t s
 }
 
 template cudaError_t launch_fixup<float>(bool, const float*, const float*, const float*, const float*, const float*,
-                                         const float*, int64_t, const float*, float*, float*, int64_t, int64_t,
+                                         const float*, const float*, const float*, float*, float*, int64_t, int64_t,
                                          int64_t, int64_t, int64_t, int64_t, bool, cudaStream_t);
 template cudaError_t launch_fixup<double>(bool, const double*, const double*, const double*, const double*,
-                                          const double*, const double*, int64_t, const double*, double*, double*,
+                                          const double*, const double*, const double*, const double*, double*,
+                                          double*,
                                           int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, bool, cudaStream_t);
 template cudaError_t launch_compose<float>(const float*, int64_t, int64_t, int64_t, const float*, float*,
                                            int64_t, cudaStream_t);

@@ -79,6 +79,16 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 
+// Tiles the stitch fix-up will revisit (the first chain positions of every
+// segment) are loaded and stored with L2 evict_last so that the fix-up, which
+// runs right after the scan, finds them in L2 instead of DRAM.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+constexpr int kKeepPositions = 2;
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }

@@ -85,12 +85,12 @@ class CudaBackend:
         capi.compose_carries(aggs.data_ptr(), first, last, step, self._p(seed), out.data_ptr(), W, 4, self._st())
 
     def fixup(self, lam, h, seg_prod, c_in, T, W, rows):
-        capi.segment_fixup(lam.data_ptr(), h.data_ptr(), seg_prod.data_ptr(), c_in.data_ptr(), T, W, rows, 4,
+        capi.segment_fixup(lam.data_ptr(), h.data_ptr(), seg_prod.data_ptr(), self._p(c_in), T, W, rows, 4,
                            self._st())
 
     def fixup_backward(self, lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T, W, rows):
         capi.segment_fixup_backward(lam.data_ptr(), self._p(hprev), h.data_ptr(), self._p(lam_next),
-                                    seg_prod.data_ptr(), y_in.data_ptr(), dlam.data_ptr(), dx.data_ptr(), T, W,
+                                    seg_prod.data_ptr(), self._p(y_in), dlam.data_ptr(), dx.data_ptr(), T, W,
                                     rows, 4, self._st())
 
 
@@ -245,8 +245,9 @@ class SequenceShardedScan:
             self._all_gather(self.agg, self.aggs)
             if r > 0:
                 self.be.compose(self.aggs, 0, r, 1, None, self.c_in, W)
+        # always: the fix-up also stitches the segment's own virtual segments
+        self.be.fixup(lam, h, self.seg_prod_f, self.c_in if r > 0 else None, T, W, self.rows_f)
         if r > 0:
-            self.be.fixup(lam, h, self.seg_prod_f, self.c_in, T, W, self.rows_f)
             self.hprev = self.c_in
         else:
             self.hprev = h0 if h0 is not None else self.zeros
@@ -278,11 +279,10 @@ class SequenceShardedScan:
             self._all_gather(self.agg, self.aggs)
             if r < R - 1:
                 self.be.compose(self.aggs, R - 1, r, -1, None, self.y_in, W)
-        if r < R - 1:
-            self.be.fixup_backward(lam, hprev, h, lam_next, self.seg_prod_b, self.y_in, dlam, dx, T, W,
-                                   self.rows_b)
-        else:
+        if r == R - 1:
             self.y_in.zero_()
+        self.be.fixup_backward(lam, hprev, h, lam_next, self.seg_prod_b, self.y_in if r < R - 1 else None, dlam, dx,
+                               T, W, self.rows_b)
         if r == 0 and dh0 is not None:
             # own aggregate only: the local fold of the all-gather path
             self.aggs[0].copy_(self.agg)

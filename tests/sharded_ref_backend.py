@@ -69,6 +69,8 @@ class RefBackend:
         _np(out).reshape(W)[:] = c
 
     def fixup(self, lam, h, seg_prod, c_in, T, W, rows):
+        if c_in is None:  # the scan above is complete: nothing pending without a carry
+            return
         L, H, SP, c = _np(lam).reshape(T, W), _np(h).reshape(T, W), _np(seg_prod), _np(c_in).reshape(W)
         for tile in range(-(-T // rows)):
             e = SP[tile] * c
@@ -77,6 +79,8 @@ class RefBackend:
                 H[t] += e
 
     def fixup_backward(self, lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T, W, rows):
+        if y_in is None:
+            return
         L, H, SP = _np(lam).reshape(T, W), _np(h).reshape(T, W), _np(seg_prod)
         DL, DX, y = _np(dlam).reshape(T, W), _np(dx).reshape(T, W), _np(y_in).reshape(W)
         hp = np.zeros(W) if hprev is None else _np(hprev).reshape(W)

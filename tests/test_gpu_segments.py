@@ -48,11 +48,12 @@ def emulate(lam, x, h0, dh, R):
                           sp_f[r].data_ptr(), aggs[r].data_ptr(), e - s, W, 4, None, st)
     aggs[0, 0].zero_()
     c_in = [h0] + [torch.empty(W, device=dev) for _ in range(1, R)]
-    for r in range(1, R):
+    for r in range(R):  # every rank: the fix-up also stitches its own virtual segments
         s, e = segs[r]
-        capi.compose_carries(aggs.data_ptr(), 0, r, 1, None, c_in[r].data_ptr(), W, 4, st)
-        capi.segment_fixup(lam[s].data_ptr(), h[s].data_ptr(), sp_f[r].data_ptr(), c_in[r].data_ptr(), e - s, W,
-                           rows_f[r], 4, st)
+        if r > 0:
+            capi.compose_carries(aggs.data_ptr(), 0, r, 1, None, c_in[r].data_ptr(), W, 4, st)
+        capi.segment_fixup(lam[s].data_ptr(), h[s].data_ptr(), sp_f[r].data_ptr(),
+                           c_in[r].data_ptr() if r > 0 else None, e - s, W, rows_f[r], 4, st)
     # backward
     ones = torch.ones(W, device=dev)
     dh0_loc = [torch.empty(W, device=dev) for _ in range(R)]
@@ -65,14 +66,16 @@ def emulate(lam, x, h0, dh, R):
                                    None, st)
     y0 = torch.zeros(W, device=dev)
     for r, (s, e) in enumerate(segs):
-        if r == R - 1:
-            continue
-        y = torch.empty(W, device=dev)
-        capi.compose_carries(baggs.data_ptr(), R - 1, r, -1, None, y.data_ptr(), W, 4, st)
-        if r == 0:
-            y0 = y
-        capi.segment_fixup_backward(lam[s].data_ptr(), c_in[r].data_ptr(), h[s].data_ptr(), ones.data_ptr(),
-                                    sp_b[r].data_ptr(), y.data_ptr(), dlam[s].data_ptr(), dx[s].data_ptr(), e - s,
+        y = None
+        if r < R - 1:
+            y = torch.empty(W, device=dev)
+            capi.compose_carries(baggs.data_ptr(), R - 1, r, -1, None, y.data_ptr(), W, 4, st)
+            if r == 0:
+                y0 = y
+        ln = ones if r < R - 1 else None
+        capi.segment_fixup_backward(lam[s].data_ptr(), c_in[r].data_ptr(), h[s].data_ptr(),
+                                    None if ln is None else ln.data_ptr(), sp_b[r].data_ptr(),
+                                    None if y is None else y.data_ptr(), dlam[s].data_ptr(), dx[s].data_ptr(), e - s,
                                     W, rows_b[r], 4, st)
     capi.compose_carries(baggs.data_ptr(), 0, 1, 1, y0.data_ptr(), dh0.data_ptr(), W, 4, st)
     torch.cuda.synchronize()
