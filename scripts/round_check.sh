@@ -21,5 +21,5 @@ timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -c 600 --
   python bench.py --workload c3 --steps 1 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_tma -s 4 -c 2 -o $O/full_c2 -f \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > $O/full_c2.log 2>&1
-timeout 900 python scripts/bench_model.py > $O/bench_model.json 2> $O/bench_model.err
+timeout 900 python scripts/bench_model.py --out $O/bench_model_r01.json > $O/bench_model.log 2>&1
 tail -3 $O/pytest_gpu.log; tail -2 $O/smoke.log
