@@ -196,6 +196,18 @@ linrec_workspace* default_ws(int device, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // device-pointer scans
 // ---------------------------------------------------------------------------
+// Parallel mode runs the per-channel kernel when the channels alone fill the
+// GPU (>= 2^17 threads of VEC channels: ~900 per SM) and the sequence is short
+// (T <= 2048): the time-chained scan has nothing to add there, and its
+// 96-row tiles are mostly padding at small T (bench_model's T=16, b=4096:
+// 112 -> 27 us per forward scan).  LINREC_CHANNEL_PARALLEL=0 disables it.
+template <class S>
+bool channel_parallel_enough(int64_t T, int64_t W, bool vok) {
+  static const bool on = linrec_impl::env_int("LINREC_CHANNEL_PARALLEL", 1) != 0;
+  const int64_t threads = vok ? W / vec_of<S>() : W;
+  return on && T <= 2048 && threads >= (int64_t(1) << 17);
+}
+
 template <class S>
 int scan_device(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W, int mode,
                 linrec_workspace_t ws, cudaStream_t st) {
@@ -205,7 +217,7 @@ int scan_device(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t 
     return rc;
   const bool vok = vec_ok<S>(W, {lam, x, h0, h});
   FwdCall<S> c{lam, x, h0, h, T, W};
-  if (mode == LINREC_SERIAL) {
+  if (mode == LINREC_SERIAL || channel_parallel_enough<S>(T, W, vok)) {
     LINREC_CUDA_TRY(linrec_impl::launch_serial_fwd<S>(c, vok, st));
     return LINREC_OK;
   }
@@ -247,7 +259,7 @@ int scan_backward_device(const S* lam, const S* h0, const S* h, const S* dh, con
     return rc;
   const bool vok = vec_ok<S>(W, {lam, h0, h, dh, lam_next, g_next, dlam, dx, dh0});
   BwdCall<S> c{lam, h0, h, dh, lam_next, g_next, dlam, dx, dh0, T, W};
-  if (mode == LINREC_SERIAL) {
+  if (mode == LINREC_SERIAL || channel_parallel_enough<S>(T, W, vok)) {
     LINREC_CUDA_TRY(linrec_impl::launch_serial_bwd<S>(c, vok, st));
     return LINREC_OK;
   }
