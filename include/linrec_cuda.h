@@ -238,6 +238,39 @@ int linrec_segment_fixup_backward_f64(const double* lam, const double* hprev, co
                                       double* dlam, double* dx, int64_t T, int64_t W, int64_t tile_rows,
                                       void* stream);
 
+/* The same steps with the carry exchange fused into the stitch kernels over
+ * peer memory (the mailboxes of linrec_ipc_alloc / linrec_p2p_mailbox_bytes
+ * below): the scan's virtual-segment fold stores this rank's aggregate
+ * straight into the consumers' mailboxes and releases their flags; the
+ * fix-up acquires the sources' flags, folds their aggregates into the
+ * incoming carry in-kernel (also written to c_in / y_in when non-NULL) and
+ * acknowledges them -- no all-gather and no compose launch.  fp32.
+ * Forward: consumers = ranks r+1..R-1, sources = 0..r-1 (step 1), zero_a on
+ * rank 0; backward: consumers = 0..r-1, sources = R-1..r+1 (step -1).  Every
+ * rank calls every step (empty ranges are fine); epoch advances by one per
+ * step and direction. */
+typedef struct {
+  void* const* mboxes;  /* DEVICE array [world] of every rank's mailbox, mapped in this process */
+  int world, rank;
+  uint64_t epoch;
+  int consumers_first, consumers_last;             /* [first, last) */
+  int sources_first, sources_last, sources_step;   /* first, first+step, ... != last */
+  int zero_a;                                      /* publish A = 0 */
+} linrec_exchange_t;
+int linrec_segment_scan_exchange_f32(const float* lam, const float* x, const float* h0, float* h, float* seg_prod,
+                                     float* agg, int64_t T, int64_t W, const linrec_exchange_t* ex,
+                                     linrec_workspace_t ws, void* stream);
+int linrec_segment_scan_backward_exchange_f32(const float* lam, const float* hprev, const float* h, const float* dh,
+                                              const float* lam_next, float* dlam, float* dx, float* dh0,
+                                              float* seg_prod, float* agg, int64_t T, int64_t W,
+                                              const linrec_exchange_t* ex, linrec_workspace_t ws, void* stream);
+int linrec_segment_fixup_exchange_f32(const float* lam, float* h, const float* seg_prod, float* c_in, int64_t T,
+                                      int64_t W, int64_t tile_rows, const linrec_exchange_t* ex, void* stream);
+int linrec_segment_fixup_backward_exchange_f32(const float* lam, const float* hprev, const float* h,
+                                               const float* lam_next, const float* seg_prod, float* y_in,
+                                               float* dlam, float* dx, int64_t T, int64_t W, int64_t tile_rows,
+                                               const linrec_exchange_t* ex, void* stream);
+
 /* ---- layer building block: tcgen05 GEMM ---------------------------------- *
  * C[M][N] (row-major, pitch ldc) (+)= sum_k A(m,k) * B(n,k) on the sm_100a
  * tensor cores (kind::tf32 MMAs, fp32 accumulate in TMEM).  A is K-major

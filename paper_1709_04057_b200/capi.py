@@ -28,6 +28,13 @@ _i64 = C.c_int64
 _int = C.c_int
 
 
+class Exchange(C.Structure):
+    """linrec_exchange_t: one direction of the fused peer-memory carry exchange."""
+    _fields_ = [("mboxes", _vp), ("world", _int), ("rank", _int), ("epoch", C.c_uint64),
+                ("consumers_first", _int), ("consumers_last", _int),
+                ("sources_first", _int), ("sources_last", _int), ("sources_step", _int), ("zero_a", _int)]
+
+
 class LinrecError(RuntimeError):
     """A non-zero linrec_status; ``code`` is the status."""
 
@@ -76,6 +83,11 @@ def _load():
     lib.linrec_p2p_publish_f32.argtypes = [_vp, _i64, _int, _int, _int, C.c_uint64, _vp, _int, _int, _vp]
     lib.linrec_p2p_compose_f32.argtypes = [_i64, _int, _int, _int, C.c_uint64, _vp, _vp, _i64, _i64, _i64, _vp,
                                            _vp, _vp]
+    _ex = C.POINTER(Exchange)
+    lib.linrec_segment_scan_exchange_f32.argtypes = [_vp] * 6 + [_i64, _i64, _ex, _vp, _vp]
+    lib.linrec_segment_scan_backward_exchange_f32.argtypes = [_vp] * 10 + [_i64, _i64, _ex, _vp, _vp]
+    lib.linrec_segment_fixup_exchange_f32.argtypes = [_vp] * 4 + [_i64, _i64, _i64, _ex, _vp]
+    lib.linrec_segment_fixup_backward_exchange_f32.argtypes = [_vp] * 8 + [_i64, _i64, _i64, _ex, _vp]
     lib.linrec_gemm_scratch_bytes.restype = C.c_size_t
     lib.linrec_gemm_scratch_bytes.argtypes = [_i64, _i64, _int]
     lib.linrec_segment_prod_rows.restype = _i64
@@ -177,6 +189,27 @@ def segment_fixup_backward(lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T,
                            stream=0):
     check(getattr(lib, f"linrec_segment_fixup_backward_{_sfx(dtype_bytes)}")(
         lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T, W, tile_rows, stream))
+
+
+# the same with the carry exchange fused into the stitch kernels (fp32; ex: Exchange)
+def segment_scan_exchange(lam, x, h0, h, seg_prod, agg, T, W, ex, ws=None, stream=0):
+    check(lib.linrec_segment_scan_exchange_f32(lam, x, h0, h, seg_prod, agg, T, W, C.byref(ex), ws, stream))
+
+
+def segment_scan_backward_exchange(lam, hprev, h, dh, lam_next, dlam, dx, dh0, seg_prod, agg, T, W, ex, ws=None,
+                                   stream=0):
+    check(lib.linrec_segment_scan_backward_exchange_f32(lam, hprev, h, dh, lam_next, dlam, dx, dh0, seg_prod, agg,
+                                                        T, W, C.byref(ex), ws, stream))
+
+
+def segment_fixup_exchange(lam, h, seg_prod, c_in, T, W, tile_rows, ex, stream=0):
+    check(lib.linrec_segment_fixup_exchange_f32(lam, h, seg_prod, c_in, T, W, tile_rows, C.byref(ex), stream))
+
+
+def segment_fixup_backward_exchange(lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T, W, tile_rows, ex,
+                                    stream=0):
+    check(lib.linrec_segment_fixup_backward_exchange_f32(lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T, W,
+                                                         tile_rows, C.byref(ex), stream))
 
 
 PREC_FP32 = 0

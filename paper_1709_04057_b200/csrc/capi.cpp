@@ -512,9 +512,42 @@ P seg_carry_rows(P seg_prod, const ChainPlan& p, int64_t W) {
   return seg_prod + p.nseg * (p.ntt + 1) * W;
 }
 
+// linrec_exchange_t -> the internal descriptor of one direction (p2p_impl.cuh)
+int to_exchange(const linrec_exchange_t* e, int64_t W, int dir, bool publish, bool compose,
+                linrec_impl::Exchange* out) {
+  if (!e || !e->mboxes || e->world < 1 || e->rank < 0 || e->rank >= e->world || e->epoch < 1)
+    return fail(LINREC_ERR_VALUE, "exchange: mboxes, world, rank and epoch >= 1 required");
+  const int f = e->sources_first, l = e->sources_last, s = e->sources_step;
+  if (e->consumers_first < 0 || e->consumers_last > e->world || (s != 1 && s != -1) ||
+      (f != l && (s == 1 ? f > l : f < l)) || l < -1 || l > e->world)
+    return fail(LINREC_ERR_VALUE, "exchange: consumer / source ranges out of [0, world) or step not +-1");
+  for (int q = e->sources_first; q != e->sources_last; q += e->sources_step)
+    if (q < 0 || q >= e->world || q == e->rank)
+      return fail(LINREC_ERR_VALUE, "exchange: sources must be other ranks in [0, world)");
+  linrec_impl::Exchange x;
+  x.mboxes = e->mboxes;
+  x.W = W;
+  x.world = e->world;
+  x.rank = e->rank;
+  x.dir = dir;
+  x.epoch = (unsigned long long)e->epoch;
+  if (publish) {
+    x.q0 = e->consumers_first;
+    x.q1 = e->consumers_last;
+    x.zero_a = e->zero_a;
+  }
+  if (compose) {
+    x.first = e->sources_first;
+    x.last = e->sources_last;
+    x.step = e->sources_step;
+  }
+  *out = x;
+  return LINREC_OK;
+}
+
 template <class S>
 int segment_scan(const S* lam, const S* x, const S* h0, S* h, S* seg_prod, S* agg, int64_t T, int64_t W,
-                 linrec_workspace_t ws, cudaStream_t st) {
+                 linrec_workspace_t ws, cudaStream_t st, const linrec_impl::Exchange* ex = nullptr) {
   int rc;
   if ((rc = check_dims(T, W)) || (rc = check_ptr(lam, "decays")) || (rc = check_ptr(x, "impulses")) ||
       (rc = check_ptr(h, "h")) || (rc = check_ptr(seg_prod, "seg_prod")) || (rc = check_ptr(agg, "agg")))
@@ -535,15 +568,16 @@ int segment_scan(const S* lam, const S* x, const S* h0, S* h, S* seg_prod, S* ag
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_fwd<S>(p, c, ws_ptrs(w, p), st));
   // the segment-level aggregate, and the virtual segments' scale and own
   // carry rows (seg_prod's tail) for the fix-up, which applies both at once
+  // (with an exchange, also stored straight into the consumers' mailboxes)
   LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, vs.vagg, p.nseg, p.tseg, seg_carry_rows(seg_prod, p, W),
-                                                       seg_scale_rows(seg_prod, p, W), agg, nullptr, W, st));
+                                                       seg_scale_rows(seg_prod, p, W), agg, nullptr, W, st, ex));
   return LINREC_OK;
 }
 
 template <class S>
 int segment_scan_backward(const S* lam, const S* hprev, const S* h, const S* dh, const S* lam_next, S* dlam,
                           S* dx, S* dh0, S* seg_prod, S* agg, int64_t T, int64_t W, linrec_workspace_t ws,
-                          cudaStream_t st) {
+                          cudaStream_t st, const linrec_impl::Exchange* ex = nullptr) {
   int rc;
   if ((rc = check_dims(T, W)) || (rc = check_ptr(lam, "decays")) || (rc = check_ptr(h, "h")) ||
       (rc = check_ptr(dh, "d_h")) || (rc = check_ptr(dlam, "d_decays")) || (rc = check_ptr(dx, "d_impulses")) ||
@@ -565,13 +599,14 @@ int segment_scan_backward(const S* lam, const S* hprev, const S* h, const S* dh,
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_bwd<S>(p, c, ws_ptrs(w, p), st));
   // (A', B') of the segment for the exchange, dh0 = lam_S * G_S, fix-up
   LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, vs.vagg, p.nseg, p.tseg, seg_carry_rows(seg_prod, p, W),
-                                                       seg_scale_rows(seg_prod, p, W), agg, dh0, W, st));
+                                                       seg_scale_rows(seg_prod, p, W), agg, dh0, W, st, ex));
   return LINREC_OK;
 }
 
 template <class S>
 int segment_fixup(bool reverse, const S* lam, const S* hprev, const S* h, const S* lam_next, const S* seg_prod,
-                  const S* carry, S* out0, S* out1, int64_t T, int64_t W, int64_t rows, cudaStream_t st) {
+                  const S* carry, S* out0, S* out1, int64_t T, int64_t W, int64_t rows, cudaStream_t st,
+                  const linrec_impl::Exchange* ex = nullptr, S* c_out = nullptr) {
   int rc;
   if ((rc = check_dims(T, W)) || (rc = check_ptr(lam, "decays")) || (rc = check_ptr(seg_prod, "seg_prod")) ||
       (rc = check_ptr(out0, "out")))
@@ -584,7 +619,7 @@ int segment_fixup(bool reverse, const S* lam, const S* hprev, const S* h, const 
   if (p.rows != rows) return fail(LINREC_ERR_VALUE, "tile_rows does not match the segment scan's plan");
   LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(reverse, lam, hprev, h, lam_next, seg_prod,
                                                seg_carry_rows(seg_prod, p, W), seg_scale_rows(seg_prod, p, W), carry,
-                                               out0, out1, T, W, rows, p.nseg, p.tseg, p.ntt, v, st));
+                                               out0, out1, T, W, rows, p.nseg, p.tseg, p.ntt, v, st, ex, c_out));
   return LINREC_OK;
 }
 
@@ -792,6 +827,43 @@ int linrec_segment_fixup_backward_f64(const double* lam, const double* hprev, co
                                       void* stream) {
   return segment_fixup<double>(true, lam, hprev, h, lam_next, seg_prod, y_in, dx, dlam, T, W, tile_rows,
                                static_cast<cudaStream_t>(stream));
+}
+
+int linrec_segment_scan_exchange_f32(const float* lam, const float* x, const float* h0, float* h, float* seg_prod,
+                                     float* agg, int64_t T, int64_t W, const linrec_exchange_t* ex,
+                                     linrec_workspace_t ws, void* stream) {
+  linrec_impl::Exchange e;
+  const int rc = to_exchange(ex, W, 0, true, false, &e);
+  if (rc) return rc;
+  return segment_scan<float>(lam, x, h0, h, seg_prod, agg, T, W, ws, static_cast<cudaStream_t>(stream), &e);
+}
+int linrec_segment_scan_backward_exchange_f32(const float* lam, const float* hprev, const float* h, const float* dh,
+                                              const float* lam_next, float* dlam, float* dx, float* dh0,
+                                              float* seg_prod, float* agg, int64_t T, int64_t W,
+                                              const linrec_exchange_t* ex, linrec_workspace_t ws, void* stream) {
+  linrec_impl::Exchange e;
+  const int rc = to_exchange(ex, W, 1, true, false, &e);
+  if (rc) return rc;
+  return segment_scan_backward<float>(lam, hprev, h, dh, lam_next, dlam, dx, dh0, seg_prod, agg, T, W, ws,
+                                      static_cast<cudaStream_t>(stream), &e);
+}
+int linrec_segment_fixup_exchange_f32(const float* lam, float* h, const float* seg_prod, float* c_in, int64_t T,
+                                      int64_t W, int64_t tile_rows, const linrec_exchange_t* ex, void* stream) {
+  linrec_impl::Exchange e;
+  const int rc = to_exchange(ex, W, 0, false, true, &e);
+  if (rc) return rc;
+  return segment_fixup<float>(false, lam, nullptr, nullptr, nullptr, seg_prod, nullptr, h, nullptr, T, W, tile_rows,
+                              static_cast<cudaStream_t>(stream), &e, c_in);
+}
+int linrec_segment_fixup_backward_exchange_f32(const float* lam, const float* hprev, const float* h,
+                                               const float* lam_next, const float* seg_prod, float* y_in,
+                                               float* dlam, float* dx, int64_t T, int64_t W, int64_t tile_rows,
+                                               const linrec_exchange_t* ex, void* stream) {
+  linrec_impl::Exchange e;
+  const int rc = to_exchange(ex, W, 1, false, true, &e);
+  if (rc) return rc;
+  return segment_fixup<float>(true, lam, hprev, h, lam_next, seg_prod, nullptr, dx, dlam, T, W, tile_rows,
+                              static_cast<cudaStream_t>(stream), &e, y_in);
 }
 int linrec_compose_carries_f32(const float* aggs, int64_t first, int64_t last, int64_t step, const float* seed,
                                float* out, int64_t W, void* stream) {

@@ -60,9 +60,10 @@ __device__ __forceinline__ bool entering(const FixupArgs<S>& f, int64_t vseg, in
   S p[VEC], c[VEC], sc[VEC], ci[VEC];
   IO::load_cg(f.seg_prod + (vseg * f.ntt + p_in) * f.W + ch, p);
   if (cr.rows != nullptr) IO::load_cg(cr.rows + vseg * f.W + ch, c);
-  if (cr.cin != nullptr) {
+  if (cr.cin != nullptr) {  // cin may live in shared memory (composed in-kernel): generic loads
     IO::load_cg(cr.scale + vseg * f.W + ch, sc);
-    IO::load_cg(cr.cin + ch, ci);
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) ci[v] = cr.cin[ch + v];
   }
   bool nz = false;
 #pragma unroll

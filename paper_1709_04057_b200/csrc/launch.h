@@ -55,6 +55,20 @@ inline int fixup_walkers() {
   return k < 1 ? 1 : (k > 8 ? 8 : k);
 }
 
+// One direction of the peer-memory carry exchange as this rank sees it
+// (p2p_impl.cuh; mboxes == nullptr: no exchange).
+struct Exchange {
+  void* const* mboxes = nullptr;  // device array [world]: every rank's mailbox, mapped here
+  int64_t W = 0;
+  int world = 1, rank = 0, dir = 0;
+  unsigned long long epoch = 0;   // >= 1, one per step and direction
+  int q0 = 0, q1 = 0;             // consumers of this rank's aggregate: [q0, q1)
+  int first = 0, last = 0, step = 1;  // sources folded into the incoming carry: first, first+step, ... != last
+  int zero_a = 0;                 // publish A = 0 (the forward's rank 0: h0 is folded into B)
+  __host__ __device__ bool has_sources() const { return mboxes != nullptr && first != last; }
+  __host__ __device__ bool has_consumers() const { return mboxes != nullptr && q0 < q1; }
+};
+
 template <class S>
 struct FwdCall {
   const S* lam;
@@ -113,10 +127,11 @@ template <class S>
 cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S* h, const S* lam_next,
                          const S* seg_prod, const S* carry_rows, const S* scale_rows, const S* cin, S* out0, S* out1,
                          int64_t T, int64_t W, int64_t rows, int64_t nseg, int64_t tseg, int64_t ntt,
-                         bool vec_ok, cudaStream_t st);
+                         bool vec_ok, cudaStream_t st, const Exchange* ex = nullptr, S* c_out = nullptr);
 template <class S>
 cudaError_t launch_vseg_finalize(bool reverse, const S* lam, const S* vagg, int64_t nseg, int64_t tseg,
-                                 S* carry, S* scale, S* agg_rank, S* dh0, int64_t W, cudaStream_t st);
+                                 S* carry, S* scale, S* agg_rank, S* dh0, int64_t W, cudaStream_t st,
+                                 const Exchange* ex = nullptr);
 template <class S>
 cudaError_t launch_compose(const S* aggs, int64_t first, int64_t last, int64_t step, const S* seed, S* out,
                            int64_t W, cudaStream_t st);

@@ -2,15 +2,9 @@
 // NVSwitch), replacing the NCCL all-gather of BASELINE.json's north star
 // ("the GPUs exchange that tiny carry ... each GPU runs a local fix-up") with
 // direct stores into the consumers' memory and a release/acquire flag --
-// SURVEY.md 7, hard part 1(c).
-//
-// Every rank owns one mailbox (cudaMalloc'd, shared by CUDA IPC):
-//   data[2 dirs][world][2][W]  the (A, B) aggregate rank q published for
-//                              direction d, in slot [d][q]
-//   flags[2][world]            epoch at which slot [d][q] became valid
-//   acks[2][world]             epoch up to which rank q has consumed THIS
-//                              rank's slot in q's mailbox (so a producer
-//                              never overwrites an unread slot)
+// SURVEY.md 7, hard part 1(c).  Mailbox layout and protocol: p2p_impl.cuh.
+// These are the standalone kernels; the sharded scan itself runs the same
+// protocol fused into its stitch kernels (segment.cu).
 // publish(d, e): for every consumer q, wait acks[d][q] >= e-1 (in the
 //   producer's own mailbox), store the aggregate into q's slot [d][r],
 //   fence.sys, st.release.sys q.flags[d][r] = e.
@@ -27,42 +21,10 @@
 
 #include "launch.h"
 #include "linrec_cuda.h"
-#include "linrec_device.cuh"
+#include "p2p_impl.cuh"
 
 namespace linrec_dev {
 namespace p2p {
-
-struct MboxLayout {
-  int64_t W;
-  int world;
-  __host__ __device__ size_t data_floats() const { return (size_t)2 * world * 2 * W; }
-  __host__ __device__ size_t flags_off() const { return (data_floats() * 4 + 255) / 256 * 256; }
-  __host__ __device__ size_t acks_off() const { return flags_off() + (size_t)2 * world * 8; }
-  __host__ __device__ size_t bytes() const { return acks_off() + (size_t)2 * world * 8; }
-  __device__ float* slot(void* base, int dir, int q) const {
-    return reinterpret_cast<float*>(base) + ((size_t)dir * world + q) * 2 * W;
-  }
-  __device__ unsigned long long* flag(void* base, int dir, int q) const {
-    return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(base) + flags_off()) + dir * world + q;
-  }
-  __device__ unsigned long long* ack(void* base, int dir, int q) const {
-    return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(base) + acks_off()) + dir * world + q;
-  }
-};
-
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void wait_geq(const unsigned long long* p, unsigned long long e) {
-  if (ld_acquire_sys(p) >= e) return;
-  SpinGuard g;
-  while (ld_acquire_sys(p) < e) g.tick();
-}
 
 // One CTA: agg [2][W] -> slot [dir][rank] of every consumer in [q0, q1).
 __global__ void k_publish(const float* __restrict__ agg, MboxLayout L, int rank, int dir, unsigned long long epoch,

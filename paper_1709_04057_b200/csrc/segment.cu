@@ -17,20 +17,37 @@
 // distribution: ~100 rows), while decays near 1 degrade to one extra pass.
 #include <cstdint>
 
+#include <type_traits>
+
 #include "chain_impl.cuh"
 #include "fixup_impl.cuh"
+#include "p2p_impl.cuh"
 
 namespace linrec_dev {
 
 // CTA j of the J walkers of chain (virtual segment, channel column):
-// fixup_chain (fixup_impl.cuh), 8 warps.
+// fixup_chain (fixup_impl.cuh), 8 warps.  With a peer exchange (fp32) the
+// CTA first composes the range's incoming carry for its column from the
+// mailboxes (p2p_impl.cuh::compose_chunk; the first walker of the first
+// virtual segment also stores it to c_out).
 template <class S, int VEC, int Q, bool REV>
 __global__ void __launch_bounds__(256, REV ? 1 : 2)  // backward: dx, dlam, h rows in flight
-k_fixup(FixupArgs<S> f, Carries<S> cr, int64_t ncols, int walkers) {
-  __shared__ S s_wp[8][Q * VEC];
+k_fixup(FixupArgs<S> f, Carries<S> cr, int64_t ncols, int walkers, linrec_impl::Exchange ex,
+        S* __restrict__ c_out) {
+  constexpr int CPW = Q * VEC;
+  __shared__ S s_wp[8][CPW];
+  __shared__ S s_cin[CPW];
   const int64_t col = blockIdx.x % ncols;
   const int j = (int)((blockIdx.x / ncols) % walkers);
   const int64_t vseg = (blockIdx.x / ncols) / walkers;
+  if constexpr (std::is_same<S, float>::value) {
+    if (ex.has_sources()) {
+      p2p::compose_chunk(ex, col * CPW, CPW, s_cin);
+      if (vseg == 0 && j == 0 && c_out != nullptr)
+        for (int t = threadIdx.x; t < CPW && col * CPW + t < f.W; t += blockDim.x) c_out[col * CPW + t] = s_cin[t];
+      cr.cin = s_cin - col * CPW;  // indexed by channel
+    }
+  }
   fixup_chain<S, VEC, Q, REV, CtaSync>(f, vseg, col, j, walkers, cr, s_wp);
 }
 
@@ -54,9 +71,16 @@ template <class S, bool REV, int G>
 __global__ void __launch_bounds__(32 * G)
 k_vseg_finalize(const S* __restrict__ lam, const S* __restrict__ vagg, int64_t nseg, int64_t tseg,
                 S* __restrict__ carry, S* __restrict__ scale, S* __restrict__ agg_rank, S* __restrict__ dh0,
-                int64_t W) {
+                int64_t W, linrec_impl::Exchange ex) {
   __shared__ S sA[G][32], sB[G][32];
   vseg_fold<S, REV, G, CtaSync>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W, blockIdx.x, sA, sB);
+  if constexpr (std::is_same<S, float>::value) {
+    // the rank aggregate of this chunk straight into the consumers' mailboxes
+    if (ex.has_consumers()) {
+      const int64_t j0 = (int64_t)blockIdx.x * 32;
+      p2p::publish_chunk(ex, agg_rank, j0, (int)(W - j0 < 32 ? W - j0 : 32));
+    }
+  }
 }
 
 }  // namespace linrec_dev
@@ -67,7 +91,8 @@ template <class S>
 cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S* h, const S* lam_next,
                          const S* seg_prod, const S* carry_rows, const S* scale_rows, const S* cin, S* out0, S* out1,
                          int64_t T, int64_t W, int64_t rows, int64_t nseg, int64_t tseg, int64_t ntt,
-                         bool vec_ok, cudaStream_t st) {
+                         bool vec_ok, cudaStream_t st, const Exchange* ex, S* c_out) {
+  const Exchange exv = ex != nullptr ? *ex : Exchange{};
   constexpr int V = Tuning<S>::VEC;
   const int64_t nvec = vec_ok ? (W + V - 1) / V : W;
   const int q = pick_q(nvec);
@@ -79,9 +104,9 @@ cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S
   const linrec_dev::Carries<S> cr{carry_rows, scale_rows, cin};
 #define FIX(VV)                                                                                       \
   LINREC_Q_SWITCH(q, if (reverse) linrec_dev::k_fixup<S, VV, Q_, true><<<grid, 256, 0, st>>>(         \
-                         fa, cr, ncols, walk);                                \
+                         fa, cr, ncols, walk, exv, c_out);                                \
                      else linrec_dev::k_fixup<S, VV, Q_, false><<<grid, 256, 0, st>>>(                \
-                         fa, cr, ncols, walk));
+                         fa, cr, ncols, walk, exv, c_out));
   if (vec_ok) {
     FIX(V)
   } else {
@@ -93,13 +118,14 @@ cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S
 
 template <class S>
 cudaError_t launch_vseg_finalize(bool reverse, const S* lam, const S* vagg, int64_t nseg, int64_t tseg, S* carry,
-                                 S* scale, S* agg_rank, S* dh0, int64_t W, cudaStream_t st) {
+                                 S* scale, S* agg_rank, S* dh0, int64_t W, cudaStream_t st, const Exchange* ex) {
+  const Exchange exv = ex != nullptr ? *ex : Exchange{};
   constexpr int G = 16;
   const unsigned g = (unsigned)((W + 31) / 32);
   if (reverse)
-    linrec_dev::k_vseg_finalize<S, true, G><<<g, 32 * G, 0, st>>>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W);
+    linrec_dev::k_vseg_finalize<S, true, G><<<g, 32 * G, 0, st>>>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W, exv);
   else
-    linrec_dev::k_vseg_finalize<S, false, G><<<g, 32 * G, 0, st>>>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W);
+    linrec_dev::k_vseg_finalize<S, false, G><<<g, 32 * G, 0, st>>>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W, exv);
   return cudaGetLastError();
 }
 
@@ -114,18 +140,20 @@ cudaError_t launch_compose(const S* aggs, int64_t first, int64_t last, int64_t s
 
 template cudaError_t launch_fixup<float>(bool, const float*, const float*, const float*, const float*, const float*,
                                          const float*, const float*, const float*, float*, float*, int64_t, int64_t,
-                                         int64_t, int64_t, int64_t, int64_t, bool, cudaStream_t);
+                                         int64_t, int64_t, int64_t, int64_t, bool, cudaStream_t, const Exchange*,
+                                         float*);
 template cudaError_t launch_fixup<double>(bool, const double*, const double*, const double*, const double*,
                                           const double*, const double*, const double*, const double*, double*,
                                           double*,
-                                          int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, bool, cudaStream_t);
+                                          int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, bool, cudaStream_t,
+                                          const Exchange*, double*);
 template cudaError_t launch_compose<float>(const float*, int64_t, int64_t, int64_t, const float*, float*,
                                            int64_t, cudaStream_t);
 template cudaError_t launch_compose<double>(const double*, int64_t, int64_t, int64_t, const double*, double*,
                                             int64_t, cudaStream_t);
 template cudaError_t launch_vseg_finalize<float>(bool, const float*, const float*, int64_t, int64_t, float*,
-                                                 float*, float*, float*, int64_t, cudaStream_t);
+                                                 float*, float*, float*, int64_t, cudaStream_t, const Exchange*);
 template cudaError_t launch_vseg_finalize<double>(bool, const double*, const double*, int64_t, int64_t, double*,
-                                                  double*, double*, double*, int64_t, cudaStream_t);
+                                                  double*, double*, double*, int64_t, cudaStream_t, const Exchange*);
 
 }  // namespace linrec_impl

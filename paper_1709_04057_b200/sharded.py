@@ -88,6 +88,26 @@ class CudaBackend:
         capi.segment_fixup(lam.data_ptr(), h.data_ptr(), seg_prod.data_ptr(), self._p(c_in), T, W, rows, 4,
                            self._st())
 
+    # the exchange fused into the stitch kernels (PeerMailboxes.exchange)
+    def segment_scan_exchange(self, lam, x, h0, h, seg_prod, agg, T, W, ex):
+        capi.segment_scan_exchange(lam.data_ptr(), x.data_ptr(), self._p(h0), h.data_ptr(), seg_prod.data_ptr(),
+                                   agg.data_ptr(), T, W, ex, None if self.ws is None else self.ws.handle, self._st())
+
+    def segment_scan_backward_exchange(self, lam, hprev, h, dh, lam_next, dlam, dx, dh0, seg_prod, agg, T, W, ex):
+        capi.segment_scan_backward_exchange(lam.data_ptr(), self._p(hprev), h.data_ptr(), dh.data_ptr(),
+                                            self._p(lam_next), dlam.data_ptr(), dx.data_ptr(), dh0.data_ptr(),
+                                            seg_prod.data_ptr(), agg.data_ptr(), T, W, ex,
+                                            None if self.ws is None else self.ws.handle, self._st())
+
+    def fixup_exchange(self, lam, h, seg_prod, c_in, T, W, rows, ex):
+        capi.segment_fixup_exchange(lam.data_ptr(), h.data_ptr(), seg_prod.data_ptr(), c_in.data_ptr(), T, W, rows,
+                                    ex, self._st())
+
+    def fixup_backward_exchange(self, lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T, W, rows, ex):
+        capi.segment_fixup_backward_exchange(lam.data_ptr(), self._p(hprev), h.data_ptr(), self._p(lam_next),
+                                             seg_prod.data_ptr(), y_in.data_ptr(), dlam.data_ptr(), dx.data_ptr(),
+                                             T, W, rows, ex, self._st())
+
     def fixup_backward(self, lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T, W, rows):
         capi.segment_fixup_backward(lam.data_ptr(), self._p(hprev), h.data_ptr(), self._p(lam_next),
                                     seg_prod.data_ptr(), self._p(y_in), dlam.data_ptr(), dx.data_ptr(), T, W,
@@ -120,6 +140,13 @@ class PeerMailboxes:
             ptrs.append(p.value)
         self.ptrs = torch.tensor(ptrs, dtype=torch.int64, device=device)  # device array of mailbox pointers
         self.epoch = [0, 0]
+
+    def exchange(self, direction, consumers, sources, zero_a=False):
+        """linrec_exchange_t of this step (epoch[direction] already advanced):
+        consumers = (first, last) ranks receiving this rank's aggregate,
+        sources = (first, last, step) ranks folded into the incoming carry."""
+        return capi.Exchange(self.ptrs.data_ptr(), self.world, self.rank, self.epoch[direction],
+                             consumers[0], consumers[1], sources[0], sources[1], sources[2], int(zero_a))
 
     def publish(self, agg, direction, q0, q1, stream):
         capi.check(capi.lib.linrec_p2p_publish_f32(agg.data_ptr(), self.W, self.world, self.rank, direction,
@@ -194,12 +221,10 @@ class SequenceShardedScan:
         r, R = self.rank, self.world
         # fwd: scan + finalize (+ fix-up when virtually segmented) + compose/fix-up
         # for r > 0; bwd likewise + the dh0 compose on rank 0
-        if use_p2p:  # scan(+finalize), publish, compose + ack, fix-up; likewise backward (+ dh0 fold)
-            self.launches_per_step = ((2 + (1 if r < R - 1 else 0) + (3 if r > 0 else 0))
-                                      + (2 + (1 if r > 0 else 0) + (3 if r < R - 1 else 0) + (1 if r == 0 else 0)))
-        else:
-            self.launches_per_step = ((2 + (2 if r > 0 else 0))
-                                      + (2 + (2 if r < R - 1 else 0) + (1 if r == 0 else 0)))
+        if use_p2p:  # per direction: scan, fold + publish, compose + fix-up (+ the dh0 fold on rank 0)
+            self.launches_per_step = 3 + 3 + (1 if r == 0 else 0)
+        else:  # per direction: scan, fold, compose of the gathered aggregates, fix-up
+            self.launches_per_step = (3 + (1 if r > 0 else 0)) + (3 + (1 if r < R - 1 else 0) + (1 if r == 0 else 0))
 
     def _on_stream(self):
         if self.stream is not None and torch.cuda.is_available() and isinstance(self.stream, torch.cuda.Stream):
@@ -231,20 +256,20 @@ class SequenceShardedScan:
 
     def _forward(self, lam, x, h0, h):
         r, R, W, T = self.rank, self.world, self.W, self.Tl
+        if self.mb is not None:
+            # the exchange runs inside the fold (publish) and the fix-up (compose)
+            self.mb.epoch[0] += 1
+            ex = self.mb.exchange(0, (r + 1, R), (0, r, 1), zero_a=(r == 0))
+            self.be.segment_scan_exchange(lam, x, h0 if r == 0 else None, h, self.seg_prod_f, self.agg, T, W, ex)
+            self.be.fixup_exchange(lam, h, self.seg_prod_f, self.c_in, T, W, self.rows_f, ex)
+            self.hprev = self.c_in if r > 0 else (h0 if h0 is not None else self.zeros)
+            return h
         self.be.segment_scan(lam, x, h0 if r == 0 else None, h, self.seg_prod_f, self.agg, T, W)
         if r == 0:
             self.agg[0].zero_()  # h0 is already folded into rank 0's segment
-        if self.mb is not None:
-            st = self.be._st()
-            self.mb.epoch[0] += 1
-            if r < R - 1:
-                self.mb.publish(self.agg, 0, r + 1, R, st)
-            if r > 0:
-                self.mb.compose(0, self.agg, 0, r, 1, None, self.c_in, st)
-        else:
-            self._all_gather(self.agg, self.aggs)
-            if r > 0:
-                self.be.compose(self.aggs, 0, r, 1, None, self.c_in, W)
+        self._all_gather(self.agg, self.aggs)
+        if r > 0:
+            self.be.compose(self.aggs, 0, r, 1, None, self.c_in, W)
         # always: the fix-up also stitches the segment's own virtual segments
         self.be.fixup(lam, h, self.seg_prod_f, self.c_in if r > 0 else None, T, W, self.rows_f)
         if r > 0:
@@ -266,23 +291,23 @@ class SequenceShardedScan:
         if hprev is None:
             hprev = self.hprev if self.hprev is not None else self._halo(h, h0)
         lam_next = self.ones if r < R - 1 else None
-        self.be.segment_scan_backward(lam, hprev, h, dh, lam_next, dlam, dx, self.dh0_loc, self.seg_prod_b,
-                                      self.agg, T, W)
+        if r == R - 1:
+            self.y_in.zero_()
         if self.mb is not None:
-            st = self.be._st()
             self.mb.epoch[1] += 1
-            if r > 0:
-                self.mb.publish(self.agg, 1, 0, r, st)
-            if r < R - 1:
-                self.mb.compose(1, self.agg, R - 1, r, -1, None, self.y_in, st)
+            ex = self.mb.exchange(1, (0, r), (R - 1, r, -1))
+            self.be.segment_scan_backward_exchange(lam, hprev, h, dh, lam_next, dlam, dx, self.dh0_loc,
+                                                   self.seg_prod_b, self.agg, T, W, ex)
+            self.be.fixup_backward_exchange(lam, hprev, h, lam_next, self.seg_prod_b, self.y_in, dlam, dx, T, W,
+                                            self.rows_b, ex)
         else:
+            self.be.segment_scan_backward(lam, hprev, h, dh, lam_next, dlam, dx, self.dh0_loc, self.seg_prod_b,
+                                          self.agg, T, W)
             self._all_gather(self.agg, self.aggs)
             if r < R - 1:
                 self.be.compose(self.aggs, R - 1, r, -1, None, self.y_in, W)
-        if r == R - 1:
-            self.y_in.zero_()
-        self.be.fixup_backward(lam, hprev, h, lam_next, self.seg_prod_b, self.y_in if r < R - 1 else None, dlam, dx,
-                               T, W, self.rows_b)
+            self.be.fixup_backward(lam, hprev, h, lam_next, self.seg_prod_b, self.y_in if r < R - 1 else None,
+                                   dlam, dx, T, W, self.rows_b)
         if r == 0 and dh0 is not None:
             # own aggregate only: the local fold of the all-gather path
             self.aggs[0].copy_(self.agg)
