@@ -159,6 +159,273 @@ cudaError_t dispatch(const GemmOperands& op, int epi, const GemmEpilogue& ep, co
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// CUDA-core path for plain GEMMs with at most 8 output columns (the first
+// layer's input width m, e.g. bench_model's m = 4): a 256-wide tensor-core
+// tile would be >= 97 % padding there, while these are HBM-bound on A.
+// Exact fp32 FMAs in a fixed order (deterministic, at least as accurate as
+// 3xTF32).
+struct SkinnyArgs {
+  // two K-concatenated operand pairs (the second with K2 = 0 when absent);
+  // fields are selected with ternaries, never indexed at run time, so the
+  // kernel parameters stay in constant space
+  const float *a0, *a1, *b0, *b1;
+  int64_t K0, K1, lda0, lda1, ldb0, ldb1;
+  int64_t M, units;
+  bool b_mn;
+  __device__ const float* a(int p) const { return p == 0 ? a0 : a1; }
+  __device__ int64_t lda(int p) const { return p == 0 ? lda0 : lda1; }
+  __device__ int64_t K(int p) const { return p == 0 ? K0 : K1; }
+  __device__ float B(int p, int64_t n, int64_t k) const {
+    const float* b = p == 0 ? b0 : b1;
+    const int64_t ld = p == 0 ? ldb0 : ldb1;
+    return b_mn ? __ldg(b + k * ld + n) : __ldg(b + n * ld + k);
+  }
+};
+
+// A K-major (rows of A contiguous along k): one warp per output row, lanes
+// along k (float4 loads when V4), B [K][N] staged in shared memory,
+// fixed-order warp reduction.
+template <int N, bool V4>
+__global__ void __launch_bounds__(256) k_skinny_rows(SkinnyArgs g, float* __restrict__ C, int64_t ldc, int acc) {
+  extern __shared__ float Bs[];  // [N][K1 + K2]: lanes read consecutive k (no bank conflicts)
+  const int64_t Kt = g.K0 + g.K1;
+  for (int64_t i = threadIdx.x; i < Kt * N; i += blockDim.x) {
+    const int64_t n = i / Kt, k = i - n * Kt;
+    const int p = k < g.K0 ? 0 : 1;
+    Bs[i] = n < g.units ? g.B(p, n, p == 0 ? k : k - g.K0) : 0.f;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warps = blockDim.x >> 5;
+  for (int64_t m = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5); m < g.M; m += (int64_t)gridDim.x * warps) {
+    float s[N];
+#pragma unroll
+    for (int n = 0; n < N; ++n) s[n] = 0.f;
+    int64_t koff = 0;
+    for (int p = 0; p < 2; ++p) {
+      const float* a = g.a(p) + m * g.lda(p);
+      const int64_t Kp = g.K(p);
+      if (V4) {  // lane owns k = 4*lane + 128*i .. +3
+        constexpr int U = 4;
+        for (int64_t k = 4 * lane; k < Kp; k += 128 * U) {
+          float4 v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            v[u] = k + 128 * u < Kp ? __ldcs(reinterpret_cast<const float4*>(a + k + 128 * u))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (k + 128 * u >= Kp) break;
+#pragma unroll
+            for (int n = 0; n < N; ++n) {
+              const float4 b = *reinterpret_cast<const float4*>(Bs + n * Kt + koff + k + 128 * u);
+              s[n] = __fmaf_rn(v[u].x, b.x, s[n]);
+              s[n] = __fmaf_rn(v[u].y, b.y, s[n]);
+              s[n] = __fmaf_rn(v[u].z, b.z, s[n]);
+              s[n] = __fmaf_rn(v[u].w, b.w, s[n]);
+            }
+          }
+        }
+      } else {
+        int64_t k = lane;
+        for (; k + 96 < Kp; k += 128) {
+          float v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = __ldcs(a + k + 32 * u);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int n = 0; n < N; ++n) s[n] = __fmaf_rn(v[u], Bs[n * Kt + koff + k + 32 * u], s[n]);
+        }
+        for (; k < Kp; k += 32) {
+          const float v = __ldcs(a + k);
+#pragma unroll
+          for (int n = 0; n < N; ++n) s[n] = __fmaf_rn(v, Bs[n * Kt + koff + k], s[n]);
+        }
+      }
+      koff += Kp;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+      for (int n = 0; n < N; ++n) s[n] += __shfl_xor_sync(0xffffffffu, s[n], off);
+    if (lane == 0)
+#pragma unroll
+      for (int n = 0; n < N; ++n)
+        if (n < g.units) {
+          float* d = C + m * ldc + n;
+          *d = acc ? *d + s[n] : s[n];
+        }
+  }
+}
+
+// A MN-major (A(m,k) = a[k*lda + m], the weight gradients' dpre^T with K =
+// T*b rows): a CTA covers 64 rows m (16 threads x float4) x 16 k-groups,
+// split-K over blockIdx.y into the tensor-core path's partial layout
+// [splits][Mp][ldp] (then k_splitk_reduce); the k-groups are summed in
+// shared memory in a fixed order.  Needs M, lda % 4 == 0 and 16-byte
+// aligned A (the ABI's pitch rule).
+template <int N>
+__global__ void __launch_bounds__(256) k_skinny_outer(SkinnyArgs g, float* __restrict__ part, int64_t Mp,
+                                                      int64_t ldp, int64_t kper) {
+  constexpr int KC = 1024, MQ = 16, KG = 256 / MQ, U = 8;  // 64 rows m x 16 k-groups per CTA
+  static_assert(KC * N >= KG * MQ * N * 4, "the k-group reduction reuses the B stage");
+  __shared__ float4 smem[KC * N / 4];
+  float(*Bs)[N] = reinterpret_cast<float(*)[N]>(smem);
+  float4(*red)[MQ][N] = reinterpret_cast<float4(*)[MQ][N]>(smem);
+  const int mq = threadIdx.x % MQ, kg = threadIdx.x / MQ;
+  const int64_t m0 = (int64_t)blockIdx.x * (4 * MQ) + 4 * mq;
+  const bool mok = m0 < g.M;
+  const int64_t Kt = g.K0 + g.K1;
+  const int64_t k0 = (int64_t)blockIdx.y * kper, k1 = k0 + kper < Kt ? k0 + kper : Kt;
+  float4 s[N];
+#pragma unroll
+  for (int n = 0; n < N; ++n) s[n] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t kc = k0; kc < k1; kc += KC) {
+    const int kn = (int)(k1 - kc < KC ? k1 - kc : KC);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kn * N; i += blockDim.x) {
+      const int kk = i / N, n = i - kk * N;
+      const int64_t k = kc + kk;
+      const int p = k < g.K0 ? 0 : 1;
+      Bs[kk][n] = n < g.units ? g.B(p, n, p == 0 ? k : k - g.K0) : 0.f;
+    }
+    __syncthreads();
+    if (!mok) continue;
+    for (int kk = kg; kk < kn; kk += KG * U) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = kc + kk + KG * u;
+        const int p = k < g.K0 ? 0 : 1;
+        v[u] = kk + KG * u < kn
+                   ? __ldcs(reinterpret_cast<const float4*>(g.a(p) + (p == 0 ? k : k - g.K0) * g.lda(p) + m0))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (kk + KG * u >= kn) break;
+#pragma unroll
+        for (int n = 0; n < N; ++n) {
+          const float b = Bs[kk + KG * u][n];
+          s[n].x = __fmaf_rn(v[u].x, b, s[n].x);
+          s[n].y = __fmaf_rn(v[u].y, b, s[n].y);
+          s[n].z = __fmaf_rn(v[u].z, b, s[n].z);
+          s[n].w = __fmaf_rn(v[u].w, b, s[n].w);
+        }
+      }
+    }
+  }
+  __syncthreads();  // the B stage is free: reuse it for the k-group sums
+#pragma unroll
+  for (int n = 0; n < N; ++n) red[kg][mq][n] = s[n];
+  __syncthreads();
+  if (kg == 0 && mok) {
+#pragma unroll
+    for (int q = 1; q < KG; ++q)  // fixed order: deterministic
+#pragma unroll
+      for (int n = 0; n < N; ++n) {
+        const float4 r = red[q][mq][n];
+        s[n].x += r.x;
+        s[n].y += r.y;
+        s[n].z += r.z;
+        s[n].w += r.w;
+      }
+    float* dst = part + ((int64_t)blockIdx.y * Mp + m0) * ldp;  // M % 4 == 0: all four rows exist
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+      if (n < g.units) {
+        dst[n] = s[n].x;
+        dst[ldp + n] = s[n].y;
+        dst[2 * ldp + n] = s[n].z;
+        dst[3 * ldp + n] = s[n].w;
+      }
+  }
+}
+
+bool skinny_enabled() {  // LINREC_SKINNY_GEMM=0: always the tensor cores (comparison runs)
+  static const bool on = env_int("LINREC_SKINNY_GEMM", 1) != 0;
+  return on;
+}
+
+// Runs the plain GEMM on CUDA cores when it qualifies; cudaErrorNotSupported
+// otherwise (the caller then uses the tensor cores).
+cudaError_t gemm_skinny(const GemmOperands& op, const GemmEpilogue& ep, int splits, float* partial, int64_t Mp,
+                        int64_t ldp, cudaStream_t st) {
+  if (op.units > 8 || op.nb != 1 || op.ntaps > 1 || op.M < 1) return cudaErrorNotSupported;
+  SkinnyArgs g{};
+  g.a0 = op.a1;
+  g.b0 = op.b1;
+  g.K0 = op.K1;
+  g.lda0 = op.lda1;
+  g.ldb0 = op.ldb1;
+  g.a1 = op.a2 != nullptr ? op.a2 : op.a1;
+  g.b1 = op.a2 != nullptr ? op.b2 : op.b1;
+  g.K1 = op.a2 != nullptr ? op.K2 : 0;
+  g.lda1 = op.a2 != nullptr ? op.lda2 : op.lda1;
+  g.ldb1 = op.a2 != nullptr ? op.ldb2 : op.ldb1;
+  g.M = op.M;
+  g.units = op.units;
+  g.b_mn = op.b_mn;
+  const int npad = op.units <= 1 ? 1 : op.units <= 2 ? 2 : op.units <= 4 ? 4 : 8;
+  const int64_t Kt = op.K1 + g.K1;
+  if (!op.a_mn) {
+    const size_t smem = (size_t)Kt * npad * sizeof(float);
+    if (smem > 48 * 1024) return cudaErrorNotSupported;
+    const bool v4 = op.K1 % 4 == 0 && op.lda1 % 4 == 0 && (reinterpret_cast<uintptr_t>(op.a1) & 15) == 0 &&
+                    (op.a2 == nullptr ||
+                     (op.K2 % 4 == 0 && op.lda2 % 4 == 0 && (reinterpret_cast<uintptr_t>(op.a2) & 15) == 0));
+    // one wave of resident CTAs, each warp walking rows (the B stage is per CTA)
+    int occ = 1;
+    if (v4) {
+      void (*kf)(SkinnyArgs, float*, int64_t, int) = npad <= 1 ? k_skinny_rows<1, true>
+                                                     : npad <= 2 ? k_skinny_rows<2, true>
+                                                     : npad <= 4 ? k_skinny_rows<4, true> : k_skinny_rows<8, true>;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, 256, smem);
+    } else {
+      void (*kf)(SkinnyArgs, float*, int64_t, int) = npad <= 1 ? k_skinny_rows<1, false>
+                                                     : npad <= 2 ? k_skinny_rows<2, false>
+                                                     : npad <= 4 ? k_skinny_rows<4, false> : k_skinny_rows<8, false>;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, 256, smem);
+    }
+    const int64_t blocks = (op.M + 7) / 8, wave = (int64_t)sm_count() * (occ < 1 ? 1 : occ);
+    const unsigned grid = (unsigned)(blocks < wave ? blocks : wave);
+#define ROWS(NN)                                                                                             \
+  (v4 ? k_skinny_rows<NN, true><<<grid, 256, smem, st>>>(g, ep.C, ep.ldc, ep.accumulate ? 1 : 0)            \
+      : k_skinny_rows<NN, false><<<grid, 256, smem, st>>>(g, ep.C, ep.ldc, ep.accumulate ? 1 : 0))
+    switch (npad) {
+      case 1: ROWS(1); break;
+      case 2: ROWS(2); break;
+      case 4: ROWS(4); break;
+      default: ROWS(8); break;
+    }
+#undef ROWS
+    return cudaGetLastError();
+  }
+  // needs the split-K scratch and float4 rows of A
+  if (splits < 2 || partial == nullptr || op.M % 4 != 0 || op.lda1 % 4 != 0 ||
+      (reinterpret_cast<uintptr_t>(op.a1) & 15) != 0 ||
+      (op.a2 != nullptr && (op.lda2 % 4 != 0 || (reinterpret_cast<uintptr_t>(op.a2) & 15) != 0)))
+    return cudaErrorNotSupported;
+  const int64_t kper = (Kt + splits - 1) / splits;
+  const dim3 grid((unsigned)((op.M + 63) / 64), (unsigned)splits);
+#define OUTER(NN) k_skinny_outer<NN><<<grid, 256, 0, st>>>(g, partial, Mp, ldp, kper)
+  switch (npad) {
+    case 1: OUTER(1); break;
+    case 2: OUTER(2); break;
+    case 4: OUTER(4); break;
+    default: OUTER(8); break;
+  }
+#undef OUTER
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t MN = op.M * op.units;
+  const int64_t blocks = (MN + 255) / 256;
+  k_splitk_reduce<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(
+      partial, splits, op.M, Mp, op.units, ldp, ep.ldc, ep.C, ep.accumulate ? 1 : 0);
+  return cudaGetLastError();
+}
+
 int gemm_splits_for(int64_t M, int64_t N, int64_t K) {
   const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
   const int64_t kb = (K + BK - 1) / BK;
@@ -227,6 +494,10 @@ cudaError_t gemm_tf32(const GemmOperands& op, int epi, const GemmEpilogue& ep, c
     partial = ep.scratch;
     p.mode = 2;
     p.Mp = (int)Mp;
+  }
+  if (epi == linrec_dev::tc::kEpiPlain && skinny_enabled()) {
+    const cudaError_t es = gemm_skinny(op, ep, splits, partial, Mp, ldp, st);
+    if (es != cudaErrorNotSupported) return es;
   }
   cudaError_t e = ep.split3 ? dispatch<true>(op, epi, ep, p, partial, Mp, ldp, st)
                             : dispatch<false>(op, epi, ep, p, partial, Mp, ldp, st);

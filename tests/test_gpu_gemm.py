@@ -60,6 +60,19 @@ def test_gemm_many_tiles_persistent():
     assert run(300, 1000, 4096, True, False, splits=5) < TOL[0]
 
 
+@pytest.mark.parametrize("precision", [0, 1])
+@pytest.mark.parametrize("N", [1, 3, 4, 8])
+def test_gemm_skinny_cuda_core_path(N, precision):
+    # <= 8 output columns: exact fp32 FMAs on CUDA cores (gemm_tc.cu::gemm_skinny), fp32-grade in both modes
+    bmn = N % 4 == 0  # an MN-major B needs a 16-byte pitch (the ABI's TMA rule)
+    assert run(5000, N, 512, False, bmn, precision=precision) < 1e-5      # dx = dpre . W (rows kernel)
+    assert run(777, N, 100, False, False, accumulate=True) < 1e-5
+    assert run(1001, N, 516, False, bmn) < 1e-5
+    assert run(512, N, 65536, True, bmn, splits=16, precision=precision) < 1e-5  # weight gradient (split-K)
+    assert run(300, N, 3000, True, False, accumulate=True, splits=5) < 1e-5
+    assert run(300, N, 3000, True, bmn, splits=1) < TOL[0]               # no scratch: tensor cores
+
+
 def test_tf32_operand_truncation():
     """The tensor core reads tf32 by dropping the low 13 mantissa bits; the
     3xTF32 split (lo = v - trunc(v)) relies on it.  A one-hot B picks single
