@@ -12,10 +12,13 @@
 // equivalents for the other status codes.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "linrec_cuda.h"
 
@@ -116,6 +119,22 @@ inline int bwd_call(const double* l, const double* h0, const double* h, const do
                     linrec_workspace_t ws, void* st) {
   return linrec_scan_backward_f64(l, h0, h, dh, dl, dx, dh0, T, W, mode, ws, st);
 }
+inline int plan_call(const float* l, const float* x, const float* h0, float* h, index_t T, index_t W,
+                     const index_t* b, index_t p, float* P, float* R, float* C, void* st) {
+  return linrec_scan_plan_f32(l, x, h0, h, T, W, b, p, P, R, C, st);
+}
+inline int plan_call(const double* l, const double* x, const double* h0, double* h, index_t T, index_t W,
+                     const index_t* b, index_t p, double* P, double* R, double* C, void* st) {
+  return linrec_scan_plan_f64(l, x, h0, h, T, W, b, p, P, R, C, st);
+}
+inline int plan_bwd_call(const float* l, const float* h0, const float* h, const float* dh, float* dl, float* dx,
+                         float* dh0, index_t T, index_t W, const index_t* b, index_t p, void* st) {
+  return linrec_scan_backward_plan_f32(l, h0, h, dh, dl, dx, dh0, T, W, b, p, st);
+}
+inline int plan_bwd_call(const double* l, const double* h0, const double* h, const double* dh, double* dl,
+                         double* dx, double* dh0, index_t T, index_t W, const index_t* b, index_t p, void* st) {
+  return linrec_scan_backward_plan_f64(l, h0, h, dh, dl, dx, dh0, T, W, b, p, st);
+}
 }  // namespace detail
 
 // scan_serial (recurrence.hpp:169-179): bit-exact serial recurrence.
@@ -137,6 +156,63 @@ void scan_parallel(const DeviceTensor3<S>& decays, const DeviceTensor3<S>& impul
   check_same_shape(decays, h, "scan_parallel(h)");
   throw_status(detail::scan_call(decays.data, impulses.data, initial.data, h.data, decays.steps,
                                  decays.step_size(), LINREC_PARALLEL, ws, stream));
+}
+
+// ChunkPlan / plan_chunks (recurrence.hpp:53-80): contiguous 1-indexed
+// inclusive chunks of steps 1..T, remainder to the front.
+struct ChunkPlan {
+  std::vector<std::pair<index_t, index_t>> bounds;
+  int workers = 0;
+  index_t chunks() const { return index_t(bounds.size()); }
+};
+inline ChunkPlan plan_chunks(index_t T, int requested_workers) {
+  if (T < 1) throw ContractViolation("plan_chunks: T must be >= 1");
+  if (requested_workers < 1) throw ContractViolation("plan_chunks: requested_workers must be >= 1");
+  const index_t p = std::min<index_t>(requested_workers, T);
+  ChunkPlan plan;
+  plan.workers = int(p);
+  const index_t base = T / p, rem = T % p;
+  index_t start = 1;
+  for (index_t i = 0; i < p; ++i) {
+    const index_t len = base + (i < rem ? 1 : 0);
+    plan.bounds.emplace_back(start, start + len - 1);
+    start += len;
+  }
+  return plan;
+}
+
+// ScanSummaries (recurrence.hpp:186-191): caller-owned [chunks, b, n] device
+// views of the chunk summaries P, R and stitched chunk-end states C.
+template <class S>
+struct ScanSummaries {
+  DeviceTensor3<S> P, R, C;
+};
+
+namespace detail {
+inline std::vector<index_t> flat_bounds(const ChunkPlan& plan) {
+  std::vector<index_t> b;
+  for (const auto& se : plan.bounds) {
+    b.push_back(se.first);
+    b.push_back(se.second);
+  }
+  return b;
+}
+}  // namespace detail
+
+// scan_parallel with an explicit plan (recurrence.hpp:193-245): the
+// reference's three phases on the device, bit-identical to its result (and
+// summaries) for the same plan; validate_plan's errors.
+template <class S>
+void scan_parallel(const DeviceTensor3<S>& decays, const DeviceTensor3<S>& impulses,
+                   const DeviceTensor2<S>& initial, const ChunkPlan& plan, DeviceTensor3<S>& h,
+                   ScanSummaries<S>* summaries = nullptr, void* stream = nullptr) {
+  validate_recurrence_shapes(decays, impulses, initial);
+  check_same_shape(decays, h, "scan_parallel(h)");
+  const auto b = detail::flat_bounds(plan);
+  throw_status(detail::plan_call(decays.data, impulses.data, initial.data, h.data, decays.steps, decays.step_size(),
+                                 b.data(), plan.chunks(), summaries ? summaries->P.data : nullptr,
+                                 summaries ? summaries->R.data : nullptr, summaries ? summaries->C.data : nullptr,
+                                 stream));
 }
 
 // scan (recurrence.hpp:255-263): mode dispatch.
@@ -170,6 +246,24 @@ void scan_backward(const DeviceTensor3<S>& decays, const DeviceTensor2<S>& initi
   throw_status(detail::bwd_call(decays.data, initial.data, h.data, d_h.data, grads.d_decays.data,
                                 grads.d_impulses.data, grads.d_initial.data, decays.steps,
                                 decays.step_size(), static_cast<int>(mode), ws, stream));
+}
+
+// scan_backward with the reversed scan chunked by an explicit plan
+// (recurrence.hpp:365-377; ScanMode::Parallel), bit-identical to the
+// reference's for the same plan.
+template <class S>
+void scan_backward(const DeviceTensor3<S>& decays, const DeviceTensor2<S>& initial, const DeviceTensor3<S>& h,
+                   const DeviceTensor3<S>& d_h, const ChunkPlan& plan, RecurrenceGradients<S>& grads,
+                   void* stream = nullptr) {
+  check_same_shape(decays, h, "scan_backward(h)");
+  check_same_shape(decays, d_h, "scan_backward(d_h)");
+  validate_recurrence_shapes(decays, d_h, initial);
+  check_same_shape(decays, grads.d_decays, "scan_backward(d_decays)");
+  check_same_shape(decays, grads.d_impulses, "scan_backward(d_impulses)");
+  const auto b = detail::flat_bounds(plan);
+  throw_status(detail::plan_bwd_call(decays.data, initial.data, h.data, d_h.data, grads.d_decays.data,
+                                     grads.d_impulses.data, grads.d_initial.data, decays.steps, decays.step_size(),
+                                     b.data(), plan.chunks(), stream));
 }
 
 }  // namespace cuda

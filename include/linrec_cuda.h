@@ -181,6 +181,29 @@ int linrec_first_nonfinite_f32(const float* v, int64_t n, int64_t* index,
 int linrec_first_nonfinite_f64(const double* v, int64_t n, int64_t* index,
                                void* stream);
 
+/* ---- the reference's chunked scan with an explicit plan ----------------- *
+ * scan_parallel(decays, impulses, initial, plan, pool, check_finite,
+ * summaries) (recurrence.hpp:193-245) and scan_backward(in, h, d_h, plan,
+ * pool) (:365-377) on the device: the reference's three phases (chunk
+ * summaries, sequential stitch, seeded chunk re-scans) in its per-channel
+ * operation order, so h and the ScanSummaries P, R, C [chunks][W]
+ * (:186-191; each nullable) are bit-identical to the reference's for the
+ * same plan.  bounds: HOST array of `chunks` (start, end) 1-based inclusive
+ * pairs, checked like validate_plan (:84-94, same messages); plan_chunks
+ * (:61-80) is linrec.plan_chunks.  The backward scans the reversed image
+ * with the plan (ScanMode::Parallel).  Device pointers, stream-ordered; the
+ * default parallel mode (linrec_scan_*) is the faster single-pass scan. */
+int linrec_scan_plan_f32(const float* lam, const float* x, const float* h0, float* h, int64_t T, int64_t W,
+                         const int64_t* bounds, int64_t chunks, float* P, float* R, float* C, void* stream);
+int linrec_scan_plan_f64(const double* lam, const double* x, const double* h0, double* h, int64_t T, int64_t W,
+                         const int64_t* bounds, int64_t chunks, double* P, double* R, double* C, void* stream);
+int linrec_scan_backward_plan_f32(const float* lam, const float* h0, const float* h, const float* dh, float* dlam,
+                                  float* dx, float* dh0, int64_t T, int64_t W, const int64_t* bounds,
+                                  int64_t chunks, void* stream);
+int linrec_scan_backward_plan_f64(const double* lam, const double* h0, const double* h, const double* dh,
+                                  double* dlam, double* dx, double* dh0, int64_t T, int64_t W,
+                                  const int64_t* bounds, int64_t chunks, void* stream);
+
 /* ---- sequence sharding across GPUs (BASELINE.json north_star) ----------- *
  * A sequence split into contiguous T-segments, one per rank.  Forward, rank r
  * (segment [S, E)):

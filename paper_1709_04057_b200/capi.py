@@ -83,6 +83,9 @@ def _load():
     lib.linrec_p2p_publish_f32.argtypes = [_vp, _i64, _int, _int, _int, C.c_uint64, _vp, _int, _int, _vp]
     lib.linrec_p2p_compose_f32.argtypes = [_i64, _int, _int, _int, C.c_uint64, _vp, _vp, _i64, _i64, _i64, _vp,
                                            _vp, _vp]
+    for s_ in ("f32", "f64"):
+        getattr(lib, f"linrec_scan_plan_{s_}").argtypes = [_vp] * 4 + [_i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp]
+        getattr(lib, f"linrec_scan_backward_plan_{s_}").argtypes = [_vp] * 7 + [_i64, _i64, _vp, _i64, _vp]
     _ex = C.POINTER(Exchange)
     lib.linrec_segment_scan_exchange_f32.argtypes = [_vp] * 6 + [_i64, _i64, _ex, _vp, _vp]
     lib.linrec_segment_scan_backward_exchange_f32.argtypes = [_vp] * 10 + [_i64, _i64, _ex, _vp, _vp]
@@ -189,6 +192,24 @@ def segment_fixup_backward(lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T,
                            stream=0):
     check(getattr(lib, f"linrec_segment_fixup_backward_{_sfx(dtype_bytes)}")(
         lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T, W, tile_rows, stream))
+
+
+# ---- the reference's chunked scan with an explicit plan ---------------------
+def _bounds(plan):
+    flat = (C.c_int64 * (2 * len(plan)))(*[v for se in plan for v in se])
+    return flat, len(plan)
+
+
+def scan_plan(lam, x, h0, h, T, W, plan, P=None, R=None, Cs=None, dtype_bytes=4, stream=0):
+    """plan: [(start, end), ...] 1-based inclusive (linrec.plan_chunks)."""
+    b, p = _bounds(plan)
+    check(getattr(lib, f"linrec_scan_plan_{_sfx(dtype_bytes)}")(lam, x, h0, h, T, W, b, p, P, R, Cs, stream))
+
+
+def scan_backward_plan(lam, h0, h, dh, dlam, dx, dh0, T, W, plan, dtype_bytes=4, stream=0):
+    b, p = _bounds(plan)
+    check(getattr(lib, f"linrec_scan_backward_plan_{_sfx(dtype_bytes)}")(lam, h0, h, dh, dlam, dx, dh0, T, W, b, p,
+                                                                         stream))
 
 
 # the same with the carry exchange fused into the stitch kernels (fp32; ex: Exchange)

@@ -623,6 +623,45 @@ int segment_fixup(bool reverse, const S* lam, const S* hprev, const S* h, const 
   return LINREC_OK;
 }
 
+// ChunkPlan checks of validate_plan (recurrence.hpp:84-94), same messages
+// (contract violations: LINREC_ERR_SHAPE, like a shape mismatch).
+int check_plan(const int64_t* bounds, int64_t p, int64_t T) {
+  if (!bounds || p < 1) return fail(LINREC_ERR_SHAPE, "ChunkPlan: no chunks");
+  if (bounds[0] != 1) return fail(LINREC_ERR_SHAPE, "ChunkPlan: first chunk must start at step 1");
+  if (bounds[2 * p - 1] != T) return fail(LINREC_ERR_SHAPE, "ChunkPlan: last chunk must end at step T");
+  for (int64_t i = 0; i < p; ++i) {
+    if (bounds[2 * i] > bounds[2 * i + 1]) return fail(LINREC_ERR_SHAPE, "ChunkPlan: chunk start exceeds end");
+    if (i + 1 < p && bounds[2 * i + 1] + 1 != bounds[2 * i + 2])
+      return fail(LINREC_ERR_SHAPE, "ChunkPlan: chunks must be contiguous");
+  }
+  return LINREC_OK;
+}
+
+// Stream-ordered scratch for the plan scans: the bounds on the device and
+// the summaries the caller did not ask for.
+template <class S>
+int plan_scan(bool reverse, const S* lam, const S* x_or_dh, const S* h0, const S* h, S* out, S* dlam, S* dh0,
+              int64_t T, int64_t W, const int64_t* bounds, int64_t p, S* P, S* R, S* C, cudaStream_t st) {
+  int rc;
+  if ((rc = check_dims(T, W)) || (rc = check_plan(bounds, p, T))) return rc;
+  const size_t bb = sizeof(int64_t) * 2 * (size_t)p, sb = sizeof(S) * (size_t)(p * W);
+  char* tmp = nullptr;
+  const size_t need = bb + (P ? 0 : sb) + (R ? 0 : sb) + (C ? 0 : sb) + 64;
+  LINREC_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&tmp), need, st));
+  int64_t* bd = reinterpret_cast<int64_t*>(tmp);
+  char* q = tmp + (bb + 15) / 16 * 16;
+  if (!P) { P = reinterpret_cast<S*>(q); q += sb; }
+  if (!R) { R = reinterpret_cast<S*>(q); q += sb; }
+  if (!C) { C = reinterpret_cast<S*>(q); q += sb; }
+  cudaError_t e = cudaMemcpyAsync(bd, bounds, bb, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = linrec_impl::launch_plan_scan<S>(reverse, lam, x_or_dh, h0, h, out, dlam, dh0, T, W, bd, p, P, R, C, st);
+  const cudaError_t ef = cudaFreeAsync(tmp, st);
+  LINREC_CUDA_TRY(e);
+  LINREC_CUDA_TRY(ef);
+  return LINREC_OK;
+}
+
 template <class S>
 int first_nonfinite(const S* v, int64_t n, int64_t* index, cudaStream_t st) {
   int rc;
@@ -827,6 +866,41 @@ int linrec_segment_fixup_backward_f64(const double* lam, const double* hprev, co
                                       void* stream) {
   return segment_fixup<double>(true, lam, hprev, h, lam_next, seg_prod, y_in, dx, dlam, T, W, tile_rows,
                                static_cast<cudaStream_t>(stream));
+}
+
+int linrec_scan_plan_f32(const float* lam, const float* x, const float* h0, float* h, int64_t T, int64_t W,
+                         const int64_t* bounds, int64_t chunks, float* P, float* R, float* C, void* stream) {
+  int rc;
+  if ((rc = check_ptr(lam, "decays")) || (rc = check_ptr(x, "impulses")) || (rc = check_ptr(h, "h"))) return rc;
+  return plan_scan<float>(false, lam, x, h0, nullptr, h, nullptr, nullptr, T, W, bounds, chunks, P, R, C,
+                          static_cast<cudaStream_t>(stream));
+}
+int linrec_scan_plan_f64(const double* lam, const double* x, const double* h0, double* h, int64_t T, int64_t W,
+                         const int64_t* bounds, int64_t chunks, double* P, double* R, double* C, void* stream) {
+  int rc;
+  if ((rc = check_ptr(lam, "decays")) || (rc = check_ptr(x, "impulses")) || (rc = check_ptr(h, "h"))) return rc;
+  return plan_scan<double>(false, lam, x, h0, nullptr, h, nullptr, nullptr, T, W, bounds, chunks, P, R, C,
+                           static_cast<cudaStream_t>(stream));
+}
+int linrec_scan_backward_plan_f32(const float* lam, const float* h0, const float* h, const float* dh, float* dlam,
+                                  float* dx, float* dh0, int64_t T, int64_t W, const int64_t* bounds,
+                                  int64_t chunks, void* stream) {
+  int rc;
+  if ((rc = check_ptr(lam, "decays")) || (rc = check_ptr(h, "h")) || (rc = check_ptr(dh, "d_h")) ||
+      (rc = check_ptr(dlam, "d_decays")) || (rc = check_ptr(dx, "d_impulses")) || (rc = check_ptr(dh0, "d_initial")))
+    return rc;
+  return plan_scan<float>(true, lam, dh, h0, h, dx, dlam, dh0, T, W, bounds, chunks, nullptr, nullptr, nullptr,
+                          static_cast<cudaStream_t>(stream));
+}
+int linrec_scan_backward_plan_f64(const double* lam, const double* h0, const double* h, const double* dh,
+                                  double* dlam, double* dx, double* dh0, int64_t T, int64_t W,
+                                  const int64_t* bounds, int64_t chunks, void* stream) {
+  int rc;
+  if ((rc = check_ptr(lam, "decays")) || (rc = check_ptr(h, "h")) || (rc = check_ptr(dh, "d_h")) ||
+      (rc = check_ptr(dlam, "d_decays")) || (rc = check_ptr(dx, "d_impulses")) || (rc = check_ptr(dh0, "d_initial")))
+    return rc;
+  return plan_scan<double>(true, lam, dh, h0, h, dx, dlam, dh0, T, W, bounds, chunks, nullptr, nullptr, nullptr,
+                           static_cast<cudaStream_t>(stream));
 }
 
 int linrec_segment_scan_exchange_f32(const float* lam, const float* x, const float* h0, float* h, float* seg_prod,

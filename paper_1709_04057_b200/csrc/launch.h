@@ -186,4 +186,13 @@ int gemm_splits_for(int64_t M, int64_t N, int64_t K);
 // split-K partial buffer (floats) gemm_tf32 needs for `splits` splits (0 for 1)
 int64_t gemm_partial_floats(int64_t M, int64_t N, int splits);
 
+// The reference's chunked scan with an explicit plan (plan_scan.cu): phases
+// 1-3 bit-identical to recurrence.hpp's scan_parallel; reverse = the
+// backward's reversed image (x_or_dh = dh, out = dx, plus dlam and dh0).
+// bounds_dev: p (start, end) 1-based pairs in device memory; P, R, C [p][W].
+template <class S>
+cudaError_t launch_plan_scan(bool reverse, const S* lam, const S* x_or_dh, const S* h0, const S* h, S* out,
+                             S* dlam, S* dh0, int64_t T, int64_t W, const int64_t* bounds_dev, int64_t p, S* P,
+                             S* R, S* C, cudaStream_t st);
+
 }  // namespace linrec_impl

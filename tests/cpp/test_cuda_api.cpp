@@ -208,6 +208,56 @@ static void test_qrnn() {
   }
 }
 
+// scan_parallel with an explicit plan and ScanSummaries: the reference's
+// hand-executed two-chunk example (test_recurrence.cpp:75-99), and the
+// plan-chunked forward against the fmaf restatement of its three phases.
+static void test_plan_scan() {
+  {
+    Dev L(std::vector<float>{1, 1, 1, 1}), X(std::vector<float>{1, 1, 1, 1}), H0(std::vector<float>{0});
+    Dev H(4), P(2), R(2), C(2);
+    DeviceTensor3<float> l{L.p, 4, 1, 1}, x{X.p, 4, 1, 1}, h{H.p, 4, 1, 1};
+    DeviceTensor2<float> i0{H0.p, 1, 1};
+    ScanSummaries<float> s{{P.p, 2, 1, 1}, {R.p, 2, 1, 1}, {C.p, 2, 1, 1}};
+    const ChunkPlan plan = plan_chunks(4, 2);
+    scan_parallel(l, x, i0, plan, h, &s);
+    cudaDeviceSynchronize();
+    CHECK(P.get() == (std::vector<float>{1, 1}) && R.get() == (std::vector<float>{2, 2}) &&
+              C.get() == (std::vector<float>{2, 4}) && H.get() == (std::vector<float>{1, 2, 3, 4}),
+          "two-chunk example: P, R, C or h differ");
+  }
+  const index_t T = 1001, W = 37;
+  auto lam = uniform(T * W, -1, 1, 11), x = uniform(T * W, -1, 1, 12), h0 = uniform(W, -1, 1, 13);
+  Dev L(lam), X(x), H0(h0), H(T * W);
+  DeviceTensor3<float> l{L.p, T, 1, W}, xx{X.p, T, 1, W}, h{H.p, T, 1, W};
+  DeviceTensor2<float> i0{H0.p, 1, W};
+  const ChunkPlan plan = plan_chunks(T, 6);
+  scan_parallel(l, xx, i0, plan, h);
+  std::vector<float> ref(T * W), C(W);
+  for (index_t j = 0; j < W; ++j) C[j] = h0[j];
+  for (const auto& se : plan.bounds) {  // phases 1-2 then 3, per chunk in order
+    for (index_t j = 0; j < W; ++j) {
+      float P = 1.f, R = 0.f;
+      for (index_t t = se.first - 1; t <= se.second - 1; ++t) {
+        R = std::fmaf(lam[t * W + j], R, x[t * W + j]);
+        P = P * lam[t * W + j];
+      }
+      float c = C[j];
+      for (index_t t = se.first - 1; t <= se.second - 1; ++t) ref[t * W + j] = c = std::fmaf(lam[t * W + j], c, x[t * W + j]);
+      C[j] = std::fmaf(P, C[j], R);
+    }
+  }
+  CHECK(H.get() == ref, "plan scan_parallel is not bit-identical to the three-phase fmaf restatement");
+  try {
+    ChunkPlan bad = plan;
+    bad.bounds[0].second += 1;
+    scan_parallel(l, xx, i0, bad, h);
+    CHECK(false, "a gap in the plan did not throw");
+  } catch (const ContractViolation& e) {
+    CHECK(std::string(e.what()).find("ChunkPlan: chunks must be contiguous") != std::string::npos, "message: %s",
+          e.what());
+  }
+}
+
 int main() {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -215,6 +265,7 @@ int main() {
     return 2;
   }
   test_scans();
+  test_plan_scan();
   test_gilr_lstm();
   test_qrnn();
   if (failures == 0) std::printf("ALL OK\n");
