@@ -181,6 +181,12 @@ int linrec_first_nonfinite_f32(const float* v, int64_t n, int64_t* index,
 int linrec_first_nonfinite_f64(const double* v, int64_t n, int64_t* index,
                                void* stream);
 
+/* Kernels one linrec_scan_* (backward = 0) / linrec_scan_backward_* call
+ * launches for this shape and mode with 16-byte aligned buffers (1, or 3 when
+ * the sequence is split into virtual segments: scan, fold, fix-up); -1 for
+ * invalid arguments.  For launch accounting (bench.py's gpu_launches). */
+int linrec_scan_kernel_count(int64_t T, int64_t W, int dtype_bytes, int backward, int mode);
+
 /* ---- the reference's chunked scan with an explicit plan ----------------- *
  * scan_parallel(decays, impulses, initial, plan, pool, check_finite,
  * summaries) (recurrence.hpp:193-245) and scan_backward(in, h, d_h, plan,

@@ -86,6 +86,7 @@ def _load():
     for s_ in ("f32", "f64"):
         getattr(lib, f"linrec_scan_plan_{s_}").argtypes = [_vp] * 4 + [_i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp]
         getattr(lib, f"linrec_scan_backward_plan_{s_}").argtypes = [_vp] * 7 + [_i64, _i64, _vp, _i64, _vp]
+    lib.linrec_scan_kernel_count.argtypes = [_i64, _i64, _int, _int, _int]
     _ex = C.POINTER(Exchange)
     lib.linrec_segment_scan_exchange_f32.argtypes = [_vp] * 6 + [_i64, _i64, _ex, _vp, _vp]
     lib.linrec_segment_scan_backward_exchange_f32.argtypes = [_vp] * 10 + [_i64, _i64, _ex, _vp, _vp]
@@ -192,6 +193,11 @@ def segment_fixup_backward(lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T,
                            stream=0):
     check(getattr(lib, f"linrec_segment_fixup_backward_{_sfx(dtype_bytes)}")(
         lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T, W, tile_rows, stream))
+
+
+def scan_kernel_count(T, W, backward=False, mode=PARALLEL, dtype_bytes=4) -> int:
+    """Kernels one scan (or scan_backward) call launches for this shape."""
+    return int(lib.linrec_scan_kernel_count(T, W, dtype_bytes, 1 if backward else 0, mode))
 
 
 # ---- the reference's chunked scan with an explicit plan ---------------------

@@ -868,6 +868,21 @@ int linrec_segment_fixup_backward_f64(const double* lam, const double* hprev, co
                                static_cast<cudaStream_t>(stream));
 }
 
+int linrec_scan_kernel_count(int64_t T, int64_t W, int dtype_bytes, int backward, int mode) {
+  if (T < 1 || W < 1 || (dtype_bytes != 4 && dtype_bytes != 8)) return -1;
+  const bool f64 = dtype_bytes == 8;
+  const bool vok = W % (f64 ? vec_of<double>() : vec_of<float>()) == 0;  // aligned buffers assumed
+  if (mode == LINREC_SERIAL ||
+      (f64 ? channel_parallel_enough<double>(T, W, vok) : channel_parallel_enough<float>(T, W, vok)))
+    return 1;
+  ChainPlan p;
+  const bool fwd = backward == 0;
+  const bool tma = vok && tma_allowed(T, W) &&
+                   (f64 ? linrec_impl::plan_tma<double>(fwd, T, W, &p) : linrec_impl::plan_tma<float>(fwd, T, W, &p));
+  if (!tma) p = f64 ? linrec_impl::plan_chain<double>(fwd, T, W, vok) : linrec_impl::plan_chain<float>(fwd, T, W, vok);
+  return p.nseg > 1 ? 3 : 1;  // the scan, plus the virtual-segment fold and fix-up
+}
+
 int linrec_scan_plan_f32(const float* lam, const float* x, const float* h0, float* h, int64_t T, int64_t W,
                          const int64_t* bounds, int64_t chunks, float* P, float* R, float* C, void* stream) {
   int rc;
