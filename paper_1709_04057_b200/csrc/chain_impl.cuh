@@ -38,6 +38,12 @@ inline int pick_q(int64_t nvec) {
 // of their best), the backward -- 20 B/el per tile, so the look-back is
 // already hidden -- at 64.  LINREC_CHAINS / LINREC_CHAINS_FWD /
 // LINREC_CHAINS_BWD override.
+inline bool chains_overridden() {
+  static const bool any = std::getenv("LINREC_CHAINS") || std::getenv("LINREC_CHAINS_FWD") ||
+                          std::getenv("LINREC_CHAINS_BWD");
+  return any;
+}
+
 inline int64_t chain_target(bool forward) {
   static const long env_all = [] { const char* e = std::getenv("LINREC_CHAINS"); return e ? std::atol(e) : 0L; }();
   static const long env_fwd = [] { const char* e = std::getenv("LINREC_CHAINS_FWD"); return e ? std::atol(e) : 0L; }();
@@ -48,11 +54,18 @@ inline int64_t chain_target(bool forward) {
   return forward ? 256 : 64;
 }
 
+// Chains shorter than this many tiles stay whole: below it the stitch (fold
+// + fix-up launches) costs more than the look-back latency it removes
+// (scripts/dev/split_sweep.py: 43 tiles -- C1 -- 36 -> 29 us forward whole,
+// 171 tiles 65 -> 41 us split).
+constexpr int64_t kMinSplitTiles = 64;
+
 inline void choose_segments(ChainPlan& p, int64_t T, bool forward) {
   const int64_t ntt_total = (T + p.rows - 1) / p.rows;
   const int64_t target = chain_target(forward);
   int64_t nseg = (target + p.ncols - 1) / p.ncols;
   if (nseg > ntt_total / 8) nseg = ntt_total / 8;
+  if (ntt_total < kMinSplitTiles && !chains_overridden()) nseg = 1;
   if (nseg < 1) nseg = 1;
   const int64_t per = (ntt_total + nseg - 1) / nseg;
   p.ntt = per;
