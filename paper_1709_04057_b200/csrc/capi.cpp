@@ -238,13 +238,10 @@ int scan_device(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t 
   }
   if (tma) LINREC_CUDA_TRY(linrec_impl::launch_tma_fwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_fwd<S>(p, c, ws_ptrs(w, p), st));
-  if (p.nseg > 1) {
-    LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, vs.vagg, p.nseg, p.tseg, vs.carry, nullptr,
-                                                         nullptr, nullptr, W, st));
-    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(false, lam, nullptr, nullptr, nullptr, vs.seg_prod, vs.carry,
+  if (p.nseg > 1)  // one stitch launch: each fix-up CTA folds its own segment's carry from vagg
+    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(false, lam, nullptr, nullptr, nullptr, vs.seg_prod, nullptr,
                                                  nullptr, nullptr, h, nullptr, T, W, p.rows, p.nseg, p.tseg, p.ntt,
-                                                 vok, st));
-  }
+                                                 vok, st, nullptr, nullptr, vs.vagg));
   return LINREC_OK;
 }
 
@@ -280,12 +277,10 @@ int scan_backward_device(const S* lam, const S* h0, const S* h, const S* dh, con
   }
   if (tma) LINREC_CUDA_TRY(linrec_impl::launch_tma_bwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_bwd<S>(p, c, ws_ptrs(w, p), st));
-  if (p.nseg > 1) {
-    LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, vs.vagg, p.nseg, p.tseg, vs.carry, nullptr,
-                                                         nullptr, dh0, W, st));
-    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(true, lam, h0, h, lam_next, vs.seg_prod, vs.carry, nullptr,
-                                                 nullptr, dx, dlam, T, W, p.rows, p.nseg, p.tseg, p.ntt, vok, st));
-  }
+  if (p.nseg > 1)  // dh0 gets its correction from the fix-up that owns row 0
+    LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(true, lam, h0, h, lam_next, vs.seg_prod, nullptr, nullptr,
+                                                 nullptr, dx, dlam, T, W, p.rows, p.nseg, p.tseg, p.ntt, vok, st,
+                                                 nullptr, nullptr, vs.vagg, dh0));
   return LINREC_OK;
 }
 
@@ -880,7 +875,7 @@ int linrec_scan_kernel_count(int64_t T, int64_t W, int dtype_bytes, int backward
   const bool tma = vok && tma_allowed(T, W) &&
                    (f64 ? linrec_impl::plan_tma<double>(fwd, T, W, &p) : linrec_impl::plan_tma<float>(fwd, T, W, &p));
   if (!tma) p = f64 ? linrec_impl::plan_chain<double>(fwd, T, W, vok) : linrec_impl::plan_chain<float>(fwd, T, W, vok);
-  return p.nseg > 1 ? 3 : 1;  // the scan, plus the virtual-segment fold and fix-up
+  return p.nseg > 1 ? 2 : 1;  // the scan, plus the fix-up that stitches the virtual segments
 }
 
 int linrec_scan_plan_f32(const float* lam, const float* x, const float* h0, float* h, int64_t T, int64_t W,

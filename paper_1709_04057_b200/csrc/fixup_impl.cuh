@@ -38,6 +38,7 @@ struct FixupArgs {
   S* out0;             // fwd: h; bwd: dx
   S* out1;             // bwd: dlam (nullable)
   int64_t T, W, rows, nseg, tseg, ntt;
+  S* dh0 = nullptr;    // bwd: dh0 += lam_0 * (correction of G_0) (when the fix-up owns the fold)
 };
 
 // The carry entering each virtual segment: its own (the fold of the earlier
@@ -49,6 +50,10 @@ struct Carries {
   const S* rows;   // [nseg][W]
   const S* scale;  // [nseg][W]
   const S* cin;    // [W]
+  // instead of rows: the segments' aggregates [nseg][2][W] (P_incl, c_incl),
+  // folded by each fix-up CTA for its own segment (fold_carry) into `own`
+  const S* vagg = nullptr;
+  const S* own = nullptr;  // indexed by channel (shared memory: generic loads)
 };
 
 // Entering correction of chain position p_in of (vseg, channels ch..): the
@@ -59,7 +64,12 @@ __device__ __forceinline__ bool entering(const FixupArgs<S>& f, int64_t vseg, in
   using IO = VecIO<S, VEC>;
   S p[VEC], c[VEC], sc[VEC], ci[VEC];
   IO::load_cg(f.seg_prod + (vseg * f.ntt + p_in) * f.W + ch, p);
-  if (cr.rows != nullptr) IO::load_cg(cr.rows + vseg * f.W + ch, c);
+  if (cr.own != nullptr) {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) c[v] = cr.own[ch + v];
+  } else if (cr.rows != nullptr) {
+    IO::load_cg(cr.rows + vseg * f.W + ch, c);
+  }
   if (cr.cin != nullptr) {  // cin may live in shared memory (composed in-kernel): generic loads
     IO::load_cg(cr.scale + vseg * f.W + ch, sc);
 #pragma unroll
@@ -68,7 +78,7 @@ __device__ __forceinline__ bool entering(const FixupArgs<S>& f, int64_t vseg, in
   bool nz = false;
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
-    if (cr.rows == nullptr) c[v] = S(0);
+    if (cr.rows == nullptr && cr.own == nullptr) c[v] = S(0);
     if (cr.cin != nullptr) c[v] = fma_(sc[v], ci[v], c[v]);
     e[v] = mul_(p[v], c[v]);
     nz = nz || e[v] != S(0);
@@ -194,6 +204,17 @@ __device__ __forceinline__ bool fixup_position(const FixupArgs<S>& f, int64_t vs
         ecur[v] = mul_(m[i][v], ecur[v]);
         m[i][v] = ecur[v];
       }
+    if (REV && f.dh0 != nullptr && t0 < RF && (int)t0 >= ilo && (int)t0 < ihi) {  // this thread holds row 0
+      S l0[VEC], d[VEC];
+      IO::load_cg(f.lam + ch, l0);
+      IO::load_cg(f.dh0 + ch, d);
+#pragma unroll
+      for (int i = 0; i < RF; ++i)
+        if (i == (int)t0)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) d[v] = fma_(l0[v], m[i][v], d[v]);
+      IO::store_cg(f.dh0 + ch, d);
+    }
     if (!dl) {
 #pragma unroll
       for (int i = 0; i < RF; ++i)
@@ -246,6 +267,60 @@ __device__ __forceinline__ bool fixup_position(const FixupArgs<S>& f, int64_t vs
   }
   Sync::sync();  // s_wp is reused by the next position
   return true;
+}
+
+// The carry entering virtual segment vseg for this thread's channels: the
+// fold of the aggregates of the segments before it (forward: 0 .. vseg-1;
+// backward, from the top: nseg-1 .. vseg+1 with each pair scaled by the
+// decay at its segment's first row, as vseg_pair), c = A c + B from 0.  The
+// 8*G walkers of the team fold contiguous groups, combined in walker order
+// through shared memory s_a / s_b [8*G][CPW] (fixed association).
+template <class S, int VEC, int Q, bool REV, class Sync>
+__device__ __forceinline__ void fold_carry(const FixupArgs<S>& f, const S* __restrict__ vagg, int64_t vseg,
+                                           int64_t col, S* s_a, S* s_b, S (&carry)[VEC]) {
+  constexpr int G = 32 / Q, CPW = Q * VEC, NWK = 8 * G;
+  using IO = VecIO<S, VEC>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane % Q, k = warp * G + lane / Q;
+  const int64_t ch = col * CPW + (int64_t)q * VEC;
+  const bool valid = ch < f.W;
+  const int64_t n = REV ? f.nseg - 1 - vseg : vseg;  // segments to fold
+  const int64_t per = (n + NWK - 1) / NWK;
+  const int64_t i0 = k * per, i1 = i0 + per < n ? i0 + per : n;
+  S A[VEC], B[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) { A[v] = S(1); B[v] = S(0); }
+  if (valid)
+#pragma unroll 8
+    for (int64_t i = i0; i < i1; ++i) {  // unrolled: the pairs' loads are in flight together
+      const int64_t sg = REV ? f.nseg - 1 - i : i;
+      S a[VEC], b[VEC];
+      IO::load_cg(vagg + sg * 2 * f.W + ch, a);
+      IO::load_cg(vagg + sg * 2 * f.W + f.W + ch, b);
+      if (REV) {
+        S l0[VEC];
+        IO::load_cg(f.lam + (sg * f.tseg) * f.W + ch, l0);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) { a[v] = mul_(l0[v], a[v]); b[v] = mul_(l0[v], b[v]); }
+      }
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        B[v] = fma_(a[v], B[v], b[v]);
+        A[v] = mul_(a[v], A[v]);
+      }
+    }
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    s_a[k * CPW + q * VEC + v] = A[v];
+    s_b[k * CPW + q * VEC + v] = B[v];
+  }
+  Sync::sync();
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) carry[v] = S(0);
+  for (int w = 0; w < NWK; ++w)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) carry[v] = fma_(s_a[w * CPW + q * VEC + v], carry[v], s_b[w * CPW + q * VEC + v]);
+  Sync::sync();  // s_a / s_b reusable
 }
 
 // Fix-up of chain (vseg, col) by walker j of J: positions p_lo + j, + J, ...

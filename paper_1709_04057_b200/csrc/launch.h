@@ -127,7 +127,8 @@ template <class S>
 cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S* h, const S* lam_next,
                          const S* seg_prod, const S* carry_rows, const S* scale_rows, const S* cin, S* out0, S* out1,
                          int64_t T, int64_t W, int64_t rows, int64_t nseg, int64_t tseg, int64_t ntt,
-                         bool vec_ok, cudaStream_t st, const Exchange* ex = nullptr, S* c_out = nullptr);
+                         bool vec_ok, cudaStream_t st, const Exchange* ex = nullptr, S* c_out = nullptr,
+                         const S* vagg = nullptr, S* dh0 = nullptr);
 template <class S>
 cudaError_t launch_vseg_finalize(bool reverse, const S* lam, const S* vagg, int64_t nseg, int64_t tseg,
                                  S* carry, S* scale, S* agg_rank, S* dh0, int64_t W, cudaStream_t st,

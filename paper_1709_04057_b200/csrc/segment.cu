@@ -34,9 +34,11 @@ template <class S, int VEC, int Q, bool REV>
 __global__ void __launch_bounds__(256, REV ? 1 : 2)  // backward: dx, dlam, h rows in flight
 k_fixup(FixupArgs<S> f, Carries<S> cr, int64_t ncols, int walkers, linrec_impl::Exchange ex,
         S* __restrict__ c_out) {
-  constexpr int CPW = Q * VEC;
+  constexpr int CPW = Q * VEC, NWK = 8 * (32 / Q);
   __shared__ S s_wp[8][CPW];
   __shared__ S s_cin[CPW];
+  __shared__ S s_own[CPW];
+  __shared__ S s_fa[NWK * CPW], s_fb[NWK * CPW];
   const int64_t col = blockIdx.x % ncols;
   const int j = (int)((blockIdx.x / ncols) % walkers);
   const int64_t vseg = (blockIdx.x / ncols) / walkers;
@@ -47,6 +49,16 @@ k_fixup(FixupArgs<S> f, Carries<S> cr, int64_t ncols, int walkers, linrec_impl::
         for (int t = threadIdx.x; t < CPW && col * CPW + t < f.W; t += blockDim.x) c_out[col * CPW + t] = s_cin[t];
       cr.cin = s_cin - col * CPW;  // indexed by channel
     }
+  }
+  if (cr.vagg != nullptr) {  // the segment's own carry, folded here instead of a separate launch
+    S c[VEC];
+    fold_carry<S, VEC, Q, REV, CtaSync>(f, cr.vagg, vseg, col, s_fa, s_fb, c);
+    const int q = (threadIdx.x & 31) % Q;
+    if (threadIdx.x < 32 && threadIdx.x < Q)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) s_own[q * VEC + v] = c[v];
+    __syncthreads();
+    cr.own = s_own - col * CPW;  // indexed by channel
   }
   fixup_chain<S, VEC, Q, REV, CtaSync>(f, vseg, col, j, walkers, cr, s_wp);
 }
@@ -91,7 +103,7 @@ template <class S>
 cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S* h, const S* lam_next,
                          const S* seg_prod, const S* carry_rows, const S* scale_rows, const S* cin, S* out0, S* out1,
                          int64_t T, int64_t W, int64_t rows, int64_t nseg, int64_t tseg, int64_t ntt,
-                         bool vec_ok, cudaStream_t st, const Exchange* ex, S* c_out) {
+                         bool vec_ok, cudaStream_t st, const Exchange* ex, S* c_out, const S* vagg, S* dh0) {
   const Exchange exv = ex != nullptr ? *ex : Exchange{};
   constexpr int V = Tuning<S>::VEC;
   const int64_t nvec = vec_ok ? (W + V - 1) / V : W;
@@ -100,8 +112,10 @@ cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S
   const int64_t ncols = (W + cpw - 1) / cpw;
   const int walk = fixup_walkers();
   const dim3 grid((unsigned)(ncols * nseg * walk));
-  const linrec_dev::FixupArgs<S> fa{lam, hprev_row, h, lam_next, seg_prod, out0, out1, T, W, rows, nseg, tseg, ntt};
-  const linrec_dev::Carries<S> cr{carry_rows, scale_rows, cin};
+  linrec_dev::FixupArgs<S> fa{lam, hprev_row, h, lam_next, seg_prod, out0, out1, T, W, rows, nseg, tseg, ntt};
+  fa.dh0 = dh0;
+  linrec_dev::Carries<S> cr{carry_rows, scale_rows, cin};
+  cr.vagg = vagg;
 #define FIX(VV)                                                                                       \
   LINREC_Q_SWITCH(q, if (reverse) linrec_dev::k_fixup<S, VV, Q_, true><<<grid, 256, 0, st>>>(         \
                          fa, cr, ncols, walk, exv, c_out);                                \
@@ -141,12 +155,12 @@ cudaError_t launch_compose(const S* aggs, int64_t first, int64_t last, int64_t s
 template cudaError_t launch_fixup<float>(bool, const float*, const float*, const float*, const float*, const float*,
                                          const float*, const float*, const float*, float*, float*, int64_t, int64_t,
                                          int64_t, int64_t, int64_t, int64_t, bool, cudaStream_t, const Exchange*,
-                                         float*);
+                                         float*, const float*, float*);
 template cudaError_t launch_fixup<double>(bool, const double*, const double*, const double*, const double*,
                                           const double*, const double*, const double*, const double*, double*,
                                           double*,
                                           int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, bool, cudaStream_t,
-                                          const Exchange*, double*);
+                                          const Exchange*, double*, const double*, double*);
 template cudaError_t launch_compose<float>(const float*, int64_t, int64_t, int64_t, const float*, float*,
                                            int64_t, cudaStream_t);
 template cudaError_t launch_compose<double>(const double*, int64_t, int64_t, int64_t, const double*, double*,
