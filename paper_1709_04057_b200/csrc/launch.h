@@ -49,10 +49,14 @@ inline int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
 }
-// CTAs per (segment, column) chain of the stitch fix-up (fixup_chain).
-inline int fixup_walkers() {
-  static const int k = env_int("LINREC_FIXUP_WALK", 2);
-  return k < 1 ? 1 : (k > 8 ? 8 : k);
+// CTAs per (segment, column) chain of the stitch fix-up (fixup_chain): the
+// forward's many segments fit one wave of resident CTAs with one walker
+// each, the backward's fewer segments gain from two (C4);
+// LINREC_FIXUP_WALK overrides both.
+inline int fixup_walkers(bool reverse) {
+  static const int k = env_int("LINREC_FIXUP_WALK", 0);
+  if (k > 0) return k > 8 ? 8 : k;
+  return reverse ? 2 : 1;
 }
 
 // One direction of the peer-memory carry exchange as this rank sees it

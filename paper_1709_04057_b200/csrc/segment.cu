@@ -110,7 +110,7 @@ cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S
   const int q = pick_q(nvec);
   const int cpw = q * (vec_ok ? V : 1);
   const int64_t ncols = (W + cpw - 1) / cpw;
-  const int walk = fixup_walkers();
+  const int walk = fixup_walkers(reverse);
   const dim3 grid((unsigned)(ncols * nseg * walk));
   linrec_dev::FixupArgs<S> fa{lam, hprev_row, h, lam_next, seg_prod, out0, out1, T, W, rows, nseg, tseg, ntt};
   fa.dh0 = dh0;
