@@ -140,19 +140,18 @@ ChainPtrs ws_ptrs(linrec_workspace* ws, const ChainPlan& p) {
   return w;
 }
 
-// Virtual-segment region, after the look-back records: vagg [nseg][2][W],
-// carry [nseg][W], scale [nseg][W], seg_prod [nseg*ntt][W].
+// Virtual-segment region, after the look-back records: vagg [nseg][2][W]
+// (each segment's chain aggregate) and seg_prod [nseg*ntt][W] (the products
+// entering its chain positions); the fix-up folds the carries from vagg.
 template <class S>
 struct VsegPtrs {
   S* vagg;
-  S* carry;
-  S* scale;
   S* seg_prod;
 };
 
 template <class S>
 size_t vseg_region_bytes(const ChainPlan& p, int64_t W) {
-  return sizeof(S) * (size_t)W * (size_t)(4 * p.nseg + p.nseg * p.ntt) + 1024;
+  return sizeof(S) * (size_t)W * (size_t)(2 * p.nseg + p.nseg * p.ntt) + 1024;
 }
 
 template <class S>
@@ -162,9 +161,7 @@ VsegPtrs<S> vseg_ptrs(linrec_workspace* ws, const ChainPlan& p, int64_t W) {
   S* v = reinterpret_cast<S*>(b);
   VsegPtrs<S> r;
   r.vagg = v;
-  r.carry = v + 2 * p.nseg * W;
-  r.scale = r.carry + p.nseg * W;
-  r.seg_prod = r.scale + p.nseg * W;
+  r.seg_prod = v + 2 * p.nseg * W;
   return r;
 }
 

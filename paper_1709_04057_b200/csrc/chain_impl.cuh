@@ -74,12 +74,12 @@ inline void choose_segments(ChainPlan& p, int64_t T, bool forward) {
   p.ntiles = p.ncols * p.nseg * p.ntt;
 }
 
-// Extra workspace of a virtually segmented launch: vagg [nseg][2][W], carry,
-// scale [nseg][W] and the internal seg_prod [nseg*ntt][W].
+// Extra workspace of a virtually segmented launch: vagg [nseg][2][W] and the
+// internal seg_prod [nseg*ntt][W] (capi.cpp::vseg_ptrs).
 template <class S>
 size_t vseg_bytes(const ChainPlan& p, int64_t W) {
   if (p.nseg <= 1) return 0;
-  return sizeof(S) * (size_t)W * (size_t)(4 * p.nseg + p.nseg * p.ntt) + 1024;
+  return sizeof(S) * (size_t)W * (size_t)(2 * p.nseg + p.nseg * p.ntt) + 1024;
 }
 
 template <class S, int VEC, int Q, int R, int NW>
