@@ -234,8 +234,10 @@ int linrec_scan_backward_plan_f64(const double* lam, const double* h0, const dou
  *      R-1 .. r+1 into y_in; 4. linrec_segment_fixup_backward_* on every
  *      rank (y_in = NULL on the last) adds P'_t*y to dx and h_{t-1}*P'_t*y to
  *      dlam; rank 0's dh0 = A'_0*y_in + B'_0 (compose with seed y_in).
- * seg_prod holds linrec_segment_prod_rows(...) rows of W values; pass
- * linrec_segment_tile_rows(...) to the fix-up.  Buffers 16-byte aligned when
+ * seg_prod holds linrec_segment_prod_rows(...) rows of W values (the decay
+ * products entering each chain position of the scan's virtual segments, then
+ * those segments' aggregates, from which the fix-up folds each virtual
+ * segment's carry); pass linrec_segment_tile_rows(...) to the fix-up.  Buffers 16-byte aligned when
  * W is a multiple of 4 (fp32) / 2 (fp64). */
 int64_t linrec_segment_prod_rows(int64_t T, int64_t W, int dtype_bytes, int backward);
 int64_t linrec_segment_tile_rows(int64_t T, int64_t W, int dtype_bytes, int backward);

@@ -494,14 +494,12 @@ ChainPlan plan_segment(bool forward, int64_t T, int64_t W) {
   return p;
 }
 
-// seg_prod layout: [nseg*ntt] position rows, [nseg] scale rows, [nseg] carry rows
+// seg_prod layout: [nseg*ntt] position rows, then the virtual segments'
+// aggregates [nseg][2][W] (vagg: the fix-up folds every segment's carry and
+// scale from them, so they travel with seg_prod from the scan to the fix-up)
 template <class P>
-P seg_scale_rows(P seg_prod, const ChainPlan& p, int64_t W) {
+P seg_vagg_rows(P seg_prod, const ChainPlan& p, int64_t W) {
   return seg_prod + p.nseg * p.ntt * W;
-}
-template <class P>
-P seg_carry_rows(P seg_prod, const ChainPlan& p, int64_t W) {
-  return seg_prod + p.nseg * (p.ntt + 1) * W;
 }
 
 // linrec_exchange_t -> the internal descriptor of one direction (p2p_impl.cuh)
@@ -553,16 +551,14 @@ int segment_scan(const S* lam, const S* x, const S* h0, S* h, S* seg_prod, S* ag
   linrec_workspace* w = ws ? ws : default_ws(dev, st);
   std::lock_guard<std::mutex> lk(w->mu);
   if ((rc = ws_reserve(w, p.ws_bytes, st))) return rc;
-  if ((rc = ws_reserve(w, p.ws_bytes + vseg_region_bytes<S>(p, W), st))) return rc;
-  const VsegPtrs<S> vs = vseg_ptrs<S>(w, p, W);
-  FwdCall<S> c{lam, x, h0, h, T, W, seg_prod, vs.vagg};
+  FwdCall<S> c{lam, x, h0, h, T, W, seg_prod, seg_vagg_rows(seg_prod, p, W)};
   if (p.kind == 1) LINREC_CUDA_TRY(linrec_impl::launch_tma_fwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_fwd<S>(p, c, ws_ptrs(w, p), st));
-  // the segment-level aggregate, and the virtual segments' scale and own
-  // carry rows (seg_prod's tail) for the fix-up, which applies both at once
-  // (with an exchange, also stored straight into the consumers' mailboxes)
-  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, vs.vagg, p.nseg, p.tseg, seg_carry_rows(seg_prod, p, W),
-                                                       seg_scale_rows(seg_prod, p, W), agg, nullptr, W, st, ex));
+  // the segment-level aggregate for the exchange (with a peer exchange also
+  // stored straight into the consumers' mailboxes); the fix-up folds the
+  // virtual segments' carries itself
+  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, c.agg_out, p.nseg, p.tseg, nullptr, nullptr, agg,
+                                                       nullptr, W, st, ex));
   return LINREC_OK;
 }
 
@@ -584,14 +580,12 @@ int segment_scan_backward(const S* lam, const S* hprev, const S* h, const S* dh,
   linrec_workspace* w = ws ? ws : default_ws(dev, st);
   std::lock_guard<std::mutex> lk(w->mu);
   if ((rc = ws_reserve(w, p.ws_bytes, st))) return rc;
-  if ((rc = ws_reserve(w, p.ws_bytes + vseg_region_bytes<S>(p, W), st))) return rc;
-  const VsegPtrs<S> vs = vseg_ptrs<S>(w, p, W);
-  BwdCall<S> c{lam, hprev, h, dh, lam_next, nullptr, dlam, dx, dh0, T, W, seg_prod, vs.vagg};
+  BwdCall<S> c{lam, hprev, h, dh, lam_next, nullptr, dlam, dx, dh0, T, W, seg_prod, seg_vagg_rows(seg_prod, p, W)};
   if (p.kind == 1) LINREC_CUDA_TRY(linrec_impl::launch_tma_bwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_bwd<S>(p, c, ws_ptrs(w, p), st));
   // (A', B') of the segment for the exchange, dh0 = lam_S * G_S, fix-up
-  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, vs.vagg, p.nseg, p.tseg, seg_carry_rows(seg_prod, p, W),
-                                                       seg_scale_rows(seg_prod, p, W), agg, dh0, W, st, ex));
+  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, c.agg_out, p.nseg, p.tseg, nullptr, nullptr, agg,
+                                                       dh0, W, st, ex));
   return LINREC_OK;
 }
 
@@ -609,9 +603,9 @@ int segment_fixup(bool reverse, const S* lam, const S* hprev, const S* h, const 
   // the same (nseg, ntt) decomposition the segment scan used
   const ChainPlan p = plan_segment<S>(!reverse, T, W);
   if (p.rows != rows) return fail(LINREC_ERR_VALUE, "tile_rows does not match the segment scan's plan");
-  LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(reverse, lam, hprev, h, lam_next, seg_prod,
-                                               seg_carry_rows(seg_prod, p, W), seg_scale_rows(seg_prod, p, W), carry,
-                                               out0, out1, T, W, rows, p.nseg, p.tseg, p.ntt, v, st, ex, c_out));
+  LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(reverse, lam, hprev, h, lam_next, seg_prod, nullptr, nullptr, carry,
+                                               out0, out1, T, W, rows, p.nseg, p.tseg, p.ntt, v, st, ex, c_out,
+                                               seg_vagg_rows(seg_prod, p, W)));
   return LINREC_OK;
 }
 
@@ -806,7 +800,7 @@ int linrec_first_nonfinite_f64(const double* v, int64_t n, int64_t* index, void*
 int64_t linrec_segment_prod_rows(int64_t T, int64_t W, int dtype_bytes, int backward) {
   if (T < 1 || W < 1) return 0;
   const ChainPlan p = dtype_bytes == 8 ? plan_segment<double>(!backward, T, W) : plan_segment<float>(!backward, T, W);
-  return p.nseg * (p.ntt + 2);  // position rows, then a scale and a carry row per virtual segment
+  return p.nseg * (p.ntt + 2);  // position rows, then the virtual segments' aggregates [nseg][2]
 }
 
 int64_t linrec_segment_tile_rows(int64_t T, int64_t W, int dtype_bytes, int backward) {

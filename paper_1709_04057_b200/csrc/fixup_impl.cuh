@@ -53,7 +53,8 @@ struct Carries {
   // instead of rows: the segments' aggregates [nseg][2][W] (P_incl, c_incl),
   // folded by each fix-up CTA for its own segment (fold_carry) into `own`
   const S* vagg = nullptr;
-  const S* own = nullptr;  // indexed by channel (shared memory: generic loads)
+  const S* own = nullptr;        // its carry, indexed by channel (shared memory: generic loads)
+  const S* own_scale = nullptr;  // with cin: the decay product from the range start to the segment
 };
 
 // Entering correction of chain position p_in of (vseg, channels ch..): the
@@ -70,8 +71,13 @@ __device__ __forceinline__ bool entering(const FixupArgs<S>& f, int64_t vseg, in
   } else if (cr.rows != nullptr) {
     IO::load_cg(cr.rows + vseg * f.W + ch, c);
   }
-  if (cr.cin != nullptr) {  // cin may live in shared memory (composed in-kernel): generic loads
-    IO::load_cg(cr.scale + vseg * f.W + ch, sc);
+  if (cr.cin != nullptr) {  // cin / own_scale may live in shared memory: generic loads
+    if (cr.own_scale != nullptr) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) sc[v] = cr.own_scale[ch + v];
+    } else {
+      IO::load_cg(cr.scale + vseg * f.W + ch, sc);
+    }
 #pragma unroll
     for (int v = 0; v < VEC; ++v) ci[v] = cr.cin[ch + v];
   }
@@ -277,7 +283,7 @@ __device__ __forceinline__ bool fixup_position(const FixupArgs<S>& f, int64_t vs
 // through shared memory s_a / s_b [8*G][CPW] (fixed association).
 template <class S, int VEC, int Q, bool REV, class Sync>
 __device__ __forceinline__ void fold_carry(const FixupArgs<S>& f, const S* __restrict__ vagg, int64_t vseg,
-                                           int64_t col, S* s_a, S* s_b, S (&carry)[VEC]) {
+                                           int64_t col, S* s_a, S* s_b, S (&carry)[VEC], S (&scale)[VEC]) {
   constexpr int G = 32 / Q, CPW = Q * VEC, NWK = 8 * G;
   using IO = VecIO<S, VEC>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -316,10 +322,13 @@ __device__ __forceinline__ void fold_carry(const FixupArgs<S>& f, const S* __res
   }
   Sync::sync();
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) carry[v] = S(0);
+  for (int v = 0; v < VEC; ++v) { carry[v] = S(0); scale[v] = S(1); }
   for (int w = 0; w < NWK; ++w)
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) carry[v] = fma_(s_a[w * CPW + q * VEC + v], carry[v], s_b[w * CPW + q * VEC + v]);
+    for (int v = 0; v < VEC; ++v) {
+      carry[v] = fma_(s_a[w * CPW + q * VEC + v], carry[v], s_b[w * CPW + q * VEC + v]);
+      scale[v] = mul_(s_a[w * CPW + q * VEC + v], scale[v]);
+    }
   Sync::sync();  // s_a / s_b reusable
 }
 

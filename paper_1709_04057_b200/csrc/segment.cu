@@ -37,7 +37,7 @@ k_fixup(FixupArgs<S> f, Carries<S> cr, int64_t ncols, int walkers, linrec_impl::
   constexpr int CPW = Q * VEC, NWK = 8 * (32 / Q);
   __shared__ S s_wp[8][CPW];
   __shared__ S s_cin[CPW];
-  __shared__ S s_own[CPW];
+  __shared__ S s_own[CPW], s_scale[CPW];
   __shared__ S s_fa[NWK * CPW], s_fb[NWK * CPW];
   const int64_t col = blockIdx.x % ncols;
   const int j = (int)((blockIdx.x / ncols) % walkers);
@@ -51,14 +51,18 @@ k_fixup(FixupArgs<S> f, Carries<S> cr, int64_t ncols, int walkers, linrec_impl::
     }
   }
   if (cr.vagg != nullptr) {  // the segment's own carry, folded here instead of a separate launch
-    S c[VEC];
-    fold_carry<S, VEC, Q, REV, CtaSync>(f, cr.vagg, vseg, col, s_fa, s_fb, c);
+    S c[VEC], sc[VEC];
+    fold_carry<S, VEC, Q, REV, CtaSync>(f, cr.vagg, vseg, col, s_fa, s_fb, c, sc);
     const int q = (threadIdx.x & 31) % Q;
     if (threadIdx.x < 32 && threadIdx.x < Q)
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) s_own[q * VEC + v] = c[v];
+      for (int v = 0; v < VEC; ++v) {
+        s_own[q * VEC + v] = c[v];
+        s_scale[q * VEC + v] = sc[v];
+      }
     __syncthreads();
     cr.own = s_own - col * CPW;  // indexed by channel
+    cr.own_scale = s_scale - col * CPW;
   }
   fixup_chain<S, VEC, Q, REV, CtaSync>(f, vseg, col, j, walkers, cr, s_wp);
 }
