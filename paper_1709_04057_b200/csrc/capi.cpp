@@ -535,6 +535,15 @@ int to_exchange(const linrec_exchange_t* e, int64_t W, int dir, bool publish, bo
   return LINREC_OK;
 }
 
+// The rank aggregate is folded in the TMA scan's tail (one CTA, 128-channel
+// float4 blocks) for W <= 256 fp32; wider or register-kernel plans keep the
+// fold kernel.  LINREC_TAIL_FOLD=0 forces the kernel (comparison runs).
+template <class S>
+bool tail_fold_ok(const ChainPlan& p, int64_t W) {
+  static const bool on = linrec_impl::env_int("LINREC_TAIL_FOLD", 1) != 0;
+  return on && sizeof(S) == 4 && p.kind == 1 && W <= 256 && W % 4 == 0;
+}
+
 template <class S>
 int segment_scan(const S* lam, const S* x, const S* h0, S* h, S* seg_prod, S* agg, int64_t T, int64_t W,
                  linrec_workspace_t ws, cudaStream_t st, const linrec_impl::Exchange* ex = nullptr) {
@@ -552,13 +561,19 @@ int segment_scan(const S* lam, const S* x, const S* h0, S* h, S* seg_prod, S* ag
   std::lock_guard<std::mutex> lk(w->mu);
   if ((rc = ws_reserve(w, p.ws_bytes, st))) return rc;
   FwdCall<S> c{lam, x, h0, h, T, W, seg_prod, seg_vagg_rows(seg_prod, p, W)};
+  const bool tail = tail_fold_ok<S>(p, W);
+  if (tail) {  // the scan's last CTA folds (and publishes) the rank aggregate
+    c.rank_agg = agg;
+    if (ex) c.ex = *ex;
+  }
   if (p.kind == 1) LINREC_CUDA_TRY(linrec_impl::launch_tma_fwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_fwd<S>(p, c, ws_ptrs(w, p), st));
-  // the segment-level aggregate for the exchange (with a peer exchange also
-  // stored straight into the consumers' mailboxes); the fix-up folds the
-  // virtual segments' carries itself
-  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, c.agg_out, p.nseg, p.tseg, nullptr, nullptr, agg,
-                                                       nullptr, W, st, ex));
+  // otherwise a fold kernel makes the segment-level aggregate for the exchange
+  // (with a peer exchange also stored straight into the consumers'
+  // mailboxes); the fix-up folds the virtual segments' carries itself
+  if (!tail)
+    LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, c.agg_out, p.nseg, p.tseg, nullptr, nullptr,
+                                                         agg, nullptr, W, st, ex));
   return LINREC_OK;
 }
 
@@ -581,11 +596,17 @@ int segment_scan_backward(const S* lam, const S* hprev, const S* h, const S* dh,
   std::lock_guard<std::mutex> lk(w->mu);
   if ((rc = ws_reserve(w, p.ws_bytes, st))) return rc;
   BwdCall<S> c{lam, hprev, h, dh, lam_next, nullptr, dlam, dx, dh0, T, W, seg_prod, seg_vagg_rows(seg_prod, p, W)};
+  const bool tail = tail_fold_ok<S>(p, W);
+  if (tail) {
+    c.rank_agg = agg;
+    if (ex) c.ex = *ex;
+  }
   if (p.kind == 1) LINREC_CUDA_TRY(linrec_impl::launch_tma_bwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_bwd<S>(p, c, ws_ptrs(w, p), st));
   // (A', B') of the segment for the exchange, dh0 = lam_S * G_S, fix-up
-  LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, c.agg_out, p.nseg, p.tseg, nullptr, nullptr, agg,
-                                                       dh0, W, st, ex));
+  if (!tail)
+    LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, c.agg_out, p.nseg, p.tseg, nullptr, nullptr, agg,
+                                                         dh0, W, st, ex));
   return LINREC_OK;
 }
 

@@ -82,6 +82,8 @@ struct FwdCall {
   int64_t T, W;
   S* seg_prod = nullptr;  // sequence sharding outputs (see segment.cu)
   S* agg_out = nullptr;
+  S* rank_agg = nullptr;  // non-null: fold agg_out into it in the scan's tail (TMA, fp32)
+  Exchange ex{};          // ... and publish it
 };
 
 template <class S>
@@ -98,6 +100,8 @@ struct BwdCall {
   int64_t T, W;
   S* seg_prod = nullptr;
   S* agg_out = nullptr;
+  S* rank_agg = nullptr;
+  Exchange ex{};
 };
 
 template <class S>

@@ -38,6 +38,7 @@
 // re-scan.
 #pragma once
 
+#include "launch.h"
 #include "linrec_device.cuh"
 
 namespace linrec_dev {
@@ -85,6 +86,13 @@ struct ChainArgs {
   int64_t ntt;        // tiles along time per chain (per virtual segment)
   int64_t nseg;       // virtual T-segments scanned as independent chains (>= 1)
   int64_t tseg;       // rows per virtual segment (a multiple of the tile rows)
+  // sequence-sharded TMA scans at W <= 256 (fp32): the CTA that retires last
+  // folds the segments' aggregates (agg_out) into the rank aggregate
+  // rank_agg [2][W] (backward: also dh0 = out2) and publishes it to the
+  // consumers' mailboxes (ex) -- no separate fold launch before the exchange
+  int tail_fold;
+  S* rank_agg;
+  linrec_impl::Exchange ex;
 };
 
 // Position of ticket k: chain = (virtual segment, channel column), tiles in
@@ -404,8 +412,10 @@ __device__ __forceinline__ void chain_ticket(const ChainWs& ws, unsigned long lo
 
 // Called by the coordinator warp once the CTA no longer needs the control
 // block; the CTA that retires last resets the ticket and advances the epoch
-// for the next launch on this workspace.
-__device__ __forceinline__ void chain_retire(const ChainWs& ws, uint32_t epoch) {
+// for the next launch on this workspace.  Returns (on lane 0) whether this
+// CTA retired last.
+__device__ __forceinline__ bool chain_retire(const ChainWs& ws, uint32_t epoch) {
+  bool last = false;
   if ((threadIdx.x & 31) == 0) {
     __threadfence();
     const unsigned long long r = atomicAdd(&ws.ctrl->retired, 1ull);
@@ -414,8 +424,10 @@ __device__ __forceinline__ void chain_retire(const ChainWs& ws, uint32_t epoch) 
       ws.ctrl->retired = 0ull;
       ws.ctrl->epoch = next_epoch(epoch);
       __threadfence();
+      last = true;
     }
   }
+  return last;
 }
 
 // ---------------------------------------------------------------------------

@@ -22,6 +22,9 @@
 // wait for their carries: the look-back latency is hidden behind TMA traffic.
 #pragma once
 
+#include <type_traits>
+
+#include "p2p_impl.cuh"
 #include "scan_chained.cuh"
 #include "tma_util.cuh"
 
@@ -101,7 +104,7 @@ __device__ __forceinline__ void tma_init_barriers(const SM& sm) {
 
 // Coordinator warp loop (both directions).
 template <class Cfg, class S, bool REV, class SM>
-__device__ __forceinline__ void tma_coordinator(const SM& sm, const ChainArgs<S>& a, const ChainWs& ws,
+__device__ __forceinline__ bool tma_coordinator(const SM& sm, const ChainArgs<S>& a, const ChainWs& ws,
                                                 uint32_t epoch) {
   constexpr int VEC = Cfg::kVEC, Q = Cfg::kQ, NW = Cfg::kNW, CPW = Cfg::CPW, STAGES = Cfg::kSTAGES;
   const int lane = threadIdx.x & 31;
@@ -153,7 +156,96 @@ __device__ __forceinline__ void tma_coordinator(const SM& sm, const ChainArgs<S>
     Lookback<S, VEC, Q, Cfg::REC>::publish(ws, epoch, k, TA, TB, c, P, valid, want_p);
     write_segment_outputs<S, VEC, Q>(a, cp, ch, valid, TA, TB, c, P);
   }
-  chain_retire(ws, epoch);
+  return chain_retire(ws, epoch);
+}
+
+// Tail of a sequence-sharded launch (ChainArgs::tail_fold), run by the whole
+// CTA that retired last: the rank aggregate (P, c) of the virtual segments'
+// aggregates -- each 128-channel block as float4 lanes, the warps folding
+// contiguous segment groups combined in order (backward: pairs scaled by the
+// decay at each segment's first row, dh0 = c) -- then stored into every
+// consumer's mailbox and their flags released.  scratch: 2 x warps x 128
+// floats of shared memory.
+template <bool REV>
+__device__ __forceinline__ void tail_fold_publish(const ChainArgs<float>& a, float* scratch) {
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5, ngr = blockDim.x >> 5;
+  float* sA = scratch;
+  float* sB = scratch + ngr * 128;
+  const int64_t W = a.W, nseg = a.nseg;
+  const int64_t per = (nseg + ngr - 1) / ngr;
+  const int64_t i0 = g * per, i1 = i0 + per < nseg ? i0 + per : nseg;
+  for (int64_t c0 = 0; c0 < W; c0 += 128) {
+    const int64_t ch = c0 + 4 * lane;
+    const bool valid = ch < W;
+    float A[4] = {1.f, 1.f, 1.f, 1.f}, B[4] = {0.f, 0.f, 0.f, 0.f};
+    if (valid)
+#pragma unroll 8
+      for (int64_t i = i0; i < i1; ++i) {  // pairs in flight together
+        const int64_t sg = REV ? nseg - 1 - i : i;
+        const float4 av = __ldcg(reinterpret_cast<const float4*>(a.agg_out + sg * 2 * W + ch));
+        const float4 bv = __ldcg(reinterpret_cast<const float4*>(a.agg_out + sg * 2 * W + W + ch));
+        float x[4] = {av.x, av.y, av.z, av.w}, y[4] = {bv.x, bv.y, bv.z, bv.w};
+        if (REV) {
+          const float4 l0 = __ldcg(reinterpret_cast<const float4*>(a.a + (sg * a.tseg) * W + ch));
+          const float l[4] = {l0.x, l0.y, l0.z, l0.w};
+#pragma unroll
+          for (int v = 0; v < 4; ++v) { x[v] = mul_(l[v], x[v]); y[v] = mul_(l[v], y[v]); }
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          B[v] = fma_(x[v], B[v], y[v]);
+          A[v] = mul_(x[v], A[v]);
+        }
+      }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      sA[g * 128 + 4 * lane + v] = A[v];
+      sB[g * 128 + 4 * lane + v] = B[v];
+    }
+    __syncthreads();
+    if (g == 0 && valid) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        float c = 0.f, pc = 1.f;
+        for (int w = 0; w < ngr; ++w) {
+          c = fma_(sA[w * 128 + 4 * lane + v], c, sB[w * 128 + 4 * lane + v]);
+          pc = mul_(sA[w * 128 + 4 * lane + v], pc);
+        }
+        a.rank_agg[ch + v] = pc;
+        a.rank_agg[W + ch + v] = c;
+        if (REV && a.out2 != nullptr) a.out2[ch + v] = c;
+      }
+    }
+    __syncthreads();
+  }
+  if (!a.ex.has_consumers()) return;
+  const p2p::MboxLayout L = p2p::layout(a.ex);
+  void* own = a.ex.mboxes[a.ex.rank];
+  for (int q = a.ex.q0; q < a.ex.q1; ++q) {
+    if (q == a.ex.rank) continue;
+    if (threadIdx.x == 0) p2p::wait_geq(L.ack(own, a.ex.dir, q), a.ex.epoch - 1);  // q read the previous epoch
+    __syncthreads();
+    float* dst = L.slot(a.ex.mboxes[q], a.ex.dir, a.ex.rank);
+    for (int64_t j = threadIdx.x; j < W; j += blockDim.x) {
+      dst[j] = a.ex.zero_a ? 0.f : a.rank_agg[j];
+      dst[W + j] = a.rank_agg[W + j];
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int q = a.ex.q0; q < a.ex.q1; ++q)
+      if (q != a.ex.rank) p2p::st_release_sys(L.flag(a.ex.mboxes[q], a.ex.dir, a.ex.rank), a.ex.epoch);
+}
+
+// Common end of the TMA kernels with a tail fold: every warp arrives here;
+// only the CTA that retired last (s_last, set by its coordinator) continues.
+template <class S, bool REV>
+__device__ __forceinline__ void tma_tail(const ChainArgs<S>& a, const int* s_last, unsigned char* scratch) {
+  __syncthreads();
+  if (!*s_last) return;
+  __threadfence();  // the other CTAs' aggregates (they fenced before retiring)
+  if constexpr (std::is_same<S, float>::value) tail_fold_publish<REV>(a, reinterpret_cast<float*>(scratch));
 }
 
 // ---------------------------------------------------------------------------
@@ -171,6 +263,7 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   tma_init_barriers<Cfg>(sm);
   const uint32_t epoch = __ldcg(&ws.ctrl->epoch);
+  __shared__ int s_last;  // tail fold: this CTA retired last
 
   if (warp == NW + 1) {  // ---------------- producer
     if (lane == 0) {
@@ -200,10 +293,13 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
         }
       }
     }
+    if (a.tail_fold) tma_tail<S, false>(a, &s_last, smem_raw);
     return;
   }
   if (warp == NW) {  // ---------------- coordinator
-    tma_coordinator<Cfg, S, false>(sm, a, ws, epoch);
+    const bool last = tma_coordinator<Cfg, S, false>(sm, a, ws, epoch);
+    if (lane == 0) s_last = last ? 1 : 0;
+    if (a.tail_fold) tma_tail<S, false>(a, &s_last, smem_raw);
     return;
   }
 
@@ -303,6 +399,7 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
       }
     }
   }
+  if (a.tail_fold) tma_tail<S, false>(a, &s_last, smem_raw);
 }
 
 // ---------------------------------------------------------------------------
@@ -321,6 +418,7 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   tma_init_barriers<Cfg>(sm);
   const uint32_t epoch = __ldcg(&ws.ctrl->epoch);
+  __shared__ int s_last;  // tail fold: this CTA retired last
 
   if (warp == NW + 1) {  // ---------------- producer
     if (lane == 0) {
@@ -354,10 +452,13 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
         }
       }
     }
+    if (a.tail_fold) tma_tail<S, true>(a, &s_last, smem_raw);
     return;
   }
   if (warp == NW) {  // ---------------- coordinator
-    tma_coordinator<Cfg, S, true>(sm, a, ws, epoch);
+    const bool last = tma_coordinator<Cfg, S, true>(sm, a, ws, epoch);
+    if (lane == 0) s_last = last ? 1 : 0;
+    if (a.tail_fold) tma_tail<S, true>(a, &s_last, smem_raw);
     return;
   }
 
@@ -491,6 +592,7 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
       }
     }
   }
+  if (a.tail_fold) tma_tail<S, true>(a, &s_last, smem_raw);
 }
 
 }  // namespace linrec_dev

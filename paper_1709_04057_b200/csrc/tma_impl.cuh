@@ -119,6 +119,9 @@ linrec_dev::ChainArgs<S> fwd_args(const ChainPlan& p, const FwdCall<S>& c) {
   a.ntt = p.ntt;
   a.nseg = p.nseg;
   a.tseg = p.tseg;
+  a.tail_fold = c.rank_agg != nullptr ? 1 : 0;
+  a.rank_agg = c.rank_agg;
+  a.ex = c.ex;
   return a;
 }
 
@@ -142,6 +145,9 @@ linrec_dev::ChainArgs<S> bwd_args(const ChainPlan& p, const BwdCall<S>& c) {
   a.ntt = p.ntt;
   a.nseg = p.nseg;
   a.tseg = p.tseg;
+  a.tail_fold = c.rank_agg != nullptr ? 1 : 0;
+  a.rank_agg = c.rank_agg;
+  a.ex = c.ex;
   return a;
 }
 
