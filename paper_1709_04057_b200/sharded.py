@@ -221,10 +221,15 @@ class SequenceShardedScan:
         r, R = self.rank, self.world
         # fwd: scan + finalize (+ fix-up when virtually segmented) + compose/fix-up
         # for r > 0; bwd likewise + the dh0 compose on rank 0
-        if use_p2p:  # per direction: scan, fold + publish, compose + fix-up (+ the dh0 fold on rank 0)
-            self.launches_per_step = 3 + 3 + (1 if r == 0 else 0)
-        else:  # per direction: scan, fold, compose of the gathered aggregates, fix-up
-            self.launches_per_step = (3 + (1 if r > 0 else 0)) + (3 + (1 if r < R - 1 else 0) + (1 if r == 0 else 0))
+        # (an estimate; bench.py counts the launches on the device): the rank
+        # aggregate is folded in the scan kernel's tail at W <= 256, else by a
+        # fold kernel
+        fold = 0 if (W <= 256 and W % 4 == 0) else 1
+        if use_p2p:  # per direction: scan (+publish), [fold + publish], compose + fix-up (+ dh0 fold on rank 0)
+            self.launches_per_step = 2 * (2 + fold) + (1 if r == 0 else 0)
+        else:  # per direction: scan, [fold], compose of the gathered aggregates, fix-up
+            self.launches_per_step = ((2 + fold + (1 if r > 0 else 0))
+                                      + (2 + fold + (1 if r < R - 1 else 0) + (1 if r == 0 else 0)))
 
     def _on_stream(self):
         if self.stream is not None and torch.cuda.is_available() and isinstance(self.stream, torch.cuda.Stream):
