@@ -343,6 +343,94 @@ __global__ void __launch_bounds__(256) k_skinny_outer(SkinnyArgs g, float* __res
   }
 }
 
+// K-major A with taps (the QRNN input gradient dx[r] = sum_s dpre[r + s*a_tap]
+// W_s, N <= 8): a CTA owns 64 output rows (8 warps x 8 rows) and walks the
+// taps, staging tap s's B [N][K] in shared memory (double-buffered) and
+// accumulating per-lane partials of its rows; rows past M read as zero (the
+// tensor-core path's TMA zero fill).  Fixed-order reduction: deterministic.
+template <int N, bool V4>
+__global__ void __launch_bounds__(256) k_skinny_taps(const float* __restrict__ A, int64_t lda, int64_t K,
+                                                     const float* __restrict__ Bm, int64_t ldb, bool b_mn,
+                                                     int64_t b_tap, int ntaps, int64_t a_tap, int64_t M,
+                                                     int64_t units, float* __restrict__ C, int64_t ldc,
+                                                     int acc) {
+  constexpr int RW = 8;  // rows per warp
+  extern __shared__ float Bs[];  // [2][N][K]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * (8 * RW) + warp * RW;
+  float s[RW][N];
+#pragma unroll
+  for (int i = 0; i < RW; ++i)
+#pragma unroll
+    for (int n = 0; n < N; ++n) s[i][n] = 0.f;
+  auto stage = [&](int tap, float* dst) {
+    for (int64_t i = threadIdx.x; i < N * K; i += blockDim.x) {
+      const int64_t n = i / K, k = i - n * K;
+      dst[i] = n < units ? (b_mn ? __ldg(Bm + (tap * b_tap + k) * ldb + n) : __ldg(Bm + (tap * b_tap + n) * ldb + k))
+                         : 0.f;
+    }
+  };
+  stage(0, Bs);
+  for (int tap = 0; tap < ntaps; ++tap) {
+    float* cur = Bs + (tap & 1) * N * K;
+    __syncthreads();  // tap's B staged; the other buffer is free
+    if (tap + 1 < ntaps) stage(tap + 1, Bs + ((tap + 1) & 1) * N * K);
+    if (V4) {  // lane owns k = 4*lane + 128*j .. +3; all RW rows' float4 in flight together
+      for (int64_t k = 4 * lane; k < K; k += 128) {
+        float4 bk[N];
+#pragma unroll
+        for (int n = 0; n < N; ++n) bk[n] = *reinterpret_cast<const float4*>(cur + n * K + k);
+        float4 v[RW];
+#pragma unroll
+        for (int i = 0; i < RW; ++i) {
+          const int64_t ar = r0 + i + tap * a_tap;  // this tap's A row
+          v[i] = (r0 + i < M && ar < M) ? __ldg(reinterpret_cast<const float4*>(A + ar * lda + k))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < RW; ++i)
+#pragma unroll
+          for (int n = 0; n < N; ++n) {
+            s[i][n] = __fmaf_rn(v[i].x, bk[n].x, s[i][n]);
+            s[i][n] = __fmaf_rn(v[i].y, bk[n].y, s[i][n]);
+            s[i][n] = __fmaf_rn(v[i].z, bk[n].z, s[i][n]);
+            s[i][n] = __fmaf_rn(v[i].w, bk[n].w, s[i][n]);
+          }
+      }
+    } else {
+      for (int64_t k = lane; k < K; k += 32) {  // all RW rows' loads of this k in flight together
+        float bk[N];
+#pragma unroll
+        for (int n = 0; n < N; ++n) bk[n] = cur[n * K + k];
+        float v[RW];
+#pragma unroll
+        for (int i = 0; i < RW; ++i) {
+          const int64_t ar = r0 + i + tap * a_tap;
+          v[i] = (r0 + i < M && ar < M) ? __ldg(A + ar * lda + k) : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < RW; ++i)
+#pragma unroll
+          for (int n = 0; n < N; ++n) s[i][n] = __fmaf_rn(v[i], bk[n], s[i][n]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < RW; ++i) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+      for (int n = 0; n < N; ++n) s[i][n] += __shfl_xor_sync(0xffffffffu, s[i][n], off);
+    if (lane == 0 && r0 + i < M)
+#pragma unroll
+      for (int n = 0; n < N; ++n)
+        if (n < units) {
+          float* d = C + (r0 + i) * ldc + n;
+          *d = acc ? *d + s[i][n] : s[i][n];
+        }
+  }
+}
+
 bool skinny_enabled() {  // LINREC_SKINNY_GEMM=0: always the tensor cores (comparison runs)
   static const bool on = env_int("LINREC_SKINNY_GEMM", 1) != 0;
   return on;
@@ -352,7 +440,36 @@ bool skinny_enabled() {  // LINREC_SKINNY_GEMM=0: always the tensor cores (compa
 // otherwise (the caller then uses the tensor cores).
 cudaError_t gemm_skinny(const GemmOperands& op, const GemmEpilogue& ep, int splits, float* partial, int64_t Mp,
                         int64_t ldp, cudaStream_t st) {
-  if (op.units > 8 || op.nb != 1 || op.ntaps > 1 || op.M < 1) return cudaErrorNotSupported;
+  if (op.units > 8 || op.nb != 1 || op.M < 1) return cudaErrorNotSupported;
+  if (op.ntaps > 1) {  // taps: K-major A, one operand pair
+    if (op.a_mn || op.a2 != nullptr) return cudaErrorNotSupported;
+    const int npad = op.units <= 1 ? 1 : op.units <= 2 ? 2 : op.units <= 4 ? 4 : 8;
+    const size_t smem = (size_t)2 * npad * op.K1 * sizeof(float);
+    if (smem > 96 * 1024) return cudaErrorNotSupported;
+    const unsigned grid = (unsigned)((op.M + 63) / 64);
+    const bool v4 = op.K1 % 4 == 0 && op.lda1 % 4 == 0 && (reinterpret_cast<uintptr_t>(op.a1) & 15) == 0;
+#define TAPS1(NN, V)                                                                                               \
+  do {                                                                                                             \
+    cudaFuncSetAttribute(k_skinny_taps<NN, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
+    k_skinny_taps<NN, V><<<grid, 256, smem, st>>>(op.a1, op.lda1, op.K1, op.b1, op.ldb1, op.b_mn, op.b_tap,         \
+                                                  op.ntaps, op.a_tap, op.M, op.units, ep.C, ep.ldc,                \
+                                                  ep.accumulate ? 1 : 0);                                          \
+  } while (0)
+#define TAPS(NN)            \
+  do {                      \
+    if (v4) TAPS1(NN, true);  \
+    else TAPS1(NN, false);  \
+  } while (0)
+    switch (npad) {
+      case 1: TAPS(1); break;
+      case 2: TAPS(2); break;
+      case 4: TAPS(4); break;
+      default: TAPS(8); break;
+    }
+#undef TAPS
+#undef TAPS1
+    return cudaGetLastError();
+  }
   SkinnyArgs g{};
   g.a0 = op.a1;
   g.b0 = op.b1;

@@ -190,7 +190,7 @@ def test_module_autograd_matches_explicit_backward():
 
 
 # ---- QRNN ----------------------------------------------------------------------------
-QRNN_SHAPES = [(1, 1, 4, 4, 1), (37, 3, 8, 12, 2), (64, 2, 36, 20, 3), (200, 2, 16, 32, 10), (129, 4, 64, 128, 2)]
+QRNN_SHAPES = [(1, 1, 4, 4, 1), (37, 3, 8, 12, 2), (300, 2, 4, 16, 10), (50, 3, 8, 8, 4), (64, 2, 36, 20, 3), (200, 2, 16, 32, 10), (129, 4, 64, 128, 2)]
 
 
 @pytest.mark.parametrize("precision", ["fp32", "tf32"])
