@@ -293,15 +293,10 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
         }
       }
     }
-    if (a.tail_fold) tma_tail<S, false>(a, &s_last, smem_raw);
-    return;
-  }
-  if (warp == NW) {  // ---------------- coordinator
+  } else if (warp == NW) {  // ---------------- coordinator
     const bool last = tma_coordinator<Cfg, S, false>(sm, a, ws, epoch);
     if (lane == 0) s_last = last ? 1 : 0;
-    if (a.tail_fold) tma_tail<S, false>(a, &s_last, smem_raw);
-    return;
-  }
+  } else {
 
   // ---------------------------------- consumers
   const uint64_t pol_keep = policy_evict_last();
@@ -399,6 +394,8 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
       }
     }
   }
+  }  // consumers
+  // one barrier site for every role (the tail fold's __syncthreads)
   if (a.tail_fold) tma_tail<S, false>(a, &s_last, smem_raw);
 }
 
@@ -452,15 +449,10 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
         }
       }
     }
-    if (a.tail_fold) tma_tail<S, true>(a, &s_last, smem_raw);
-    return;
-  }
-  if (warp == NW) {  // ---------------- coordinator
+  } else if (warp == NW) {  // ---------------- coordinator
     const bool last = tma_coordinator<Cfg, S, true>(sm, a, ws, epoch);
     if (lane == 0) s_last = last ? 1 : 0;
-    if (a.tail_fold) tma_tail<S, true>(a, &s_last, smem_raw);
-    return;
-  }
+  } else {
 
   // ---------------------------------- consumers
   const uint64_t pol_keep = policy_evict_last();
@@ -592,6 +584,8 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
       }
     }
   }
+  }  // consumers
+  // one barrier site for every role (the tail fold's __syncthreads)
   if (a.tail_fold) tma_tail<S, true>(a, &s_last, smem_raw);
 }
 
