@@ -12,8 +12,12 @@ Parameters are row-major exactly as GilrParams / GilrLstmParams (gate blocks
 f, i, o, z stacked along the rows of U, V, bias).  Gradients ACCUMULATE into
 the grads objects (tensor.hpp:272-296); dx is returned.  ``precision`` is
 "fp32" (3xTF32 on the tensor cores, fp32-grade; default) or "tf32" (one TF32
-pass, ~1e-3 relative).  Inputs: x [T, b, m] fp32 contiguous; m, n multiples
-of 4.  ``GilrLstm`` wraps the pair as a torch.nn.Module with autograd.
+pass, ~1e-3 relative).  Inputs: x [T, b, m] fp32 contiguous.  Widths that
+are not multiples of 4 (the kernels' 16-byte TMA rows) are zero-padded here:
+padded input columns meet zero weights and padded hidden units start at 0,
+see only zero weights and so stay exactly 0 -- outputs and gradients are the
+unpadded problem's (``_Pad``).  ``GilrLstm`` wraps the pair as a
+torch.nn.Module with autograd.
 """
 from __future__ import annotations
 
@@ -285,7 +289,7 @@ def _call(rc):
 
 
 # ---- GILR ------------------------------------------------------------------------
-def gilr_forward(p: GilrParams, x, h0=None, mode="parallel", precision="fp32", cache: GilrCache | None = None):
+def _gilr_forward_core(p: GilrParams, x, h0=None, mode="parallel", precision="fp32", cache: GilrCache | None = None):
     """gilr_forward (layers.hpp:78-100) -> h [T, b, n]; fills ``cache`` (g, i, h)."""
     lib = _bind()
     T, b, m, n = _dims(x, p.hidden())
@@ -310,7 +314,7 @@ def gilr_forward(p: GilrParams, x, h0=None, mode="parallel", precision="fp32", c
     return h
 
 
-def gilr_backward(p: GilrParams, x, h0, cache: GilrCache, d_h, grads: GilrGrads, mode="parallel",
+def _gilr_backward_core(p: GilrParams, x, h0, cache: GilrCache, d_h, grads: GilrGrads, mode="parallel",
                   precision="fp32", want_dh0=True):
     """gilr_backward (layers.hpp:102-133): accumulates into ``grads``; returns (dx, dh0)."""
     lib = _bind()
@@ -329,7 +333,7 @@ def gilr_backward(p: GilrParams, x, h0, cache: GilrCache, d_h, grads: GilrGrads,
 
 
 # ---- GILR-LSTM ---------------------------------------------------------------------
-def gilr_lstm_forward(p: GilrLstmParams, x, htil0=None, c0=None, mode="parallel", precision="fp32",
+def _gilr_lstm_forward_core(p: GilrLstmParams, x, htil0=None, c0=None, mode="parallel", precision="fp32",
                       cache: GilrLstmCache | None = None):
     """gilr_lstm_forward (layers.hpp:245-293) -> h [T, b, n]; fills ``cache``."""
     lib = _bind()
@@ -355,7 +359,7 @@ def gilr_lstm_forward(p: GilrLstmParams, x, htil0=None, c0=None, mode="parallel"
     return h
 
 
-def gilr_lstm_backward(p: GilrLstmParams, x, htil0, c0, cache: GilrLstmCache, d_h, grads: GilrLstmGrads,
+def _gilr_lstm_backward_core(p: GilrLstmParams, x, htil0, c0, cache: GilrLstmCache, d_h, grads: GilrLstmGrads,
                        mode="parallel", precision="fp32", want_initial=True):
     """gilr_lstm_backward (layers.hpp:295-375): accumulates into ``grads``;
     returns (dx, d_htil0, d_c0)."""
@@ -432,7 +436,7 @@ def qrnn_init(gen: torch.Generator, m: int, n: int, k: int, gate_bias: float = 1
     return QrnnParams(W.contiguous(), bias)
 
 
-def qrnn_forward(p: QrnnParams, x, c0=None, mode="parallel", precision="fp32", cache: QrnnCache | None = None):
+def _qrnn_forward_core(p: QrnnParams, x, c0=None, mode="parallel", precision="fp32", cache: QrnnCache | None = None):
     """qrnn_forward (layers.hpp:449-494) -> h [T, b, n]; fills ``cache``."""
     lib = _bind()
     T, b, m, n = _dims(x, p.hidden())
@@ -460,7 +464,7 @@ def qrnn_forward(p: QrnnParams, x, c0=None, mode="parallel", precision="fp32", c
     return h
 
 
-def qrnn_backward(p: QrnnParams, x, c0, cache: QrnnCache, d_h, grads: QrnnGrads, mode="parallel",
+def _qrnn_backward_core(p: QrnnParams, x, c0, cache: QrnnCache, d_h, grads: QrnnGrads, mode="parallel",
                   precision="fp32", want_dc0=True):
     """qrnn_backward (layers.hpp:496-548): accumulates into ``grads``; returns (dx, dc0)."""
     lib = _bind()
@@ -519,3 +523,154 @@ class GilrLstm(torch.nn.Module):
         htil0 = z if htil0 is None else htil0
         c0 = z if c0 is None else c0
         return _GilrLstmFn.apply(x, htil0, c0, *[getattr(self, nm) for nm in self.names], self.precision)
+
+
+# ---- widths that are not multiples of 4 --------------------------------------------
+def _r4(v: int) -> int:
+    return (v + 3) // 4 * 4
+
+
+class _Pad:
+    """Zero padding of a layer problem to widths m4, n4 (multiples of 4).
+    Gate blocks stacked along rows (f, i, o, z / f, o, z, per tap) are padded
+    block by block, so every block keeps its place."""
+
+    def __init__(self, m, n):
+        self.m, self.n, self.m4, self.n4 = m, n, _r4(m), _r4(n)
+
+    def needed(self):
+        return self.m4 != self.m or self.n4 != self.n
+
+    def rows(self, t, blocks, cols, cols4):  # [blocks*n, cols] -> [blocks*n4, cols4]
+        out = t.new_zeros(blocks, self.n4, cols4)
+        out[:, :self.n, :cols] = t.reshape(blocks, self.n, cols)
+        return out.reshape(blocks * self.n4, cols4)
+
+    def vec(self, t, blocks):  # [blocks*n] -> [blocks*n4]
+        out = t.new_zeros(blocks, self.n4)
+        out[:, :self.n] = t.reshape(blocks, self.n)
+        return out.reshape(-1)
+
+    def last(self, t, width, width4):  # zero-pad the last dimension
+        if t is None:
+            return None
+        out = t.new_zeros(*t.shape[:-1], width4)
+        out[..., :width] = t
+        return out
+
+    def add_rows(self, dst, src, blocks, cols, cols4):
+        dst += src.reshape(blocks, self.n4, cols4)[:, :self.n, :cols].reshape(dst.shape)
+
+    def add_vec(self, dst, src, blocks):
+        dst += src.reshape(blocks, self.n4)[:, :self.n].reshape(dst.shape)
+
+    # parameters
+    def gilr(self, p: GilrParams) -> GilrParams:
+        return GilrParams(self.rows(p.U, 1, self.m, self.m4), self.rows(p.V, 1, self.m, self.m4),
+                          self.vec(p.b_g, 1), self.vec(p.b_z, 1), p.act)
+
+    def lstm(self, p: GilrLstmParams) -> GilrLstmParams:
+        return GilrLstmParams(self.gilr(p.surrogate), self.rows(p.U, 4, self.n, self.n4),
+                              self.rows(p.V, 4, self.m, self.m4), self.vec(p.bias, 4))
+
+    def qrnn(self, p: QrnnParams) -> QrnnParams:
+        k = p.window()
+        W = self.rows(p.W.reshape(3 * k * self.n, self.m), 3 * k, self.m, self.m4).reshape(k, 3 * self.n4, self.m4)
+        return QrnnParams(W.contiguous(), self.vec(p.bias, 3))
+
+
+def gilr_forward(p: GilrParams, x, h0=None, mode="parallel", precision="fp32", cache: GilrCache | None = None):
+    """gilr_forward (layers.hpp:78-100) -> h [T, b, n]; fills ``cache`` (g, i, h)."""
+    pad = _Pad(x.shape[-1] if x.dim() == 3 else p.input(), p.hidden())
+    if not pad.needed():
+        return _gilr_forward_core(p, x, h0, mode, precision, cache)
+    if x.shape[-1] != p.input():
+        raise RuntimeError("gilr_forward: input feature mismatch")
+    inner = cache if cache is not None else GilrCache()
+    h = _gilr_forward_core(pad.gilr(p), pad.last(x, pad.m, pad.m4), pad.last(h0, pad.n, pad.n4), mode, precision,
+                           inner)
+    return h[..., :pad.n].contiguous()
+
+
+def gilr_backward(p: GilrParams, x, h0, cache: GilrCache, d_h, grads: GilrGrads, mode="parallel",
+                  precision="fp32", want_dh0=True):
+    """gilr_backward (layers.hpp:102-133): accumulates into ``grads``; returns (dx, dh0)."""
+    pad = _Pad(p.input(), p.hidden())
+    if not pad.needed():
+        return _gilr_backward_core(p, x, h0, cache, d_h, grads, mode, precision, want_dh0)
+    pp = pad.gilr(p)
+    g4 = GilrGrads.zeros_like(pp)
+    dx, dh0 = _gilr_backward_core(pp, pad.last(x, pad.m, pad.m4), pad.last(h0, pad.n, pad.n4), cache,
+                                  pad.last(d_h, pad.n, pad.n4), g4, mode, precision, want_dh0)
+    pad.add_rows(grads.U, g4.U, 1, pad.m, pad.m4)
+    pad.add_rows(grads.V, g4.V, 1, pad.m, pad.m4)
+    pad.add_vec(grads.b_g, g4.b_g, 1)
+    pad.add_vec(grads.b_z, g4.b_z, 1)
+    return dx[..., :pad.m].contiguous(), None if dh0 is None else dh0[..., :pad.n].contiguous()
+
+
+def gilr_lstm_forward(p: GilrLstmParams, x, htil0=None, c0=None, mode="parallel", precision="fp32",
+                      cache: GilrLstmCache | None = None):
+    """gilr_lstm_forward (layers.hpp:245-293) -> h [T, b, n]; fills ``cache``
+    (padded to the kernels' widths when m or n is not a multiple of 4)."""
+    pad = _Pad(x.shape[-1] if x.dim() == 3 else p.input(), p.hidden())
+    if not pad.needed():
+        return _gilr_lstm_forward_core(p, x, htil0, c0, mode, precision, cache)
+    if x.shape[-1] != p.input():
+        raise RuntimeError("gilr_lstm_forward: input feature mismatch")
+    h = _gilr_lstm_forward_core(pad.lstm(p), pad.last(x, pad.m, pad.m4), pad.last(htil0, pad.n, pad.n4),
+                                pad.last(c0, pad.n, pad.n4), mode, precision,
+                                cache if cache is not None else GilrLstmCache())
+    return h[..., :pad.n].contiguous()
+
+
+def gilr_lstm_backward(p: GilrLstmParams, x, htil0, c0, cache: GilrLstmCache, d_h, grads: GilrLstmGrads,
+                       mode="parallel", precision="fp32", want_initial=True):
+    """gilr_lstm_backward (layers.hpp:295-375): accumulates into ``grads``;
+    returns (dx, d_htil0, d_c0)."""
+    pad = _Pad(p.input(), p.hidden())
+    if not pad.needed():
+        return _gilr_lstm_backward_core(p, x, htil0, c0, cache, d_h, grads, mode, precision, want_initial)
+    pp = pad.lstm(p)
+    g4 = GilrLstmGrads.zeros_like(pp)
+    dx, dht0, dc0 = _gilr_lstm_backward_core(pp, pad.last(x, pad.m, pad.m4), pad.last(htil0, pad.n, pad.n4),
+                                             pad.last(c0, pad.n, pad.n4), cache, pad.last(d_h, pad.n, pad.n4), g4,
+                                             mode, precision, want_initial)
+    s, s4 = grads.surrogate, g4.surrogate
+    pad.add_rows(s.U, s4.U, 1, pad.m, pad.m4)
+    pad.add_rows(s.V, s4.V, 1, pad.m, pad.m4)
+    pad.add_vec(s.b_g, s4.b_g, 1)
+    pad.add_vec(s.b_z, s4.b_z, 1)
+    pad.add_rows(grads.U, g4.U, 4, pad.n, pad.n4)
+    pad.add_rows(grads.V, g4.V, 4, pad.m, pad.m4)
+    pad.add_vec(grads.bias, g4.bias, 4)
+    cut = lambda t: None if t is None else t[..., :pad.n].contiguous()  # noqa: E731
+    return dx[..., :pad.m].contiguous(), cut(dht0), cut(dc0)
+
+
+def qrnn_forward(p: QrnnParams, x, c0=None, mode="parallel", precision="fp32", cache: QrnnCache | None = None):
+    """qrnn_forward (layers.hpp:449-494) -> h [T, b, n]; fills ``cache``."""
+    pad = _Pad(x.shape[-1] if x.dim() == 3 else p.input(), p.hidden())
+    if not pad.needed():
+        return _qrnn_forward_core(p, x, c0, mode, precision, cache)
+    if x.shape[-1] != p.input():
+        raise RuntimeError("qrnn_forward: input feature mismatch")
+    h = _qrnn_forward_core(pad.qrnn(p), pad.last(x, pad.m, pad.m4), pad.last(c0, pad.n, pad.n4), mode, precision,
+                           cache if cache is not None else QrnnCache())
+    return h[..., :pad.n].contiguous()
+
+
+def qrnn_backward(p: QrnnParams, x, c0, cache: QrnnCache, d_h, grads: QrnnGrads, mode="parallel",
+                  precision="fp32", want_dc0=True):
+    """qrnn_backward (layers.hpp:496-548): accumulates into ``grads``; returns (dx, dc0)."""
+    pad = _Pad(p.input(), p.hidden())
+    if not pad.needed():
+        return _qrnn_backward_core(p, x, c0, cache, d_h, grads, mode, precision, want_dc0)
+    pp = pad.qrnn(p)
+    g4 = QrnnGrads.zeros_like(pp)
+    dx, dc0 = _qrnn_backward_core(pp, pad.last(x, pad.m, pad.m4), pad.last(c0, pad.n, pad.n4), cache,
+                                  pad.last(d_h, pad.n, pad.n4), g4, mode, precision, want_dc0)
+    k = p.window()
+    pad.add_rows(grads.W.view(3 * k * pad.n, pad.m), g4.W.view(3 * k * pad.n4, pad.m4), 3 * k, pad.m, pad.m4)
+    pad.add_vec(grads.bias, g4.bias, 3)
+    return dx[..., :pad.m].contiguous(), None if dc0 is None else dc0[..., :pad.n].contiguous()

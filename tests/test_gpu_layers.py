@@ -49,7 +49,14 @@ def _err(a, ref):
     return max_rel_error(a.detach().cpu().numpy().astype(np.float64), ref)
 
 
-SHAPES = [(1, 1, 4, 4), (37, 3, 8, 12), (200, 2, 16, 32), (129, 5, 36, 20), (64, 4, 64, 128)]
+SHAPES = [(1, 1, 4, 4), (37, 3, 8, 12), (200, 2, 16, 32), (129, 5, 36, 20), (64, 4, 64, 128),
+          # widths that are not multiples of 4 (the reference's test_layers.cpp settings {T, b, m, n}
+          # {1,1,1,1}, {7,2,3,4}, {33,3,5,2}; training's 8 -> 6): zero-padded in layers.py
+          (1, 1, 1, 1), (7, 2, 3, 4), (33, 3, 5, 2), (40, 2, 8, 6)]
+
+
+def _aligned(m, n):
+    return m % 4 == 0 and n % 4 == 0
 
 
 @pytest.mark.parametrize("precision", ["fp32", "tf32"])
@@ -69,9 +76,10 @@ def test_gilr_lstm_forward_backward_vs_oracle(oracle, T, b, m, n, precision):
     torch.cuda.synchronize()
     tol = TOL[precision]
     assert _err(h, h_ref) < tol
-    assert _err(cache.c, cache_ref["c"]) < tol
-    assert _err(cache.surrogate_h(), cache_ref["htil"]) < tol
-    assert _err(cache.gates_interleaved(), cache_ref["gates"]) < tol
+    if _aligned(m, n):  # padded runs keep padded (opaque) caches
+        assert _err(cache.c, cache_ref["c"]) < tol
+        assert _err(cache.surrogate_h(), cache_ref["htil"]) < tol
+        assert _err(cache.gates_interleaved(), cache_ref["gates"]) < tol
     names = ["sU", "sV", "sbg", "sbz", "U", "V", "bias"]
     for nm, t in zip(names, grads.tensors()):
         assert _err(t, g_ref[nm]) < tol, nm
@@ -120,13 +128,13 @@ def test_gilr_lstm_deterministic():
 
 
 @pytest.mark.parametrize("act", ["tanh", "identity", "relu"])
-def test_gilr_layer_vs_oracle(oracle, act):
+@pytest.mark.parametrize("T,b,m,n", [(90, 3, 12, 16), (33, 3, 5, 2), (7, 2, 3, 4)])
+def test_gilr_layer_vs_oracle(oracle, act, T, b, m, n):
     """Standalone GILR layer (layers.hpp:78-133) against the oracle's GILR
     (the LSTM's surrogate path), every candidate activation."""
     import ctypes as C
     from oracle.oracle import _ptr
     from paper_1709_04057_b200 import layers as L
-    T, b, m, n = 90, 3, 12, 16
     rng = np.random.default_rng(11)
     U, V = rng.uniform(-.5, .5, (n, m)), rng.uniform(-.5, .5, (n, m))
     bg, bz = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
@@ -149,7 +157,9 @@ def test_gilr_layer_vs_oracle(oracle, act):
     dx, dh0 = L.gilr_backward(p, xd, h0d, cache, _dev(dh), grads)
     torch.cuda.synchronize()
     tol = TOL["fp32"]
-    assert _err(h, h_r) < tol and _err(cache.g, g_r) < tol and _err(cache.i, i_r) < tol
+    assert _err(h, h_r) < tol
+    if _aligned(m, n):
+        assert _err(cache.g, g_r) < tol and _err(cache.i, i_r) < tol
     for t, r in zip(grads.tensors(), (dU, dV, dbg, dbz)):
         assert _err(t, r) < tol
     assert _err(dx, dx_r) < tol and _err(dh0, dh0_r) < tol
@@ -158,10 +168,10 @@ def test_gilr_layer_vs_oracle(oracle, act):
 def test_layer_errors():
     from paper_1709_04057_b200 import capi, layers as L
     gen = torch.Generator().manual_seed(0)
-    p = L.gilr_lstm_init(gen, 6, 8)  # m = 6: not a multiple of 4
+    p = L.gilr_lstm_init(gen, 6, 8)  # m = 6: the C ABI wants multiples of 4 (layers.py pads)
     x = torch.zeros(4, 1, 6, device="cuda")
     with pytest.raises(capi.LinrecError, match="multiples of 4"):
-        L.gilr_lstm_forward(p, x)
+        L._gilr_lstm_forward_core(p, x)
     p = L.gilr_lstm_init(gen, 8, 8)
     with pytest.raises(RuntimeError, match="input feature mismatch"):
         L.gilr_lstm_forward(p, torch.zeros(4, 1, 12, device="cuda"))
@@ -190,7 +200,9 @@ def test_module_autograd_matches_explicit_backward():
 
 
 # ---- QRNN ----------------------------------------------------------------------------
-QRNN_SHAPES = [(1, 1, 4, 4, 1), (37, 3, 8, 12, 2), (300, 2, 4, 16, 10), (50, 3, 8, 8, 4), (64, 2, 36, 20, 3), (200, 2, 16, 32, 10), (129, 4, 64, 128, 2)]
+QRNN_SHAPES = [(1, 1, 4, 4, 1), (37, 3, 8, 12, 2), (300, 2, 4, 16, 10), (50, 3, 8, 8, 4), (64, 2, 36, 20, 3),
+               (200, 2, 16, 32, 10), (129, 4, 64, 128, 2),
+               (9, 2, 3, 4, 1), (20, 1, 3, 4, 5), (33, 3, 5, 2, 3)]  # the reference's odd widths: padded
 
 
 @pytest.mark.parametrize("precision", ["fp32", "tf32"])
@@ -214,8 +226,9 @@ def test_qrnn_forward_backward_vs_oracle(oracle, T, b, m, n, k, precision):
     torch.cuda.synchronize()
     tol = TOL[precision]
     assert _err(h, h_ref) < tol
-    assert _err(cache.gates_interleaved(), cache_ref["gates"]) < tol
-    assert _err(cache.c, cache_ref["c"]) < tol
+    if _aligned(m, n):
+        assert _err(cache.gates_interleaved(), cache_ref["gates"]) < tol
+        assert _err(cache.c, cache_ref["c"]) < tol
     assert _err(grads.W, g_ref["W"]) < tol
     assert _err(grads.bias, g_ref["bias"]) < tol
     assert _err(dx, dx_ref) < tol

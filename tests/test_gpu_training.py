@@ -58,10 +58,11 @@ def test_build_model_matches_reference_init():
     assert m.parameter_count() == expect  # test_training.cpp:97-100
 
 
-def test_train_steps_follow_the_oracle(oracle):
+@pytest.mark.parametrize("hidden", [8, 6])  # 6: test_training.cpp's hidden width (padded in layers.py)
+def test_train_steps_follow_the_oracle(oracle, hidden):
     from oracle.train_oracle import run_experiment as orun
     from paper_1709_04057_b200.training import run_experiment
-    cfg, ocfg = _cfgs(max_iters=4, learning_rate=1e-2)
+    cfg, ocfg = _cfgs(max_iters=4, learning_rate=1e-2, hidden=hidden)
     keep = []
     rep = run_experiment(cfg, trainer_out=keep)
     orep, otr = orun(ocfg, oracle=oracle)
