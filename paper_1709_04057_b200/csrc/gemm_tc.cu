@@ -431,6 +431,105 @@ __global__ void __launch_bounds__(256) k_skinny_taps(const float* __restrict__ A
   }
 }
 
+// The QRNN weight gradients of all k taps in one launch, <= 8 input columns:
+// dW_s[M][N] += sum_{t < R - s*shift} A[t + s*shift][.]^T B[t][.] with A
+// (dpre, MN-major, lda) and B (x, MN-major, ldb).  Tap s = blockIdx.x is the
+// fastest grid dimension, so the k CTAs reading the same rows of A (shifted
+// by s*shift) run together and share them through L2 -- one HBM pass over
+// dpre instead of k.  Per tap the split-K partials use the tensor-core
+// path's layout [splits][Mp][ldp] at part + s * splits*Mp*ldp.
+template <int N>
+__global__ void __launch_bounds__(256) k_skinny_outer_taps(const float* __restrict__ A, int64_t lda,
+                                                           const float* __restrict__ Bm, int64_t ldb, int64_t R,
+                                                           int64_t shift, int64_t M, int64_t units,
+                                                           float* __restrict__ part, int64_t Mp, int64_t ldp,
+                                                           int splits) {
+  constexpr int KC = 1024, MQ = 16, KG = 256 / MQ, U = 8;
+  __shared__ float4 smem[KC * N / 4];
+  float(*Bs)[N] = reinterpret_cast<float(*)[N]>(smem);
+  float4(*red)[MQ][N] = reinterpret_cast<float4(*)[MQ][N]>(smem);
+  const int tap = blockIdx.x, split = blockIdx.z;
+  const int mq = threadIdx.x % MQ, kg = threadIdx.x / MQ;
+  const int64_t m0 = (int64_t)blockIdx.y * (4 * MQ) + 4 * mq;
+  const bool mok = m0 < M;
+  const int64_t Kt = R - tap * shift;  // rows of this tap
+  const int64_t kper = (Kt + splits - 1) / splits;
+  const int64_t k0 = split * kper, k1 = k0 + kper < Kt ? k0 + kper : Kt;
+  const float* a = A + tap * shift * lda;
+  float4 s[N];
+#pragma unroll
+  for (int n = 0; n < N; ++n) s[n] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t kc = k0; kc < k1; kc += KC) {
+    const int kn = (int)(k1 - kc < KC ? k1 - kc : KC);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kn * N; i += blockDim.x) {
+      const int kk = i / N, n = i - kk * N;
+      Bs[kk][n] = n < units ? __ldg(Bm + (kc + kk) * ldb + n) : 0.f;
+    }
+    __syncthreads();
+    if (!mok) continue;
+    for (int kk = kg; kk < kn; kk += KG * U) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        v[u] = kk + KG * u < kn ? __ldg(reinterpret_cast<const float4*>(a + (kc + kk + KG * u) * lda + m0))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (kk + KG * u >= kn) break;
+#pragma unroll
+        for (int n = 0; n < N; ++n) {
+          const float b = Bs[kk + KG * u][n];
+          s[n].x = __fmaf_rn(v[u].x, b, s[n].x);
+          s[n].y = __fmaf_rn(v[u].y, b, s[n].y);
+          s[n].z = __fmaf_rn(v[u].z, b, s[n].z);
+          s[n].w = __fmaf_rn(v[u].w, b, s[n].w);
+        }
+      }
+    }
+  }
+  __syncthreads();  // the B stage is free: reuse it for the k-group sums
+#pragma unroll
+  for (int n = 0; n < N; ++n) red[kg][mq][n] = s[n];
+  __syncthreads();
+  if (kg == 0 && mok) {
+#pragma unroll
+    for (int q = 1; q < KG; ++q)
+#pragma unroll
+      for (int n = 0; n < N; ++n) {
+        const float4 r = red[q][mq][n];
+        s[n].x += r.x;
+        s[n].y += r.y;
+        s[n].z += r.z;
+        s[n].w += r.w;
+      }
+    float* dst = part + (((int64_t)tap * splits + split) * Mp + m0) * ldp;
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+      if (n < units) {
+        dst[n] = s[n].x;
+        dst[ldp + n] = s[n].y;
+        dst[2 * ldp + n] = s[n].z;
+        dst[3 * ldp + n] = s[n].w;
+      }
+  }
+}
+
+// Per-tap split reduction of k_skinny_outer_taps (blockIdx.y = tap), summed in
+// split order into dW_s (accumulating).
+__global__ void k_splitk_reduce_taps(const float* __restrict__ part, int splits, int64_t M, int64_t Mp, int64_t N,
+                                     int64_t ldp, float* __restrict__ dW) {
+  const int tap = blockIdx.y;
+  const float* pt = part + (int64_t)tap * splits * Mp * ldp;
+  float* C = dW + (int64_t)tap * M * N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * N; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / N, c = i - r * N;
+    float v = 0.f;
+    for (int z = 0; z < splits; ++z) v += pt[((int64_t)z * Mp + r) * ldp + c];
+    C[i] += v;
+  }
+}
+
 bool skinny_enabled() {  // LINREC_SKINNY_GEMM=0: always the tensor cores (comparison runs)
   static const bool on = env_int("LINREC_SKINNY_GEMM", 1) != 0;
   return on;
@@ -576,6 +675,36 @@ cudaError_t tf32_lo(const float* src, float* dst, int64_t count, cudaStream_t st
 
 int64_t gemm_partial_floats(int64_t M, int64_t N, int splits) {
   return splits > 1 ? (int64_t)splits * round_up(M, 2 * BM) * round_up(N, 4) : 0;
+}
+
+int64_t wgrad_taps_partial_floats(int64_t M, int64_t N, int64_t R, int ntaps) {
+  // partials are written even for one split (gemm_partial_floats is 0 there)
+  return (int64_t)ntaps * gemm_splits_for(M, N, R) * round_up(M, 2 * BM) * round_up(N, 4);
+}
+
+cudaError_t wgrad_taps_skinny(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t R, int64_t shift,
+                              int ntaps, int64_t M, int64_t N, float* dW, float* scratch, cudaStream_t st) {
+  static const bool on = env_int("LINREC_TAP_WGRAD", 1) != 0;
+  if (!on || N > 8 || M % 4 || lda % 4 || (reinterpret_cast<uintptr_t>(A) & 15) || ntaps < 1 || !skinny_enabled())
+    return cudaErrorNotSupported;
+  const int splits = gemm_splits_for(M, N, R);
+  const int64_t Mp = round_up(M, 2 * BM), ldp = round_up(N, 4);
+  const dim3 grid((unsigned)ntaps, (unsigned)((M + 63) / 64), (unsigned)splits);
+  const int npad = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : 8;
+#define TAPW(NN) k_skinny_outer_taps<NN><<<grid, 256, 0, st>>>(A, lda, B, ldb, R, shift, M, N, scratch, Mp, ldp, splits)
+  switch (npad) {
+    case 1: TAPW(1); break;
+    case 2: TAPW(2); break;
+    case 4: TAPW(4); break;
+    default: TAPW(8); break;
+  }
+#undef TAPW
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t blocks = (M * N + 255) / 256;
+  k_splitk_reduce_taps<<<dim3((unsigned)(blocks < 1024 ? blocks : 1024), (unsigned)ntaps), 256, 0, st>>>(
+      scratch, splits, M, Mp, N, ldp, dW);
+  return cudaGetLastError();
 }
 
 cudaError_t gemm_tf32(const GemmOperands& op, int epi, const GemmEpilogue& ep, cudaStream_t st) {

@@ -194,6 +194,12 @@ cudaError_t tf32_lo(const float* src, float* dst, int64_t count, cudaStream_t st
 int gemm_splits_for(int64_t M, int64_t N, int64_t K);
 // split-K partial buffer (floats) gemm_tf32 needs for `splits` splits (0 for 1)
 int64_t gemm_partial_floats(int64_t M, int64_t N, int splits);
+// All k taps' weight gradients dW_s[M][N] += A[. + s*shift]^T B (A, B MN-major,
+// N <= 8) in one CUDA-core launch (the QRNN's first layer); cudaErrorNotSupported
+// when the shape does not qualify.  scratch: wgrad_taps_partial_floats floats.
+int64_t wgrad_taps_partial_floats(int64_t M, int64_t N, int64_t R, int ntaps);
+cudaError_t wgrad_taps_skinny(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t R, int64_t shift,
+                              int ntaps, int64_t M, int64_t N, float* dW, float* scratch, cudaStream_t st);
 
 // The reference's chunked scan with an explicit plan (plan_scan.cu): phases
 // 1-3 bit-identical to recurrence.hpp's scan_parallel; reverse = the

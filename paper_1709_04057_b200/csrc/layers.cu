@@ -339,7 +339,9 @@ int64_t qrnn_scratch(float* base, int64_t T, int64_t b, int64_t m, int64_t n, in
   t.w_lo = c.take(k * 3 * n * m);
   const RowPlan rp = row_plan(R, n);
   t.part = c.take(rp.nbx * 3 * n);
-  t.split = c.take(wsplit_floats(R, 3 * n, m));
+  const int64_t sp1 = wsplit_floats(R, 3 * n, m);
+  const int64_t spk = m <= 8 ? linrec_impl::wgrad_taps_partial_floats(3 * n, m, R, (int)k) : 0;
+  t.split = c.take(sp1 > spk ? sp1 : spk);  // one tap's partials, or all taps' (CUDA-core tap batch)
   const int64_t common = c.off;
   Carve f{base, common};
   t.imp = f.take(R * n);
@@ -604,11 +606,19 @@ int linrec_qrnn_backward_f32(const float* W, const float* x, const float* c0, co
     LTRY(cudaGetLastError());
   }
   mark(st, "dpre_gates");
-  // dW_s += dpre[s*b ..]^T x[.. R - s*b]  (layers.hpp:536-539)
-  if (dW)
-    for (int64_t tap = 0; tap < k; ++tap)
-      LTRY(wgrad(s.dpre + tap * b * 3 * n, 3 * n, 3 * n, x, m, R - tap * b, dW + tap * 3 * n * m, split3, s.split,
-                 st));
+  // dW_s += dpre[s*b ..]^T x[.. R - s*b]  (layers.hpp:536-539): all taps in one
+  // CUDA-core launch when x is narrow (one HBM pass over dpre), else per tap
+  if (dW) {
+    const cudaError_t et =
+        linrec_impl::wgrad_taps_skinny(s.dpre, 3 * n, x, m, R, b, (int)k, 3 * n, m, dW, s.split, st);
+    if (et == cudaErrorNotSupported) {
+      for (int64_t tap = 0; tap < k; ++tap)
+        LTRY(wgrad(s.dpre + tap * b * 3 * n, 3 * n, 3 * n, x, m, R - tap * b, dW + tap * 3 * n * m, split3,
+                   s.split, st));
+    } else {
+      LTRY(et);
+    }
+  }
   mark(st, "wgrad_W");
   // dx[r] = sum_s dpre[r + s*b] W_s  (:540-543): one GEMM over the taps,
   // tap s reading dpre shifted s*b rows up (zero-filled past row R)
