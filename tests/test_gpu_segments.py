@@ -89,6 +89,7 @@ def emulate(lam, x, h0, dh, R):
     (5000, 256, -1.0, 1.0, 2),
     (3001, 7, 0.05, 0.95, 5),       # W % 4 != 0: register kernels, scalar fix-up
     (700, 16, 0.9, 1.0, 8),
+    (9000, 512, 0.05, 0.95, 3),     # W > 256: the rank aggregate from the fold kernel
 ])
 def test_emulated_sequence_sharding(oracle, T, W, lo, hi, R):
     rng = np.random.default_rng(T + W + R)

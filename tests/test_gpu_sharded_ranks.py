@@ -54,7 +54,8 @@ def _worker(rank, world, port, T, W, lo, hi, seed, q, exchange="auto", reps=1):
 
 @pytest.mark.parametrize("exchange,reps", [("p2p", 3), ("collective", 1)])
 @pytest.mark.parametrize("world,T,W,lo,hi", [(2, 40000, 128, 0.05, 0.95), (3, 30001, 64, 0.99, 1.0),
-                                             (2, 5000, 12, -1.0, 1.0)])
+                                             (2, 5000, 12, -1.0, 1.0),
+                                             (3, 9000, 384, 0.05, 0.95)])  # W > 256: fold kernel publishes
 def test_sequence_sharded_ranks_on_gpu(oracle, world, T, W, lo, hi, exchange, reps):
     import torch.multiprocessing as mp
     from oracle.oracle import max_rel_error
