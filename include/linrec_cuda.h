@@ -217,8 +217,8 @@ int linrec_scan_backward_plan_f64(const double* lam, const double* h0, const dou
  *      on rank 0 and with 0 elsewhere, split internally into virtual
  *      segments whose stitch is left to step 4; it writes seg_prod (the decay
  *      products entering each chain position, plus the virtual segments'
- *      scale and carry rows) and agg[2][W] = (prod lam over the segment,
- *      zero-carry state at its last row);
+ *      aggregates) and agg[2][W] = (prod lam over the segment, zero-carry
+ *      state at its last row);
  *   2. all-gather of agg over the ranks (NCCL, the caller's communicator);
  *   3. linrec_compose_carries_*: c_in = fold of the aggregates of ranks
  *      0..r-1 (c = A_q*c + B_q from 0; rank 0 publishes A = 0);
