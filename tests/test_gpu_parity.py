@@ -460,3 +460,23 @@ def test_virtual_segments_against_oracle(ops, oracle, policy, T, W, lo, hi):
     gw = oracle.scan_backward_wide(lam, h0, ref, dh)
     for a, r in zip(g, gw):
         assert rel(a.cpu().numpy(), r) <= 1e-5
+
+
+@pytest.mark.parametrize("T,W,lo,hi", [(300000, 16, 0.05, 0.95), (100000, 8, 0.999, 1.0), (50000, 3, -1.0, 1.0)])
+def test_virtual_segments_fp64_against_oracle(ops, oracle, T, W, lo, hi):
+    """fp64 through the same stitch (the fix-up's in-CTA carry fold in
+    double): bit-identical serial reference, 1e-12 normwise."""
+    rng = np.random.default_rng(T + W + 1)
+    lam = rng.uniform(lo, hi, (T, 1, W))
+    x = rng.uniform(-1, 1, (T, 1, W))
+    h0 = rng.uniform(-1, 1, (1, W))
+    dh = rng.uniform(-1, 1, (T, 1, W))
+    tl, tx, th0, tdh = cuda(lam), cuda(x), cuda(h0), cuda(dh)
+    h = ops.scan(tl, tx, th0)
+    ref = oracle.scan_serial(lam, x, h0)
+    assert rel(h.cpu().numpy(), ref) <= 1e-12
+    assert torch.equal(h, ops.scan(tl, tx, th0))
+    g = ops.scan_backward(tl, th0, cuda(ref), tdh)
+    gr = oracle.scan_backward(lam, h0, ref, dh)
+    for a, r in zip(g, gr):
+        assert rel(a.cpu().numpy(), r) <= 1e-12
