@@ -27,57 +27,58 @@ def emulate(lam, x, h0, dh, R):
     from paper_1709_04057_b200 import capi
     from paper_1709_04057_b200.sharded import segment_bounds
     T, W = lam.shape
+    es = lam.element_size()  # 4: fp32, 8: fp64
     st = torch.cuda.current_stream().cuda_stream
     dev = lam.device
     h = torch.empty_like(lam)
     dlam, dx = torch.empty_like(lam), torch.empty_like(lam)
-    dh0 = torch.empty(W, device=dev)
-    aggs = torch.zeros(R, 2, W, device=dev)
+    dh0 = torch.empty(W, device=dev, dtype=lam.dtype)
+    aggs = torch.zeros(R, 2, W, device=dev, dtype=lam.dtype)
     segs, sp_f, sp_b, rows_f, rows_b = [], [], [], [], []
     for r in range(R):
         s, e = segment_bounds(T, R, r)
         segs.append((s, e))
-        rf, rb = capi.segment_tile_rows(e - s, W, False), capi.segment_tile_rows(e - s, W, True)
+        rf, rb = capi.segment_tile_rows(e - s, W, False, es), capi.segment_tile_rows(e - s, W, True, es)
         rows_f.append(rf)
         rows_b.append(rb)
-        sp_f.append(torch.empty(capi.segment_prod_rows(e - s, W, False), W, device=dev))
-        sp_b.append(torch.empty(capi.segment_prod_rows(e - s, W, True), W, device=dev))
+        sp_f.append(torch.empty(capi.segment_prod_rows(e - s, W, False, es), W, device=dev, dtype=lam.dtype))
+        sp_b.append(torch.empty(capi.segment_prod_rows(e - s, W, True, es), W, device=dev, dtype=lam.dtype))
     # forward: local scans
     for r, (s, e) in enumerate(segs):
         capi.segment_scan(lam[s].data_ptr(), x[s].data_ptr(), h0.data_ptr() if r == 0 else None, h[s].data_ptr(),
-                          sp_f[r].data_ptr(), aggs[r].data_ptr(), e - s, W, 4, None, st)
+                          sp_f[r].data_ptr(), aggs[r].data_ptr(), e - s, W, es, None, st)
     aggs[0, 0].zero_()
-    c_in = [h0] + [torch.empty(W, device=dev) for _ in range(1, R)]
+    c_in = [h0] + [torch.empty(W, device=dev, dtype=lam.dtype) for _ in range(1, R)]
     for r in range(R):  # every rank: the fix-up also stitches its own virtual segments
         s, e = segs[r]
         if r > 0:
-            capi.compose_carries(aggs.data_ptr(), 0, r, 1, None, c_in[r].data_ptr(), W, 4, st)
+            capi.compose_carries(aggs.data_ptr(), 0, r, 1, None, c_in[r].data_ptr(), W, es, st)
         capi.segment_fixup(lam[s].data_ptr(), h[s].data_ptr(), sp_f[r].data_ptr(),
-                           c_in[r].data_ptr() if r > 0 else None, e - s, W, rows_f[r], 4, st)
+                           c_in[r].data_ptr() if r > 0 else None, e - s, W, rows_f[r], es, st)
     # backward
-    ones = torch.ones(W, device=dev)
-    dh0_loc = [torch.empty(W, device=dev) for _ in range(R)]
-    baggs = torch.zeros(R, 2, W, device=dev)
+    ones = torch.ones(W, device=dev, dtype=lam.dtype)
+    dh0_loc = [torch.empty(W, device=dev, dtype=lam.dtype) for _ in range(R)]
+    baggs = torch.zeros(R, 2, W, device=dev, dtype=lam.dtype)
     for r, (s, e) in enumerate(segs):
         ln = ones if r < R - 1 else None
         capi.segment_scan_backward(lam[s].data_ptr(), c_in[r].data_ptr(), h[s].data_ptr(), dh[s].data_ptr(),
                                    None if ln is None else ln.data_ptr(), dlam[s].data_ptr(), dx[s].data_ptr(),
-                                   dh0_loc[r].data_ptr(), sp_b[r].data_ptr(), baggs[r].data_ptr(), e - s, W, 4,
+                                   dh0_loc[r].data_ptr(), sp_b[r].data_ptr(), baggs[r].data_ptr(), e - s, W, es,
                                    None, st)
-    y0 = torch.zeros(W, device=dev)
+    y0 = torch.zeros(W, device=dev, dtype=lam.dtype)
     for r, (s, e) in enumerate(segs):
         y = None
         if r < R - 1:
-            y = torch.empty(W, device=dev)
-            capi.compose_carries(baggs.data_ptr(), R - 1, r, -1, None, y.data_ptr(), W, 4, st)
+            y = torch.empty(W, device=dev, dtype=lam.dtype)
+            capi.compose_carries(baggs.data_ptr(), R - 1, r, -1, None, y.data_ptr(), W, es, st)
             if r == 0:
                 y0 = y
         ln = ones if r < R - 1 else None
         capi.segment_fixup_backward(lam[s].data_ptr(), c_in[r].data_ptr(), h[s].data_ptr(),
                                     None if ln is None else ln.data_ptr(), sp_b[r].data_ptr(),
                                     None if y is None else y.data_ptr(), dlam[s].data_ptr(), dx[s].data_ptr(), e - s,
-                                    W, rows_b[r], 4, st)
-    capi.compose_carries(baggs.data_ptr(), 0, 1, 1, y0.data_ptr(), dh0.data_ptr(), W, 4, st)
+                                    W, rows_b[r], es, st)
+    capi.compose_carries(baggs.data_ptr(), 0, 1, 1, y0.data_ptr(), dh0.data_ptr(), W, es, st)
     torch.cuda.synchronize()
     return h, dlam, dx, dh0
 
@@ -106,6 +107,25 @@ def test_emulated_sequence_sharding(oracle, T, W, lo, hi, R):
     g = oracle.scan_backward_wide(lam, h0, ref, dh)
     for a, r in zip((dlam, dx, dh0), g):
         assert rel(a.cpu().numpy(), r) <= 1e-5
+
+
+@pytest.mark.parametrize("T,W,lo,hi,R", [(65536, 128, 0.05, 0.95, 4), (3001, 7, 0.05, 0.95, 5),
+                                         (9000, 512, 0.05, 0.95, 3)])
+def test_emulated_sequence_sharding_fp64(oracle, T, W, lo, hi, R):
+    """fp64 segments: the fold kernel (no tail fold in double) and the fix-up's
+    carry fold in double; 1e-12 normwise against the unsharded serial scan."""
+    rng = np.random.default_rng(T + W + R + 1)
+    lam = rng.uniform(lo, hi, (T, W))
+    x = rng.uniform(-1, 1, (T, W))
+    h0 = rng.uniform(-1, 1, (W,))
+    dh = rng.uniform(-1, 1, (T, W))
+    cu = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+    h, dlam, dx, dh0 = emulate(cu(lam), cu(x), cu(h0), cu(dh), R)
+    ref = oracle.scan_serial(lam, x, h0)
+    assert rel(h.cpu().numpy(), ref) <= 1e-12
+    g = oracle.scan_backward(lam, h0, ref, dh)
+    for a, r in zip((dlam, dx, dh0), g):
+        assert rel(a.cpu().numpy(), r) <= 1e-12
 
 
 def test_runner_world_one_nccl(oracle):
