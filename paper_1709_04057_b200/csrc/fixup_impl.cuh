@@ -230,8 +230,10 @@ __device__ __forceinline__ bool fixup_position(const FixupArgs<S>& f, int64_t vs
           IO::store_cg(out_p + i * step, o[i]);
         }
     } else {
-      // backward with dlam: dx, dlam and h_{t-1} of CH rows per load round
-      // (loads ahead of the stores, which may alias them)
+      // backward with dlam: dx and h_{t-1} of CH rows per load round (loads
+      // ahead of the stores, which may alias them); dlam is recomputed from
+      // the corrected dx as the scan computes it (dlam_t = h_{t-1} * g_t), so
+      // the old dlam is not read
       constexpr int CH = 6;
       S* d_p = f.out1 + t0 * W + ch;
       const S* h_p = f.h + (t0 - 1) * W + ch;
@@ -243,7 +245,6 @@ __device__ __forceinline__ bool fixup_position(const FixupArgs<S>& f, int64_t vs
         for (int i = 0; i < CH; ++i)
           if (c + i >= ilo && c + i < ihi) {
             IO::load_cg(out_p + (c + i) * step, oc[i]);
-            IO::load_cg(d_p + (c + i) * step, d[i]);
             if (c + i != izero) {
               IO::load_cg(h_p + (c + i) * step, hp[i]);
             } else {
@@ -257,7 +258,7 @@ __device__ __forceinline__ bool fixup_position(const FixupArgs<S>& f, int64_t vs
 #pragma unroll
             for (int v = 0; v < VEC; ++v) {
               oc[i][v] = oc[i][v] + m[c + i][v];
-              d[i][v] = fma_(hp[i][v], m[c + i][v], d[i][v]);
+              d[i][v] = mul_(hp[i][v], oc[i][v]);
             }
             IO::store_cg(out_p + (c + i) * step, oc[i]);
             IO::store_cg(d_p + (c + i) * step, d[i]);
@@ -339,9 +340,6 @@ __device__ __forceinline__ void fold_carry(const FixupArgs<S>& f, const S* __res
 template <class S, int VEC, int Q, bool REV, class Sync>
 __device__ __forceinline__ void fixup_chain(const FixupArgs<S>& f, int64_t vseg, int64_t col, int j, int J,
                                             const Carries<S>& cr, S (*s_wp)[Q * VEC]) {
-  constexpr int CPW = Q * VEC;
-  const int lane = threadIdx.x & 31;
-  const int64_t ch = col * CPW + (int64_t)(lane % Q) * VEC;
   // positions holding rows < T: the last virtual segment is usually short,
   // and its tiles past T (decay 1, nothing to fix) would keep the walk going
   const int64_t seg_rows = (vseg + 1) * f.tseg < f.T ? f.tseg : f.T - vseg * f.tseg;
