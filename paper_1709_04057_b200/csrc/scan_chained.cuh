@@ -238,18 +238,26 @@ struct Lookback<float, VEC, Q, REC> {
       float a[VEC], b[VEC];
       if (load_words<VEC>(rg, a, tagg) & load_words<VEC>(rg + REC, b, tagg)) --j;
     }
-    // apply the aggregates of j+1 .. pos-1, oldest first (all visible now)
+    // apply the aggregates of j+1 .. pos-1, oldest first (all visible now),
+    // four positions' loads in flight per round
 #pragma unroll 1
-    for (int64_t i = j + 1; i < pos; ++i) {
-      float a[VEC], b[VEC];
-      const uint64_t* rg = agg + (i * ncols + col) * 2 * REC + off;
-      load_words<VEC>(rg, a, tagg);
-      load_words<VEC>(rg + REC, b, tagg);
+    for (int64_t i = j + 1; i < pos; i += 4) {
+      float a[4][VEC], b[4][VEC];
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        c[v] = fma_(a[v], c[v], b[v]);
-        if (WANT_P) P[v] = mul_(a[v], P[v]);
-      }
+      for (int u = 0; u < 4; ++u)
+        if (i + u < pos) {
+          const uint64_t* rg = agg + ((i + u) * ncols + col) * 2 * REC + off;
+          load_words<VEC>(rg, a[u], tagg);
+          load_words<VEC>(rg + REC, b[u], tagg);
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i + u < pos)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            c[v] = fma_(a[u][v], c[v], b[u][v]);
+            if (WANT_P) P[v] = mul_(a[u][v], P[v]);
+          }
     }
   }
 
