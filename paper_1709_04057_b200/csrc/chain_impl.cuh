@@ -56,9 +56,10 @@ inline int64_t chain_target(bool forward) {
 
 // Chains shorter than this many tiles stay whole: below it the stitch (fold
 // + fix-up launches) costs more than the look-back latency it removes
-// (scripts/dev/split_sweep.py: 43 tiles -- C1 -- 36 -> 29 us forward whole,
-// 171 tiles 65 -> 41 us split).
-constexpr int64_t kMinSplitTiles = 64;
+// (scripts/dev/split_sweep.py at W = 256 with the batched look-back apply:
+// 64 tiles 29.1 us forward whole / 33.2 split, 86 tiles 31.7 / 34.3,
+// 107 tiles 36.4 / 35.8, 128 tiles 39.5 / 36.5).
+constexpr int64_t kMinSplitTiles = 96;
 
 inline void choose_segments(ChainPlan& p, int64_t T, bool forward) {
   const int64_t ntt_total = (T + p.rows - 1) / p.rows;
