@@ -501,8 +501,8 @@ k_gemm(const __grid_constant__ CUtensorMap ta1, const __grid_constant__ CUtensor
           mbar_wait(&full[s], (it / STAGES) & 1);
           const float4* src = reinterpret_cast<const float4*>(smem + s * Cfg::STAGE_BYTES);
           float4* dst = reinterpret_cast<float4*>(smem + Cfg::LO_OFF + s * Cfg::STAGE_BYTES);
-#pragma unroll 4
           const int nsplit = (p.b_lo ? GA::BYTES : Cfg::STAGE_BYTES) / 16;  // A only when B's lo is loaded
+#pragma unroll 4
           for (int e = st; e < nsplit; e += kSplitWarps * 32) {
             const float4 v = src[e];
             dst[e] = make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z), v.w - tf32_hi(v.w));
