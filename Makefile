@@ -27,21 +27,26 @@ KERNEL_SRCS := $(CSRC)/chain_fwd_f32.cu $(CSRC)/chain_bwd_f32.cu $(CSRC)/chain_f
                $(CSRC)/chain_bwd_f64.cu $(CSRC)/serial_misc.cu $(CSRC)/tma_fwd_f32.cu \
                $(CSRC)/tma_bwd_f32.cu $(CSRC)/tma_f64.cu $(CSRC)/segment.cu $(CSRC)/gemm_tc.cu \
                $(CSRC)/layers.cu $(CSRC)/training.cu $(CSRC)/p2p.cu $(CSRC)/plan_scan.cu
-HOST_SRCS   := $(CSRC)/capi.cpp
+HOST_SRCS   := $(CSRC)/capi.cpp $(CSRC)/sharded_capi.cpp
 HDRS        := $(wildcard $(CSRC)/*.cuh) $(CSRC)/launch.h include/linrec_cuda.h
-OBJS        := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(KERNEL_SRCS)) $(BUILD)/capi.o
+OBJS        := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(KERNEL_SRCS)) $(BUILD)/capi.o $(BUILD)/sharded_capi.o
 
 LIB   := $(PKG)/liblinrec_cuda.so
 PYMOD := $(PKG)/linrec$(EXT)
 
 CPPTEST := $(BUILD)/test_cuda_api
+CPPSHARD := $(BUILD)/test_sharded
 
 .PHONY: all lib py oracle ref clean cpp-tests
 all: lib py oracle cpp-tests
 
 # C++ caller of include/linrec/cuda_scan.hpp + cuda_layers.hpp (host code only:
 # g++ against the C ABI and the CUDA runtime for device buffers).
-cpp-tests: $(CPPTEST)
+cpp-tests: $(CPPTEST) $(CPPSHARD)
+$(CPPSHARD): tests/cpp/test_sharded.cpp include/linrec/cuda_sharded.hpp include/linrec/cuda_scan.hpp include/linrec_cuda.h $(LIB)
+	@mkdir -p $(BUILD)
+	$(CXX) -std=c++17 -O2 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -llinrec_cuda \
+	  -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
 $(CPPTEST): tests/cpp/test_cuda_api.cpp include/linrec/cuda_scan.hpp include/linrec/cuda_layers.hpp include/linrec_cuda.h $(LIB)
 	@mkdir -p $(BUILD)
 	$(CXX) -std=c++17 -O2 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -llinrec_cuda \
@@ -55,6 +60,10 @@ $(BUILD)/%.o: $(CSRC)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(BUILD)/capi.o: $(CSRC)/capi.cpp $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
+
+$(BUILD)/sharded_capi.o: $(CSRC)/sharded_capi.cpp include/linrec_cuda.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
 

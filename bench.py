@@ -2,30 +2,38 @@
 """Benchmark of the linear-recurrence hot path (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2|c4|c1|c3] [--precision fp32|tf32]
+                    [--workload c2|c4|c1|c3|c5] [--precision fp32|tf32]
 
 One step = one forward scan (lam, x, h0 -> h) + one reverse-time backward scan
 (lam, h0, h, dh -> dlam, dx, dh0) over one batch of synthetic input, fp32.
-Default workload = BASELINE configs[1] ("C2"): T=65536, B=8, D=1024 on 1 GPU.
+Default workload = BASELINE configs[1] ("C2"): T=65536, B=8, D=1024.
 
 * ``value``      elements/s fwd+bwd (N_elements / step time), inputs resident in
-                 HBM, device-timed with CUDA events on the launching stream, max
-                 over ranks; each tensor is 2 GiB >> the 126 MB L2, so no flush
-                 is needed between steps.
-* ``e2e``        the same metric through the numpy-facing C ABI host entry points
-                 (linrec_scan_host_f32 / linrec_scan_backward_host_f32) from
-                 pinned host buffers: H2D of the inputs and D2H of every output
-                 inside the timed region.
+                 HBM, device-timed with CUDA events on the launching stream
+                 around exactly K steps, max over ranks; each tensor is 2 GiB
+                 >> the 126 MB L2, so no flush is needed between steps.  An
+                 untimed guard re-runs a channel subset over the full sequence
+                 with the bit-exact serial kernels (<= 1e-5 or the run fails).
+* ``slow_decay`` the same with lam ~ U(0.99, 1) (the fix-up's worst case).
+* ``c4`` / ``c4_seq_sharded``  the 1M-step workload (configs[3]) beside the
+                 headline: 1 GPU, and at N > 1 sequence-sharded over all ranks
+                 with its strong-scaling speed-up over rank 0 alone.
+* ``e2e``        the same metric through the reference's Python API
+                 (``linrec.scan`` / ``linrec.scan_backward``) on pageable numpy
+                 arrays, outputs allocated per call; ``e2e.pinned`` the C ABI
+                 host entry points from pinned buffers.
 * ``roofline``   dominant kernel (the backward scan: 20 of the 32 algorithmic
                  B/element) -- algorithmic bytes / measured launch time vs the
                  measured HBM copy peak (MEASURED_PEAKS.json).
 * ``cpu_baseline`` the reference's own CPU path (oracle/_ref, compiled from
-                 /root/reference) on this host's cores, bounded sample.
+                 /root/reference) on this host's cores, on the GPU arm's exact
+                 inputs, whole problem; plus its 1-core serial path.
 
-Multi-GPU (torchrun, one rank per GPU): workload c2 is channel-sharded (each
-rank owns an independent [T, W] block, no data-path collective; weak scaling);
-workload c4 (T = 2^20, W = 128) is sequence-sharded with one carry all-gather
-per direction (strong scaling).
+--gpus N without torchrun re-executes itself under torch.distributed.run (one
+rank per GPU).  Multi-GPU: c2 is channel-sharded (each rank an independent
+[T, W] block, no data-path collective; weak scaling); c4 is sequence-sharded
+with a peer-memory carry exchange (strong scaling); c5 (2^28 elements per
+(T, W) point) shards channels at large W and the sequence at small W.
 """
 from __future__ import annotations
 
@@ -162,129 +170,362 @@ def count_our_kernels(step, stream=None):
 
 
 # ---------------------------------------------------------------------------
-# our arm
+# synthetic inputs (bench.hpp:134-143 distributions), generated on the host
+# so the GPU arm, the e2e leg, the CPU baseline and the reference arm see the
+# SAME numbers; a global [T, ...] array is defined independently of how many
+# ranks share it (fixed row blocks, one PCG64 stream per block).
 # ---------------------------------------------------------------------------
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
-    from paper_1709_04057_b200 import capi
+LAM_BENCH = (0.05, 0.95)   # bench.hpp:134-143
+LAM_SLOW = (0.99, 1.0)     # slow decays: the fix-up walks whole segments
 
-    world, rank, local = dist_env()
-    # LINREC_BENCH_SHARE_GPU=1 (tests only): ranks share the visible GPUs and
-    # talk over gloo, to exercise the N > 1 code paths on a 1-GPU box.
-    share = os.environ.get("LINREC_BENCH_SHARE_GPU") == "1"
-    if share:
-        local = local % max(1, torch.cuda.device_count())
-    if world > 1:
-        if share:
-            dist.init_process_group("gloo")
+
+def host_rows(T, row_shape, lo, hi, seed, r0=0, r1=None):
+    """Rows [r0, r1) of a global float32 [T, *row_shape] array ~ U(lo, hi)."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+    r1 = T if r1 is None else r1
+    W = 1
+    for d in row_shape:
+        W *= d
+    bs = max(1, -(-T // 256))
+    nb = -(-T // bs)
+    seqs = np.random.SeedSequence(seed).spawn(nb)
+    out = np.empty((r1 - r0,) + tuple(row_shape), np.float32)
+    flat = out.reshape(r1 - r0, W)
+
+    def fill(k):
+        s, e = k * bs, min(T, (k + 1) * bs)
+        a, b = max(s, r0), min(e, r1)
+        if a >= b:
+            return
+        g = np.random.Generator(np.random.PCG64(seqs[k]))
+        dst = flat[a - r0:b - r0]
+        if (a, b) == (s, e):
+            g.random(out=dst, dtype=np.float32)
         else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    wl = WORKLOADS[args.workload]
-    T, B, D = wl["T"], wl["B"], wl["D"]
-    W = B * D
-    seq_sharded = args.workload == "c4" and world > 1
-    if seq_sharded:
-        from paper_1709_04057_b200 import sharded
-        Tl = sharded.segment_rows(T, world, rank)
-    else:
-        Tl = T
-    N_local = Tl * W
-    stream = torch.cuda.Stream(device=dev)
-    st = stream.cuda_stream
-    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
-    with torch.cuda.stream(stream):
-        lam = torch.empty(Tl, B, D, device=dev).uniform_(0.05, 0.95, generator=gen)
-        x = torch.empty(Tl, B, D, device=dev).uniform_(-1.0, 1.0, generator=gen)
-        h0 = torch.empty(B, D, device=dev).uniform_(-1.0, 1.0, generator=gen)
-        dh = torch.empty(Tl, B, D, device=dev).uniform_(-1.0, 1.0, generator=gen)
-        h = torch.empty_like(lam)
-        dlam = torch.empty_like(lam)
-        dx = torch.empty_like(lam)
-        dh0 = torch.empty_like(h0)
-    ws = capi.Workspace(local)
-    stream.synchronize()
+            dst[:] = g.random((e - s, W), dtype=np.float32)[a - s:b - s]
+        dst *= np.float32(hi - lo)
+        dst += np.float32(lo)
 
-    if seq_sharded:
-        runner = sharded.SequenceShardedScan(T, W, dist.group.WORLD, ws=ws, stream=stream)
+    with ThreadPoolExecutor(max(1, min(16, os.cpu_count() or 1))) as ex:
+        list(ex.map(fill, range(nb)))
+    return out
 
-        def fwd():
-            runner.forward(lam, x, h0 if rank == 0 else None, h)
 
-        def bwd():
-            runner.backward(lam, h0 if rank == 0 else None, h, dh, dlam, dx, dh0)
-        launches_per_step = runner.launches_per_step
-    else:
-        def fwd():
-            capi.scan(lam.data_ptr(), x.data_ptr(), h0.data_ptr(), h.data_ptr(), Tl, W,
-                      capi.PARALLEL, 4, ws.handle, st)
+def host_problem(T, B, D, seed, r0=0, r1=None, lam=LAM_BENCH):
+    """(lam, x, h0, dh) rows [r0, r1) of the global problem `seed`; h0 is the
+    global [B, D] initial state."""
+    return (host_rows(T, (B, D), lam[0], lam[1], seed * 10 + 1, r0, r1),
+            host_rows(T, (B, D), -1.0, 1.0, seed * 10 + 2, r0, r1),
+            host_rows(1, (B, D), -1.0, 1.0, seed * 10 + 3)[0],
+            host_rows(T, (B, D), -1.0, 1.0, seed * 10 + 4, r0, r1))
 
-        def bwd():
-            capi.scan_backward(lam.data_ptr(), h0.data_ptr(), h.data_ptr(), dh.data_ptr(),
-                               dlam.data_ptr(), dx.data_ptr(), dh0.data_ptr(), Tl, W,
-                               capi.PARALLEL, 4, ws.handle, st)
-        launches_per_step = capi.scan_kernel_count(Tl, W, False) + capi.scan_kernel_count(Tl, W, True)
 
-    # correctness guard (bench.hpp:204-216 analogue, untimed): chained scan vs
-    # the bit-exact serial kernel on the same device inputs.
-    if not seq_sharded:
-        with torch.cuda.stream(stream):
-            fwd()
-            hs = torch.empty_like(h)
-            capi.scan(lam.data_ptr(), x.data_ptr(), h0.data_ptr(), hs.data_ptr(), Tl, W,
-                      capi.SERIAL, 4, None, st)
-            err = ((h - hs).abs().max() / hs.abs().max().clamp_min(1.0)).item()
-            del hs
-        if err > 2e-4:
-            raise SystemExit(f"bench guard: chained vs serial disagreement {err:.3e}")
+SEED_C2, SEED_C4 = 1000, 4000
 
-    for _ in range(args.warmup):
-        fwd()
-        bwd()
-    # kernels per step counted on the device (untimed); the planner's count as fallback
-    counted = count_our_kernels(lambda: (fwd(), bwd()))
-    if counted is not None:
-        launches_per_step = counted
-    n_ev = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n_ev)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+# process group plumbing
+# ---------------------------------------------------------------------------
+class Ranks:
+    """world / rank / device; gloo when ranks share one GPU (tests)."""
+
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+        self.world, self.rank, self.local = dist_env()
+        # LINREC_BENCH_SHARE_GPU=1 (tests only): ranks share the visible GPUs and
+        # talk over gloo, to exercise the N > 1 code paths on a 1-GPU box.
+        self.share = os.environ.get("LINREC_BENCH_SHARE_GPU") == "1"
+        if self.share:
+            self.local = self.local % max(1, torch.cuda.device_count())
+        if self.world > 1:
+            if self.share:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+
+    def barrier(self):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+
+    def max(self, v):
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return v
+        t = torch.tensor([float(v)], dtype=torch.float64, device="cpu" if self.share else self.dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    def gather(self, obj):
+        import torch.distributed as dist
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        dist.all_gather_object(out, obj)
+        return out
+
+    def bcast(self, obj):
+        import torch.distributed as dist
+        if self.world == 1:
+            return obj
+        lst = [obj]
+        dist.broadcast_object_list(lst, src=0)
+        return lst[0]
+
+    def close(self):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+def time_steps(rk, fwd, bwd, steps, stream):
+    """EXACTLY `steps` (fwd, bwd) steps between a barrier + synchronize on
+    both sides, CUDA events on the launching stream, max over ranks; NVML
+    clocks sampled during the timed region."""
+    import torch
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    rk.barrier()
+    torch.cuda.synchronize(rk.dev)
+    with ClockSampler(rk.local) as clocks:
         start.record(stream)
-        for i in range(args.steps):
+        for i in range(steps):
             ev[i][0].record(stream)
             fwd()
             ev[i][1].record(stream)
             bwd()
             ev[i][2].record(stream)
         end.record(stream)
-        torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    total_ms = start.elapsed_time(end)
+        torch.cuda.synchronize(rk.dev)
+    rk.barrier()
+    total = rk.max(start.elapsed_time(end))
     fwd_ms = [e[0].elapsed_time(e[1]) for e in ev]
     bwd_ms = [e[1].elapsed_time(e[2]) for e in ev]
-    if world > 1:
-        t = torch.tensor([total_ms], device="cpu" if share else dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = t.item()
-    ms_step = total_ms / args.steps
-    N_total = (T * W) if seq_sharded else N_local * world
-    value = N_total / (ms_step / 1e3)
+    return {
+        "ms_per_step": total / steps,
+        "median_ms_per_step": rk.max(statistics.median(f + b for f, b in zip(fwd_ms, bwd_ms))),
+        "fwd_ms": rk.max(statistics.mean(fwd_ms)),
+        "bwd_ms": rk.max(statistics.mean(bwd_ms)),
+        "clocks": clocks.summary(),
+    }
 
+
+def rel_err(a, b):
+    """max|a - b| / max|b| (oracles.hpp:73-82), on the device."""
+    den = b.abs().max().item()
+    num = (a.double() - b.double()).abs().max().item()
+    return num / den if den else (0.0 if num == 0 else float("inf"))
+
+
+# ---------------------------------------------------------------------------
+# scan problems on the device: single GPU or sequence-sharded
+# ---------------------------------------------------------------------------
+class DeviceProblem:
+    """lam, x, h0, dh (inputs) and h, dlam, dx, dh0 (outputs) on the device,
+    [Tl, B, D] rows of a [T, B, D] problem."""
+
+    def __init__(self, host, dev, stream):
+        import torch
+        lam, x, h0, dh = host
+        with torch.cuda.stream(stream):
+            self.lam, self.x, self.h0, self.dh = (torch.from_numpy(a).to(dev, non_blocking=False)
+                                                  for a in (lam, x, h0, dh))
+            self.h = torch.empty_like(self.lam)
+            self.dlam = torch.empty_like(self.lam)
+            self.dx = torch.empty_like(self.lam)
+            self.dh0 = torch.empty_like(self.h0)
+        stream.synchronize()
+        self.Tl = self.lam.shape[0]
+        self.W = self.lam[0].numel()
+
+    def regen_lam(self, lo, hi, seed):
+        """Decays replaced in place (device RNG; the slow-decay variant)."""
+        import torch
+        g = torch.Generator(device=self.lam.device).manual_seed(seed)
+        self.lam.uniform_(lo, hi, generator=g)
+
+    def free(self):
+        for k in ("lam", "x", "h0", "dh", "h", "dlam", "dx", "dh0"):
+            setattr(self, k, None)
+
+
+def single_gpu_steps(P, ws, st):
+    from paper_1709_04057_b200 import capi
+
+    def fwd():
+        capi.scan(P.lam.data_ptr(), P.x.data_ptr(), P.h0.data_ptr(), P.h.data_ptr(), P.Tl, P.W,
+                  capi.PARALLEL, 4, ws.handle, st)
+
+    def bwd():
+        capi.scan_backward(P.lam.data_ptr(), P.h0.data_ptr(), P.h.data_ptr(), P.dh.data_ptr(),
+                           P.dlam.data_ptr(), P.dx.data_ptr(), P.dh0.data_ptr(), P.Tl, P.W,
+                           capi.PARALLEL, 4, ws.handle, st)
+    return fwd, bwd
+
+
+def sharded_steps(rk, P, T, ws, stream):
+    from paper_1709_04057_b200 import sharded
+    import torch.distributed as dist
+    runner = sharded.SequenceShardedScan(T, P.W, dist.group.WORLD, ws=ws, stream=stream)
+    r = rk.rank
+
+    def fwd():
+        runner.forward(P.lam, P.x, P.h0 if r == 0 else None, P.h)
+
+    def bwd():
+        runner.backward(P.lam, P.h0 if r == 0 else None, P.h, P.dh, P.dlam, P.dx, P.dh0)
+    return fwd, bwd, runner
+
+
+def guard(rk, P, stream, cols=8):
+    """Untimed correctness guard (the bench.hpp:204-216 analogue): a channel
+    subset over the FULL sequence -- every rank's rows gathered on rank 0 --
+    re-run with the bit-exact per-channel serial kernels (pinned to the
+    reference by the parity tests) and compared with what the timed path
+    produced.  Returns the max normwise error over h, dlam, dx, dh0."""
+    import numpy as np
+    import torch
+    from paper_1709_04057_b200 import capi
+    W = P.W
+    idx = torch.arange(0, W, max(1, W // cols), device=P.lam.device)[:cols]
+    with torch.cuda.stream(stream):
+        part = [t.view(t.shape[0], W).index_select(1, idx).cpu().numpy()
+                for t in (P.lam, P.x, P.dh, P.h, P.dlam, P.dx)]
+        h0s = P.h0.view(W).index_select(0, idx).cpu().numpy()
+        dh0s = P.dh0.view(W).index_select(0, idx).cpu().numpy()
+    parts = rk.gather(part)
+    err = None
+    if rk.rank == 0:
+        full = [np.ascontiguousarray(np.concatenate([p[i] for p in parts])) for i in range(6)]
+        L, X, DH, H, DL, DX = (torch.from_numpy(a).to(rk.dev) for a in full)
+        H0, DH0 = torch.from_numpy(h0s).to(rk.dev), torch.from_numpy(dh0s).to(rk.dev)
+        T, n = L.shape
+        st = torch.cuda.current_stream(rk.dev).cuda_stream
+        hs, dls, dxs, dh0r = (torch.empty_like(L), torch.empty_like(L), torch.empty_like(L),
+                              torch.empty_like(H0))
+        capi.scan(L.data_ptr(), X.data_ptr(), H0.data_ptr(), hs.data_ptr(), T, n, capi.SERIAL, 4, None, st)
+        capi.scan_backward(L.data_ptr(), H0.data_ptr(), hs.data_ptr(), DH.data_ptr(), dls.data_ptr(),
+                           dxs.data_ptr(), dh0r.data_ptr(), T, n, capi.SERIAL, 4, None, st)
+        torch.cuda.synchronize(rk.dev)
+        err = max(rel_err(H, hs), rel_err(DL, dls), rel_err(DX, dxs), rel_err(DH0, dh0r))
+    return rk.bcast(err)
+
+
+GUARD_TOL = 1e-5  # the north star's fp32 tolerance (test_smoke.py:35)
+
+
+def check_guard(err, what):
+    if err is None or not (err <= GUARD_TOL):
+        raise SystemExit(f"bench guard ({what}): max normwise error {err} > {GUARD_TOL}")
+
+
+def run_problem(rk, P, T, args, stream, ws, sharded_run, steps=None, count=False):
+    """Warm-up, guard and the timed region for one problem; returns the
+    timing record (+ the runner for sharded runs)."""
+    st = stream.cuda_stream
+    runner = None
+    if sharded_run:
+        fwd, bwd, runner = sharded_steps(rk, P, T, ws, stream)
+    else:
+        fwd, bwd = single_gpu_steps(P, ws, st)
+    for _ in range(args.warmup):
+        fwd()
+        bwd()
+    # sequence-sharded: rank 0 checks the gathered full sequence; otherwise
+    # every rank checks its own independent block
+    g = guard(rk, P, stream) if sharded_run else rk.max(guard(_Solo(rk), P, stream))
+    rec = time_steps(rk, fwd, bwd, steps or args.steps, stream)
+    rec["guard_max_rel_err"] = g
+    if count:
+        n = count_our_kernels(lambda: (fwd(), bwd()))
+        rec["launches_per_step"] = n
+    if runner is not None:
+        rec["exchange"] = runner.exchange
+        runner.close()
+    return rec
+
+
+def summarize(rec, N_total, N_local, peak):
+    ms = rec["ms_per_step"]
+    out = {
+        "value": N_total / (ms / 1e3),
+        "ms_per_step": ms,
+        "median_ms_per_step": rec["median_ms_per_step"],
+        "fwd_ms": rec["fwd_ms"],
+        "bwd_ms": rec["bwd_ms"],
+        "hbm_gbs_per_gpu": (FWD_BYTES + BWD_BYTES) * N_local / (ms / 1e3) / 1e9,
+        "guard_max_rel_err": rec["guard_max_rel_err"],
+    }
+    out["frac_of_peak_per_gpu"] = out["hbm_gbs_per_gpu"] / peak
+    return out
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    from paper_1709_04057_b200 import capi
+
+    rk = Ranks()
+    world, rank = rk.world, rk.rank
+    wl = WORKLOADS[args.workload]
+    T, B, D = wl["T"], wl["B"], wl["D"]
+    W = B * D
+    seq_sharded = args.workload == "c4" and world > 1
+    stream = torch.cuda.Stream(device=rk.dev)
+    st = stream.cuda_stream
+    ws = capi.Workspace(rk.local)
     peak, peak_kind = peaks()
-    fwd_avg = statistics.mean(fwd_ms)
-    bwd_avg = statistics.mean(bwd_ms)
-    fwd_gbs = FWD_BYTES * N_local / (fwd_avg / 1e3) / 1e9
-    bwd_gbs = BWD_BYTES * N_local / (bwd_avg / 1e3) / 1e9
-    step_gbs = (FWD_BYTES + BWD_BYTES) * N_local / (ms_step / 1e3) / 1e9 if not seq_sharded else \
-        (FWD_BYTES + BWD_BYTES) * N_local / (ms_step / 1e3) / 1e9
-    traffic = traffic_from_profile(N_local)
+
+    # the headline problem: c2 -> every rank its own [T, B, D] block (channel
+    # sharding: no collective, weak scaling); c4 -> rank r rows of the global
+    # problem (sequence sharding, strong scaling)
+    if seq_sharded:
+        from paper_1709_04057_b200 import sharded
+        r0, r1 = sharded.segment_bounds(T, world, rank)
+        host = host_problem(T, B, D, SEED_C4, r0, r1)
+    else:
+        seed = (SEED_C4 if args.workload == "c4" else SEED_C2) + (rank if world > 1 else 0)
+        host = host_problem(T, B, D, seed)
+    P = DeviceProblem(host, rk.dev, stream)
+    N_local = P.Tl * W
+    N_total = T * W if seq_sharded else N_local * world
+
+    rec = run_problem(rk, P, T, args, stream, ws, seq_sharded, count=True)
+    check_guard(rec["guard_max_rel_err"], args.workload)
+    ms_step = rec["ms_per_step"]
+    value = N_total / (ms_step / 1e3)
+    fwd_gbs = FWD_BYTES * N_local / (rec["fwd_ms"] / 1e3) / 1e9
+    bwd_gbs = BWD_BYTES * N_local / (rec["bwd_ms"] / 1e3) / 1e9
+    step_gbs = (FWD_BYTES + BWD_BYTES) * N_local / (ms_step / 1e3) / 1e9
+    launches = rec.get("launches_per_step")
+
+    # the same problem with slow decays lam ~ U(0.99, 1) (DESIGN.md 4)
+    slow = None
+    if not args.no_slow:
+        P.regen_lam(*LAM_SLOW, seed=77 + rank)
+        srec = run_problem(rk, P, T, args, stream, ws, seq_sharded, steps=min(args.steps, 10))
+        check_guard(srec["guard_max_rel_err"], args.workload + " slow decays")
+        slow = dict(summarize(srec, N_total, N_local, peak), lam="U(0.99,1)")
 
     result = None
     if rank == 0:
@@ -296,26 +537,32 @@ def run_ours(args):
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": ms_step,
+            "median_ms_per_step": rec["median_ms_per_step"],
             "higher_is_better": True,
             "scaling": "strong" if seq_sharded else "weak",
             "vs_baseline": None,
             "dtype": "f32",
-            "data": "synthetic: lam~U(0.05,0.95), x,h0,dh~U(-1,1) (bench.hpp:134-143), torch RNG on device",
+            "data": ("synthetic: lam~U(0.05,0.95), x,h0,dh~U(-1,1) (bench.hpp:134-143), generated on the host "
+                     "(numpy PCG64, seeded) and copied to HBM; the CPU baseline / e2e leg / reference arm use "
+                     "the same arrays"),
             "config": {
                 "workload": wl["desc"],
                 "T": T, "B": B, "D": D, "elements_per_step": N_total,
                 "parallelism": ("sequence-sharded x%d (carry exchange: %s)" % (
-                    world, "peer-memory mailboxes over NVLink" if runner.exchange == "p2p" else "all-gather"))
+                    world, "peer-memory mailboxes over NVLink" if rec.get("exchange") == "p2p" else "all-gather"))
                 if seq_sharded
-                else ("single GPU" if world == 1 else "channel-sharded x%d (independent [T,W] blocks, no collective)" % world),
-                "l2": "no flush: every tensor is %.0f MiB >> 126 MB L2" % (N_local * 4 / 2**20),
-                "timing": "CUDA events on the launching stream, max over ranks",
+                else ("single GPU" if world == 1 else
+                      "channel-sharded x%d (every rank an independent [T, B*D] block, no collective)" % world),
+                "l2": "no flush: every tensor is %.0f MiB per GPU >> 126 MB L2" % (N_local * 4 / 2**20),
+                "timing": "CUDA events on the launching stream, barrier + synchronize around exactly `steps` "
+                          "steps, max over ranks; value = elements / (total / steps)",
+                "guard_max_rel_err": rec["guard_max_rel_err"],
             },
             "hbm_gbs": step_gbs,
             "pct_of_peak": 100.0 * step_gbs / peak,
             "kernels": {
-                "fwd": {"ms": fwd_avg, "gbs": fwd_gbs, "bytes_per_element": FWD_BYTES},
-                "bwd": {"ms": bwd_avg, "gbs": bwd_gbs, "bytes_per_element": BWD_BYTES},
+                "fwd": {"ms": rec["fwd_ms"], "gbs": fwd_gbs, "bytes_per_element": FWD_BYTES},
+                "bwd": {"ms": rec["bwd_ms"], "gbs": bwd_gbs, "bytes_per_element": BWD_BYTES},
             },
             "roofline": {
                 "bound": "hbm",
@@ -325,172 +572,351 @@ def run_ours(args):
                 "peak_kind": peak_kind,
                 "unit": "GB/s",
                 "frac": bwd_gbs / peak,
-                "traffic": traffic,
+                "traffic": traffic_from_profile(N_local),
                 "algorithmic_bytes_per_launch": BWD_BYTES * N_local,
                 "fwd": {"achieved": fwd_gbs, "frac": fwd_gbs / peak, "algorithmic_bytes_per_launch": FWD_BYTES * N_local},
             },
-            "gpu_launches": launches_per_step * args.steps,
-            "gpu_launches_method": "kernels of this repo per step counted with torch.profiler (CUPTI) over one untimed step, x steps",
-            "clocks": clocks.summary(),
+            "gpu_launches": (launches * args.steps) if launches is not None else None,
+            "gpu_launches_method": "kernels of this repo per step counted with torch.profiler (CUPTI) over one "
+                                   "untimed step, x steps",
+            "clocks": rec["clocks"],
         }
-    # free device memory before the e2e leg
-    del lam, x, h0, dh, h, dlam, dx, dh0
+        if slow is not None:
+            result["slow_decay"] = slow
+    P.free()
     torch.cuda.empty_cache()
-    if world > 1:
-        dist.barrier()
-    e2e = None
+
+    # C4 (BASELINE configs[3], the 1M-step workload) beside the C2 headline:
+    # at N = 1 the single-GPU scan; at N > 1 also the sequence-sharded run over
+    # all ranks and its strong-scaling speed-up over rank 0 alone.
+    if args.workload == "c2" and not args.no_c4:
+        c4 = c4_records(rk, args, stream, ws, peak)
+        if rank == 0:
+            result.update(c4)
+
+    # end to end through the public API with host buffers
     if not args.no_e2e and not seq_sharded:
-        e2e = e2e_leg(args, T, B, D, local, world, share)
-    if rank == 0:
-        if e2e is not None:
+        e2e = e2e_legs(rk, args, host, T, B, D)
+        if rank == 0:
             result["e2e"] = e2e
-        if not args.no_cpu and world == 1:
-            result["cpu_baseline"] = cpu_baseline_leg(args, T, B, D)
+    if rank == 0 and not args.no_cpu and world == 1:
+        result["cpu_baseline"] = cpu_baseline_leg(args, host, T, B, D)
+    del host
+    if rank == 0:
         print(json.dumps(result), flush=True)
-    if world > 1:
-        if seq_sharded:
-            runner.close()
-        dist.barrier()
-        dist.destroy_process_group()
+    rk.close()
 
 
-def e2e_leg(args, T, B, D, device, world=1, share=False):
-    """Same metric through the host-pointer C ABI from pinned host memory; at
-    N > 1 every rank runs its own block concurrently (max time over ranks)."""
+def c4_records(rk, args, stream, ws, peak):
+    """{"c4": ...} at N = 1; {"c4": ..., "c4_seq_sharded": ...} at N > 1."""
+    import torch
+    from paper_1709_04057_b200 import sharded
+    wl = WORKLOADS["c4"]
+    T, B, D = wl["T"], wl["B"], wl["D"]
+    W = B * D
+    out = {}
+    # rank 0 alone: the 1-GPU C4 (the strong-scaling base)
+    one = None
+    if rk.rank == 0:
+        one_rk = _Solo(rk)
+        P = DeviceProblem(host_problem(T, B, D, SEED_C4), rk.dev, stream)
+        rec = run_problem(one_rk, P, T, args, stream, ws, False)
+        check_guard(rec["guard_max_rel_err"], "c4")
+        one = summarize(rec, T * W, T * W, peak)
+        if not args.no_slow:
+            P.regen_lam(*LAM_SLOW, seed=78)
+            srec = run_problem(one_rk, P, T, args, stream, ws, False, steps=min(args.steps, 10))
+            check_guard(srec["guard_max_rel_err"], "c4 slow decays")
+            one["slow_decay"] = dict(summarize(srec, T * W, T * W, peak), lam="U(0.99,1)")
+        P.free()
+        torch.cuda.empty_cache()
+        out["c4"] = dict(one, workload=wl["desc"], n_gpus=1, T=T, W=W)
+    rk.barrier()
+    if rk.world > 1:
+        r0, r1 = sharded.segment_bounds(T, rk.world, rk.rank)
+        P = DeviceProblem(host_problem(T, B, D, SEED_C4, r0, r1), rk.dev, stream)
+        rec = run_problem(rk, P, T, args, stream, ws, True, count=True)
+        check_guard(rec["guard_max_rel_err"], "c4 sequence-sharded")
+        rec_n = summarize(rec, T * W, P.Tl * W, peak)
+        rec_n["exchange"] = rec.get("exchange")
+        rec_n["launches_per_step_rank0"] = rec.get("launches_per_step")
+        if not args.no_slow:
+            P.regen_lam(*LAM_SLOW, seed=79 + rk.rank)
+            srec = run_problem(rk, P, T, args, stream, ws, True, steps=min(args.steps, 10))
+            check_guard(srec["guard_max_rel_err"], "c4 sequence-sharded slow decays")
+            rec_n["slow_decay"] = dict(summarize(srec, T * W, P.Tl * W, peak), lam="U(0.99,1)")
+        P.free()
+        torch.cuda.empty_cache()
+        if rk.rank == 0:
+            rec_n.update(workload=wl["desc"] + " sequence-sharded", n_gpus=rk.world, T=T, W=W,
+                         scaling="strong", n1_value=one["value"], n1_ms_per_step=one["ms_per_step"],
+                         speedup=rec_n["value"] / one["value"])
+            if "slow_decay" in rec_n and "slow_decay" in one:
+                rec_n["slow_decay"]["speedup"] = rec_n["slow_decay"]["value"] / one["slow_decay"]["value"]
+            out["c4_seq_sharded"] = rec_n
+    return out
+
+
+class _Solo:
+    """Ranks view of rank 0 alone (no collectives)."""
+
+    def __init__(self, rk):
+        self.world, self.rank, self.local, self.dev, self.share = 1, 0, rk.local, rk.dev, rk.share
+
+    def barrier(self):
+        pass
+
+    def max(self, v):
+        return v
+
+    def gather(self, obj):
+        return [obj]
+
+    def bcast(self, obj):
+        return obj
+
+
+def e2e_legs(rk, args, host, T, B, D):
+    """The metric end to end through the public API a reference user calls:
+    ``linrec.scan`` / ``linrec.scan_backward`` on ordinary (pageable) numpy
+    arrays, outputs freshly allocated per call (linrec_py.cpp:91-140) -- the
+    headline e2e.  Secondary (N = 1): the host-pointer C ABI from pinned
+    buffers.  At N > 1 every rank runs its own block concurrently (max over
+    ranks)."""
     import numpy as np
     import torch
-    import torch.distributed as dist
-    from paper_1709_04057_b200 import capi
+    from paper_1709_04057_b200 import capi, linrec
 
+    lam, x, h0, dh = host
     W = B * D
     N = T * W
-    shape = (T, B, D)
-    pin = lambda s: torch.empty(s, dtype=torch.float32, pin_memory=True)  # noqa: E731
-    lam, x, dh, h, dlam, dx = (pin(shape) for _ in range(6))
-    h0, dh0 = pin((B, D)), pin((B, D))
-    rng = np.random.default_rng(5)
-    chunk = 1 << 14
-    for t0 in range(0, T, chunk):  # fill without a 2 GiB temporary
-        sl = slice(t0, min(T, t0 + chunk))
-        n = (sl.stop - sl.start, B, D)
-        lam[sl].numpy()[:] = rng.uniform(0.05, 0.95, n)
-        x[sl].numpy()[:] = rng.uniform(-1, 1, n)
-        dh[sl].numpy()[:] = rng.uniform(-1, 1, n)
-    h0.numpy()[:] = rng.uniform(-1, 1, (B, D))
-    p = lambda t: t.data_ptr()  # noqa: E731
+    steps = max(1, min(args.steps, args.e2e_steps))
 
     def step():
-        capi.scan_host(p(lam), p(x), p(h0), p(h), T, W, capi.PARALLEL, 4, device)
-        capi.scan_backward_host(p(lam), p(h0), p(h), p(dh), p(dlam), p(dx), p(dh0), T, W,
-                                capi.PARALLEL, 4, device)
+        h = linrec.scan(lam, x, h0)
+        linrec.scan_backward(lam, h0, h, dh)
 
-    steps = max(1, min(args.steps, args.e2e_steps))
-    for _ in range(max(1, min(args.warmup, 2))):
-        step()
-    if world > 1:
-        dist.barrier()
+    step()  # warm: pipeline buffers, staging
+    rk.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         step()
-    dt = (time.perf_counter() - t0) / steps
-    if world > 1:
-        t = torch.tensor([dt], device="cpu" if share else torch.device("cuda", device))
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = t.item()
-    return {
-        "value": world * N / dt,
+    dt = rk.max((time.perf_counter() - t0) / steps)
+    out = {
+        "value": rk.world * N / dt,
         "unit": "elements/s",
         "ms_per_step": dt * 1e3,
         "steps": steps,
-        # per rank x ranks; fwd: lam, x, h0 in / h out; bwd: lam, h, dh, h0 in / dlam, dx, dh0 out
-        "h2d_bytes_per_step": world * (4 * (2 * N + W) + 4 * (3 * N + W)),
-        "d2h_bytes_per_step": world * (4 * N + 4 * (2 * N + W)),
-        "api": "linrec_scan_host_f32 + linrec_scan_backward_host_f32 (the numpy boundary of linrec.scan / linrec.scan_backward), pinned buffers",
-        "timing": "host wall clock, synchronous calls, max over ranks",
-        "ranks": world,
+        # fwd: lam, x, h0 in / h out; bwd: lam, h0, h, dh in / dlam, dx, dh0 out (per rank x ranks)
+        "h2d_bytes_per_step": rk.world * (4 * (2 * N + W) + 4 * (3 * N + W)),
+        "d2h_bytes_per_step": rk.world * (4 * N + 4 * (2 * N + W)),
+        "api": "paper_1709_04057_b200.linrec.scan + linrec.scan_backward (the reference's Python API, "
+               "linrec_py.cpp:91-140) on pageable numpy arrays, outputs allocated per call",
+        "timing": "host wall clock around synchronous calls, max over ranks",
+        "ranks": rk.world,
     }
+    if rk.world == 1 and not args.no_pinned:
+        pin = lambda s: torch.empty(s, dtype=torch.float32, pin_memory=True)  # noqa: E731
+        shape = (T, B, D)
+        pl, px, pdh, ph, pdl, pdx = (pin(shape) for _ in range(6))
+        ph0, pdh0 = pin((B, D)), pin((B, D))
+        for dst, src in ((pl, lam), (px, x), (pdh, dh), (ph0, h0)):
+            dst.numpy()[...] = src
+        p = lambda t: t.data_ptr()  # noqa: E731
+        dev = rk.local
+
+        def pstep():
+            capi.scan_host(p(pl), p(px), p(ph0), p(ph), T, W, capi.PARALLEL, 4, dev)
+            capi.scan_backward_host(p(pl), p(ph0), p(ph), p(pdh), p(pdl), p(pdx), p(pdh0), T, W,
+                                    capi.PARALLEL, 4, dev)
+        pstep()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            pstep()
+        dtp = (time.perf_counter() - t0) / steps
+        out["pinned"] = {"value": N / dtp, "unit": "elements/s", "ms_per_step": dtp * 1e3, "steps": steps,
+                         "api": "linrec_scan_host_f32 + linrec_scan_backward_host_f32 (C ABI) from pinned buffers"}
+        del pl, px, pdh, ph, pdl, pdx, ph0, pdh0
+    return out
 
 
-def cpu_baseline_leg(args, T, B, D):
-    """The reference's CPU implementation (oracle/_ref) on this host's cores,
-    bounded sample, bench.hpp:93-107 protocol."""
-    import numpy as np
+def cpu_baseline_leg(args, host, T, B, D):
+    """The reference's own CPU implementation (oracle/_ref, compiled from
+    /root/reference with its -march=native flags where they fit this host) on
+    the GPU arm's exact inputs, the whole C2 problem (no sampling): its
+    scan_parallel + scan_backward(Parallel) with workers = all host cores, and
+    the 1-core scan_serial + scan_backward(Serial); bench.hpp:93-107 protocol
+    (median of reps, allocation inside the calls timed)."""
     try:
-        from oracle.oracle import RefLib
-        ref = RefLib()
+        from oracle.oracle import RefLib, ref_build
+        ref_dir, march = ref_build()
+        ref = RefLib(os.path.join(ref_dir, "liblinrec_ref.so"))
     except Exception as e:
         return {"value": None, "unit": "elements/s", "cores": 0, "kind": "reference",
                 "sample": f"unavailable: {e}"}
+    lam, x, h0, dh = host
     cores = os.cpu_count() or 1
-    Ts = min(T, args.cpu_rows)
-    rng = np.random.default_rng(7)
-    lam = rng.uniform(0.05, 0.95, (Ts, B, D)).astype(np.float32)
-    x = rng.uniform(-1, 1, (Ts, B, D)).astype(np.float32)
-    h0 = rng.uniform(-1, 1, (B, D)).astype(np.float32)
-    dh = rng.uniform(-1, 1, (Ts, B, D)).astype(np.float32)
-    f, b = ref.bench_fwd_bwd(lam, x, h0, dh, cores, warmup=1, reps=args.cpu_reps)
-    n = Ts * B * D
-    return {
+    n = T * B * D
+    f, b = ref.bench_fwd_bwd(lam, x, h0, dh, cores, warmup=0, reps=args.cpu_reps)
+    out = {
         "value": n / (f + b),
         "unit": "elements/s",
         "cores": cores,
         "kind": "reference",
-        "sample": (f"T={Ts} of {T} rows x B={B} x D={D} ({n} elements): reference scan_parallel + "
-                   f"scan_backward(ScanMode::Parallel), workers={cores}, median of {args.cpu_reps} reps"),
+        "sample": (f"the whole workload T={T} x B={B} x D={D} ({n} elements), the GPU arm's inputs: reference "
+                   f"scan_parallel + scan_backward(ScanMode::Parallel), workers={cores}, median of "
+                   f"{args.cpu_reps} rep(s)"),
+        "cpu_model": cpu_model(),
+        "build": f"oracle/_ref ({march}): recurrence.hpp + thread_pool.cpp compiled from /root/reference",
         "fwd_elements_per_s": n / f,
         "bwd_elements_per_s": n / b,
     }
+    if not args.no_serial_cpu:
+        fs, bs = ref.bench_serial(lam, x, h0, dh, warmup=0, reps=1)
+        out["serial_1core"] = {"value": n / (fs + bs), "cores": 1,
+                               "fwd_elements_per_s": n / fs, "bwd_elements_per_s": n / bs,
+                               "sample": "same inputs: reference scan_serial + scan_backward(ScanMode::Serial)"}
+    return out
+
+
+# ---------------------------------------------------------------------------
+# C5: the fixed-2^28-element sweep (BASELINE configs[4])
+# ---------------------------------------------------------------------------
+C5_POINTS = [(1 << 8, 1 << 20), (1 << 12, 1 << 16), (1 << 16, 1 << 12), (1 << 20, 1 << 8), (1 << 24, 1 << 4)]
+C5_SEQ_SHARD_MAX_W = 256  # at N > 1: sequence sharding at W <= 256, channel sharding above
+
+
+def run_c5(args):
+    """Every (T, W) point at N = T*W = 2^28: one GPU, or N ranks sharing the
+    fixed problem (strong scaling) -- channels split at large W (each rank a
+    contiguous [T, W/N] block: no collective), the sequence at small W."""
+    import torch
+    from paper_1709_04057_b200 import capi, sharded
+    rk = Ranks()
+    stream = torch.cuda.Stream(device=rk.dev)
+    ws = capi.Workspace(rk.local)
+    peak, peak_kind = peaks()
+    points = []
+    total_ms = 0.0
+    clocks = None
+    launches = 0
+    for k, (T, W) in enumerate(C5_POINTS):
+        seq = rk.world > 1 and W <= C5_SEQ_SHARD_MAX_W
+        if seq:
+            r0, r1 = sharded.segment_bounds(T, rk.world, rk.rank)
+            host = host_problem(T, 1, W, 5000 + k, r0, r1)
+        elif rk.world > 1:
+            c0, c1 = sharded.channel_shard(W, rk.world, rk.rank)
+            host = host_problem(T, 1, c1 - c0, 5000 + 10 * k + rk.rank)
+        else:
+            host = host_problem(T, 1, W, 5000 + k)
+        P = DeviceProblem(host, rk.dev, stream)
+        del host
+        rec = run_problem(rk, P, T, args, stream, ws, seq, count=True)
+        check_guard(rec["guard_max_rel_err"], f"c5 T={T} W={W}")
+        rec_s = summarize(rec, T * W, P.Tl * P.W, peak)
+        rec_s.update(T=T, W=W, sharding=("sequence" if seq else "channel" if rk.world > 1 else "none"))
+        points.append(rec_s)
+        total_ms += rec["ms_per_step"]
+        launches += rec.get("launches_per_step") or 0
+        clocks = rec["clocks"]
+        P.free()
+        torch.cuda.empty_cache()
+    if rk.rank == 0:
+        n_total = sum(T * W for T, W in C5_POINTS)
+        best = max(points, key=lambda p: p["frac_of_peak_per_gpu"])
+        worst = min(points, key=lambda p: p["frac_of_peak_per_gpu"])
+        print(json.dumps({
+            "metric": METRIC,
+            "value": n_total / (total_ms / 1e3),
+            "unit": "elements/s",
+            "n_gpus": rk.world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": total_ms,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic: lam~U(0.05,0.95), x,h0,dh~U(-1,1), host-generated",
+            "config": {"workload": "C5 fixed 2^28 elements per point, (T, W) in " +
+                       ", ".join(f"(2^{T.bit_length() - 1}, 2^{W.bit_length() - 1})" for T, W in C5_POINTS) +
+                       " (BASELINE configs[4]); a step = one fwd+bwd of every point",
+                       "parallelism": "single GPU" if rk.world == 1 else
+                       f"x{rk.world}: sequence-sharded at W <= {C5_SEQ_SHARD_MAX_W}, channel-sharded above",
+                       "l2": "no flush: every tensor is 1 GiB (/N per GPU)"},
+            "points": points,
+            "roofline": {"bound": "hbm", "kernel": "fwd+bwd chained scans per point", "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s",
+                         "achieved": best["hbm_gbs_per_gpu"], "frac": best["frac_of_peak_per_gpu"],
+                         "worst_point": {"T": worst["T"], "W": worst["W"], "frac": worst["frac_of_peak_per_gpu"]},
+                         "traffic": None},
+            "gpu_launches": launches * args.steps,
+            "clocks": clocks,
+        }), flush=True)
+    rk.close()
 
 
 # ---------------------------------------------------------------------------
 # reference arm: the reference's own CPU implementation through its public
 # Python API (oracle/_ref/linrec*.so = proj/bindings/linrec_py.cpp compiled
-# from /root/reference), on this host's cores.
+# from /root/reference), on this host's cores, on the SAME config and inputs
+# as our arm's rank 0 (no sampling).
 # ---------------------------------------------------------------------------
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    import numpy as np
-    wl = WORKLOADS[args.workload]
-    T, B, D = wl["T"], wl["B"], wl["D"]
     try:
-        from oracle.oracle import load_reference_module
-        ref = load_reference_module()
+        from oracle.oracle import load_reference_module, ref_build
+        ref_dir, march = ref_build()
+        ref = load_reference_module(ref_dir)
     except Exception as e:
         print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built: {e}"}))
         return
     cores = os.cpu_count() or 1
-    Ts = min(T, args.cpu_rows)
-    rng = np.random.default_rng(7)
-    lam = rng.uniform(0.05, 0.95, (Ts, B, D)).astype(np.float32)
-    x = rng.uniform(-1, 1, (Ts, B, D)).astype(np.float32)
-    h0 = rng.uniform(-1, 1, (B, D)).astype(np.float32)
-    dh = rng.uniform(-1, 1, (Ts, B, D)).astype(np.float32)
+    if args.workload == "c5":
+        points = C5_POINTS
+        seeds = [5000 + k for k in range(len(points))]
+        desc = "C5 fixed 2^28 elements per point (BASELINE configs[4])"
+        shapes = [(T, 1, W) for T, W in points]
+    else:
+        wl = WORKLOADS[args.workload]
+        shapes = [(wl["T"], wl["B"], wl["D"])]
+        seeds = [SEED_C4 if args.workload == "c4" else SEED_C2]
+        desc = wl["desc"]
+    probs = [host_problem(*shp, seed) for shp, seed in zip(shapes, seeds)]
 
     def step():
-        h = ref.scan(lam, x, h0, workers=cores)
-        ref.scan_backward(lam, h0, h, dh, workers=cores)
+        for lam, x, h0, dh in probs:
+            h = ref.scan(lam, x, h0, workers=cores)
+            ref.scan_backward(lam, h0, h, dh, workers=cores)
 
-    for _ in range(args.warmup):
+    steps, warmup = args.steps, args.warmup
+    if args.workload == "c5":  # 5 x 2^28 elements per step on the host: bounded
+        steps, warmup = min(steps, 2), min(warmup, 1)
+    for _ in range(warmup):
         step()
     times = []
-    for _ in range(args.steps):
+    for _ in range(steps):
         t0 = time.perf_counter()
         step()
         times.append(time.perf_counter() - t0)
     ms = 1e3 * sum(times) / len(times)
-    n = Ts * B * D
+    n = sum(T * B * D for T, B, D in shapes)
     value = n / (ms / 1e3)
-    sample = (f"T={Ts} of {T} rows x B={B} x D={D} ({n} elements) per step: linrec.scan + "
-              f"linrec.scan_backward (reference pybind11 API, numpy in/out), workers={cores}")
+    sample = (f"the whole workload ({n} elements per step, the same seeded inputs as our arm's rank 0): "
+              f"linrec.scan + linrec.scan_backward (reference pybind11 API, numpy in/out), workers={cores}, "
+              f"build {march}")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "elements/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "n_gpus": world, "steps": steps, "warmup": warmup, "ms_per_step": ms,
+        "median_ms_per_step": 1e3 * statistics.median(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic: lam~U(0.05,0.95), x,h0,dh~U(-1,1)",
-        "config": {"workload": wl["desc"], "T": T, "B": B, "D": D, "sampled_rows": Ts},
-        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": cores, "kind": "reference", "sample": sample},
+        "data": "synthetic: lam~U(0.05,0.95), x,h0,dh~U(-1,1), host-generated (numpy PCG64, seeded)",
+        "config": {"workload": desc, "shapes": shapes, "sampled": False},
+        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": cores, "kind": "reference",
+                         "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -743,27 +1169,56 @@ def run_reference_layer(args):
     }), flush=True)
 
 
+def relaunch(args):
+    """--gpus N without torchrun: re-exec this script under
+    torch.distributed.run, one rank per GPU (the driver's own launch form)."""
+    import subprocess
+    import socket
+    if os.environ.get("LINREC_BENCH_SHARE_GPU") != "1" and args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} GPU(s) visible "
+                             "(LINREC_BENCH_SHARE_GPU=1 lets ranks share GPUs, for tests)")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["c5"], default="c2")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-rows", type=int, default=4096)
-    ap.add_argument("--cpu-reps", type=int, default=5)
+    ap.add_argument("--cpu-reps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-pinned", action="store_true", help="skip the secondary pinned-buffer e2e figure")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-serial-cpu", action="store_true", help="skip the 1-core reference row")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 records beside the C2 headline")
+    ap.add_argument("--no-slow", action="store_true", help="skip the lam~U(0.99,1) re-runs")
     ap.add_argument("--precision", choices=["fp32", "tf32"], default="fp32", help="c3 GEMM precision")
     ap.add_argument("--layer-cpu-rows", type=int, default=16)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch(args)
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} launched with WORLD_SIZE={world}")
     if args.workload == "c3":
         run_reference_layer(args) if args.impl == "reference" else run_layer(args)
     elif args.impl == "reference":
         run_reference(args)
+    elif args.workload == "c5":
+        run_c5(args)
     else:
         run_ours(args)
 

@@ -135,14 +135,42 @@ inline int plan_bwd_call(const double* l, const double* h0, const double* h, con
                          double* dx, double* dh0, index_t T, index_t W, const index_t* b, index_t p, void* st) {
   return linrec_scan_backward_plan_f64(l, h0, h, dh, dl, dx, dh0, T, W, b, p, st);
 }
+inline int screen_call(const float* v, index_t T, index_t b, index_t n, const char* name, void* st) {
+  return linrec_screen_finite_f32(v, T, b, n, name, st);
+}
+inline int screen_call(const double* v, index_t T, index_t b, index_t n, const char* name, void* st) {
+  return linrec_screen_finite_f64(v, T, b, n, name, st);
+}
 }  // namespace detail
+
+// screen_finite (recurrence.hpp:133-155): ContractViolation naming the first
+// non-finite element, "non-finite value in <name> at [t=.., b=.., n=..]".
+template <class S>
+void screen_finite(const DeviceTensor3<S>& t, const char* name, void* stream = nullptr) {
+  throw_status(detail::screen_call(t.data, t.steps, t.batch, t.features, name, stream));
+}
+template <class S>
+void screen_finite(const DeviceTensor2<S>& t, const char* name, void* stream = nullptr) {
+  if (t.data == nullptr) return;  // "zeros": finite
+  throw_status(detail::screen_call(t.data, 0, t.rows, t.cols, name, stream));
+}
+// screen_recurrence (recurrence.hpp:157-163).
+template <class S>
+void screen_recurrence(const DeviceTensor3<S>& decays, const DeviceTensor3<S>& impulses,
+                       const DeviceTensor2<S>& initial, void* stream = nullptr) {
+  screen_finite(decays, "decays", stream);
+  screen_finite(impulses, "impulses", stream);
+  screen_finite(initial, "initial", stream);
+}
 
 // scan_serial (recurrence.hpp:169-179): bit-exact serial recurrence.
 template <class S>
 void scan_serial(const DeviceTensor3<S>& decays, const DeviceTensor3<S>& impulses,
-                 const DeviceTensor2<S>& initial, DeviceTensor3<S>& h, void* stream = nullptr) {
+                 const DeviceTensor2<S>& initial, DeviceTensor3<S>& h, void* stream = nullptr,
+                 bool check_finite = false) {
   validate_recurrence_shapes(decays, impulses, initial);
   check_same_shape(decays, h, "scan_serial(h)");
+  if (check_finite) screen_recurrence(decays, impulses, initial, stream);
   throw_status(detail::scan_call(decays.data, impulses.data, initial.data, h.data, decays.steps,
                                  decays.step_size(), LINREC_SERIAL, nullptr, stream));
 }
@@ -151,9 +179,10 @@ void scan_serial(const DeviceTensor3<S>& decays, const DeviceTensor3<S>& impulse
 template <class S>
 void scan_parallel(const DeviceTensor3<S>& decays, const DeviceTensor3<S>& impulses,
                    const DeviceTensor2<S>& initial, DeviceTensor3<S>& h, void* stream = nullptr,
-                   linrec_workspace_t ws = nullptr) {
+                   linrec_workspace_t ws = nullptr, bool check_finite = false) {
   validate_recurrence_shapes(decays, impulses, initial);
   check_same_shape(decays, h, "scan_parallel(h)");
+  if (check_finite) screen_recurrence(decays, impulses, initial, stream);
   throw_status(detail::scan_call(decays.data, impulses.data, initial.data, h.data, decays.steps,
                                  decays.step_size(), LINREC_PARALLEL, ws, stream));
 }
@@ -181,6 +210,19 @@ inline ChunkPlan plan_chunks(index_t T, int requested_workers) {
   return plan;
 }
 
+// validate_plan (recurrence.hpp:84-94), the reference's messages (the C ABI
+// checks the same again).
+inline void validate_plan(const ChunkPlan& plan, index_t T) {
+  if (plan.bounds.empty()) throw ContractViolation("ChunkPlan: no chunks");
+  if (plan.bounds.front().first != 1) throw ContractViolation("ChunkPlan: first chunk must start at step 1");
+  if (plan.bounds.back().second != T) throw ContractViolation("ChunkPlan: last chunk must end at step T");
+  for (size_t i = 0; i < plan.bounds.size(); ++i) {
+    if (plan.bounds[i].first > plan.bounds[i].second) throw ContractViolation("ChunkPlan: chunk start exceeds end");
+    if (i + 1 < plan.bounds.size() && plan.bounds[i].second + 1 != plan.bounds[i + 1].first)
+      throw ContractViolation("ChunkPlan: chunks must be contiguous");
+  }
+}
+
 // ScanSummaries (recurrence.hpp:186-191): caller-owned [chunks, b, n] device
 // views of the chunk summaries P, R and stitched chunk-end states C.
 template <class S>
@@ -205,9 +247,13 @@ inline std::vector<index_t> flat_bounds(const ChunkPlan& plan) {
 template <class S>
 void scan_parallel(const DeviceTensor3<S>& decays, const DeviceTensor3<S>& impulses,
                    const DeviceTensor2<S>& initial, const ChunkPlan& plan, DeviceTensor3<S>& h,
-                   ScanSummaries<S>* summaries = nullptr, void* stream = nullptr) {
+                   ScanSummaries<S>* summaries = nullptr, void* stream = nullptr, bool check_finite = false) {
   validate_recurrence_shapes(decays, impulses, initial);
   check_same_shape(decays, h, "scan_parallel(h)");
+  if (check_finite) {  // after validate_plan, as the reference (recurrence.hpp:198-200)
+    validate_plan(plan, decays.steps);
+    screen_recurrence(decays, impulses, initial, stream);
+  }
   const auto b = detail::flat_bounds(plan);
   throw_status(detail::plan_call(decays.data, impulses.data, initial.data, h.data, decays.steps, decays.step_size(),
                                  b.data(), plan.chunks(), summaries ? summaries->P.data : nullptr,
@@ -219,9 +265,9 @@ void scan_parallel(const DeviceTensor3<S>& decays, const DeviceTensor3<S>& impul
 template <class S>
 void scan(const DeviceTensor3<S>& decays, const DeviceTensor3<S>& impulses,
           const DeviceTensor2<S>& initial, DeviceTensor3<S>& h, ScanMode mode,
-          void* stream = nullptr, linrec_workspace_t ws = nullptr) {
-  if (mode == ScanMode::Serial) return scan_serial(decays, impulses, initial, h, stream);
-  scan_parallel(decays, impulses, initial, h, stream, ws);
+          void* stream = nullptr, linrec_workspace_t ws = nullptr, bool check_finite = false) {
+  if (mode == ScanMode::Serial) return scan_serial(decays, impulses, initial, h, stream, check_finite);
+  scan_parallel(decays, impulses, initial, h, stream, ws, check_finite);
 }
 
 // RecurrenceGradients (recurrence.hpp:265-271) as output views.
@@ -237,10 +283,14 @@ template <class S>
 void scan_backward(const DeviceTensor3<S>& decays, const DeviceTensor2<S>& initial,
                    const DeviceTensor3<S>& h, const DeviceTensor3<S>& d_h,
                    RecurrenceGradients<S>& grads, ScanMode mode, void* stream = nullptr,
-                   linrec_workspace_t ws = nullptr) {
+                   linrec_workspace_t ws = nullptr, bool check_finite = false) {
   check_same_shape(decays, h, "scan_backward(h)");
   check_same_shape(decays, d_h, "scan_backward(d_h)");
   validate_recurrence_shapes(decays, d_h, initial);
+  if (check_finite) {  // recurrence.hpp:292-296
+    screen_finite(decays, "decays", stream);
+    screen_finite(d_h, "d_h", stream);
+  }
   check_same_shape(decays, grads.d_decays, "scan_backward(d_decays)");
   check_same_shape(decays, grads.d_impulses, "scan_backward(d_impulses)");
   throw_status(detail::bwd_call(decays.data, initial.data, h.data, d_h.data, grads.d_decays.data,
@@ -254,10 +304,15 @@ void scan_backward(const DeviceTensor3<S>& decays, const DeviceTensor2<S>& initi
 template <class S>
 void scan_backward(const DeviceTensor3<S>& decays, const DeviceTensor2<S>& initial, const DeviceTensor3<S>& h,
                    const DeviceTensor3<S>& d_h, const ChunkPlan& plan, RecurrenceGradients<S>& grads,
-                   void* stream = nullptr) {
+                   void* stream = nullptr, bool check_finite = false) {
+  validate_plan(plan, decays.steps);  // recurrence.hpp:373
   check_same_shape(decays, h, "scan_backward(h)");
   check_same_shape(decays, d_h, "scan_backward(d_h)");
   validate_recurrence_shapes(decays, d_h, initial);
+  if (check_finite) {
+    screen_finite(decays, "decays", stream);
+    screen_finite(d_h, "d_h", stream);
+  }
   check_same_shape(decays, grads.d_decays, "scan_backward(d_decays)");
   check_same_shape(decays, grads.d_impulses, "scan_backward(d_impulses)");
   const auto b = detail::flat_bounds(plan);

@@ -181,6 +181,23 @@ int linrec_first_nonfinite_f32(const float* v, int64_t n, int64_t* index,
 int linrec_first_nonfinite_f64(const double* v, int64_t n, int64_t* index,
                                void* stream);
 
+/* screen_finite (recurrence.hpp:133-155) of a device tensor
+ * [T][batch][features] (T = 0: a [batch][features] tensor such as h0): OK,
+ * or LINREC_ERR_NONFINITE with the reference's message
+ * "non-finite value in <name> at [t=<1-based step>, b=<batch>, n=<feature>]"
+ * ("[b=.., n=..]" for T = 0) naming the FIRST non-finite element in memory
+ * order.  The check_finite option of scan_serial / scan_parallel / scan /
+ * scan_backward (recurrence.hpp:169-377) is this screen on decays, impulses
+ * and initial (forward) or decays and d_h (backward, :292-296) before the
+ * scan; include/linrec/cuda_scan.hpp exposes it under those names.
+ * Synchronous on `stream`. */
+int linrec_screen_finite_f32(const float* v, int64_t T, int64_t batch,
+                             int64_t features, const char* name,
+                             void* stream);
+int linrec_screen_finite_f64(const double* v, int64_t T, int64_t batch,
+                             int64_t features, const char* name,
+                             void* stream);
+
 /* Kernels one linrec_scan_* (backward = 0) / linrec_scan_backward_* call
  * launches for this shape and mode with 16-byte aligned buffers (1, or 3 when
  * the sequence is split into virtual segments: scan, fold, fix-up); -1 for
@@ -301,6 +318,39 @@ int linrec_segment_fixup_backward_exchange_f32(const float* lam, const float* hp
                                                const float* lam_next, const float* seg_prod, float* y_in,
                                                float* dlam, float* dx, int64_t T, int64_t W, int64_t tile_rows,
                                                const linrec_exchange_t* ex, void* stream);
+
+/* ---- sequence-sharded scan: one call per rank and step ------------------- *
+ * The whole sharded step of SURVEY.md 8e for a C/C++ host (the Python
+ * driver paper_1709_04057_b200/sharded.py runs the same sequence): T rows of
+ * a [T][W] fp32 problem split into `world` contiguous segments
+ * (linrec_sharded_bounds: plan_chunks' rule, recurrence.hpp:61-80, applied
+ * to ranks), rank r owning rows [row0, row0 + rows) on its own GPU.  Each
+ * direction runs the segment scan (which publishes the rank's (A, B)
+ * aggregate into the consumers' mailboxes over NVLink) and the compose +
+ * fix-up (which acquires the sources' aggregates) -- the reference's
+ * phase-2/3 stitch (recurrence.hpp:219-237) across ranks, with no
+ * collective and no host synchronisation.
+ *   mboxes: HOST array [world] of every rank's mailbox mapped in this
+ *   process (own: linrec_ipc_alloc of linrec_p2p_mailbox_bytes(W, world);
+ *   peers: linrec_ipc_open of their handles, exchanged out of band).
+ *   Requirements: T >= world, W % 4 == 0, 16-byte aligned buffers.
+ * Every rank calls every step in the same order (epochs advance per call).
+ * scan: lam, x, h [rows][W] of this rank; h0 [W] read on rank 0 only (NULL =
+ * zeros).  scan_backward: lam, h, dh -> dlam, dx [rows][W]; hprev = h at the
+ * row before the segment (NULL: rank 0 uses h0, the others the carry their
+ * last forward computed); dh0 [W] written on rank 0 only (others may pass
+ * NULL).  Stream-ordered on `stream`; the context is not thread-safe. */
+typedef struct linrec_sharded* linrec_sharded_t;
+void linrec_sharded_bounds(int64_t T, int world, int rank, int64_t* row0, int64_t* rows);
+int linrec_sharded_create(linrec_sharded_t* ctx, int64_t T, int64_t W, int world, int rank, void* const* mboxes,
+                          int device);
+int linrec_sharded_destroy(linrec_sharded_t ctx);
+int linrec_sharded_rows(linrec_sharded_t ctx, int64_t* row0, int64_t* rows);
+int linrec_sharded_scan_f32(linrec_sharded_t ctx, const float* lam, const float* x, const float* h0, float* h,
+                            linrec_workspace_t ws, void* stream);
+int linrec_sharded_scan_backward_f32(linrec_sharded_t ctx, const float* lam, const float* h0, const float* hprev,
+                                     const float* h, const float* dh, float* dlam, float* dx, float* dh0,
+                                     linrec_workspace_t ws, void* stream);
 
 /* ---- layer building block: tcgen05 GEMM ---------------------------------- *
  * C[M][N] (row-major, pitch ldc) (+)= sum_k A(m,k) * B(n,k) on the sm_100a

@@ -30,6 +30,37 @@ ORACLE_SO = os.path.join(HERE, "liblinrec_oracle.so")
 REF_DIR = os.path.join(HERE, "_ref")
 REF_SO = os.path.join(REF_DIR, "liblinrec_ref.so")
 REF_PY = os.path.join(REF_DIR, "linrec" + sysconfig.get_config_var("EXT_SUFFIX"))
+NATIVE_DIR = os.path.join(REF_DIR, "native")
+
+
+def _host_cpu_flags():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    return set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    return set()
+
+
+def native_ref_usable() -> bool:
+    """The -march=native reference build (oracle/Makefile) runs here iff this
+    host's CPU has every flag of the CPU it was compiled on."""
+    try:
+        with open(os.path.join(NATIVE_DIR, "cpu_flags.txt")) as f:
+            need = set(f.read().split())
+    except OSError:
+        return False
+    return bool(need) and need <= _host_cpu_flags()
+
+
+def ref_build():
+    """(directory, -march) of the reference build the timed baselines load:
+    the reference's own -march=native flags where they fit this host."""
+    if native_ref_usable() and os.path.exists(os.path.join(NATIVE_DIR, "liblinrec_ref.so")):
+        return NATIVE_DIR, "native"
+    return REF_DIR, "x86-64-v3"
 
 _i64 = C.c_int64
 _vp = C.c_void_p
@@ -333,6 +364,7 @@ class RefLib:
         lib.ref_rng_first.argtypes = [C.c_uint64, C.c_int]
         lib.ref_hardware_workers.restype = C.c_int
         lib.ref_bench_fwd_bwd_f32.argtypes = [_vp] * 4 + [_i64] * 3 + [C.c_int] * 3 + [_vp, _vp]
+        lib.ref_bench_serial_f32.argtypes = [_vp] * 4 + [_i64] * 3 + [C.c_int] * 2 + [_vp, _vp]
         lib.ref_gilr_lstm_oracle.argtypes = [_vp] * 11 + [_i64] * 4
         lib.ref_gilr_oracle.argtypes = [_vp] * 7 + [_i64] * 4
         lib.ref_qrnn_oracle.argtypes = [_vp] * 5 + [_i64] * 5
@@ -390,6 +422,17 @@ class RefLib:
             C.byref(f), C.byref(bw)))
         return f.value, bw.value
 
+    def bench_serial(self, lam, x, h0, dh, warmup=0, reps=1):
+        """Median seconds of (scan_serial, scan_backward(Serial)): the
+        reference's 1-core path, same protocol."""
+        lam, x, h0, dh = (np.ascontiguousarray(a, dtype=np.float32) for a in (lam, x, h0, dh))
+        T, b, n = lam.shape
+        f = C.c_double(0.0)
+        bw = C.c_double(0.0)
+        self._check(self.lib.ref_bench_serial_f32(
+            _ptr(lam), _ptr(x), _ptr(h0), _ptr(dh), T, b, n, warmup, reps, C.byref(f), C.byref(bw)))
+        return f.value, bw.value
+
     def gilr_lstm_oracle(self, P, x, htil0, c0):
         """The reference's per-step GILR-LSTM (layer_oracles.hpp:52-82), fp64."""
         x = np.ascontiguousarray(x, dtype=np.float64)
@@ -419,14 +462,16 @@ class RefLib:
         return int(self.lib.ref_hardware_workers())
 
 
-def load_reference_module():
+def load_reference_module(ref_dir: str = REF_DIR):
     """The reference's own pybind11 module ``linrec`` (bindings/linrec_py.cpp)
-    built into oracle/_ref.  Loaded without touching sys.modules so it never
-    shadows the product module of the same name."""
-    if not os.path.exists(REF_PY):
-        raise FileNotFoundError(f"{REF_PY} missing: run `make -C oracle ref`")
-    loader = importlib.machinery.ExtensionFileLoader("linrec", REF_PY)
-    spec = importlib.util.spec_from_file_location("linrec", REF_PY, loader=loader)
+    built into oracle/_ref (or ref_build()'s directory).  Loaded without
+    touching sys.modules so it never shadows the product module of the same
+    name."""
+    path = os.path.join(ref_dir, os.path.basename(REF_PY))
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} missing: run `make -C oracle ref`")
+    loader = importlib.machinery.ExtensionFileLoader("linrec", path)
+    spec = importlib.util.spec_from_file_location("linrec", path, loader=loader)
     mod = importlib.util.module_from_spec(spec)
     loader.exec_module(mod)
     return mod

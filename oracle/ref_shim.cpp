@@ -175,6 +175,48 @@ int ref_bench_fwd_bwd_f32(const float* lam, const float* x, const float* h0,
   }
 }
 
+// The same protocol for the 1-core serial path: scan_serial
+// (recurrence.hpp:169-184) and scan_backward(ScanMode::Serial) -- the
+// reference's single-thread baseline (SURVEY.md 8d "CPU baseline" row).
+int ref_bench_serial_f32(const float* lam, const float* x, const float* h0,
+                         const float* dh, int64_t T, int64_t b, int64_t n,
+                         int warmup, int reps, double* fwd_s, double* bwd_s) {
+  try {
+    auto L = t3(lam, T, b, n);
+    auto X = t3(x, T, b, n);
+    auto DH = t3(dh, T, b, n);
+    auto H0 = t2(h0, b, n);
+    linrec::ThreadPool pool(1);
+    linrec::Tensor3<float> h;
+    linrec::RecurrenceGradients<float> g;
+    auto median = [](std::vector<double> v) {
+      std::sort(v.begin(), v.end());
+      const size_t m = v.size() / 2;
+      return v.size() % 2 ? v[m] : 0.5 * (v[m - 1] + v[m]);
+    };
+    for (int i = 0; i < warmup; ++i) {
+      h = linrec::scan_serial(L, X, H0);
+      g = linrec::scan_backward(L, H0, h, DH, linrec::ScanMode::Serial, pool);
+    }
+    std::vector<double> tf, tb;
+    for (int i = 0; i < reps; ++i) {
+      const auto t0 = std::chrono::steady_clock::now();
+      h = linrec::scan_serial(L, X, H0);
+      const auto t1 = std::chrono::steady_clock::now();
+      g = linrec::scan_backward(L, H0, h, DH, linrec::ScanMode::Serial, pool);
+      const auto t2 = std::chrono::steady_clock::now();
+      tf.push_back(std::chrono::duration<double>(t1 - t0).count());
+      tb.push_back(std::chrono::duration<double>(t2 - t1).count());
+    }
+    *fwd_s = median(tf);
+    *bwd_s = median(tb);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
 // The reference's per-step GILR / GILR-LSTM oracles
 // (proj/tests/support/layer_oracles.hpp:28-82, fp64).  Parameters row-major
 // as GilrParams / GilrLstmParams (layers.hpp:28-40, :148-165).

@@ -66,6 +66,7 @@ def _load():
         getattr(lib, f"linrec_scan_host_{s}").argtypes = [_vp] * 4 + [_i64, _i64, _int, _int]
         getattr(lib, f"linrec_scan_backward_host_{s}").argtypes = [_vp] * 7 + [_i64, _i64, _int, _int]
         getattr(lib, f"linrec_first_nonfinite_{s}").argtypes = [_vp, _i64, C.POINTER(_i64), _vp]
+        getattr(lib, f"linrec_screen_finite_{s}").argtypes = [_vp, _i64, _i64, _i64, C.c_char_p, _vp]
         getattr(lib, f"linrec_segment_scan_{s}").argtypes = [_vp] * 6 + [_i64, _i64, _vp, _vp]
         getattr(lib, f"linrec_segment_scan_backward_{s}").argtypes = [_vp] * 10 + [_i64, _i64, _vp, _vp]
         getattr(lib, f"linrec_compose_carries_{s}").argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp]
@@ -160,6 +161,13 @@ def first_nonfinite(v, n, dtype_bytes=4, stream=0) -> int:
     out = _i64(-1)
     check(getattr(lib, f"linrec_first_nonfinite_{_sfx(dtype_bytes)}")(v, n, C.byref(out), stream))
     return int(out.value)
+
+
+def screen_finite(v, T, batch, features, name, dtype_bytes=4, stream=0):
+    """screen_finite (recurrence.hpp:133-155): raises LinrecError (code
+    ERR_NONFINITE) with the reference's message; T = 0 for a [batch, features]
+    tensor."""
+    check(getattr(lib, f"linrec_screen_finite_{_sfx(dtype_bytes)}")(v, T, batch, features, name.encode(), stream))
 
 
 # ---- sequence sharding (see include/linrec_cuda.h) ---------------------------

@@ -9,6 +9,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -16,6 +19,7 @@
 #include <mutex>
 #include <sstream>
 #include <string>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -287,6 +291,84 @@ int scan_backward_device(const S* lam, const S* h0, const S* h, const S* dh, con
 constexpr int kSlots = 3;
 constexpr size_t kChunkBytes = size_t(64) << 20;  // per array per chunk
 
+// Parallel host memcpy for staging pageable numpy buffers through pinned
+// bounce buffers: one pageable<->pinned copy per byte, split over worker
+// threads (the calling thread takes a share), so the copies and the page
+// faults of freshly allocated outputs run at host-memory rather than
+// single-core speed while the DMA engines move the previous chunk.
+class CopyPool {
+ public:
+  explicit CopyPool(int n) {
+    for (int i = 0; i < n; ++i) th_.emplace_back([this, i] { loop(i + 1); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return int(th_.size()) + 1; }
+  // dst[k] <- src[k] for every (dst, src, bytes) job, split across the pool.
+  void copy(const std::vector<std::tuple<void*, const void*, size_t>>& jobs) {
+    size_t total = 0;
+    for (auto& j : jobs) total += std::get<2>(j);
+    if (total == 0) return;
+    const int parts = std::max(1, std::min<int>(size(), int(total >> 20)));  // >= 1 MiB each
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      jobs_ = &jobs;
+      total_ = total;
+      parts_ = parts;
+      pending_ = parts - 1;  // part 0 runs on the caller
+      ++gen_;
+    }
+    cv_.notify_all();
+    run_part(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [this] { return pending_ == 0; });
+    jobs_ = nullptr;
+  }
+
+ private:
+  void run_part(int k) {
+    const size_t lo = total_ * size_t(k) / size_t(parts_), hi = total_ * size_t(k + 1) / size_t(parts_);
+    size_t off = 0;
+    for (auto& j : *jobs_) {
+      const size_t n = std::get<2>(j);
+      const size_t a = std::max(lo, off), b = std::min(hi, off + n);
+      if (a < b)
+        std::memcpy(static_cast<char*>(std::get<0>(j)) + (a - off), static_cast<const char*>(std::get<1>(j)) + (a - off),
+                    b - a);
+      off += n;
+    }
+  }
+  void loop(int k) {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        if (k >= parts_) continue;
+      }
+      run_part(k);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::vector<std::tuple<void*, const void*, size_t>>* jobs_ = nullptr;
+  size_t total_ = 0;
+  int parts_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
 struct HostPipe {
   int device = -1;
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_out = nullptr;
@@ -295,6 +377,11 @@ struct HostPipe {
   size_t buf_bytes = 0;
   void* small = nullptr;  // h0 / dh0 staging, 2 rows
   size_t small_bytes = 0;
+  // pageable staging: pinned bounce buffers per slot (3 inputs, 2 outputs)
+  void* bounce[kSlots][5] = {};
+  size_t bounce_bytes = 0;
+  void* small_host = nullptr;  // pinned h0 / dh0 bounce
+  std::unique_ptr<CopyPool> pool;
   linrec_workspace ws;
   std::mutex mu;
 };
@@ -356,10 +443,48 @@ int pipe_reserve(HostPipe* hp, size_t bytes, size_t small_bytes) {
   return LINREC_OK;
 }
 
+// Pinned bounce buffers + copy threads for pageable host arrays.
+int pipe_reserve_bounce(HostPipe* hp, size_t bytes, size_t small_bytes) {
+  if (!hp->pool) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    hp->pool.reset(new CopyPool(int(std::max(1u, std::min(hw ? hw : 1u, 16u))) - 1));
+  }
+  if (bytes > hp->bounce_bytes) {
+    for (int i = 0; i < kSlots; ++i)
+      for (int j = 0; j < 5; ++j) {
+        if (hp->bounce[i][j]) LINREC_CUDA_TRY(cudaFreeHost(hp->bounce[i][j]));
+        hp->bounce[i][j] = nullptr;
+      }
+    hp->bounce_bytes = 0;
+    for (int i = 0; i < kSlots; ++i)
+      for (int j = 0; j < 5; ++j) LINREC_CUDA_TRY(cudaHostAlloc(&hp->bounce[i][j], bytes, cudaHostAllocDefault));
+    hp->bounce_bytes = bytes;
+  }
+  if (!hp->small_host) LINREC_CUDA_TRY(cudaHostAlloc(&hp->small_host, std::max<size_t>(small_bytes, 1 << 20), 0));
+  return LINREC_OK;
+}
+
+// true when every non-null host pointer is page-locked (or device-mapped):
+// those DMA straight from the caller's memory; anything else is staged.
+bool all_pinned(std::initializer_list<const void*> ptrs) {
+  for (const void* p : ptrs) {
+    if (!p) continue;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (a.type == cudaMemoryTypeUnregistered) return false;
+  }
+  return true;
+}
+
 int64_t chunk_rows(int64_t T, int64_t W, size_t elem) {
   const int64_t rows = (int64_t)(kChunkBytes / (size_t(W) * elem));
   return std::max<int64_t>(1, std::min<int64_t>(T, rows));
 }
+
+using CopyJobs = std::vector<std::tuple<void*, const void*, size_t>>;
 
 template <class S>
 int scan_host(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W, int mode,
@@ -375,12 +500,27 @@ int scan_host(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W,
   const int64_t Tc = chunk_rows(T, W, sizeof(S));
   const size_t row = size_t(W) * sizeof(S);
   if ((rc = pipe_reserve(hp, size_t(Tc) * row, 2 * row))) return rc;
+  // pageable arrays (numpy) go through pinned bounce buffers; pinned ones DMA directly
+  const bool staged = !all_pinned({lam, x, h0, h});
+  if (staged && (rc = pipe_reserve_bounce(hp, size_t(Tc) * row, 2 * row))) return rc;
   S* d_h0 = nullptr;
   if (h0) {
     d_h0 = static_cast<S*>(hp->small);
-    LINREC_CUDA_TRY(cudaMemcpyAsync(d_h0, h0, row, cudaMemcpyHostToDevice, hp->s_comp));
+    const S* src = h0;
+    if (staged) {
+      std::memcpy(hp->small_host, h0, row);
+      src = static_cast<const S*>(hp->small_host);
+    }
+    LINREC_CUDA_TRY(cudaMemcpyAsync(d_h0, src, row, cudaMemcpyHostToDevice, hp->s_comp));
   }
   const int64_t nchunks = (T + Tc - 1) / Tc;
+  auto drain = [&](int64_t k) -> int {  // chunk k's h: pinned bounce -> caller
+    const int s = int(k % kSlots);
+    const int64_t t0 = k * Tc, rows = std::min<int64_t>(Tc, T - t0);
+    LINREC_CUDA_TRY(cudaEventSynchronize(hp->ev_out[s]));
+    hp->pool->copy(CopyJobs{{h + t0 * W, hp->bounce[s][3], size_t(rows) * row}});
+    return LINREC_OK;
+  };
   const S* seed = d_h0;
   for (int64_t k = 0; k < nchunks; ++k) {
     const int s = int(k % kSlots);
@@ -389,19 +529,31 @@ int scan_host(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W,
     S* dxv = static_cast<S*>(hp->buf[s][1]);
     S* dhv = static_cast<S*>(hp->buf[s][2]);
     const size_t bytes = size_t(rows) * row;
+    const S* src_l = lam + t0 * W;
+    const S* src_x = x + t0 * W;
+    if (staged) {  // bounce slot s is free once chunk k - kSlots's H2D finished
+      if (k >= kSlots) LINREC_CUDA_TRY(cudaEventSynchronize(hp->ev_in[s]));
+      hp->pool->copy(CopyJobs{{hp->bounce[s][0], src_l, bytes}, {hp->bounce[s][1], src_x, bytes}});
+      src_l = static_cast<const S*>(hp->bounce[s][0]);
+      src_x = static_cast<const S*>(hp->bounce[s][1]);
+    }
     if (k >= kSlots) LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_in, hp->ev_comp[s], 0));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(dl, lam + t0 * W, bytes, cudaMemcpyHostToDevice, hp->s_in));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(dxv, x + t0 * W, bytes, cudaMemcpyHostToDevice, hp->s_in));
+    LINREC_CUDA_TRY(cudaMemcpyAsync(dl, src_l, bytes, cudaMemcpyHostToDevice, hp->s_in));
+    LINREC_CUDA_TRY(cudaMemcpyAsync(dxv, src_x, bytes, cudaMemcpyHostToDevice, hp->s_in));
     LINREC_CUDA_TRY(cudaEventRecord(hp->ev_in[s], hp->s_in));
     LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_comp, hp->ev_in[s], 0));
     if (k >= kSlots) LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_comp, hp->ev_out[s], 0));
     if ((rc = scan_device<S>(dl, dxv, seed, dhv, rows, W, mode, &hp->ws, hp->s_comp))) return rc;
     LINREC_CUDA_TRY(cudaEventRecord(hp->ev_comp[s], hp->s_comp));
     LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_out, hp->ev_comp[s], 0));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(h + t0 * W, dhv, bytes, cudaMemcpyDeviceToHost, hp->s_out));
+    LINREC_CUDA_TRY(cudaMemcpyAsync(staged ? hp->bounce[s][3] : static_cast<void*>(h + t0 * W), dhv, bytes,
+                                    cudaMemcpyDeviceToHost, hp->s_out));
     LINREC_CUDA_TRY(cudaEventRecord(hp->ev_out[s], hp->s_out));
     seed = dhv + (rows - 1) * W;  // carry into the next chunk
+    // the previous chunk's result leaves the bounce buffer while this one runs
+    if (staged && k >= 1 && (rc = drain(k - 1))) return rc;
   }
+  if (staged && (rc = drain(nchunks - 1))) return rc;
   LINREC_CUDA_TRY(cudaStreamSynchronize(hp->s_out));
   LINREC_CUDA_TRY(cudaStreamSynchronize(hp->s_comp));
   return LINREC_OK;
@@ -424,11 +576,31 @@ int scan_backward_host(const S* lam, const S* h0, const S* h, const S* dh, S* dl
   // per slot: buf0 = [lam | dlam], buf1 = [h shifted by one row | dx],
   // buf2 = [dh]; each half holds Tc rows.
   if ((rc = pipe_reserve(hp, size_t(2) * size_t(Tc) * row, 3 * row))) return rc;
+  const bool staged = !all_pinned({lam, h0, h, dh, dlam, dx, dh0});
+  if (staged && (rc = pipe_reserve_bounce(hp, size_t(Tc) * row, 3 * row))) return rc;
   S* d_h0 = static_cast<S*>(hp->small);
   S* d_dh0 = d_h0 + W;
-  if (h0) LINREC_CUDA_TRY(cudaMemcpyAsync(d_h0, h0, row, cudaMemcpyHostToDevice, hp->s_comp));
-  else LINREC_CUDA_TRY(cudaMemsetAsync(d_h0, 0, row, hp->s_comp));
+  S* h_dh0 = staged ? static_cast<S*>(hp->small_host) + W : dh0;  // where dh0 lands on the host
+  if (h0) {
+    const S* src = h0;
+    if (staged) {
+      std::memcpy(hp->small_host, h0, row);
+      src = static_cast<const S*>(hp->small_host);
+    }
+    LINREC_CUDA_TRY(cudaMemcpyAsync(d_h0, src, row, cudaMemcpyHostToDevice, hp->s_comp));
+  } else {
+    LINREC_CUDA_TRY(cudaMemsetAsync(d_h0, 0, row, hp->s_comp));
+  }
   const int64_t nchunks = (T + Tc - 1) / Tc;
+  auto drain = [&](int64_t i) -> int {  // chunk i's dlam, dx: pinned bounce -> caller
+    const int s = int(i % kSlots);
+    const int64_t k = nchunks - 1 - i;
+    const int64_t t0 = k * Tc, rows = std::min<int64_t>(Tc, T - t0);
+    const size_t bytes = size_t(rows) * row;
+    LINREC_CUDA_TRY(cudaEventSynchronize(hp->ev_out[s]));
+    hp->pool->copy(CopyJobs{{dlam + t0 * W, hp->bounce[s][3], bytes}, {dx + t0 * W, hp->bounce[s][4], bytes}});
+    return LINREC_OK;
+  };
   const S* lam_next = nullptr;
   const S* g_next = nullptr;
   for (int64_t i = 0; i < nchunks; ++i) {
@@ -444,21 +616,33 @@ int scan_backward_host(const S* lam, const S* h0, const S* h, const S* dh, S* dl
     S* d_h = b1;  // rows t0-1 .. t0+rows-2 (or 0 .. rows-2 for t0 == 0)
     S* d_dx = b1 + Tc * W;
     S* d_dh = b2;
+    // host sources of this chunk: lam and dh rows, and h shifted by one row
+    const S* src_l = lam + t0 * W;
+    const S* src_dh = dh + t0 * W;
+    const S* src_h = t0 > 0 ? h + (t0 - 1) * W : h;
+    const size_t h_bytes = t0 > 0 ? bytes : bytes - row;
+    if (staged) {
+      if (i >= kSlots) LINREC_CUDA_TRY(cudaEventSynchronize(hp->ev_in[s]));
+      hp->pool->copy(CopyJobs{{hp->bounce[s][0], src_l, bytes}, {hp->bounce[s][1], src_h, h_bytes},
+                              {hp->bounce[s][2], src_dh, bytes}});
+      src_l = static_cast<const S*>(hp->bounce[s][0]);
+      src_h = static_cast<const S*>(hp->bounce[s][1]);
+      src_dh = static_cast<const S*>(hp->bounce[s][2]);
+    }
     // slot s was last filled at chunk i-3, whose lam row 0 and G row 0 are
     // also read by chunk i-2 (lam_next / g_next): wait for that compute.
     if (i >= kSlots)
       LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_in, hp->ev_comp[(i - 2) % kSlots], 0));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(d_lam, lam + t0 * W, bytes, cudaMemcpyHostToDevice, hp->s_in));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(d_dh, dh + t0 * W, bytes, cudaMemcpyHostToDevice, hp->s_in));
+    LINREC_CUDA_TRY(cudaMemcpyAsync(d_lam, src_l, bytes, cudaMemcpyHostToDevice, hp->s_in));
+    LINREC_CUDA_TRY(cudaMemcpyAsync(d_dh, src_dh, bytes, cudaMemcpyHostToDevice, hp->s_in));
     const S* hprev_row;
     const S* hrows;
     if (t0 > 0) {
-      LINREC_CUDA_TRY(cudaMemcpyAsync(d_h, h + (t0 - 1) * W, bytes, cudaMemcpyHostToDevice, hp->s_in));
+      LINREC_CUDA_TRY(cudaMemcpyAsync(d_h, src_h, h_bytes, cudaMemcpyHostToDevice, hp->s_in));
       hprev_row = d_h;
       hrows = d_h + W;
     } else {
-      if (rows > 1)
-        LINREC_CUDA_TRY(cudaMemcpyAsync(d_h, h, bytes - row, cudaMemcpyHostToDevice, hp->s_in));
+      if (rows > 1) LINREC_CUDA_TRY(cudaMemcpyAsync(d_h, src_h, h_bytes, cudaMemcpyHostToDevice, hp->s_in));
       hprev_row = d_h0;
       hrows = d_h;
     }
@@ -470,15 +654,20 @@ int scan_backward_host(const S* lam, const S* h0, const S* h, const S* dh, S* dl
       return rc;
     LINREC_CUDA_TRY(cudaEventRecord(hp->ev_comp[s], hp->s_comp));
     LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_out, hp->ev_comp[s], 0));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(dlam + t0 * W, d_dlam, bytes, cudaMemcpyDeviceToHost, hp->s_out));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(dx + t0 * W, d_dx, bytes, cudaMemcpyDeviceToHost, hp->s_out));
-    if (k == 0) LINREC_CUDA_TRY(cudaMemcpyAsync(dh0, d_dh0, row, cudaMemcpyDeviceToHost, hp->s_out));
+    LINREC_CUDA_TRY(cudaMemcpyAsync(staged ? hp->bounce[s][3] : static_cast<void*>(dlam + t0 * W), d_dlam, bytes,
+                                    cudaMemcpyDeviceToHost, hp->s_out));
+    LINREC_CUDA_TRY(cudaMemcpyAsync(staged ? hp->bounce[s][4] : static_cast<void*>(dx + t0 * W), d_dx, bytes,
+                                    cudaMemcpyDeviceToHost, hp->s_out));
+    if (k == 0) LINREC_CUDA_TRY(cudaMemcpyAsync(h_dh0, d_dh0, row, cudaMemcpyDeviceToHost, hp->s_out));
     LINREC_CUDA_TRY(cudaEventRecord(hp->ev_out[s], hp->s_out));
     lam_next = d_lam;  // lam at row t0 and G at row t0 feed the previous chunk
     g_next = d_dx;
+    if (staged && i >= 1 && (rc = drain(i - 1))) return rc;
   }
+  if (staged && (rc = drain(nchunks - 1))) return rc;
   LINREC_CUDA_TRY(cudaStreamSynchronize(hp->s_out));
   LINREC_CUDA_TRY(cudaStreamSynchronize(hp->s_comp));
+  if (staged) std::memcpy(dh0, h_dh0, row);
   return LINREC_OK;
 }
 
@@ -677,6 +866,25 @@ int first_nonfinite(const S* v, int64_t n, int64_t* index, cudaStream_t st) {
   LINREC_CUDA_TRY(linrec_impl::first_nonfinite<S>(v, n, index, st));
   return LINREC_OK;
 }
+// screen_finite (recurrence.hpp:133-155): the first non-finite element of a
+// [T][batch][features] tensor (T == 0: a [batch][features] one), reported
+// with the reference's message -- steps 1-based, batch / feature 0-based.
+template <class S>
+int screen_finite(const S* v, int64_t T, int64_t batch, int64_t features, const char* name, cudaStream_t st) {
+  int rc;
+  if (batch < 1 || features < 1 || T < 0) return fail(LINREC_ERR_SHAPE, "Tensor3 dimensions must be >= 1");
+  if ((rc = check_ptr(v, "v"))) return rc;
+  const int64_t W = batch * features;
+  int64_t bad = -1;
+  LINREC_CUDA_TRY(linrec_impl::first_nonfinite<S>(v, (T > 0 ? T : 1) * W, &bad, st));
+  if (bad < 0) return LINREC_OK;
+  std::ostringstream os;
+  os << "non-finite value in " << (name ? name : "tensor") << " at [";
+  if (T > 0) os << "t=" << bad / W + 1 << ", ";
+  const int64_t rest = bad % W;
+  os << "b=" << rest / features << ", n=" << rest % features << "]";
+  return fail(LINREC_ERR_NONFINITE, os.str());
+}
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -816,6 +1024,15 @@ int linrec_first_nonfinite_f32(const float* v, int64_t n, int64_t* index, void* 
 }
 int linrec_first_nonfinite_f64(const double* v, int64_t n, int64_t* index, void* stream) {
   return first_nonfinite<double>(v, n, index, static_cast<cudaStream_t>(stream));
+}
+
+int linrec_screen_finite_f32(const float* v, int64_t T, int64_t batch, int64_t features, const char* name,
+                             void* stream) {
+  return screen_finite<float>(v, T, batch, features, name, static_cast<cudaStream_t>(stream));
+}
+int linrec_screen_finite_f64(const double* v, int64_t T, int64_t batch, int64_t features, const char* name,
+                             void* stream) {
+  return screen_finite<double>(v, T, batch, features, name, static_cast<cudaStream_t>(stream));
 }
 
 int64_t linrec_segment_prod_rows(int64_t T, int64_t W, int dtype_bytes, int backward) {

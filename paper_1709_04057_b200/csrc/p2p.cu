@@ -100,6 +100,10 @@ int linrec_ipc_alloc(size_t bytes, void** ptr, unsigned char* handle64) {
   if (!ptr || !handle64 || bytes == 0) return perr(LINREC_ERR_VALUE, "ipc_alloc: bytes, ptr and handle required");
   PTRY(cudaMalloc(ptr, bytes));
   PTRY(cudaMemset(*ptr, 0, bytes));
+  // cudaMemset is asynchronous for device memory: finish it before a peer
+  // can open the handle and publish into the mailbox (its epoch-1 flag
+  // would otherwise be wiped by the pending zero-fill).
+  PTRY(cudaDeviceSynchronize());
   cudaIpcMemHandle_t h;
   PTRY(cudaIpcGetMemHandle(&h, *ptr));
   static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");

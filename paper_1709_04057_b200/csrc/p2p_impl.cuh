@@ -70,12 +70,17 @@ __device__ __forceinline__ void wait_geq(const unsigned long long* p, unsigned l
 using linrec_impl::Exchange;
 __device__ __forceinline__ MboxLayout layout(const Exchange& ex) { return MboxLayout{ex.W, ex.world}; }
 
-// The CTA that completes a grid-wide count (across epochs: counts grow by
-// gridDim.x per launch) -- called by thread 0 after the CTA's part is done.
+// The CTA that completes this launch's grid-wide count -- called by thread 0
+// after the CTA's part is done.  The last CTA resets the counter, so every
+// launch counts from 0 whatever its grid size (T or W may change between
+// steps on the same mailboxes); the next launch that uses the counter is
+// stream-ordered after this one, so the reset cannot race with it.
 __device__ __forceinline__ bool last_cta(unsigned long long* counter) {
   __threadfence_system();
   const unsigned long long old = atomicAdd(counter, 1ull);
-  return (old + 1) % gridDim.x == 0;
+  if (old + 1 != gridDim.x) return false;
+  atomicExch(counter, 0ull);
+  return true;
 }
 
 // Publish channels [j0, j0 + n) of agg [2][W] to every consumer; the whole

@@ -113,6 +113,18 @@ def _check_f32(t, name):
         raise ValueError(f"{name} must be C-contiguous")
 
 
+def _check_shape(t, name, shape):
+    """The C ABI sees raw pointers only: an initial state, adjoint or cache
+    of the wrong shape would be an out-of-bounds device access, so reject it
+    with the reference's contract error (layers.hpp check_same_shape /
+    tensor.hpp:168-189)."""
+    if t is None:
+        return
+    _check_f32(t, name)
+    if list(t.shape) != list(shape):
+        raise RuntimeError(f"{name}: shape mismatch, {list(shape)} vs {list(t.shape)}")
+
+
 _scratch = {}
 
 
@@ -239,6 +251,15 @@ class GilrLstmCache:
         self.c = torch.empty(T, b, n, **kw)
         return self
 
+    def check(self, T, b, n):
+        """Shapes a backward pass reads through raw pointers."""
+        for t, nm, shp in ((self.sg, "cache.sg", (T, b, n)), (self.si, "cache.si", (T, b, n)),
+                           (self.htil, "cache.htil", (T + 1, b, n)), (self.gates, "cache.gates", (4, T, b, n)),
+                           (self.c, "cache.c", (T, b, n))):
+            if t is None:
+                raise RuntimeError(f"{nm}: cache not filled by a forward pass")
+            _check_shape(t, nm, shp)
+
     def surrogate_h(self):
         return self.htil[1:]
 
@@ -297,8 +318,7 @@ def _gilr_forward_core(p: GilrParams, x, h0=None, mode="parallel", precision="fp
         raise RuntimeError("gilr_forward: input feature mismatch")
     for t, nm in zip(p.tensors(), ("U", "V", "b_g", "b_z")):
         _check_f32(t, nm)
-    if h0 is not None:
-        _check_f32(h0, "h0")
+    _check_shape(h0, "h0", (b, n))
     dev = x.device
     h = torch.empty(T, b, n, dtype=torch.float32, device=dev)
     g = torch.empty_like(h)
@@ -319,7 +339,10 @@ def _gilr_backward_core(p: GilrParams, x, h0, cache: GilrCache, d_h, grads: Gilr
     """gilr_backward (layers.hpp:102-133): accumulates into ``grads``; returns (dx, dh0)."""
     lib = _bind()
     T, b, m, n = _dims(x, p.hidden())
-    _check_f32(d_h, "d_h")
+    _check_shape(d_h, "d_h", (T, b, n))
+    _check_shape(h0, "h0", (b, n))
+    for t, nm in ((cache.g, "cache.g"), (cache.i, "cache.i"), (cache.h, "cache.h")):
+        _check_shape(t, nm, (T, b, n))
     dev = x.device
     dx = torch.empty(T, b, m, dtype=torch.float32, device=dev)
     dh0 = torch.empty(b, n, dtype=torch.float32, device=dev) if want_dh0 else None
@@ -343,8 +366,7 @@ def _gilr_lstm_forward_core(p: GilrLstmParams, x, htil0=None, c0=None, mode="par
     for t in p.tensors():
         _check_f32(t, "parameter")
     for t, nm in ((htil0, "htil0"), (c0, "c0")):
-        if t is not None:
-            _check_f32(t, nm)
+        _check_shape(t, nm, (b, n))
     dev = x.device
     if cache is None:
         cache = GilrLstmCache()
@@ -365,7 +387,10 @@ def _gilr_lstm_backward_core(p: GilrLstmParams, x, htil0, c0, cache: GilrLstmCac
     returns (dx, d_htil0, d_c0)."""
     lib = _bind()
     T, b, m, n = _dims(x, p.hidden())
-    _check_f32(d_h, "d_h")
+    _check_shape(d_h, "d_h", (T, b, n))
+    for t, nm in ((htil0, "htil0"), (c0, "c0")):
+        _check_shape(t, nm, (b, n))
+    cache.check(T, b, n)
     dev = x.device
     dx = torch.empty(T, b, m, dtype=torch.float32, device=dev)
     dht0 = torch.empty(b, n, dtype=torch.float32, device=dev) if want_initial else None
@@ -447,8 +472,7 @@ def _qrnn_forward_core(p: QrnnParams, x, c0=None, mode="parallel", precision="fp
         raise RuntimeError("qrnn_forward: filter window exceeds sequence length")
     for t, nm in ((p.W, "W"), (p.bias, "bias")):
         _check_f32(t, nm)
-    if c0 is not None:
-        _check_f32(c0, "c0")
+    _check_shape(c0, "c0", (b, n))
     dev = x.device
     if cache is None:
         cache = QrnnCache()
@@ -470,7 +494,10 @@ def _qrnn_backward_core(p: QrnnParams, x, c0, cache: QrnnCache, d_h, grads: Qrnn
     lib = _bind()
     T, b, m, n = _dims(x, p.hidden())
     k = p.window()
-    _check_f32(d_h, "d_h")
+    _check_shape(d_h, "d_h", (T, b, n))
+    _check_shape(c0, "c0", (b, n))
+    _check_shape(cache.gates, "cache.gates", (3, T, b, n))
+    _check_shape(cache.c, "cache.c", (T, b, n))
     dev = x.device
     dx = torch.empty(T, b, m, dtype=torch.float32, device=dev)
     dc0 = torch.empty(b, n, dtype=torch.float32, device=dev) if want_dc0 else None

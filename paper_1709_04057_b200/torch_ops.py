@@ -30,6 +30,17 @@ def _dims(lam):
     return T, W
 
 
+def _check_like(t, name, shape):
+    """Exact-shape check for h0 / out buffers: the C ABI only sees pointers
+    and reads or writes T*W (or W) elements, so a mis-sized tensor must be
+    rejected here with the reference's contract message
+    (recurrence.hpp:39-51 validate_recurrence_shapes)."""
+    if list(t.shape) != list(shape):
+        if name == "initial":
+            raise RuntimeError(f"recurrence: initial state {list(t.shape)} does not match {list(shape)}")
+        raise RuntimeError(f"{name}: shape mismatch, {list(shape)} vs {list(t.shape)}")
+
+
 def _ptr(t):
     return None if t is None else t.data_ptr()
 
@@ -38,35 +49,68 @@ def _stream():
     return torch.cuda.current_stream().cuda_stream
 
 
-def scan(lam, x, h0=None, mode="parallel", out=None, ws=None):
+def _screen(t, name):
+    """check_finite (recurrence.hpp:133-163): RuntimeError naming the first
+    non-finite element, "non-finite value in <name> at [t=.., b=.., n=..]"."""
+    if t is None:
+        return
+    if t.dim() == 3:
+        T, b, n = t.shape
+    else:
+        T, (b, n) = 0, t.shape
+    try:
+        capi.screen_finite(t.data_ptr(), T, b, n, name, t.element_size(), _stream())
+    except capi.LinrecError as e:
+        raise RuntimeError(str(e)) from None
+
+
+def scan(lam, x, h0=None, mode="parallel", out=None, ws=None, check_finite=False):
     _check(lam, "decays")
     _check(x, "impulses", lam.dtype)
     if lam.shape != x.shape:
         raise RuntimeError(f"recurrence: shape mismatch, {list(lam.shape)} vs {list(x.shape)}")
+    T, W = _dims(lam)
     if h0 is not None:
         _check(h0, "initial", lam.dtype)
-    T, W = _dims(lam)
-    h = torch.empty_like(lam) if out is None else out
+        _check_like(h0, "initial", lam.shape[1:])
+    if out is None:
+        h = torch.empty_like(lam)
+    else:
+        h = out
+        _check(h, "out", lam.dtype)
+        _check_like(h, "out", lam.shape)
+    if check_finite:  # screen_recurrence (recurrence.hpp:157-163)
+        _screen(lam, "decays")
+        _screen(x, "impulses")
+        _screen(h0, "initial")
     capi.scan(lam.data_ptr(), x.data_ptr(), _ptr(h0), h.data_ptr(), T, W,
               capi.SERIAL if mode == "serial" else capi.PARALLEL, lam.element_size(),
               None if ws is None else ws.handle, _stream())
     return h
 
 
-def scan_backward(lam, h0, h, dh, mode="parallel", out=None, ws=None):
+def scan_backward(lam, h0, h, dh, mode="parallel", out=None, ws=None, check_finite=False):
     _check(lam, "decays")
     for t, n in ((h, "h"), (dh, "d_h")):
         _check(t, n, lam.dtype)
         if t.shape != lam.shape:
             raise RuntimeError(f"scan_backward({n}): shape mismatch, {list(lam.shape)} vs {list(t.shape)}")
+    T, W = _dims(lam)
     if h0 is not None:
         _check(h0, "initial", lam.dtype)
-    T, W = _dims(lam)
+        _check_like(h0, "initial", lam.shape[1:])
     if out is None:
         dlam, dx = torch.empty_like(lam), torch.empty_like(lam)
         dh0 = torch.empty(lam.shape[1:], dtype=lam.dtype, device=lam.device)
     else:
         dlam, dx, dh0 = out
+        for t, n, shp in ((dlam, "d_decays", lam.shape), (dx, "d_impulses", lam.shape),
+                          (dh0, "d_initial", lam.shape[1:])):
+            _check(t, n, lam.dtype)
+            _check_like(t, n, shp)
+    if check_finite:  # recurrence.hpp:292-296
+        _screen(lam, "decays")
+        _screen(dh, "d_h")
     capi.scan_backward(lam.data_ptr(), _ptr(h0), h.data_ptr(), dh.data_ptr(), dlam.data_ptr(),
                        dx.data_ptr(), dh0.data_ptr(), T, W,
                        capi.SERIAL if mode == "serial" else capi.PARALLEL, lam.element_size(),
@@ -79,7 +123,9 @@ class LinearRecurrence(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, lam, x, h0):
-        h = scan(lam.contiguous(), x.contiguous(), None if h0 is None else h0.contiguous())
+        lam = lam.contiguous()
+        h0 = None if h0 is None else h0.contiguous()
+        h = scan(lam, x.contiguous(), h0)
         ctx.save_for_backward(lam, h, h0 if h0 is not None else torch.empty(0, device=lam.device))
         ctx.has_h0 = h0 is not None
         return h
@@ -87,7 +133,7 @@ class LinearRecurrence(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dh):
         lam, h, h0 = ctx.saved_tensors
-        dlam, dx, dh0 = scan_backward(lam.contiguous(), h0 if ctx.has_h0 else None, h, dh.contiguous())
+        dlam, dx, dh0 = scan_backward(lam, h0 if ctx.has_h0 else None, h, dh.contiguous())
         return dlam, dx, (dh0 if ctx.has_h0 else None)
 
 

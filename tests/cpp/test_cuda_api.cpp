@@ -258,6 +258,70 @@ static void test_plan_scan() {
   }
 }
 
+// "finite screening pinpoints the poisoned element" (test_recurrence.cpp:328-350):
+// check_finite off -> no throw; on -> ContractViolation naming the tensor and
+// the 1-based step, batch and feature of the first non-finite element.
+static void test_check_finite() {
+  const index_t T = 9, b = 2, n = 4, W = b * n;
+  std::vector<float> lam = uniform(T * W, 0.05f, 0.95f, 108), x = uniform(T * W, -1, 1, 109);
+  std::vector<float> h0 = uniform(W, -1, 1, 110), dh = uniform(T * W, -1, 1, 111);
+  x[(5 * b + 1) * n + 2] = std::nanf("");  // in.impulses.at(5, 1, 2)
+  Dev L(lam), X(x), H0(h0), H(T * W), DH(dh), DL(T * W), DX(T * W), D0(W);
+  DeviceTensor3<float> tl{L.p, T, b, n}, tx{X.p, T, b, n}, th{H.p, T, b, n}, tdh{DH.p, T, b, n};
+  DeviceTensor2<float> t0{H0.p, b, n};
+  bool threw = false;
+  try {
+    scan_serial(tl, tx, t0, th);  // screening off: garbage in, garbage out
+  } catch (...) {
+    threw = true;
+  }
+  CHECK(!threw, "check_finite=false threw");
+  auto expect = [&](auto fn, const char* name, const char* where) {
+    std::string msg;
+    try {
+      fn();
+    } catch (const ContractViolation& e) {
+      msg = e.what();
+    }
+    CHECK(msg.find(std::string("non-finite value in ") + name) != std::string::npos && msg.find(where) != std::string::npos,
+          "screen message '%s' (want %s %s)", msg.c_str(), name, where);
+  };
+  expect([&] { scan_serial(tl, tx, t0, th, nullptr, true); }, "impulses", "[t=6, b=1, n=2]");
+  expect([&] { scan_parallel(tl, tx, t0, th, nullptr, nullptr, true); }, "impulses", "[t=6, b=1, n=2]");
+  expect([&] { scan_parallel(tl, tx, t0, plan_chunks(T, 2), th, (ScanSummaries<float>*)nullptr, nullptr, true); }, "impulses",
+         "[t=6, b=1, n=2]");
+  expect([&] { scan(tl, tx, t0, th, ScanMode::Parallel, nullptr, nullptr, true); }, "impulses", "[t=6, b=1, n=2]");
+  // decays are screened first; the initial state reports [b, n]
+  std::vector<float> lam2 = lam;
+  lam2[(8 * b + 0) * n + 3] = INFINITY;
+  Dev L2(lam2);
+  DeviceTensor3<float> tl2{L2.p, T, b, n};
+  expect([&] { scan_serial(tl2, tx, t0, th, nullptr, true); }, "decays", "[t=9, b=0, n=3]");
+  std::vector<float> x_ok = uniform(T * W, -1, 1, 112), h0b = h0;
+  h0b[1 * n + 1] = -INFINITY;
+  Dev X2(x_ok), H0b(h0b);
+  DeviceTensor3<float> tx2{X2.p, T, b, n};
+  DeviceTensor2<float> t0b{H0b.p, b, n};
+  expect([&] { scan_serial(tl, tx2, t0b, th, nullptr, true); }, "initial", "[b=1, n=1]");
+  // backward screens decays and d_h (recurrence.hpp:292-296)
+  std::vector<float> dh2 = dh;
+  dh2[(0 * b + 0) * n + 0] = std::nanf("");
+  Dev DH2(dh2);
+  DeviceTensor3<float> tdh2{DH2.p, T, b, n};
+  RecurrenceGradients<float> g{{DL.p, T, b, n}, {DX.p, T, b, n}, {D0.p, b, n}};
+  scan_serial(tl, tx2, t0, th, nullptr, true);  // finite: no throw
+  expect([&] { scan_backward(tl, t0, th, tdh2, g, ScanMode::Parallel, nullptr, nullptr, true); }, "d_h",
+         "[t=1, b=0, n=0]");
+  expect([&] { scan_backward(tl, t0, th, tdh2, plan_chunks(T, 3), g, nullptr, true); }, "d_h", "[t=1, b=0, n=0]");
+  threw = false;
+  try {
+    scan_backward(tl, t0, th, tdh, g, ScanMode::Serial, nullptr, nullptr, true);
+  } catch (...) {
+    threw = true;
+  }
+  CHECK(!threw, "finite backward inputs threw");
+}
+
 int main() {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -266,6 +330,7 @@ int main() {
   }
   test_scans();
   test_plan_scan();
+  test_check_finite();
   test_gilr_lstm();
   test_qrnn();
   if (failures == 0) std::printf("ALL OK\n");

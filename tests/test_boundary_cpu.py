@@ -137,3 +137,21 @@ def test_planner_kernel_counts():
     assert capi.scan_kernel_count(65536, 8192, backward=True) == 1
     assert capi.scan_kernel_count(1 << 20, 128, mode=capi.SERIAL) == 1
     assert capi.scan_kernel_count(0, 128) == -1
+
+
+def test_bench_host_inputs_shard_independent():
+    """bench.py's host inputs: rows [r0, r1) generated alone equal the same
+    rows of the global array, so the sequence-sharded ranks, the 1-GPU run,
+    the CPU baseline and the reference arm all see one problem."""
+    import numpy as np
+    import bench
+    full = bench.host_rows(1000, (2, 3), 0.05, 0.95, 7)
+    assert full.dtype == np.float32 and full.shape == (1000, 2, 3)
+    assert full.min() >= 0.05 and full.max() <= 0.95
+    for world in (2, 3, 8):
+        from paper_1709_04057_b200.sharded import segment_bounds
+        parts = [bench.host_rows(1000, (2, 3), 0.05, 0.95, 7, *segment_bounds(1000, world, r))
+                 for r in range(world)]
+        assert np.array_equal(np.concatenate(parts), full)
+    lam, x, h0, dh = bench.host_problem(64, 1, 4, 3)
+    assert h0.shape == (1, 4) and lam.shape == x.shape == dh.shape == (64, 1, 4)

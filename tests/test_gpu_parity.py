@@ -382,6 +382,58 @@ def test_first_nonfinite(oracle):
     assert idx == 5 * 8 + 1 * 4 + 2 == oracle.first_nonfinite(a.cpu().numpy())
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_check_finite_pinpoints_the_poisoned_element(dtype):
+    """test_recurrence.cpp:328-350 through the device path: screening off
+    passes garbage through; on, the error names the tensor and the 1-based
+    step (t=6), batch (b=1) and feature (n=2) of the NaN in impulses."""
+    from paper_1709_04057_b200 import torch_ops
+    g = torch.Generator(device="cuda").manual_seed(108)
+    lam = torch.empty(9, 2, 4, device="cuda", dtype=dtype).uniform_(0.05, 0.95, generator=g)
+    x = torch.empty_like(lam).uniform_(-1, 1, generator=g)
+    h0 = torch.empty(2, 4, device="cuda", dtype=dtype).uniform_(-1, 1, generator=g)
+    x[5, 1, 2] = float("nan")
+    torch_ops.scan(lam, x, h0)  # no throw
+    for mode in ("serial", "parallel"):
+        with pytest.raises(RuntimeError) as e:
+            torch_ops.scan(lam, x, h0, mode=mode, check_finite=True)
+        msg = str(e.value)
+        assert "non-finite value in impulses" in msg and "t=6" in msg and "b=1" in msg and "n=2" in msg
+    x[5, 1, 2] = 0.5
+    h0[0, 3] = float("inf")
+    with pytest.raises(RuntimeError, match=r"non-finite value in initial at \[b=0, n=3\]"):
+        torch_ops.scan(lam, x, h0, check_finite=True)
+    h0[0, 3] = 0.0
+    h = torch_ops.scan(lam, x, h0, check_finite=True)
+    dh = torch.ones_like(h)
+    dh[8, 0, 1] = float("-inf")
+    with pytest.raises(RuntimeError, match=r"non-finite value in d_h at \[t=9, b=0, n=1\]"):
+        torch_ops.scan_backward(lam, h0, h, dh, check_finite=True)
+    lam[0, 0, 0] = float("nan")
+    with pytest.raises(RuntimeError, match=r"non-finite value in decays at \[t=1, b=0, n=0\]"):
+        torch_ops.scan_backward(lam, h0, h, dh, check_finite=True)
+
+
+def test_torch_ops_shape_contract():
+    """h0 / out buffers of the wrong shape are contract errors, not
+    out-of-bounds device accesses (the C ABI sees pointers only)."""
+    from paper_1709_04057_b200 import torch_ops
+    lam = torch.rand(5, 2, 3, device="cuda")
+    with pytest.raises(RuntimeError, match=r"initial state \[3\] does not match \[2, 3\]"):
+        torch_ops.scan(lam, lam, torch.zeros(3, device="cuda"))
+    with pytest.raises(RuntimeError, match="shape mismatch"):
+        torch_ops.scan(lam, lam, out=torch.empty(5, 2, 2, device="cuda"))
+    h = torch_ops.scan(lam, lam)
+    with pytest.raises(RuntimeError, match="shape mismatch"):
+        torch_ops.scan_backward(lam, None, h, h, out=(torch.empty_like(h), torch.empty_like(h),
+                                                      torch.empty(3, device="cuda")))
+    # a non-contiguous h0 works through autograd forward AND backward
+    lam_r = lam.clone().requires_grad_()
+    h0 = torch.rand(3, 2, device="cuda").t().requires_grad_()
+    torch_ops.linear_recurrence(lam_r, lam, h0).sum().backward()
+    assert h0.grad.shape == (2, 3)
+
+
 def test_cuda_array_interface_zero_copy(lr, oracle):
     rng = np.random.default_rng(16)
     lam = rng.uniform(0.05, 0.95, (300, 2, 20)).astype(np.float32)

@@ -89,26 +89,53 @@ def test_sequence_sharded_ranks_on_gpu(oracle, world, T, W, lo, hi, exchange, re
             assert max_rel_error(DH0, g[2]) <= 1e-5
 
 
-@pytest.mark.parametrize("workload", ["c4", "c2"])
-def test_bench_two_ranks_sharing_the_gpu(workload):
-    """bench.py at --gpus 2 under torchrun (ranks share the one GPU: gloo for
-    the host-side plumbing, CUDA IPC for the C4 carry mailboxes): one JSON line
-    from rank 0 with the whole-job value."""
+@pytest.mark.parametrize("workload,launch", [("c4", "torchrun"), ("c2", "torchrun"), ("c5", "self")])
+def test_bench_two_ranks_sharing_the_gpu(workload, launch):
+    """bench.py at --gpus 2 (ranks share the one GPU: gloo for the host-side
+    plumbing, CUDA IPC for the carry mailboxes), launched by torchrun or by
+    bench.py re-executing itself: one JSON line from rank 0 with the
+    whole-job value, every guard passed."""
     import json
     import subprocess
     import sys
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     env = dict(os.environ, LINREC_BENCH_SHARE_GPU="1")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--steps", "3", "--warmup", "3", "--workload", workload, "--no-e2e", "--no-cpu"]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    env.pop("WORLD_SIZE", None)
+    args = ["--gpus", "2", "--steps", "3", "--warmup", "3", "--workload", workload, "--no-e2e", "--no-cpu"]
+    if launch == "torchrun":
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+               "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py")] + args
+    else:
+        cmd = [sys.executable, os.path.join(ROOT, "bench.py")] + args
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, out.stdout
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0
-    assert d["scaling"] == ("strong" if workload == "c4" else "weak")
+    assert d["scaling"] == {"c4": "strong", "c2": "weak", "c5": "strong"}[workload]
     if workload == "c4":
         assert "peer-memory" in d["config"]["parallelism"]
+    if workload == "c2":
+        # the 1M-step workload beside the headline: 1 GPU and sequence-sharded
+        assert d["c4"]["n_gpus"] == 1 and d["c4"]["guard_max_rel_err"] <= 1e-5
+        s = d["c4_seq_sharded"]
+        assert s["n_gpus"] == 2 and s["exchange"] == "p2p" and s["guard_max_rel_err"] <= 1e-5
+        assert s["speedup"] > 0 and s["slow_decay"]["guard_max_rel_err"] <= 1e-5
+    if workload == "c5":
+        assert [p["sharding"] for p in d["points"]] == ["channel"] * 3 + ["sequence"] * 2
+        assert all(p["guard_max_rel_err"] <= 1e-5 for p in d["points"])
+
+
+def test_bench_refuses_missing_gpus():
+    """--gpus N with fewer visible GPUs is an error, not a silent 1-GPU run."""
+    import subprocess
+    import sys
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    n = torch.cuda.device_count() + 1
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "LINREC_BENCH_SHARE_GPU")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--steps", "3"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert out.returncode != 0 and "GPU(s) visible" in (out.stderr + out.stdout)
