@@ -711,7 +711,9 @@ def e2e_legs(rk, args, host, T, B, D):
         "h2d_bytes_per_step": rk.world * (4 * (2 * N + W) + 4 * (3 * N + W)),
         "d2h_bytes_per_step": rk.world * (4 * N + 4 * (2 * N + W)),
         "api": "paper_1709_04057_b200.linrec.scan + linrec.scan_backward (the reference's Python API, "
-               "linrec_py.cpp:91-140) on pageable numpy arrays, outputs allocated per call",
+               "linrec_py.cpp:91-140) on pageable numpy arrays (staged through pinned bounce buffers by the library's "
+               "copy threads), result arrays allocated per call (page-locked, from the library's caching host "
+               "allocator)",
         "timing": "host wall clock around synchronous calls, max over ranks",
         "ranks": rk.world,
     }

@@ -173,6 +173,14 @@ int linrec_scan_backward_host_f64(const double* lam, const double* h0,
                                   double* dlam, double* dx, double* dh0,
                                   int64_t T, int64_t W, int mode, int device);
 
+/* Page-locked host memory from a caching allocator (blocks are recycled by
+ * size; at most a quarter of RAM stays pinned while idle).  Host buffers
+ * from here run the host entry points above at full link speed: the Python
+ * module allocates its numpy results with it (linrec_py.cpp:56-69 returns
+ * fresh arrays; these are fresh too, just page-locked). */
+int linrec_host_alloc(void** ptr, size_t bytes);
+int linrec_host_free(void* ptr);
+
 /* ---- finite screening (recurrence.hpp:133-163) -------------------------- *
  * Index of the first non-finite element of v[n] (device pointer), or -1.
  * Synchronous on `stream`. */

@@ -6,6 +6,7 @@
 #include "linrec_cuda.h"
 
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -464,19 +465,17 @@ int pipe_reserve_bounce(HostPipe* hp, size_t bytes, size_t small_bytes) {
   return LINREC_OK;
 }
 
-// true when every non-null host pointer is page-locked (or device-mapped):
-// those DMA straight from the caller's memory; anything else is staged.
-bool all_pinned(std::initializer_list<const void*> ptrs) {
-  for (const void* p : ptrs) {
-    if (!p) continue;
-    cudaPointerAttributes a;
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    if (a.type == cudaMemoryTypeUnregistered) return false;
+// Page-locked (or device-mapped) host buffers DMA straight from / into the
+// caller's memory; pageable ones (ordinary numpy arrays) are staged through
+// the pinned bounce buffers.  Decided per array.
+bool pageable(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
   }
-  return true;
+  return a.type == cudaMemoryTypeUnregistered;
 }
 
 int64_t chunk_rows(int64_t T, int64_t W, size_t elem) {
@@ -485,6 +484,27 @@ int64_t chunk_rows(int64_t T, int64_t W, size_t elem) {
 }
 
 using CopyJobs = std::vector<std::tuple<void*, const void*, size_t>>;
+
+// Caching allocator of page-locked host memory (linrec_host_alloc/free): the
+// Python module allocates its numpy RESULTS here, so device->host copies land
+// straight in the caller's array at full link speed (no bounce, no first-touch
+// page faults) and repeated calls of one shape recycle the same blocks.
+struct PinnedCache {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_blocks;  // rounded size -> block
+  std::map<void*, size_t> live;
+  size_t cached = 0, cap = 0;
+};
+PinnedCache& pinned_cache() {
+  static PinnedCache* c = [] {
+    auto* pc = new PinnedCache();  // leaked on purpose: outlives static destructors that free arrays
+    const long pages = sysconf(_SC_PHYS_PAGES), psize = sysconf(_SC_PAGE_SIZE);
+    const size_t phys = pages > 0 && psize > 0 ? size_t(pages) * size_t(psize) : (size_t(16) << 30);
+    pc->cap = phys / 4;  // keep at most a quarter of RAM pinned while unused
+    return pc;
+  }();
+  return *c;
+}
 
 template <class S>
 int scan_host(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W, int mode,
@@ -501,13 +521,14 @@ int scan_host(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W,
   const size_t row = size_t(W) * sizeof(S);
   if ((rc = pipe_reserve(hp, size_t(Tc) * row, 2 * row))) return rc;
   // pageable arrays (numpy) go through pinned bounce buffers; pinned ones DMA directly
-  const bool staged = !all_pinned({lam, x, h0, h});
+  const bool st_l = pageable(lam), st_x = pageable(x), st_h = pageable(h);
+  const bool staged = st_l || st_x || st_h || pageable(h0);
   if (staged && (rc = pipe_reserve_bounce(hp, size_t(Tc) * row, 2 * row))) return rc;
   S* d_h0 = nullptr;
   if (h0) {
     d_h0 = static_cast<S*>(hp->small);
     const S* src = h0;
-    if (staged) {
+    if (pageable(h0)) {
       std::memcpy(hp->small_host, h0, row);
       src = static_cast<const S*>(hp->small_host);
     }
@@ -531,11 +552,14 @@ int scan_host(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W,
     const size_t bytes = size_t(rows) * row;
     const S* src_l = lam + t0 * W;
     const S* src_x = x + t0 * W;
-    if (staged) {  // bounce slot s is free once chunk k - kSlots's H2D finished
+    if (st_l || st_x) {  // bounce slot s is free once chunk k - kSlots's H2D finished
       if (k >= kSlots) LINREC_CUDA_TRY(cudaEventSynchronize(hp->ev_in[s]));
-      hp->pool->copy(CopyJobs{{hp->bounce[s][0], src_l, bytes}, {hp->bounce[s][1], src_x, bytes}});
-      src_l = static_cast<const S*>(hp->bounce[s][0]);
-      src_x = static_cast<const S*>(hp->bounce[s][1]);
+      CopyJobs jobs;
+      if (st_l) jobs.emplace_back(hp->bounce[s][0], src_l, bytes);
+      if (st_x) jobs.emplace_back(hp->bounce[s][1], src_x, bytes);
+      hp->pool->copy(jobs);
+      if (st_l) src_l = static_cast<const S*>(hp->bounce[s][0]);
+      if (st_x) src_x = static_cast<const S*>(hp->bounce[s][1]);
     }
     if (k >= kSlots) LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_in, hp->ev_comp[s], 0));
     LINREC_CUDA_TRY(cudaMemcpyAsync(dl, src_l, bytes, cudaMemcpyHostToDevice, hp->s_in));
@@ -546,14 +570,14 @@ int scan_host(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W,
     if ((rc = scan_device<S>(dl, dxv, seed, dhv, rows, W, mode, &hp->ws, hp->s_comp))) return rc;
     LINREC_CUDA_TRY(cudaEventRecord(hp->ev_comp[s], hp->s_comp));
     LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_out, hp->ev_comp[s], 0));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(staged ? hp->bounce[s][3] : static_cast<void*>(h + t0 * W), dhv, bytes,
+    LINREC_CUDA_TRY(cudaMemcpyAsync(st_h ? hp->bounce[s][3] : static_cast<void*>(h + t0 * W), dhv, bytes,
                                     cudaMemcpyDeviceToHost, hp->s_out));
     LINREC_CUDA_TRY(cudaEventRecord(hp->ev_out[s], hp->s_out));
     seed = dhv + (rows - 1) * W;  // carry into the next chunk
     // the previous chunk's result leaves the bounce buffer while this one runs
-    if (staged && k >= 1 && (rc = drain(k - 1))) return rc;
+    if (st_h && k >= 1 && (rc = drain(k - 1))) return rc;
   }
-  if (staged && (rc = drain(nchunks - 1))) return rc;
+  if (st_h && (rc = drain(nchunks - 1))) return rc;
   LINREC_CUDA_TRY(cudaStreamSynchronize(hp->s_out));
   LINREC_CUDA_TRY(cudaStreamSynchronize(hp->s_comp));
   return LINREC_OK;
@@ -576,14 +600,16 @@ int scan_backward_host(const S* lam, const S* h0, const S* h, const S* dh, S* dl
   // per slot: buf0 = [lam | dlam], buf1 = [h shifted by one row | dx],
   // buf2 = [dh]; each half holds Tc rows.
   if ((rc = pipe_reserve(hp, size_t(2) * size_t(Tc) * row, 3 * row))) return rc;
-  const bool staged = !all_pinned({lam, h0, h, dh, dlam, dx, dh0});
+  const bool st_l = pageable(lam), st_h = pageable(h), st_dh = pageable(dh);
+  const bool st_dl = pageable(dlam), st_dx = pageable(dx), st_h0 = pageable(h0), st_d0 = pageable(dh0);
+  const bool staged = st_l || st_h || st_dh || st_dl || st_dx || st_h0 || st_d0;
   if (staged && (rc = pipe_reserve_bounce(hp, size_t(Tc) * row, 3 * row))) return rc;
   S* d_h0 = static_cast<S*>(hp->small);
   S* d_dh0 = d_h0 + W;
-  S* h_dh0 = staged ? static_cast<S*>(hp->small_host) + W : dh0;  // where dh0 lands on the host
+  S* h_dh0 = st_d0 ? static_cast<S*>(hp->small_host) + W : dh0;  // where dh0 lands on the host
   if (h0) {
     const S* src = h0;
-    if (staged) {
+    if (st_h0) {
       std::memcpy(hp->small_host, h0, row);
       src = static_cast<const S*>(hp->small_host);
     }
@@ -598,9 +624,13 @@ int scan_backward_host(const S* lam, const S* h0, const S* h, const S* dh, S* dl
     const int64_t t0 = k * Tc, rows = std::min<int64_t>(Tc, T - t0);
     const size_t bytes = size_t(rows) * row;
     LINREC_CUDA_TRY(cudaEventSynchronize(hp->ev_out[s]));
-    hp->pool->copy(CopyJobs{{dlam + t0 * W, hp->bounce[s][3], bytes}, {dx + t0 * W, hp->bounce[s][4], bytes}});
+    CopyJobs jobs;
+    if (st_dl) jobs.emplace_back(dlam + t0 * W, hp->bounce[s][3], bytes);
+    if (st_dx) jobs.emplace_back(dx + t0 * W, hp->bounce[s][4], bytes);
+    hp->pool->copy(jobs);
     return LINREC_OK;
   };
+  const bool drains = st_dl || st_dx;
   const S* lam_next = nullptr;
   const S* g_next = nullptr;
   for (int64_t i = 0; i < nchunks; ++i) {
@@ -621,13 +651,16 @@ int scan_backward_host(const S* lam, const S* h0, const S* h, const S* dh, S* dl
     const S* src_dh = dh + t0 * W;
     const S* src_h = t0 > 0 ? h + (t0 - 1) * W : h;
     const size_t h_bytes = t0 > 0 ? bytes : bytes - row;
-    if (staged) {
+    if (st_l || st_h || st_dh) {
       if (i >= kSlots) LINREC_CUDA_TRY(cudaEventSynchronize(hp->ev_in[s]));
-      hp->pool->copy(CopyJobs{{hp->bounce[s][0], src_l, bytes}, {hp->bounce[s][1], src_h, h_bytes},
-                              {hp->bounce[s][2], src_dh, bytes}});
-      src_l = static_cast<const S*>(hp->bounce[s][0]);
-      src_h = static_cast<const S*>(hp->bounce[s][1]);
-      src_dh = static_cast<const S*>(hp->bounce[s][2]);
+      CopyJobs jobs;
+      if (st_l) jobs.emplace_back(hp->bounce[s][0], src_l, bytes);
+      if (st_h) jobs.emplace_back(hp->bounce[s][1], src_h, h_bytes);
+      if (st_dh) jobs.emplace_back(hp->bounce[s][2], src_dh, bytes);
+      hp->pool->copy(jobs);
+      if (st_l) src_l = static_cast<const S*>(hp->bounce[s][0]);
+      if (st_h) src_h = static_cast<const S*>(hp->bounce[s][1]);
+      if (st_dh) src_dh = static_cast<const S*>(hp->bounce[s][2]);
     }
     // slot s was last filled at chunk i-3, whose lam row 0 and G row 0 are
     // also read by chunk i-2 (lam_next / g_next): wait for that compute.
@@ -654,20 +687,20 @@ int scan_backward_host(const S* lam, const S* h0, const S* h, const S* dh, S* dl
       return rc;
     LINREC_CUDA_TRY(cudaEventRecord(hp->ev_comp[s], hp->s_comp));
     LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_out, hp->ev_comp[s], 0));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(staged ? hp->bounce[s][3] : static_cast<void*>(dlam + t0 * W), d_dlam, bytes,
+    LINREC_CUDA_TRY(cudaMemcpyAsync(st_dl ? hp->bounce[s][3] : static_cast<void*>(dlam + t0 * W), d_dlam, bytes,
                                     cudaMemcpyDeviceToHost, hp->s_out));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(staged ? hp->bounce[s][4] : static_cast<void*>(dx + t0 * W), d_dx, bytes,
+    LINREC_CUDA_TRY(cudaMemcpyAsync(st_dx ? hp->bounce[s][4] : static_cast<void*>(dx + t0 * W), d_dx, bytes,
                                     cudaMemcpyDeviceToHost, hp->s_out));
     if (k == 0) LINREC_CUDA_TRY(cudaMemcpyAsync(h_dh0, d_dh0, row, cudaMemcpyDeviceToHost, hp->s_out));
     LINREC_CUDA_TRY(cudaEventRecord(hp->ev_out[s], hp->s_out));
     lam_next = d_lam;  // lam at row t0 and G at row t0 feed the previous chunk
     g_next = d_dx;
-    if (staged && i >= 1 && (rc = drain(i - 1))) return rc;
+    if (drains && i >= 1 && (rc = drain(i - 1))) return rc;
   }
-  if (staged && (rc = drain(nchunks - 1))) return rc;
+  if (drains && (rc = drain(nchunks - 1))) return rc;
   LINREC_CUDA_TRY(cudaStreamSynchronize(hp->s_out));
   LINREC_CUDA_TRY(cudaStreamSynchronize(hp->s_comp));
-  if (staged) std::memcpy(dh0, h_dh0, row);
+  if (st_d0) std::memcpy(dh0, h_dh0, row);
   return LINREC_OK;
 }
 
@@ -1017,6 +1050,53 @@ int linrec_scan_backward_host_f64(const double* lam, const double* h0, const dou
                                   const double* dh, double* dlam, double* dx, double* dh0,
                                   int64_t T, int64_t W, int mode, int device) {
   return scan_backward_host<double>(lam, h0, h, dh, dlam, dx, dh0, T, W, mode, device);
+}
+
+int linrec_host_alloc(void** ptr, size_t bytes) {
+  if (!ptr) return fail(LINREC_ERR_VALUE, "host_alloc: ptr required");
+  *ptr = nullptr;
+  const size_t rounded = (std::max<size_t>(bytes, 1) + (size_t(2) << 20) - 1) / (size_t(2) << 20) * (size_t(2) << 20);
+  PinnedCache& c = pinned_cache();
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.free_blocks.find(rounded);
+    if (it != c.free_blocks.end()) {
+      *ptr = it->second;
+      c.free_blocks.erase(it);
+      c.cached -= rounded;
+      c.live[*ptr] = rounded;
+      return LINREC_OK;
+    }
+  }
+  void* p = nullptr;
+  LINREC_CUDA_TRY(cudaHostAlloc(&p, rounded, cudaHostAllocPortable));
+  std::lock_guard<std::mutex> lk(c.mu);
+  c.live[p] = rounded;
+  *ptr = p;
+  return LINREC_OK;
+}
+
+int linrec_host_free(void* ptr) {
+  if (!ptr) return LINREC_OK;
+  PinnedCache& c = pinned_cache();
+  std::vector<void*> release;
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.live.find(ptr);
+    if (it == c.live.end()) return fail(LINREC_ERR_VALUE, "host_free: not a linrec_host_alloc block");
+    const size_t n = it->second;
+    c.live.erase(it);
+    c.free_blocks.emplace(n, ptr);
+    c.cached += n;
+    while (c.cached > c.cap && !c.free_blocks.empty()) {  // trim the largest idle blocks
+      auto big = std::prev(c.free_blocks.end());
+      c.cached -= big->first;
+      release.push_back(big->second);
+      c.free_blocks.erase(big);
+    }
+  }
+  for (void* q : release) LINREC_CUDA_TRY(cudaFreeHost(q));
+  return LINREC_OK;
 }
 
 int linrec_first_nonfinite_f32(const float* v, int64_t n, int64_t* index, void* stream) {

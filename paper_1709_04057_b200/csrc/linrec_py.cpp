@@ -212,6 +212,23 @@ class DeviceArray {
 };
 
 // ---- host (numpy) path --------------------------------------------------------
+// Result arrays: freshly allocated numpy arrays as in the reference
+// (linrec_py.cpp:56-69), backed by page-locked memory from the library's
+// caching allocator when large, so the device->host copies land in them
+// directly.  Falls back to ordinary numpy memory if pinning fails.
+template <class S>
+py::array_t<S> result_array(const std::vector<py::ssize_t>& shape) {
+  size_t n = 1;
+  for (auto d : shape) n *= size_t(d);
+  const size_t bytes = n * sizeof(S);
+  void* p = nullptr;
+  if (bytes >= (size_t(4) << 20) && linrec_host_alloc(&p, bytes) == LINREC_OK) {
+    py::capsule owner(p, [](void* q) { linrec_host_free(q); });
+    return py::array_t<S>(shape, static_cast<S*>(p), owner);
+  }
+  return py::array_t<S>(shape);
+}
+
 template <class S>
 int host_scan(const S* l, const S* x, const S* h0, S* h, index_t T, index_t W, int mode, int dev) {
   if constexpr (sizeof(S) == 4) return linrec_scan_host_f32(l, x, h0, h, T, W, mode, dev);
@@ -238,7 +255,7 @@ py::object scan_numpy(const py::array& decays, const py::array& impulses, const 
   check_same3(dl, dx, "recurrence");  // validate_recurrence_shapes, recurrence.hpp:43
   if (!initial.is_none()) check_initial(dl, r, c);
   const int dev = resolve_device(device);
-  py::array_t<S> out({py::ssize_t(dl.T), py::ssize_t(dl.b), py::ssize_t(dl.n)});
+  py::array_t<S> out = result_array<S>({py::ssize_t(dl.T), py::ssize_t(dl.b), py::ssize_t(dl.n)});
   S* hp = out.mutable_data();
   const S* h0p = initial.is_none() ? nullptr : h0.data();
   int rc;
@@ -269,7 +286,7 @@ py::object scan_backward_numpy(const py::array& decays, const py::object& initia
   if (!initial.is_none()) check_initial(dl, r, c);
   const int dev = resolve_device(device);
   const auto shape3 = std::vector<py::ssize_t>{py::ssize_t(dl.T), py::ssize_t(dl.b), py::ssize_t(dl.n)};
-  py::array_t<S> g_lam(shape3), g_x(shape3);
+  py::array_t<S> g_lam = result_array<S>(shape3), g_x = result_array<S>(shape3);
   py::array_t<S> g_h0({py::ssize_t(dl.b), py::ssize_t(dl.n)});
   S* p_lam = g_lam.mutable_data();
   S* p_x = g_x.mutable_data();
