@@ -47,7 +47,7 @@ $(CPPSHARD): tests/cpp/test_sharded.cpp include/linrec/cuda_sharded.hpp include/
 	@mkdir -p $(BUILD)
 	$(CXX) -std=c++17 -O2 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -llinrec_cuda \
 	  -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
-$(CPPTEST): tests/cpp/test_cuda_api.cpp include/linrec/cuda_scan.hpp include/linrec/cuda_layers.hpp include/linrec_cuda.h $(LIB)
+$(CPPTEST): tests/cpp/test_cuda_api.cpp include/linrec/cuda_scan.hpp include/linrec/cuda_layers.hpp include/linrec/cuda_sharded.hpp include/linrec_cuda.h $(LIB)
 	@mkdir -p $(BUILD)
 	$(CXX) -std=c++17 -O2 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -llinrec_cuda \
 	  -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64

@@ -18,6 +18,7 @@
 
 #include <array>
 #include <cstdint>
+#include <sstream>
 #include <string>
 #include <utility>
 #include <vector>
@@ -121,6 +122,74 @@ class SequenceShardedScan {
   index_t T_, W_;
   linrec_sharded_t ctx_ = nullptr;
 };
+
+// ---- channel sharding of HOST tensors over several GPUs -------
+// Channels are independent (recurrence.hpp:109), so the columns of a host
+// [T][b*n] tensor split into per-GPU blocks (linrec_column_block) with no
+// communication: one host thread per GPU stages its block with 2-D copies,
+// scans it and writes its columns back.  The reference's scan / scan_backward
+// over host Tensor3 (recurrence.hpp:255-263, :352-363), many GPUs at once.
+template <class S>
+struct HostTensor3 {
+  S* data = nullptr;
+  index_t steps = 0, batch = 0, features = 0;
+  index_t step_size() const { return batch * features; }
+};
+
+namespace detail {
+inline int multi_call(const float* l, const float* x, const float* h0, float* h, index_t T, index_t W, int mode,
+                      const int* d, int n) {
+  return linrec_scan_host_multi_f32(l, x, h0, h, T, W, mode, d, n);
+}
+inline int multi_call(const double* l, const double* x, const double* h0, double* h, index_t T, index_t W, int mode,
+                      const int* d, int n) {
+  return linrec_scan_host_multi_f64(l, x, h0, h, T, W, mode, d, n);
+}
+inline int multi_bwd_call(const float* l, const float* h0, const float* h, const float* dh, float* dl, float* dx,
+                          float* dh0, index_t T, index_t W, int mode, const int* d, int n) {
+  return linrec_scan_backward_host_multi_f32(l, h0, h, dh, dl, dx, dh0, T, W, mode, d, n);
+}
+inline int multi_bwd_call(const double* l, const double* h0, const double* h, const double* dh, double* dl,
+                          double* dx, double* dh0, index_t T, index_t W, int mode, const int* d, int n) {
+  return linrec_scan_backward_host_multi_f64(l, h0, h, dh, dl, dx, dh0, T, W, mode, d, n);
+}
+template <class S, class U>
+void check_host_shape(const HostTensor3<S>& a, const HostTensor3<U>& b, const char* op) {
+  if (a.steps != b.steps || a.batch != b.batch || a.features != b.features) {
+    std::ostringstream os;
+    os << op << ": shape mismatch, [" << a.steps << "," << a.batch << "," << a.features << "] vs [" << b.steps
+       << "," << b.batch << "," << b.features << "]";
+    throw ContractViolation(os.str());
+  }
+}
+}  // namespace detail
+
+// h = scan(decays, impulses, initial) with the channels split over `devices`;
+// initial: [b*n] host row or nullptr (zeros).
+template <class S>
+void scan_channel_sharded(const HostTensor3<S>& decays, const HostTensor3<S>& impulses, const S* initial,
+                          HostTensor3<S>& h, const std::vector<int>& devices, ScanMode mode = ScanMode::Parallel) {
+  detail::check_host_shape(decays, impulses, "recurrence");
+  detail::check_host_shape(decays, h, "scan_parallel(h)");
+  throw_status(detail::multi_call(decays.data, impulses.data, initial, h.data, decays.steps, decays.step_size(),
+                                  static_cast<int>(mode), devices.data(), int(devices.size())));
+}
+
+// (d_decays, d_impulses, d_initial[b*n]) = scan_backward(...) with the
+// channels split over `devices`.
+template <class S>
+void scan_backward_channel_sharded(const HostTensor3<S>& decays, const S* initial, const HostTensor3<S>& h,
+                                   const HostTensor3<S>& d_h, HostTensor3<S>& d_decays, HostTensor3<S>& d_impulses,
+                                   S* d_initial, const std::vector<int>& devices,
+                                   ScanMode mode = ScanMode::Parallel) {
+  detail::check_host_shape(decays, h, "scan_backward(h)");
+  detail::check_host_shape(decays, d_h, "scan_backward(d_h)");
+  detail::check_host_shape(decays, d_decays, "scan_backward(d_decays)");
+  detail::check_host_shape(decays, d_impulses, "scan_backward(d_impulses)");
+  throw_status(detail::multi_bwd_call(decays.data, initial, h.data, d_h.data, d_decays.data, d_impulses.data,
+                                      d_initial, decays.steps, decays.step_size(), static_cast<int>(mode),
+                                      devices.data(), int(devices.size())));
+}
 
 }  // namespace cuda
 }  // namespace linrec

@@ -173,6 +173,56 @@ int linrec_scan_backward_host_f64(const double* lam, const double* h0,
                                   double* dlam, double* dx, double* dh0,
                                   int64_t T, int64_t W, int mode, int device);
 
+/* ---- channel sharding of host arrays ---------------------- *
+ * Channels are independent (recurrence.hpp:109: the inner loop of scan_span
+ * runs over j), so a [T][W] problem splits into column blocks with no
+ * communication.  *_columns: scan columns [c0, c1) of the FULL host arrays
+ * (row stride W; h0 / dh0 are full [W] rows) on `device`, staging the strided
+ * block with 2-D copies; only those columns of the outputs are written.
+ * *_multi: split the columns over `ndev` devices (linrec_column_block: blocks
+ * of multiples of 4 channels where W allows, longer first), one host thread
+ * per device, each with its own streams -- the single-process form of the
+ * channel-sharded multi-GPU scan.  Replaces: scan / scan_backward over host
+ * Tensor3 (recurrence.hpp:255-263, :352-363) for the channel-parallel case. */
+int linrec_scan_host_columns_f32(const float* lam, const float* x,
+                                 const float* h0, float* h, int64_t T,
+                                 int64_t W, int64_t c0, int64_t c1, int mode,
+                                 int device);
+int linrec_scan_host_columns_f64(const double* lam, const double* x,
+                                 const double* h0, double* h, int64_t T,
+                                 int64_t W, int64_t c0, int64_t c1, int mode,
+                                 int device);
+int linrec_scan_backward_host_columns_f32(const float* lam, const float* h0,
+                                          const float* h, const float* dh,
+                                          float* dlam, float* dx, float* dh0,
+                                          int64_t T, int64_t W, int64_t c0,
+                                          int64_t c1, int mode, int device);
+int linrec_scan_backward_host_columns_f64(const double* lam,
+                                          const double* h0, const double* h,
+                                          const double* dh, double* dlam,
+                                          double* dx, double* dh0, int64_t T,
+                                          int64_t W, int64_t c0, int64_t c1,
+                                          int mode, int device);
+int linrec_scan_host_multi_f32(const float* lam, const float* x,
+                               const float* h0, float* h, int64_t T, int64_t W,
+                               int mode, const int* devices, int ndev);
+int linrec_scan_host_multi_f64(const double* lam, const double* x,
+                               const double* h0, double* h, int64_t T,
+                               int64_t W, int mode, const int* devices,
+                               int ndev);
+int linrec_scan_backward_host_multi_f32(const float* lam, const float* h0,
+                                        const float* h, const float* dh,
+                                        float* dlam, float* dx, float* dh0,
+                                        int64_t T, int64_t W, int mode,
+                                        const int* devices, int ndev);
+int linrec_scan_backward_host_multi_f64(const double* lam, const double* h0,
+                                        const double* h, const double* dh,
+                                        double* dlam, double* dx, double* dh0,
+                                        int64_t T, int64_t W, int mode,
+                                        const int* devices, int ndev);
+/* Column block [c0, c1) of device d of n under channel sharding. */
+int linrec_column_block(int64_t W, int n, int d, int64_t* c0, int64_t* c1);
+
 /* Page-locked host memory from a caching allocator (blocks are recycled by
  * size; at most a quarter of RAM stays pinned while idle).  Host buffers
  * from here run the host entry points above at full link speed: the Python

@@ -99,6 +99,13 @@ def _load():
     lib.linrec_segment_prod_rows.argtypes = [_i64, _i64, _int, _int]
     lib.linrec_segment_tile_rows.restype = _i64
     lib.linrec_segment_tile_rows.argtypes = [_i64, _i64, _int, _int]
+    for s_ in ("f32", "f64"):
+        getattr(lib, f"linrec_scan_host_columns_{s_}").argtypes = [_vp] * 4 + [_i64] * 4 + [_int, _int]
+        getattr(lib, f"linrec_scan_backward_host_columns_{s_}").argtypes = [_vp] * 7 + [_i64] * 4 + [_int, _int]
+        getattr(lib, f"linrec_scan_host_multi_{s_}").argtypes = [_vp] * 4 + [_i64, _i64, _int, C.POINTER(_int), _int]
+        getattr(lib, f"linrec_scan_backward_host_multi_{s_}").argtypes = [_vp] * 7 + [_i64, _i64, _int,
+                                                                                     C.POINTER(_int), _int]
+    lib.linrec_column_block.argtypes = [_i64, _int, _int, C.POINTER(_i64), C.POINTER(_i64)]
     return lib
 
 
@@ -155,6 +162,42 @@ def scan_host(lam, x, h0, h, T, W, mode=PARALLEL, dtype_bytes=4, device=0):
 def scan_backward_host(lam, h0, h, dh, dlam, dx, dh0, T, W, mode=PARALLEL, dtype_bytes=4, device=0):
     check(getattr(lib, f"linrec_scan_backward_host_{_sfx(dtype_bytes)}")(
         lam, h0, h, dh, dlam, dx, dh0, T, W, mode, device))
+
+
+# ---- channel sharding of host arrays ----------------------------------------
+def scan_host_columns(lam, x, h0, h, T, W, c0, c1, mode=PARALLEL, dtype_bytes=4, device=0):
+    """Columns [c0, c1) of host [T][W] arrays on `device` (2-D staged copies)."""
+    check(getattr(lib, f"linrec_scan_host_columns_{_sfx(dtype_bytes)}")(lam, x, h0, h, T, W, c0, c1, mode, device))
+
+
+def scan_backward_host_columns(lam, h0, h, dh, dlam, dx, dh0, T, W, c0, c1, mode=PARALLEL, dtype_bytes=4,
+                               device=0):
+    check(getattr(lib, f"linrec_scan_backward_host_columns_{_sfx(dtype_bytes)}")(
+        lam, h0, h, dh, dlam, dx, dh0, T, W, c0, c1, mode, device))
+
+
+def _devs(devices):
+    devices = list(devices)
+    return (_int * len(devices))(*devices), len(devices)
+
+
+def scan_host_multi(lam, x, h0, h, T, W, devices, mode=PARALLEL, dtype_bytes=4):
+    """Channel-sharded scan of host [T][W] arrays over `devices` (one host thread each)."""
+    d, n = _devs(devices)
+    check(getattr(lib, f"linrec_scan_host_multi_{_sfx(dtype_bytes)}")(lam, x, h0, h, T, W, mode, d, n))
+
+
+def scan_backward_host_multi(lam, h0, h, dh, dlam, dx, dh0, T, W, devices, mode=PARALLEL, dtype_bytes=4):
+    d, n = _devs(devices)
+    check(getattr(lib, f"linrec_scan_backward_host_multi_{_sfx(dtype_bytes)}")(
+        lam, h0, h, dh, dlam, dx, dh0, T, W, mode, d, n))
+
+
+def column_block(W, n, d):
+    """Columns [c0, c1) of device d of n under channel sharding."""
+    c0, c1 = _i64(), _i64()
+    check(lib.linrec_column_block(W, n, d, C.byref(c0), C.byref(c1)))
+    return int(c0.value), int(c1.value)
 
 
 def first_nonfinite(v, n, dtype_bytes=4, stream=0) -> int:

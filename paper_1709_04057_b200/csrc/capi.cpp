@@ -485,6 +485,26 @@ int64_t chunk_rows(int64_t T, int64_t W, size_t elem) {
 
 using CopyJobs = std::vector<std::tuple<void*, const void*, size_t>>;
 
+// Host arrays may be a column block of a wider [T][ld] array (channel
+// sharding, linrec_scan_host_columns_*): rows of `width` bytes at a host
+// stride of ld_bytes.  Contiguous blocks stay one job / one copy.
+void add_rows(CopyJobs& jobs, void* dst, size_t dst_ld, const void* src, size_t src_ld, size_t width, int64_t rows) {
+  if (rows <= 0) return;
+  if (dst_ld == width && src_ld == width) {
+    jobs.emplace_back(dst, src, width * size_t(rows));
+    return;
+  }
+  for (int64_t r = 0; r < rows; ++r)
+    jobs.emplace_back(static_cast<char*>(dst) + size_t(r) * dst_ld, static_cast<const char*>(src) + size_t(r) * src_ld,
+                      width);
+}
+cudaError_t copy_rows_async(void* dst, size_t dst_ld, const void* src, size_t src_ld, size_t width, int64_t rows,
+                            cudaMemcpyKind kind, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  if (dst_ld == width && src_ld == width) return cudaMemcpyAsync(dst, src, width * size_t(rows), kind, st);
+  return cudaMemcpy2DAsync(dst, dst_ld, src, src_ld, width, size_t(rows), kind, st);
+}
+
 // Caching allocator of page-locked host memory (linrec_host_alloc/free): the
 // Python module allocates its numpy RESULTS here, so device->host copies land
 // straight in the caller's array at full link speed (no bounce, no first-touch
@@ -508,7 +528,8 @@ PinnedCache& pinned_cache() {
 
 template <class S>
 int scan_host(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W, int mode,
-              int device) {
+              int device, int64_t ld = -1) {
+  if (ld < 0) ld = W;  // host row stride (elements): > W for a column block
   int rc;
   if ((rc = check_dims(T, W)) || (rc = check_mode(mode)) || (rc = check_ptr(lam, "decays")) ||
       (rc = check_ptr(x, "impulses")) || (rc = check_ptr(h, "h")))
@@ -535,11 +556,14 @@ int scan_host(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W,
     LINREC_CUDA_TRY(cudaMemcpyAsync(d_h0, src, row, cudaMemcpyHostToDevice, hp->s_comp));
   }
   const int64_t nchunks = (T + Tc - 1) / Tc;
+  const size_t hrow = size_t(ld) * sizeof(S);  // host row stride in bytes
   auto drain = [&](int64_t k) -> int {  // chunk k's h: pinned bounce -> caller
     const int s = int(k % kSlots);
     const int64_t t0 = k * Tc, rows = std::min<int64_t>(Tc, T - t0);
     LINREC_CUDA_TRY(cudaEventSynchronize(hp->ev_out[s]));
-    hp->pool->copy(CopyJobs{{h + t0 * W, hp->bounce[s][3], size_t(rows) * row}});
+    CopyJobs jobs;
+    add_rows(jobs, h + t0 * ld, hrow, hp->bounce[s][3], row, row, rows);
+    hp->pool->copy(jobs);
     return LINREC_OK;
   };
   const S* seed = d_h0;
@@ -549,29 +573,31 @@ int scan_host(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W,
     S* dl = static_cast<S*>(hp->buf[s][0]);
     S* dxv = static_cast<S*>(hp->buf[s][1]);
     S* dhv = static_cast<S*>(hp->buf[s][2]);
-    const size_t bytes = size_t(rows) * row;
-    const S* src_l = lam + t0 * W;
-    const S* src_x = x + t0 * W;
+    const S* src_l = lam + t0 * ld;
+    const S* src_x = x + t0 * ld;
+    size_t ld_l = hrow, ld_x = hrow;
     if (st_l || st_x) {  // bounce slot s is free once chunk k - kSlots's H2D finished
       if (k >= kSlots) LINREC_CUDA_TRY(cudaEventSynchronize(hp->ev_in[s]));
       CopyJobs jobs;
-      if (st_l) jobs.emplace_back(hp->bounce[s][0], src_l, bytes);
-      if (st_x) jobs.emplace_back(hp->bounce[s][1], src_x, bytes);
+      if (st_l) add_rows(jobs, hp->bounce[s][0], row, src_l, hrow, row, rows);
+      if (st_x) add_rows(jobs, hp->bounce[s][1], row, src_x, hrow, row, rows);
       hp->pool->copy(jobs);
-      if (st_l) src_l = static_cast<const S*>(hp->bounce[s][0]);
-      if (st_x) src_x = static_cast<const S*>(hp->bounce[s][1]);
+      if (st_l) { src_l = static_cast<const S*>(hp->bounce[s][0]); ld_l = row; }
+      if (st_x) { src_x = static_cast<const S*>(hp->bounce[s][1]); ld_x = row; }
     }
     if (k >= kSlots) LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_in, hp->ev_comp[s], 0));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(dl, src_l, bytes, cudaMemcpyHostToDevice, hp->s_in));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(dxv, src_x, bytes, cudaMemcpyHostToDevice, hp->s_in));
+    LINREC_CUDA_TRY(copy_rows_async(dl, row, src_l, ld_l, row, rows, cudaMemcpyHostToDevice, hp->s_in));
+    LINREC_CUDA_TRY(copy_rows_async(dxv, row, src_x, ld_x, row, rows, cudaMemcpyHostToDevice, hp->s_in));
     LINREC_CUDA_TRY(cudaEventRecord(hp->ev_in[s], hp->s_in));
     LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_comp, hp->ev_in[s], 0));
     if (k >= kSlots) LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_comp, hp->ev_out[s], 0));
     if ((rc = scan_device<S>(dl, dxv, seed, dhv, rows, W, mode, &hp->ws, hp->s_comp))) return rc;
     LINREC_CUDA_TRY(cudaEventRecord(hp->ev_comp[s], hp->s_comp));
     LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_out, hp->ev_comp[s], 0));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(st_h ? hp->bounce[s][3] : static_cast<void*>(h + t0 * W), dhv, bytes,
-                                    cudaMemcpyDeviceToHost, hp->s_out));
+    if (st_h)
+      LINREC_CUDA_TRY(copy_rows_async(hp->bounce[s][3], row, dhv, row, row, rows, cudaMemcpyDeviceToHost, hp->s_out));
+    else
+      LINREC_CUDA_TRY(copy_rows_async(h + t0 * ld, hrow, dhv, row, row, rows, cudaMemcpyDeviceToHost, hp->s_out));
     LINREC_CUDA_TRY(cudaEventRecord(hp->ev_out[s], hp->s_out));
     seed = dhv + (rows - 1) * W;  // carry into the next chunk
     // the previous chunk's result leaves the bounce buffer while this one runs
@@ -585,7 +611,8 @@ int scan_host(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W,
 
 template <class S>
 int scan_backward_host(const S* lam, const S* h0, const S* h, const S* dh, S* dlam, S* dx, S* dh0,
-                       int64_t T, int64_t W, int mode, int device) {
+                       int64_t T, int64_t W, int mode, int device, int64_t ld = -1) {
+  if (ld < 0) ld = W;  // host row stride (elements): > W for a column block
   int rc;
   if ((rc = check_dims(T, W)) || (rc = check_mode(mode)) || (rc = check_ptr(lam, "decays")) ||
       (rc = check_ptr(h, "h")) || (rc = check_ptr(dh, "d_h")) || (rc = check_ptr(dlam, "d_decays")) ||
@@ -618,15 +645,15 @@ int scan_backward_host(const S* lam, const S* h0, const S* h, const S* dh, S* dl
     LINREC_CUDA_TRY(cudaMemsetAsync(d_h0, 0, row, hp->s_comp));
   }
   const int64_t nchunks = (T + Tc - 1) / Tc;
+  const size_t hrow = size_t(ld) * sizeof(S);  // host row stride in bytes
   auto drain = [&](int64_t i) -> int {  // chunk i's dlam, dx: pinned bounce -> caller
     const int s = int(i % kSlots);
     const int64_t k = nchunks - 1 - i;
     const int64_t t0 = k * Tc, rows = std::min<int64_t>(Tc, T - t0);
-    const size_t bytes = size_t(rows) * row;
     LINREC_CUDA_TRY(cudaEventSynchronize(hp->ev_out[s]));
     CopyJobs jobs;
-    if (st_dl) jobs.emplace_back(dlam + t0 * W, hp->bounce[s][3], bytes);
-    if (st_dx) jobs.emplace_back(dx + t0 * W, hp->bounce[s][4], bytes);
+    if (st_dl) add_rows(jobs, dlam + t0 * ld, hrow, hp->bounce[s][3], row, row, rows);
+    if (st_dx) add_rows(jobs, dx + t0 * ld, hrow, hp->bounce[s][4], row, row, rows);
     hp->pool->copy(jobs);
     return LINREC_OK;
   };
@@ -637,7 +664,6 @@ int scan_backward_host(const S* lam, const S* h0, const S* h, const S* dh, S* dl
     const int64_t k = nchunks - 1 - i;  // reverse time
     const int s = int(i % kSlots);
     const int64_t t0 = k * Tc, rows = std::min<int64_t>(Tc, T - t0);
-    const size_t bytes = size_t(rows) * row;
     S* b0 = static_cast<S*>(hp->buf[s][0]);
     S* b1 = static_cast<S*>(hp->buf[s][1]);
     S* b2 = static_cast<S*>(hp->buf[s][2]);
@@ -647,35 +673,35 @@ int scan_backward_host(const S* lam, const S* h0, const S* h, const S* dh, S* dl
     S* d_dx = b1 + Tc * W;
     S* d_dh = b2;
     // host sources of this chunk: lam and dh rows, and h shifted by one row
-    const S* src_l = lam + t0 * W;
-    const S* src_dh = dh + t0 * W;
-    const S* src_h = t0 > 0 ? h + (t0 - 1) * W : h;
-    const size_t h_bytes = t0 > 0 ? bytes : bytes - row;
+    const S* src_l = lam + t0 * ld;
+    const S* src_dh = dh + t0 * ld;
+    const S* src_h = t0 > 0 ? h + (t0 - 1) * ld : h;
+    const int64_t h_rows = t0 > 0 ? rows : rows - 1;
+    size_t ld_l = hrow, ld_h = hrow, ld_dh = hrow;
     if (st_l || st_h || st_dh) {
       if (i >= kSlots) LINREC_CUDA_TRY(cudaEventSynchronize(hp->ev_in[s]));
       CopyJobs jobs;
-      if (st_l) jobs.emplace_back(hp->bounce[s][0], src_l, bytes);
-      if (st_h) jobs.emplace_back(hp->bounce[s][1], src_h, h_bytes);
-      if (st_dh) jobs.emplace_back(hp->bounce[s][2], src_dh, bytes);
+      if (st_l) add_rows(jobs, hp->bounce[s][0], row, src_l, hrow, row, rows);
+      if (st_h) add_rows(jobs, hp->bounce[s][1], row, src_h, hrow, row, h_rows);
+      if (st_dh) add_rows(jobs, hp->bounce[s][2], row, src_dh, hrow, row, rows);
       hp->pool->copy(jobs);
-      if (st_l) src_l = static_cast<const S*>(hp->bounce[s][0]);
-      if (st_h) src_h = static_cast<const S*>(hp->bounce[s][1]);
-      if (st_dh) src_dh = static_cast<const S*>(hp->bounce[s][2]);
+      if (st_l) { src_l = static_cast<const S*>(hp->bounce[s][0]); ld_l = row; }
+      if (st_h) { src_h = static_cast<const S*>(hp->bounce[s][1]); ld_h = row; }
+      if (st_dh) { src_dh = static_cast<const S*>(hp->bounce[s][2]); ld_dh = row; }
     }
     // slot s was last filled at chunk i-3, whose lam row 0 and G row 0 are
     // also read by chunk i-2 (lam_next / g_next): wait for that compute.
     if (i >= kSlots)
       LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_in, hp->ev_comp[(i - 2) % kSlots], 0));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(d_lam, src_l, bytes, cudaMemcpyHostToDevice, hp->s_in));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(d_dh, src_dh, bytes, cudaMemcpyHostToDevice, hp->s_in));
+    LINREC_CUDA_TRY(copy_rows_async(d_lam, row, src_l, ld_l, row, rows, cudaMemcpyHostToDevice, hp->s_in));
+    LINREC_CUDA_TRY(copy_rows_async(d_dh, row, src_dh, ld_dh, row, rows, cudaMemcpyHostToDevice, hp->s_in));
     const S* hprev_row;
     const S* hrows;
+    LINREC_CUDA_TRY(copy_rows_async(d_h, row, src_h, ld_h, row, h_rows, cudaMemcpyHostToDevice, hp->s_in));
     if (t0 > 0) {
-      LINREC_CUDA_TRY(cudaMemcpyAsync(d_h, src_h, h_bytes, cudaMemcpyHostToDevice, hp->s_in));
       hprev_row = d_h;
       hrows = d_h + W;
     } else {
-      if (rows > 1) LINREC_CUDA_TRY(cudaMemcpyAsync(d_h, src_h, h_bytes, cudaMemcpyHostToDevice, hp->s_in));
       hprev_row = d_h0;
       hrows = d_h;
     }
@@ -687,10 +713,14 @@ int scan_backward_host(const S* lam, const S* h0, const S* h, const S* dh, S* dl
       return rc;
     LINREC_CUDA_TRY(cudaEventRecord(hp->ev_comp[s], hp->s_comp));
     LINREC_CUDA_TRY(cudaStreamWaitEvent(hp->s_out, hp->ev_comp[s], 0));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(st_dl ? hp->bounce[s][3] : static_cast<void*>(dlam + t0 * W), d_dlam, bytes,
-                                    cudaMemcpyDeviceToHost, hp->s_out));
-    LINREC_CUDA_TRY(cudaMemcpyAsync(st_dx ? hp->bounce[s][4] : static_cast<void*>(dx + t0 * W), d_dx, bytes,
-                                    cudaMemcpyDeviceToHost, hp->s_out));
+    if (st_dl)
+      LINREC_CUDA_TRY(copy_rows_async(hp->bounce[s][3], row, d_dlam, row, row, rows, cudaMemcpyDeviceToHost, hp->s_out));
+    else
+      LINREC_CUDA_TRY(copy_rows_async(dlam + t0 * ld, hrow, d_dlam, row, row, rows, cudaMemcpyDeviceToHost, hp->s_out));
+    if (st_dx)
+      LINREC_CUDA_TRY(copy_rows_async(hp->bounce[s][4], row, d_dx, row, row, rows, cudaMemcpyDeviceToHost, hp->s_out));
+    else
+      LINREC_CUDA_TRY(copy_rows_async(dx + t0 * ld, hrow, d_dx, row, row, rows, cudaMemcpyDeviceToHost, hp->s_out));
     if (k == 0) LINREC_CUDA_TRY(cudaMemcpyAsync(h_dh0, d_dh0, row, cudaMemcpyDeviceToHost, hp->s_out));
     LINREC_CUDA_TRY(cudaEventRecord(hp->ev_out[s], hp->s_out));
     lam_next = d_lam;  // lam at row t0 and G at row t0 feed the previous chunk
@@ -923,6 +953,97 @@ int screen_finite(const S* v, int64_t T, int64_t batch, int64_t features, const 
 // ---------------------------------------------------------------------------
 // exported symbols
 // ---------------------------------------------------------------------------
+namespace {
+// ---- channel sharding of host arrays -------------------------
+// Columns [c0, c1) of host [T][W] arrays: staged with strided (2-D) copies,
+// scanned on one device as a contiguous [T][c1-c0] block, written back into
+// the same columns.  Channels are independent (recurrence.hpp:109), so the
+// block's results are exactly the full scan's columns.
+int check_columns(int64_t W, int64_t c0, int64_t c1) {
+  if (c0 < 0 || c1 > W || c0 >= c1) return fail(LINREC_ERR_VALUE, "columns: need 0 <= c0 < c1 <= W");
+  return LINREC_OK;
+}
+
+template <class S>
+int scan_host_columns(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W, int64_t c0, int64_t c1,
+                      int mode, int device) {
+  int rc;
+  if ((rc = check_dims(T, W)) || (rc = check_columns(W, c0, c1)) || (rc = check_ptr(lam, "decays")) ||
+      (rc = check_ptr(x, "impulses")) || (rc = check_ptr(h, "h")))
+    return rc;
+  return scan_host<S>(lam + c0, x + c0, h0 ? h0 + c0 : nullptr, h + c0, T, c1 - c0, mode, device, W);
+}
+
+template <class S>
+int scan_backward_host_columns(const S* lam, const S* h0, const S* h, const S* dh, S* dlam, S* dx, S* dh0,
+                               int64_t T, int64_t W, int64_t c0, int64_t c1, int mode, int device) {
+  int rc;
+  if ((rc = check_dims(T, W)) || (rc = check_columns(W, c0, c1)) || (rc = check_ptr(lam, "decays")) ||
+      (rc = check_ptr(h, "h")) || (rc = check_ptr(dh, "d_h")) || (rc = check_ptr(dlam, "d_decays")) ||
+      (rc = check_ptr(dx, "d_impulses")) || (rc = check_ptr(dh0, "d_initial")))
+    return rc;
+  return scan_backward_host<S>(lam + c0, h0 ? h0 + c0 : nullptr, h + c0, dh + c0, dlam + c0, dx + c0, dh0 + c0,
+                               T, c1 - c0, mode, device, W);
+}
+
+// Column block of device d of n: contiguous, sizes in multiples of 4 channels
+// where W allows (16-byte rows for the vector kernels), longer blocks first.
+void column_block(int64_t W, int n, int d, int64_t* c0, int64_t* c1) {
+  const int64_t unit = W % 4 == 0 ? 4 : 1, units = W / unit;
+  const int64_t base = units / n, rem = units % n;
+  *c0 = unit * (d * base + std::min<int64_t>(d, rem));
+  *c1 = *c0 + unit * (base + (d < rem ? 1 : 0));
+}
+
+// One host thread per device, each running the host pipeline on its column
+// block (its own streams, bounce buffers and copy threads); the first error
+// (code and message) is returned on the calling thread.
+template <class F>
+int run_on_devices(int64_t W, const int* devices, int ndev, F&& per_device) {
+  if (!devices || ndev < 1) return fail(LINREC_ERR_VALUE, "devices: need ndev >= 1 device ids");
+  int count = 0;
+  LINREC_CUDA_TRY(cudaGetDeviceCount(&count));
+  for (int i = 0; i < ndev; ++i)
+    if (devices[i] < 0 || devices[i] >= count) return fail(LINREC_ERR_VALUE, "devices: id out of range");
+  const int n = int(std::min<int64_t>(ndev, W));
+  std::vector<int> rcs(n, LINREC_OK);
+  std::vector<std::string> msgs(n);
+  std::vector<std::thread> th;
+  for (int d = 0; d < n; ++d)
+    th.emplace_back([&, d] {
+      int64_t c0, c1;
+      column_block(W, n, d, &c0, &c1);
+      if (c0 < c1) rcs[d] = per_device(devices[d], c0, c1);
+      if (rcs[d] != LINREC_OK) msgs[d] = g_last_error;
+    });
+  for (auto& t : th) t.join();
+  for (int d = 0; d < n; ++d)
+    if (rcs[d] != LINREC_OK) return fail(rcs[d], msgs[d]);
+  return LINREC_OK;
+}
+
+template <class S>
+int scan_host_multi(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W, int mode,
+                    const int* devices, int ndev) {
+  int rc;
+  if ((rc = check_dims(T, W)) || (rc = check_mode(mode))) return rc;
+  return run_on_devices(W, devices, ndev, [&](int dev, int64_t c0, int64_t c1) {
+    return scan_host_columns<S>(lam, x, h0, h, T, W, c0, c1, mode, dev);
+  });
+}
+
+template <class S>
+int scan_backward_host_multi(const S* lam, const S* h0, const S* h, const S* dh, S* dlam, S* dx, S* dh0,
+                             int64_t T, int64_t W, int mode, const int* devices, int ndev) {
+  int rc;
+  if ((rc = check_dims(T, W)) || (rc = check_mode(mode))) return rc;
+  return run_on_devices(W, devices, ndev, [&](int dev, int64_t c0, int64_t c1) {
+    return scan_backward_host_columns<S>(lam, h0, h, dh, dlam, dx, dh0, T, W, c0, c1, mode, dev);
+  });
+}
+
+}  // namespace
+
 extern "C" {
 
 int linrec_abi_version(void) { return LINREC_ABI_VERSION; }
@@ -1050,6 +1171,48 @@ int linrec_scan_backward_host_f64(const double* lam, const double* h0, const dou
                                   const double* dh, double* dlam, double* dx, double* dh0,
                                   int64_t T, int64_t W, int mode, int device) {
   return scan_backward_host<double>(lam, h0, h, dh, dlam, dx, dh0, T, W, mode, device);
+}
+
+int linrec_scan_host_columns_f32(const float* lam, const float* x, const float* h0, float* h, int64_t T,
+                                 int64_t W, int64_t c0, int64_t c1, int mode, int device) {
+  return scan_host_columns<float>(lam, x, h0, h, T, W, c0, c1, mode, device);
+}
+int linrec_scan_host_columns_f64(const double* lam, const double* x, const double* h0, double* h, int64_t T,
+                                 int64_t W, int64_t c0, int64_t c1, int mode, int device) {
+  return scan_host_columns<double>(lam, x, h0, h, T, W, c0, c1, mode, device);
+}
+int linrec_scan_backward_host_columns_f32(const float* lam, const float* h0, const float* h, const float* dh,
+                                          float* dlam, float* dx, float* dh0, int64_t T, int64_t W, int64_t c0,
+                                          int64_t c1, int mode, int device) {
+  return scan_backward_host_columns<float>(lam, h0, h, dh, dlam, dx, dh0, T, W, c0, c1, mode, device);
+}
+int linrec_scan_backward_host_columns_f64(const double* lam, const double* h0, const double* h, const double* dh,
+                                          double* dlam, double* dx, double* dh0, int64_t T, int64_t W, int64_t c0,
+                                          int64_t c1, int mode, int device) {
+  return scan_backward_host_columns<double>(lam, h0, h, dh, dlam, dx, dh0, T, W, c0, c1, mode, device);
+}
+int linrec_scan_host_multi_f32(const float* lam, const float* x, const float* h0, float* h, int64_t T, int64_t W,
+                               int mode, const int* devices, int ndev) {
+  return scan_host_multi<float>(lam, x, h0, h, T, W, mode, devices, ndev);
+}
+int linrec_scan_host_multi_f64(const double* lam, const double* x, const double* h0, double* h, int64_t T,
+                               int64_t W, int mode, const int* devices, int ndev) {
+  return scan_host_multi<double>(lam, x, h0, h, T, W, mode, devices, ndev);
+}
+int linrec_scan_backward_host_multi_f32(const float* lam, const float* h0, const float* h, const float* dh,
+                                        float* dlam, float* dx, float* dh0, int64_t T, int64_t W, int mode,
+                                        const int* devices, int ndev) {
+  return scan_backward_host_multi<float>(lam, h0, h, dh, dlam, dx, dh0, T, W, mode, devices, ndev);
+}
+int linrec_scan_backward_host_multi_f64(const double* lam, const double* h0, const double* h, const double* dh,
+                                        double* dlam, double* dx, double* dh0, int64_t T, int64_t W, int mode,
+                                        const int* devices, int ndev) {
+  return scan_backward_host_multi<double>(lam, h0, h, dh, dlam, dx, dh0, T, W, mode, devices, ndev);
+}
+int linrec_column_block(int64_t W, int n, int d, int64_t* c0, int64_t* c1) {
+  if (n < 1 || d < 0 || d >= n || !c0 || !c1) return fail(LINREC_ERR_VALUE, "column_block: need 0 <= d < n");
+  column_block(W, n, d, c0, c1);
+  return LINREC_OK;
 }
 
 int linrec_host_alloc(void** ptr, size_t bytes) {

@@ -46,8 +46,141 @@ def segment_rows(T: int, world: int, rank: int) -> int:
 
 
 def channel_shard(W: int, world: int, rank: int):
-    """Channels [start, end) owned by rank under channel sharding."""
-    return segment_bounds(W, world, rank)
+    """Channels [start, end) owned by rank under channel sharding: contiguous
+    blocks, multiples of 4 channels when W allows (16-byte rows for the
+    vector kernels), longer blocks first (linrec_column_block)."""
+    unit = 4 if W % 4 == 0 else 1
+    s, e = segment_bounds(W // unit, world, rank)
+    return s * unit, e * unit
+
+
+def _host_arrays(*arrays):
+    import numpy as np
+    out = []
+    dt = None
+    for a in arrays:
+        if a is None:
+            out.append(None)
+            continue
+        a = np.ascontiguousarray(a)
+        if dt is None:
+            dt = a.dtype
+            if dt not in (np.float32, np.float64):
+                raise TypeError("decays must be float32 or float64")
+        elif a.dtype != dt:
+            raise TypeError("all arrays must share the decays dtype")
+        out.append(a)
+    return out, dt
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def _mode(mode):
+    if mode not in ("parallel", "serial"):
+        raise ValueError(f"unknown mode '{mode}' (expected 'serial' or 'parallel')")
+    return capi.SERIAL if mode == "serial" else capi.PARALLEL
+
+
+def channel_sharded_scan(decays, impulses, initial=None, *, devices=None, mode="parallel"):
+    """scan (recurrence.hpp:255-263) of host [T, b, n] arrays with the channels
+    split over `devices` (default: every visible GPU) -- one host thread per
+    GPU, each staging its column block with 2-D copies; no communication
+    (channels are independent, recurrence.hpp:109).  numpy in, numpy out."""
+    import numpy as np
+    (lam, x, h0), dt = _host_arrays(decays, impulses, initial)
+    if lam.ndim != 3:
+        raise ValueError("decays must have shape [T, batch, features]")
+    if lam.shape != x.shape:
+        raise RuntimeError(f"recurrence: shape mismatch, {list(lam.shape)} vs {list(x.shape)}")
+    if h0 is not None and h0.shape != lam.shape[1:]:
+        raise RuntimeError(f"recurrence: initial state {list(h0.shape)} does not match {list(lam.shape[1:])}")
+    T, W = lam.shape[0], lam.shape[1] * lam.shape[2]
+    devices = list(range(torch.cuda.device_count())) if devices is None else list(devices)
+    h = np.empty_like(lam)
+    capi.scan_host_multi(_ptr(lam), _ptr(x), _ptr(h0), _ptr(h), T, W, devices, _mode(mode), dt.itemsize)
+    return h
+
+
+def channel_sharded_scan_backward(decays, initial, h, d_h, *, devices=None, mode="parallel"):
+    """scan_backward (recurrence.hpp:352-363) of host arrays, channels split
+    over `devices` like channel_sharded_scan: (d_decays, d_impulses, d_initial)."""
+    import numpy as np
+    (lam, h0, hh, dh), dt = _host_arrays(decays, initial, h, d_h)
+    if lam.ndim != 3:
+        raise ValueError("decays must have shape [T, batch, features]")
+    for a, n in ((hh, "h"), (dh, "d_h")):
+        if a.shape != lam.shape:
+            raise RuntimeError(f"scan_backward({n}): shape mismatch, {list(lam.shape)} vs {list(a.shape)}")
+    if h0 is not None and h0.shape != lam.shape[1:]:
+        raise RuntimeError(f"recurrence: initial state {list(h0.shape)} does not match {list(lam.shape[1:])}")
+    T, W = lam.shape[0], lam.shape[1] * lam.shape[2]
+    devices = list(range(torch.cuda.device_count())) if devices is None else list(devices)
+    dlam, dx = np.empty_like(lam), np.empty_like(lam)
+    dh0 = np.empty(lam.shape[1:], dtype=dt)
+    capi.scan_backward_host_multi(_ptr(lam), _ptr(h0), _ptr(hh), _ptr(dh), _ptr(dlam), _ptr(dx), _ptr(dh0), T, W,
+                                  devices, _mode(mode), dt.itemsize)
+    return dlam, dx, dh0
+
+
+class ChannelShardedScan:
+    """One process per GPU: rank r scans its channel block (channel_shard) of
+    the caller's full host arrays on its own device and writes those columns
+    of the outputs; `gather=True` all-gathers the other ranks' columns over
+    the process group (host tensors), so every rank ends with the full
+    result.  No collective on the data path otherwise."""
+
+    def __init__(self, group=None, device=None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.device = torch.cuda.current_device() if device is None else device
+
+    def columns(self, W):
+        return channel_shard(W, self.world, self.rank)
+
+    def _gather(self, arr, W):
+        if self.world == 1:
+            return
+        import numpy as np
+        T = arr.shape[0]
+        flat = arr.reshape(T, W)
+        blocks = [channel_shard(W, self.world, q) for q in range(self.world)]
+        mine = torch.from_numpy(np.ascontiguousarray(flat[:, blocks[self.rank][0]:blocks[self.rank][1]]))
+        parts = [torch.empty(T, e - s, dtype=mine.dtype) for s, e in blocks]
+        dist.all_gather(parts, mine, group=self.group)
+        for (s, e), part in zip(blocks, parts):
+            flat[:, s:e] = part.numpy()
+
+    def scan(self, decays, impulses, initial=None, *, mode="parallel", gather=False):
+        import numpy as np
+        (lam, x, h0), dt = _host_arrays(decays, impulses, initial)
+        T, W = lam.shape[0], lam.shape[1] * lam.shape[2]
+        c0, c1 = self.columns(W)
+        h = np.zeros_like(lam)
+        if c0 < c1:
+            capi.scan_host_columns(_ptr(lam), _ptr(x), _ptr(h0), _ptr(h), T, W, c0, c1, _mode(mode), dt.itemsize,
+                                   self.device)
+        if gather:
+            self._gather(h, W)
+        return h
+
+    def scan_backward(self, decays, initial, h, d_h, *, mode="parallel", gather=False):
+        import numpy as np
+        (lam, h0, hh, dh), dt = _host_arrays(decays, initial, h, d_h)
+        T, W = lam.shape[0], lam.shape[1] * lam.shape[2]
+        c0, c1 = self.columns(W)
+        dlam, dx = np.zeros_like(lam), np.zeros_like(lam)
+        dh0 = np.zeros(lam.shape[1:], dtype=dt)
+        if c0 < c1:
+            capi.scan_backward_host_columns(_ptr(lam), _ptr(h0), _ptr(hh), _ptr(dh), _ptr(dlam), _ptr(dx),
+                                            _ptr(dh0), T, W, c0, c1, _mode(mode), dt.itemsize, self.device)
+        if gather:
+            for a in (dlam, dx):
+                self._gather(a, W)
+            self._gather(dh0.reshape(1, -1), W)
+        return dlam, dx, dh0
 
 
 class CudaBackend:

@@ -79,6 +79,38 @@ for _ in range(reps):
     gtf += e3[0].elapsed_time(e3[1])
     gtb += e3[1].elapsed_time(e3[2])
 print(f"N={N} graph-replayed: fwd {gtf / reps * 1e3:.1f} us  bwd {gtb / reps * 1e3:.1f} us", flush=True)
+# per kernel (each launch its own graph, replayed back to back in step order)
+parts = {
+    "fwd scan": lambda: capi.segment_scan(p(lam), p(x), None, p(h), p(spf), p(agg), Tl, W, 4, ws.handle, st),
+    "fwd compose": lambda: capi.compose_carries(p(aggs), 0, 1, 1, None, p(c_in), W, 4, st),
+    "fwd fixup": lambda: capi.segment_fixup(p(lam), p(h), p(spf), p(c_in), Tl, W, rf, 4, st),
+    "bwd scan": lambda: capi.segment_scan_backward(p(lam), p(hprev), p(h), p(dh), p(ones), p(dlam), p(dx), p(dh0),
+                                                   p(spb), p(agg), Tl, W, 4, ws.handle, st),
+    "bwd compose": lambda: capi.compose_carries(p(aggs), N - 1, 1, -1, None, p(y_in), W, 4, st),
+    "bwd fixup": lambda: capi.segment_fixup_backward(p(lam), p(hprev), p(h), p(ones), p(spb), p(y_in), p(dlam),
+                                                     p(dx), Tl, W, rb, 4, st),
+}
+graphs = {}
+with torch.cuda.stream(s2):
+    st = s2.cuda_stream
+    for name, fn in parts.items():
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s2):
+            fn()
+        graphs[name] = g
+torch.cuda.synchronize()
+st = st_saved
+evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(parts) + 1)]
+acc = dict.fromkeys(parts, 0.0)
+for _ in range(reps):
+    evs[0].record()
+    for i, name in enumerate(parts):
+        graphs[name].replay()
+        evs[i + 1].record()
+    torch.cuda.synchronize()
+    for i, name in enumerate(parts):
+        acc[name] += evs[i].elapsed_time(evs[i + 1])
+print("  per kernel: " + ", ".join(f"{k} {v / reps * 1e3:.1f}" for k, v in acc.items()) + " us", flush=True)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 tf = tb = 0.0
 for _ in range(reps):

@@ -19,6 +19,7 @@
 
 #include "linrec/cuda_layers.hpp"
 #include "linrec/cuda_scan.hpp"
+#include "linrec/cuda_sharded.hpp"
 
 using namespace linrec::cuda;
 
@@ -322,6 +323,49 @@ static void test_check_finite() {
   CHECK(!threw, "finite backward inputs threw");
 }
 
+// Channel sharding of host tensors (cuda_sharded.hpp): the columns split over
+// two "devices" (device 0 twice on a one-GPU box: two host threads, each its
+// own column block) must reproduce the single-GPU serial scan bit for bit.
+static void test_channel_sharded() {
+  const index_t T = 2500, b = 3, n = 68, W = b * n;
+  auto lam = uniform(T * W, 0.05f, 0.95f, 11), x = uniform(T * W, -1, 1, 12), h0 = uniform(W, -1, 1, 13);
+  auto dh = uniform(T * W, -1, 1, 14);
+  std::vector<float> h(T * W), hs(T * W), dl(T * W), dx(T * W), dh0(W);
+  HostTensor3<float> L{lam.data(), T, b, n}, X{x.data(), T, b, n}, H{h.data(), T, b, n}, Hs{hs.data(), T, b, n};
+  const std::vector<int> devs{0, 0};
+  scan_channel_sharded(L, X, h0.data(), Hs, devs, ScanMode::Serial);
+  scan_channel_sharded(L, X, h0.data(), H, devs);
+  std::vector<float> ref(T * W);
+  for (index_t j = 0; j < W; ++j) {
+    float prev = h0[j];
+    for (index_t t = 0; t < T; ++t) ref[t * W + j] = prev = std::fmaf(lam[t * W + j], prev, x[t * W + j]);
+  }
+  CHECK(hs == ref, "channel-sharded serial scan is not bit-identical to the serial loop");
+  CHECK(normwise_f(h, ref) < 1e-5, "channel-sharded parallel scan error %g", normwise_f(h, ref));
+  HostTensor3<float> DHt{dh.data(), T, b, n}, DL{dl.data(), T, b, n}, DX{dx.data(), T, b, n};
+  scan_backward_channel_sharded(L, h0.data(), Hs, DHt, DL, DX, dh0.data(), devs, ScanMode::Serial);
+  std::vector<float> rdx(T * W), rdl(T * W), rdh0(W);
+  for (index_t j = 0; j < W; ++j) {
+    float G = 0.f;
+    for (index_t t = T - 1; t >= 0; --t) {
+      const float mu = t + 1 < T ? lam[(t + 1) * W + j] : 0.f;
+      G = std::fmaf(mu, G, dh[t * W + j]);
+      rdx[t * W + j] = G;
+      rdl[t * W + j] = (t == 0 ? h0[j] : ref[(t - 1) * W + j]) * G;
+    }
+    rdh0[j] = lam[j] * G;
+  }
+  CHECK(dx == rdx && dl == rdl && dh0 == rdh0, "channel-sharded serial backward is not bit-identical");
+  bool threw = false;
+  try {
+    HostTensor3<float> bad{x.data(), T - 1, b, n};
+    scan_channel_sharded(L, bad, h0.data(), H, devs);
+  } catch (const ContractViolation& e) {
+    threw = std::string(e.what()).find("recurrence: shape mismatch") != std::string::npos;
+  }
+  CHECK(threw, "shape mismatch did not throw the reference's ContractViolation");
+}
+
 int main() {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -333,6 +377,7 @@ int main() {
   test_check_finite();
   test_gilr_lstm();
   test_qrnn();
+  test_channel_sharded();
   if (failures == 0) std::printf("ALL OK\n");
   return failures == 0 ? 0 : 1;
 }

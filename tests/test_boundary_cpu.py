@@ -155,3 +155,20 @@ def test_bench_host_inputs_shard_independent():
         assert np.array_equal(np.concatenate(parts), full)
     lam, x, h0, dh = bench.host_problem(64, 1, 4, 3)
     assert h0.shape == (1, 4) and lam.shape == x.shape == dh.shape == (64, 1, 4)
+
+
+def test_column_blocks_partition_channels():
+    """Channel sharding's column blocks (linrec_column_block, no GPU needed):
+    contiguous, covering [0, W), multiples of 4 channels when W allows, longer
+    first -- and the same as sharded.channel_shard."""
+    from paper_1709_04057_b200 import capi, sharded
+    for W in (1, 7, 128, 130, 8192, 65536):
+        for n in (1, 2, 3, 8):
+            blocks = [capi.column_block(W, n, d) for d in range(n)]
+            assert blocks == [sharded.channel_shard(W, n, d) for d in range(n)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == W
+            assert all(a[1] == b[0] for a, b in zip(blocks, blocks[1:]))
+            sizes = [e - s for s, e in blocks]
+            assert sizes == sorted(sizes, reverse=True)
+            if W % 4 == 0:
+                assert all(s % 4 == 0 for s in sizes)
