@@ -367,8 +367,16 @@ class DeviceProblem:
             setattr(self, k, None)
 
 
-def single_gpu_steps(P, ws, st):
+def single_gpu_steps(P, ws, stream):
+    """fwd / bwd of one step, each captured once into a CUDA graph and replayed
+    (no host launch gaps between steps: the small workloads -- C1 is ~20 us
+    per direction -- would otherwise time Python + ctypes overhead).  The
+    workspace's control block is device-resident, so replays are exact
+    re-launches (tests/test_gpu_parity.py::test_workspace_reuse_and_cuda_graph_replay).
+    The eager callables are kept as .eager for the kernel count."""
+    import torch
     from paper_1709_04057_b200 import capi
+    st = stream.cuda_stream
 
     def fwd():
         capi.scan(P.lam.data_ptr(), P.x.data_ptr(), P.h0.data_ptr(), P.h.data_ptr(), P.Tl, P.W,
@@ -378,7 +386,27 @@ def single_gpu_steps(P, ws, st):
         capi.scan_backward(P.lam.data_ptr(), P.h0.data_ptr(), P.h.data_ptr(), P.dh.data_ptr(),
                            P.dlam.data_ptr(), P.dx.data_ptr(), P.dh0.data_ptr(), P.Tl, P.W,
                            capi.PARALLEL, 4, ws.handle, st)
-    return fwd, bwd
+    fwd(), bwd()  # workspace sized before capture
+    stream.synchronize()
+    gf, gb = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gf, stream=stream):
+        fwd()
+    with torch.cuda.graph(gb, stream=stream):
+        bwd()
+    return _Replay(gf, fwd, stream), _Replay(gb, bwd, stream)
+
+
+class _Replay:
+    """A captured graph replayed on the bench stream (CUDAGraph.replay
+    launches on the CURRENT stream)."""
+
+    def __init__(self, graph, eager, stream):
+        self.graph, self.eager, self.stream = graph, eager, stream
+
+    def __call__(self):
+        import torch
+        with torch.cuda.stream(self.stream):
+            self.graph.replay()
 
 
 def sharded_steps(rk, P, T, ws, stream):
@@ -445,7 +473,7 @@ def run_problem(rk, P, T, args, stream, ws, sharded_run, steps=None, count=False
     if sharded_run:
         fwd, bwd, runner = sharded_steps(rk, P, T, ws, stream)
     else:
-        fwd, bwd = single_gpu_steps(P, ws, st)
+        fwd, bwd = single_gpu_steps(P, ws, stream)
     for _ in range(args.warmup):
         fwd()
         bwd()
@@ -455,7 +483,7 @@ def run_problem(rk, P, T, args, stream, ws, sharded_run, steps=None, count=False
     rec = time_steps(rk, fwd, bwd, steps or args.steps, stream)
     rec["guard_max_rel_err"] = g
     if count:
-        n = count_our_kernels(lambda: (fwd(), bwd()))
+        n = count_our_kernels(lambda: (getattr(fwd, "eager", fwd)(), getattr(bwd, "eager", bwd)()))
         rec["launches_per_step"] = n
     if runner is not None:
         rec["exchange"] = runner.exchange
@@ -554,6 +582,8 @@ def run_ours(args):
                 else ("single GPU" if world == 1 else
                       "channel-sharded x%d (every rank an independent [T, B*D] block, no collective)" % world),
                 "l2": "no flush: every tensor is %.0f MiB per GPU >> 126 MB L2" % (N_local * 4 / 2**20),
+                "launch": "single GPU: fwd and bwd each one CUDA graph (captured once, replayed every step); "
+                          "sequence-sharded: eager (the exchange's epochs advance per step)",
                 "timing": "CUDA events on the launching stream, barrier + synchronize around exactly `steps` "
                           "steps, max over ranks; value = elements / (total / steps)",
                 "guard_max_rel_err": rec["guard_max_rel_err"],

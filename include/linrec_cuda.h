@@ -220,6 +220,11 @@ int linrec_scan_backward_host_multi_f64(const double* lam, const double* h0,
                                         double* dlam, double* dx, double* dh0,
                                         int64_t T, int64_t W, int mode,
                                         const int* devices, int ndev);
+/* FNV-1a 64-bit hash of host bytes, continuing from h (start: 0xcbf29ce484222325):
+ * the input checksum of the reference's bench_kernel protocol
+ * (bench.hpp:69-85 fnv1a64 / checksum_inputs), so a GPU bench row can be
+ * matched to the reference's row on identical inputs. */
+uint64_t linrec_fnv1a64(const void* data, size_t len, uint64_t h);
 /* Column block [c0, c1) of device d of n under channel sharding. */
 int linrec_column_block(int64_t W, int n, int d, int64_t* c0, int64_t* c1);
 

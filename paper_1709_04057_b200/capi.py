@@ -106,6 +106,8 @@ def _load():
         getattr(lib, f"linrec_scan_backward_host_multi_{s_}").argtypes = [_vp] * 7 + [_i64, _i64, _int,
                                                                                      C.POINTER(_int), _int]
     lib.linrec_column_block.argtypes = [_i64, _int, _int, C.POINTER(_i64), C.POINTER(_i64)]
+    lib.linrec_fnv1a64.restype = C.c_uint64
+    lib.linrec_fnv1a64.argtypes = [_vp, C.c_size_t, C.c_uint64]
     return lib
 
 
@@ -191,6 +193,16 @@ def scan_backward_host_multi(lam, h0, h, dh, dlam, dx, dh0, T, W, devices, mode=
     d, n = _devs(devices)
     check(getattr(lib, f"linrec_scan_backward_host_multi_{_sfx(dtype_bytes)}")(
         lam, h0, h, dh, dlam, dx, dh0, T, W, mode, d, n))
+
+
+FNV_OFFSET = 0xCBF29CE484222325
+
+
+def fnv1a64(*arrays, h=FNV_OFFSET) -> int:
+    """checksum_inputs (bench.hpp:69-85): FNV-1a 64 over the arrays' bytes in order."""
+    for a in arrays:
+        h = int(lib.linrec_fnv1a64(a.ctypes.data, a.nbytes, h))
+    return h
 
 
 def column_block(W, n, d):

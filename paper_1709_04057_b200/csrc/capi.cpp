@@ -223,6 +223,10 @@ int scan_device(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t 
     LINREC_CUDA_TRY(linrec_impl::launch_serial_fwd<S>(c, vok, st));
     return LINREC_OK;
   }
+  if (linrec_impl::local_scan_ok<S>(T, W, vok)) {  // short sequence: one CTA per channel vector
+    LINREC_CUDA_TRY(linrec_impl::launch_local_fwd<S>(c, vok, st));
+    return LINREC_OK;
+  }
   int dev;
   if ((rc = check_rows(T)) || (rc = current_device(&dev))) return rc;
   linrec_workspace* w = ws ? ws : default_ws(dev, st);
@@ -260,6 +264,10 @@ int scan_backward_device(const S* lam, const S* h0, const S* h, const S* dh, con
   BwdCall<S> c{lam, h0, h, dh, lam_next, g_next, dlam, dx, dh0, T, W};
   if (mode == LINREC_SERIAL || channel_parallel_enough<S>(T, W, vok)) {
     LINREC_CUDA_TRY(linrec_impl::launch_serial_bwd<S>(c, vok, st));
+    return LINREC_OK;
+  }
+  if (linrec_impl::local_scan_ok<S>(T, W, vok)) {
+    LINREC_CUDA_TRY(linrec_impl::launch_local_bwd<S>(c, vok, st));
     return LINREC_OK;
   }
   int dev;
@@ -1213,6 +1221,15 @@ int linrec_column_block(int64_t W, int n, int d, int64_t* c0, int64_t* c1) {
   if (n < 1 || d < 0 || d >= n || !c0 || !c1) return fail(LINREC_ERR_VALUE, "column_block: need 0 <= d < n");
   column_block(W, n, d, c0, c1);
   return LINREC_OK;
+}
+
+uint64_t linrec_fnv1a64(const void* data, size_t len, uint64_t h) {
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < len; ++i) {
+    h ^= p[i];
+    h *= 0x100000001b3ull;
+  }
+  return h;
 }
 
 int linrec_host_alloc(void** ptr, size_t bytes) {

@@ -126,6 +126,14 @@ cudaError_t launch_tma_bwd(const ChainPlan& p, const BwdCall<S>& c, const ChainP
 
 cudaError_t launch_ws_init(void* ctrl, cudaStream_t st);
 
+// local_scan.cu: one CTA per channel vector over the whole (short) sequence
+template <class S>
+bool local_scan_ok(int64_t T, int64_t W, bool vec_ok);
+template <class S>
+cudaError_t launch_local_fwd(const FwdCall<S>& c, bool vec_ok, cudaStream_t st);
+template <class S>
+cudaError_t launch_local_bwd(const BwdCall<S>& c, bool vec_ok, cudaStream_t st);
+
 // segment.cu
 // Fix-up of the tiles of (nseg x ntt) chain positions: e_in = seg_prod[pos] *
 // carry[seg or 0] (carry_stride W or 0); when scale != nullptr each position's
