@@ -99,11 +99,13 @@ __device__ __forceinline__ bool entering(const FixupArgs<S>& f, int64_t vseg, in
 // correction entering p_next (*more: non-zero in this thread's channels);
 // returns false (nothing stored) when this position's correction is zero in
 // every channel of the tile.
-template <class S, int VEC, int Q, bool REV, class Sync>
+template <class S, int VEC, int Q, bool REV, class Sync, int RF = 12>
 __device__ __forceinline__ bool fixup_position(const FixupArgs<S>& f, int64_t vseg, int64_t col, int64_t p_in,
                                                const Carries<S>& cr, S (*s_wp)[Q * VEC], int64_t p_next = -1,
                                                bool* more = nullptr) {
-  constexpr int NW = 8, RF = 12, G = 32 / Q, CPW = Q * VEC, NSEG = NW * G, PR = NSEG * RF;  // PR = a TMA tile
+  // RF rows per thread: PR = NSEG * RF rows per pass (12: one 96-row tile per
+  // pass; 6: two passes at half the registers, two CTAs per SM)
+  constexpr int NW = 8, G = 32 / Q, CPW = Q * VEC, NSEG = NW * G, PR = NSEG * RF;
   using IO = VecIO<S, VEC>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = lane % Q, g = lane / Q;
@@ -234,7 +236,7 @@ __device__ __forceinline__ bool fixup_position(const FixupArgs<S>& f, int64_t vs
       // ahead of the stores, which may alias them); dlam is recomputed from
       // the corrected dx as the scan computes it (dlam_t = h_{t-1} * g_t), so
       // the old dlam is not read
-      constexpr int CH = 6;
+      constexpr int CH = RF > 6 ? 6 : 3;  // rows of dx / h_{t-1} per load round
       S* d_p = f.out1 + t0 * W + ch;
       const S* h_p = f.h + (t0 - 1) * W + ch;
       const int izero = (int)t0;  // i of row 0 (h_{-1} = hprev_row)
@@ -297,8 +299,9 @@ __device__ __forceinline__ void fold_carry(const FixupArgs<S>& f, const S* __res
   S A[VEC], B[VEC];
 #pragma unroll
   for (int v = 0; v < VEC; ++v) { A[v] = S(1); B[v] = S(0); }
+  constexpr int FOLD_UNROLL = REV ? 4 : 8;  // backward pairs carry a third load (the decay)
   if (valid)
-#pragma unroll 8
+#pragma unroll FOLD_UNROLL
     for (int64_t i = i0; i < i1; ++i) {  // unrolled: the pairs' loads are in flight together
       const int64_t sg = REV ? f.nseg - 1 - i : i;
       S a[VEC], b[VEC];
@@ -337,7 +340,7 @@ __device__ __forceinline__ void fold_carry(const FixupArgs<S>& f, const S* __res
 // in order, each tile loaded together with the entering correction of the
 // walker's next position (one load round per position); the walk stops at
 // the first position whose correction is zero in every channel.
-template <class S, int VEC, int Q, bool REV, class Sync>
+template <class S, int VEC, int Q, bool REV, class Sync, int RF = 12>
 __device__ __forceinline__ void fixup_chain(const FixupArgs<S>& f, int64_t vseg, int64_t col, int j, int J,
                                             const Carries<S>& cr, S (*s_wp)[Q * VEC]) {
   // positions holding rows < T: the last virtual segment is usually short,
@@ -347,7 +350,7 @@ __device__ __forceinline__ void fixup_chain(const FixupArgs<S>& f, int64_t vseg,
   const int64_t p_lo = REV ? f.ntt - nreal : 0, p_hi = REV ? f.ntt : nreal;
   for (int64_t p = p_lo + j; p < p_hi; p += J) {
     bool more = false;
-    if (!fixup_position<S, VEC, Q, REV, Sync>(f, vseg, col, p, cr, s_wp, p + J < p_hi ? p + J : -1, &more))
+    if (!fixup_position<S, VEC, Q, REV, Sync, RF>(f, vseg, col, p, cr, s_wp, p + J < p_hi ? p + J : -1, &more))
       return;
     if (!Sync::sync_or(more)) return;
   }

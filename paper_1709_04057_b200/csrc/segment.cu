@@ -30,8 +30,8 @@ namespace linrec_dev {
 // CTA first composes the range's incoming carry for its column from the
 // mailboxes (p2p_impl.cuh::compose_chunk; the first walker of the first
 // virtual segment also stores it to c_out).
-template <class S, int VEC, int Q, bool REV>
-__global__ void __launch_bounds__(256, REV ? 1 : 2)  // backward: dx, dlam, h rows in flight
+template <class S, int VEC, int Q, bool REV, int RF>
+__global__ void __launch_bounds__(256, (REV && RF > 6) ? 1 : 2)  // backward at RF 12: dx, dlam, h rows in flight
 k_fixup(FixupArgs<S> f, Carries<S> cr, int64_t ncols, int walkers, linrec_impl::Exchange ex,
         S* __restrict__ c_out) {
   constexpr int CPW = Q * VEC, NWK = 8 * (32 / Q);
@@ -64,7 +64,7 @@ k_fixup(FixupArgs<S> f, Carries<S> cr, int64_t ncols, int walkers, linrec_impl::
     cr.own = s_own - col * CPW;  // indexed by channel
     cr.own_scale = s_scale - col * CPW;
   }
-  fixup_chain<S, VEC, Q, REV, CtaSync>(f, vseg, col, j, walkers, cr, s_wp);
+  fixup_chain<S, VEC, Q, REV, CtaSync, RF>(f, vseg, col, j, walkers, cr, s_wp);
 }
 
 // out[j] = fold over q in [first, last) by `step` of c = A_q[j] * c + B_q[j],
@@ -120,17 +120,28 @@ cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S
   fa.dh0 = dh0;
   linrec_dev::Carries<S> cr{carry_rows, scale_rows, cin};
   cr.vagg = vagg;
-#define FIX(VV)                                                                                       \
-  LINREC_Q_SWITCH(q, if (reverse) linrec_dev::k_fixup<S, VV, Q_, true><<<grid, 256, 0, st>>>(         \
+  // rows per thread of the fix-up pass (LINREC_FIXUP_RF_FWD / _BWD: 12 or 6)
+  static const int rf_fwd = env_int("LINREC_FIXUP_RF_FWD", 6) == 12 ? 12 : 6;
+  static const int rf_bwd = env_int("LINREC_FIXUP_RF_BWD", 12) == 6 ? 6 : 12;
+  const int rf = reverse ? rf_bwd : rf_fwd;
+#define FIXRF(VV, RFV)                                                                                \
+  LINREC_Q_SWITCH(q, if (reverse) linrec_dev::k_fixup<S, VV, Q_, true, RFV><<<grid, 256, 0, st>>>(    \
                          fa, cr, ncols, walk, exv, c_out);                                \
-                     else linrec_dev::k_fixup<S, VV, Q_, false><<<grid, 256, 0, st>>>(                \
+                     else linrec_dev::k_fixup<S, VV, Q_, false, RFV><<<grid, 256, 0, st>>>(           \
                          fa, cr, ncols, walk, exv, c_out));
+#define FIX(VV)         \
+  if (rf == 6) {        \
+    FIXRF(VV, 6)        \
+  } else {              \
+    FIXRF(VV, 12)       \
+  }
   if (vec_ok) {
     FIX(V)
   } else {
     FIX(1)
   }
 #undef FIX
+#undef FIXRF
   return cudaGetLastError();
 }
 

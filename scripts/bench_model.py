@@ -89,7 +89,7 @@ def timed(fn, stream):
     return a.elapsed_time(b) / 1e3, out
 
 
-def main():
+def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--archs", nargs="+", default=["gilr", "gilr-lstm", "qrnn-k2", "qrnn-k10"])
     ap.add_argument("--seq-lens", nargs="+", type=int, default=[16, 256, 4096, 65536])
@@ -100,7 +100,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32"])
     ap.add_argument("--out", default=None)
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
     records = []
@@ -154,6 +154,7 @@ def main():
                 else:
                     f.write(f"| {r['arch']} | {r['T']} | {r['b']} | {r['serial']['events_per_sec']:.3e} | "
                             f"{r['parallel']['events_per_sec']:.3e} | {r['speedup']:.2f} |\n")
+    return records
 
 
 if __name__ == "__main__":
