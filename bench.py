@@ -624,6 +624,13 @@ def run_ours(args):
         if rank == 0:
             result.update(c4)
 
+    # the other BASELINE configs beside the C2 headline (1 GPU): C1, the C5
+    # sweep and the C3 layer, so one default run records every config
+    if args.workload == "c2" and world == 1 and not args.no_extra:
+        extra = extra_records(rk, args, stream, ws, peak)
+        if rank == 0:
+            result.update(extra)
+
     # end to end through the public API with host buffers
     if not args.no_e2e and not seq_sharded:
         e2e = e2e_legs(rk, args, host, T, B, D)
@@ -684,6 +691,46 @@ def c4_records(rk, args, stream, ws, peak):
             if "slow_decay" in rec_n and "slow_decay" in one:
                 rec_n["slow_decay"]["speedup"] = rec_n["slow_decay"]["value"] / one["slow_decay"]["value"]
             out["c4_seq_sharded"] = rec_n
+    return out
+
+
+def extra_records(rk, args, stream, ws, peak):
+    """{"c1": ..., "c5": ..., "c3": ...} on one GPU with bounded step counts
+    (guards as in their own workloads; slow decays not repeated)."""
+    import torch
+    out = {}
+    steps = min(args.steps, 20)
+    solo = _Solo(rk)
+    # C1 (configs[0]): the reference's correctness config
+    wl = WORKLOADS["c1"]
+    T, W = wl["T"], wl["B"] * wl["D"]
+    P = DeviceProblem(host_problem(T, wl["B"], wl["D"], SEED_C2), rk.dev, stream)
+    rec = run_problem(solo, P, T, args, stream, ws, False, steps=steps)
+    check_guard(rec["guard_max_rel_err"], "c1")
+    out["c1"] = dict(summarize(rec, T * W, T * W, peak), workload=wl["desc"], T=T, W=W)
+    P.free()
+    # C5 (configs[4]): 2^28 elements per (T, W) point
+    pts, total = [], 0.0
+    for k, (T, W) in enumerate(C5_POINTS):
+        P = DeviceProblem(host_problem(T, 1, W, 5000 + k), rk.dev, stream)
+        rec = run_problem(solo, P, T, args, stream, ws, False, steps=min(steps, 5))
+        check_guard(rec["guard_max_rel_err"], f"c5 T={T} W={W}")
+        pts.append(dict(summarize(rec, T * W, T * W, peak), T=T, W=W))
+        total += rec["ms_per_step"]
+        P.free()
+        torch.cuda.empty_cache()
+    n5 = sum(T * W for T, W in C5_POINTS)
+    worst = min(pts, key=lambda p: p["frac_of_peak_per_gpu"])
+    out["c5"] = {"value": n5 / (total / 1e3), "ms_per_step": total, "points": pts,
+                 "worst_point": {"T": worst["T"], "W": worst["W"], "frac": worst["frac_of_peak_per_gpu"]},
+                 "workload": "C5 fixed 2^28 elements per point, one fwd+bwd of every point per step (configs[4])"}
+    # C3 (configs[2]): one GILR-LSTM layer fwd + bwd, tensor-core gate GEMMs + chained scans
+    lr = layer_record(args, min(args.steps, 10), min(args.warmup, 3), False, False)
+    out["c3"] = {k: lr[k] for k in ("value", "unit", "ms_per_step", "dtype", "events_per_s", "gemm_tflops_total",
+                                    "gemm_share_of_step", "roofline")}
+    out["c3"]["workload"] = lr["config"]["workload"]
+    out["c3"]["guard_serial_vs_parallel"] = lr["config"]["guard_serial_vs_parallel"]
+    torch.cuda.empty_cache()
     return out
 
 
@@ -990,12 +1037,20 @@ def tensor_peak():
 
 
 def run_layer(args):
+    world, rank, local = dist_env()
+    if world > 1:
+        raise SystemExit("c3 is a single-GPU workload (the layer shards like C2 over channels: run replicas)")
+    result = layer_record(args, args.steps, args.warmup, not args.no_e2e, not args.no_cpu)
+    print(json.dumps(result), flush=True)
+
+
+def layer_record(args, steps, warmup, with_e2e, with_cpu):
+    """One GILR-LSTM layer fwd + bwd at C3 (BASELINE configs[2]): the timed
+    record (per-stage GEMM / scan rates, roofline, guard)."""
     import torch
     from paper_1709_04057_b200 import layers as L
 
     world, rank, local = dist_env()
-    if world > 1:
-        raise SystemExit("c3 is a single-GPU workload (the layer shards like C2 over channels: run replicas)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     wl = WORKLOADS["c3"]
@@ -1020,7 +1075,7 @@ def run_layer(args):
             dx, _, _ = L.gilr_lstm_backward(p, x, z, z, cache, dh, grads, precision=prec)
             return h, dx
 
-        for _ in range(args.warmup):
+        for _ in range(warmup):
             step()
         # correctness guard (untimed; bench.hpp:375-384 analogue): the same
         # layer forward with the per-channel serial scans vs the chained ones
@@ -1035,20 +1090,20 @@ def run_layer(args):
     L.profile_begin()
     with ClockSampler(local) as clocks, torch.cuda.stream(stream):
         start.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             step()
         end.record(stream)
         torch.cuda.synchronize(dev)
     stages = L.profile_end()
-    ms = start.elapsed_time(end) / args.steps
+    ms = start.elapsed_time(end) / steps
     E = T * b * n
     work = layer_stage_work(T, b, m, n)
     hbm, hbm_kind = peaks()
     tpk, tpk_kind = tensor_peak()
     st_out, best = {}, None
     for name, (tot, cnt) in stages.items():
-        avg = tot / args.steps
-        rec = {"ms": avg, "launch_sets_per_step": cnt / args.steps}
+        avg = tot / steps
+        rec = {"ms": avg, "launch_sets_per_step": cnt / steps}
         if name in work:
             kind, amount = work[name]
             if kind == "flop":
@@ -1070,8 +1125,8 @@ def run_layer(args):
         "value": E / (ms / 1e3),
         "unit": "elements/s",
         "n_gpus": 1,
-        "steps": args.steps,
-        "warmup": args.warmup,
+        "steps": steps,
+        "warmup": warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
         "scaling": "weak",
@@ -1109,17 +1164,17 @@ def run_layer(args):
     }
     # kernels per step counted on the device with torch.profiler (untimed pass)
     counted = count_our_kernels(step)
-    result["gpu_launches"] = (counted * args.steps if counted is not None
-                              else sum(round(v["launch_sets_per_step"]) for v in st_out.values()) * args.steps)
+    result["gpu_launches"] = (counted * steps if counted is not None
+                              else sum(round(v["launch_sets_per_step"]) for v in st_out.values()) * steps)
     result["gpu_launches_method"] = ("kernels of this repo per step counted with torch.profiler (CUPTI) over one "
                                      "untimed step, x steps" if counted is not None else "stage call count")
     del cache, grads
     torch.cuda.empty_cache()
-    if not args.no_e2e:
+    if with_e2e:
         result["e2e"] = layer_e2e(args, p, T, b, m, n, dev)
-    if not args.no_cpu:
+    if with_cpu:
         result["cpu_baseline"] = layer_cpu_baseline(args, m, n, b)
-    print(json.dumps(result), flush=True)
+    return result
 
 
 def layer_e2e(args, p, T, b, m, n, dev):
@@ -1235,6 +1290,8 @@ def main():
     ap.add_argument("--no-serial-cpu", action="store_true", help="skip the 1-core reference row")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 records beside the C2 headline")
     ap.add_argument("--no-slow", action="store_true", help="skip the lam~U(0.99,1) re-runs")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the C1 / C5 / C3 records beside the C2 headline (1 GPU)")
     ap.add_argument("--precision", choices=["fp32", "tf32"], default="fp32", help="c3 GEMM precision")
     ap.add_argument("--layer-cpu-rows", type=int, default=16)
     args = ap.parse_args()
