@@ -142,13 +142,29 @@ __device__ __forceinline__ bool fixup_position(const FixupArgs<S>& f, int64_t vs
     const S* lam_p = f.lam + (t0 + (REV ? 1 : 0)) * W + ch;  // the decay applied at row t0
     S* out_p = f.out0 + t0 * W + ch;
     const int itop = REV ? (int)(t0 - (seg_top - 1)) : -1;  // i of the segment's top row
-    S m[RF][VEC], o[RF][VEC];
+    // backward with dlam: dx and h_{t-1} are loaded in the same round as the
+    // decays (one load round per position: the fix-up of a deep walk -- decays
+    // near 1 -- is a streaming pass, bounded by the bytes each SM has in flight)
+    S* d_p = REV ? f.out1 + t0 * W + ch : nullptr;
+    const S* h_p = REV ? f.h + (t0 - 1) * W + ch : nullptr;
+    const int izero = (int)t0;  // i of row 0 (h_{-1} = hprev_row)
+    S m[RF][VEC], o[RF][VEC], hq[REV ? RF : 1][VEC];
 #pragma unroll
     for (int i = 0; i < RF; ++i) {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) m[i][v] = S(1);
       if (i >= ilo && i < ihi) {
-        if (!dl) IO::load_cg(out_p + i * step, o[i]);  // in flight with the decays
+        IO::load_cg(out_p + i * step, o[i]);  // in flight with the decays
+        if constexpr (REV) {
+          if (dl) {
+            if (i != izero) {
+              IO::load_cg(h_p + i * step, hq[i]);
+            } else {
+#pragma unroll
+              for (int v = 0; v < VEC; ++v) hq[i][v] = f.hprev_row != nullptr ? f.hprev_row[ch + v] : S(0);
+            }
+          }
+        }
         if (!REV || i != itop) {
           IO::load_cg(lam_p + i * step, m[i]);
         } else if (seg_top == T) {
@@ -231,41 +247,21 @@ __device__ __forceinline__ bool fixup_position(const FixupArgs<S>& f, int64_t vs
           for (int v = 0; v < VEC; ++v) o[i][v] = o[i][v] + m[i][v];
           IO::store_cg(out_p + i * step, o[i]);
         }
-    } else {
-      // backward with dlam: dx and h_{t-1} of CH rows per load round (loads
-      // ahead of the stores, which may alias them); dlam is recomputed from
-      // the corrected dx as the scan computes it (dlam_t = h_{t-1} * g_t), so
-      // the old dlam is not read
-      constexpr int CH = RF > 6 ? 6 : 3;  // rows of dx / h_{t-1} per load round
-      S* d_p = f.out1 + t0 * W + ch;
-      const S* h_p = f.h + (t0 - 1) * W + ch;
-      const int izero = (int)t0;  // i of row 0 (h_{-1} = hprev_row)
+    } else if constexpr (REV) {
+      // backward with dlam: dlam is recomputed from the corrected dx as the
+      // scan computes it (dlam_t = h_{t-1} * g_t), so the old dlam is not read
 #pragma unroll
-      for (int c = 0; c < RF; c += CH) {
-        S oc[CH][VEC], hp[CH][VEC], d[CH][VEC];
+      for (int i = 0; i < RF; ++i)
+        if (i >= ilo && i < ihi) {
+          S d[VEC];
 #pragma unroll
-        for (int i = 0; i < CH; ++i)
-          if (c + i >= ilo && c + i < ihi) {
-            IO::load_cg(out_p + (c + i) * step, oc[i]);
-            if (c + i != izero) {
-              IO::load_cg(h_p + (c + i) * step, hp[i]);
-            } else {
-#pragma unroll
-              for (int v = 0; v < VEC; ++v) hp[i][v] = f.hprev_row != nullptr ? f.hprev_row[ch + v] : S(0);
-            }
+          for (int v = 0; v < VEC; ++v) {
+            o[i][v] = o[i][v] + m[i][v];
+            d[v] = mul_(hq[i][v], o[i][v]);
           }
-#pragma unroll
-        for (int i = 0; i < CH; ++i)
-          if (c + i >= ilo && c + i < ihi) {
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) {
-              oc[i][v] = oc[i][v] + m[c + i][v];
-              d[i][v] = mul_(hp[i][v], oc[i][v]);
-            }
-            IO::store_cg(out_p + (c + i) * step, oc[i]);
-            IO::store_cg(d_p + (c + i) * step, d[i]);
-          }
-      }
+          IO::store_cg(out_p + i * step, o[i]);
+          IO::store_cg(d_p + i * step, d);
+        }
     }
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
