@@ -79,6 +79,23 @@ for _ in range(reps):
     gtf += e3[0].elapsed_time(e3[1])
     gtb += e3[1].elapsed_time(e3[2])
 print(f"N={N} graph-replayed: fwd {gtf / reps * 1e3:.1f} us  bwd {gtb / reps * 1e3:.1f} us", flush=True)
+# the whole step (fwd + bwd) as ONE graph, as bench.py times a single-GPU step
+with torch.cuda.stream(s2):
+    st = s2.cuda_stream
+    gstep = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gstep, stream=s2):
+        fwd()
+        bwd()
+torch.cuda.synchronize()
+st = st_saved
+e2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+e2[0].record()
+for _ in range(reps):
+    gstep.replay()
+e2[1].record()
+torch.cuda.synchronize()
+print(f"N={N} one-graph step: {e2[0].elapsed_time(e2[1]) / reps * 1e3:.1f} us per rank-step "
+      f"(7x over the 1-GPU C4 step needs <= {721.3 / 7:.0f} us)", flush=True)
 # per kernel (each launch its own graph, replayed back to back in step order)
 parts = {
     "fwd scan": lambda: capi.segment_scan(p(lam), p(x), None, p(h), p(spf), p(agg), Tl, W, 4, ws.handle, st),
