@@ -203,11 +203,17 @@ linrec_workspace* default_ws(int device, cudaStream_t st) {
 // (T <= 2048): the time-chained scan has nothing to add there, and its
 // 96-row tiles are mostly padding at small T (bench_model's T=16, b=4096:
 // 112 -> 27 us per forward scan).  LINREC_CHANNEL_PARALLEL=0 disables it.
+// Short sequences over many channels: the per-channel kernel's T dependent
+// steps are cheaper than any split of a few rows (scripts/bench_kernel.py,
+// b = 1: T = 16, W = 65536 -- 2.9 us per-channel against 40.5 us split;
+// T = 64, W = 16384 -- 6.2 against 13.8; at T = 256 the split scans win
+// from W = 256 to 65536).
 template <class S>
 bool channel_parallel_enough(int64_t T, int64_t W, bool vok) {
   static const bool on = linrec_impl::env_int("LINREC_CHANNEL_PARALLEL", 1) != 0;
   const int64_t threads = vok ? W / vec_of<S>() : W;
-  return on && T <= 2048 && threads >= (int64_t(1) << 17);
+  return on && ((T <= 2048 && threads >= (int64_t(1) << 17)) || (T <= 32 && threads >= 1024) ||
+                (T <= 128 && threads >= 4096));
 }
 
 template <class S>
