@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "launch.h"
+#include "linrec_device.cuh"
 
 using linrec_impl::BwdCall;
 using linrec_impl::ChainPlan;
@@ -152,11 +153,12 @@ template <class S>
 struct VsegPtrs {
   S* vagg;
   S* seg_prod;
+  S* carry;  // [nseg][W]: the carries a deep (adaptive) scan seeds its segments with
 };
 
 template <class S>
 size_t vseg_region_bytes(const ChainPlan& p, int64_t W) {
-  return sizeof(S) * (size_t)W * (size_t)(2 * p.nseg + p.nseg * p.ntt) + 1024;
+  return sizeof(S) * (size_t)W * (size_t)(3 * p.nseg + p.nseg * p.ntt) + 1024;
 }
 
 template <class S>
@@ -167,7 +169,33 @@ VsegPtrs<S> vseg_ptrs(linrec_workspace* ws, const ChainPlan& p, int64_t W) {
   VsegPtrs<S> r;
   r.vagg = v;
   r.seg_prod = v + 2 * p.nseg * W;
+  r.carry = r.seg_prod + p.nseg * p.ntt * W;
   return r;
+}
+
+// ---------------------------------------------------------------------------
+// Decay-adaptive stitch (fp32 TMA scans with virtual segments).  The fix-up
+// that stitches virtual segments touches only the positions whose decay
+// product has not underflowed: ~2 tiles per segment for the reference's bench
+// decays, but the whole segment when decays are near 1 -- then it is a second
+// pass (12 B/el forward, 20 B/el backward).  A probe kernel
+// estimates the fix-up depth from 64 sampled rows and sets a mode word on the
+// device; the launches that follow read it: in "deep" mode a reduce-only pass
+// (8-12 B/el, no outputs) gives every segment's aggregate, a fold gives the
+// carries entering them, the scan seeds its segments with those carries and
+// the fix-up exits at once; otherwise the reduce pass and the fold exit at
+// once and the stitch runs as before.  All decisions stay on the device, so
+// the sequence is stream-ordered and graph-capturable.  Thresholds: the mean
+// fraction of a segment the fix-up would walk, above which the reduce pass
+// is cheaper (forward: 8 B/el < 12 B/el x f; backward: 12 B/el (its h
+// stream rides along) < 20 B/el x f / 0.76).  LINREC_ADAPTIVE=0 disables it.
+bool adaptive_stitch_on() {
+  static const bool on = linrec_impl::env_int("LINREC_ADAPTIVE", 1) != 0;
+  return on;
+}
+constexpr float kDeepFracFwd = 0.67f, kDeepFracBwd = 0.45f;
+const int* decay_mode_ptr(linrec_workspace* ws) {
+  return reinterpret_cast<const int*>(static_cast<char*>(ws->base) + offsetof(linrec_dev::Ctrl, decay_mode));
 }
 
 std::atomic<int> g_kernel_policy{0};  // LINREC_KERNEL_AUTO
@@ -248,12 +276,28 @@ int scan_device(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t 
     c.seg_prod = vs.seg_prod;
     c.agg_out = vs.vagg;
   }
+  const bool adapt = tma && sizeof(S) == 4 && p.nseg > 1 && adaptive_stitch_on();
+  const int* dmode = adapt ? decay_mode_ptr(w) : nullptr;
+  if (adapt) {  // probe -> (deep only) reduce pass + segment carries; the scan seeds from them
+    LINREC_CUDA_TRY(linrec_impl::launch_decay_probe<float>(reinterpret_cast<const float*>(lam), T, W, p.cpw, p.tseg,
+                                                           kDeepFracFwd, w->base, st));
+    FwdCall<S> r = c;
+    r.h = nullptr;
+    r.seg_prod = nullptr;
+    r.mode = dmode;
+    r.role = 1;
+    LINREC_CUDA_TRY(linrec_impl::launch_tma_fwd<S>(p, r, ws_ptrs(w, p), st));
+    LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, vs.vagg, p.nseg, p.tseg, vs.carry, nullptr,
+                                                         nullptr, nullptr, W, st, nullptr, dmode));
+    c.mode = dmode;
+    c.seed_rows = vs.carry;
+  }
   if (tma) LINREC_CUDA_TRY(linrec_impl::launch_tma_fwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_fwd<S>(p, c, ws_ptrs(w, p), st));
   if (p.nseg > 1)  // one stitch launch: each fix-up CTA folds its own segment's carry from vagg
     LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(false, lam, nullptr, nullptr, nullptr, vs.seg_prod, nullptr,
                                                  nullptr, nullptr, h, nullptr, T, W, p.rows, p.nseg, p.tseg, p.ntt,
-                                                 vok, st, nullptr, nullptr, vs.vagg));
+                                                 vok, st, nullptr, nullptr, vs.vagg, nullptr, dmode));
   return LINREC_OK;
 }
 
@@ -291,12 +335,30 @@ int scan_backward_device(const S* lam, const S* h0, const S* h, const S* dh, con
     c.seg_prod = vs.seg_prod;
     c.agg_out = vs.vagg;
   }
+  const bool adapt = tma && sizeof(S) == 4 && p.nseg > 1 && adaptive_stitch_on();
+  const int* dmode = adapt ? decay_mode_ptr(w) : nullptr;
+  if (adapt) {  // the forward's decay-adaptive stitch in reverse time (see above)
+    LINREC_CUDA_TRY(linrec_impl::launch_decay_probe<float>(reinterpret_cast<const float*>(lam), T, W, p.cpw, p.tseg,
+                                                           kDeepFracBwd, w->base, st));
+    BwdCall<S> r = c;
+    r.dlam = nullptr;
+    r.dx = nullptr;
+    r.dh0 = nullptr;
+    r.seg_prod = nullptr;
+    r.mode = dmode;
+    r.role = 1;
+    LINREC_CUDA_TRY(linrec_impl::launch_tma_bwd<S>(p, r, ws_ptrs(w, p), st));
+    LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, vs.vagg, p.nseg, p.tseg, vs.carry, nullptr,
+                                                         nullptr, nullptr, W, st, nullptr, dmode));
+    c.mode = dmode;
+    c.seed_rows = vs.carry;
+  }
   if (tma) LINREC_CUDA_TRY(linrec_impl::launch_tma_bwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_bwd<S>(p, c, ws_ptrs(w, p), st));
   if (p.nseg > 1)  // dh0 gets its correction from the fix-up that owns row 0
     LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(true, lam, h0, h, lam_next, vs.seg_prod, nullptr, nullptr,
                                                  nullptr, dx, dlam, T, W, p.rows, p.nseg, p.tseg, p.ntt, vok, st,
-                                                 nullptr, nullptr, vs.vagg, dh0));
+                                                 nullptr, nullptr, vs.vagg, dh0, dmode));
   return LINREC_OK;
 }
 
@@ -1363,14 +1425,19 @@ int linrec_scan_kernel_count(int64_t T, int64_t W, int dtype_bytes, int backward
   const bool f64 = dtype_bytes == 8;
   const bool vok = W % (f64 ? vec_of<double>() : vec_of<float>()) == 0;  // aligned buffers assumed
   if (mode == LINREC_SERIAL ||
-      (f64 ? channel_parallel_enough<double>(T, W, vok) : channel_parallel_enough<float>(T, W, vok)))
+      (f64 ? channel_parallel_enough<double>(T, W, vok) : channel_parallel_enough<float>(T, W, vok)) ||
+      (f64 ? linrec_impl::local_scan_ok<double>(T, W, vok) : linrec_impl::local_scan_ok<float>(T, W, vok)))
     return 1;
   ChainPlan p;
   const bool fwd = backward == 0;
   const bool tma = vok && tma_allowed(T, W) &&
                    (f64 ? linrec_impl::plan_tma<double>(fwd, T, W, &p) : linrec_impl::plan_tma<float>(fwd, T, W, &p));
   if (!tma) p = f64 ? linrec_impl::plan_chain<double>(fwd, T, W, vok) : linrec_impl::plan_chain<float>(fwd, T, W, vok);
-  return p.nseg > 1 ? 2 : 1;  // the scan, plus the fix-up that stitches the virtual segments
+  if (p.nseg <= 1) return 1;
+  // the scan and the fix-up that stitches the virtual segments; with the
+  // decay-adaptive stitch also the probe, the reduce pass and the carry fold
+  // (launched always, the unused ones exit at once)
+  return (tma && !f64 && adaptive_stitch_on()) ? 5 : 2;
 }
 
 int linrec_scan_plan_f32(const float* lam, const float* x, const float* h0, float* h, int64_t T, int64_t W,

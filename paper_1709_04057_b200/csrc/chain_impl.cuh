@@ -80,7 +80,8 @@ inline void choose_segments(ChainPlan& p, int64_t T, bool forward) {
 template <class S>
 size_t vseg_bytes(const ChainPlan& p, int64_t W) {
   if (p.nseg <= 1) return 0;
-  return sizeof(S) * (size_t)W * (size_t)(2 * p.nseg + p.nseg * p.ntt) + 1024;
+  // vagg [nseg][2][W], seg_prod [nseg*ntt][W], carry [nseg][W] (adaptive stitch)
+  return sizeof(S) * (size_t)W * (size_t)(3 * p.nseg + p.nseg * p.ntt) + 1024;
 }
 
 template <class S, int VEC, int Q, int R, int NW>

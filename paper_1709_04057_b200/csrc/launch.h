@@ -84,6 +84,13 @@ struct FwdCall {
   S* agg_out = nullptr;
   S* rank_agg = nullptr;  // non-null: fold agg_out into it in the scan's tail (TMA, fp32)
   Exchange ex{};          // ... and publish it
+  // decay-adaptive stitch (capi.cpp::adaptive_stitch): device mode word
+  // (1 = "deep": the decays do not underflow within a virtual segment), the
+  // launch's role (0 = the scan, which seeds virtual segments from seed_rows
+  // when deep; 1 = the reduce-only pass, skipped unless deep)
+  const int* mode = nullptr;
+  int role = 0;
+  const S* seed_rows = nullptr;
 };
 
 template <class S>
@@ -102,6 +109,9 @@ struct BwdCall {
   S* agg_out = nullptr;
   S* rank_agg = nullptr;
   Exchange ex{};
+  const int* mode = nullptr;  // as FwdCall
+  int role = 0;
+  const S* seed_rows = nullptr;
 };
 
 template <class S>
@@ -144,11 +154,16 @@ cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S
                          const S* seg_prod, const S* carry_rows, const S* scale_rows, const S* cin, S* out0, S* out1,
                          int64_t T, int64_t W, int64_t rows, int64_t nseg, int64_t tseg, int64_t ntt,
                          bool vec_ok, cudaStream_t st, const Exchange* ex = nullptr, S* c_out = nullptr,
-                         const S* vagg = nullptr, S* dh0 = nullptr);
+                         const S* vagg = nullptr, S* dh0 = nullptr, const int* skip_if_deep = nullptr);
 template <class S>
 cudaError_t launch_vseg_finalize(bool reverse, const S* lam, const S* vagg, int64_t nseg, int64_t tseg,
                                  S* carry, S* scale, S* agg_rank, S* dh0, int64_t W, cudaStream_t st,
-                                 const Exchange* ex = nullptr);
+                                 const Exchange* ex = nullptr, const int* run_if_deep = nullptr);
+// decay probe of the adaptive stitch (segment.cu::k_decay_probe): sets the
+// workspace's ctrl->decay_mode
+template <class S>
+cudaError_t launch_decay_probe(const S* lam, int64_t T, int64_t W, int cpw, int64_t tseg, float thr, void* ctrl,
+                               cudaStream_t st);
 template <class S>
 cudaError_t launch_compose(const S* aggs, int64_t first, int64_t last, int64_t step, const S* seed, S* out,
                            int64_t W, cudaStream_t st);

@@ -137,7 +137,14 @@ struct Ctrl {
   uint32_t pad0;
   unsigned long long ticket;
   unsigned long long retired;
-  unsigned long long pad1[5];
+  // decay-adaptive stitch (segment.cu::k_decay_probe): the column fractions
+  // summed by the probe's CTAs, their count, and the resulting mode word
+  // (1 = deep) read by the launches that follow on this workspace
+  float decay_sum;
+  uint32_t decay_count;
+  int32_t decay_mode;
+  uint32_t pad2;
+  unsigned long long pad1[3];
 };
 static_assert(sizeof(Ctrl) == 64, "Ctrl must be one 64-byte block");
 

@@ -93,6 +93,13 @@ struct ChainArgs {
   int tail_fold;
   S* rank_agg;
   linrec_impl::Exchange ex;
+  // decay-adaptive stitch (TMA kernels): mode word (nullable; 1 = deep),
+  // role (1 = reduce-only pass: runs only when deep, stores no outputs), and
+  // the carries entering the virtual segments [nseg][W] a deep scan seeds
+  // its chains with (no fix-up follows)
+  const int* mode;
+  int role;
+  const S* seed_rows;
 };
 
 // Position of ticket k: chain = (virtual segment, channel column), tiles in

@@ -105,7 +105,7 @@ __device__ __forceinline__ void tma_init_barriers(const SM& sm) {
 // Coordinator warp loop (both directions).
 template <class Cfg, class S, bool REV, class SM>
 __device__ __forceinline__ bool tma_coordinator(const SM& sm, const ChainArgs<S>& a, const ChainWs& ws,
-                                                uint32_t epoch) {
+                                                uint32_t epoch, bool deep) {
   constexpr int VEC = Cfg::kVEC, Q = Cfg::kQ, NW = Cfg::kNW, CPW = Cfg::CPW, STAGES = Cfg::kSTAGES;
   const int lane = threadIdx.x & 31;
   for (int n = 0;; ++n) {
@@ -143,6 +143,11 @@ __device__ __forceinline__ bool tma_coordinator(const SM& sm, const ChainArgs<S>
       if (cp.pos == 0 && cp.seg == (REV ? a.nseg - 1 : 0) && a.seed != nullptr && valid) {
 #pragma unroll
         for (int v = 0; v < VEC; ++v) c[v] = a.seed[ch + v];
+      } else if (deep && cp.pos == 0 && a.seed_rows != nullptr && valid) {
+        // decay-adaptive stitch, deep mode: the true carry entering this
+        // virtual segment (reduce pass + fold), so no fix-up follows
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) c[v] = a.seed_rows[cp.seg * a.W + ch + v];
       }
     }
     const bool want_p = a.seg_prod != nullptr || a.agg_out != nullptr;
@@ -261,6 +266,9 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const TmaSmem<Cfg, S> sm{smem_raw};
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // decay-adaptive stitch: the reduce-only pass runs only in deep mode
+  const bool deep = a.mode != nullptr && __ldcg(a.mode) != 0;
+  if (a.role == 1 && !deep) return;
   tma_init_barriers<Cfg>(sm);
   const uint32_t epoch = __ldcg(&ws.ctrl->epoch);
   __shared__ int s_last;  // tail fold: this CTA retired last
@@ -294,7 +302,7 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
       }
     }
   } else if (warp == NW) {  // ---------------- coordinator
-    const bool last = tma_coordinator<Cfg, S, false>(sm, a, ws, epoch);
+    const bool last = tma_coordinator<Cfg, S, false>(sm, a, ws, epoch, deep);
     if (lane == 0) s_last = last ? 1 : 0;
   } else {
 
@@ -388,7 +396,7 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
 #pragma unroll
       for (int v = 0; v < VEC; ++v) cs[v] = fma_(l[i][v], cs[v], xv[i][v]);
       const int t = t0 + i;
-      if (valid && t < Ti) {
+      if (valid && t < Ti && a.out0 != nullptr) {  // (reduce-only pass: no outputs)
         if (keep) IO::store_hint(a.out0 + t * W + ch, cs, pol_keep);
         else IO::store_stream(a.out0 + t * W + ch, cs);
       }
@@ -413,6 +421,9 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const TmaSmem<Cfg, S> sm{smem_raw};
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // decay-adaptive stitch: the reduce-only pass runs only in deep mode
+  const bool deep = a.mode != nullptr && __ldcg(a.mode) != 0;
+  if (a.role == 1 && !deep) return;
   tma_init_barriers<Cfg>(sm);
   const uint32_t epoch = __ldcg(&ws.ctrl->epoch);
   __shared__ int s_last;  // tail fold: this CTA retired last
@@ -450,7 +461,7 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
       }
     }
   } else if (warp == NW) {  // ---------------- coordinator
-    const bool last = tma_coordinator<Cfg, S, true>(sm, a, ws, epoch);
+    const bool last = tma_coordinator<Cfg, S, true>(sm, a, ws, epoch, deep);
     if (lane == 0) s_last = last ? 1 : 0;
   } else {
 
@@ -566,7 +577,7 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
         dl[v] = mul_(hp[i][v], cs[v]);
       }
       const int t = t0 + i;
-      if (valid && t < Ti) {
+      if (valid && t < Ti && a.out0 != nullptr) {  // (reduce-only pass: no outputs)
         if (keep) {
           IO::store_hint(a.out0 + t * W + ch, cs, pol_keep);
           if (a.out1 != nullptr) IO::store_hint(a.out1 + t * W + ch, dl, pol_keep);

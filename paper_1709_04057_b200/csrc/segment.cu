@@ -33,8 +33,9 @@ namespace linrec_dev {
 template <class S, int VEC, int Q, bool REV, int RF>
 __global__ void __launch_bounds__(256, (REV && RF > 6) ? 1 : 2)  // backward at RF 12: dx, dlam, h rows in flight
 k_fixup(FixupArgs<S> f, Carries<S> cr, int64_t ncols, int walkers, linrec_impl::Exchange ex,
-        S* __restrict__ c_out) {
+        S* __restrict__ c_out, const int* __restrict__ skip_if_deep) {
   constexpr int CPW = Q * VEC, NWK = 8 * (32 / Q);
+  if (skip_if_deep != nullptr && __ldcg(skip_if_deep) != 0) return;  // the deep scan seeded its segments
   __shared__ S s_wp[8][CPW];
   __shared__ S s_cin[CPW];
   __shared__ S s_own[CPW], s_scale[CPW];
@@ -87,14 +88,69 @@ template <class S, bool REV, int G>
 __global__ void __launch_bounds__(32 * G)
 k_vseg_finalize(const S* __restrict__ lam, const S* __restrict__ vagg, int64_t nseg, int64_t tseg,
                 S* __restrict__ carry, S* __restrict__ scale, S* __restrict__ agg_rank, S* __restrict__ dh0,
-                int64_t W, linrec_impl::Exchange ex) {
+                int64_t W, linrec_impl::Exchange ex, const int* __restrict__ run_if_deep) {
   __shared__ S sA[G][32], sB[G][32];
+  if (run_if_deep != nullptr && __ldcg(run_if_deep) == 0) return;  // adaptive stitch: shallow decays
   vseg_fold<S, REV, G, CtaSync>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W, blockIdx.x, sA, sB);
   if constexpr (std::is_same<S, float>::value) {
     // the rank aggregate of this chunk straight into the consumers' mailboxes
     if (ex.has_consumers()) {
       const int64_t j0 = (int64_t)blockIdx.x * 32;
       p2p::publish_chunk(ex, agg_rank, j0, (int)(W - j0 < 32 ? W - j0 : 32));
+    }
+  }
+}
+
+// Decay probe of the adaptive stitch: is the fix-up of the virtual segments
+// going to be a second pass?  CTA `col` estimates, for each channel of its
+// column, how many rows the decay product takes to underflow (fp32: to
+// 2^-149) from the mean log2|lam| over 64 rows sampled across T, takes the
+// column's maximum (a fix-up tile is touched while ANY of its channels is
+// non-zero), and adds min(1, depth / tseg) -- the fraction of each segment
+// the fix-up would walk -- to a sum; the last CTA sets ctrl->decay_mode = 1
+// when the mean fraction exceeds `thr` (the fix-up would cost more than the
+// reduce-only pass it replaces) and resets the sum for the next launch.
+// Graph-safe (device state only), no host synchronisation.
+template <class S>
+__global__ void __launch_bounds__(512) k_decay_probe(const S* __restrict__ lam, int64_t T, int64_t W, int cpw,
+                                                     int64_t tseg, float thr, Ctrl* ctrl) {
+  // 64 sampled rows: 4 row groups x 16 rows per thread, all 16 loads in
+  // flight at once (one DRAM round trip), then the groups combine
+  constexpr int NS = 64, NG = 4, RPG = NS / NG;
+  __shared__ float s_sum[NG][128];
+  __shared__ float s_max[4];
+  const int c = threadIdx.x & 127, grp = threadIdx.x >> 7;
+  const int64_t ch = (int64_t)blockIdx.x * cpw + c;
+  const bool ok = c < cpw && ch < W;
+  float v[RPG];
+#pragma unroll
+  for (int k = 0; k < RPG; ++k) {
+    const int64_t t = (T * (grp * RPG + k)) / NS;
+    v[k] = ok ? (float)__ldcg(lam + t * W + ch) : 1.f;
+  }
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < RPG; ++k) sum += log2f(fabsf(v[k]));  // |lam| = 0 -> -inf -> depth 0
+  s_sum[grp][c] = sum;
+  __syncthreads();
+  float depth = 0.f;
+  if (grp == 0) {
+    const float mean = (s_sum[0][c] + s_sum[1][c] + s_sum[2][c] + s_sum[3][c]) / NS;
+    depth = !ok ? 0.f : (mean < 0.f ? 149.f / -mean : 3.0e38f);
+    for (int off = 16; off > 0; off >>= 1) depth = fmaxf(depth, __shfl_xor_sync(0xffffffffu, depth, off));
+    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = depth;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const float d = fmaxf(fmaxf(s_max[0], s_max[1]), fmaxf(s_max[2], s_max[3]));
+    const float frac = fminf(1.f, d / (float)tseg);
+    atomicAdd(&ctrl->decay_sum, frac);
+    __threadfence();
+    if (atomicAdd(&ctrl->decay_count, 1u) == gridDim.x - 1) {
+      __threadfence();
+      const float mean = atomicExch(&ctrl->decay_sum, 0.f) / (float)gridDim.x;
+      ctrl->decay_count = 0u;
+      ctrl->decay_mode = mean > thr ? 1 : 0;
     }
   }
 }
@@ -107,7 +163,8 @@ template <class S>
 cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S* h, const S* lam_next,
                          const S* seg_prod, const S* carry_rows, const S* scale_rows, const S* cin, S* out0, S* out1,
                          int64_t T, int64_t W, int64_t rows, int64_t nseg, int64_t tseg, int64_t ntt,
-                         bool vec_ok, cudaStream_t st, const Exchange* ex, S* c_out, const S* vagg, S* dh0) {
+                         bool vec_ok, cudaStream_t st, const Exchange* ex, S* c_out, const S* vagg, S* dh0,
+                         const int* skip_if_deep) {
   const Exchange exv = ex != nullptr ? *ex : Exchange{};
   constexpr int V = Tuning<S>::VEC;
   const int64_t nvec = vec_ok ? (W + V - 1) / V : W;
@@ -126,9 +183,9 @@ cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S
   const int rf = reverse ? rf_bwd : rf_fwd;
 #define FIXRF(VV, RFV)                                                                                \
   LINREC_Q_SWITCH(q, if (reverse) linrec_dev::k_fixup<S, VV, Q_, true, RFV><<<grid, 256, 0, st>>>(    \
-                         fa, cr, ncols, walk, exv, c_out);                                \
+                         fa, cr, ncols, walk, exv, c_out, skip_if_deep);                  \
                      else linrec_dev::k_fixup<S, VV, Q_, false, RFV><<<grid, 256, 0, st>>>(           \
-                         fa, cr, ncols, walk, exv, c_out));
+                         fa, cr, ncols, walk, exv, c_out, skip_if_deep));
 #define FIX(VV)         \
   if (rf == 6) {        \
     FIXRF(VV, 6)        \
@@ -147,14 +204,15 @@ cudaError_t launch_fixup(bool reverse, const S* lam, const S* hprev_row, const S
 
 template <class S>
 cudaError_t launch_vseg_finalize(bool reverse, const S* lam, const S* vagg, int64_t nseg, int64_t tseg, S* carry,
-                                 S* scale, S* agg_rank, S* dh0, int64_t W, cudaStream_t st, const Exchange* ex) {
+                                 S* scale, S* agg_rank, S* dh0, int64_t W, cudaStream_t st, const Exchange* ex,
+                                 const int* run_if_deep) {
   const Exchange exv = ex != nullptr ? *ex : Exchange{};
   constexpr int G = 16;
   const unsigned g = (unsigned)((W + 31) / 32);
   if (reverse)
-    linrec_dev::k_vseg_finalize<S, true, G><<<g, 32 * G, 0, st>>>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W, exv);
+    linrec_dev::k_vseg_finalize<S, true, G><<<g, 32 * G, 0, st>>>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W, exv, run_if_deep);
   else
-    linrec_dev::k_vseg_finalize<S, false, G><<<g, 32 * G, 0, st>>>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W, exv);
+    linrec_dev::k_vseg_finalize<S, false, G><<<g, 32 * G, 0, st>>>(lam, vagg, nseg, tseg, carry, scale, agg_rank, dh0, W, exv, run_if_deep);
   return cudaGetLastError();
 }
 
@@ -167,22 +225,35 @@ cudaError_t launch_compose(const S* aggs, int64_t first, int64_t last, int64_t s
   return cudaGetLastError();
 }
 
+template <class S>
+cudaError_t launch_decay_probe(const S* lam, int64_t T, int64_t W, int cpw, int64_t tseg, float thr, void* ctrl,
+                               cudaStream_t st) {
+  const unsigned ncols = (unsigned)((W + cpw - 1) / cpw);
+  linrec_dev::k_decay_probe<S><<<ncols, 512, 0, st>>>(lam, T, W, cpw, tseg, thr,
+                                                      reinterpret_cast<linrec_dev::Ctrl*>(ctrl));
+  return cudaGetLastError();
+}
+template cudaError_t launch_decay_probe<float>(const float*, int64_t, int64_t, int, int64_t, float, void*,
+                                               cudaStream_t);
+
 template cudaError_t launch_fixup<float>(bool, const float*, const float*, const float*, const float*, const float*,
                                          const float*, const float*, const float*, float*, float*, int64_t, int64_t,
                                          int64_t, int64_t, int64_t, int64_t, bool, cudaStream_t, const Exchange*,
-                                         float*, const float*, float*);
+                                         float*, const float*, float*, const int*);
 template cudaError_t launch_fixup<double>(bool, const double*, const double*, const double*, const double*,
                                           const double*, const double*, const double*, const double*, double*,
                                           double*,
                                           int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, bool, cudaStream_t,
-                                          const Exchange*, double*, const double*, double*);
+                                          const Exchange*, double*, const double*, double*, const int*);
 template cudaError_t launch_compose<float>(const float*, int64_t, int64_t, int64_t, const float*, float*,
                                            int64_t, cudaStream_t);
 template cudaError_t launch_compose<double>(const double*, int64_t, int64_t, int64_t, const double*, double*,
                                             int64_t, cudaStream_t);
 template cudaError_t launch_vseg_finalize<float>(bool, const float*, const float*, int64_t, int64_t, float*,
-                                                 float*, float*, float*, int64_t, cudaStream_t, const Exchange*);
+                                                 float*, float*, float*, int64_t, cudaStream_t, const Exchange*,
+                                                 const int*);
 template cudaError_t launch_vseg_finalize<double>(bool, const double*, const double*, int64_t, int64_t, double*,
-                                                  double*, double*, double*, int64_t, cudaStream_t, const Exchange*);
+                                                  double*, double*, double*, int64_t, cudaStream_t, const Exchange*,
+                                                  const int*);
 
 }  // namespace linrec_impl

@@ -122,6 +122,9 @@ linrec_dev::ChainArgs<S> fwd_args(const ChainPlan& p, const FwdCall<S>& c) {
   a.tail_fold = c.rank_agg != nullptr ? 1 : 0;
   a.rank_agg = c.rank_agg;
   a.ex = c.ex;
+  a.mode = c.mode;
+  a.role = c.role;
+  a.seed_rows = c.seed_rows;
   return a;
 }
 
@@ -148,6 +151,9 @@ linrec_dev::ChainArgs<S> bwd_args(const ChainPlan& p, const BwdCall<S>& c) {
   a.tail_fold = c.rank_agg != nullptr ? 1 : 0;
   a.rank_agg = c.rank_agg;
   a.ex = c.ex;
+  a.mode = c.mode;
+  a.role = c.role;
+  a.seed_rows = c.seed_rows;
   return a;
 }
 

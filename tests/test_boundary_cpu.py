@@ -125,15 +125,17 @@ def test_product_does_not_import_oracle():
 
 def test_planner_kernel_counts():
     """linrec_scan_kernel_count (the planner, no GPU needed): one kernel for
-    the per-channel and whole-chain cases, the scan + one fix-up launch when
-    the sequence is split into virtual segments."""
+    the per-channel, CTA-local and whole-chain cases; when the sequence is
+    split into virtual segments, the scan + the fix-up + the decay-adaptive
+    stitch's probe, reduce pass and carry fold (the unused ones exit at once,
+    DESIGN.md 4)."""
     from paper_1709_04057_b200 import capi
     assert capi.scan_kernel_count(16, 1 << 20) == 1            # channels fill the GPU: per-channel kernel
     assert capi.scan_kernel_count(4096, 256) == 1              # C1: 43-tile chains stay whole
     assert capi.scan_kernel_count(4096, 256, backward=True) == 1
-    assert capi.scan_kernel_count(1 << 20, 128) == 2           # C4: virtual segments + fix-up
-    assert capi.scan_kernel_count(1 << 20, 128, backward=True) == 2
-    assert capi.scan_kernel_count(65536, 8192) == 2            # C2 forward: 4 segments
+    assert capi.scan_kernel_count(1 << 20, 128) == 5           # C4: virtual segments + adaptive stitch
+    assert capi.scan_kernel_count(1 << 20, 128, backward=True) == 5
+    assert capi.scan_kernel_count(65536, 8192) == 5            # C2 forward: 4 segments
     assert capi.scan_kernel_count(65536, 8192, backward=True) == 1
     assert capi.scan_kernel_count(1 << 20, 128, mode=capi.SERIAL) == 1
     assert capi.scan_kernel_count(0, 128) == -1
