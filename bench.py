@@ -419,6 +419,31 @@ def single_gpu_steps(P, ws, stream):
     return _Replay(gf, fwd, stream), _Replay(gb, bwd, stream), _Replay(gs, None, stream)
 
 
+def device_ms_per_step(P, ws, stream, k=16, reps=5):
+    import torch
+    from paper_1709_04057_b200 import capi
+    st = stream.cuda_stream
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for _ in range(k):
+            capi.scan(P.lam.data_ptr(), P.x.data_ptr(), P.h0.data_ptr(), P.h.data_ptr(), P.Tl, P.W,
+                      capi.PARALLEL, 4, ws.handle, st)
+            capi.scan_backward(P.lam.data_ptr(), P.h0.data_ptr(), P.h.data_ptr(), P.dh.data_ptr(),
+                               P.dlam.data_ptr(), P.dx.data_ptr(), P.dh0.data_ptr(), P.Tl, P.W,
+                               capi.PARALLEL, 4, ws.handle, st)
+    times = []
+    with torch.cuda.stream(stream):
+        g.replay()
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+            b.synchronize()
+            times.append(a.elapsed_time(b) / k)
+    return statistics.median(times)
+
+
 class _Replay:
     """A captured graph replayed on the bench stream (CUDAGraph.replay
     launches on the CURRENT stream)."""
@@ -506,6 +531,11 @@ def run_problem(rk, P, T, args, stream, ws, sharded_run, steps=None, count=False
     g = guard(rk, P, stream) if sharded_run else rk.max(guard(_Solo(rk), P, stream))
     rec = time_steps(rk, fwd, bwd, steps or args.steps, stream, step=step)
     rec["guard_max_rel_err"] = g
+    if step is not None and rec["ms_per_step"] < 0.2:
+        # a step this short is bound by the host's graph replay (~10 us from
+        # Python): also report the device time per step with 16 steps in one
+        # graph (informational; `ms_per_step` stays one replay per step)
+        rec["device_ms_per_step"] = device_ms_per_step(P, ws, stream)
     if count:
         n = count_our_kernels(lambda: (getattr(fwd, "eager", fwd)(), getattr(bwd, "eager", bwd)()))
         rec["launches_per_step"] = n
@@ -527,6 +557,11 @@ def summarize(rec, N_total, N_local, peak):
         "guard_max_rel_err": rec["guard_max_rel_err"],
     }
     out["frac_of_peak_per_gpu"] = out["hbm_gbs_per_gpu"] / peak
+    if "device_ms_per_step" in rec:  # short steps: the device time with 16 steps per graph
+        d = rec["device_ms_per_step"]
+        out["device_ms_per_step"] = d
+        out["device_value"] = N_total / (d / 1e3)
+        out["device_frac_of_peak_per_gpu"] = (FWD_BYTES + BWD_BYTES) * N_local / (d / 1e3) / 1e9 / peak
     return out
 
 
