@@ -147,11 +147,14 @@ class ChannelShardedScan:
         T = arr.shape[0]
         flat = arr.reshape(T, W)
         blocks = [channel_shard(W, self.world, q) for q in range(self.world)]
-        mine = torch.from_numpy(np.ascontiguousarray(flat[:, blocks[self.rank][0]:blocks[self.rank][1]]))
-        parts = [torch.empty(T, e - s, dtype=mine.dtype) for s, e in blocks]
+        wmax = max(e - s for s, e in blocks)  # all_gather needs equal sizes: pad to the widest block
+        s0, e0 = blocks[self.rank]
+        mine = torch.zeros(T, wmax, dtype=torch.from_numpy(flat[:0, :0]).dtype)
+        mine[:, :e0 - s0] = torch.from_numpy(np.ascontiguousarray(flat[:, s0:e0]))
+        parts = [torch.empty_like(mine) for _ in blocks]
         dist.all_gather(parts, mine, group=self.group)
         for (s, e), part in zip(blocks, parts):
-            flat[:, s:e] = part.numpy()
+            flat[:, s:e] = part[:, :e - s].numpy()
 
     def scan(self, decays, impulses, initial=None, *, mode="parallel", gather=False):
         import numpy as np

@@ -98,3 +98,79 @@ def test_segment_and_channel_bounds():
             sizes = [e - s for s, e in b]
             assert max(sizes) - min(sizes) <= 1 and sizes == sorted(sizes, reverse=True)
     assert channel_shard(8192 * 8, 8, 3) == (3 * 8192, 4 * 8192)
+
+
+def _channel_worker(rank, world, port, T, b, n, seed, q):
+    """One rank of sharded.ChannelShardedScan with gather=True over gloo; the
+    column entry points (linrec_scan_host_columns_*: CUDA) are replaced by the
+    oracle on the rank's column block, so this checks the partition, the
+    per-rank column writes and the host all-gather."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import ctypes
+        from oracle.oracle import Oracle
+        from paper_1709_04057_b200 import capi, sharded
+        orc = Oracle()
+
+        def arr(ptr, shape):
+            return np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_double)), shape)
+
+        def cols_fwd(lam, x, h0, h, T_, W, c0, c1, mode, dtype_bytes, device):
+            L, X, H = (arr(p, (T_, W)) for p in (lam, x, h))
+            H0 = arr(h0, (W,))[None, c0:c1].copy() if h0 else None
+            H[:, c0:c1] = orc.scan_serial(L[:, None, c0:c1].copy(), X[:, None, c0:c1].copy(),
+                                          H0)[:, 0, :]
+
+        def cols_bwd(lam, h0, h, dh, dlam, dx, dh0, T_, W, c0, c1, mode, dtype_bytes, device):
+            L, H, DHh, DL, DX = (arr(p, (T_, W)) for p in (lam, h, dh, dlam, dx))
+            D0 = arr(dh0, (W,))
+            H0 = arr(h0, (W,))[None, c0:c1].copy() if h0 else None
+            g = orc.scan_backward(L[:, None, c0:c1].copy(), H0, H[:, None, c0:c1].copy(),
+                                  DHh[:, None, c0:c1].copy())
+            DL[:, c0:c1], DX[:, c0:c1], D0[c0:c1] = g[0][:, 0], g[1][:, 0], g[2][0]
+
+        capi.scan_host_columns = cols_fwd
+        capi.scan_backward_host_columns = cols_bwd
+        rng = np.random.default_rng(seed)
+        lam = rng.uniform(0.05, 0.95, (T, b, n))
+        x = rng.uniform(-1.0, 1.0, (T, b, n))
+        h0 = rng.uniform(-1.0, 1.0, (b, n))
+        dh = rng.uniform(-1.0, 1.0, (T, b, n))
+        run = sharded.ChannelShardedScan(device=0)
+        h = run.scan(lam, x, h0, gather=True)
+        g = run.scan_backward(lam, h0, h, dh, gather=True)
+        q.put((rank, run.columns(b * n), h, g[0], g[1], g[2]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,T,b,n", [(2, 40, 2, 8), (3, 17, 1, 13)])
+def test_channel_sharded_scan_gather(oracle, world, T, b, n):
+    seed = 7 + world
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_channel_worker, args=(r, world, port, T, b, n, seed, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(seed)
+    lam = rng.uniform(0.05, 0.95, (T, b, n))
+    x = rng.uniform(-1.0, 1.0, (T, b, n))
+    h0 = rng.uniform(-1.0, 1.0, (b, n))
+    dh = rng.uniform(-1.0, 1.0, (T, b, n))
+    h_ref = oracle.scan_serial(lam, x, h0)
+    g_ref = oracle.scan_backward(lam, h0, h_ref, dh)
+    blocks = sorted(o[1] for o in outs)
+    assert blocks[0][0] == 0 and blocks[-1][1] == b * n
+    assert all(a[1] == c[0] for a, c in zip(blocks, blocks[1:]))
+    for rank, cols, h, dl, dx, d0 in outs:  # every rank holds the full, gathered result
+        assert np.array_equal(h, h_ref)
+        for a, r in zip((dl, dx, d0), g_ref):
+            assert np.array_equal(a, r)
