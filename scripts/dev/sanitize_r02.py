@@ -28,3 +28,17 @@ lam = np.random.rand(500, 2, 40).astype(np.float32) * 0.9
 x = np.random.rand(500, 2, 40).astype(np.float32) - 0.5
 h = sharded.channel_sharded_scan(lam, x, None, devices=[0, 0])
 print("channel-sharded ok", h.shape)
+# decay-adaptive stitch: deep (lam ~ U(0.99, 1)) and shallow decays on split scans
+for lo in (0.05, 0.995):
+    T, W = 300000, 128
+    lam = torch.rand(T, 1, W, device="cuda") * (1 - lo) + lo
+    x = torch.rand_like(lam) - 0.5
+    dh = torch.rand_like(lam) - 0.5
+    h0 = torch.rand(1, W, device="cuda")
+    h = ops.scan(lam, x, h0)
+    hs = ops.scan(lam, x, h0, mode="serial")
+    g = ops.scan_backward(lam, h0, hs, dh)
+    gs = ops.scan_backward(lam, h0, hs, dh, mode="serial")
+    torch.cuda.synchronize()
+    print("adaptive", lo, ((h - hs).abs().max() / hs.abs().max()).item(),
+          max(((a - b).abs().max() / b.abs().max()).item() for a, b in zip(g, gs)), flush=True)
