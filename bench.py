@@ -1088,6 +1088,9 @@ def layer_stage_work(T, b, m, n):
     }
 
 
+CUBLAS_TF32_TFLOPS = 755.0  # measured: torch.matmul fp32 with allow_tf32, 262144 x 2048 x 1024 (C3's gate GEMM shape)
+
+
 def tensor_peak():
     """Dense TF32 tensor-core peak for the roofline: the nominal 1.1 PFLOP/s
     of B200_PROFILING.md.  MEASURED_PEAKS.json has no TF32 figure, and half of
@@ -1215,6 +1218,10 @@ def layer_record(args, steps, warmup, with_e2e, with_cpu):
             "frac": achieved / tpk,
             # 3xTF32 issues three MMAs per algorithmic product
             "mma_issue_frac": (3 if prec == "fp32" else 1) * achieved / tpk,
+            # cuBLAS's own TF32 GEMM on this pool's B200s (scripts/dev/cublas_tf32.py: 703-755 TF/s
+            # at 8192^3 and the C3 shapes): the practical ceiling of the MMA issue rate
+            "cublas_tf32_tflops": CUBLAS_TF32_TFLOPS,
+            "mma_issue_frac_of_cublas": (3 if prec == "fp32" else 1) * achieved / CUBLAS_TF32_TFLOPS,
             "effective_peak_for_precision": tpk / (3 if prec == "fp32" else 1),
             "traffic": None,
             "algorithmic_flops_per_launch": bflop,
