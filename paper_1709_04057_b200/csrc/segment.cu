@@ -104,7 +104,8 @@ k_vseg_finalize(const S* __restrict__ lam, const S* __restrict__ vagg, int64_t n
 // Decay probe of the adaptive stitch: is the fix-up of the virtual segments
 // going to be a second pass?  CTA `col` estimates, for each channel of its
 // column, how many rows the decay product takes to underflow (fp32: to
-// 2^-149) from the mean log2|lam| over 64 rows sampled across T, takes the
+// 2^-149) from the mean log2|lam| over 64 rows sampled across T (8 blocks of
+// 8 rows; a row past T counts as |lam| = 1), takes the
 // column's maximum (a fix-up tile is touched while ANY of its channels is
 // non-zero), and adds min(1, depth / tseg) -- the fraction of each segment
 // the fix-up would walk -- to a sum; the last CTA sets ctrl->decay_mode = 1
@@ -125,8 +126,11 @@ __global__ void __launch_bounds__(512) k_decay_probe(const S* __restrict__ lam, 
   float v[RPG];
 #pragma unroll
   for (int k = 0; k < RPG; ++k) {
-    const int64_t t = (T * (grp * RPG + k)) / NS;
-    v[k] = ok ? (float)__ldcg(lam + t * W + ch) : 1.f;
+    // 8 blocks of 8 consecutive rows spread over T (few pages: the probe's one
+    // DRAM round trip is not stretched by TLB misses)
+    const int j = grp * RPG + k;
+    const int64_t t = (T * (j >> 3)) / (NS / 8) + (j & 7);
+    v[k] = ok && t < T ? (float)__ldcg(lam + t * W + ch) : 1.f;
   }
   float sum = 0.f;
 #pragma unroll
