@@ -1074,8 +1074,7 @@ def layer_stage_work(T, b, m, n):
         "gemm_gates": ("flop", 2 * R * (m + n) * 4 * n),
         "scan_cell": ("byte", 12 * E),
         "h_out": ("byte", 12 * E),
-        "dc": ("byte", 12 * E),
-        "scan_bwd_cell": ("byte", 16 * E),       # dlam not stored: dpre forms it from c
+        "scan_bwd_cell": ("byte", 20 * E),       # f, dh, o (dc = dh * o fused in), c in; G out (dlam: in dpre)
         "dpre_gates": ("byte", 44 * E),          # f i o z diz dh c in, 4 dpre planes out
         "wgrad_U": ("flop", 2 * 4 * n * n * R),
         "wgrad_V": ("flop", 2 * 4 * n * m * R),

@@ -136,6 +136,17 @@ int linrec_scan_backward_f64(const double* lam, const double* h0,
  * the true end of the sequence, G_T := 0).  G_{T-1} = lam_next*g_next +
  * dh_{T-1} is evaluated as one fused multiply-add, as in the unsplit scan,
  * so LINREC_SERIAL stays bit-exact when chained. */
+/* Gated adjoint (fused layer backward): scan_backward on d_h * gate
+ * elementwise, for a layer whose output is h = gate * c of the recurrence's
+ * state c -- GILR-LSTM's h = o * c (layers.hpp:312-324: dc = dh * o into
+ * scan_backward) and QRNN's (layers.hpp:510-521).  The product is taken as the adjoint is staged
+ * into shared memory (no dc array); dh0 and dlam (nullable) as
+ * linrec_scan_backward_f32. */
+int linrec_scan_backward_gated_f32(const float* lam, const float* h0,
+                                   const float* h, const float* dh,
+                                   const float* gate, float* dlam, float* dx,
+                                   float* dh0, int64_t T, int64_t W, int mode,
+                                   linrec_workspace_t ws, void* stream);
 int linrec_scan_backward_segment_f32(const float* lam, const float* h0,
                                      const float* h, const float* dh,
                                      const float* lam_next,

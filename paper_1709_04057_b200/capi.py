@@ -106,6 +106,7 @@ def _load():
         getattr(lib, f"linrec_scan_backward_host_multi_{s_}").argtypes = [_vp] * 7 + [_i64, _i64, _int,
                                                                                      C.POINTER(_int), _int]
     lib.linrec_column_block.argtypes = [_i64, _int, _int, C.POINTER(_i64), C.POINTER(_i64)]
+    lib.linrec_scan_backward_gated_f32.argtypes = [_vp] * 8 + [_i64, _i64, _int, _vp, _vp]
     lib.linrec_fnv1a64.restype = C.c_uint64
     lib.linrec_fnv1a64.argtypes = [_vp, C.c_size_t, C.c_uint64]
     return lib

@@ -244,6 +244,31 @@ bool channel_parallel_enough(int64_t T, int64_t W, bool vok) {
                 (T <= 128 && threads >= 4096));
 }
 
+// dx = dh * gate (the unfused gated adjoint)
+template <class S>
+__global__ void k_mul_rows(const S* __restrict__ a, const S* __restrict__ b, S* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a[i] * b[i];
+}
+template <class S>
+cudaError_t launch_mul(const S* a, const S* b, S* out, int64_t n, cudaStream_t st) {
+  const int64_t blocks = (n + 255) / 256;
+  k_mul_rows<S><<<(unsigned)(blocks < 8192 ? blocks : 8192), 256, 0, st>>>(a, b, out, n);
+  return cudaGetLastError();
+}
+
+// The fused gated backward (k_tma_bwd<..., GATED>) exists for the default
+// fp32 TMA configuration of the chained scan; other shapes / paths run
+// dx = dh * gate first.
+template <class S>
+bool gated_fused_ok(int64_t T, int64_t W, int mode, bool vok) {
+  if (sizeof(S) != 4 || mode == LINREC_SERIAL || !vok || !tma_allowed(T, W) ||
+      channel_parallel_enough<S>(T, W, vok) || linrec_impl::local_scan_ok<S>(T, W, vok))
+    return false;
+  ChainPlan p;
+  return linrec_impl::plan_tma<S>(false, T, W, &p) && p.q == 32 && p.r == 12 && p.stages == 1 && p.nw == 8;
+}
+
 template <class S>
 int scan_device(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t W, int mode,
                 linrec_workspace_t ws, cudaStream_t st) {
@@ -304,14 +329,21 @@ int scan_device(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t 
 template <class S>
 int scan_backward_device(const S* lam, const S* h0, const S* h, const S* dh, const S* lam_next,
                          const S* g_next, S* dlam, S* dx, S* dh0, int64_t T, int64_t W, int mode,
-                         linrec_workspace_t ws, cudaStream_t st) {
+                         linrec_workspace_t ws, cudaStream_t st, const S* gate = nullptr) {
   int rc;
   if ((rc = check_dims(T, W)) || (rc = check_mode(mode)) || (rc = check_ptr(lam, "decays")) ||
       (rc = check_ptr(h, "h")) || (rc = check_ptr(dh, "d_h")) ||
       (rc = check_ptr(dx, "d_impulses")))
     return rc;
-  const bool vok = vec_ok<S>(W, {lam, h0, h, dh, lam_next, g_next, dlam, dx, dh0});
+  const bool vok = vec_ok<S>(W, {lam, h0, h, dh, lam_next, g_next, dlam, dx, dh0, gate});
+  if (gate != nullptr && !gated_fused_ok<S>(T, W, mode, vok)) {
+    // gated adjoint without the fused kernel: dx = dh * gate, then the scan in
+    // place (every kernel reads a row of the adjoint before writing that row)
+    LINREC_CUDA_TRY(launch_mul<S>(dh, gate, dx, T * W, st));
+    return scan_backward_device<S>(lam, h0, h, dx, lam_next, g_next, dlam, dx, dh0, T, W, mode, ws, st);
+  }
   BwdCall<S> c{lam, h0, h, dh, lam_next, g_next, dlam, dx, dh0, T, W};
+  c.gate = gate;
   if (mode == LINREC_SERIAL || channel_parallel_enough<S>(T, W, vok)) {
     LINREC_CUDA_TRY(linrec_impl::launch_serial_bwd<S>(c, vok, st));
     return LINREC_OK;
@@ -1212,6 +1244,15 @@ int linrec_scan_backward_f64(const double* lam, const double* h0, const double* 
   if ((rc = check_ptr(dh0, "d_initial"))) return rc;
   return scan_backward_device<double>(lam, h0, h, dh, nullptr, nullptr, dlam, dx, dh0, T, W, mode,
                                       ws, static_cast<cudaStream_t>(stream));
+}
+
+int linrec_scan_backward_gated_f32(const float* lam, const float* h0, const float* h, const float* dh,
+                                   const float* gate, float* dlam, float* dx, float* dh0, int64_t T, int64_t W,
+                                   int mode, linrec_workspace_t ws, void* stream) {
+  int rc;
+  if ((rc = check_ptr(gate, "gate"))) return rc;
+  return scan_backward_device<float>(lam, h0, h, dh, nullptr, nullptr, dlam, dx, dh0, T, W, mode, ws,
+                                     static_cast<cudaStream_t>(stream), gate);
 }
 
 int linrec_scan_backward_segment_f32(const float* lam, const float* h0, const float* h,

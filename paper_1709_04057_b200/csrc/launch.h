@@ -112,6 +112,9 @@ struct BwdCall {
   const int* mode = nullptr;  // as FwdCall
   int role = 0;
   const S* seed_rows = nullptr;
+  // gated adjoint (fused layer backward): the scan runs on dh * gate, e.g.
+  // dc = dh * o for h = o * c (GILR-LSTM / QRNN); TMA fp32 default config
+  const S* gate = nullptr;
 };
 
 template <class S>

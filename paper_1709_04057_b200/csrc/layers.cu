@@ -592,10 +592,9 @@ int linrec_qrnn_backward_f32(const float* W, const float* x, const float* c0, co
   const float* go = gf + N;
   const float* gz = go + N;
   mark(st, "begin");
-  k_mul<<<grid_for(N / 4, 256), 256, 0, st>>>(dh, go, s.dc, N / 4);
-  LTRY(cudaGetLastError());
-  mark(st, "dc");
-  LRC(linrec_scan_backward_f32(gf, c0, c, s.dc, nullptr, s.dimp, dc0 ? dc0 : s.tmp0, T, b * n, mode, nullptr, st));
+  // dc = dh * o fused into the cell scan's backward (layers.hpp:510-521)
+  LRC(linrec_scan_backward_gated_f32(gf, c0, c, dh, go, nullptr, s.dimp, dc0 ? dc0 : s.tmp0, T, b * n, mode, nullptr,
+                                     st));
   mark(st, "scan_bwd_cell");
   const RowPlan rp = row_plan(R, n);
   k_qrnn_dpre<<<dim3((unsigned)rp.nbx, (unsigned)rp.gy), rp.thr, 0, st>>>(gf, go, gz, c0, s.dimp, dh, c, s.dpre,
@@ -827,11 +826,11 @@ int linrec_gilr_lstm_backward_f32(const linrec_gilr_lstm_params_f32* p, const fl
     LTRY(linrec_impl::tf32_lo(p->V, s.v_lo, 4 * n * m, st));
     LTRY(linrec_impl::tf32_lo(p->U, s.u_lo, 4 * n * n, st));
   }
-  // h = o * c  ->  dc = dh * o (d_o is formed inside k_lstm_dpre)
-  k_mul<<<grid_for(N / 4, 256), 256, 0, st>>>(dh, go, s.dc, N / 4);
-  LTRY(cudaGetLastError());
-  mark(st, "dc");
-  LRC(linrec_scan_backward_f32(gf, c0, cache->c, s.dc, nullptr, s.diz, dc0 ? dc0 : s.tmp0, T, BN, mode, nullptr, st));
+  // h = o * c  ->  dc = dh * o, fused into the cell scan's backward (the scan
+  // stages dh and o and multiplies them as it reads; layers.hpp:312-324);
+  // d_o is formed inside k_lstm_dpre
+  LRC(linrec_scan_backward_gated_f32(gf, c0, cache->c, dh, go, nullptr, s.diz, dc0 ? dc0 : s.tmp0, T, BN, mode,
+                                     nullptr, st));
   mark(st, "scan_bwd_cell");
   const RowPlan rp = row_plan(R, n);
   k_lstm_dpre<<<dim3((unsigned)rp.nbx, (unsigned)rp.gy), rp.thr, 0, st>>>(gf, gi, go, gz, c0, s.diz, dh, cache->c,

@@ -410,12 +410,15 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
 // ---------------------------------------------------------------------------
 // backward (reverse time): arrays mu = lam shifted +1 row, dh, h shifted -1 row
 // ---------------------------------------------------------------------------
-template <class S, int VEC, int Q, int R, int NW, int STAGES>
+// GATED: a fourth staged array g (map_gate) multiplies the adjoint as it is
+// copied out of shared memory -- the scan runs on dh * g, so a gated layer
+// output h = g * c needs no separate dc = dh * g pass (GILR-LSTM / QRNN).
+template <class S, int VEC, int Q, int R, int NW, int STAGES, bool GATED = false>
 __global__ void __launch_bounds__((NW + 2) * 32, 1)
 k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ CUtensorMap map_dh,
-          const __grid_constant__ CUtensorMap map_h, const ChainArgs<S> a, const ChainWs ws,
-          const long long ntiles) {
-  using Cfg = TmaCfg<S, VEC, Q, R, NW, STAGES, 3>;
+          const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_gate,
+          const ChainArgs<S> a, const ChainWs ws, const long long ntiles) {
+  using Cfg = TmaCfg<S, VEC, Q, R, NW, STAGES, GATED ? 4 : 3>;
   using IO = VecIO<S, VEC>;
   constexpr int G = Cfg::G, CPW = Cfg::CPW, L = Cfg::L;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -433,6 +436,7 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
       prefetch_tmap(&map_lam);
       prefetch_tmap(&map_dh);
       prefetch_tmap(&map_h);
+      if (GATED) prefetch_tmap(&map_gate);
       const uint64_t pol = policy_evict_first(), pol_keep = policy_evict_last();
       for (int n = 0;; ++n) {
         const int s = n % STAGES;
@@ -457,6 +461,7 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
           tma_load_2d(sm.arr(s, 1) + b * Cfg::BOX_ROWS * CPW, &map_dh, c0, rb, sm.full(s), pol);
           tma_load_2d(sm.arr(s, 2) + b * Cfg::BOX_ROWS * CPW, &map_h, c0, rb - 1, sm.full(s),
                       keep ? pol_keep : pol);
+          if (GATED) tma_load_2d(sm.arr(s, GATED ? 3 : 0) + b * Cfg::BOX_ROWS * CPW, &map_gate, c0, rb, sm.full(s), pol);
         }
       }
     }
@@ -485,6 +490,7 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
     const S* smu = sm.arr(s, 0) + seg * R * CPW + q * VEC;
     const S* sdh = sm.arr(s, 1) + seg * R * CPW + q * VEC;
     const S* shp = sm.arr(s, 2) + seg * R * CPW + q * VEC;
+    const S* sg = sm.arr(s, GATED ? 3 : 0) + seg * R * CPW + q * VEC;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int t = t0 + i;
@@ -492,7 +498,7 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
           mu[i][v] = smu[i * CPW + v];
-          dh[i][v] = sdh[i * CPW + v];
+          dh[i][v] = GATED ? sdh[i * CPW + v] * sg[i * CPW + v] : sdh[i * CPW + v];
           hp[i][v] = shp[i * CPW + v];
         }
         const int mk = mu_kind(t, Ti, se);

@@ -15,9 +15,21 @@ cudaError_t launch_tma_bwd<float>(const ChainPlan& p, const BwdCall<float>& c, c
   if ((e = make_tmap_2d(&mh, c.h, false, c.W, c.T, p.box_cols, p.box_rows)) != cudaSuccess) return e;
   const auto a = bwd_args<float>(p, c);
   const auto d = to_dev(w);
+  if (c.gate != nullptr) {  // gated adjoint: the default configuration only (capi falls back otherwise)
+    using GCfg = linrec_dev::TmaCfg<float, 4, 32, 12, 8, 1, 4>;
+    auto kern = linrec_dev::k_tma_bwd<float, 4, 32, 12, 8, 1, true>;
+    if (!(p.q == 32 && p.r == 12 && p.stages == 1 && p.nw == 8)) return cudaErrorNotSupported;
+    static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         GCfg::SMEM);
+    if (attr != cudaSuccess) return attr;
+    CUtensorMap mg;
+    if ((e = make_tmap_2d(&mg, c.gate, false, c.W, c.T, p.box_cols, p.box_rows)) != cudaSuccess) return e;
+    kern<<<p.grid, p.threads, GCfg::SMEM, st>>>(ml, md, mh, mg, a, d, p.ntiles);
+    return cudaGetLastError();
+  }
 #define X(Q, R, ST, NW)                                                                  \
   if (p.q == Q && p.r == R && p.stages == ST && p.nw == NW) {                                      \
-    BWD_KERN(Q, R, ST, NW)<<<p.grid, p.threads, p.smem, st>>>(ml, md, mh, a, d, p.ntiles); \
+    BWD_KERN(Q, R, ST, NW)<<<p.grid, p.threads, p.smem, st>>>(ml, md, mh, md, a, d, p.ntiles); \
     return cudaGetLastError();                                                       \
   }
   LINREC_TMA_BWD_TABLE(X)

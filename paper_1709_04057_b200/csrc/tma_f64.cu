@@ -37,7 +37,7 @@ cudaError_t launch_tma_bwd<double>(const ChainPlan& p, const BwdCall<double>& c,
   const auto d = to_dev(w);
 #define X(Q, R, ST, NW)                                                                \
   if (p.q == Q && p.r == R && p.stages == ST && p.nw == NW) {                                    \
-    BWD64(Q, R, ST, NW)<<<p.grid, p.threads, p.smem, st>>>(ml, md, mh, a, d, p.ntiles); \
+    BWD64(Q, R, ST, NW)<<<p.grid, p.threads, p.smem, st>>>(ml, md, mh, md, a, d, p.ntiles); \
     return cudaGetLastError();                                                     \
   }
   LINREC_TMA_F64_BWD_TABLE(X)
