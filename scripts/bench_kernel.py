@@ -85,7 +85,7 @@ def median_rep_us(fn, warmup, reps, stream, per_graph=20):
     return statistics.median(ev[2 * r].elapsed_time(ev[2 * r + 1]) * 1e3 / per_graph for r in range(reps))
 
 
-def main():
+def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--seq-lens", default="16,256,4096,65536")
     ap.add_argument("--features", default="4,32,128")
@@ -94,7 +94,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "bench_kernel_r02.csv"))
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -143,6 +143,7 @@ def main():
         for T, n, b, w, impl, eps, sp, _ in rows:
             f.write(f"{T},{n},{b},{w},{impl},{eps:.9g},{sp:.9g}\n")
     print(f"wrote {args.out}")
+    return rows, sums
 
 
 if __name__ == "__main__":
