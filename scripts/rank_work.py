@@ -96,6 +96,28 @@ e2[1].record()
 torch.cuda.synchronize()
 print(f"N={N} one-graph step: {e2[0].elapsed_time(e2[1]) / reps * 1e3:.1f} us per rank-step "
       f"(7x over the 1-GPU C4 step needs <= {721.3 / 7:.0f} us)", flush=True)
+# the peer-exchange path has no compose launch: the fix-up CTAs fold the
+# peers' aggregates from their mailboxes (p2p_impl.cuh::compose_chunk); here
+# c_in / y_in stay as computed above
+with torch.cuda.stream(s2):
+    st = s2.cuda_stream
+    gstep2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gstep2, stream=s2):
+        capi.segment_scan(p(lam), p(x), None, p(h), p(spf), p(agg), Tl, W, 4, ws.handle, st)
+        capi.segment_fixup(p(lam), p(h), p(spf), p(c_in), Tl, W, rf, 4, st)
+        capi.segment_scan_backward(p(lam), p(hprev), p(h), p(dh), p(ones), p(dlam), p(dx), p(dh0), p(spb), p(agg),
+                                   Tl, W, 4, ws.handle, st)
+        capi.segment_fixup_backward(p(lam), p(hprev), p(h), p(ones), p(spb), p(y_in), p(dlam), p(dx), Tl, W, rb, 4,
+                                    st)
+torch.cuda.synchronize()
+st = st_saved
+e2[0].record()
+for _ in range(reps):
+    gstep2.replay()
+e2[1].record()
+torch.cuda.synchronize()
+print(f"N={N} one-graph step without the compose launches (as the peer-exchange path): "
+      f"{e2[0].elapsed_time(e2[1]) / reps * 1e3:.1f} us per rank-step", flush=True)
 # per kernel (each launch its own graph, replayed back to back in step order)
 parts = {
     "fwd scan": lambda: capi.segment_scan(p(lam), p(x), None, p(h), p(spf), p(agg), Tl, W, 4, ws.handle, st),
