@@ -6,6 +6,7 @@
 #include "linrec_cuda.h"
 
 #include <cuda_runtime.h>
+#include <immintrin.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -405,6 +406,41 @@ constexpr size_t kChunkBytes = size_t(64) << 20;  // per array per chunk
 // threads (the calling thread takes a share), so the copies and the page
 // faults of freshly allocated outputs run at host-memory rather than
 // single-core speed while the DMA engines move the previous chunk.
+// Host copy for the staging pool: non-temporal (streaming) AVX2 stores for
+// large ranges, so a pageable -> pinned copy moves 2 bytes of host DRAM
+// traffic per byte (read source, write destination) instead of 3 (a cached
+// store first reads the destination line) -- the pageable e2e path is bound
+// by host DRAM bandwidth, which the DMA engines share.  LINREC_NT_COPY=0
+// falls back to memcpy.
+__attribute__((target("avx2"))) void stream_copy_avx2(char* dst, const char* src, size_t n) {
+  const size_t head = (32 - (reinterpret_cast<uintptr_t>(dst) & 31)) & 31;
+  if (head) {
+    std::memcpy(dst, src, head);
+    dst += head;
+    src += head;
+    n -= head;
+  }
+  size_t i = 0;
+  for (; i + 128 <= n; i += 128) {
+    const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i));
+    const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 32));
+    const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 64));
+    const __m256i d = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 96));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), a);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 32), b);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 64), c);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 96), d);
+  }
+  if (i < n) std::memcpy(dst + i, src + i, n - i);
+  _mm_sfence();
+}
+
+void stage_copy(char* dst, const char* src, size_t n) {
+  static const bool nt = linrec_impl::env_int("LINREC_NT_COPY", 1) != 0 && __builtin_cpu_supports("avx2");
+  if (nt && n >= (size_t(1) << 16)) stream_copy_avx2(dst, src, n);
+  else std::memcpy(dst, src, n);
+}
+
 class CopyPool {
  public:
   explicit CopyPool(int n) {
@@ -448,8 +484,8 @@ class CopyPool {
       const size_t n = std::get<2>(j);
       const size_t a = std::max(lo, off), b = std::min(hi, off + n);
       if (a < b)
-        std::memcpy(static_cast<char*>(std::get<0>(j)) + (a - off), static_cast<const char*>(std::get<1>(j)) + (a - off),
-                    b - a);
+        stage_copy(static_cast<char*>(std::get<0>(j)) + (a - off), static_cast<const char*>(std::get<1>(j)) + (a - off),
+                   b - a);
       off += n;
     }
   }
