@@ -261,17 +261,31 @@ class PeerMailboxes:
         self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
         nbytes = lib.linrec_p2p_mailbox_bytes(W, self.world)
         own, handle = C.c_void_p(), C.create_string_buffer(64)
-        capi.check(lib.linrec_ipc_alloc(nbytes, C.byref(own), handle))
-        self.own = own.value
+        # no rank raises before the collectives: a failure is recorded
+        # (self.error) and every rank still takes part, so the caller can
+        # agree on a fallback (SequenceShardedScan, exchange="auto")
+        self.error = None
+        rc = lib.linrec_ipc_alloc(nbytes, C.byref(own), handle)
+        if rc != capi.OK:
+            self.error = capi.LinrecError(rc, lib.linrec_last_error().decode())
+        self.own = own.value if rc == capi.OK else None
         handles = [None] * self.world
-        dist.all_gather_object(handles, handle.raw, group=group)
+        dist.all_gather_object(handles, handle.raw if rc == capi.OK else None, group=group)
         self.opened, ptrs = [], []
         for q, h in enumerate(handles):
             if q == self.rank:
-                ptrs.append(self.own)
+                ptrs.append(self.own or 0)
                 continue
             p = C.c_void_p()
-            capi.check(lib.linrec_ipc_open(h, C.byref(p)))
+            if h is None:
+                self.error = self.error or RuntimeError(f"rank {q} could not allocate its mailbox")
+                ptrs.append(0)
+                continue
+            rc = lib.linrec_ipc_open(h, C.byref(p))
+            if rc != capi.OK:
+                self.error = self.error or capi.LinrecError(rc, lib.linrec_last_error().decode())
+                ptrs.append(0)
+                continue
             self.opened.append(p.value)
             ptrs.append(p.value)
         self.ptrs = torch.tensor(ptrs, dtype=torch.int64, device=device)  # device array of mailbox pointers
@@ -351,7 +365,23 @@ class SequenceShardedScan:
         self.hprev = None
         use_p2p = exchange == "p2p" or (exchange == "auto" and backend is None and self.world > 1
                                         and _same_node(self.group))
-        self.mb = PeerMailboxes(W, self.group, dev) if use_p2p else None
+        self.mb = None
+        if use_p2p:
+            # every rank must agree on the exchange: a rank whose IPC setup
+            # fails makes all of them fall back to the all-gather ("auto" only)
+            self.mb = PeerMailboxes(W, self.group, dev)
+            err = self.mb.error
+            if exchange == "auto":
+                ok = torch.tensor([0.0 if err is not None else 1.0],
+                                  device=dev if dist.get_backend(self.group) == "nccl" else "cpu")
+                dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+                if ok.item() < 1.0:
+                    self.mb.close()
+                    self.mb = None
+                    use_p2p = False
+            elif err is not None:
+                self.mb.close()
+                raise err
         self.exchange = "p2p" if use_p2p else "collective"
         # kernels launched per step on this rank (for bench.py's gpu_launches)
         r, R = self.rank, self.world

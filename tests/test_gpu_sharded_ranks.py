@@ -22,7 +22,7 @@ def _port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, T, W, lo, hi, seed, q, exchange="auto", reps=1):
+def _worker(rank, world, port, T, W, lo, hi, seed, q, exchange="auto", reps=1, fail_rank=None):
     import sys
     import torch.distributed as dist
     sys.path.insert(0, ROOT)
@@ -40,8 +40,12 @@ def _worker(rank, world, port, T, W, lo, hi, seed, q, exchange="auto", reps=1):
         cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
         L, X, DH, H0 = cu(lam[s:e]), cu(x[s:e]), cu(dh[s:e]), cu(h0)
         H, DL, DX, DH0 = torch.empty_like(L), torch.empty_like(L), torch.empty_like(L), torch.zeros_like(H0)
+        if rank == fail_rank:  # fault injection: this rank's CUDA-IPC mailbox allocation fails
+            from paper_1709_04057_b200 import capi
+            capi.lib.linrec_ipc_alloc = lambda *a: capi.ERR_CUDA
         run = SequenceShardedScan(T, W, stream=torch.cuda.current_stream(), exchange=exchange)
-        assert run.exchange == ("collective" if exchange == "collective" else "p2p")
+        want = "collective" if exchange == "collective" or fail_rank is not None else "p2p"
+        assert run.exchange == want, (rank, run.exchange)
         for _ in range(reps):  # repeated steps reuse the mailboxes (epochs, acks)
             run.forward(L, X, H0, H)
             run.backward(L, H0, H, DH, DL, DX, DH0)
@@ -52,20 +56,13 @@ def _worker(rank, world, port, T, W, lo, hi, seed, q, exchange="auto", reps=1):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("exchange,reps", [("p2p", 3), ("collective", 1)])
-@pytest.mark.parametrize("world,T,W,lo,hi", [(2, 40000, 128, 0.05, 0.95), (3, 30001, 64, 0.99, 1.0),
-                                             (2, 5000, 12, -1.0, 1.0),
-                                             (3, 9000, 384, 0.05, 0.95)])  # W > 256: fold kernel publishes
-def test_sequence_sharded_ranks_on_gpu(oracle, world, T, W, lo, hi, exchange, reps):
+def _run_ranks(world, T, W, lo, hi, exchange, reps, fail_rank=None):
     import torch.multiprocessing as mp
-    from oracle.oracle import max_rel_error
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
     seed = T + W
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, T, W, lo, hi, seed, q, exchange, reps))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, T, W, lo, hi, seed, q, exchange, reps, fail_rank))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -73,6 +70,11 @@ def test_sequence_sharded_ranks_on_gpu(oracle, world, T, W, lo, hi, exchange, re
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
+    return seed, outs
+
+
+def _check_ranks(oracle, outs, seed, T, W, lo, hi):
+    from oracle.oracle import max_rel_error
     rng = np.random.default_rng(seed)
     lam = rng.uniform(lo, hi, (T, W)).astype(np.float32)
     x = rng.uniform(-1, 1, (T, W)).astype(np.float32)
@@ -87,6 +89,30 @@ def test_sequence_sharded_ranks_on_gpu(oracle, world, T, W, lo, hi, exchange, re
         assert max_rel_error(DX, g[1][s:e]) <= 1e-5, rank
         if rank == 0:
             assert max_rel_error(DH0, g[2]) <= 1e-5
+
+
+@pytest.mark.parametrize("world,fail_rank", [(2, 1), (3, 0)])
+def test_mailbox_failure_falls_back_on_every_rank(oracle, world, fail_rank):
+    """exchange="auto": when one rank cannot set up its CUDA-IPC mailbox,
+    every rank agrees (an all-reduce of the setup flag) on the all-gather
+    exchange instead of hanging in the peer-memory protocol, and the results
+    still match the oracle."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    T, W = 20000, 64
+    seed, outs = _run_ranks(world, T, W, 0.05, 0.95, "auto", 2, fail_rank)
+    _check_ranks(oracle, outs, seed, T, W, 0.05, 0.95)
+
+
+@pytest.mark.parametrize("exchange,reps", [("p2p", 3), ("collective", 1)])
+@pytest.mark.parametrize("world,T,W,lo,hi", [(2, 40000, 128, 0.05, 0.95), (3, 30001, 64, 0.99, 1.0),
+                                             (2, 5000, 12, -1.0, 1.0),
+                                             (3, 9000, 384, 0.05, 0.95)])  # W > 256: fold kernel publishes
+def test_sequence_sharded_ranks_on_gpu(oracle, world, T, W, lo, hi, exchange, reps):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    seed, outs = _run_ranks(world, T, W, lo, hi, exchange, reps)
+    _check_ranks(oracle, outs, seed, T, W, lo, hi)
 
 
 @pytest.mark.parametrize("workload,launch", [("c4", "torchrun"), ("c2", "torchrun"), ("c5", "self")])
