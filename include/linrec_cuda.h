@@ -555,6 +555,83 @@ int linrec_qrnn_backward_f32(const float* W, const float* x, const float* c0, co
                              int64_t m, int64_t n, int64_t k, int mode, int precision, void* scratch,
                              size_t scratch_bytes, void* stream);
 
+/* ---- the same layers in double precision ---------------------------------- *
+ * layers.hpp is templated on S and proj/tests/test_layers.cpp runs it in
+ * double.  Same buffers, layouts, NULL rules and accumulate semantics as the
+ * _f32 entry points above (caches: gates as activated planes); the
+ * projections run on a CUDA-core fp64 GEMM (linrec_gemm_f64, no tensor-core
+ * fp64 operand type on the tcgen05 TF32 path) and the recurrences on
+ * linrec_scan_f64 / linrec_scan_backward_f64.  m and n may be any width.
+ * No precision argument: every product is fp64. */
+typedef struct linrec_gilr_params_f64 { /* GilrParams<double> (layers.hpp:30-40) */
+  const double* U;
+  const double* V;
+  const double* b_g;
+  const double* b_z;
+  int act;
+} linrec_gilr_params_f64;
+
+typedef struct linrec_gilr_grads_f64 { /* GilrGrads<double> (layers.hpp:66-76) */
+  double* U;
+  double* V;
+  double* b_g;
+  double* b_z;
+} linrec_gilr_grads_f64;
+
+typedef struct linrec_gilr_lstm_params_f64 { /* GilrLstmParams<double> (layers.hpp:146-160) */
+  linrec_gilr_params_f64 surrogate;
+  const double* U;
+  const double* V;
+  const double* bias;
+} linrec_gilr_lstm_params_f64;
+
+typedef struct linrec_gilr_lstm_grads_f64 { /* GilrLstmGrads<double> (layers.hpp:192-211) */
+  linrec_gilr_grads_f64 surrogate;
+  double* U;
+  double* V;
+  double* bias;
+} linrec_gilr_lstm_grads_f64;
+
+typedef struct linrec_gilr_lstm_cache_f64 { /* GilrLstmCache<double> (layers.hpp:183-188) */
+  double* sg;
+  double* si;
+  double* htil;
+  double* gates;
+  double* c;
+} linrec_gilr_lstm_cache_f64;
+
+/* C[M][N] (+)= sum_k A(m,k) * B(n,k) in fp64 on the CUDA cores; operand
+ * layouts as linrec_gemm_f32 (a_mn / b_mn select MN-major). */
+int linrec_gemm_f64(const double* A, int a_mn, int64_t lda, const double* B, int b_mn, int64_t ldb, double* C,
+                    int64_t ldc, int64_t M, int64_t N, int64_t K, int accumulate, void* stream);
+
+size_t linrec_gilr_scratch_bytes_f64(int64_t T, int64_t b, int64_t m, int64_t n);
+size_t linrec_gilr_lstm_scratch_bytes_f64(int64_t T, int64_t b, int64_t m, int64_t n);
+size_t linrec_qrnn_scratch_bytes_f64(int64_t T, int64_t b, int64_t m, int64_t n, int64_t k);
+int linrec_gilr_forward_f64(const linrec_gilr_params_f64* p, const double* x, const double* h0, double* h,
+                            double* g, double* i, int64_t T, int64_t b, int64_t m, int64_t n, int mode,
+                            void* scratch, size_t scratch_bytes, void* stream);
+int linrec_gilr_backward_f64(const linrec_gilr_params_f64* p, const double* x, const double* h0, const double* g,
+                             const double* i, const double* h, const double* dh, linrec_gilr_grads_f64* grads,
+                             double* dx, double* dh0, int64_t T, int64_t b, int64_t m, int64_t n, int mode,
+                             void* scratch, size_t scratch_bytes, void* stream);
+int linrec_gilr_lstm_forward_f64(const linrec_gilr_lstm_params_f64* p, const double* x, const double* htil0,
+                                 const double* c0, double* h, const linrec_gilr_lstm_cache_f64* cache, int64_t T,
+                                 int64_t b, int64_t m, int64_t n, int mode, void* scratch, size_t scratch_bytes,
+                                 void* stream);
+int linrec_gilr_lstm_backward_f64(const linrec_gilr_lstm_params_f64* p, const double* x, const double* htil0,
+                                  const double* c0, const linrec_gilr_lstm_cache_f64* cache, const double* dh,
+                                  linrec_gilr_lstm_grads_f64* grads, double* dx, double* dhtil0, double* dc0,
+                                  int64_t T, int64_t b, int64_t m, int64_t n, int mode, void* scratch,
+                                  size_t scratch_bytes, void* stream);
+int linrec_qrnn_forward_f64(const double* W, const double* bias, const double* x, const double* c0, double* h,
+                            double* gates, double* c, int64_t T, int64_t b, int64_t m, int64_t n, int64_t k, int mode,
+                            void* scratch, size_t scratch_bytes, void* stream);
+int linrec_qrnn_backward_f64(const double* W, const double* x, const double* c0, const double* gates, const double* c,
+                             const double* dh, double* dW, double* dbias, double* dx, double* dc0, int64_t T,
+                             int64_t b, int64_t m, int64_t n, int64_t k, int mode, void* scratch,
+                             size_t scratch_bytes, void* stream);
+
 /* ---- training loop (training.hpp) ----------------------------------------- *
  * The reference's synthetic long-dependency task: generate_batch (:30-43)
  * from the reference Rng's counter-based splitmix64 stream (rng.hpp:21-27;

@@ -231,6 +231,42 @@ class Oracle:
             setattr(self, f"_layers_{sfx}", True)
         return sfx
 
+    def gilr_forward(self, P, x, h0=None, act=0):
+        """gilr_forward (layers.hpp:78-100).  P: dict U, V, b_g, b_z.
+        Returns h and the cache dict (g, i)."""
+        x = np.ascontiguousarray(x)
+        dt = x.dtype
+        sfx = self._layer_fns(dt)
+        T, b, m = x.shape
+        n = P["U"].shape[0]
+        P = {k: np.ascontiguousarray(v, dtype=dt) for k, v in P.items()}
+        h0 = None if h0 is None else np.ascontiguousarray(h0, dtype=dt)
+        h = np.empty((T, b, n), dt)
+        cache = {"g": np.empty((T, b, n), dt), "i": np.empty((T, b, n), dt)}
+        getattr(self.lib, f"oracle_gilr_forward_{sfx}")(
+            _ptr(x), _ptr(P["U"]), _ptr(P["V"]), _ptr(P["b_g"]), _ptr(P["b_z"]), _ptr(h0), act, _ptr(cache["g"]),
+            _ptr(cache["i"]), _ptr(h), T, b, m, n)
+        return h, cache
+
+    def gilr_backward(self, P, x, h0, cache, h, dh, act=0):
+        """gilr_backward (layers.hpp:102-133).  Returns (grads dict, dx, dh0);
+        the parameter gradients start at zero."""
+        x = np.ascontiguousarray(x)
+        dt = x.dtype
+        sfx = self._layer_fns(dt)
+        T, b, m = x.shape
+        n = P["U"].shape[0]
+        P = {k: np.ascontiguousarray(v, dtype=dt) for k, v in P.items()}
+        h0 = None if h0 is None else np.ascontiguousarray(h0, dtype=dt)
+        g = {k: np.zeros_like(v) for k, v in P.items()}
+        dx = np.empty((T, b, m), dt)
+        dh0 = np.empty((b, n), dt)
+        getattr(self.lib, f"oracle_gilr_backward_{sfx}")(
+            _ptr(x), _ptr(P["U"]), _ptr(P["V"]), _ptr(h0), act, _ptr(cache["g"]), _ptr(cache["i"]),
+            _ptr(np.ascontiguousarray(h, dtype=dt)), _ptr(np.ascontiguousarray(dh, dtype=dt)), _ptr(g["U"]),
+            _ptr(g["V"]), _ptr(g["b_g"]), _ptr(g["b_z"]), _ptr(dx), _ptr(dh0), T, b, m, n)
+        return g, dx, dh0
+
     def gilr_lstm_forward(self, P, x, htil0=None, c0=None):
         """layers.hpp:245-293.  P: dict sU, sV, sbg, sbz, U, V, bias.
         Returns h and the cache dict (sg, si, htil, gates, c)."""

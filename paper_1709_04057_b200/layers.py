@@ -12,7 +12,11 @@ Parameters are row-major exactly as GilrParams / GilrLstmParams (gate blocks
 f, i, o, z stacked along the rows of U, V, bias).  Gradients ACCUMULATE into
 the grads objects (tensor.hpp:272-296); dx is returned.  ``precision`` is
 "fp32" (3xTF32 on the tensor cores, fp32-grade; default) or "tf32" (one TF32
-pass, ~1e-3 relative).  Inputs: x [T, b, m] fp32 contiguous.  Widths that
+pass, ~1e-3 relative).  Inputs: x [T, b, m] fp32 contiguous, or fp64: then
+every parameter, state and adjoint is fp64 too and the call runs the
+double-precision entry points (linrec_*_f64: fp64 CUDA-core GEMMs and the
+fp64 scans; ``precision`` does not apply) -- the reference's layers are
+templated on S and its test_layers.cpp runs them in double.  Widths that
 are not multiples of 4 (the kernels' 16-byte TMA rows) are zero-padded here:
 padded input columns meet zero weights and padded hidden units start at 0,
 see only zero weights and so stay exactly 0 -- outputs and gradients are the
@@ -79,6 +83,24 @@ def _bind():
     qtail = [_i64] * 5 + [_int, _int, _vp, C.c_size_t, _vp]
     lib.linrec_qrnn_forward_f32.argtypes = [_vp] * 7 + qtail
     lib.linrec_qrnn_backward_f32.argtypes = [_vp] * 10 + qtail
+    # fp64 entry points: the same structs (void* fields), no precision argument
+    for nm in ("linrec_gilr_scratch_bytes_f64", "linrec_gilr_lstm_scratch_bytes_f64"):
+        getattr(lib, nm).restype = C.c_size_t
+        getattr(lib, nm).argtypes = [_i64] * 4
+    lib.linrec_qrnn_scratch_bytes_f64.restype = C.c_size_t
+    lib.linrec_qrnn_scratch_bytes_f64.argtypes = [_i64] * 5
+    tail64 = [_i64] * 4 + [_int, _vp, C.c_size_t, _vp]
+    lib.linrec_gilr_forward_f64.argtypes = [C.POINTER(_GilrParamsC)] + [_vp] * 5 + tail64
+    lib.linrec_gilr_backward_f64.argtypes = ([C.POINTER(_GilrParamsC)] + [_vp] * 6 + [C.POINTER(_GilrGradsC)]
+                                             + [_vp] * 2 + tail64)
+    lib.linrec_gilr_lstm_forward_f64.argtypes = ([C.POINTER(_LstmParamsC)] + [_vp] * 4 + [C.POINTER(_LstmCacheC)]
+                                                 + tail64)
+    lib.linrec_gilr_lstm_backward_f64.argtypes = ([C.POINTER(_LstmParamsC)] + [_vp] * 3 + [C.POINTER(_LstmCacheC)]
+                                                  + [_vp] + [C.POINTER(_LstmGradsC)] + [_vp] * 3 + tail64)
+    qtail64 = [_i64] * 5 + [_int, _vp, C.c_size_t, _vp]
+    lib.linrec_qrnn_forward_f64.argtypes = [_vp] * 7 + qtail64
+    lib.linrec_qrnn_backward_f64.argtypes = [_vp] * 10 + qtail64
+    lib.linrec_gemm_f64.argtypes = [_vp, _int, _i64, _vp, _int, _i64, _vp, _i64, _i64, _i64, _i64, _int, _vp]
     lib._layers_bound = True
     return lib
 
@@ -104,23 +126,28 @@ def _p(t):
     return None if t is None else t.data_ptr()
 
 
-def _check_f32(t, name):
+def _check_f32(t, name, dtype=None):
+    """CUDA, C-contiguous, and float32 -- or `dtype` (the call's dtype, taken
+    from x: float32 or float64, no silent cast, linrec_py.cpp:21-29)."""
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError(f"{name} must be a CUDA tensor")
-    if t.dtype != torch.float32:
-        raise TypeError(f"{name} must be float32 (the layers' device path is fp32)")
+    want = torch.float32 if dtype is None else dtype
+    if want not in (torch.float32, torch.float64):
+        raise TypeError(f"{name}: the layers run float32 or float64, got {want}")
+    if t.dtype != want:
+        raise TypeError(f"{name} must be {str(want).replace('torch.', '')} like x")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be C-contiguous")
 
 
-def _check_shape(t, name, shape):
+def _check_shape(t, name, shape, dtype=None):
     """The C ABI sees raw pointers only: an initial state, adjoint or cache
     of the wrong shape would be an out-of-bounds device access, so reject it
     with the reference's contract error (layers.hpp check_same_shape /
     tensor.hpp:168-189)."""
     if t is None:
         return
-    _check_f32(t, name)
+    _check_f32(t, name, dtype)
     if list(t.shape) != list(shape):
         raise RuntimeError(f"{name}: shape mismatch, {list(shape)} vs {list(t.shape)}")
 
@@ -240,10 +267,11 @@ class GilrLstmCache:
     gates: torch.Tensor = None
     c: torch.Tensor = None
 
-    def allocate(self, T, b, n, device):
-        if self.c is not None and tuple(self.c.shape) == (T, b, n) and self.c.device == torch.device(device):
+    def allocate(self, T, b, n, device, dtype=torch.float32):
+        if (self.c is not None and tuple(self.c.shape) == (T, b, n) and self.c.device == torch.device(device)
+                and self.c.dtype == dtype):
             return self  # reuse (e.g. one cache per layer across training steps)
-        kw = dict(dtype=torch.float32, device=device)
+        kw = dict(dtype=dtype, device=device)
         self.sg = torch.empty(T, b, n, **kw)
         self.si = torch.empty(T, b, n, **kw)
         self.htil = torch.empty(T + 1, b, n, **kw)
@@ -251,14 +279,14 @@ class GilrLstmCache:
         self.c = torch.empty(T, b, n, **kw)
         return self
 
-    def check(self, T, b, n):
+    def check(self, T, b, n, dtype=None):
         """Shapes a backward pass reads through raw pointers."""
         for t, nm, shp in ((self.sg, "cache.sg", (T, b, n)), (self.si, "cache.si", (T, b, n)),
                            (self.htil, "cache.htil", (T + 1, b, n)), (self.gates, "cache.gates", (4, T, b, n)),
                            (self.c, "cache.c", (T, b, n))):
             if t is None:
                 raise RuntimeError(f"{nm}: cache not filled by a forward pass")
-            _check_shape(t, nm, shp)
+            _check_shape(t, nm, shp, dtype)
 
     def surrogate_h(self):
         return self.htil[1:]
@@ -273,32 +301,37 @@ class GilrLstmCache:
         return _LstmCacheC(_p(self.sg), _p(self.si), _p(self.htil), _p(self.gates), _p(self.c))
 
 
-def _uniform(gen, rows, cols, scale, device):
+def _uniform(gen, rows, cols, scale, device, dtype=torch.float32):
     return ((torch.rand(rows, cols, generator=gen, dtype=torch.float64) * 2 - 1) * scale).to(
-        device=device, dtype=torch.float32)
+        device=device, dtype=dtype)
 
 
 def gilr_init(gen: torch.Generator, m: int, n: int, gate_bias: float = 1.0, device="cuda",
-              act: str = "tanh") -> GilrParams:
+              act: str = "tanh", dtype=torch.float32) -> GilrParams:
     """gilr_init (layers.hpp:42-55): U, V ~ U(+-1/sqrt(m)), b_g = gate_bias, b_z = 0."""
     s = 1.0 / math.sqrt(m)
-    return GilrParams(_uniform(gen, n, m, s, device), _uniform(gen, n, m, s, device),
-                      torch.full((n,), gate_bias, dtype=torch.float32, device=device),
-                      torch.zeros(n, dtype=torch.float32, device=device), act)
+    return GilrParams(_uniform(gen, n, m, s, device, dtype), _uniform(gen, n, m, s, device, dtype),
+                      torch.full((n,), gate_bias, dtype=dtype, device=device),
+                      torch.zeros(n, dtype=dtype, device=device), act)
 
 
-def gilr_lstm_init(gen: torch.Generator, m: int, n: int, gate_bias: float = 1.0, device="cuda") -> GilrLstmParams:
+def gilr_lstm_init(gen: torch.Generator, m: int, n: int, gate_bias: float = 1.0, device="cuda",
+                   dtype=torch.float32) -> GilrLstmParams:
     """gilr_lstm_init (layers.hpp:165-176): surrogate as gilr_init, U ~ U(+-1/sqrt(n)),
     V ~ U(+-1/sqrt(m)), bias = gate_bias on the f block."""
-    sur = gilr_init(gen, m, n, gate_bias, device)
-    bias = torch.zeros(4 * n, dtype=torch.float32, device=device)
+    sur = gilr_init(gen, m, n, gate_bias, device, dtype=dtype)
+    bias = torch.zeros(4 * n, dtype=dtype, device=device)
     bias[:n] = gate_bias
-    return GilrLstmParams(sur, _uniform(gen, 4 * n, n, 1.0 / math.sqrt(n), device),
-                          _uniform(gen, 4 * n, m, 1.0 / math.sqrt(m), device), bias)
+    return GilrLstmParams(sur, _uniform(gen, 4 * n, n, 1.0 / math.sqrt(n), device, dtype),
+                          _uniform(gen, 4 * n, m, 1.0 / math.sqrt(m), device, dtype), bias)
+
+
+def _f64(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.dtype == torch.float64
 
 
 def _dims(x, n):
-    _check_f32(x, "x")
+    _check_f32(x, "x", x.dtype if _f64(x) else None)
     if x.dim() != 3:
         raise ValueError("x must have shape [T, batch, features]")
     T, b, m = x.shape
@@ -316,19 +349,24 @@ def _gilr_forward_core(p: GilrParams, x, h0=None, mode="parallel", precision="fp
     T, b, m, n = _dims(x, p.hidden())
     if m != p.input():
         raise RuntimeError("gilr_forward: input feature mismatch")
+    dt = x.dtype
     for t, nm in zip(p.tensors(), ("U", "V", "b_g", "b_z")):
-        _check_f32(t, nm)
-    _check_shape(h0, "h0", (b, n))
+        _check_f32(t, nm, dt)
+    _check_shape(h0, "h0", (b, n), dt)
     dev = x.device
-    h = torch.empty(T, b, n, dtype=torch.float32, device=dev)
+    h = torch.empty(T, b, n, dtype=dt, device=dev)
     g = torch.empty_like(h)
     i = torch.empty_like(h)
-    need = lib.linrec_gilr_scratch_bytes(T, b, m, n)
-    scr = _scratch_for(need, dev)
     pc = p._c()
-    _call(lib.linrec_gilr_forward_f32(C.byref(pc), _p(x), _p(h0), _p(h), _p(g), _p(i), T, b, m, n, MODE[mode],
-                                      PRECISION[precision], _p(scr), scr.numel(),
-                                      torch.cuda.current_stream(dev).cuda_stream))
+    st = torch.cuda.current_stream(dev).cuda_stream
+    if _f64(x):
+        scr = _scratch_for(lib.linrec_gilr_scratch_bytes_f64(T, b, m, n), dev)
+        _call(lib.linrec_gilr_forward_f64(C.byref(pc), _p(x), _p(h0), _p(h), _p(g), _p(i), T, b, m, n, MODE[mode],
+                                          _p(scr), scr.numel(), st))
+    else:
+        scr = _scratch_for(lib.linrec_gilr_scratch_bytes(T, b, m, n), dev)
+        _call(lib.linrec_gilr_forward_f32(C.byref(pc), _p(x), _p(h0), _p(h), _p(g), _p(i), T, b, m, n, MODE[mode],
+                                          PRECISION[precision], _p(scr), scr.numel(), st))
     if cache is not None:
         cache.g, cache.i, cache.h = g, i, h
     return h
@@ -339,19 +377,29 @@ def _gilr_backward_core(p: GilrParams, x, h0, cache: GilrCache, d_h, grads: Gilr
     """gilr_backward (layers.hpp:102-133): accumulates into ``grads``; returns (dx, dh0)."""
     lib = _bind()
     T, b, m, n = _dims(x, p.hidden())
-    _check_shape(d_h, "d_h", (T, b, n))
-    _check_shape(h0, "h0", (b, n))
+    dt = x.dtype
+    _check_shape(d_h, "d_h", (T, b, n), dt)
+    _check_shape(h0, "h0", (b, n), dt)
     for t, nm in ((cache.g, "cache.g"), (cache.i, "cache.i"), (cache.h, "cache.h")):
-        _check_shape(t, nm, (T, b, n))
+        _check_shape(t, nm, (T, b, n), dt)
+    for t, nm in zip(p.tensors() + grads.tensors(), ("U", "V", "b_g", "b_z") * 2):
+        if t is not None:
+            _check_f32(t, nm, dt)
     dev = x.device
-    dx = torch.empty(T, b, m, dtype=torch.float32, device=dev)
-    dh0 = torch.empty(b, n, dtype=torch.float32, device=dev) if want_dh0 else None
-    need = lib.linrec_gilr_scratch_bytes(T, b, m, n)
-    scr = _scratch_for(need, dev)
+    dx = torch.empty(T, b, m, dtype=dt, device=dev)
+    dh0 = torch.empty(b, n, dtype=dt, device=dev) if want_dh0 else None
     pc, gc = p._c(), grads._c()
-    _call(lib.linrec_gilr_backward_f32(C.byref(pc), _p(x), _p(h0), _p(cache.g), _p(cache.i), _p(cache.h), _p(d_h),
-                                       C.byref(gc), _p(dx), _p(dh0), T, b, m, n, MODE[mode], PRECISION[precision],
-                                       _p(scr), scr.numel(), torch.cuda.current_stream(dev).cuda_stream))
+    st = torch.cuda.current_stream(dev).cuda_stream
+    if _f64(x):
+        scr = _scratch_for(lib.linrec_gilr_scratch_bytes_f64(T, b, m, n), dev)
+        _call(lib.linrec_gilr_backward_f64(C.byref(pc), _p(x), _p(h0), _p(cache.g), _p(cache.i), _p(cache.h),
+                                           _p(d_h), C.byref(gc), _p(dx), _p(dh0), T, b, m, n, MODE[mode], _p(scr),
+                                           scr.numel(), st))
+    else:
+        scr = _scratch_for(lib.linrec_gilr_scratch_bytes(T, b, m, n), dev)
+        _call(lib.linrec_gilr_backward_f32(C.byref(pc), _p(x), _p(h0), _p(cache.g), _p(cache.i), _p(cache.h),
+                                           _p(d_h), C.byref(gc), _p(dx), _p(dh0), T, b, m, n, MODE[mode],
+                                           PRECISION[precision], _p(scr), scr.numel(), st))
     return dx, dh0
 
 
@@ -363,21 +411,26 @@ def _gilr_lstm_forward_core(p: GilrLstmParams, x, htil0=None, c0=None, mode="par
     T, b, m, n = _dims(x, p.hidden())
     if m != p.input():
         raise RuntimeError("gilr_lstm_forward: input feature mismatch")
+    dt = x.dtype
     for t in p.tensors():
-        _check_f32(t, "parameter")
+        _check_f32(t, "parameter", dt)
     for t, nm in ((htil0, "htil0"), (c0, "c0")):
-        _check_shape(t, nm, (b, n))
+        _check_shape(t, nm, (b, n), dt)
     dev = x.device
     if cache is None:
         cache = GilrLstmCache()
-    cache.allocate(T, b, n, dev)
-    h = torch.empty(T, b, n, dtype=torch.float32, device=dev)
-    need = lib.linrec_gilr_lstm_scratch_bytes(T, b, m, n)
-    scr = _scratch_for(need, dev)
+    cache.allocate(T, b, n, dev, dt)
+    h = torch.empty(T, b, n, dtype=dt, device=dev)
     pc, cc = p._c(), cache._c()
-    _call(lib.linrec_gilr_lstm_forward_f32(C.byref(pc), _p(x), _p(htil0), _p(c0), _p(h), C.byref(cc), T, b, m, n,
-                                           MODE[mode], PRECISION[precision], _p(scr), scr.numel(),
-                                           torch.cuda.current_stream(dev).cuda_stream))
+    st = torch.cuda.current_stream(dev).cuda_stream
+    if _f64(x):
+        scr = _scratch_for(lib.linrec_gilr_lstm_scratch_bytes_f64(T, b, m, n), dev)
+        _call(lib.linrec_gilr_lstm_forward_f64(C.byref(pc), _p(x), _p(htil0), _p(c0), _p(h), C.byref(cc), T, b, m,
+                                               n, MODE[mode], _p(scr), scr.numel(), st))
+    else:
+        scr = _scratch_for(lib.linrec_gilr_lstm_scratch_bytes(T, b, m, n), dev)
+        _call(lib.linrec_gilr_lstm_forward_f32(C.byref(pc), _p(x), _p(htil0), _p(c0), _p(h), C.byref(cc), T, b, m,
+                                               n, MODE[mode], PRECISION[precision], _p(scr), scr.numel(), st))
     return h
 
 
@@ -387,21 +440,30 @@ def _gilr_lstm_backward_core(p: GilrLstmParams, x, htil0, c0, cache: GilrLstmCac
     returns (dx, d_htil0, d_c0)."""
     lib = _bind()
     T, b, m, n = _dims(x, p.hidden())
-    _check_shape(d_h, "d_h", (T, b, n))
+    dt = x.dtype
+    _check_shape(d_h, "d_h", (T, b, n), dt)
     for t, nm in ((htil0, "htil0"), (c0, "c0")):
-        _check_shape(t, nm, (b, n))
-    cache.check(T, b, n)
+        _check_shape(t, nm, (b, n), dt)
+    cache.check(T, b, n, dt)
+    for t in p.tensors() + grads.tensors():
+        if t is not None:
+            _check_f32(t, "parameter", dt)
     dev = x.device
-    dx = torch.empty(T, b, m, dtype=torch.float32, device=dev)
-    dht0 = torch.empty(b, n, dtype=torch.float32, device=dev) if want_initial else None
-    dc0 = torch.empty(b, n, dtype=torch.float32, device=dev) if want_initial else None
-    need = lib.linrec_gilr_lstm_scratch_bytes(T, b, m, n)
-    scr = _scratch_for(need, dev)
+    dx = torch.empty(T, b, m, dtype=dt, device=dev)
+    dht0 = torch.empty(b, n, dtype=dt, device=dev) if want_initial else None
+    dc0 = torch.empty(b, n, dtype=dt, device=dev) if want_initial else None
     pc, cc, gc = p._c(), cache._c(), grads._c()
-    _call(lib.linrec_gilr_lstm_backward_f32(C.byref(pc), _p(x), _p(htil0), _p(c0), C.byref(cc), _p(d_h),
-                                            C.byref(gc), _p(dx), _p(dht0), _p(dc0), T, b, m, n, MODE[mode],
-                                            PRECISION[precision], _p(scr), scr.numel(),
-                                            torch.cuda.current_stream(dev).cuda_stream))
+    st = torch.cuda.current_stream(dev).cuda_stream
+    if _f64(x):
+        scr = _scratch_for(lib.linrec_gilr_lstm_scratch_bytes_f64(T, b, m, n), dev)
+        _call(lib.linrec_gilr_lstm_backward_f64(C.byref(pc), _p(x), _p(htil0), _p(c0), C.byref(cc), _p(d_h),
+                                                C.byref(gc), _p(dx), _p(dht0), _p(dc0), T, b, m, n, MODE[mode],
+                                                _p(scr), scr.numel(), st))
+    else:
+        scr = _scratch_for(lib.linrec_gilr_lstm_scratch_bytes(T, b, m, n), dev)
+        _call(lib.linrec_gilr_lstm_backward_f32(C.byref(pc), _p(x), _p(htil0), _p(c0), C.byref(cc), _p(d_h),
+                                                C.byref(gc), _p(dx), _p(dht0), _p(dc0), T, b, m, n, MODE[mode],
+                                                PRECISION[precision], _p(scr), scr.numel(), st))
     return dx, dht0, dc0
 
 
@@ -450,13 +512,14 @@ class QrnnCache:
         return self.gates.permute(1, 2, 0, 3).reshape(self.gates.shape[1], self.gates.shape[2], -1)
 
 
-def qrnn_init(gen: torch.Generator, m: int, n: int, k: int, gate_bias: float = 1.0, device="cuda") -> QrnnParams:
+def qrnn_init(gen: torch.Generator, m: int, n: int, k: int, gate_bias: float = 1.0, device="cuda",
+              dtype=torch.float32) -> QrnnParams:
     """qrnn_init (layers.hpp:411-422): W_s ~ U(+-1/sqrt(m k)), bias = gate_bias on f."""
     if k < 1:
         raise RuntimeError("qrnn_init: window must be >= 1")
     s = 1.0 / math.sqrt(m * k)
-    W = torch.stack([_uniform(gen, 3 * n, m, s, device) for _ in range(k)])
-    bias = torch.zeros(3 * n, dtype=torch.float32, device=device)
+    W = torch.stack([_uniform(gen, 3 * n, m, s, device, dtype) for _ in range(k)])
+    bias = torch.zeros(3 * n, dtype=dtype, device=device)
     bias[:n] = gate_bias
     return QrnnParams(W.contiguous(), bias)
 
@@ -470,21 +533,26 @@ def _qrnn_forward_core(p: QrnnParams, x, c0=None, mode="parallel", precision="fp
         raise RuntimeError("qrnn_forward: input feature mismatch")
     if k > T:
         raise RuntimeError("qrnn_forward: filter window exceeds sequence length")
+    dt = x.dtype
     for t, nm in ((p.W, "W"), (p.bias, "bias")):
-        _check_f32(t, nm)
-    _check_shape(c0, "c0", (b, n))
+        _check_f32(t, nm, dt)
+    _check_shape(c0, "c0", (b, n), dt)
     dev = x.device
     if cache is None:
         cache = QrnnCache()
-    if cache.c is None or tuple(cache.c.shape) != (T, b, n):
-        cache.gates = torch.empty(3, T, b, n, dtype=torch.float32, device=dev)
-        cache.c = torch.empty(T, b, n, dtype=torch.float32, device=dev)
-    h = torch.empty(T, b, n, dtype=torch.float32, device=dev)
-    need = lib.linrec_qrnn_scratch_bytes(T, b, m, n, k)
-    scr = _scratch_for(need, dev)
-    _call(lib.linrec_qrnn_forward_f32(_p(p.W), _p(p.bias), _p(x), _p(c0), _p(h), _p(cache.gates), _p(cache.c),
-                                      T, b, m, n, k, MODE[mode], PRECISION[precision], _p(scr), scr.numel(),
-                                      torch.cuda.current_stream(dev).cuda_stream))
+    if cache.c is None or tuple(cache.c.shape) != (T, b, n) or cache.c.dtype != dt:
+        cache.gates = torch.empty(3, T, b, n, dtype=dt, device=dev)
+        cache.c = torch.empty(T, b, n, dtype=dt, device=dev)
+    h = torch.empty(T, b, n, dtype=dt, device=dev)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    if _f64(x):
+        scr = _scratch_for(lib.linrec_qrnn_scratch_bytes_f64(T, b, m, n, k), dev)
+        _call(lib.linrec_qrnn_forward_f64(_p(p.W), _p(p.bias), _p(x), _p(c0), _p(h), _p(cache.gates), _p(cache.c),
+                                          T, b, m, n, k, MODE[mode], _p(scr), scr.numel(), st))
+    else:
+        scr = _scratch_for(lib.linrec_qrnn_scratch_bytes(T, b, m, n, k), dev)
+        _call(lib.linrec_qrnn_forward_f32(_p(p.W), _p(p.bias), _p(x), _p(c0), _p(h), _p(cache.gates), _p(cache.c),
+                                          T, b, m, n, k, MODE[mode], PRECISION[precision], _p(scr), scr.numel(), st))
     return h
 
 
@@ -494,19 +562,28 @@ def _qrnn_backward_core(p: QrnnParams, x, c0, cache: QrnnCache, d_h, grads: Qrnn
     lib = _bind()
     T, b, m, n = _dims(x, p.hidden())
     k = p.window()
-    _check_shape(d_h, "d_h", (T, b, n))
-    _check_shape(c0, "c0", (b, n))
-    _check_shape(cache.gates, "cache.gates", (3, T, b, n))
-    _check_shape(cache.c, "cache.c", (T, b, n))
+    dt = x.dtype
+    _check_shape(d_h, "d_h", (T, b, n), dt)
+    _check_shape(c0, "c0", (b, n), dt)
+    _check_shape(cache.gates, "cache.gates", (3, T, b, n), dt)
+    _check_shape(cache.c, "cache.c", (T, b, n), dt)
+    for t, nm in ((p.W, "W"), (grads.W, "grads.W"), (grads.bias, "grads.bias")):
+        if t is not None:
+            _check_f32(t, nm, dt)
     dev = x.device
-    dx = torch.empty(T, b, m, dtype=torch.float32, device=dev)
-    dc0 = torch.empty(b, n, dtype=torch.float32, device=dev) if want_dc0 else None
-    need = lib.linrec_qrnn_scratch_bytes(T, b, m, n, k)
-    scr = _scratch_for(need, dev)
-    _call(lib.linrec_qrnn_backward_f32(_p(p.W), _p(x), _p(c0), _p(cache.gates), _p(cache.c), _p(d_h),
-                                       _p(grads.W), _p(grads.bias), _p(dx), _p(dc0), T, b, m, n, k, MODE[mode],
-                                       PRECISION[precision], _p(scr), scr.numel(),
-                                       torch.cuda.current_stream(dev).cuda_stream))
+    dx = torch.empty(T, b, m, dtype=dt, device=dev)
+    dc0 = torch.empty(b, n, dtype=dt, device=dev) if want_dc0 else None
+    st = torch.cuda.current_stream(dev).cuda_stream
+    if _f64(x):
+        scr = _scratch_for(lib.linrec_qrnn_scratch_bytes_f64(T, b, m, n, k), dev)
+        _call(lib.linrec_qrnn_backward_f64(_p(p.W), _p(x), _p(c0), _p(cache.gates), _p(cache.c), _p(d_h),
+                                           _p(grads.W), _p(grads.bias), _p(dx), _p(dc0), T, b, m, n, k, MODE[mode],
+                                           _p(scr), scr.numel(), st))
+    else:
+        scr = _scratch_for(lib.linrec_qrnn_scratch_bytes(T, b, m, n, k), dev)
+        _call(lib.linrec_qrnn_backward_f32(_p(p.W), _p(x), _p(c0), _p(cache.gates), _p(cache.c), _p(d_h),
+                                           _p(grads.W), _p(grads.bias), _p(dx), _p(dc0), T, b, m, n, k, MODE[mode],
+                                           PRECISION[precision], _p(scr), scr.numel(), st))
     return dx, dc0
 
 
@@ -565,7 +642,9 @@ class _Pad:
     def __init__(self, m, n):
         self.m, self.n, self.m4, self.n4 = m, n, _r4(m), _r4(n)
 
-    def needed(self):
+    def needed(self, x=None):
+        if _f64(x):  # the fp64 entry points take any width
+            return False
         return self.m4 != self.m or self.n4 != self.n
 
     def rows(self, t, blocks, cols, cols4):  # [blocks*n, cols] -> [blocks*n4, cols4]
@@ -609,7 +688,7 @@ class _Pad:
 def gilr_forward(p: GilrParams, x, h0=None, mode="parallel", precision="fp32", cache: GilrCache | None = None):
     """gilr_forward (layers.hpp:78-100) -> h [T, b, n]; fills ``cache`` (g, i, h)."""
     pad = _Pad(x.shape[-1] if x.dim() == 3 else p.input(), p.hidden())
-    if not pad.needed():
+    if not pad.needed(x):
         return _gilr_forward_core(p, x, h0, mode, precision, cache)
     if x.shape[-1] != p.input():
         raise RuntimeError("gilr_forward: input feature mismatch")
@@ -623,7 +702,7 @@ def gilr_backward(p: GilrParams, x, h0, cache: GilrCache, d_h, grads: GilrGrads,
                   precision="fp32", want_dh0=True):
     """gilr_backward (layers.hpp:102-133): accumulates into ``grads``; returns (dx, dh0)."""
     pad = _Pad(p.input(), p.hidden())
-    if not pad.needed():
+    if not pad.needed(x):
         return _gilr_backward_core(p, x, h0, cache, d_h, grads, mode, precision, want_dh0)
     pp = pad.gilr(p)
     g4 = GilrGrads.zeros_like(pp)
@@ -641,7 +720,7 @@ def gilr_lstm_forward(p: GilrLstmParams, x, htil0=None, c0=None, mode="parallel"
     """gilr_lstm_forward (layers.hpp:245-293) -> h [T, b, n]; fills ``cache``
     (padded to the kernels' widths when m or n is not a multiple of 4)."""
     pad = _Pad(x.shape[-1] if x.dim() == 3 else p.input(), p.hidden())
-    if not pad.needed():
+    if not pad.needed(x):
         return _gilr_lstm_forward_core(p, x, htil0, c0, mode, precision, cache)
     if x.shape[-1] != p.input():
         raise RuntimeError("gilr_lstm_forward: input feature mismatch")
@@ -656,7 +735,7 @@ def gilr_lstm_backward(p: GilrLstmParams, x, htil0, c0, cache: GilrLstmCache, d_
     """gilr_lstm_backward (layers.hpp:295-375): accumulates into ``grads``;
     returns (dx, d_htil0, d_c0)."""
     pad = _Pad(p.input(), p.hidden())
-    if not pad.needed():
+    if not pad.needed(x):
         return _gilr_lstm_backward_core(p, x, htil0, c0, cache, d_h, grads, mode, precision, want_initial)
     pp = pad.lstm(p)
     g4 = GilrLstmGrads.zeros_like(pp)
@@ -678,7 +757,7 @@ def gilr_lstm_backward(p: GilrLstmParams, x, htil0, c0, cache: GilrLstmCache, d_
 def qrnn_forward(p: QrnnParams, x, c0=None, mode="parallel", precision="fp32", cache: QrnnCache | None = None):
     """qrnn_forward (layers.hpp:449-494) -> h [T, b, n]; fills ``cache``."""
     pad = _Pad(x.shape[-1] if x.dim() == 3 else p.input(), p.hidden())
-    if not pad.needed():
+    if not pad.needed(x):
         return _qrnn_forward_core(p, x, c0, mode, precision, cache)
     if x.shape[-1] != p.input():
         raise RuntimeError("qrnn_forward: input feature mismatch")
@@ -691,7 +770,7 @@ def qrnn_backward(p: QrnnParams, x, c0, cache: QrnnCache, d_h, grads: QrnnGrads,
                   precision="fp32", want_dc0=True):
     """qrnn_backward (layers.hpp:496-548): accumulates into ``grads``; returns (dx, dc0)."""
     pad = _Pad(p.input(), p.hidden())
-    if not pad.needed():
+    if not pad.needed(x):
         return _qrnn_backward_core(p, x, c0, cache, d_h, grads, mode, precision, want_dc0)
     pp = pad.qrnn(p)
     g4 = QrnnGrads.zeros_like(pp)

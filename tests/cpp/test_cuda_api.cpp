@@ -6,7 +6,8 @@
 //   * shape errors throw ContractViolation with the reference's message;
 //   * gilr_lstm_forward/backward and qrnn_forward/backward run through the
 //     C++ mirror: parallel and serial scan modes agree within 1e-5 and the
-//     gradients are finite and non-zero.
+//     gradients are finite and non-zero; the double instantiation of the
+//     layer mirror agrees with itself across modes and with the fp32 path.
 // Built by `make cpp-tests`; run by tests/test_gpu_cpp_api.py on a GPU.
 #include <cuda_runtime.h>
 
@@ -209,6 +210,89 @@ static void test_qrnn() {
   }
 }
 
+// The double instantiation of the layer mirror (GilrLstmParamsT<double>,
+// linrec_gilr_lstm_*_f64): parallel and serial scan modes agree within
+// 1e-12, and the fp64 outputs / gradients match the fp32 path (3xTF32 GEMMs)
+// within its 1e-5 on the same inputs.
+static void test_gilr_lstm_f64() {
+  const index_t T = 129, b = 2, m = 12, n = 16, R = T * b;
+  auto sU = uniform(n * m, -.3f, .3f, 5), sV = uniform(n * m, -.3f, .3f, 6), sbg = uniform(n, 0, 1, 7);
+  auto sbz = uniform(n, -.1f, .1f, 8), U = uniform(4 * n * n, -.25f, .25f, 9), V = uniform(4 * n * m, -.3f, .3f, 10);
+  auto bias = uniform(4 * n, -.5f, .5f, 11), x = uniform(R * m, -1, 1, 12), dh = uniform(R * n, -1, 1, 13);
+  struct DevD {
+    double* p = nullptr;
+    size_t n;
+    explicit DevD(size_t c) : n(c) {
+      if (cudaMalloc(&p, c * 8 + 16) != cudaSuccess) std::abort();
+      cudaMemset(p, 0, c * 8 + 16);
+    }
+    explicit DevD(const std::vector<float>& h) : DevD(h.size()) {
+      std::vector<double> d(h.begin(), h.end());
+      cudaMemcpy(p, d.data(), d.size() * 8, cudaMemcpyHostToDevice);
+    }
+    ~DevD() { cudaFree(p); }
+    std::vector<double> get() const {
+      std::vector<double> h(n);
+      cudaMemcpy(h.data(), p, n * 8, cudaMemcpyDeviceToHost);
+      return h;
+    }
+  };
+  auto nw = [](const std::vector<double>& a, const std::vector<double>& r) {
+    double num = 0, den = 0;
+    for (size_t i = 0; i < a.size(); ++i) {
+      num = std::fmax(num, std::fabs(a[i] - r[i]));
+      den = std::fmax(den, std::fabs(r[i]));
+    }
+    return den > 0 ? num / den : num;
+  };
+  DevD dsU(sU), dsV(sV), dsbg(sbg), dsbz(sbz), dU(U), dV(V), dbias(bias), X(x), DH(dh);
+  GilrLstmParamsT<double> p;
+  p.surrogate = GilrParamsT<double>{dsU.p, dsV.p, dsbg.p, dsbz.p, Activation::Tanh, m, n};
+  p.U = dU.p;
+  p.V = dV.p;
+  p.bias = dbias.p;
+  LayerContext ctx;
+  std::vector<double> h_par, dx_par, gV_par;
+  for (ScanMode mode : {ScanMode::Parallel, ScanMode::Serial}) {
+    DevD sg(R * n), si(R * n), htil((T + 1) * b * n), gates(4 * R * n), c(R * n), H(R * n), DX(R * m);
+    DevD gsU(n * m), gsV(n * m), gsbg(n), gsbz(n), gU(4 * n * n), gV(4 * n * m), gbias(4 * n);
+    GilrLstmCacheT<double> cache{sg.p, si.p, htil.p, gates.p, c.p};
+    DeviceTensor3<double> xx{X.p, T, b, m}, h{H.p, T, b, n}, d_h{DH.p, T, b, n}, dx{DX.p, T, b, m};
+    DeviceTensor2<double> zero{};
+    gilr_lstm_forward(p, xx, zero, zero, mode, ctx, cache, h);
+    GilrLstmGradsT<double> g{{gsU.p, gsV.p, gsbg.p, gsbz.p}, gU.p, gV.p, gbias.p};
+    gilr_lstm_backward(p, xx, zero, zero, cache, d_h, mode, ctx, g, dx);
+    cudaDeviceSynchronize();
+    if (mode == ScanMode::Parallel) {
+      h_par = H.get();
+      dx_par = DX.get();
+      gV_par = gV.get();
+    } else {
+      CHECK(nw(h_par, H.get()) < 1e-12 && nw(dx_par, DX.get()) < 1e-12 && nw(gV_par, gV.get()) < 1e-12,
+            "gilr_lstm f64: parallel vs serial %g", nw(h_par, H.get()));
+    }
+  }
+  // the fp32 path on the same inputs
+  Dev fsU(sU), fsV(sV), fsbg(sbg), fsbz(sbz), fU(U), fV(V), fbias(bias), FX(x), FDH(dh);
+  GilrLstmParams q;
+  q.surrogate = GilrParams{fsU.p, fsV.p, fsbg.p, fsbz.p, Activation::Tanh, m, n};
+  q.U = fU.p;
+  q.V = fV.p;
+  q.bias = fbias.p;
+  Dev sg(R * n), si(R * n), htil((T + 1) * b * n), gates(4 * R * n), c(R * n), H(R * n), DX(R * m);
+  Dev gsU(n * m), gsV(n * m), gsbg(n), gsbz(n), gU(4 * n * n), gV(4 * n * m), gbias(4 * n);
+  GilrLstmCache cache{sg.p, si.p, htil.p, gates.p, c.p};
+  DeviceTensor3<float> xx{FX.p, T, b, m}, h{H.p, T, b, n}, d_h{FDH.p, T, b, n}, dx{DX.p, T, b, m};
+  gilr_lstm_forward(q, xx, DeviceTensor2<float>{}, DeviceTensor2<float>{}, ScanMode::Parallel, ctx, cache, h);
+  GilrLstmGrads g{{gsU.p, gsV.p, gsbg.p, gsbz.p}, gU.p, gV.p, gbias.p};
+  gilr_lstm_backward(q, xx, DeviceTensor2<float>{}, DeviceTensor2<float>{}, cache, d_h, ScanMode::Parallel, ctx, g,
+                     dx);
+  cudaDeviceSynchronize();
+  CHECK(normwise(H.get(), h_par) < 1e-5 && normwise(DX.get(), dx_par) < 1e-5 && normwise(gV.get(), gV_par) < 1e-5,
+        "gilr_lstm fp32 vs fp64: h %g dx %g dV %g", normwise(H.get(), h_par), normwise(DX.get(), dx_par),
+        normwise(gV.get(), gV_par));
+}
+
 // scan_parallel with an explicit plan and ScanSummaries: the reference's
 // hand-executed two-chunk example (test_recurrence.cpp:75-99), and the
 // plan-chunked forward against the fmaf restatement of its three phases.
@@ -376,6 +460,7 @@ int main() {
   test_plan_scan();
   test_check_finite();
   test_gilr_lstm();
+  test_gilr_lstm_f64();
   test_qrnn();
   test_channel_sharded();
   if (failures == 0) std::printf("ALL OK\n");
