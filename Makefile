@@ -26,7 +26,7 @@ PYINC   := $(shell $(PY) -c "import pybind11,sysconfig;print('-I'+pybind11.get_i
 KERNEL_SRCS := $(CSRC)/chain_fwd_f32.cu $(CSRC)/chain_bwd_f32.cu $(CSRC)/chain_fwd_f64.cu \
                $(CSRC)/chain_bwd_f64.cu $(CSRC)/serial_misc.cu $(CSRC)/tma_fwd_f32.cu \
                $(CSRC)/tma_bwd_f32.cu $(CSRC)/tma_f64.cu $(CSRC)/segment.cu $(CSRC)/gemm_tc.cu \
-               $(CSRC)/layers.cu $(CSRC)/layers_f64.cu $(CSRC)/training.cu $(CSRC)/p2p.cu $(CSRC)/plan_scan.cu $(CSRC)/local_scan.cu
+               $(CSRC)/layers.cu $(CSRC)/layers_f64.cu $(CSRC)/training.cu $(CSRC)/p2p.cu $(CSRC)/plan_scan.cu $(CSRC)/local_scan.cu $(CSRC)/cluster_scan.cu
 HOST_SRCS   := $(CSRC)/capi.cpp $(CSRC)/sharded_capi.cpp
 HDRS        := $(wildcard $(CSRC)/*.cuh) $(CSRC)/launch.h include/linrec_cuda.h
 OBJS        := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(KERNEL_SRCS)) $(BUILD)/capi.o $(BUILD)/sharded_capi.o

@@ -52,6 +52,15 @@ sys.path.insert(0, ROOT)
 METRIC = "scan elements/s fwd+bwd and HBM GB/s (% of peak) at 1/2/4/8 B200 vs host CPU"
 FWD_BYTES = 12  # fp32 algorithmic bytes per element: read lam, x; write h
 BWD_BYTES = 20  # read lam, h, dh; write dlam, dx
+# the roofline line's dominant kernel (the backward), by the family the library
+# picks for the shape (capi.scan_kernel_name)
+BWD_KERNEL_DESC = {
+    "tma": "k_tma_bwd (persistent TMA-fed reverse-time chained scan, fused dlam/dx/dh0)",
+    "chained": "k_chain_bwd (register-tiled reverse-time chained scan, fused dlam/dx/dh0)",
+    "cluster": "k_cluster_bwd (thread-block cluster over the sequence, DSMEM carry exchange, fused dlam/dx/dh0)",
+    "local": "k_local_bwd (CTA-local reverse-time scan, fused dlam/dx/dh0)",
+    "serial": "k_serial_bwd (per-channel reverse-time scan)",
+}
 WORKLOADS = {
     "c1": dict(T=4096, B=1, D=256, desc="C1 fp32 linear recurrence T=4096 B=1 D=256 (BASELINE configs[0])"),
     "c2": dict(T=65536, B=8, D=1024, desc="C2 fp32 forward+backward linear recurrence T=65536 B=8 D=1024 (BASELINE configs[1])"),
@@ -656,7 +665,7 @@ def run_ours(args):
             },
             "roofline": {
                 "bound": "hbm",
-                "kernel": "k_tma_bwd (persistent TMA-fed reverse-time chained scan, fused dlam/dx/dh0)",
+                "kernel": BWD_KERNEL_DESC[capi.scan_kernel_name(P.Tl, W, backward=True)],
                 "achieved": bwd_gbs,
                 "peak": peak,
                 "peak_kind": peak_kind,

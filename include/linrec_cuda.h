@@ -273,10 +273,16 @@ int linrec_screen_finite_f64(const double* v, int64_t T, int64_t batch,
                              void* stream);
 
 /* Kernels one linrec_scan_* (backward = 0) / linrec_scan_backward_* call
- * launches for this shape and mode with 16-byte aligned buffers (1, or 3 when
- * the sequence is split into virtual segments: scan, fold, fix-up); -1 for
- * invalid arguments.  For launch accounting (bench.py's gpu_launches). */
+ * launches for this shape and mode with 16-byte aligned buffers (1; 2 when
+ * the sequence is split into virtual segments: scan and fix-up; 5 with the
+ * decay-adaptive stitch); -1 for invalid arguments.  For launch accounting
+ * (bench.py's gpu_launches). */
 int linrec_scan_kernel_count(int64_t T, int64_t W, int dtype_bytes, int backward, int mode);
+/* The kernel family that call runs (static string): "serial" (per-channel),
+ * "cluster" (thread-block cluster over a short sequence), "local" (CTA-local),
+ * "tma" (persistent TMA-fed chained scan), "chained" (register chained scan);
+ * NULL for invalid arguments.  For reports (bench.py's roofline kernel). */
+const char* linrec_scan_kernel_name(int64_t T, int64_t W, int dtype_bytes, int backward, int mode);
 
 /* ---- the reference's chunked scan with an explicit plan ----------------- *
  * scan_parallel(decays, impulses, initial, plan, pool, check_finite,

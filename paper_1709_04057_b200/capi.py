@@ -88,6 +88,8 @@ def _load():
         getattr(lib, f"linrec_scan_plan_{s_}").argtypes = [_vp] * 4 + [_i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp]
         getattr(lib, f"linrec_scan_backward_plan_{s_}").argtypes = [_vp] * 7 + [_i64, _i64, _vp, _i64, _vp]
     lib.linrec_scan_kernel_count.argtypes = [_i64, _i64, _int, _int, _int]
+    lib.linrec_scan_kernel_name.restype = C.c_char_p
+    lib.linrec_scan_kernel_name.argtypes = [_i64, _i64, _int, _int, _int]
     _ex = C.POINTER(Exchange)
     lib.linrec_segment_scan_exchange_f32.argtypes = [_vp] * 6 + [_i64, _i64, _ex, _vp, _vp]
     lib.linrec_segment_scan_backward_exchange_f32.argtypes = [_vp] * 10 + [_i64, _i64, _ex, _vp, _vp]
@@ -262,6 +264,14 @@ def segment_fixup_backward(lam, hprev, h, lam_next, seg_prod, y_in, dlam, dx, T,
 def scan_kernel_count(T, W, backward=False, mode=PARALLEL, dtype_bytes=4) -> int:
     """Kernels one scan (or scan_backward) call launches for this shape."""
     return int(lib.linrec_scan_kernel_count(T, W, dtype_bytes, 1 if backward else 0, mode))
+
+
+def scan_kernel_name(T, W, backward=False, mode=PARALLEL, dtype_bytes=4) -> str:
+    """Kernel family of that call: serial, cluster, local, tma or chained."""
+    r = lib.linrec_scan_kernel_name(T, W, dtype_bytes, 1 if backward else 0, mode)
+    if r is None:
+        raise LinrecError(ERR_VALUE, "scan_kernel_name: invalid arguments")
+    return r.decode()
 
 
 # ---- the reference's chunked scan with an explicit plan ---------------------

@@ -264,7 +264,8 @@ cudaError_t launch_mul(const S* a, const S* b, S* out, int64_t n, cudaStream_t s
 template <class S>
 bool gated_fused_ok(int64_t T, int64_t W, int mode, bool vok) {
   if (sizeof(S) != 4 || mode == LINREC_SERIAL || !vok || !tma_allowed(T, W) ||
-      channel_parallel_enough<S>(T, W, vok) || linrec_impl::local_scan_ok<S>(T, W, vok))
+      channel_parallel_enough<S>(T, W, vok) || linrec_impl::cluster_scan_ok<S>(T, W, vok) ||
+      linrec_impl::local_scan_ok<S>(T, W, vok))
     return false;
   ChainPlan p;
   return linrec_impl::plan_tma<S>(false, T, W, &p) && p.q == 32 && p.r == 12 && p.stages == 1 && p.nw == 8;
@@ -281,6 +282,10 @@ int scan_device(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t 
   FwdCall<S> c{lam, x, h0, h, T, W};
   if (mode == LINREC_SERIAL || channel_parallel_enough<S>(T, W, vok)) {
     LINREC_CUDA_TRY(linrec_impl::launch_serial_fwd<S>(c, vok, st));
+    return LINREC_OK;
+  }
+  if (linrec_impl::cluster_scan_ok<S>(T, W, vok)) {  // short sequence, few channels: one cluster per column
+    LINREC_CUDA_TRY(linrec_impl::launch_cluster_fwd<S>(c, st));
     return LINREC_OK;
   }
   if (linrec_impl::local_scan_ok<S>(T, W, vok)) {  // short sequence: one CTA per channel vector
@@ -347,6 +352,10 @@ int scan_backward_device(const S* lam, const S* h0, const S* h, const S* dh, con
   c.gate = gate;
   if (mode == LINREC_SERIAL || channel_parallel_enough<S>(T, W, vok)) {
     LINREC_CUDA_TRY(linrec_impl::launch_serial_bwd<S>(c, vok, st));
+    return LINREC_OK;
+  }
+  if (linrec_impl::cluster_scan_ok<S>(T, W, vok)) {
+    LINREC_CUDA_TRY(linrec_impl::launch_cluster_bwd<S>(c, st));
     return LINREC_OK;
   }
   if (linrec_impl::local_scan_ok<S>(T, W, vok)) {
@@ -1503,7 +1512,8 @@ int linrec_scan_kernel_count(int64_t T, int64_t W, int dtype_bytes, int backward
   const bool vok = W % (f64 ? vec_of<double>() : vec_of<float>()) == 0;  // aligned buffers assumed
   if (mode == LINREC_SERIAL ||
       (f64 ? channel_parallel_enough<double>(T, W, vok) : channel_parallel_enough<float>(T, W, vok)) ||
-      (f64 ? linrec_impl::local_scan_ok<double>(T, W, vok) : linrec_impl::local_scan_ok<float>(T, W, vok)))
+      (f64 ? linrec_impl::local_scan_ok<double>(T, W, vok) : linrec_impl::local_scan_ok<float>(T, W, vok)) ||
+      (!f64 && linrec_impl::cluster_scan_ok<float>(T, W, vok)))
     return 1;
   ChainPlan p;
   const bool fwd = backward == 0;
@@ -1515,6 +1525,23 @@ int linrec_scan_kernel_count(int64_t T, int64_t W, int dtype_bytes, int backward
   // decay-adaptive stitch also the probe, the reduce pass and the carry fold
   // (launched always, the unused ones exit at once)
   return (tma && !f64 && adaptive_stitch_on()) ? 5 : 2;
+}
+
+const char* linrec_scan_kernel_name(int64_t T, int64_t W, int dtype_bytes, int backward, int mode) {
+  if (T < 1 || W < 1 || (dtype_bytes != 4 && dtype_bytes != 8)) return nullptr;
+  const bool f64 = dtype_bytes == 8;
+  const bool vok = W % (f64 ? vec_of<double>() : vec_of<float>()) == 0;
+  if (mode == LINREC_SERIAL ||
+      (f64 ? channel_parallel_enough<double>(T, W, vok) : channel_parallel_enough<float>(T, W, vok)))
+    return "serial";
+  if (!f64 && linrec_impl::cluster_scan_ok<float>(T, W, vok)) return "cluster";
+  if (f64 ? linrec_impl::local_scan_ok<double>(T, W, vok) : linrec_impl::local_scan_ok<float>(T, W, vok))
+    return "local";
+  ChainPlan p;
+  const bool fwd = backward == 0;
+  const bool tma = vok && tma_allowed(T, W) &&
+                   (f64 ? linrec_impl::plan_tma<double>(fwd, T, W, &p) : linrec_impl::plan_tma<float>(fwd, T, W, &p));
+  return tma ? "tma" : "chained";
 }
 
 int linrec_scan_plan_f32(const float* lam, const float* x, const float* h0, float* h, int64_t T, int64_t W,

@@ -139,6 +139,15 @@ cudaError_t launch_tma_bwd(const ChainPlan& p, const BwdCall<S>& c, const ChainP
 
 cudaError_t launch_ws_init(void* ctrl, cudaStream_t st);
 
+// cluster_scan.cu: a thread-block cluster splits a short sequence, the CTAs
+// exchanging their chunk aggregates through distributed shared memory
+template <class S>
+bool cluster_scan_ok(int64_t T, int64_t W, bool vec_ok);
+template <class S>
+cudaError_t launch_cluster_fwd(const FwdCall<S>& c, cudaStream_t st);
+template <class S>
+cudaError_t launch_cluster_bwd(const BwdCall<S>& c, cudaStream_t st);
+
 // local_scan.cu: one CTA per channel vector over the whole (short) sequence
 template <class S>
 bool local_scan_ok(int64_t T, int64_t W, bool vec_ok);
