@@ -510,7 +510,16 @@ def guard(rk, P, stream, cols=8):
         capi.scan_backward(L.data_ptr(), H0.data_ptr(), hs.data_ptr(), DH.data_ptr(), dls.data_ptr(),
                            dxs.data_ptr(), dh0r.data_ptr(), T, n, capi.SERIAL, 4, None, st)
         torch.cuda.synchronize(rk.dev)
-        err = max(rel_err(H, hs), rel_err(DL, dls), rel_err(DX, dxs), rel_err(DH0, dh0r))
+        errs = {"h": rel_err(H, hs), "dlam": rel_err(DL, dls), "dx": rel_err(DX, dxs), "dh0": rel_err(DH0, dh0r)}
+        err = max(errs.values())
+        if not err <= GUARD_TOL:  # diagnostics: where the timed path's results differ
+            for nm, a, b in (("h", H, hs), ("dlam", DL, dls), ("dx", DX, dxs)):
+                bad = ((a - b).abs() > GUARD_TOL * max(1.0, b.abs().max().item())).nonzero()
+                if len(bad):
+                    print(f"bench guard: {nm} differs at {len(bad)} of {a.numel()} sampled elements; rows "
+                          f"{bad[:, 0].min().item()}..{bad[:, 0].max().item()}, sampled channels "
+                          f"{sorted(set(idx[bad[:, 1]].tolist()))[:8]} (T={T}, W={W}, errors {errs})",
+                          file=sys.stderr, flush=True)
     return rk.bcast(err)
 
 
