@@ -32,6 +32,17 @@ namespace cg = cooperative_groups;
 
 namespace linrec_dev {
 
+// Programmatic dependent launch: the kernels are launched with programmatic
+// stream serialisation, so the next kernel in the stream may be scheduled
+// while this one runs (its launch and prologue overlap this kernel); every
+// kernel waits for its predecessor's completion and memory flush before
+// touching global memory (griddepcontrol.wait), and lets its successor launch
+// once all of its own CTAs are resident (launch_dependents at entry).
+__device__ __forceinline__ void pdl_wait_and_release_successor() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void cluster_arrive_release() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 }
@@ -149,6 +160,7 @@ __device__ __forceinline__ void cluster_carry(cg::cluster_group& cl, int rank, c
 template <class S, int VEC, int Q, int R, int CS>
 __global__ void __launch_bounds__(256) k_cluster_fwd(const S* __restrict__ lam, const S* __restrict__ x,
                                                      const S* __restrict__ h0, S* __restrict__ h, int T, int64_t W) {
+  pdl_wait_and_release_successor();
   constexpr int G = 32 / Q, CPB = Q * VEC, RC = 8 * G * R;
   using IO = VecIO<S, VEC>;
   __shared__ S sA[8][CPB], sB[8][CPB];
@@ -204,6 +216,7 @@ __global__ void __launch_bounds__(256)
     k_cluster_bwd(const S* __restrict__ lam, const S* __restrict__ h0, const S* __restrict__ h,
                   const S* __restrict__ dh, const S* __restrict__ lam_next, const S* __restrict__ g_next,
                   S* __restrict__ dlam, S* __restrict__ dx, S* __restrict__ dh0, int T, int64_t W) {
+  pdl_wait_and_release_successor();
   constexpr int G = 32 / Q, CPB = Q * VEC, RC = 8 * G * R;
   using IO = VecIO<S, VEC>;
   __shared__ S sA[8][CPB], sB[8][CPB];
@@ -336,13 +349,16 @@ cudaError_t launch_cluster_kernel(const FwdCall<S>* f, const BwdCall<S>* b, int6
   cfg.gridDim = dim3((unsigned)(ncols * CS));
   cfg.blockDim = dim3(256);
   cfg.stream = st;
-  cudaLaunchAttribute at;
-  at.id = cudaLaunchAttributeClusterDimension;
-  at.val.clusterDim.x = CS;
-  at.val.clusterDim.y = 1;
-  at.val.clusterDim.z = 1;
-  cfg.attrs = &at;
-  cfg.numAttrs = 1;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  static const bool pdl = env_int("LINREC_PDL", 1) != 0;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 2 : 1;
   if constexpr (FWD) {
     auto k = linrec_dev::k_cluster_fwd<S, VEC, Q, R, CS>;
     static const bool once = CS > 8 && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

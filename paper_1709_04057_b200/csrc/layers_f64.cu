@@ -46,7 +46,7 @@ struct Gm {
 __global__ void __launch_bounds__(256) k_dgemm(Gm g) {
   __shared__ double As[BK][BM + 1], Bs[BK][BN + 1];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;  // rows on x: R may exceed 65535 tiles
   const int64_t kb = (int64_t)blockIdx.z * g.kchunk;
   const int64_t ke = kb + g.kchunk < g.K ? kb + g.kchunk : g.K;
   const bool a_m1 = g.sam == 1, b_n1 = g.sbn == 1;
@@ -332,7 +332,8 @@ int dgemm(const double* A, int64_t sam, int64_t sak, const double* B, int64_t sb
   kchunk = (kchunk + BK - 1) / BK * BK;
   const int used = (int)((K + kchunk - 1) / kchunk);
   Gm g{A, sam, sak, B, sbk, sbn, C, ldc, M, N, K, kchunk, accumulate ? 1 : 0, used > 1 ? part : nullptr};
-  const dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)used);
+  if ((N + BN - 1) / BN > 65535) return err64(LINREC_ERR_SHAPE, "gemm_f64: N too large");
+  const dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN), (unsigned)used);
   k_dgemm<<<grid, 256, 0, st>>>(g);
   DTRY(cudaGetLastError());
   if (used > 1) {
