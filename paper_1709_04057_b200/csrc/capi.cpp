@@ -188,13 +188,14 @@ VsegPtrs<S> vseg_ptrs(linrec_workspace* ws, const ChainPlan& p, int64_t W) {
 // once and the stitch runs as before.  All decisions stay on the device, so
 // the sequence is stream-ordered and graph-capturable.  Thresholds: the mean
 // fraction of a segment the fix-up would walk, above which the reduce pass
-// is cheaper (forward: 8 B/el < 12 B/el x f; backward: 12 B/el (its h
-// stream rides along) < 20 B/el x f / 0.76).  LINREC_ADAPTIVE=0 disables it.
+// is cheaper (forward: 8 B/el < 12 B/el x f; backward: 8 B/el -- the reduce
+// pass stages mu and dh, not h -- < 20 B/el x f / 0.76).  LINREC_ADAPTIVE=0
+// disables it.
 bool adaptive_stitch_on() {
   static const bool on = linrec_impl::env_int("LINREC_ADAPTIVE", 1) != 0;
   return on;
 }
-constexpr float kDeepFracFwd = 0.67f, kDeepFracBwd = 0.45f;
+constexpr float kDeepFracFwd = 0.67f, kDeepFracBwd = 0.30f;
 const int* decay_mode_ptr(linrec_workspace* ws) {
   return reinterpret_cast<const int*>(static_cast<char*>(ws->base) + offsetof(linrec_dev::Ctrl, decay_mode));
 }

@@ -452,15 +452,19 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
         const int c0 = (int)(cp.col * CPW);
         const int r0 = (int)tile_row0<true>(a, cp, L);
         const bool keep = a.seg_prod != nullptr && cp.pos < kKeepPositions;  // revisited by the fix-up
-        mbar_arrive_expect_tx(sm.full(s), Cfg::TX_BYTES);
+        // the reduce-only pass (role 1) needs mu and the adjoint, not h: it
+        // stages 8 B/el instead of 12 (the h box is not loaded)
+        const bool need_h = a.role != 1;
+        mbar_arrive_expect_tx(sm.full(s), need_h ? Cfg::TX_BYTES : Cfg::TX_BYTES / Cfg::kNARR * (Cfg::kNARR - 1));
 #pragma unroll
         for (int b = 0; b < Cfg::NBOX; ++b) {
           const int rb = r0 + b * Cfg::BOX_ROWS;
           tma_load_2d(sm.arr(s, 0) + b * Cfg::BOX_ROWS * CPW, &map_lam, c0, rb + 1, sm.full(s),
                       keep ? pol_keep : pol);
           tma_load_2d(sm.arr(s, 1) + b * Cfg::BOX_ROWS * CPW, &map_dh, c0, rb, sm.full(s), pol);
-          tma_load_2d(sm.arr(s, 2) + b * Cfg::BOX_ROWS * CPW, &map_h, c0, rb - 1, sm.full(s),
-                      keep ? pol_keep : pol);
+          if (need_h)
+            tma_load_2d(sm.arr(s, 2) + b * Cfg::BOX_ROWS * CPW, &map_h, c0, rb - 1, sm.full(s),
+                        keep ? pol_keep : pol);
           if (GATED) tma_load_2d(sm.arr(s, GATED ? 3 : 0) + b * Cfg::BOX_ROWS * CPW, &map_gate, c0, rb, sm.full(s), pol);
         }
       }
