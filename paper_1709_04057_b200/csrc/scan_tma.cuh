@@ -150,14 +150,25 @@ __device__ __forceinline__ bool tma_coordinator(const SM& sm, const ChainArgs<S>
         for (int v = 0; v < VEC; ++v) c[v] = a.seed_rows[cp.seg * a.W + ch + v];
       }
     }
+    // the reduce-only pass (role 1) stores nothing: its consumers need no
+    // carry, so they are released as soon as this tile's totals are read and
+    // run ahead at load speed while the look-back below resolves the chain
+    // (its aggregate, agg_out, is what the pass is for).  The slot's totals
+    // are not overwritten early: the consumers' next use of this slot waits
+    // for this release.
+    const bool early = a.role == 1;
+    if (early) {
+      __syncwarp();
+      mbar_arrive(sm.carry_bar(slot));
+    }
     const bool want_p = a.seg_prod != nullptr || a.agg_out != nullptr;
     Lookback<S, VEC, Q, Cfg::REC>::exclusive(ws, epoch, k, cp.pos, cp.chain, cp.nchains, TA, TB, c, P, valid,
                                              want_p);
-    if (lane < Q) {
+    if (lane < Q && !early) {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) sm.carry(slot)[lane * VEC + v] = c[v];
     }
-    mbar_arrive(sm.carry_bar(slot));  // consumers re-scan while the carry is published
+    if (!early) mbar_arrive(sm.carry_bar(slot));  // consumers re-scan while the carry is published
     Lookback<S, VEC, Q, Cfg::REC>::publish(ws, epoch, k, TA, TB, c, P, valid, want_p);
     write_segment_outputs<S, VEC, Q>(a, cp, ch, valid, TA, TB, c, P);
   }
