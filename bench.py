@@ -385,11 +385,14 @@ class DeviceProblem:
         self.Tl = self.lam.shape[0]
         self.W = self.lam[0].numel()
 
-    def regen_lam(self, lo, hi, seed):
-        """Decays replaced in place (device RNG; the slow-decay variant)."""
+    def regen_lam(self, lo, hi, seed, stream):
+        """Decays replaced in place (device RNG; the slow-decay variant), on the
+        bench stream and finished before anything reads them."""
         import torch
         g = torch.Generator(device=self.lam.device).manual_seed(seed)
-        self.lam.uniform_(lo, hi, generator=g)
+        with torch.cuda.stream(stream):
+            self.lam.uniform_(lo, hi, generator=g)
+        stream.synchronize()
 
     def free(self):
         for k in ("lam", "x", "h0", "dh", "h", "dlam", "dx", "dh0"):
@@ -490,8 +493,8 @@ def guard(rk, P, stream, cols=8):
     import torch
     from paper_1709_04057_b200 import capi
     W = P.W
-    idx = torch.arange(0, W, max(1, W // cols), device=P.lam.device)[:cols]
-    with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream):  # idx on the same stream as its users (no cross-stream read)
+        idx = torch.arange(0, W, max(1, W // cols), device=P.lam.device)[:cols]
         part = [t.view(t.shape[0], W).index_select(1, idx).cpu().numpy()
                 for t in (P.lam, P.x, P.dh, P.h, P.dlam, P.dx)]
         h0s = P.h0.view(W).index_select(0, idx).cpu().numpy()
@@ -627,7 +630,7 @@ def run_ours(args):
     # the same problem with slow decays lam ~ U(0.99, 1)
     slow = None
     if not args.no_slow:
-        P.regen_lam(*LAM_SLOW, seed=77 + rank)
+        P.regen_lam(*LAM_SLOW, seed=77 + rank, stream=stream)
         srec = run_problem(rk, P, T, args, stream, ws, seq_sharded, steps=min(args.steps, 10))
         check_guard(srec["guard_max_rel_err"], args.workload + " slow decays")
         slow = dict(summarize(srec, N_total, N_local, peak), lam="U(0.99,1)")
@@ -739,7 +742,7 @@ def c4_records(rk, args, stream, ws, peak):
         check_guard(rec["guard_max_rel_err"], "c4")
         one = summarize(rec, T * W, T * W, peak)
         if not args.no_slow:
-            P.regen_lam(*LAM_SLOW, seed=78)
+            P.regen_lam(*LAM_SLOW, seed=78, stream=stream)
             srec = run_problem(one_rk, P, T, args, stream, ws, False, steps=min(args.steps, 10))
             check_guard(srec["guard_max_rel_err"], "c4 slow decays")
             one["slow_decay"] = dict(summarize(srec, T * W, T * W, peak), lam="U(0.99,1)")
@@ -756,7 +759,7 @@ def c4_records(rk, args, stream, ws, peak):
         rec_n["exchange"] = rec.get("exchange")
         rec_n["launches_per_step_rank0"] = rec.get("launches_per_step")
         if not args.no_slow:
-            P.regen_lam(*LAM_SLOW, seed=79 + rk.rank)
+            P.regen_lam(*LAM_SLOW, seed=79 + rk.rank, stream=stream)
             srec = run_problem(rk, P, T, args, stream, ws, True, steps=min(args.steps, 10))
             check_guard(srec["guard_max_rel_err"], "c4 sequence-sharded slow decays")
             rec_n["slow_decay"] = dict(summarize(srec, T * W, P.Tl * W, peak), lam="U(0.99,1)")
