@@ -353,15 +353,16 @@ class SequenceShardedScan:
         self.rows_b = self.be.tile_rows(self.Tl, W, True)
         nf = self.be.prod_rows(self.Tl, W, False)
         nb = self.be.prod_rows(self.Tl, W, True)
-        self.seg_prod_f = torch.empty(nf, W, **f)
-        self.seg_prod_b = torch.empty(nb, W, **f)
-        self.agg = torch.empty(2, W, **f)
-        self.aggs = torch.empty(self.world, 2, W, **f)
-        self.c_in = torch.zeros(W, **f)
-        self.y_in = torch.zeros(W, **f)
-        self.dh0_loc = torch.empty(W, **f)
-        self.ones = torch.ones(W, **f)
-        self.zeros = torch.zeros(W, **f)
+        with self._on_stream():  # filled on the stream the steps run on (no cross-stream read)
+            self.seg_prod_f = torch.empty(nf, W, **f)
+            self.seg_prod_b = torch.empty(nb, W, **f)
+            self.agg = torch.empty(2, W, **f)
+            self.aggs = torch.empty(self.world, 2, W, **f)
+            self.c_in = torch.zeros(W, **f)
+            self.y_in = torch.zeros(W, **f)
+            self.dh0_loc = torch.empty(W, **f)
+            self.ones = torch.ones(W, **f)
+            self.zeros = torch.zeros(W, **f)
         self.hprev = None
         use_p2p = exchange == "p2p" or (exchange == "auto" and backend is None and self.world > 1
                                         and _same_node(self.group))
