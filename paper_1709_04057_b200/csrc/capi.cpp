@@ -196,6 +196,35 @@ bool adaptive_stitch_on() {
   return on;
 }
 constexpr float kDeepFracFwd = 0.67f, kDeepFracBwd = 0.30f;
+
+// Wide scans (many channel columns) keep enough chains without virtual
+// segments: there the deep branch is not reduce pass + seeded scan (20 / 28
+// B/el) but an UNSPLIT twin of the scan, one chain per column, launched
+// beside the split one (each exits in the other's mode) -- one pass.  From
+// LINREC_UNSPLIT_COLS columns (default 8: 1024 channels) up; measured at
+// lam ~ U(0.99, 1), fwd + bwd (scripts/dev/time_shape.py): C2 1.64 -> 1.96,
+// 65536 x 2048 1.17 -> 1.48, 131072 x 1024 -> 1.29 x 10^11 el/s; at 4
+// columns (262144 x 512) the twin loses (1.16 -> 1.03).
+int64_t unsplit_cols() {
+  static const int v = linrec_impl::env_int("LINREC_UNSPLIT_COLS", 8);
+  return v > 0 ? v : (int64_t(1) << 40);
+}
+
+// The plan of that twin: the same tiles and kernel configuration, one chain
+// per column (its look-back state fits the split plan's workspace).
+ChainPlan unsplit_plan(const ChainPlan& p, int64_t T) {
+  ChainPlan u = p;
+  const int64_t ntt = (T + p.rows - 1) / p.rows;
+  u.nseg = 1;
+  u.ntt = ntt;
+  u.tseg = ntt * p.rows;
+  u.ntiles = p.ncols * ntt;
+  u.flags_bytes = ((size_t)u.ntiles * 4 + 255) / 256 * 256;
+  u.rec_bytes = (size_t)u.ntiles * 2 * p.rec * 8;
+  u.ws_bytes = 256 + u.flags_bytes + 2 * u.rec_bytes;
+  u.grid = (int)(p.grid < u.ntiles ? p.grid : u.ntiles);
+  return u;
+}
 const int* decay_mode_ptr(linrec_workspace* ws) {
   return reinterpret_cast<const int*>(static_cast<char*>(ws->base) + offsetof(linrec_dev::Ctrl, decay_mode));
 }
@@ -309,23 +338,34 @@ int scan_device(const S* lam, const S* x, const S* h0, S* h, int64_t T, int64_t 
     c.agg_out = vs.vagg;
   }
   const bool adapt = tma && sizeof(S) == 4 && p.nseg > 1 && adaptive_stitch_on();
+  const bool twin = adapt && p.ncols >= unsplit_cols();
   const int* dmode = adapt ? decay_mode_ptr(w) : nullptr;
-  if (adapt) {  // probe -> (deep only) reduce pass + segment carries; the scan seeds from them
+  if (adapt) {
     LINREC_CUDA_TRY(linrec_impl::launch_decay_probe<float>(reinterpret_cast<const float*>(lam), T, W, p.cpw, p.tseg,
                                                            kDeepFracFwd, w->base, st));
-    FwdCall<S> r = c;
-    r.h = nullptr;
-    r.seg_prod = nullptr;
-    r.mode = dmode;
-    r.role = 1;
-    LINREC_CUDA_TRY(linrec_impl::launch_tma_fwd<S>(p, r, ws_ptrs(w, p), st));
-    LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, vs.vagg, p.nseg, p.tseg, vs.carry, nullptr,
-                                                         nullptr, nullptr, W, st, nullptr, dmode));
     c.mode = dmode;
-    c.seed_rows = vs.carry;
+    if (twin) {  // deep: the unsplit twin below scans instead of the split scan
+      c.role = 3;
+    } else {  // deep: reduce pass + segment carries; the split scan seeds from them
+      FwdCall<S> r = c;
+      r.h = nullptr;
+      r.seg_prod = nullptr;
+      r.role = 1;
+      LINREC_CUDA_TRY(linrec_impl::launch_tma_fwd<S>(p, r, ws_ptrs(w, p), st));
+      LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(false, lam, vs.vagg, p.nseg, p.tseg, vs.carry, nullptr,
+                                                           nullptr, nullptr, W, st, nullptr, dmode));
+      c.seed_rows = vs.carry;
+    }
   }
   if (tma) LINREC_CUDA_TRY(linrec_impl::launch_tma_fwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_fwd<S>(p, c, ws_ptrs(w, p), st));
+  if (twin) {
+    const ChainPlan u = unsplit_plan(p, T);
+    FwdCall<S> t{lam, x, h0, h, T, W};
+    t.mode = dmode;
+    t.role = 2;
+    LINREC_CUDA_TRY(linrec_impl::launch_tma_fwd<S>(u, t, ws_ptrs(w, u), st));
+  }
   if (p.nseg > 1)  // one stitch launch: each fix-up CTA folds its own segment's carry from vagg
     LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(false, lam, nullptr, nullptr, nullptr, vs.seg_prod, nullptr,
                                                  nullptr, nullptr, h, nullptr, T, W, p.rows, p.nseg, p.tseg, p.ntt,
@@ -379,25 +419,37 @@ int scan_backward_device(const S* lam, const S* h0, const S* h, const S* dh, con
     c.agg_out = vs.vagg;
   }
   const bool adapt = tma && sizeof(S) == 4 && p.nseg > 1 && adaptive_stitch_on();
+  const bool twin = adapt && p.ncols >= unsplit_cols();
   const int* dmode = adapt ? decay_mode_ptr(w) : nullptr;
   if (adapt) {  // the forward's decay-adaptive stitch in reverse time (see above)
     LINREC_CUDA_TRY(linrec_impl::launch_decay_probe<float>(reinterpret_cast<const float*>(lam), T, W, p.cpw, p.tseg,
                                                            kDeepFracBwd, w->base, st));
-    BwdCall<S> r = c;
-    r.dlam = nullptr;
-    r.dx = nullptr;
-    r.dh0 = nullptr;
-    r.seg_prod = nullptr;
-    r.mode = dmode;
-    r.role = 1;
-    LINREC_CUDA_TRY(linrec_impl::launch_tma_bwd<S>(p, r, ws_ptrs(w, p), st));
-    LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, vs.vagg, p.nseg, p.tseg, vs.carry, nullptr,
-                                                         nullptr, nullptr, W, st, nullptr, dmode));
     c.mode = dmode;
-    c.seed_rows = vs.carry;
+    if (twin) {
+      c.role = 3;
+    } else {
+      BwdCall<S> r = c;
+      r.dlam = nullptr;
+      r.dx = nullptr;
+      r.dh0 = nullptr;
+      r.seg_prod = nullptr;
+      r.role = 1;
+      LINREC_CUDA_TRY(linrec_impl::launch_tma_bwd<S>(p, r, ws_ptrs(w, p), st));
+      LINREC_CUDA_TRY(linrec_impl::launch_vseg_finalize<S>(true, lam, vs.vagg, p.nseg, p.tseg, vs.carry, nullptr,
+                                                           nullptr, nullptr, W, st, nullptr, dmode));
+      c.seed_rows = vs.carry;
+    }
   }
   if (tma) LINREC_CUDA_TRY(linrec_impl::launch_tma_bwd<S>(p, c, ws_ptrs(w, p), st));
   else LINREC_CUDA_TRY(linrec_impl::launch_chain_bwd<S>(p, c, ws_ptrs(w, p), st));
+  if (twin) {
+    const ChainPlan u = unsplit_plan(p, T);
+    BwdCall<S> t{lam, h0, h, dh, lam_next, g_next, dlam, dx, dh0, T, W};
+    t.gate = gate;
+    t.mode = dmode;
+    t.role = 2;
+    LINREC_CUDA_TRY(linrec_impl::launch_tma_bwd<S>(u, t, ws_ptrs(w, u), st));
+  }
   if (p.nseg > 1)  // dh0 gets its correction from the fix-up that owns row 0
     LINREC_CUDA_TRY(linrec_impl::launch_fixup<S>(true, lam, h0, h, lam_next, vs.seg_prod, nullptr, nullptr,
                                                  nullptr, dx, dlam, T, W, p.rows, p.nseg, p.tseg, p.ntt, vok, st,
@@ -1523,9 +1575,11 @@ int linrec_scan_kernel_count(int64_t T, int64_t W, int dtype_bytes, int backward
   if (!tma) p = f64 ? linrec_impl::plan_chain<double>(fwd, T, W, vok) : linrec_impl::plan_chain<float>(fwd, T, W, vok);
   if (p.nseg <= 1) return 1;
   // the scan and the fix-up that stitches the virtual segments; with the
-  // decay-adaptive stitch also the probe, the reduce pass and the carry fold
-  // (launched always, the unused ones exit at once)
-  return (tma && !f64 && adaptive_stitch_on()) ? 5 : 2;
+  // decay-adaptive stitch also the probe and either the reduce pass and the
+  // carry fold or, on wide scans, the unsplit twin (launched always, the
+  // unused ones exit at once)
+  if (tma && !f64 && adaptive_stitch_on()) return p.ncols >= unsplit_cols() ? 4 : 5;
+  return 2;
 }
 
 const char* linrec_scan_kernel_name(int64_t T, int64_t W, int dtype_bytes, int backward, int mode) {

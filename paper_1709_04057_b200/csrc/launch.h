@@ -87,7 +87,9 @@ struct FwdCall {
   // decay-adaptive stitch (capi.cpp::adaptive_stitch): device mode word
   // (1 = "deep": the decays do not underflow within a virtual segment), the
   // launch's role (0 = the scan, which seeds virtual segments from seed_rows
-  // when deep; 1 = the reduce-only pass, skipped unless deep)
+  // when deep; 1 = the reduce-only pass, skipped unless deep; 2 = the
+  // unsplit twin of a wide scan, skipped unless deep; 3 = the split scan
+  // with such a twin, skipped when deep)
   const int* mode = nullptr;
   int role = 0;
   const S* seed_rows = nullptr;

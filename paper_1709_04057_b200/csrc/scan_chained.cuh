@@ -94,13 +94,21 @@ struct ChainArgs {
   S* rank_agg;
   linrec_impl::Exchange ex;
   // decay-adaptive stitch (TMA kernels): mode word (nullable; 1 = deep),
-  // role (1 = reduce-only pass: runs only when deep, stores no outputs), and
+  // role (1 = reduce-only pass: runs only when deep, stores no outputs;
+  // 2 = the unsplit twin of a wide scan, one chain per column: runs only when
+  // deep; 3 = the split scan whose twin exists: runs only when not deep), and
   // the carries entering the virtual segments [nseg][W] a deep scan seeds
   // its chains with (no fix-up follows)
   const int* mode;
   int role;
   const S* seed_rows;
 };
+
+// Does a launch of this role sit out the current decay mode (decay-adaptive
+// stitch, capi.cpp)?  Role 0 always runs.
+__device__ __forceinline__ bool role_skips(int role, bool deep) {
+  return ((role == 1 || role == 2) && !deep) || (role == 3 && deep);
+}
 
 // Position of ticket k: chain = (virtual segment, channel column), tiles in
 // ticket order along the chain (so the look-back predecessor is k - nchains).

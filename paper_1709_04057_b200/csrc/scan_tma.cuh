@@ -279,7 +279,7 @@ k_tma_fwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // decay-adaptive stitch: the reduce-only pass runs only in deep mode
   const bool deep = a.mode != nullptr && __ldcg(a.mode) != 0;
-  if (a.role == 1 && !deep) return;
+  if (role_skips(a.role, deep)) return;
   tma_init_barriers<Cfg>(sm);
   const uint32_t epoch = __ldcg(&ws.ctrl->epoch);
   __shared__ int s_last;  // tail fold: this CTA retired last
@@ -437,7 +437,7 @@ k_tma_bwd(const __grid_constant__ CUtensorMap map_lam, const __grid_constant__ C
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // decay-adaptive stitch: the reduce-only pass runs only in deep mode
   const bool deep = a.mode != nullptr && __ldcg(a.mode) != 0;
-  if (a.role == 1 && !deep) return;
+  if (role_skips(a.role, deep)) return;
   tma_init_barriers<Cfg>(sm);
   const uint32_t epoch = __ldcg(&ws.ctrl->epoch);
   __shared__ int s_last;  // tail fold: this CTA retired last

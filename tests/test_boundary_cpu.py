@@ -135,7 +135,7 @@ def test_planner_kernel_counts():
     assert capi.scan_kernel_count(4096, 256, backward=True) == 1
     assert capi.scan_kernel_count(1 << 20, 128) == 5           # C4: virtual segments + adaptive stitch
     assert capi.scan_kernel_count(1 << 20, 128, backward=True) == 5
-    assert capi.scan_kernel_count(65536, 8192) == 5            # C2 forward: 4 segments
+    assert capi.scan_kernel_count(65536, 8192) == 4            # C2 forward: 4 segments, probe + unsplit twin
     assert capi.scan_kernel_count(65536, 8192, backward=True) == 1
     assert capi.scan_kernel_count(1 << 20, 128, mode=capi.SERIAL) == 1
     assert capi.scan_kernel_count(0, 128) == -1
