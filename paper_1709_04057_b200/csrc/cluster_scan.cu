@@ -361,13 +361,19 @@ cudaError_t launch_cluster_kernel(const FwdCall<S>* f, const BwdCall<S>* b, int6
   cfg.numAttrs = pdl ? 2 : 1;
   if constexpr (FWD) {
     auto k = linrec_dev::k_cluster_fwd<S, VEC, Q, R, CS>;
-    static const bool once = CS > 8 && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    (void)once;
+    if (CS > 8) {
+      const cudaError_t e = func_attr_once(reinterpret_cast<const void*>(k),
+                                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
     return cudaLaunchKernelEx(&cfg, k, f->lam, f->x, f->h0, f->h, (int)f->T, f->W);
   } else {
     auto k = linrec_dev::k_cluster_bwd<S, VEC, Q, R, CS>;
-    static const bool once = CS > 8 && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    (void)once;
+    if (CS > 8) {
+      const cudaError_t e = func_attr_once(reinterpret_cast<const void*>(k),
+                                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
     return cudaLaunchKernelEx(&cfg, k, b->lam, b->h0, b->h, b->dh, b->lam_next, b->g_next, b->dlam, b->dx, b->dh0,
                               (int)b->T, b->W);
   }

@@ -6,6 +6,10 @@
 #include <cstdlib>
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <set>
+#include <tuple>
+
 namespace linrec_impl {
 
 // Sets the thread-local linrec_last_error() message; returns `code`.
@@ -48,6 +52,22 @@ struct ChainPtrs {  // host mirror of linrec_dev::ChainWs
 inline int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
+}
+
+// cudaFuncSetAttribute once per (kernel, attribute, device): function
+// attributes are per device, so a process-wide "once" would leave the other
+// GPUs of a multi-GPU process unconfigured.
+inline cudaError_t func_attr_once(const void* kernel, cudaFuncAttribute attr, int value) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(std::make_tuple(kernel, dev, (int)attr, value))) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, attr, value);
+  if (e == cudaSuccess) done.insert(std::make_tuple(kernel, dev, (int)attr, value));
+  return e;
 }
 // CTAs per (segment, column) chain of the stitch fix-up (fixup_chain): the
 // forward's many segments fit one wave of resident CTAs with one walker

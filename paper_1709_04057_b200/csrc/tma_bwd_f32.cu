@@ -19,8 +19,8 @@ cudaError_t launch_tma_bwd<float>(const ChainPlan& p, const BwdCall<float>& c, c
     using GCfg = linrec_dev::TmaCfg<float, 4, 32, 12, 8, 1, 4>;
     auto kern = linrec_dev::k_tma_bwd<float, 4, 32, 12, 8, 1, true>;
     if (!(p.q == 32 && p.r == 12 && p.stages == 1 && p.nw == 8)) return cudaErrorNotSupported;
-    static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         GCfg::SMEM);
+    const cudaError_t attr = func_attr_once(reinterpret_cast<const void*>(kern),
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, GCfg::SMEM);
     if (attr != cudaSuccess) return attr;
     CUtensorMap mg;
     if ((e = make_tmap_2d(&mg, c.gate, false, c.W, c.T, p.box_cols, p.box_rows)) != cudaSuccess) return e;
